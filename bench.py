@@ -1,0 +1,345 @@
+#!/usr/bin/env python
+"""bench.py -- L-GreCo data-parallel hot path on B200 (one process per GPU).
+
+One STEP = one pass of the whole hot path over one synthetic gradient batch
+(SURVEY.md §8(a)): profile every layer x every candidate (a2) -> Algorithm 1 DP
+(a5-a6) -> plan agreement (a7) -> compress + EF + compressed all-reduce (a8-a10).
+
+Default workload: C4 = ResNet-50 / ImageNet gradient shapes (25,557,032 fp32,
+161 tensors, 54 compressed), QSGD bits {2..8}, default 4, bucket 128, D = 10000
+(BASELINE.json configs[3], the north_star target).  Metric: gradient GB/s =
+4 * N bytes per rank per step, aggregated over ranks (weak scaling).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...        (N > 1)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2210_17357_b200 import workloads as W  # noqa: E402
+
+METRIC = "gradient GB/s profile+solve+compress+allreduce"
+WORKLOAD = "C4 ResNet-50/ImageNet gradient (25,557,032 fp32), QSGD bits 2..8 default 4, bucket 128, D=10000"
+D_BINS = 10000
+SEED = 0x5EED
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+def _cpu_info():
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return os.cpu_count(), len(os.sched_getaffinity(0)), model
+
+
+# ------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"lgreco_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            p = [x.strip() for x in line.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx = float(p[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, p[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2210_17357_b200 import lgreco
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE {world}"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    stream = torch.cuda.current_stream()
+
+    layers = W.config_layers("C4")
+    N = W.total_numel(layers)
+    L, K = len(layers), len(W.QSGD_BITS)
+    g_np, e_np = W.gaussian_outliers(layers, seed=W.rank_seed(SEED, rank))
+    g = torch.from_numpy(g_np).to(dev)
+    e0 = torch.from_numpy(e_np).to(dev)
+    ef = e0.clone()
+    out = torch.empty_like(g)
+    err = torch.empty(L, K, dtype=torch.float64, device=dev)
+    bits = torch.empty(L, K, dtype=torch.int64, device=dev)
+    dflt = torch.full((L,), W.QSGD_BITS.index(4), dtype=torch.int32, device=dev)
+    comp = torch.tensor([l.compress for l in layers], dtype=torch.int32, device=dev)
+    choice_d = torch.empty(L, dtype=torch.int32, device=dev)
+    info_d = torch.empty(48, dtype=torch.uint8, device=dev)
+    ws = torch.empty(lgreco.solve_workspace_bytes(L, K, D_BINS), dtype=torch.uint8, device=dev)
+    choice_h = torch.empty(L, dtype=torch.int32).pin_memory()
+    l2_flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    nccl_id = None
+    if world > 1:
+        obj = [lgreco.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    ctx = lgreco.Context(layers, lgreco.QSGD, W.QSGD_BITS, qbucket=128, seed=SEED, rank=rank, world=world,
+                         nccl_id=nccl_id)
+
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    def step(s, marks=None):
+        if marks: marks[0].record(stream)
+        ctx.profile(g, ef, s, err, bits)
+        if marks: marks[1].record(stream)
+        lgreco.solve(err, bits, dflt, comp, D=D_BINS, choice=choice_d, info=info_d, workspace=ws)
+        ctx.plan_broadcast(choice_d)
+        if marks: marks[2].record(stream)
+        choice_h.copy_(choice_d, non_blocking=True)
+        stream.synchronize()  # the plan is host-side state of the comm engine (NCCL counts)
+        if marks: marks[3].record(stream)
+        ctx.compress_allreduce(choice_h.tolist(), g, ef, out, s)
+        if marks: marks[4].record(stream)
+
+    for s in range(args.warmup):
+        step(s)
+    torch.cuda.synchronize()
+    ctx.check()
+
+    clocks = ClockSampler(local)
+    times = {"step": [], "profile": [], "solve": [], "compress_allreduce": []}
+    launches0 = ctx.launches()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    t_wall0 = time.perf_counter()
+    for s in range(args.steps):
+        l2_flush.zero_()  # flush L2 between timed steps (outside the timed events)
+        marks = [ev() for _ in range(5)]
+        step(args.warmup + s, marks)
+        torch.cuda.synchronize()
+        times["step"].append(marks[0].elapsed_time(marks[4]))
+        times["profile"].append(marks[0].elapsed_time(marks[1]))
+        times["solve"].append(marks[1].elapsed_time(marks[2]))
+        times["compress_allreduce"].append(marks[3].elapsed_time(marks[4]))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    wall = time.perf_counter() - t_wall0
+    clk = clocks.stop()
+    launches = ctx.launches() - launches0 + args.steps  # + one solve kernel per step
+    ctx.check()
+
+    ms = sum(times["step"]) / args.steps
+    stage = {k: sum(v) / len(v) for k, v in times.items()}
+    if world > 1:
+        t = torch.tensor([ms] + [stage[k] for k in ("profile", "solve", "compress_allreduce")], device=dev,
+                         dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t[0])
+        stage.update(profile=float(t[1]), solve=float(t[2]), compress_allreduce=float(t[3]))
+
+    # ---- e2e: public API with host buffers (H2D of g, D2H of the mean gradient)
+    g_host = torch.from_numpy(g_np).pin_memory()
+    out_host = torch.empty(N, dtype=torch.float32).pin_memory()
+    e2e_ms = []
+    ef.copy_(e0)
+    for s in range(max(1, args.steps)):
+        l2_flush.zero_()
+        a, b = ev(), ev()
+        a.record(stream)
+        g.copy_(g_host, non_blocking=True)
+        step(s)
+        out_host.copy_(out, non_blocking=True)
+        b.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms.append(a.elapsed_time(b))
+    e2e = sum(e2e_ms) / len(e2e_ms)
+    if world > 1:
+        t = torch.tensor([e2e], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e = float(t[0])
+
+    if rank == 0:
+        peaks, src = _peaks()
+        gbs = world * 4.0 * N / (ms * 1e-3) / 1e9
+        # dominant kernel: K1 qprofile, algorithmic bytes = 8 B per compressed element (g + e)
+        ncomp = sum(l.numel for l in layers if l.compress)
+        prof_bytes = 8.0 * ncomp
+        prof_gbs = prof_bytes / (stage["profile"] * 1e-3) / 1e9
+        traffic = _ncu_traffic()
+        line = {
+            "metric": METRIC, "value": round(gbs, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded Gaussian + 1% outliers, EF ~ N(0,(0.1s)^2))",
+            "config": {"workload": WORKLOAD, "global_batch": None, "parallelism": f"dp{world}",
+                       "l2": "flushed (512 MiB memset) before every timed step", "family": "qsgd"},
+            "dp_solve_ms": round(stage["solve"], 4),
+            "stage_ms": {k: round(v, 4) for k, v in stage.items()},
+            "roofline": {"bound": "hbm", "kernel": "k_qprofile (K1)", "achieved": round(prof_gbs, 1),
+                         "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": round(prof_gbs / peaks["hbm_gbs"], 4),
+                         "traffic": traffic, "peak_source": src,
+                         "algorithmic_bytes_per_launch": prof_bytes},
+            "e2e": {"value": round(world * 4.0 * N / (e2e * 1e-3) / 1e9, 3), "unit": "GB/s",
+                    "h2d_bytes_per_step": 4 * N, "d2h_bytes_per_step": 4 * N, "ms_per_step": round(e2e, 4)},
+            "gpu_launches": int(launches),
+            "clocks": clk,
+            "wall_s": round(wall, 3),
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline_full()
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _ncu_traffic():
+    """dram bytes per launch of K1 from the committed ncu capture, if present."""
+    p = os.path.join(ROOT, "profiles", "k1_dram_bytes.json")
+    try:
+        return json.load(open(p))["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------- oracle arm
+def _oracle_step(ref, layers, g, e, step):
+    K = len(W.QSGD_BITS)
+    err, bits = ref.qsgd_profile(layers, g, e, W.QSGD_BITS, seed=SEED, step=step)
+    st, choice, info = ref.solve(err, bits, [W.QSGD_BITS.index(4)] * len(layers), [l.compress for l in layers],
+                                 D=D_BINS)
+    lbits = [W.QSGD_BITS[c] if c >= 0 else 0 for c in choice]
+    out, es, _, _ = ref.qsgd_allreduce(layers, lbits, [g], [e], seed=SEED, step=step)
+    return es[0]
+
+
+def cpu_baseline_full():
+    """The oracle as it stands, one full C4 step (profile + solve + compress, W=1)."""
+    from oracle import ref
+    layers = W.config_layers("C4")
+    N = W.total_numel(layers)
+    g, e = W.gaussian_outliers(layers, seed=SEED)
+    t0 = time.perf_counter()
+    _oracle_step(ref, layers, g, e, 0)
+    dt = time.perf_counter() - t0
+    cores, aff, model = _cpu_info()
+    return {"value": round(4.0 * N / dt / 1e9, 6), "unit": "GB/s", "cores": 1, "kind": "oracle",
+            "sample": f"one full C4 step (N={N}), single thread, {dt:.2f} s; host {model}, {cores} cpus"}
+
+
+def _sample_layers():
+    layers = W.config_layers("C4")
+    out, n = [], 0
+    for l in layers:  # a prefix of ~1/8 of the model: bounded CPU work per step
+        out.append(l)
+        n += l.numel
+        if n >= 3_200_000:
+            break
+    return out
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import ref
+    layers = _sample_layers()
+    n = W.total_numel(layers)
+    g, e = W.gaussian_outliers(layers, seed=SEED)
+    for s in range(args.warmup):
+        e = _oracle_step(ref, layers, g, e, s)
+    t0 = time.perf_counter()
+    for s in range(args.steps):
+        e = _oracle_step(ref, layers, g, e, args.warmup + s)
+    dt = (time.perf_counter() - t0) / max(1, args.steps)
+    cores, aff, model = _cpu_info()
+    v = 4.0 * n / dt / 1e9
+    sample = f"first {len(layers)} C4 layers ({n} fp32) per step, single thread; host {model}"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(v, 6), "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "parallelism": "oracle (CPU, 1 thread)"},
+        "cpu_baseline": {"value": round(v, 6), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": round(v, 6), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

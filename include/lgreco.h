@@ -1,0 +1,186 @@
+/*
+ * lgreco.h -- C ABI of the B200-native L-GreCo data-parallel hot path.
+ *
+ * L-GreCo (Alimohammadi, Markov, Frantar, Alistarh, MLSys'23, arXiv 2210.17357)
+ * chooses one compression parameter per layer by (1) profiling the L2 error of
+ * every candidate on every layer, (2) solving the knapsack DP of Algorithm 1 and
+ * (3) compressing + exchanging the gradient with the chosen parameters.
+ * Citations: PAPER.md = the paper's text; DESIGN.md lists readings R1..R21 for
+ * every point the paper leaves open.
+ *
+ * Conventions (all entry points):
+ *  - Return value: LGRECO_OK (0) or a negative status; no exception crosses the
+ *    ABI.  lgreco_last_error() returns a thread-local message for the last error.
+ *  - Pointers prefixed d_ are DEVICE pointers (cuda:current), h_ are HOST pointers.
+ *    The caller owns every buffer it passes; the library never frees them.
+ *  - `stream` is a cudaStream_t passed as void*.  All device work is enqueued on
+ *    it, asynchronously, unless stated otherwise.  No entry point allocates device
+ *    memory except lgreco_ctx_create.
+ *  - Flat gradient layout: one contiguous fp32 vector of N elements; layer l owns
+ *    [offset, offset+numel) (DDP-style flattening).
+ *  - Non-finite gradient values (PAPER.md is silent) set a sticky
+ *    device flag read by lgreco_ctx_check(); non-finite error tables make
+ *    lgreco_solve report LGRECO_ENONFINITE in info->status.
+ */
+#ifndef LGRECO_H
+#define LGRECO_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LGRECO_OK 0
+#define LGRECO_EINVAL (-1)      /* bad argument (layer table, K, params, D ...) */
+#define LGRECO_ENONFINITE (-2)  /* NaN/Inf in the gradient or in the error table */
+#define LGRECO_EINFEASIBLE (-3) /* reserved: the solve falls back to the defaults instead */
+#define LGRECO_ECUDA (-4)       /* a CUDA runtime call failed */
+#define LGRECO_ENCCL (-5)       /* an NCCL call failed */
+#define LGRECO_ENOMEM (-6)      /* allocation failed (ctx_create only) */
+#define LGRECO_EUNSUPPORTED (-7)
+
+/* compressor families */
+#define LGRECO_QSGD 0     /* bucketed min/max stochastic quantisation, params = bits 1..16 */
+#define LGRECO_TOPK 1     /* per-layer TopK, params = density in ppm (1..1e6) */
+#define LGRECO_POWERSGD 2 /* PowerSGD rank-r, params = rank >= 1 */
+
+/* lgreco_solve flags (R1, R16) */
+#define LGRECO_METRIC_SQ 1u   /* use squared L2 instead of L2 (PAPER.md:180 vs :183) */
+#define LGRECO_DISC_FLOOR 2u  /* floor discretisation instead of ceil */
+
+/* One layer of the flat gradient.  rows*cols == numel for matrices (the view is
+ * (shape[0], numel/shape[0])); rows == 0 marks a vector.  compress == 0 sends the
+ * layer lossless (raw fp32) and excludes it from the DP (R8). */
+typedef struct {
+    int64_t offset, numel;
+    int32_t rows, cols, compress;
+} lgreco_layer;
+
+/* Candidate set C = {c^1..c^K} (Alg.1 input), ascending fidelity. */
+typedef struct {
+    int32_t family;        /* LGRECO_QSGD | LGRECO_TOPK | LGRECO_POWERSGD */
+    int32_t K;             /* number of candidates, 1..255 */
+    const int32_t* params; /* HOST array of K parameters */
+    int32_t qbucket;       /* QSGD bucket size B, a multiple of 128 (<= 8192) */
+    int32_t power_steps;   /* PowerSGD power steps for the profile (5) */
+    uint64_t seed;         /* Philox key (R3) */
+} lgreco_candidates;
+
+/* Result summary of lgreco_solve (device-resident struct). */
+typedef struct {
+    double emax;          /* Emax = sum_l metric(err[l][default_l])  (Alg.1 line 2) */
+    double total_err;     /* sum_l metric(err[l][choice_l]) of the returned plan */
+    int64_t total_bits;   /* sum_l bits[l][choice_l] */
+    int64_t default_bits; /* sum_l bits[l][default_l] */
+    int32_t used_default; /* 1 if the defaults were returned (R20) */
+    int32_t n_active;     /* layers with compress != 0 */
+    int32_t status;       /* LGRECO_OK or LGRECO_ENONFINITE / LGRECO_EINVAL */
+    int32_t pad;
+} lgreco_solve_info;
+
+typedef struct lgreco_ctx lgreco_ctx;
+
+const char* lgreco_last_error(void);
+int32_t lgreco_version(void);
+
+/* Writes a fresh 128-byte ncclUniqueId into h_out (rank 0 calls this and
+ * broadcasts the bytes over its own process group). */
+int lgreco_nccl_unique_id(void* h_out);
+
+/* Create a context for one rank of a `world`-rank data-parallel group.
+ * layers: HOST array of L layers (ascending, non-overlapping); cand: candidate set.
+ * nccl_unique_id: HOST 128 bytes (ignored when world == 1).  Allocates every
+ * workspace the hot calls need and, for world > 1, an NCCL communicator on the
+ * current device.  Owns PowerSGD warm-start state. */
+int lgreco_ctx_create(lgreco_ctx** out, const lgreco_layer* layers, int32_t L,
+                      const lgreco_candidates* cand, int32_t rank, int32_t world,
+                      const void* nccl_unique_id, void* stream);
+void lgreco_ctx_destroy(lgreco_ctx* ctx);
+
+/* Synchronises `stream` and returns LGRECO_ENONFINITE if any kernel saw a
+ * non-finite gradient value since the last check (then clears the flag). */
+int lgreco_ctx_check(lgreco_ctx* ctx, void* stream);
+
+/* Number of kernels this ctx has launched (evidence counter). */
+int64_t lgreco_ctx_launches(lgreco_ctx* ctx);
+
+/* (a2-a4) Profile: for every layer l and candidate j, d_err[l*K+j] = the L2 norm of
+ * x_l - decompress(compress(x_l, c^j)) and d_bits[l*K+j] = its transmitted size in
+ * bits ("simulate the compression/decompression ... without
+ * applying error feedback").  x = d_g + d_ef (d_ef nullable: x = d_g, the paper's
+ * accumulated-gradient mode).  The EF buffer is read, never written.  `step`
+ * selects the Philox counter (QSGD: the same uniforms the compress call of this
+ * step draws, R6).  Lossless layers: err 0, bits 32*numel.
+ * d_err: L*K doubles, d_bits: L*K int64, row-major by layer. */
+int lgreco_profile(lgreco_ctx* ctx, const float* d_g, const float* d_ef, uint64_t step,
+                   double* d_err, int64_t* d_bits, void* stream);
+
+/* Device workspace bytes lgreco_solve needs for (L, K, D). */
+size_t lgreco_solve_workspace_bytes(int32_t L, int32_t K, int32_t D);
+
+/* (a5-a6) Algorithm 1: Emax from the defaults, discretise
+ * errors into D bins of Emax/D (ceil, R16), minimise sum bits s.t. sum disc <= D
+ * by DP over layers, argmin + backtrack; falls back to the defaults when the plan
+ * is not strictly within bits and raw error (R20).  All pointers are DEVICE:
+ * d_err/d_bits L*K (from lgreco_profile or any table), d_default_idx L,
+ * d_compress L (nullable: all active), d_choice L (out; -1 for inactive layers),
+ * d_info (out), d_workspace of lgreco_solve_workspace_bytes(L,K,D) bytes.
+ * Single CTA-resident DP on `stream`; no host synchronisation. */
+int lgreco_solve(const double* d_err, const int64_t* d_bits, int32_t L, int32_t K,
+                 const int32_t* d_default_idx, const int32_t* d_compress, int32_t D,
+                 uint32_t flags, int32_t* d_choice, lgreco_solve_info* d_info,
+                 void* d_workspace, size_t workspace_bytes, void* stream);
+
+/* (a7) Plan agreement: broadcast d_choice (L int32) from rank 0.
+ * No-op when world == 1. */
+int lgreco_plan_broadcast(lgreco_ctx* ctx, int32_t* d_choice, void* stream);
+
+/* (a8-a10) Compress with the plan h_choice (HOST, L candidate indices; ignored for
+ * lossless layers), update error feedback and exchange: d_out (N fp32) receives the
+ * mean over ranks of the decompressed gradients, identical on every rank.
+ * x = d_g + d_ef; d_ef <- x - decompress_stage1(x) (d_ef nullable: no EF).
+ * QSGD: pack -> all-to-all of byte-balanced bucket shards -> ordered dequantise-
+ * sum-requantise on the owner -> all-gather -> decode (R13).  TopK: select ->
+ * all-gather (idx,val) -> ordered sparse sum (R10).  PowerSGD: P=MQ, all-reduce,
+ * orthogonalise, Q=M^T P, all-reduce, out = P Q^T (R12). */
+int lgreco_compress_allreduce(lgreco_ctx* ctx, const int32_t* h_choice, const float* d_g,
+                              float* d_ef, float* d_out, uint64_t step, void* stream);
+
+/* ---- stage entry points (the steps lgreco_compress_allreduce composes; used by
+ * ---- the parity tests to simulate W ranks on one GPU) ------------------------ */
+
+/* Payload bytes S of the packed stage-1 gradient under plan h_choice. */
+int64_t lgreco_payload_bytes(lgreco_ctx* ctx, const int32_t* h_choice);
+
+/* Record (bucket) bounds and byte bounds of the W byte-balanced shards (R13):
+ * h_rec_bounds, h_byte_bounds: W+1 int64 each. */
+int lgreco_shard_bounds(lgreco_ctx* ctx, const int32_t* h_choice, int32_t W,
+                        int64_t* h_rec_bounds, int64_t* h_byte_bounds);
+
+/* QSGD stage 1 (K5): pack x = d_g + d_ef for rank field `rank` into d_payload
+ * (S bytes, record layout R7), update d_ef (nullable), write decoded values to
+ * d_dec (nullable). */
+int lgreco_qsgd_pack(lgreco_ctx* ctx, const int32_t* h_choice, const float* d_g, float* d_ef,
+                     uint8_t* d_payload, float* d_dec, uint32_t rank, uint64_t step, void* stream);
+
+/* QSGD owner reduce (K8): records [rec_begin, rec_end) (one shard).  d_recv holds W
+ * copies of that shard's stage-1 bytes, rank-major (W * shard_bytes); writes the
+ * stage-2 records to d_stage2 + (byte offset of rec_begin). */
+int lgreco_qsgd_reduce(lgreco_ctx* ctx, const int32_t* h_choice, int32_t W, int64_t rec_begin,
+                       int64_t rec_end, const uint8_t* d_recv, uint8_t* d_stage2, uint64_t step,
+                       void* stream);
+
+/* QSGD decode (K9): d_payload (S bytes) -> d_out (N fp32). */
+int lgreco_qsgd_unpack(lgreco_ctx* ctx, const int32_t* h_choice, const uint8_t* d_payload,
+                       float* d_out, void* stream);
+
+/* Debug: Philox4x32-10 of n counters (d_ctr: n*4 u32, key) -> d_out n*4 u32. */
+int lgreco_debug_philox(const uint32_t* d_ctr, uint32_t key0, uint32_t key1, int64_t n,
+                        uint32_t* d_out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LGRECO_H */

@@ -1,0 +1,473 @@
+// api.cu -- the C ABI declared in include/lgreco.h: context, plan layout,
+// dispatch of the kernels and the NCCL exchange (one process per GPU).
+#include <nccl.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.h"
+
+static thread_local char g_err[1024] = "";
+
+void lg_set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+#define LG_NCCL(call)                                                                   \
+  do {                                                                                  \
+    ncclResult_t _r = (call);                                                           \
+    if (_r != ncclSuccess) {                                                            \
+      lg_set_error("%s:%d %s: %s", __FILE__, __LINE__, #call, ncclGetErrorString(_r));  \
+      return LGRECO_ENCCL;                                                              \
+    }                                                                                   \
+  } while (0)
+
+#define LG_TRY(call)                 \
+  do {                               \
+    int _s = (call);                 \
+    if (_s != LGRECO_OK) return _s;  \
+  } while (0)
+
+#define LG_LAUNCH(ctx, call)                                                              \
+  do {                                                                                    \
+    cudaError_t _e = (call);                                                              \
+    if (_e != cudaSuccess) {                                                              \
+      lg_set_error("%s:%d launch %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(_e)); \
+      return LGRECO_ECUDA;                                                                \
+    }                                                                                     \
+  } while (0)
+
+struct lgreco_ctx {
+  int L = 0, rank = 0, world = 1;
+  int family = 0, K = 0, B = 128, power_steps = 5;
+  uint64_t seed = 0;
+  std::vector<lgreco_layer> layers;
+  std::vector<int32_t> params;
+  std::vector<int64_t> bucket0;  // L+1
+  int64_t N = 0, R = 0;
+  int64_t launches = 0;
+  // device tables
+  lg::DevLayer* d_layers = nullptr;
+  int64_t* d_bucket0 = nullptr;
+  float* d_cand_s = nullptr;
+  int32_t* d_params = nullptr;
+  lg::ProfChunk* d_chunks = nullptr;
+  int nchunks = 0;
+  int32_t* d_layer_chunk0 = nullptr;
+  double* d_partial = nullptr;
+  unsigned* d_flag = nullptr;
+  // plan
+  std::vector<int32_t> plan_choice;
+  bool plan_valid = false;
+  std::vector<lg::DevPlan> h_plan_v;
+  lg::DevPlan* h_plan_pinned = nullptr;
+  lg::DevPlan* d_plan = nullptr;
+  cudaEvent_t plan_evt = nullptr;
+  int64_t S = 0;
+  std::vector<int64_t> rec_bounds, byte_bounds;
+  // exchange buffers
+  uint8_t *d_pay1 = nullptr, *d_recv = nullptr, *d_pay2 = nullptr;
+  int64_t pay_cap = 0;
+  ncclComm_t comm = nullptr;
+};
+
+extern "C" {
+
+const char* lgreco_last_error(void) { return g_err; }
+int32_t lgreco_version(void) { return 1; }
+
+int lgreco_nccl_unique_id(void* h_out) {
+  ncclUniqueId id;
+  LG_NCCL(ncclGetUniqueId(&id));
+  memcpy(h_out, &id, sizeof(id));
+  return LGRECO_OK;
+}
+
+}  // extern "C"
+
+static int64_t max_param(const lgreco_ctx* c) {
+  int64_t m = 0;
+  for (int32_t p : c->params) m = std::max<int64_t>(m, p);
+  return m;
+}
+
+static int64_t rec_bytes_full(int bits, int B) { return bits > 0 ? (int64_t)16 * bits * (B / 128) + 8 : (int64_t)4 * B; }
+
+// Host layout of plan `choice` (QSGD): per-layer DevPlan, total bytes S (R7).
+static int qsgd_layout(const lgreco_ctx* c, const int32_t* choice, std::vector<lg::DevPlan>& plan, int64_t& S) {
+  plan.resize(c->L);
+  int64_t off = 0;
+  for (int l = 0; l < c->L; ++l) {
+    const lgreco_layer& ly = c->layers[l];
+    int bits = 0;
+    if (ly.compress) {
+      const int ci = choice[l];
+      if (ci < 0 || ci >= c->K) {
+        lg_set_error("choice[%d]=%d out of range [0,%d)", l, ci, c->K);
+        return LGRECO_EINVAL;
+      }
+      bits = c->params[ci];
+    }
+    const int64_t nb = c->bucket0[l + 1] - c->bucket0[l];
+    plan[l].pay_off = off;
+    plan[l].bits = bits;
+    plan[l].rec_bytes = (int32_t)rec_bytes_full(bits, c->B);
+    off += bits > 0 ? nb * rec_bytes_full(bits, c->B) : 4 * ly.numel;
+  }
+  S = off;
+  return LGRECO_OK;
+}
+
+// byte offset of record r under plan
+static int64_t rec_off(const lgreco_ctx* c, const std::vector<lg::DevPlan>& plan, int64_t r) {
+  if (r >= c->R) return plan.empty() ? 0 : (plan.back().pay_off + (plan.back().bits > 0
+      ? (c->bucket0[c->L] - c->bucket0[c->L - 1]) * (int64_t)plan.back().rec_bytes
+      : 4 * c->layers[c->L - 1].numel));
+  const int l = (int)(std::upper_bound(c->bucket0.begin(), c->bucket0.begin() + c->L, r) - c->bucket0.begin()) - 1;
+  const int64_t jb = r - c->bucket0[l];
+  return plan[l].pay_off + (plan[l].bits > 0 ? jb * (int64_t)plan[l].rec_bytes : jb * 4 * (int64_t)c->B);
+}
+
+static void shard_bounds(const lgreco_ctx* c, const std::vector<lg::DevPlan>& plan, int64_t S, int W,
+                         std::vector<int64_t>& rb, std::vector<int64_t>& bb) {
+  rb.assign(W + 1, 0);
+  bb.assign(W + 1, 0);
+  for (int j = 1; j < W; ++j) {
+    const int64_t target = (int64_t)((__int128)j * S / W);
+    int64_t lo = 0, hi = c->R;  // first r with off(r) >= target
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) / 2;
+      if (rec_off(c, plan, mid) >= target) hi = mid; else lo = mid + 1;
+    }
+    rb[j] = lo;
+    bb[j] = rec_off(c, plan, lo);
+  }
+  rb[W] = c->R;
+  bb[W] = S;
+}
+
+// Upload the plan if it changed (pinned staging guarded by an event).
+static int set_plan(lgreco_ctx* c, const int32_t* choice, cudaStream_t st) {
+  std::vector<int32_t> ch(choice, choice + c->L);
+  for (int l = 0; l < c->L; ++l)
+    if (!c->layers[l].compress) ch[l] = -1;
+  if (c->plan_valid && ch == c->plan_choice) return LGRECO_OK;
+  std::vector<lg::DevPlan> plan;
+  int64_t S = 0;
+  LG_TRY(qsgd_layout(c, choice, plan, S));
+  LG_CUDA(cudaEventSynchronize(c->plan_evt));
+  memcpy(c->h_plan_pinned, plan.data(), sizeof(lg::DevPlan) * c->L);
+  LG_CUDA(cudaMemcpyAsync(c->d_plan, c->h_plan_pinned, sizeof(lg::DevPlan) * c->L, cudaMemcpyHostToDevice, st));
+  LG_CUDA(cudaEventRecord(c->plan_evt, st));
+  c->h_plan_v = plan;
+  c->S = S;
+  shard_bounds(c, plan, S, c->world, c->rec_bounds, c->byte_bounds);
+  c->plan_choice = ch;
+  c->plan_valid = true;
+  return LGRECO_OK;
+}
+
+static void key_of(const lgreco_ctx* c, uint32_t& k0, uint32_t& k1) {
+  k0 = (uint32_t)c->seed;
+  k1 = (uint32_t)(c->seed >> 32);
+}
+
+extern "C" {
+
+int lgreco_ctx_create(lgreco_ctx** out, const lgreco_layer* layers, int32_t L, const lgreco_candidates* cand,
+                      int32_t rank, int32_t world, const void* nccl_unique_id, void* stream) {
+  if (!out || !layers || L <= 0 || !cand || !cand->params) { lg_set_error("null argument or L <= 0"); return LGRECO_EINVAL; }
+  if (world < 1 || rank < 0 || rank >= world) { lg_set_error("bad rank/world %d/%d", rank, world); return LGRECO_EINVAL; }
+  if (cand->K <= 0 || cand->K > 255) { lg_set_error("K=%d out of range", cand->K); return LGRECO_EINVAL; }
+  if (cand->family != LGRECO_QSGD && cand->family != LGRECO_TOPK && cand->family != LGRECO_POWERSGD) {
+    lg_set_error("unknown family %d", cand->family);
+    return LGRECO_EINVAL;
+  }
+  for (int j = 0; j < cand->K; ++j) {
+    const int p = cand->params[j];
+    if ((cand->family == LGRECO_QSGD && (p < 1 || p > 16)) || (cand->family == LGRECO_TOPK && (p < 1 || p > 1000000)) ||
+        (cand->family == LGRECO_POWERSGD && p < 1)) {
+      lg_set_error("candidate %d parameter %d invalid for family %d", j, p, cand->family);
+      return LGRECO_EINVAL;
+    }
+  }
+  if (cand->family == LGRECO_QSGD && (cand->K > 16 || cand->qbucket < 128 || cand->qbucket % 128 || cand->qbucket > 8192)) {
+    lg_set_error("QSGD needs K <= 16 and bucket a multiple of 128 in [128, 8192]");
+    return LGRECO_EINVAL;
+  }
+  int64_t end = 0;
+  for (int l = 0; l < L; ++l) {
+    const lgreco_layer& ly = layers[l];
+    if (ly.numel < 1 || ly.offset < end || (ly.rows > 0 && (int64_t)ly.rows * ly.cols != ly.numel) || ly.rows < 0) {
+      lg_set_error("layer %d invalid (offset %lld numel %lld rows %d cols %d)", l, (long long)ly.offset,
+                   (long long)ly.numel, ly.rows, ly.cols);
+      return LGRECO_EINVAL;
+    }
+    end = ly.offset + ly.numel;
+  }
+  if (cand->family != LGRECO_QSGD) {
+    lg_set_error("family %d not available in this build", cand->family);
+    return LGRECO_EUNSUPPORTED;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  lgreco_ctx* c = new lgreco_ctx();
+  c->L = L; c->rank = rank; c->world = world;
+  c->family = cand->family; c->K = cand->K; c->B = cand->qbucket; c->power_steps = cand->power_steps;
+  c->seed = cand->seed;
+  c->layers.assign(layers, layers + L);
+  c->params.assign(cand->params, cand->params + cand->K);
+  c->N = end;
+  c->bucket0.resize(L + 1);
+  std::vector<lg::DevLayer> dl(L);
+  std::vector<lg::ProfChunk> chunks;
+  std::vector<int32_t> lc0(L + 1);
+  const int CB = 64;  // buckets per profile chunk
+  int64_t gb = 0;
+  for (int l = 0; l < L; ++l) {
+    const int64_t nb = (layers[l].numel + c->B - 1) / c->B;
+    c->bucket0[l] = gb;
+    dl[l] = lg::DevLayer{layers[l].offset, layers[l].numel, gb, layers[l].rows, layers[l].cols, layers[l].compress, 0};
+    lc0[l] = (int32_t)chunks.size();
+    if (layers[l].compress)
+      for (int64_t j = 0; j < nb; j += CB) chunks.push_back(lg::ProfChunk{l, (int32_t)std::min<int64_t>(CB, nb - j), j});
+    gb += nb;
+  }
+  c->bucket0[L] = gb;
+  lc0[L] = (int32_t)chunks.size();
+  c->R = gb;
+  c->nchunks = (int)chunks.size();
+  std::vector<float> cs(c->K);
+  for (int j = 0; j < c->K; ++j) cs[j] = (float)((1u << c->params[j]) - 1u);
+  // max payload over all plans: every compressed layer at the largest candidate
+  const int bmax = (int)max_param(c);
+  int64_t cap = 0;
+  for (int l = 0; l < L; ++l)
+    cap += layers[l].compress ? (c->bucket0[l + 1] - c->bucket0[l]) * rec_bytes_full(bmax, c->B) : 4 * layers[l].numel;
+  c->pay_cap = cap;
+  int st_ = LGRECO_OK;
+  auto fail = [&](int s) { lgreco_ctx_destroy(c); return s; };
+#define LG_ALLOC(ptr, bytes)                                                   \
+  if (cudaMalloc((void**)&(ptr), std::max<size_t>((size_t)(bytes), 16)) != cudaSuccess) { \
+    lg_set_error("cudaMalloc %zu bytes failed", (size_t)(bytes));               \
+    return fail(LGRECO_ENOMEM);                                                \
+  }
+  LG_ALLOC(c->d_layers, sizeof(lg::DevLayer) * L);
+  LG_ALLOC(c->d_bucket0, sizeof(int64_t) * (L + 1));
+  LG_ALLOC(c->d_cand_s, sizeof(float) * c->K);
+  LG_ALLOC(c->d_params, sizeof(int32_t) * c->K);
+  LG_ALLOC(c->d_chunks, sizeof(lg::ProfChunk) * std::max(1, c->nchunks));
+  LG_ALLOC(c->d_layer_chunk0, sizeof(int32_t) * (L + 1));
+  LG_ALLOC(c->d_partial, sizeof(double) * (size_t)std::max(1, c->nchunks) * c->K);
+  LG_ALLOC(c->d_flag, sizeof(unsigned));
+  LG_ALLOC(c->d_plan, sizeof(lg::DevPlan) * L);
+  if (world > 1) {
+    LG_ALLOC(c->d_pay1, cap);
+    LG_ALLOC(c->d_recv, cap + (int64_t)world * 4 * 8192 * 4);
+    LG_ALLOC(c->d_pay2, cap);
+  }
+#undef LG_ALLOC
+  if (cudaMallocHost((void**)&c->h_plan_pinned, sizeof(lg::DevPlan) * L) != cudaSuccess) return fail(LGRECO_ENOMEM);
+  if (cudaEventCreateWithFlags(&c->plan_evt, cudaEventDisableTiming) != cudaSuccess) return fail(LGRECO_ECUDA);
+  cudaError_t e = cudaSuccess;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(c->d_layers, dl.data(), sizeof(lg::DevLayer) * L, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(c->d_bucket0, c->bucket0.data(), sizeof(int64_t) * (L + 1), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(c->d_cand_s, cs.data(), sizeof(float) * c->K, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(c->d_params, c->params.data(), sizeof(int32_t) * c->K, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess && c->nchunks)
+    e = cudaMemcpyAsync(c->d_chunks, chunks.data(), sizeof(lg::ProfChunk) * c->nchunks, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(c->d_layer_chunk0, lc0.data(), sizeof(int32_t) * (L + 1), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(c->d_flag, 0, sizeof(unsigned), st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    lg_set_error("ctx upload: %s", cudaGetErrorString(e));
+    return fail(LGRECO_ECUDA);
+  }
+  if (world > 1) {
+    if (!nccl_unique_id) { lg_set_error("world > 1 needs an ncclUniqueId"); return fail(LGRECO_EINVAL); }
+    ncclUniqueId id;
+    memcpy(&id, nccl_unique_id, sizeof(id));
+    ncclResult_t r = ncclCommInitRank(&c->comm, world, id, rank);
+    if (r != ncclSuccess) {
+      lg_set_error("ncclCommInitRank: %s", ncclGetErrorString(r));
+      c->comm = nullptr;
+      return fail(LGRECO_ENCCL);
+    }
+  }
+  (void)st_;
+  *out = c;
+  return LGRECO_OK;
+}
+
+void lgreco_ctx_destroy(lgreco_ctx* c) {
+  if (!c) return;
+  if (c->comm) ncclCommDestroy(c->comm);
+  cudaFree(c->d_layers); cudaFree(c->d_bucket0); cudaFree(c->d_cand_s); cudaFree(c->d_params);
+  cudaFree(c->d_chunks); cudaFree(c->d_layer_chunk0); cudaFree(c->d_partial); cudaFree(c->d_flag);
+  cudaFree(c->d_plan); cudaFree(c->d_pay1); cudaFree(c->d_recv); cudaFree(c->d_pay2);
+  if (c->h_plan_pinned) cudaFreeHost(c->h_plan_pinned);
+  if (c->plan_evt) cudaEventDestroy(c->plan_evt);
+  delete c;
+}
+
+int lgreco_ctx_check(lgreco_ctx* c, void* stream) {
+  if (!c) return LGRECO_EINVAL;
+  unsigned f = 0;
+  LG_CUDA(cudaMemcpyAsync(&f, c->d_flag, sizeof(unsigned), cudaMemcpyDeviceToHost, (cudaStream_t)stream));
+  LG_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  if (f) {
+    LG_CUDA(cudaMemsetAsync(c->d_flag, 0, sizeof(unsigned), (cudaStream_t)stream));
+    lg_set_error("non-finite gradient value seen");
+    return LGRECO_ENONFINITE;
+  }
+  return LGRECO_OK;
+}
+
+int64_t lgreco_ctx_launches(lgreco_ctx* c) { return c ? c->launches : -1; }
+
+int lgreco_profile(lgreco_ctx* c, const float* d_g, const float* d_ef, uint64_t step, double* d_err,
+                   int64_t* d_bits, void* stream) {
+  if (!c || !d_g || !d_err || !d_bits) { lg_set_error("null argument"); return LGRECO_EINVAL; }
+  cudaStream_t st = (cudaStream_t)stream;
+  uint32_t k0, k1;
+  key_of(c, k0, k1);
+  if (c->family == LGRECO_QSGD) {
+    lg::QProfileArgs a{d_g, d_ef, c->d_layers, c->L, c->d_chunks, c->nchunks, c->d_layer_chunk0,
+                       c->B, c->d_cand_s, c->d_params, c->K, k0, k1, (uint32_t)c->rank, (uint32_t)step,
+                       c->d_partial, d_err, d_bits};
+    LG_LAUNCH(c, lg::launch_qprofile(a, st));
+    c->launches += (c->nchunks > 0) + 1;
+    return LGRECO_OK;
+  }
+  lg_set_error("profile: family %d unsupported", c->family);
+  return LGRECO_EUNSUPPORTED;
+}
+
+size_t lgreco_solve_workspace_bytes(int32_t L, int32_t K, int32_t D) {
+  if (L < 0 || K <= 0 || D <= 0) return 0;
+  return lg::solve_workspace_bytes(L, K, D);
+}
+
+int lgreco_solve(const double* d_err, const int64_t* d_bits, int32_t L, int32_t K, const int32_t* d_default_idx,
+                 const int32_t* d_compress, int32_t D, uint32_t flags, int32_t* d_choice, lgreco_solve_info* d_info,
+                 void* d_ws, size_t ws_bytes, void* stream) {
+  if (L <= 0 || K <= 0 || K > 255 || D <= 0) { lg_set_error("bad L/K/D %d/%d/%d", L, K, D); return LGRECO_EINVAL; }
+  if (!d_err || !d_bits || !d_default_idx || !d_choice || !d_info || !d_ws) { lg_set_error("null argument"); return LGRECO_EINVAL; }
+  if (ws_bytes < lg::solve_workspace_bytes(L, K, D)) { lg_set_error("workspace too small"); return LGRECO_EINVAL; }
+  lg::SolveArgs a{d_err, d_bits, L, K, d_default_idx, d_compress, D, flags, d_choice, d_info, nullptr, nullptr};
+  cudaError_t e = lg::launch_solve(a, d_ws, (cudaStream_t)stream);
+  if (e != cudaSuccess) { lg_set_error("solve launch: %s", cudaGetErrorString(e)); return LGRECO_ECUDA; }
+  return LGRECO_OK;
+}
+
+int lgreco_plan_broadcast(lgreco_ctx* c, int32_t* d_choice, void* stream) {
+  if (!c || !d_choice) return LGRECO_EINVAL;
+  if (c->world == 1) return LGRECO_OK;
+  LG_NCCL(ncclBroadcast(d_choice, d_choice, (size_t)c->L, ncclInt32, 0, c->comm, (cudaStream_t)stream));
+  return LGRECO_OK;
+}
+
+int64_t lgreco_payload_bytes(lgreco_ctx* c, const int32_t* h_choice) {
+  if (!c || !h_choice) return LGRECO_EINVAL;
+  std::vector<lg::DevPlan> plan;
+  int64_t S = 0;
+  int s = qsgd_layout(c, h_choice, plan, S);
+  return s == LGRECO_OK ? S : s;
+}
+
+int lgreco_shard_bounds(lgreco_ctx* c, const int32_t* h_choice, int32_t W, int64_t* h_rb, int64_t* h_bb) {
+  if (!c || !h_choice || W < 1 || !h_rb || !h_bb) return LGRECO_EINVAL;
+  std::vector<lg::DevPlan> plan;
+  int64_t S = 0;
+  LG_TRY(qsgd_layout(c, h_choice, plan, S));
+  std::vector<int64_t> rb, bb;
+  shard_bounds(c, plan, S, W, rb, bb);
+  memcpy(h_rb, rb.data(), sizeof(int64_t) * (W + 1));
+  memcpy(h_bb, bb.data(), sizeof(int64_t) * (W + 1));
+  return LGRECO_OK;
+}
+
+int lgreco_qsgd_pack(lgreco_ctx* c, const int32_t* h_choice, const float* d_g, float* d_ef, uint8_t* d_payload,
+                     float* d_dec, uint32_t rank, uint64_t step, void* stream) {
+  if (!c || !h_choice || !d_g) return LGRECO_EINVAL;
+  if (c->family != LGRECO_QSGD) return LGRECO_EUNSUPPORTED;
+  cudaStream_t st = (cudaStream_t)stream;
+  LG_TRY(set_plan(c, h_choice, st));
+  uint32_t k0, k1;
+  key_of(c, k0, k1);
+  lg::QPackArgs a{d_g, d_ef, d_payload, d_dec, c->d_layers, c->d_plan, c->d_bucket0, c->L, c->R, c->B,
+                  k0, k1, rank, (uint32_t)step, c->d_flag};
+  LG_LAUNCH(c, lg::launch_qpack(a, st));
+  c->launches += 1;
+  return LGRECO_OK;
+}
+
+int lgreco_qsgd_reduce(lgreco_ctx* c, const int32_t* h_choice, int32_t W, int64_t r0, int64_t r1,
+                       const uint8_t* d_recv, uint8_t* d_stage2, uint64_t step, void* stream) {
+  if (!c || !h_choice || W < 1 || r0 < 0 || r1 < r0 || r1 > c->R) return LGRECO_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  LG_TRY(set_plan(c, h_choice, st));
+  const int64_t b0 = rec_off(c, c->h_plan_v, r0), b1 = rec_off(c, c->h_plan_v, r1);
+  uint32_t k0, k1;
+  key_of(c, k0, k1);
+  lg::QReduceArgs a{d_recv, b1 - b0, b0, d_stage2, c->d_layers, c->d_plan, c->d_bucket0, c->L, r0, r1,
+                    c->B, W, k0, k1, (uint32_t)step};
+  LG_LAUNCH(c, lg::launch_qreduce(a, st));
+  c->launches += 1;
+  return LGRECO_OK;
+}
+
+int lgreco_qsgd_unpack(lgreco_ctx* c, const int32_t* h_choice, const uint8_t* d_payload, float* d_out, void* stream) {
+  if (!c || !h_choice || !d_payload || !d_out) return LGRECO_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  LG_TRY(set_plan(c, h_choice, st));
+  lg::QUnpackArgs a{d_payload, d_out, c->d_layers, c->d_plan, c->d_bucket0, c->L, c->R, c->B};
+  LG_LAUNCH(c, lg::launch_qunpack(a, st));
+  c->launches += 1;
+  return LGRECO_OK;
+}
+
+int lgreco_compress_allreduce(lgreco_ctx* c, const int32_t* h_choice, const float* d_g, float* d_ef, float* d_out,
+                              uint64_t step, void* stream) {
+  if (!c || !h_choice || !d_g || !d_out) { lg_set_error("null argument"); return LGRECO_EINVAL; }
+  if (c->family != LGRECO_QSGD) { lg_set_error("family unsupported"); return LGRECO_EUNSUPPORTED; }
+  cudaStream_t st = (cudaStream_t)stream;
+  if (c->world == 1)  // stage 2 skipped (R13): fused pack + EF + decode, nothing leaves the GPU
+    return lgreco_qsgd_pack(c, h_choice, d_g, d_ef, nullptr, d_out, 0u, step, stream);
+  LG_TRY(lgreco_qsgd_pack(c, h_choice, d_g, d_ef, c->d_pay1, nullptr, (uint32_t)c->rank, step, stream));
+  const int W = c->world, me = c->rank;
+  const int64_t mine = c->byte_bounds[me + 1] - c->byte_bounds[me];
+  // all-to-all of stage-1 shards: shard j -> rank j (the reduce-scatter pattern)
+  LG_NCCL(ncclGroupStart());
+  for (int j = 0; j < W; ++j) {
+    const int64_t bj = c->byte_bounds[j + 1] - c->byte_bounds[j];
+    if (bj > 0) LG_NCCL(ncclSend(c->d_pay1 + c->byte_bounds[j], (size_t)bj, ncclUint8, j, c->comm, st));
+    if (mine > 0) LG_NCCL(ncclRecv(c->d_recv + (int64_t)j * mine, (size_t)mine, ncclUint8, j, c->comm, st));
+  }
+  LG_NCCL(ncclGroupEnd());
+  LG_TRY(lgreco_qsgd_reduce(c, h_choice, W, c->rec_bounds[me], c->rec_bounds[me + 1], c->d_recv, c->d_pay2, step, stream));
+  // all-gather of the stage-2 shards (ragged: grouped send/recv)
+  LG_NCCL(ncclGroupStart());
+  for (int j = 0; j < W; ++j) {
+    if (j == me) continue;
+    const int64_t bj = c->byte_bounds[j + 1] - c->byte_bounds[j];
+    if (mine > 0) LG_NCCL(ncclSend(c->d_pay2 + c->byte_bounds[me], (size_t)mine, ncclUint8, j, c->comm, st));
+    if (bj > 0) LG_NCCL(ncclRecv(c->d_pay2 + c->byte_bounds[j], (size_t)bj, ncclUint8, j, c->comm, st));
+  }
+  LG_NCCL(ncclGroupEnd());
+  return lgreco_qsgd_unpack(c, h_choice, c->d_pay2, d_out, stream);
+}
+
+int lgreco_debug_philox(const uint32_t* d_ctr, uint32_t key0, uint32_t key1, int64_t n, uint32_t* d_out, void* stream) {
+  cudaError_t e = lg::launch_philox(d_ctr, key0, key1, n, d_out, (cudaStream_t)stream);
+  if (e != cudaSuccess) { lg_set_error("philox: %s", cudaGetErrorString(e)); return LGRECO_ECUDA; }
+  return LGRECO_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,223 @@
+"""Thin ctypes binding of include/lgreco.h (argument marshalling only).
+
+Every step of the hot path runs in liblgreco.so's CUDA kernels; PyTorch only
+supplies device memory (tensors), the current stream and process groups.  There
+is no CPU fallback: if the library is missing this module raises on import of
+any entry point.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "liblgreco.so")
+
+OK, EINVAL, ENONFINITE, EINFEASIBLE, ECUDA, ENCCL, ENOMEM, EUNSUPPORTED = 0, -1, -2, -3, -4, -5, -6, -7
+QSGD, TOPK, POWERSGD = 0, 1, 2
+METRIC_SQ, DISC_FLOOR = 1, 2
+
+
+class LGrecoError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"lgreco status {status}: {msg}")
+        self.status = status
+
+
+class Layer(C.Structure):
+    _fields_ = [("offset", C.c_int64), ("numel", C.c_int64), ("rows", C.c_int32),
+                ("cols", C.c_int32), ("compress", C.c_int32)]
+
+
+class Candidates(C.Structure):
+    _fields_ = [("family", C.c_int32), ("K", C.c_int32), ("params", C.POINTER(C.c_int32)),
+                ("qbucket", C.c_int32), ("power_steps", C.c_int32), ("seed", C.c_uint64)]
+
+
+class SolveInfo(C.Structure):
+    _fields_ = [("emax", C.c_double), ("total_err", C.c_double), ("total_bits", C.c_int64),
+                ("default_bits", C.c_int64), ("used_default", C.c_int32), ("n_active", C.c_int32),
+                ("status", C.c_int32), ("pad", C.c_int32)]
+
+
+_lib = None
+_VP, _I32, _I64, _U32, _U64 = C.c_void_p, C.c_int32, C.c_int64, C.c_uint32, C.c_uint64
+
+_SIGS = {
+    "lgreco_last_error": (C.c_char_p, []),
+    "lgreco_version": (_I32, []),
+    "lgreco_nccl_unique_id": (C.c_int, [_VP]),
+    "lgreco_ctx_create": (C.c_int, [C.POINTER(_VP), _VP, _I32, _VP, _I32, _I32, _VP, _VP]),
+    "lgreco_ctx_destroy": (None, [_VP]),
+    "lgreco_ctx_check": (C.c_int, [_VP, _VP]),
+    "lgreco_ctx_launches": (_I64, [_VP]),
+    "lgreco_profile": (C.c_int, [_VP, _VP, _VP, _U64, _VP, _VP, _VP]),
+    "lgreco_solve_workspace_bytes": (C.c_size_t, [_I32, _I32, _I32]),
+    "lgreco_solve": (C.c_int, [_VP, _VP, _I32, _I32, _VP, _VP, _I32, _U32, _VP, _VP, _VP, C.c_size_t, _VP]),
+    "lgreco_plan_broadcast": (C.c_int, [_VP, _VP, _VP]),
+    "lgreco_compress_allreduce": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _U64, _VP]),
+    "lgreco_payload_bytes": (_I64, [_VP, _VP]),
+    "lgreco_shard_bounds": (C.c_int, [_VP, _VP, _I32, _VP, _VP]),
+    "lgreco_qsgd_pack": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _U32, _U64, _VP]),
+    "lgreco_qsgd_reduce": (C.c_int, [_VP, _VP, _I32, _I64, _I64, _VP, _VP, _U64, _VP]),
+    "lgreco_qsgd_unpack": (C.c_int, [_VP, _VP, _VP, _VP, _VP]),
+    "lgreco_debug_philox": (C.c_int, [_VP, _U32, _U32, _I64, _VP, _VP]),
+}
+EXPORTED = tuple(_SIGS)
+
+
+def lib():
+    """Load liblgreco.so (fails loudly if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run `make` (or __graft_entry__.build()); "
+                              "there is no CPU fallback")
+        _lib = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(_lib, name)
+            f.restype = res
+            f.argtypes = args
+    return _lib
+
+
+def _check(st, what=""):
+    if st != OK:
+        raise LGrecoError(st, f"{what}: {lib().lgreco_last_error().decode()}")
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    assert t.is_contiguous(), "tensors passed to lgreco must be contiguous"
+    return C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _i32(vals):
+    arr = (C.c_int32 * max(1, len(vals)))(*[int(v) for v in vals])
+    return arr
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(lib().lgreco_nccl_unique_id(buf), "nccl_unique_id")
+    return buf.raw
+
+
+class Context:
+    """Owns an lgreco_ctx (workspaces, NCCL communicator, PowerSGD state)."""
+
+    def __init__(self, layers, family, params, *, qbucket=128, power_steps=5, seed=0, rank=0, world=1,
+                 nccl_id: bytes | None = None, stream=None):
+        self.layers = list(layers)
+        self.L = len(self.layers)
+        self.family = family
+        self.params = [int(p) for p in params]
+        self.K = len(self.params)
+        self.rank, self.world = rank, world
+        self.N = max(l.offset + l.numel for l in self.layers)
+        arr = (Layer * self.L)(*[Layer(l.offset, l.numel, l.rows, l.cols, l.compress) for l in self.layers])
+        self._params_arr = _i32(self.params)
+        cand = Candidates(family, self.K, C.cast(self._params_arr, C.POINTER(C.c_int32)), qbucket, power_steps,
+                          seed)
+        h = C.c_void_p()
+        idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id is not None else None
+        _check(lib().lgreco_ctx_create(C.byref(h), C.cast(arr, C.c_void_p), self.L, C.cast(C.pointer(cand), C.c_void_p),
+                                       rank, world, C.cast(idbuf, C.c_void_p) if idbuf is not None else None,
+                                       _stream(stream)), "ctx_create")
+        self.h = h
+
+    def close(self):
+        if self.h:
+            lib().lgreco_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- hot path ------------------------------------------------------------
+    def profile(self, g, ef, step, err, bits, stream=None):
+        _check(lib().lgreco_profile(self.h, _ptr(g), _ptr(ef), step, _ptr(err), _ptr(bits), _stream(stream)),
+               "profile")
+
+    def compress_allreduce(self, choice, g, ef, out, step, stream=None):
+        _check(lib().lgreco_compress_allreduce(self.h, _i32(choice), _ptr(g), _ptr(ef), _ptr(out), step,
+                                               _stream(stream)), "compress_allreduce")
+
+    def plan_broadcast(self, d_choice, stream=None):
+        _check(lib().lgreco_plan_broadcast(self.h, _ptr(d_choice), _stream(stream)), "plan_broadcast")
+
+    def check(self, stream=None):
+        _check(lib().lgreco_ctx_check(self.h, _stream(stream)), "ctx_check")
+
+    def launches(self) -> int:
+        return int(lib().lgreco_ctx_launches(self.h))
+
+    # ---- stages ----------------------------------------------------------------
+    def payload_bytes(self, choice) -> int:
+        v = int(lib().lgreco_payload_bytes(self.h, _i32(choice)))
+        if v < 0:
+            _check(v, "payload_bytes")
+        return v
+
+    def shard_bounds(self, choice, W):
+        rb = (C.c_int64 * (W + 1))()
+        bb = (C.c_int64 * (W + 1))()
+        _check(lib().lgreco_shard_bounds(self.h, _i32(choice), W, rb, bb), "shard_bounds")
+        return list(rb), list(bb)
+
+    def qsgd_pack(self, choice, g, ef, payload, dec, rank, step, stream=None):
+        _check(lib().lgreco_qsgd_pack(self.h, _i32(choice), _ptr(g), _ptr(ef), _ptr(payload), _ptr(dec), rank, step,
+                                      _stream(stream)), "qsgd_pack")
+
+    def qsgd_reduce(self, choice, W, r0, r1, recv, stage2, step, stream=None):
+        _check(lib().lgreco_qsgd_reduce(self.h, _i32(choice), W, r0, r1, _ptr(recv), _ptr(stage2), step,
+                                        _stream(stream)), "qsgd_reduce")
+
+    def qsgd_unpack(self, choice, payload, out, stream=None):
+        _check(lib().lgreco_qsgd_unpack(self.h, _i32(choice), _ptr(payload), _ptr(out), _stream(stream)),
+               "qsgd_unpack")
+
+
+def solve_workspace_bytes(L, K, D) -> int:
+    return int(lib().lgreco_solve_workspace_bytes(L, K, D))
+
+
+def solve(err, bits, default_idx, compress=None, D=10000, flags=0, choice=None, info=None, workspace=None,
+          stream=None):
+    """Device-side Algorithm 1.  err (L,K) f64, bits (L,K) i64, default_idx (L,) i32,
+    compress (L,) i32 or None, all cuda tensors.  Returns (choice i32 (L,), info u8 tensor)."""
+    L, K = err.shape
+    dev = err.device
+    if choice is None:
+        choice = torch.empty(L, dtype=torch.int32, device=dev)
+    if info is None:
+        info = torch.empty(C.sizeof(SolveInfo), dtype=torch.uint8, device=dev)
+    if workspace is None:
+        workspace = torch.empty(solve_workspace_bytes(L, K, D), dtype=torch.uint8, device=dev)
+    _check(lib().lgreco_solve(_ptr(err), _ptr(bits), L, K, _ptr(default_idx), _ptr(compress), D, flags,
+                              _ptr(choice), _ptr(info), _ptr(workspace), workspace.numel(), _stream(stream)),
+           "solve")
+    return choice, info
+
+
+def read_info(info_tensor) -> SolveInfo:
+    raw = bytes(info_tensor.cpu().numpy().tobytes())
+    return SolveInfo.from_buffer_copy(raw)
+
+
+def debug_philox(ctr, key0, key1, stream=None):
+    n = ctr.numel() // 4
+    out = torch.empty_like(ctr)
+    _check(lib().lgreco_debug_philox(_ptr(ctr), key0, key1, n, _ptr(out), _stream(stream)), "debug_philox")
+    return out

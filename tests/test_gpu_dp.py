@@ -1,0 +1,80 @@
+"""GPU parity of K4 (Algorithm 1 on device) vs the oracle: identical tables in,
+bit-exact choices and summary out."""
+import numpy as np
+import pytest
+import torch
+
+from paper_2210_17357_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def lg():
+    from paper_2210_17357_b200 import lgreco
+    return lgreco
+
+
+def _run(lg, err, bits, dflt, compress, D, flags):
+    e = torch.from_numpy(np.ascontiguousarray(err)).cuda()
+    b = torch.from_numpy(np.ascontiguousarray(bits)).cuda()
+    d = torch.from_numpy(np.asarray(dflt, np.int32)).cuda()
+    c = None if compress is None else torch.from_numpy(np.asarray(compress, np.int32)).cuda()
+    choice, info = lg.solve(e, b, d, c, D=D, flags=flags)
+    torch.cuda.synchronize()
+    return choice.cpu().numpy(), lg.read_info(info)
+
+
+def _table(rng, L, K, zero_frac=0.0):
+    err = np.sort(rng.uniform(0, 1, (L, K)) * rng.uniform(0.01, 10, (L, 1)), 1)[:, ::-1].copy()
+    if zero_frac:
+        err[rng.random((L, K)) < zero_frac] = 0.0
+    bits = np.sort(rng.integers(64, 10 ** 7, (L, K)), 1).astype(np.int64)
+    return err, bits
+
+
+@pytest.mark.parametrize("flags", [0, 1, 2, 3])
+def test_random_tables(lg, ref, flags):
+    rng = np.random.default_rng(flags)
+    for trial in range(40):
+        L = int(rng.integers(1, 30))
+        K = int(rng.integers(1, 9))
+        D = int(rng.choice([1, 7, 100, 1000, 10000]))
+        err, bits = _table(rng, L, K, zero_frac=0.2 if trial % 4 == 0 else 0.0)
+        dflt = rng.integers(0, K, L).astype(np.int32)
+        comp = (rng.random(L) < 0.8).astype(np.int32) if trial % 3 == 0 else None
+        st, c_ref, i_ref = ref.solve(err, bits, dflt, comp, D=D, flags=flags)
+        c_gpu, i_gpu = _run(lg, err, bits, dflt, comp, D, flags)
+        assert st == 0 and i_gpu.status == 0
+        assert list(c_gpu) == list(c_ref)
+        assert (i_gpu.total_bits, i_gpu.default_bits, i_gpu.used_default, i_gpu.n_active) == \
+            (i_ref.total_bits, i_ref.default_bits, i_ref.used_default, i_ref.n_active)
+        assert i_gpu.emax == i_ref.emax and i_gpu.total_err == i_ref.total_err
+
+
+@pytest.mark.parametrize("cfg,K", [("C4", 7), ("C3", 100), ("C5", 100), ("C5", 49)])
+def test_model_sized_tables(lg, ref, cfg, K):
+    layers = W.config_layers(cfg)
+    L = len(layers)
+    rng = np.random.default_rng(K + L)
+    err, bits = _table(rng, L, K)
+    comp = np.array([l.compress for l in layers], np.int32)
+    dflt = np.full(L, K // 3, np.int32)
+    st, c_ref, i_ref = ref.solve(err, bits, dflt, comp, D=10000)
+    c_gpu, i_gpu = _run(lg, err, bits, dflt, comp, 10000, 0)
+    assert list(c_gpu) == list(c_ref) and i_gpu.total_bits == i_ref.total_bits
+    assert i_gpu.total_bits <= i_gpu.default_bits
+
+
+def test_nonfinite_table(lg):
+    err = np.array([[1.0, np.inf], [0.5, 0.2]])
+    bits = np.array([[1, 2], [1, 2]], np.int64)
+    c, info = _run(lg, err, bits, [0, 0], None, 100, 0)
+    assert info.status == lg.ENONFINITE
+
+
+def test_worked_example(lg):
+    err = np.array([[0.0, 1.0, 2.0], [0.0, 2.0, 5.0]])
+    bits = np.array([[100, 60, 20], [120, 100, 40]], np.int64)
+    c, info = _run(lg, err, bits, [1, 1], None, 300, 0)
+    assert list(c) == [2, 0] and info.total_bits == 140

@@ -1,0 +1,205 @@
+"""GPU parity: the CUDA QSGD path (through the C ABI) vs the CPU oracle on the same
+seeded inputs.  Bit-exact for payload bytes, codes, EF and exchange outputs; 1e-5
+relative for the fp64 error norms (BASELINE.json north_star)."""
+import numpy as np
+import pytest
+import torch
+
+from paper_2210_17357_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+BITS = W.QSGD_BITS  # 2..8
+
+
+@pytest.fixture(scope="module")
+def lg():
+    from paper_2210_17357_b200 import lgreco
+    assert torch.cuda.is_available()
+    return lgreco
+
+
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _edge_layers():
+    """Ragged sizes, misaligned offsets, a lossless layer, constant/zero layers."""
+    sizes = [(1, 1), (3, 1), (127, 1), (128, 1), (129, 1), (1000, 1), (4097, 1), (77, 0), (12800, 1), (5, 1)]
+    out, off = [], 0
+    for n, c in sizes:
+        out.append(W.Layer(off, n, 0, 0, c))
+        off += n
+    return out
+
+
+def _edge_data(layers, seed):
+    g, e = W.gaussian_outliers(layers, seed=seed)
+    # constant layer, all-zero layer, on-grid layer, -0.0 entries
+    l = layers[5]
+    g[l.offset:l.offset + l.numel] = 0.5
+    e[l.offset:l.offset + l.numel] = 0.0
+    l = layers[1]
+    g[l.offset:l.offset + l.numel] = 0.0
+    e[l.offset:l.offset + l.numel] = -0.0
+    g[layers[8].offset] = -0.0
+    e[layers[8].offset] = -0.0
+    return g, e
+
+
+def test_philox_matches_kat(lg, ref):
+    ctr = torch.tensor([[0, 0, 0, 0], [0xffffffff] * 4, [0x243f6a88, 0x85a308d3, 0x13198a2e, 0x03707344]],
+                       dtype=torch.int64).to(torch.int32).cuda()
+    keys = [(0, 0), (0xffffffff, 0xffffffff), (0xa4093822, 0x299f31d0)]
+    for i, (k0, k1) in enumerate(keys):
+        out = lg.debug_philox(ctr[i:i + 1].contiguous(), k0, k1).cpu().numpy().view(np.uint32)
+        c = [int(v) & 0xffffffff for v in ctr[i].cpu().numpy().view(np.uint32)]
+        assert tuple(out.ravel()) == ref.philox(c, (k0, k1))
+
+
+@pytest.mark.parametrize("cfg,B,with_ef", [("C1", 128, True), ("C1", 128, False), ("edge", 128, True),
+                                           ("edge", 256, True)])
+def test_profile_parity(lg, ref, cfg, B, with_ef):
+    layers = W.config_layers("C1") if cfg == "C1" else _edge_layers()
+    g, e = (W.gaussian_outliers(layers, seed=3) if cfg == "C1" else _edge_data(layers, 3))
+    if not with_ef:
+        e = None
+    seed, step, rank = 0x1234ABCD5678, 7, 0
+    ctx = lg.Context(layers, lg.QSGD, BITS, qbucket=B, seed=seed)
+    L, K = len(layers), len(BITS)
+    err = torch.empty(L, K, dtype=torch.float64, device="cuda")
+    bits = torch.empty(L, K, dtype=torch.int64, device="cuda")
+    ctx.profile(_dev(g), None if e is None else _dev(e), step, err, bits)
+    ref_err, ref_bits = ref.qsgd_profile(layers, g, e, BITS, B=B, seed=seed, rank=rank, step=step)
+    assert np.array_equal(bits.cpu().numpy(), ref_bits)
+    ge = err.cpu().numpy()
+    rel = np.abs(ge - ref_err) / np.maximum(ref_err, 1e-300)
+    assert np.all((ref_err == 0) == (ge == 0))
+    assert rel.max() <= 1e-5, rel.max()
+
+
+def _choice_for(layers, rng):
+    return [int(rng.integers(0, len(BITS))) if l.compress else -1 for l in layers]
+
+
+@pytest.mark.parametrize("cfg,B", [("C1", 128), ("edge", 128), ("edge", 256)])
+def test_pack_parity(lg, ref, cfg, B):
+    layers = W.config_layers("C1") if cfg == "C1" else _edge_layers()
+    g, e = (W.gaussian_outliers(layers, seed=5) if cfg == "C1" else _edge_data(layers, 5))
+    rng = np.random.default_rng(1)
+    choice = _choice_for(layers, rng)
+    lbits = [BITS[c] if l.compress else 0 for c, l in zip(choice, layers)]
+    seed, step, rank = 99, 3, 2
+    ctx = lg.Context(layers, lg.QSGD, BITS, qbucket=B, seed=seed)
+    S = ctx.payload_bytes(choice)
+    pay_ref, e_ref, dec_ref = ref.qsgd_pack(layers, lbits, g, e, B=B, seed=seed, rank=rank, step=step, want_dec=True)
+    assert S == pay_ref.size
+    gd, ed = _dev(g), _dev(e)
+    pay = torch.zeros(S, dtype=torch.uint8, device="cuda")
+    dec = torch.empty_like(gd)
+    ctx.qsgd_pack(choice, gd, ed, pay, dec, rank, step)
+    torch.cuda.synchronize()
+    assert np.array_equal(pay.cpu().numpy(), pay_ref)
+    assert np.array_equal(ed.cpu().numpy().view(np.uint32), e_ref.view(np.uint32))
+    assert np.array_equal(dec.cpu().numpy().view(np.uint32), dec_ref.view(np.uint32))
+    out = torch.empty_like(gd)
+    ctx.qsgd_unpack(choice, pay, out)
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), dec_ref.view(np.uint32))
+    ctx.check()
+
+
+@pytest.mark.parametrize("Wn", [1, 2, 3, 4, 8])
+def test_exchange_parity_simulated_ranks(lg, ref, Wn):
+    """W ranks simulated on one GPU through the stage entry points: pack per rank,
+    byte-balanced shards (all-to-all as copies), owner reduce, all-gather, decode."""
+    layers = _edge_layers()
+    rng = np.random.default_rng(Wn)
+    choice = _choice_for(layers, rng)
+    lbits = [BITS[c] if l.compress else 0 for c, l in zip(choice, layers)]
+    seed, step, B = 4242, 11, 128
+    gs, es = [], []
+    for w in range(Wn):
+        g, e = _edge_data(layers, 100 + w)
+        gs.append(g)
+        es.append(e)
+    out_ref, es_ref, p1_ref, p2_ref = ref.qsgd_allreduce(layers, lbits, gs, es, B=B, seed=seed, step=step)
+    ctx = lg.Context(layers, lg.QSGD, BITS, qbucket=B, seed=seed)
+    S = ctx.payload_bytes(choice)
+    rb, bb = ctx.shard_bounds(choice, Wn)
+    rb_ref, bb_ref = ref.shard_bounds(layers, lbits, B, Wn)
+    assert list(rb) == list(rb_ref) and list(bb) == list(bb_ref)
+    pays, eds = [], []
+    for w in range(Wn):
+        pay = torch.zeros(S, dtype=torch.uint8, device="cuda")
+        ed = _dev(es[w])
+        ctx.qsgd_pack(choice, _dev(gs[w]), ed, pay, None, w, step)
+        pays.append(pay)
+        eds.append(ed)
+    for w in range(Wn):
+        assert np.array_equal(pays[w].cpu().numpy(), p1_ref[w])
+        assert np.array_equal(eds[w].cpu().numpy().view(np.uint32), es_ref[w].view(np.uint32))
+    out = torch.empty(len(gs[0]), dtype=torch.float32, device="cuda")
+    if Wn == 1:
+        ctx.qsgd_unpack(choice, pays[0], out)
+    else:
+        stage2 = torch.zeros(S, dtype=torch.uint8, device="cuda")
+        for j in range(Wn):
+            nbytes = bb[j + 1] - bb[j]
+            recv = torch.cat([pays[w][bb[j]:bb[j + 1]] for w in range(Wn)]) if nbytes else \
+                torch.zeros(1, dtype=torch.uint8, device="cuda")
+            ctx.qsgd_reduce(choice, Wn, rb[j], rb[j + 1], recv.contiguous(), stage2, step)
+        torch.cuda.synchronize()
+        assert np.array_equal(stage2.cpu().numpy(), p2_ref)
+        ctx.qsgd_unpack(choice, stage2, out)
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), out_ref.view(np.uint32))
+
+
+def test_compress_allreduce_w1(lg, ref):
+    layers = W.config_layers("C1")
+    g, e = W.gaussian_outliers(layers, seed=8)
+    choice = _choice_for(layers, np.random.default_rng(8))
+    lbits = [BITS[c] for c in choice]
+    ctx = lg.Context(layers, lg.QSGD, BITS, seed=5)
+    gd, ed = _dev(g), _dev(e)
+    out = torch.empty_like(gd)
+    ctx.compress_allreduce(choice, gd, ed, out, 2)
+    out_ref, es_ref, _, _ = ref.qsgd_allreduce(layers, lbits, [g], [e], seed=5, step=2)
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), out_ref.view(np.uint32))
+    assert np.array_equal(ed.cpu().numpy().view(np.uint32), es_ref[0].view(np.uint32))
+
+
+def test_nonfinite_flag(lg):
+    layers = W.config_layers("C1")[:3]
+    g, e = W.gaussian_outliers(layers, seed=1)
+    g[5] = np.nan
+    ctx = lg.Context(layers, lg.QSGD, BITS)
+    out = torch.empty(len(g), dtype=torch.float32, device="cuda")
+    ctx.compress_allreduce([2, 2, 2], _dev(g), _dev(e), out, 0)
+    with pytest.raises(lg.LGrecoError) as ei:
+        ctx.check()
+    assert ei.value.status == lg.ENONFINITE
+    ctx.check()  # flag cleared
+
+
+def test_c4_full_size(lg, ref):
+    """C4 (ResNet-50, 25.6M fp32) at full size in the launch configuration bench.py
+    times: profile err/bits vs the oracle on every layer, pack + EF + decode bitwise."""
+    layers = W.config_layers("C4")
+    g, e = W.gaussian_outliers(layers, seed=W.rank_seed(0x5EED, 0))
+    ctx = lg.Context(layers, lg.QSGD, BITS, seed=0x5EED)
+    L, K = len(layers), len(BITS)
+    gd, ed = _dev(g), _dev(e)
+    err = torch.empty(L, K, dtype=torch.float64, device="cuda")
+    bits = torch.empty(L, K, dtype=torch.int64, device="cuda")
+    ctx.profile(gd, ed, 0, err, bits)
+    ref_err, ref_bits = ref.qsgd_profile(layers, g, e, BITS, seed=0x5EED, step=0)
+    assert np.array_equal(bits.cpu().numpy(), ref_bits)
+    ge = err.cpu().numpy()
+    assert (np.abs(ge - ref_err) / np.maximum(ref_err, 1e-300)).max() <= 1e-5
+    choice = [BITS.index(4) if l.compress else -1 for l in layers]
+    out = torch.empty_like(gd)
+    ctx.compress_allreduce(choice, gd, ed, out, 0)
+    lbits = [4 if l.compress else 0 for l in layers]
+    out_ref, es_ref, _, _ = ref.qsgd_allreduce(layers, lbits, [g], [e], seed=0x5EED, step=0)
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), out_ref.view(np.uint32))
+    assert np.array_equal(ed.cpu().numpy().view(np.uint32), es_ref[0].view(np.uint32))
