@@ -153,6 +153,7 @@ int ref_quantize_bucket(const float* x, int32_t nvalid, int32_t bits, const floa
 /*   compressed layer, b bits, bucket B=128m: (4*b*m) u32 code words, mn, unit */
 /*     word (t*b + p)*4 + s, bit l  <-  bit p of code of element 128t+4l+s     */
 /*   lossless layer: records of B raw fp32 values (last one partial)           */
+/*   each layer's block of records starts at a 16-byte boundary (zero pad)    */
 /* ------------------------------------------------------------------------ */
 static int64_t nbuckets(int64_t n, int32_t B) { return (n + B - 1) / B; }
 
@@ -170,6 +171,7 @@ int64_t ref_layout(const ref_layer* layers, int32_t L, const int32_t* lbits, int
         int64_t nb = nbuckets(layers[l].numel, B);
         gb += nb;
         off += lbits[l] > 0 ? nb * rec_bytes_full(lbits[l], B) : 4 * layers[l].numel;
+        off = (off + 15) & ~(int64_t)15; /* each layer's records start 16-byte aligned (R7) */
     }
     bucket_start[L] = gb;
     byte_off[L] = off;

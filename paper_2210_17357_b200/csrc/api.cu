@@ -58,8 +58,11 @@ struct lgreco_ctx {
   int64_t* d_bucket0 = nullptr;
   float* d_cand_s = nullptr;
   int32_t* d_params = nullptr;
-  lg::ProfChunk* d_chunks = nullptr;
+  lg::ProfChunk* d_chunks = nullptr;      // chunks of compressed layers (profile)
   int nchunks = 0;
+  lg::ProfChunk* d_chunks_all = nullptr;  // chunks of every layer (pack / unpack)
+  int nchunks_all = 0;
+  lg::CandS cs{};
   int32_t* d_layer_chunk0 = nullptr;
   double* d_partial = nullptr;
   unsigned* d_flag = nullptr;
@@ -120,16 +123,15 @@ static int qsgd_layout(const lgreco_ctx* c, const int32_t* choice, std::vector<l
     plan[l].bits = bits;
     plan[l].rec_bytes = (int32_t)rec_bytes_full(bits, c->B);
     off += bits > 0 ? nb * rec_bytes_full(bits, c->B) : 4 * ly.numel;
+    off = (off + 15) & ~(int64_t)15;  // every layer's records start 16-byte aligned (R7)
   }
   S = off;
   return LGRECO_OK;
 }
 
 // byte offset of record r under plan
-static int64_t rec_off(const lgreco_ctx* c, const std::vector<lg::DevPlan>& plan, int64_t r) {
-  if (r >= c->R) return plan.empty() ? 0 : (plan.back().pay_off + (plan.back().bits > 0
-      ? (c->bucket0[c->L] - c->bucket0[c->L - 1]) * (int64_t)plan.back().rec_bytes
-      : 4 * c->layers[c->L - 1].numel));
+static int64_t rec_off(const lgreco_ctx* c, const std::vector<lg::DevPlan>& plan, int64_t r, int64_t S) {
+  if (r >= c->R) return S;
   const int l = (int)(std::upper_bound(c->bucket0.begin(), c->bucket0.begin() + c->L, r) - c->bucket0.begin()) - 1;
   const int64_t jb = r - c->bucket0[l];
   return plan[l].pay_off + (plan[l].bits > 0 ? jb * (int64_t)plan[l].rec_bytes : jb * 4 * (int64_t)c->B);
@@ -144,10 +146,10 @@ static void shard_bounds(const lgreco_ctx* c, const std::vector<lg::DevPlan>& pl
     int64_t lo = 0, hi = c->R;  // first r with off(r) >= target
     while (lo < hi) {
       const int64_t mid = (lo + hi) / 2;
-      if (rec_off(c, plan, mid) >= target) hi = mid; else lo = mid + 1;
+      if (rec_off(c, plan, mid, S) >= target) hi = mid; else lo = mid + 1;
     }
     rb[j] = lo;
-    bb[j] = rec_off(c, plan, lo);
+    bb[j] = rec_off(c, plan, lo, S);
   }
   rb[W] = c->R;
   bb[W] = S;
@@ -226,7 +228,7 @@ int lgreco_ctx_create(lgreco_ctx** out, const lgreco_layer* layers, int32_t L, c
   c->N = end;
   c->bucket0.resize(L + 1);
   std::vector<lg::DevLayer> dl(L);
-  std::vector<lg::ProfChunk> chunks;
+  std::vector<lg::ProfChunk> chunks, chunks_all;
   std::vector<int32_t> lc0(L + 1);
   const int CB = 64;  // buckets per profile chunk
   int64_t gb = 0;
@@ -235,23 +237,27 @@ int lgreco_ctx_create(lgreco_ctx** out, const lgreco_layer* layers, int32_t L, c
     c->bucket0[l] = gb;
     dl[l] = lg::DevLayer{layers[l].offset, layers[l].numel, gb, layers[l].rows, layers[l].cols, layers[l].compress, 0};
     lc0[l] = (int32_t)chunks.size();
-    if (layers[l].compress)
-      for (int64_t j = 0; j < nb; j += CB) chunks.push_back(lg::ProfChunk{l, (int32_t)std::min<int64_t>(CB, nb - j), j});
+    for (int64_t j = 0; j < nb; j += CB) {
+      const lg::ProfChunk ch{l, (int32_t)std::min<int64_t>(CB, nb - j), j};
+      if (layers[l].compress) chunks.push_back(ch);
+      chunks_all.push_back(ch);
+    }
     gb += nb;
   }
   c->bucket0[L] = gb;
   lc0[L] = (int32_t)chunks.size();
   c->R = gb;
   c->nchunks = (int)chunks.size();
+  c->nchunks_all = (int)chunks_all.size();
   std::vector<float> cs(c->K);
-  for (int j = 0; j < c->K; ++j) cs[j] = (float)((1u << c->params[j]) - 1u);
+  for (int j = 0; j < c->K; ++j) cs[j] = c->family == LGRECO_QSGD ? (float)((1u << c->params[j]) - 1u) : 0.f;
+  for (int j = 0; j < c->K && j < 16; ++j) c->cs.s[j] = cs[j];
   // max payload over all plans: every compressed layer at the largest candidate
   const int bmax = (int)max_param(c);
   int64_t cap = 0;
   for (int l = 0; l < L; ++l)
-    cap += layers[l].compress ? (c->bucket0[l + 1] - c->bucket0[l]) * rec_bytes_full(bmax, c->B) : 4 * layers[l].numel;
+    cap += (layers[l].compress ? (c->bucket0[l + 1] - c->bucket0[l]) * rec_bytes_full(bmax, c->B) : 4 * layers[l].numel) + 16;
   c->pay_cap = cap;
-  int st_ = LGRECO_OK;
   auto fail = [&](int s) { lgreco_ctx_destroy(c); return s; };
 #define LG_ALLOC(ptr, bytes)                                                   \
   if (cudaMalloc((void**)&(ptr), std::max<size_t>((size_t)(bytes), 16)) != cudaSuccess) { \
@@ -263,6 +269,7 @@ int lgreco_ctx_create(lgreco_ctx** out, const lgreco_layer* layers, int32_t L, c
   LG_ALLOC(c->d_cand_s, sizeof(float) * c->K);
   LG_ALLOC(c->d_params, sizeof(int32_t) * c->K);
   LG_ALLOC(c->d_chunks, sizeof(lg::ProfChunk) * std::max(1, c->nchunks));
+  LG_ALLOC(c->d_chunks_all, sizeof(lg::ProfChunk) * std::max(1, c->nchunks_all));
   LG_ALLOC(c->d_layer_chunk0, sizeof(int32_t) * (L + 1));
   LG_ALLOC(c->d_partial, sizeof(double) * (size_t)std::max(1, c->nchunks) * c->K);
   LG_ALLOC(c->d_flag, sizeof(unsigned));
@@ -282,6 +289,9 @@ int lgreco_ctx_create(lgreco_ctx** out, const lgreco_layer* layers, int32_t L, c
   if (e == cudaSuccess) e = cudaMemcpyAsync(c->d_params, c->params.data(), sizeof(int32_t) * c->K, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess && c->nchunks)
     e = cudaMemcpyAsync(c->d_chunks, chunks.data(), sizeof(lg::ProfChunk) * c->nchunks, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess && c->nchunks_all)
+    e = cudaMemcpyAsync(c->d_chunks_all, chunks_all.data(), sizeof(lg::ProfChunk) * c->nchunks_all,
+                        cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = cudaMemcpyAsync(c->d_layer_chunk0, lc0.data(), sizeof(int32_t) * (L + 1), cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(c->d_flag, 0, sizeof(unsigned), st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
@@ -300,7 +310,6 @@ int lgreco_ctx_create(lgreco_ctx** out, const lgreco_layer* layers, int32_t L, c
       return fail(LGRECO_ENCCL);
     }
   }
-  (void)st_;
   *out = c;
   return LGRECO_OK;
 }
@@ -309,7 +318,7 @@ void lgreco_ctx_destroy(lgreco_ctx* c) {
   if (!c) return;
   if (c->comm) ncclCommDestroy(c->comm);
   cudaFree(c->d_layers); cudaFree(c->d_bucket0); cudaFree(c->d_cand_s); cudaFree(c->d_params);
-  cudaFree(c->d_chunks); cudaFree(c->d_layer_chunk0); cudaFree(c->d_partial); cudaFree(c->d_flag);
+  cudaFree(c->d_chunks); cudaFree(c->d_chunks_all); cudaFree(c->d_layer_chunk0); cudaFree(c->d_partial); cudaFree(c->d_flag);
   cudaFree(c->d_plan); cudaFree(c->d_pay1); cudaFree(c->d_recv); cudaFree(c->d_pay2);
   if (c->h_plan_pinned) cudaFreeHost(c->h_plan_pinned);
   if (c->plan_evt) cudaEventDestroy(c->plan_evt);
@@ -339,7 +348,7 @@ int lgreco_profile(lgreco_ctx* c, const float* d_g, const float* d_ef, uint64_t 
   key_of(c, k0, k1);
   if (c->family == LGRECO_QSGD) {
     lg::QProfileArgs a{d_g, d_ef, c->d_layers, c->L, c->d_chunks, c->nchunks, c->d_layer_chunk0,
-                       c->B, c->d_cand_s, c->d_params, c->K, k0, k1, (uint32_t)c->rank, (uint32_t)step,
+                       c->B, c->cs, c->d_params, c->K, k0, k1, (uint32_t)c->rank, (uint32_t)step,
                        c->d_partial, d_err, d_bits};
     LG_LAUNCH(c, lg::launch_qprofile(a, st));
     c->launches += (c->nchunks > 0) + 1;
@@ -401,7 +410,7 @@ int lgreco_qsgd_pack(lgreco_ctx* c, const int32_t* h_choice, const float* d_g, f
   LG_TRY(set_plan(c, h_choice, st));
   uint32_t k0, k1;
   key_of(c, k0, k1);
-  lg::QPackArgs a{d_g, d_ef, d_payload, d_dec, c->d_layers, c->d_plan, c->d_bucket0, c->L, c->R, c->B,
+  lg::QPackArgs a{d_g, d_ef, d_payload, d_dec, c->d_layers, c->d_plan, c->d_chunks_all, c->nchunks_all, c->B,
                   k0, k1, rank, (uint32_t)step, c->d_flag};
   LG_LAUNCH(c, lg::launch_qpack(a, st));
   c->launches += 1;
@@ -413,7 +422,7 @@ int lgreco_qsgd_reduce(lgreco_ctx* c, const int32_t* h_choice, int32_t W, int64_
   if (!c || !h_choice || W < 1 || r0 < 0 || r1 < r0 || r1 > c->R) return LGRECO_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
   LG_TRY(set_plan(c, h_choice, st));
-  const int64_t b0 = rec_off(c, c->h_plan_v, r0), b1 = rec_off(c, c->h_plan_v, r1);
+  const int64_t b0 = rec_off(c, c->h_plan_v, r0, c->S), b1 = rec_off(c, c->h_plan_v, r1, c->S);
   uint32_t k0, k1;
   key_of(c, k0, k1);
   lg::QReduceArgs a{d_recv, b1 - b0, b0, d_stage2, c->d_layers, c->d_plan, c->d_bucket0, c->L, r0, r1,
@@ -427,7 +436,7 @@ int lgreco_qsgd_unpack(lgreco_ctx* c, const int32_t* h_choice, const uint8_t* d_
   if (!c || !h_choice || !d_payload || !d_out) return LGRECO_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
   LG_TRY(set_plan(c, h_choice, st));
-  lg::QUnpackArgs a{d_payload, d_out, c->d_layers, c->d_plan, c->d_bucket0, c->L, c->R, c->B};
+  lg::QUnpackArgs a{d_payload, d_out, c->d_layers, c->d_plan, c->d_chunks_all, c->nchunks_all, c->B};
   LG_LAUNCH(c, lg::launch_qunpack(a, st));
   c->launches += 1;
   return LGRECO_OK;

@@ -11,6 +11,8 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -31,7 +33,7 @@ __device__ __forceinline__ int32_t discretise(double m, double emax, int D, uint
 }
 
 __global__ void __launch_bounds__(DP_THREADS, 1)
-k_solve(const double* __restrict__ err, const int64_t* __restrict__ bits, int L, int K,
+k_solve_generic(const double* __restrict__ err, const int64_t* __restrict__ bits, int L, int K,
         const int32_t* __restrict__ default_idx, const int32_t* __restrict__ compress, int D, uint32_t flags,
         int32_t* __restrict__ choice, lgreco_solve_info* __restrict__ info, uint8_t* __restrict__ PD,
         int32_t* __restrict__ act, int64_t* __restrict__ grows, int rows_in_smem) {
@@ -171,6 +173,251 @@ k_solve(const double* __restrict__ err, const int64_t* __restrict__ bits, int L,
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Fast path: cells in registers, packed (value << cbits | c) keys.
+// Costs are divided by g = gcd of all active costs (an exact order-preserving
+// rescale), so the DP runs on 32-bit keys whenever the largest possible plan
+// cost fits in 31 - cbits bits, else on 64-bit keys.  min() over packed keys
+// picks the smallest cost and, among equal costs, the first candidate in list
+// order -- exactly Alg.1's strict-< update in candidate order (R19).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t gcd64(uint64_t a, uint64_t b) {
+  while (b) { const uint64_t t = a % b; a = b; b = t; }
+  return a;
+}
+
+template <int CPT>
+__global__ void __launch_bounds__(DP_THREADS, 1)
+k_solve_fast(const double* __restrict__ err, const int64_t* __restrict__ bits, int L, int K,
+             const int32_t* __restrict__ default_idx, const int32_t* __restrict__ compress, int D, uint32_t flags,
+             int32_t* __restrict__ choice, lgreco_solve_info* __restrict__ info, uint8_t* __restrict__ PD,
+             int32_t* __restrict__ act) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int32_t s_disc[256];
+  __shared__ uint64_t s_add[256];
+  __shared__ int s_La, s_status, s_wide, s_cbits;
+  __shared__ double s_emax;
+  __shared__ int64_t s_defbits;
+  __shared__ uint64_t s_g[DP_THREADS / 32];
+  __shared__ uint64_t s_redk[DP_THREADS / 32];
+  __shared__ int s_rede[DP_THREADS / 32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  // ---- Alg.1 lines 1-2: active layers, Emax, default bits (thread 0, layer order)
+  if (tid == 0) {
+    int La = 0, status = LGRECO_OK;
+    double emax = 0.0;
+    int64_t defb = 0;
+    for (int l = 0; l < L; ++l) {
+      choice[l] = -1;
+      if (compress && !compress[l]) continue;
+      const int d = default_idx[l];
+      if (d < 0 || d >= K) { status = LGRECO_EINVAL; continue; }
+      act[La++] = l;
+      emax = __dadd_rn(emax, metric(err[(int64_t)l * K + d], flags));
+      defb += bits[(int64_t)l * K + d];
+    }
+    s_La = La; s_status = status; s_emax = emax; s_defbits = defb;
+    int cb = 0;
+    while ((1 << cb) < K) ++cb;
+    s_cbits = cb;
+  }
+  __syncthreads();
+  const int La = s_La;
+  // ---- validation + gcd + max plan cost (all threads)
+  uint64_t gg = 0;
+  int bad = 0;
+  for (int i = tid; i < La * K; i += DP_THREADS) {
+    const int l = act[i / K];
+    const double v = err[(int64_t)l * K + (i % K)];
+    const int64_t b = bits[(int64_t)l * K + (i % K)];
+    if (!isfinite(v) || v < 0.0) bad |= 1;
+    if (b < 0) bad |= 2;
+    gg = gcd64(gg, (uint64_t)(b < 0 ? 0 : b));
+  }
+  bad = __reduce_or_sync(LG_FULL, bad);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) gg = gcd64(gg, __shfl_xor_sync(LG_FULL, gg, o));
+  if (lane == 0) { s_g[warp] = gg; if (bad) atomicOr(&s_status, bad & 1 ? LGRECO_ENONFINITE : LGRECO_EINVAL); }
+  __syncthreads();
+  if (tid == 0) {
+    uint64_t g = 0;
+    for (int w = 0; w < DP_THREADS / 32; ++w) g = gcd64(g, s_g[w]);
+    if (g == 0) g = 1;
+    s_g[0] = g;
+    // largest reachable plan cost in units of g
+    uint64_t mx = 0;
+    for (int a = 0; a < La; ++a) {
+      uint64_t m = 0;
+      for (int c = 0; c < K; ++c) m = max(m, (uint64_t)bits[(int64_t)act[a] * K + c] / g);
+      mx += m;
+    }
+    s_wide = (mx >= (1ull << (31 - s_cbits))) ? 1 : 0;
+    if (mx >= (1ull << (62 - s_cbits))) s_status = LGRECO_EINVAL;
+    if (s_status != LGRECO_OK && s_status != LGRECO_ENONFINITE && s_status != LGRECO_EINVAL) s_status = LGRECO_EINVAL;
+  }
+  __syncthreads();
+  if (s_status != LGRECO_OK || La == 0) {
+    if (tid == 0) {
+      lgreco_solve_info inf = {};
+      inf.n_active = La;
+      inf.status = s_status;
+      *info = inf;
+    }
+    return;
+  }
+  const double emax = s_emax;
+  const uint64_t g = s_g[0];
+  const int cbits = s_cbits;
+  const uint64_t cmask = (1ull << cbits) - 1;
+  const bool wide = s_wide;
+  const int W1 = D + 1;
+  // rows: 32-bit keys -> two rows padded with W1 INF entries in front (no bounds test);
+  //       64-bit keys -> two rows with one INF sentinel at index -1 (clamped index)
+  // (+ DP_THREADS tail entries: the last register cell of a thread may lie past D)
+  const int row32 = 2 * W1 + DP_THREADS, row64 = W1 + 1 + DP_THREADS;
+  uint32_t* r32a = reinterpret_cast<uint32_t*>(smem_raw);
+  uint32_t* r32b = r32a + row32;
+  uint64_t* r64a = reinterpret_cast<uint64_t*>(smem_raw);
+  uint64_t* r64b = r64a + row64;
+  const uint32_t INF32 = 0x7FFFFFFFu;
+  const uint64_t INF64 = 1ull << 62;
+  if (!wide) {
+    for (int i = tid; i < row32; i += DP_THREADS) { r32a[i] = INF32; r32b[i] = INF32; }
+    __syncthreads();
+    if (tid == 0) r32a[W1] = 0;  // virtual layer 0: DP0[0] = 0 (R18)
+  } else {
+    for (int i = tid; i < row64; i += DP_THREADS) { r64a[i] = INF64; r64b[i] = INF64; }
+    __syncthreads();
+    if (tid == 0) r64a[1] = 0;
+  }
+  __syncthreads();
+  int cur_is_b = 1;
+  for (int a = 0; a < La; ++a) {
+    const int l = act[a];
+    if (tid < K) {
+      const int d = discretise(metric(err[(int64_t)l * K + tid], flags), emax, D, flags);
+      s_disc[tid] = d;
+      s_add[tid] = (((uint64_t)bits[(int64_t)l * K + tid] / g) << cbits) | (uint64_t)tid;
+    }
+    __syncthreads();
+    uint8_t* pdrow = PD + (int64_t)a * W1;
+    if (!wide) {
+      const uint32_t* prev = (cur_is_b ? r32a : r32b) + W1;  // index e-d >= -W1 is padded
+      uint32_t* cur = (cur_is_b ? r32b : r32a) + W1;
+      uint32_t best[CPT];
+#pragma unroll
+      for (int i = 0; i < CPT; ++i) best[i] = 0xFFFFFFFFu;
+      for (int c = 0; c < K; ++c) {
+        const int d = s_disc[c];
+        if (d < 0) continue;
+        const uint32_t ak = (uint32_t)s_add[c];
+        const uint32_t* pv = prev - d + tid;
+#pragma unroll
+        for (int i = 0; i < CPT; ++i) best[i] = min(best[i], pv[i * DP_THREADS] + ak);
+      }
+#pragma unroll
+      for (int i = 0; i < CPT; ++i) {
+        const int e = tid + i * DP_THREADS;
+        if (e < W1) {
+          const uint32_t k = best[i];
+          cur[e] = (k >= INF32) ? INF32 : (k & ~(uint32_t)cmask);
+          pdrow[e] = (uint8_t)((k >= INF32) ? 0 : (k & (uint32_t)cmask));
+        }
+      }
+    } else {
+      const uint64_t* prev = (cur_is_b ? r64a : r64b) + 1;  // index -1 is the INF sentinel
+      uint64_t* cur = (cur_is_b ? r64b : r64a) + 1;
+      uint64_t best[CPT];
+#pragma unroll
+      for (int i = 0; i < CPT; ++i) best[i] = ~0ull;
+      for (int c = 0; c < K; ++c) {
+        const int d = s_disc[c];
+        if (d < 0) continue;
+        const uint64_t ak = s_add[c];
+#pragma unroll
+        for (int i = 0; i < CPT; ++i) {
+          const int idx = max(tid + i * DP_THREADS - d, -1);
+          best[i] = min(best[i], prev[idx] + ak);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < CPT; ++i) {
+        const int e = tid + i * DP_THREADS;
+        if (e < W1) {
+          const uint64_t k = best[i];
+          cur[e] = (k >= INF64) ? INF64 : (k & ~cmask);
+          pdrow[e] = (uint8_t)((k >= INF64) ? 0 : (k & cmask));
+        }
+      }
+    }
+    cur_is_b ^= 1;
+    __syncthreads();
+  }
+  // ---- line 23: argmin of the last row, smallest e on ties
+  uint64_t bk = ~0ull;
+  int be = 0x7fffffff;
+  for (int e = tid; e < W1; e += DP_THREADS) {
+    uint64_t v;
+    if (!wide) { const uint32_t x = ((cur_is_b ? r32a : r32b) + W1)[e]; v = (x >= INF32) ? ~0ull : x; }
+    else { const uint64_t x = ((cur_is_b ? r64a : r64b) + 1)[e]; v = (x >= INF64) ? ~0ull : x; }
+    if (v < bk) { bk = v; be = e; }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const uint64_t ov = __shfl_xor_sync(LG_FULL, bk, o);
+    const int oe = __shfl_xor_sync(LG_FULL, be, o);
+    if (ov < bk || (ov == bk && oe < be)) { bk = ov; be = oe; }
+  }
+  if (lane == 0) { s_redk[warp] = bk; s_rede[warp] = be; }
+  __syncthreads();
+  // ---- lines 24-27 backtrack + R20 (thread 0)
+  if (tid == 0) {
+    bk = ~0ull; be = 0x7fffffff;
+    for (int w = 0; w < DP_THREADS / 32; ++w)
+      if (s_redk[w] < bk || (s_redk[w] == bk && s_rede[w] < be)) { bk = s_redk[w]; be = s_rede[w]; }
+    int used_default = 0;
+    if (bk == ~0ull) {
+      used_default = 1;
+    } else {
+      int e = be;
+      for (int a = La - 1; a >= 0; --a) {
+        const int l = act[a];
+        const int c = PD[(int64_t)a * W1 + e];
+        choice[l] = c;
+        e -= discretise(metric(err[(int64_t)l * K + c], flags), emax, D, flags);
+      }
+      int64_t pb = 0;
+      double pe = 0.0;
+      for (int a = 0; a < La; ++a) {
+        const int l = act[a];
+        pb += bits[(int64_t)l * K + choice[l]];
+        pe = __dadd_rn(pe, metric(err[(int64_t)l * K + choice[l]], flags));
+      }
+      if (pb > s_defbits || pe > emax) used_default = 1;
+    }
+    if (used_default)
+      for (int a = 0; a < La; ++a) choice[act[a]] = default_idx[act[a]];
+    int64_t tb = 0;
+    double te = 0.0;
+    for (int a = 0; a < La; ++a) {
+      const int l = act[a];
+      tb += bits[(int64_t)l * K + choice[l]];
+      te = __dadd_rn(te, metric(err[(int64_t)l * K + choice[l]], flags));
+    }
+    lgreco_solve_info inf = {};
+    inf.emax = emax;
+    inf.total_err = te;
+    inf.total_bits = tb;
+    inf.default_bits = s_defbits;
+    inf.used_default = used_default;
+    inf.n_active = La;
+    inf.status = LGRECO_OK;
+    *info = inf;
+  }
+}
+
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 size_t solve_workspace_bytes(int L, int K, int D) {
@@ -185,13 +432,31 @@ cudaError_t launch_solve(const SolveArgs& a, void* ws, cudaStream_t st) {
   int32_t* act = reinterpret_cast<int32_t*>(base + align_up((size_t)a.L * (a.D + 1)));
   int64_t* grows = reinterpret_cast<int64_t*>(base + align_up((size_t)a.L * (a.D + 1)) +
                                               align_up(sizeof(int32_t) * (size_t)(a.L + 1)));
+  const int W1 = a.D + 1;
+  const int cpt = (W1 + DP_THREADS - 1) / DP_THREADS;
+  // fast path: two padded 32-bit rows or two 64-bit rows in smem (see k_solve_fast)
+  const size_t fast_smem = std::max((size_t)8 * (2 * W1 + DP_THREADS), (size_t)16 * (W1 + 1 + DP_THREADS));
+  if (cpt <= 12 && fast_smem <= 200 * 1024) {
+    cudaError_t e = cudaSuccess;
+#define LG_SF(C)                                                                                       \
+  case C:                                                                                              \
+    e = cudaFuncSetAttribute(k_solve_fast<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
+    if (e != cudaSuccess) return e;                                                                    \
+    k_solve_fast<C><<<1, DP_THREADS, fast_smem, st>>>(a.err, a.bits, a.L, a.K, a.default_idx, a.compress, a.D, \
+                                                     a.flags, a.choice, a.info, pd, act);              \
+    break;
+    switch (cpt) { LG_SF(1) LG_SF(2) LG_SF(3) LG_SF(4) LG_SF(5) LG_SF(6) LG_SF(7) LG_SF(8) LG_SF(9) LG_SF(10)
+                   LG_SF(11) LG_SF(12) }
+#undef LG_SF
+    return cudaGetLastError();
+  }
   const size_t row_bytes = sizeof(int64_t) * 2 * (size_t)(a.D + 1);
   const int in_smem = row_bytes <= 200 * 1024;
   const size_t smem = in_smem ? row_bytes : 0;
-  cudaError_t e = cudaFuncSetAttribute(k_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(200 * 1024));
+  cudaError_t e = cudaFuncSetAttribute(k_solve_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(200 * 1024));
   if (e != cudaSuccess) return e;
-  k_solve<<<1, DP_THREADS, smem, st>>>(a.err, a.bits, a.L, a.K, a.default_idx, a.compress, a.D, a.flags,
-                                       a.choice, a.info, pd, act, grows, in_smem);
+  k_solve_generic<<<1, DP_THREADS, smem, st>>>(a.err, a.bits, a.L, a.K, a.default_idx, a.compress, a.D, a.flags,
+                                               a.choice, a.info, pd, act, grows, in_smem);
   return cudaGetLastError();
 }
 

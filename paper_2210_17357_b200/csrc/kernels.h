@@ -13,24 +13,26 @@ struct ProfChunk {
   int64_t first;  // first bucket index within the layer
 };
 
+struct CandS { float s[16]; };  // s_j = 2^{b_j} - 1, passed by value (constant bank)
+
 struct QProfileArgs {
   const float* g; const float* e;
   const DevLayer* layers; int L;
   const ProfChunk* chunks; int nchunks; const int32_t* layer_chunk0;
-  int B; const float* cand_s; const int32_t* params; int K;
+  int B; CandS cs; const int32_t* params; int K;
   uint32_t k0, k1, rankfield, step;
   double* partial; double* err; int64_t* bits;
 };
 
 struct QPackArgs {
   const float* g; float* ef; uint8_t* payload; float* dec;
-  const DevLayer* layers; const DevPlan* plan; const int64_t* bucket0; int L; int64_t R; int B;
+  const DevLayer* layers; const DevPlan* plan; const ProfChunk* chunks; int nchunks; int B;
   uint32_t k0, k1, rankfield, step; unsigned* flag;
 };
 
 struct QUnpackArgs {
   const uint8_t* payload; float* out;
-  const DevLayer* layers; const DevPlan* plan; const int64_t* bucket0; int L; int64_t R; int B;
+  const DevLayer* layers; const DevPlan* plan; const ProfChunk* chunks; int nchunks; int B;
 };
 
 struct QReduceArgs {

@@ -1,19 +1,23 @@
 // qsgd.cu -- QSGD-style bucketed min/max stochastic quantisation on sm_100a.
 //
-//   K1  k_qprofile   (a2)  one HBM pass over x = g + e per bucket; per-bucket
-//                          min/max by warp shuffles, then the realised squared error
-//                          of EVERY candidate bit-width from the same Philox uniforms
+//   K1  k_qprofile   (a2)  one HBM pass over x = g + e; per bucket min/max by warp
+//                          shuffles, then the realised squared error of EVERY
+//                          candidate bit-width from the same Philox uniforms
 //                          (R5, R6).  Deterministic:
-//                          fixed chunk -> partial -> ordered reduce.
+//                          fixed chunk -> per-chunk partial -> ordered reduce.
 //   K1b k_qprofile_reduce  per-layer fixed-order fp64 sum of chunk partials, sqrt.
 //   K5  k_qpack      (a8)  quantise with the chosen bits, bit-plane pack via
-//                          __ballot_sync, fused error feedback e <- x - dec.
+//                          __ballot_sync, fused error feedback e <- x - dec
+//                          (and, for W == 1, the decoded output).
 //   K8  k_qreduce    (a9)  owner shard: decode W stage-1 records, ordered fp32 sum,
 //                          x fl(1/W), requantise (stream 1) and pack stage 2.
 //   K9  k_qunpack    (a10) decode a payload into the fp32 mean gradient.
 //
 // One warp owns one bucket (record) of B = 128*m elements; lane l holds elements
-// 128t + 4l .. 4l+3 of sub-block t (float4 loads when the layer is 16B aligned).
+// 128t + 4l .. 4l+3 of sub-block t.  Every CTA owns a fixed chunk of <= 64 buckets
+// of ONE layer (no per-record layer search).  Full buckets of 16B-aligned layers
+// at B = 128 take a branch-free float4 fast path; the ragged last bucket of a layer,
+// misaligned layers and B > 128 take the generic path.
 #include <math.h>
 
 #include "common.cuh"
@@ -25,25 +29,49 @@ constexpr int QP_THREADS = 256;
 constexpr int QP_WARPS = QP_THREADS / 32;
 
 // ---------------------------------------------------------------------------
-// element loads
+// small helpers
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ float fmin_nan(float a, float b) {
+  float r;
+  asm("min.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float fmax_nan(float a, float b) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void warp_minmax_nan(float& mn, float& mx) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    mn = fmin_nan(mn, __shfl_xor_sync(LG_FULL, mn, o));
+    mx = fmax_nan(mx, __shfl_xor_sync(LG_FULL, mx, o));
+  }
+}
+
 struct X4 { float v[4]; };
 
-// Load the 4 elements of lane `lane` in sub-block (flat base index `base`), nv valid.
+__device__ __forceinline__ X4 canon4(float4 a, float4 b) {
+  X4 r;
+  r.v[0] = canon(a.x, b.x); r.v[1] = canon(a.y, b.y);
+  r.v[2] = canon(a.z, b.z); r.v[3] = canon(a.w, b.w);
+  return r;
+}
+
+__device__ __forceinline__ float4 ld4(const float* __restrict__ p) {
+  return __ldg(reinterpret_cast<const float4*>(p));
+}
+
+// Generic load: 4 elements of the lane starting at flat index base, nv valid.
 __device__ __forceinline__ X4 load_x4(const float* __restrict__ g, const float* __restrict__ e,
                                       int64_t base, int nv, bool aligned) {
   X4 r;
   if (nv >= 4 && aligned) {
-    float4 a = __ldg(reinterpret_cast<const float4*>(g + base));
-    float4 b = e ? __ldg(reinterpret_cast<const float4*>(e + base)) : make_float4(0.f, 0.f, 0.f, 0.f);
-    r.v[0] = canon(a.x, b.x); r.v[1] = canon(a.y, b.y);
-    r.v[2] = canon(a.z, b.z); r.v[3] = canon(a.w, b.w);
+    r = canon4(ld4(g + base), e ? ld4(e + base) : make_float4(0.f, 0.f, 0.f, 0.f));
   } else {
 #pragma unroll
-    for (int s = 0; s < 4; ++s) {
-      if (s < nv) r.v[s] = canon(__ldg(g + base + s), e ? __ldg(e + base + s) : 0.f);
-      else r.v[s] = 0.f;
-    }
+    for (int s = 0; s < 4; ++s)
+      r.v[s] = (s < nv) ? canon(__ldg(g + base + s), e ? __ldg(e + base + s) : 0.f) : 0.f;
   }
   return r;
 }
@@ -78,84 +106,104 @@ __device__ __forceinline__ float qcode(float t, float inv, float u, float s) {
   return fminf(q, s);
 }
 
+__device__ __forceinline__ void uniforms4(uint32_t c0, uint32_t rankfield, uint32_t step, uint32_t stream,
+                                          uint32_t k0, uint32_t k1, float* u) {
+  const U4 r = philox10(c0, rankfield, step, stream, k0, k1);
+  u[0] = word_u(r.x); u[1] = word_u(r.y); u[2] = word_u(r.z); u[3] = word_u(r.w);
+}
+
 // ---------------------------------------------------------------------------
 // K1 profile
 // ---------------------------------------------------------------------------
-template <int KMAX, bool SINGLE>
-__global__ void __launch_bounds__(QP_THREADS)
+// Quantise 4 elements with every candidate and accumulate the lane's SSE (fp32).
+template <int KT>
+__device__ __forceinline__ void prof_candidates(const float* x, float mn, const float* u, float my_inv,
+                                                float my_unit, const CandS& cs, int K, float* acc) {
+  float tt[4];
+#pragma unroll
+  for (int s = 0; s < 4; ++s) tt[s] = __fsub_rn(x[s], mn);
+#pragma unroll
+  for (int j = 0; j < KT; ++j) {
+    if (j < K) {
+      const float inv = __shfl_sync(LG_FULL, my_inv, j);
+      const float unit = __shfl_sync(LG_FULL, my_unit, j);
+      float sse = 0.f;
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        const float q = qcode(tt[s], inv, u[s], cs.s[j]);
+        const float d = __fsub_rn(x[s], __fmaf_rn(q, unit, mn));
+        sse = __fmaf_rn(d, d, sse);
+      }
+      acc[j] = __fadd_rn(acc[j], sse);
+    }
+  }
+}
+
+template <int KT>
+__global__ void __launch_bounds__(QP_THREADS, 4)
 k_qprofile(const float* __restrict__ g, const float* __restrict__ e, const DevLayer* __restrict__ layers,
-           const ProfChunk* __restrict__ chunks, int B, const float* __restrict__ cand_s, int K,
-           uint32_t k0, uint32_t k1, uint32_t rankfield, uint32_t step, double* __restrict__ partial) {
-  __shared__ double red[QP_WARPS][KMAX];
+           const ProfChunk* __restrict__ chunks, int B, const CandS cs, int K, uint32_t k0, uint32_t k1,
+           uint32_t rankfield, uint32_t step, double* __restrict__ partial) {
+  __shared__ double red[QP_WARPS][KT];
   const ProfChunk ch = chunks[blockIdx.x];
   const DevLayer ly = layers[ch.layer];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const bool aligned = (ly.offset & 3) == 0;
+  const bool fast_layer = ((ly.offset & 3) == 0) && B == 128;
   const int M = B >> 7;
-
-  float sj[KMAX];
+  const float my_s = (lane < K) ? cs.s[lane] : 1.f;
+  float acc[KT];
 #pragma unroll
-  for (int j = 0; j < KMAX; ++j) sj[j] = (j < K) ? cand_s[j] : 1.f;
-  const float my_s = (lane < K) ? cand_s[lane] : 1.f;
-  double acc[KMAX];
-#pragma unroll
-  for (int j = 0; j < KMAX; ++j) acc[j] = 0.0;
+  for (int j = 0; j < KT; ++j) acc[j] = 0.f;
 
   for (int bi = warp; bi < ch.nbk; bi += QP_WARPS) {
-    const int64_t jb = ch.first + bi;             // bucket index within the layer
-    const int64_t gb = ly.bucket0 + jb;           // global record index
-    const int64_t e0 = jb * (int64_t)B;           // first element (layer-relative)
-    // ---- pass 1: min / max over the bucket
-    float mn = INFINITY, mx = -INFINITY;
-    X4 xs;
-    for (int t = 0; t < M; ++t) {
-      const int64_t i0 = e0 + 128 * t + 4 * lane;
-      const int nv = (int)max((int64_t)0, min((int64_t)4, ly.numel - i0));
-      xs = load_x4(g, e, ly.offset + i0, nv, aligned);
+    const int64_t jb = ch.first + bi;
+    const int64_t gb = ly.bucket0 + jb;
+    const int64_t e0 = jb * (int64_t)B;
+    if (fast_layer && e0 + 128 <= ly.numel) {
+      // ---- fast path: one full, aligned bucket of 128
+      const int64_t base = ly.offset + e0 + 4 * lane;
+      const X4 xs = canon4(ld4(g + base), e ? ld4(e + base) : make_float4(0.f, 0.f, 0.f, 0.f));
+      float mn = fmin_nan(fmin_nan(xs.v[0], xs.v[1]), fmin_nan(xs.v[2], xs.v[3]));
+      float mx = fmax_nan(fmax_nan(xs.v[0], xs.v[1]), fmax_nan(xs.v[2], xs.v[3]));
+      warp_minmax_nan(mn, mx);
+      float my_inv, my_unit;
+      qparams(mn, mx, my_s, my_inv, my_unit);
+      float u[4];
+      uniforms4((uint32_t)(gb * 32 + lane), rankfield, step, 0u, k0, k1, u);
+      prof_candidates<KT>(xs.v, mn, u, my_inv, my_unit, cs, K, acc);
+    } else {
+      // ---- generic path: ragged / misaligned / B > 128
+      const bool aligned = (ly.offset & 3) == 0;
+      float mn = INFINITY, mx = -INFINITY;
+      X4 xs;
+      for (int t = 0; t < M; ++t) {
+        const int64_t i0 = e0 + 128 * t + 4 * lane;
+        const int nv = (int)max((int64_t)0, min((int64_t)4, ly.numel - i0));
+        xs = load_x4(g, e, ly.offset + i0, nv, aligned);
 #pragma unroll
-      for (int s = 0; s < 4; ++s)
-        if (s < nv) { mn = fminf(mn, xs.v[s]); mx = fmaxf(mx, xs.v[s]); }
-    }
-    mn = warp_min(mn);
-    mx = warp_max(mx);
-    float my_inv, my_unit;
-    qparams(mn, mx, my_s, my_inv, my_unit);
-    // ---- pass 2: all candidates on the same uniforms
-    for (int t = 0; t < M; ++t) {
-      const int64_t i0 = e0 + 128 * t + 4 * lane;
-      const int nv = (int)max((int64_t)0, min((int64_t)4, ly.numel - i0));
-      if (!SINGLE) xs = load_x4(g, e, ly.offset + i0, nv, aligned);
-      const U4 r = philox10((uint32_t)(gb * (B >> 2) + 32 * t + lane), rankfield, step, 0u, k0, k1);
-      const float u[4] = {word_u(r.x), word_u(r.y), word_u(r.z), word_u(r.w)};
-      float tt[4], x[4];
-#pragma unroll
-      for (int s = 0; s < 4; ++s) {
-        x[s] = (s < nv) ? xs.v[s] : mn;   // invalid -> x = mn -> d = 0
-        tt[s] = __fsub_rn(x[s], mn);
+        for (int s = 0; s < 4; ++s)
+          if (s < nv) { mn = fmin_nan(mn, xs.v[s]); mx = fmax_nan(mx, xs.v[s]); }
       }
+      warp_minmax_nan(mn, mx);
+      float my_inv, my_unit;
+      qparams(mn, mx, my_s, my_inv, my_unit);
+      for (int t = 0; t < M; ++t) {
+        const int64_t i0 = e0 + 128 * t + 4 * lane;
+        const int nv = (int)max((int64_t)0, min((int64_t)4, ly.numel - i0));
+        if (M > 1) xs = load_x4(g, e, ly.offset + i0, nv, aligned);
+        float u[4], x[4];
+        uniforms4((uint32_t)(gb * (B >> 2) + 32 * t + lane), rankfield, step, 0u, k0, k1, u);
 #pragma unroll
-      for (int j = 0; j < KMAX; ++j) {
-        if (j < K) {
-          const float inv = __shfl_sync(LG_FULL, my_inv, j);
-          const float unit = __shfl_sync(LG_FULL, my_unit, j);
-          float sse = 0.f;
-#pragma unroll
-          for (int s = 0; s < 4; ++s) {
-            const float q = qcode(tt[s], inv, u[s], sj[j]);
-            const float dec = __fmaf_rn(q, unit, mn);
-            const float d = __fsub_rn(x[s], dec);
-            sse = __fmaf_rn(d, d, sse);
-          }
-          acc[j] += (double)sse;
-        }
+        for (int s = 0; s < 4; ++s) x[s] = (s < nv) ? xs.v[s] : mn;  // invalid -> d = 0
+        prof_candidates<KT>(x, mn, u, my_inv, my_unit, cs, K, acc);
       }
     }
   }
-  // ---- deterministic block reduction
+  // ---- deterministic block reduction (fp64)
 #pragma unroll
-  for (int j = 0; j < KMAX; ++j) {
+  for (int j = 0; j < KT; ++j) {
     if (j < K) {
-      const double v = warp_sum_d(acc[j]);
+      const double v = warp_sum_d((double)acc[j]);
       if (lane == 0) red[warp][j] = v;
     }
   }
@@ -201,10 +249,9 @@ k_qprofile_reduce(const DevLayer* __restrict__ layers, const int32_t* __restrict
 }
 
 // ---------------------------------------------------------------------------
-// quantise + pack one record (shared by K5 stage 1 and K8 stage 2)
-// x[t][4] for sub-block t is produced by `getx(t, nv, xs)`; writes the record.
+// bit-plane packing / unpacking (R7)
 // ---------------------------------------------------------------------------
-// Pack the codes q[4] of sub-block t as bit planes: word (t*b+p)*4+s, bit lane.
+// Codes q[4] of sub-block t: word (t*b+p)*4+s gets bit p of code(128t+4l+s) in bit l.
 __device__ __forceinline__ void pack_planes(uint32_t* __restrict__ words, int t, int b, const uint32_t* q,
                                             int lane) {
   for (int p = 0; p < b; ++p) {
@@ -220,52 +267,121 @@ __device__ __forceinline__ void pack_planes(uint32_t* __restrict__ words, int t,
   }
 }
 
+// Decode sub-block t of a record with b bits -> dec[4] of this lane.
+__device__ __forceinline__ void decode_sub(const uint8_t* __restrict__ rec, int t, int b, int M, int lane,
+                                           float* dec) {
+  const uint32_t* words = reinterpret_cast<const uint32_t*>(rec);
+  const float2 mu = __ldg(reinterpret_cast<const float2*>(rec + 16 * b * M));
+  uint32_t q0 = 0, q1 = 0, q2 = 0, q3 = 0;
+  for (int p = 0; p < b; ++p) {
+    const uint2 a = __ldg(reinterpret_cast<const uint2*>(words + (t * b + p) * 4));
+    const uint2 c = __ldg(reinterpret_cast<const uint2*>(words + (t * b + p) * 4 + 2));
+    q0 |= ((a.x >> lane) & 1u) << p;
+    q1 |= ((a.y >> lane) & 1u) << p;
+    q2 |= ((c.x >> lane) & 1u) << p;
+    q3 |= ((c.y >> lane) & 1u) << p;
+  }
+  dec[0] = __fmaf_rn((float)q0, mu.y, mu.x);
+  dec[1] = __fmaf_rn((float)q1, mu.y, mu.x);
+  dec[2] = __fmaf_rn((float)q2, mu.y, mu.x);
+  dec[3] = __fmaf_rn((float)q3, mu.y, mu.x);
+}
+
 // ---------------------------------------------------------------------------
-// K5 stage-1 pack + EF (+ optional fused decode for W == 1)
+// K5 stage-1 pack + EF (+ fused decode for W == 1)
 // ---------------------------------------------------------------------------
-template <bool SINGLE>
+// Quantise/pack/EF of one full aligned bucket (fast path); returns NaN-flag input.
+__device__ __forceinline__ void pack_bucket_fast(const X4& xs, int b, int64_t gb, uint32_t rankfield,
+                                                 uint32_t step, uint32_t k0, uint32_t k1, int lane,
+                                                 uint8_t* __restrict__ rec, float* __restrict__ ef,
+                                                 float* __restrict__ dec_out, int64_t base, float& bad) {
+  const float s_b = (float)((1u << b) - 1u);
+  float mn = fmin_nan(fmin_nan(xs.v[0], xs.v[1]), fmin_nan(xs.v[2], xs.v[3]));
+  float mx = fmax_nan(fmax_nan(xs.v[0], xs.v[1]), fmax_nan(xs.v[2], xs.v[3]));
+  warp_minmax_nan(mn, mx);
+  float inv, unit;
+  qparams(mn, mx, s_b, inv, unit);
+  bad = __fadd_rn(bad, __fmul_rn(__fsub_rn(mx, mn), 0.f));  // NaN / inf range -> NaN
+  float u[4];
+  uniforms4((uint32_t)(gb * 32 + lane), rankfield, step, 0u, k0, k1, u);
+  uint32_t q[4];
+  float dec[4], en[4];
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    const float qf = qcode(__fsub_rn(xs.v[s], mn), inv, u[s], s_b);
+    q[s] = (uint32_t)qf;
+    dec[s] = __fmaf_rn(qf, unit, mn);
+    en[s] = __fsub_rn(xs.v[s], dec[s]);
+  }
+  if (rec) {
+    pack_planes(reinterpret_cast<uint32_t*>(rec), 0, b, q, lane);
+    if (lane == 0) *reinterpret_cast<float2*>(rec + 16 * b) = make_float2(mn, unit);
+  }
+  if (ef) *reinterpret_cast<float4*>(ef + base) = make_float4(en[0], en[1], en[2], en[3]);
+  if (dec_out) *reinterpret_cast<float4*>(dec_out + base) = make_float4(dec[0], dec[1], dec[2], dec[3]);
+}
+
 __global__ void __launch_bounds__(QP_THREADS)
 k_qpack(const float* __restrict__ g, float* __restrict__ ef, uint8_t* __restrict__ payload,
         float* __restrict__ dec_out, const DevLayer* __restrict__ layers, const DevPlan* __restrict__ plan,
-        const int64_t* __restrict__ bucket0, int L, int64_t R, int B, uint32_t k0, uint32_t k1,
-        uint32_t rankfield, uint32_t step, int rec_per_warp, unsigned* __restrict__ flag) {
-  extern __shared__ int64_t sb0[];
-  for (int i = threadIdx.x; i <= L; i += blockDim.x) sb0[i] = bucket0[i];
-  __syncthreads();
+        const ProfChunk* __restrict__ chunks, int B, uint32_t k0, uint32_t k1, uint32_t rankfield,
+        uint32_t step, unsigned* __restrict__ flag) {
+  const ProfChunk ch = chunks[blockIdx.x];
+  const DevLayer ly = layers[ch.layer];
+  const DevPlan pl = plan[ch.layer];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int M = B >> 7;
-  const int64_t wbase = ((int64_t)blockIdx.x * QP_WARPS + warp) * rec_per_warp;
+  const bool aligned = (ly.offset & 3) == 0;
   float bad = 0.f;
-  for (int ri = 0; ri < rec_per_warp; ++ri) {
-    const int64_t gb = wbase + ri;
-    if (gb >= R) break;
-    const int l = find_layer(sb0, L, gb);
-    const DevLayer ly = layers[l];
-    const DevPlan pl = plan[l];
-    const int64_t jb = gb - ly.bucket0;
+  if (pl.bits == 0) {
+    // lossless layer: raw x records, e' = 0 (R14, R15)
+    float* raw = payload ? reinterpret_cast<float*>(payload + pl.pay_off) : nullptr;
+    const int64_t i_beg = ch.first * (int64_t)B;
+    const int64_t i_end = min(ly.numel, (ch.first + ch.nbk) * (int64_t)B);
+    for (int64_t i = i_beg + threadIdx.x; i < i_end; i += blockDim.x) {
+      const float x = canon(__ldg(g + ly.offset + i), ef ? ef[ly.offset + i] : 0.f);
+      bad = __fadd_rn(bad, __fmul_rn(x, 0.f));
+      if (raw) raw[i] = x;
+      if (dec_out) dec_out[ly.offset + i] = x;
+      if (ef) ef[ly.offset + i] = 0.f;
+    }
+    if (!isfinite(bad)) atomicOr(flag, 1u);
+    return;
+  }
+  const int b = pl.bits;
+  const float s_b = (float)((1u << b) - 1u);
+  const bool fast_layer = aligned && B == 128;
+  int bi = warp;
+  // ---- fast path, two buckets per iteration for memory-level parallelism
+  if (fast_layer) {
+    for (; bi + QP_WARPS < ch.nbk; bi += 2 * QP_WARPS) {
+      const int64_t jbA = ch.first + bi, jbB = jbA + QP_WARPS;
+      if ((jbB + 1) * 128 > ly.numel) break;  // B bucket not full: finish in the loop below
+      const int64_t baseA = ly.offset + jbA * 128 + 4 * lane, baseB = ly.offset + jbB * 128 + 4 * lane;
+      const float4 gA = ld4(g + baseA), gB = ld4(g + baseB);
+      const float4 eA = ef ? ld4(ef + baseA) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 eB = ef ? ld4(ef + baseB) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const X4 xA = canon4(gA, eA), xB = canon4(gB, eB);
+      pack_bucket_fast(xA, b, ly.bucket0 + jbA, rankfield, step, k0, k1, lane,
+                       payload ? payload + pl.pay_off + jbA * (int64_t)pl.rec_bytes : nullptr, ef, dec_out,
+                       baseA, bad);
+      pack_bucket_fast(xB, b, ly.bucket0 + jbB, rankfield, step, k0, k1, lane,
+                       payload ? payload + pl.pay_off + jbB * (int64_t)pl.rec_bytes : nullptr, ef, dec_out,
+                       baseB, bad);
+    }
+  }
+  for (; bi < ch.nbk; bi += QP_WARPS) {
+    const int64_t jb = ch.first + bi;
+    const int64_t gb = ly.bucket0 + jb;
     const int64_t e0 = jb * (int64_t)B;
-    const bool aligned = (ly.offset & 3) == 0;
-    if (pl.bits == 0) {
-      // lossless record: raw x, e' = 0
-      float* rawdst = payload ? reinterpret_cast<float*>(payload + pl.pay_off) : nullptr;
-      for (int t = 0; t < M; ++t) {
-        const int64_t i0 = e0 + 128 * t + 4 * lane;
-        const int nv = (int)max((int64_t)0, min((int64_t)4, ly.numel - i0));
-        if (nv <= 0) continue;
-        X4 xs = load_x4(g, ef, ly.offset + i0, nv, aligned);
-#pragma unroll
-        for (int s = 0; s < 4; ++s) if (s < nv) bad = __fmaf_rn(xs.v[s], 0.f, bad);
-        if (rawdst) {
-#pragma unroll
-          for (int s = 0; s < 4; ++s) if (s < nv) rawdst[i0 + s] = xs.v[s];
-        }
-        if (dec_out) store_x4(dec_out, ly.offset + i0, nv, aligned, xs.v);
-        if (ef) { const float z[4] = {0.f, 0.f, 0.f, 0.f}; store_x4(ef, ly.offset + i0, nv, aligned, z); }
-      }
+    uint8_t* rec = payload ? payload + pl.pay_off + jb * (int64_t)pl.rec_bytes : nullptr;
+    if (fast_layer && e0 + 128 <= ly.numel) {
+      const int64_t base = ly.offset + e0 + 4 * lane;
+      const X4 xs = canon4(ld4(g + base), ef ? ld4(ef + base) : make_float4(0.f, 0.f, 0.f, 0.f));
+      pack_bucket_fast(xs, b, gb, rankfield, step, k0, k1, lane, rec, ef, dec_out, base, bad);
       continue;
     }
-    const int b = pl.bits;
-    const float s_b = (float)((1u << b) - 1u);
+    // ---- generic path
     float mn = INFINITY, mx = -INFINITY;
     X4 xs;
     for (int t = 0; t < M; ++t) {
@@ -274,20 +390,18 @@ k_qpack(const float* __restrict__ g, float* __restrict__ ef, uint8_t* __restrict
       xs = load_x4(g, ef, ly.offset + i0, nv, aligned);
 #pragma unroll
       for (int s = 0; s < 4; ++s)
-        if (s < nv) { mn = fminf(mn, xs.v[s]); mx = fmaxf(mx, xs.v[s]); bad = __fmaf_rn(xs.v[s], 0.f, bad); }
+        if (s < nv) { mn = fmin_nan(mn, xs.v[s]); mx = fmax_nan(mx, xs.v[s]); }
     }
-    mn = warp_min(mn);
-    mx = warp_max(mx);
+    warp_minmax_nan(mn, mx);
     float inv, unit;
     qparams(mn, mx, s_b, inv, unit);
-    if (!isfinite(unit)) bad = __int_as_float(0x7fc00000);  // range overflow (R5)
-    uint8_t* rec = payload ? payload + pl.pay_off + jb * (int64_t)pl.rec_bytes : nullptr;
+    bad = __fadd_rn(bad, __fmul_rn(__fsub_rn(mx, mn), 0.f));
     for (int t = 0; t < M; ++t) {
       const int64_t i0 = e0 + 128 * t + 4 * lane;
       const int nv = (int)max((int64_t)0, min((int64_t)4, ly.numel - i0));
-      if (!SINGLE) xs = load_x4(g, ef, ly.offset + i0, nv, aligned);
-      const U4 r = philox10((uint32_t)(gb * (B >> 2) + 32 * t + lane), rankfield, step, 0u, k0, k1);
-      const float u[4] = {word_u(r.x), word_u(r.y), word_u(r.z), word_u(r.w)};
+      if (M > 1) xs = load_x4(g, ef, ly.offset + i0, nv, aligned);
+      float u[4];
+      uniforms4((uint32_t)(gb * (B >> 2) + 32 * t + lane), rankfield, step, 0u, k0, k1, u);
       uint32_t q[4];
       float dec[4], en[4];
 #pragma unroll
@@ -304,37 +418,9 @@ k_qpack(const float* __restrict__ g, float* __restrict__ ef, uint8_t* __restrict
         if (dec_out) store_x4(dec_out, ly.offset + i0, nv, aligned, dec);
       }
     }
-    if (rec && lane == 0) {
-      float* meta = reinterpret_cast<float*>(rec + 16 * b * M);
-      meta[0] = mn;
-      meta[1] = unit;
-    }
+    if (rec && lane == 0) *reinterpret_cast<float2*>(rec + 16 * b * M) = make_float2(mn, unit);
   }
   if (!isfinite(bad)) atomicOr(flag, 1u);
-}
-
-// ---------------------------------------------------------------------------
-// decode helpers
-// ---------------------------------------------------------------------------
-// Decode sub-block t of a record with b bits: codes of lane's 4 elements -> dec[4]
-__device__ __forceinline__ void decode_sub(const uint8_t* __restrict__ rec, int t, int b, int M, int lane,
-                                           float* dec) {
-  const uint32_t* words = reinterpret_cast<const uint32_t*>(rec);
-  const float mn = __ldg(reinterpret_cast<const float*>(rec + 16 * b * M));
-  const float unit = __ldg(reinterpret_cast<const float*>(rec + 16 * b * M + 4));
-  uint32_t q0 = 0, q1 = 0, q2 = 0, q3 = 0;
-  for (int p = 0; p < b; ++p) {
-    const uint2 a = __ldg(reinterpret_cast<const uint2*>(words + (t * b + p) * 4));
-    const uint2 c = __ldg(reinterpret_cast<const uint2*>(words + (t * b + p) * 4 + 2));
-    q0 |= ((a.x >> lane) & 1u) << p;
-    q1 |= ((a.y >> lane) & 1u) << p;
-    q2 |= ((c.x >> lane) & 1u) << p;
-    q3 |= ((c.y >> lane) & 1u) << p;
-  }
-  dec[0] = __fmaf_rn((float)q0, unit, mn);
-  dec[1] = __fmaf_rn((float)q1, unit, mn);
-  dec[2] = __fmaf_rn((float)q2, unit, mn);
-  dec[3] = __fmaf_rn((float)q3, unit, mn);
 }
 
 // ---------------------------------------------------------------------------
@@ -342,34 +428,29 @@ __device__ __forceinline__ void decode_sub(const uint8_t* __restrict__ rec, int 
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(QP_THREADS)
 k_qunpack(const uint8_t* __restrict__ payload, float* __restrict__ out, const DevLayer* __restrict__ layers,
-          const DevPlan* __restrict__ plan, const int64_t* __restrict__ bucket0, int L, int64_t R, int B,
-          int rec_per_warp) {
-  extern __shared__ int64_t sb0[];
-  for (int i = threadIdx.x; i <= L; i += blockDim.x) sb0[i] = bucket0[i];
-  __syncthreads();
+          const DevPlan* __restrict__ plan, const ProfChunk* __restrict__ chunks, int B) {
+  const ProfChunk ch = chunks[blockIdx.x];
+  const DevLayer ly = layers[ch.layer];
+  const DevPlan pl = plan[ch.layer];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int M = B >> 7;
-  const int64_t wbase = ((int64_t)blockIdx.x * QP_WARPS + warp) * rec_per_warp;
-  for (int ri = 0; ri < rec_per_warp; ++ri) {
-    const int64_t gb = wbase + ri;
-    if (gb >= R) break;
-    const int l = find_layer(sb0, L, gb);
-    const DevLayer ly = layers[l];
-    const DevPlan pl = plan[l];
-    const int64_t jb = gb - ly.bucket0;
+  const bool aligned = (ly.offset & 3) == 0;
+  if (pl.bits == 0) {
+    const float* raw = reinterpret_cast<const float*>(payload + pl.pay_off);
+    const int64_t i_beg = ch.first * (int64_t)B;
+    const int64_t i_end = min(ly.numel, (ch.first + ch.nbk) * (int64_t)B);
+    for (int64_t i = i_beg + threadIdx.x; i < i_end; i += blockDim.x) out[ly.offset + i] = __ldg(raw + i);
+    return;
+  }
+  for (int bi = warp; bi < ch.nbk; bi += QP_WARPS) {
+    const int64_t jb = ch.first + bi;
     const int64_t e0 = jb * (int64_t)B;
-    const bool aligned = (ly.offset & 3) == 0;
+    const uint8_t* rec = payload + pl.pay_off + jb * (int64_t)pl.rec_bytes;
     for (int t = 0; t < M; ++t) {
       const int64_t i0 = e0 + 128 * t + 4 * lane;
       const int nv = (int)max((int64_t)0, min((int64_t)4, ly.numel - i0));
       float dec[4];
-      if (pl.bits == 0) {
-        const float* raw = reinterpret_cast<const float*>(payload + pl.pay_off);
-#pragma unroll
-        for (int s = 0; s < 4; ++s) dec[s] = (s < nv) ? __ldg(raw + i0 + s) : 0.f;
-      } else {
-        decode_sub(payload + pl.pay_off + jb * (int64_t)pl.rec_bytes, t, pl.bits, M, lane, dec);
-      }
+      decode_sub(rec, t, pl.bits, M, lane, dec);
       if (nv > 0) store_x4(out, ly.offset + i0, nv, aligned, dec);
     }
   }
@@ -378,7 +459,6 @@ k_qunpack(const uint8_t* __restrict__ payload, float* __restrict__ out, const De
 // ---------------------------------------------------------------------------
 // K8 owner reduce: records [r0, r1); recv = W x shard bytes (rank-major)
 // ---------------------------------------------------------------------------
-template <bool SINGLE>
 __global__ void __launch_bounds__(QP_THREADS)
 k_qreduce(const uint8_t* __restrict__ recv, int64_t shard_bytes, int64_t byte0, uint8_t* __restrict__ stage2,
           const DevLayer* __restrict__ layers, const DevPlan* __restrict__ plan, const int64_t* __restrict__ bucket0,
@@ -399,7 +479,7 @@ k_qreduce(const uint8_t* __restrict__ recv, int64_t shard_bytes, int64_t byte0, 
     const int64_t jb = gb - ly.bucket0;
     const int64_t e0 = jb * (int64_t)B;
     if (pl.bits == 0) {
-      const int64_t roff = pl.pay_off + e0 * 4;  // record byte offset
+      const int64_t roff = pl.pay_off + e0 * 4;
       for (int t = 0; t < M; ++t) {
         const int64_t i0 = e0 + 128 * t + 4 * lane;
         const int nv = (int)max((int64_t)0, min((int64_t)4, ly.numel - i0));
@@ -418,59 +498,46 @@ k_qreduce(const uint8_t* __restrict__ recv, int64_t shard_bytes, int64_t byte0, 
     const int b = pl.bits;
     const float s_b = (float)((1u << b) - 1u);
     const int64_t roff = pl.pay_off + jb * (int64_t)pl.rec_bytes;
-    // pass 1: averaged values and their min / max
     float mn = INFINITY, mx = -INFINITY;
     float m4[4];
-    for (int t = 0; t < M; ++t) {
-      const int64_t i0 = e0 + 128 * t + 4 * lane;
-      const int nv = (int)max((int64_t)0, min((int64_t)4, ly.numel - i0));
-      float a[4] = {0.f, 0.f, 0.f, 0.f};
-      for (int w = 0; w < W; ++w) {
-        float d[4];
-        decode_sub(recv + w * shard_bytes + (roff - byte0), t, b, M, lane, d);
-#pragma unroll
-        for (int s = 0; s < 4; ++s) a[s] = (w == 0) ? d[s] : __fadd_rn(a[s], d[s]);
+    for (int pass = 0; pass < 2; ++pass) {
+      float inv = 0.f, unit = 0.f;
+      if (pass == 1) {
+        warp_minmax_nan(mn, mx);
+        qparams(mn, mx, s_b, inv, unit);
       }
+      for (int t = 0; t < M; ++t) {
+        const int64_t i0 = e0 + 128 * t + 4 * lane;
+        const int nv = (int)max((int64_t)0, min((int64_t)4, ly.numel - i0));
+        if (pass == 0 || M > 1) {
+          float a[4] = {0.f, 0.f, 0.f, 0.f};
+          for (int w = 0; w < W; ++w) {
+            float d[4];
+            decode_sub(recv + w * shard_bytes + (roff - byte0), t, b, M, lane, d);
 #pragma unroll
-      for (int s = 0; s < 4; ++s) {
-        m4[s] = __fmul_rn(a[s], invW);
-        if (s < nv) { mn = fminf(mn, m4[s]); mx = fmaxf(mx, m4[s]); }
-      }
-    }
-    mn = warp_min(mn);
-    mx = warp_max(mx);
-    float inv, unit;
-    qparams(mn, mx, s_b, inv, unit);
-    uint8_t* rec = stage2 + roff;
-    for (int t = 0; t < M; ++t) {
-      const int64_t i0 = e0 + 128 * t + 4 * lane;
-      const int nv = (int)max((int64_t)0, min((int64_t)4, ly.numel - i0));
-      if (!SINGLE) {
-        float a[4] = {0.f, 0.f, 0.f, 0.f};
-        for (int w = 0; w < W; ++w) {
-          float d[4];
-          decode_sub(recv + w * shard_bytes + (roff - byte0), t, b, M, lane, d);
+            for (int s = 0; s < 4; ++s) a[s] = (w == 0) ? d[s] : __fadd_rn(a[s], d[s]);
+          }
 #pragma unroll
-          for (int s = 0; s < 4; ++s) a[s] = (w == 0) ? d[s] : __fadd_rn(a[s], d[s]);
+          for (int s = 0; s < 4; ++s) m4[s] = __fmul_rn(a[s], invW);
         }
+        if (pass == 0) {
 #pragma unroll
-        for (int s = 0; s < 4; ++s) m4[s] = __fmul_rn(a[s], invW);
-      }
-      const U4 r = philox10((uint32_t)(gb * (B >> 2) + 32 * t + lane), 0xFFFFFFFFu, step, 1u, k0, k1);
-      const float u[4] = {word_u(r.x), word_u(r.y), word_u(r.z), word_u(r.w)};
-      uint32_t q[4];
+          for (int s = 0; s < 4; ++s)
+            if (s < nv) { mn = fmin_nan(mn, m4[s]); mx = fmax_nan(mx, m4[s]); }
+          continue;
+        }
+        float u[4];
+        uniforms4((uint32_t)(gb * (B >> 2) + 32 * t + lane), 0xFFFFFFFFu, step, 1u, k0, k1, u);
+        uint32_t q[4];
 #pragma unroll
-      for (int s = 0; s < 4; ++s) {
-        const float x = (s < nv) ? m4[s] : mn;
-        const float qf = qcode(__fsub_rn(x, mn), inv, u[s], s_b);
-        q[s] = (s < nv) ? (uint32_t)qf : 0u;
+        for (int s = 0; s < 4; ++s) {
+          const float x = (s < nv) ? m4[s] : mn;
+          const float qf = qcode(__fsub_rn(x, mn), inv, u[s], s_b);
+          q[s] = (s < nv) ? (uint32_t)qf : 0u;
+        }
+        pack_planes(reinterpret_cast<uint32_t*>(stage2 + roff), t, b, q, lane);
       }
-      pack_planes(reinterpret_cast<uint32_t*>(rec), t, b, q, lane);
-    }
-    if (lane == 0) {
-      float* meta = reinterpret_cast<float*>(rec + 16 * b * M);
-      meta[0] = mn;
-      meta[1] = unit;
+      if (pass == 1 && lane == 0) *reinterpret_cast<float2*>(stage2 + roff + 16 * b * M) = make_float2(mn, unit);
     }
   }
 }
@@ -486,24 +553,21 @@ __global__ void k_philox(const uint32_t* __restrict__ ctr, uint32_t k0, uint32_t
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
-static int grid_for(int64_t R, int rpw) {
-  return (int)((R + (int64_t)QP_WARPS * rpw - 1) / ((int64_t)QP_WARPS * rpw));
-}
-
 cudaError_t launch_qprofile(const QProfileArgs& a, cudaStream_t st) {
   if (a.nchunks > 0) {
-    const bool single = a.B == 128;
-#define LG_QP(KM)                                                                              \
-  if (single)                                                                                  \
-    k_qprofile<KM, true><<<a.nchunks, QP_THREADS, 0, st>>>(a.g, a.e, a.layers, a.chunks, a.B,  \
-        a.cand_s, a.K, a.k0, a.k1, a.rankfield, a.step, a.partial);                            \
-  else                                                                                         \
-    k_qprofile<KM, false><<<a.nchunks, QP_THREADS, 0, st>>>(a.g, a.e, a.layers, a.chunks, a.B, \
-        a.cand_s, a.K, a.k0, a.k1, a.rankfield, a.step, a.partial);
-    if (a.K <= 4) { LG_QP(4) }
-    else if (a.K <= 7) { LG_QP(7) }
-    else if (a.K <= 8) { LG_QP(8) }
-    else { LG_QP(16) }
+#define LG_QP(KT)                                                                          \
+  k_qprofile<KT><<<a.nchunks, QP_THREADS, 0, st>>>(a.g, a.e, a.layers, a.chunks, a.B, a.cs, a.K, \
+                                                    a.k0, a.k1, a.rankfield, a.step, a.partial)
+    switch (a.K) {
+      case 4: LG_QP(4); break;
+      case 5: LG_QP(5); break;
+      case 6: LG_QP(6); break;
+      case 7: LG_QP(7); break;
+      case 8: LG_QP(8); break;
+      default:
+        if (a.K < 4) LG_QP(4);
+        else LG_QP(16);
+    }
 #undef LG_QP
   }
   k_qprofile_reduce<<<a.L, 256, 0, st>>>(a.layers, a.layer_chunk0, a.partial, a.params, a.K, a.B, a.err, a.bits);
@@ -511,39 +575,26 @@ cudaError_t launch_qprofile(const QProfileArgs& a, cudaStream_t st) {
 }
 
 cudaError_t launch_qpack(const QPackArgs& a, cudaStream_t st) {
-  const int rpw = 4;
-  const int grid = grid_for(a.R, rpw);
-  if (grid == 0) return cudaSuccess;
-  const size_t smem = sizeof(int64_t) * (a.L + 1);
-  if (a.B == 128)
-    k_qpack<true><<<grid, QP_THREADS, smem, st>>>(a.g, a.ef, a.payload, a.dec, a.layers, a.plan, a.bucket0,
-                                                  a.L, a.R, a.B, a.k0, a.k1, a.rankfield, a.step, rpw, a.flag);
-  else
-    k_qpack<false><<<grid, QP_THREADS, smem, st>>>(a.g, a.ef, a.payload, a.dec, a.layers, a.plan, a.bucket0,
-                                                   a.L, a.R, a.B, a.k0, a.k1, a.rankfield, a.step, rpw, a.flag);
+  if (a.nchunks == 0) return cudaSuccess;
+  k_qpack<<<a.nchunks, QP_THREADS, 0, st>>>(a.g, a.ef, a.payload, a.dec, a.layers, a.plan, a.chunks, a.B, a.k0,
+                                            a.k1, a.rankfield, a.step, a.flag);
   return cudaGetLastError();
 }
 
 cudaError_t launch_qunpack(const QUnpackArgs& a, cudaStream_t st) {
-  const int rpw = 4;
-  const int grid = grid_for(a.R, rpw);
-  if (grid == 0) return cudaSuccess;
-  const size_t smem = sizeof(int64_t) * (a.L + 1);
-  k_qunpack<<<grid, QP_THREADS, smem, st>>>(a.payload, a.out, a.layers, a.plan, a.bucket0, a.L, a.R, a.B, rpw);
+  if (a.nchunks == 0) return cudaSuccess;
+  k_qunpack<<<a.nchunks, QP_THREADS, 0, st>>>(a.payload, a.out, a.layers, a.plan, a.chunks, a.B);
   return cudaGetLastError();
 }
 
 cudaError_t launch_qreduce(const QReduceArgs& a, cudaStream_t st) {
   const int rpw = 2;
-  const int grid = grid_for(a.r1 - a.r0, rpw);
+  const int64_t n = a.r1 - a.r0;
+  const int grid = (int)((n + (int64_t)QP_WARPS * rpw - 1) / ((int64_t)QP_WARPS * rpw));
   if (grid == 0) return cudaSuccess;
   const size_t smem = sizeof(int64_t) * (a.L + 1);
-  if (a.B == 128)
-    k_qreduce<true><<<grid, QP_THREADS, smem, st>>>(a.recv, a.shard_bytes, a.byte0, a.stage2, a.layers, a.plan,
-                                                    a.bucket0, a.L, a.r0, a.r1, a.B, a.W, a.k0, a.k1, a.step, rpw);
-  else
-    k_qreduce<false><<<grid, QP_THREADS, smem, st>>>(a.recv, a.shard_bytes, a.byte0, a.stage2, a.layers, a.plan,
-                                                     a.bucket0, a.L, a.r0, a.r1, a.B, a.W, a.k0, a.k1, a.step, rpw);
+  k_qreduce<<<grid, QP_THREADS, smem, st>>>(a.recv, a.shard_bytes, a.byte0, a.stage2, a.layers, a.plan, a.bucket0,
+                                            a.L, a.r0, a.r1, a.B, a.W, a.k0, a.k1, a.step, rpw);
   return cudaGetLastError();
 }
 
