@@ -176,6 +176,17 @@ int lgreco_qsgd_reduce(lgreco_ctx* ctx, const int32_t* h_choice, int32_t W, int6
 int lgreco_qsgd_unpack(lgreco_ctx* ctx, const int32_t* h_choice, const uint8_t* d_payload,
                        float* d_out, void* stream);
 
+/* TopK stage 1 (K2 select with the chosen densities + K6 compaction): pairs
+ * (u32 idx, f32 val) ascending per layer into d_payload (S bytes, nullable), e' into
+ * d_ef (nullable), the decoded values (kept at idx, 0 elsewhere) into d_out (nullable). */
+int lgreco_topk_pack(lgreco_ctx* ctx, const int32_t* h_choice, const float* d_g, float* d_ef,
+                     uint8_t* d_payload, float* d_out, void* stream);
+
+/* TopK exchange combine (K10): d_gathered = W payloads of S bytes, rank-major (the
+ * all-gather result); d_out <- ordered mean over ranks (R10). */
+int lgreco_topk_combine(lgreco_ctx* ctx, const int32_t* h_choice, int32_t W, const uint8_t* d_gathered,
+                        float* d_out, void* stream);
+
 /* Debug: Philox4x32-10 of n counters (d_ctr: n*4 u32, key) -> d_out n*4 u32. */
 int lgreco_debug_philox(const uint32_t* d_ctr, uint32_t key0, uint32_t key1, int64_t n,
                         uint32_t* d_out, void* stream);

@@ -476,12 +476,14 @@ int ref_topk_profile(const ref_layer* layers, int32_t L, const float* g, const f
     return REF_OK;
 }
 
-/* TopK payload byte offsets: per layer 8*k (idx,val) pairs, lossless 4n. */
+/* TopK payload byte offsets: per layer 8*k (idx,val) pairs, lossless 4n, each layer
+ * block 16-byte aligned (zero padding). */
 int64_t ref_topk_layout(const ref_layer* layers, int32_t L, const int32_t* lppm, int64_t* byte_off) {
     int64_t off = 0;
     for (int l = 0; l < L; l++) {
         byte_off[l] = off;
         off += lppm[l] > 0 ? 8 * ref_topk_k(layers[l].numel, lppm[l]) : 4 * layers[l].numel;
+        off = (off + 15) & ~(int64_t)15; /* 16-byte aligned layer blocks (R9) */
     }
     byte_off[L] = off;
     return off;

@@ -1,15 +1,11 @@
 // api.cu -- the C ABI declared in include/lgreco.h: context, plan layout,
 // dispatch of the kernels and the NCCL exchange (one process per GPU).
-#include <nccl.h>
 #include <stdarg.h>
 #include <stdio.h>
-#include <string.h>
 
 #include <algorithm>
-#include <vector>
 
-#include "common.cuh"
-#include "kernels.h"
+#include "ctx.h"
 
 static thread_local char g_err[1024] = "";
 
@@ -19,67 +15,6 @@ void lg_set_error(const char* fmt, ...) {
   vsnprintf(g_err, sizeof(g_err), fmt, ap);
   va_end(ap);
 }
-
-#define LG_NCCL(call)                                                                   \
-  do {                                                                                  \
-    ncclResult_t _r = (call);                                                           \
-    if (_r != ncclSuccess) {                                                            \
-      lg_set_error("%s:%d %s: %s", __FILE__, __LINE__, #call, ncclGetErrorString(_r));  \
-      return LGRECO_ENCCL;                                                              \
-    }                                                                                   \
-  } while (0)
-
-#define LG_TRY(call)                 \
-  do {                               \
-    int _s = (call);                 \
-    if (_s != LGRECO_OK) return _s;  \
-  } while (0)
-
-#define LG_LAUNCH(ctx, call)                                                              \
-  do {                                                                                    \
-    cudaError_t _e = (call);                                                              \
-    if (_e != cudaSuccess) {                                                              \
-      lg_set_error("%s:%d launch %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(_e)); \
-      return LGRECO_ECUDA;                                                                \
-    }                                                                                     \
-  } while (0)
-
-struct lgreco_ctx {
-  int L = 0, rank = 0, world = 1;
-  int family = 0, K = 0, B = 128, power_steps = 5;
-  uint64_t seed = 0;
-  std::vector<lgreco_layer> layers;
-  std::vector<int32_t> params;
-  std::vector<int64_t> bucket0;  // L+1
-  int64_t N = 0, R = 0;
-  int64_t launches = 0;
-  // device tables
-  lg::DevLayer* d_layers = nullptr;
-  int64_t* d_bucket0 = nullptr;
-  float* d_cand_s = nullptr;
-  int32_t* d_params = nullptr;
-  lg::ProfChunk* d_chunks = nullptr;      // chunks of compressed layers (profile)
-  int nchunks = 0;
-  lg::ProfChunk* d_chunks_all = nullptr;  // chunks of every layer (pack / unpack)
-  int nchunks_all = 0;
-  lg::CandS cs{};
-  int32_t* d_layer_chunk0 = nullptr;
-  double* d_partial = nullptr;
-  unsigned* d_flag = nullptr;
-  // plan
-  std::vector<int32_t> plan_choice;
-  bool plan_valid = false;
-  std::vector<lg::DevPlan> h_plan_v;
-  lg::DevPlan* h_plan_pinned = nullptr;
-  lg::DevPlan* d_plan = nullptr;
-  cudaEvent_t plan_evt = nullptr;
-  int64_t S = 0;
-  std::vector<int64_t> rec_bounds, byte_bounds;
-  // exchange buffers
-  uint8_t *d_pay1 = nullptr, *d_recv = nullptr, *d_pay2 = nullptr;
-  int64_t pay_cap = 0;
-  ncclComm_t comm = nullptr;
-};
 
 extern "C" {
 
@@ -214,14 +149,15 @@ int lgreco_ctx_create(lgreco_ctx** out, const lgreco_layer* layers, int32_t L, c
     }
     end = ly.offset + ly.numel;
   }
-  if (cand->family != LGRECO_QSGD) {
+  if (cand->family == LGRECO_POWERSGD) {
     lg_set_error("family %d not available in this build", cand->family);
     return LGRECO_EUNSUPPORTED;
   }
   cudaStream_t st = (cudaStream_t)stream;
   lgreco_ctx* c = new lgreco_ctx();
   c->L = L; c->rank = rank; c->world = world;
-  c->family = cand->family; c->K = cand->K; c->B = cand->qbucket; c->power_steps = cand->power_steps;
+  c->family = cand->family; c->K = cand->K; c->power_steps = cand->power_steps;
+  c->B = cand->family == LGRECO_QSGD ? cand->qbucket : 128;  // bucket tables only used by QSGD
   c->seed = cand->seed;
   c->layers.assign(layers, layers + L);
   c->params.assign(cand->params, cand->params + cand->K);
@@ -253,7 +189,7 @@ int lgreco_ctx_create(lgreco_ctx** out, const lgreco_layer* layers, int32_t L, c
   for (int j = 0; j < c->K; ++j) cs[j] = c->family == LGRECO_QSGD ? (float)((1u << c->params[j]) - 1u) : 0.f;
   for (int j = 0; j < c->K && j < 16; ++j) c->cs.s[j] = cs[j];
   // max payload over all plans: every compressed layer at the largest candidate
-  const int bmax = (int)max_param(c);
+  const int bmax = c->family == LGRECO_QSGD ? (int)max_param(c) : 0;
   int64_t cap = 0;
   for (int l = 0; l < L; ++l)
     cap += (layers[l].compress ? (c->bucket0[l + 1] - c->bucket0[l]) * rec_bytes_full(bmax, c->B) : 4 * layers[l].numel) + 16;
@@ -274,7 +210,7 @@ int lgreco_ctx_create(lgreco_ctx** out, const lgreco_layer* layers, int32_t L, c
   LG_ALLOC(c->d_partial, sizeof(double) * (size_t)std::max(1, c->nchunks) * c->K);
   LG_ALLOC(c->d_flag, sizeof(unsigned));
   LG_ALLOC(c->d_plan, sizeof(lg::DevPlan) * L);
-  if (world > 1) {
+  if (world > 1 && c->family == LGRECO_QSGD) {
     LG_ALLOC(c->d_pay1, cap);
     LG_ALLOC(c->d_recv, cap + (int64_t)world * 4 * 8192 * 4);
     LG_ALLOC(c->d_pay2, cap);
@@ -299,6 +235,10 @@ int lgreco_ctx_create(lgreco_ctx** out, const lgreco_layer* layers, int32_t L, c
     lg_set_error("ctx upload: %s", cudaGetErrorString(e));
     return fail(LGRECO_ECUDA);
   }
+  if (c->family == LGRECO_TOPK) {
+    const int s = topk_init(c, st);
+    if (s != LGRECO_OK) return fail(s);
+  }
   if (world > 1) {
     if (!nccl_unique_id) { lg_set_error("world > 1 needs an ncclUniqueId"); return fail(LGRECO_EINVAL); }
     ncclUniqueId id;
@@ -316,6 +256,7 @@ int lgreco_ctx_create(lgreco_ctx** out, const lgreco_layer* layers, int32_t L, c
 
 void lgreco_ctx_destroy(lgreco_ctx* c) {
   if (!c) return;
+  topk_destroy(c);
   if (c->comm) ncclCommDestroy(c->comm);
   cudaFree(c->d_layers); cudaFree(c->d_bucket0); cudaFree(c->d_cand_s); cudaFree(c->d_params);
   cudaFree(c->d_chunks); cudaFree(c->d_chunks_all); cudaFree(c->d_layer_chunk0); cudaFree(c->d_partial); cudaFree(c->d_flag);
@@ -354,6 +295,7 @@ int lgreco_profile(lgreco_ctx* c, const float* d_g, const float* d_ef, uint64_t 
     c->launches += (c->nchunks > 0) + 1;
     return LGRECO_OK;
   }
+  if (c->family == LGRECO_TOPK) return topk_profile(c, d_g, d_ef, d_err, d_bits, st);
   lg_set_error("profile: family %d unsupported", c->family);
   return LGRECO_EUNSUPPORTED;
 }
@@ -384,6 +326,7 @@ int lgreco_plan_broadcast(lgreco_ctx* c, int32_t* d_choice, void* stream) {
 
 int64_t lgreco_payload_bytes(lgreco_ctx* c, const int32_t* h_choice) {
   if (!c || !h_choice) return LGRECO_EINVAL;
+  if (c->family == LGRECO_TOPK) return topk_payload_bytes(c, h_choice);
   std::vector<lg::DevPlan> plan;
   int64_t S = 0;
   int s = qsgd_layout(c, h_choice, plan, S);
@@ -445,8 +388,9 @@ int lgreco_qsgd_unpack(lgreco_ctx* c, const int32_t* h_choice, const uint8_t* d_
 int lgreco_compress_allreduce(lgreco_ctx* c, const int32_t* h_choice, const float* d_g, float* d_ef, float* d_out,
                               uint64_t step, void* stream) {
   if (!c || !h_choice || !d_g || !d_out) { lg_set_error("null argument"); return LGRECO_EINVAL; }
-  if (c->family != LGRECO_QSGD) { lg_set_error("family unsupported"); return LGRECO_EUNSUPPORTED; }
   cudaStream_t st = (cudaStream_t)stream;
+  if (c->family == LGRECO_TOPK) return topk_compress_allreduce(c, h_choice, d_g, d_ef, d_out, st);
+  if (c->family != LGRECO_QSGD) { lg_set_error("family unsupported"); return LGRECO_EUNSUPPORTED; }
   if (c->world == 1)  // stage 2 skipped (R13): fused pack + EF + decode, nothing leaves the GPU
     return lgreco_qsgd_pack(c, h_choice, d_g, d_ef, nullptr, d_out, 0u, step, stream);
   LG_TRY(lgreco_qsgd_pack(c, h_choice, d_g, d_ef, c->d_pay1, nullptr, (uint32_t)c->rank, step, stream));
@@ -471,6 +415,20 @@ int lgreco_compress_allreduce(lgreco_ctx* c, const int32_t* h_choice, const floa
   }
   LG_NCCL(ncclGroupEnd());
   return lgreco_qsgd_unpack(c, h_choice, c->d_pay2, d_out, stream);
+}
+
+int lgreco_topk_pack(lgreco_ctx* c, const int32_t* h_choice, const float* d_g, float* d_ef, uint8_t* d_payload,
+                     float* d_out, void* stream) {
+  if (!c || !h_choice || !d_g) return LGRECO_EINVAL;
+  if (c->family != LGRECO_TOPK) return LGRECO_EUNSUPPORTED;
+  return topk_pack(c, h_choice, d_g, d_ef, d_payload, d_out, (cudaStream_t)stream);
+}
+
+int lgreco_topk_combine(lgreco_ctx* c, const int32_t* h_choice, int32_t W, const uint8_t* d_gathered, float* d_out,
+                        void* stream) {
+  if (!c || !h_choice || W < 1 || !d_gathered || !d_out) return LGRECO_EINVAL;
+  if (c->family != LGRECO_TOPK) return LGRECO_EUNSUPPORTED;
+  return topk_combine(c, h_choice, W, d_gathered, d_out, (cudaStream_t)stream);
 }
 
 int lgreco_debug_philox(const uint32_t* d_ctr, uint32_t key0, uint32_t key1, int64_t n, uint32_t* d_out, void* stream) {

@@ -1,0 +1,87 @@
+// ctx.h -- internal definition of lgreco_ctx shared by the C-ABI translation units.
+#pragma once
+#include <nccl.h>
+#include <string.h>
+
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.h"
+
+#define LG_NCCL(call)                                                                   \
+  do {                                                                                  \
+    ncclResult_t _r = (call);                                                           \
+    if (_r != ncclSuccess) {                                                            \
+      lg_set_error("%s:%d %s: %s", __FILE__, __LINE__, #call, ncclGetErrorString(_r));  \
+      return LGRECO_ENCCL;                                                              \
+    }                                                                                   \
+  } while (0)
+
+#define LG_TRY(call)                 \
+  do {                               \
+    int _s = (call);                 \
+    if (_s != LGRECO_OK) return _s;  \
+  } while (0)
+
+#define LG_LAUNCH(ctx, call)                                                              \
+  do {                                                                                    \
+    cudaError_t _e = (call);                                                              \
+    if (_e != cudaSuccess) {                                                              \
+      lg_set_error("%s:%d launch %s: %s", __FILE__, __LINE__, #call, cudaGetErrorString(_e)); \
+      return LGRECO_ECUDA;                                                                \
+    }                                                                                     \
+  } while (0)
+
+struct lgreco_ctx {
+  int L = 0, rank = 0, world = 1;
+  int family = 0, K = 0, B = 128, power_steps = 5;
+  uint64_t seed = 0;
+  std::vector<lgreco_layer> layers;
+  std::vector<int32_t> params;
+  std::vector<int64_t> bucket0;  // L+1
+  int64_t N = 0, R = 0;
+  int64_t launches = 0;
+  // device tables
+  lg::DevLayer* d_layers = nullptr;
+  int64_t* d_bucket0 = nullptr;
+  float* d_cand_s = nullptr;
+  int32_t* d_params = nullptr;
+  lg::ProfChunk* d_chunks = nullptr;      // chunks of compressed layers (profile)
+  int nchunks = 0;
+  lg::ProfChunk* d_chunks_all = nullptr;  // chunks of every layer (pack / unpack)
+  int nchunks_all = 0;
+  lg::CandS cs{};
+  int32_t* d_layer_chunk0 = nullptr;
+  double* d_partial = nullptr;
+  unsigned* d_flag = nullptr;
+  // plan
+  std::vector<int32_t> plan_choice;
+  bool plan_valid = false;
+  std::vector<lg::DevPlan> h_plan_v;
+  lg::DevPlan* h_plan_pinned = nullptr;
+  lg::DevPlan* d_plan = nullptr;
+  cudaEvent_t plan_evt = nullptr;
+  int64_t S = 0;
+  std::vector<int64_t> rec_bounds, byte_bounds;
+  // exchange buffers
+  uint8_t *d_pay1 = nullptr, *d_recv = nullptr, *d_pay2 = nullptr;
+  int64_t pay_cap = 0;
+  ncclComm_t comm = nullptr;
+  // TopK state (family == LGRECO_TOPK)
+  struct Topk* tk = nullptr;
+  // PowerSGD state (family == LGRECO_POWERSGD)
+  struct Psgd* ps = nullptr;
+};
+
+// family-specific parts (api_topk.cu, api_psgd.cu)
+int topk_init(lgreco_ctx* c, cudaStream_t st);
+void topk_destroy(lgreco_ctx* c);
+int topk_profile(lgreco_ctx* c, const float* g, const float* e, double* err, int64_t* bits, cudaStream_t st);
+int topk_pack(lgreco_ctx* c, const int32_t* choice, const float* g, float* ef, uint8_t* payload, float* out,
+              cudaStream_t st);
+int topk_combine(lgreco_ctx* c, const int32_t* choice, int W, const uint8_t* gathered, float* out, cudaStream_t st);
+int topk_compress_allreduce(lgreco_ctx* c, const int32_t* choice, const float* g, float* ef, float* out,
+                            cudaStream_t st);
+int64_t topk_payload_bytes(lgreco_ctx* c, const int32_t* choice);
+
+

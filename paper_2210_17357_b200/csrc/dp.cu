@@ -192,40 +192,59 @@ __global__ void __launch_bounds__(DP_THREADS, 1)
 k_solve_fast(const double* __restrict__ err, const int64_t* __restrict__ bits, int L, int K,
              const int32_t* __restrict__ default_idx, const int32_t* __restrict__ compress, int D, uint32_t flags,
              int32_t* __restrict__ choice, lgreco_solve_info* __restrict__ info, uint8_t* __restrict__ PD,
-             int32_t* __restrict__ act) {
+             int32_t* __restrict__ act, int32_t* __restrict__ wdisc, uint64_t* __restrict__ wadd) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ int32_t s_disc[256];
-  __shared__ uint64_t s_add[256];
+  __shared__ int32_t s_disc[2][256];
+  __shared__ uint64_t s_add[2][256];
   __shared__ int s_La, s_status, s_wide, s_cbits;
   __shared__ double s_emax;
   __shared__ int64_t s_defbits;
+  __shared__ unsigned long long s_mx;
   __shared__ uint64_t s_g[DP_THREADS / 32];
   __shared__ uint64_t s_redk[DP_THREADS / 32];
   __shared__ int s_rede[DP_THREADS / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int W1 = D + 1;
 
-  // ---- Alg.1 lines 1-2: active layers, Emax, default bits (thread 0, layer order)
+  // ---- prelude, parallel: stage flags/defaults in smem (row area is free yet)
+  int32_t* sm_flag = reinterpret_cast<int32_t*>(smem_raw);   // [L]
+  int32_t* sm_def = sm_flag + L;                             // [L]
+  double* sm_de = reinterpret_cast<double*>(sm_def + L + (L & 1));  // [L] metric(err[l][def])
+  int64_t* sm_db = reinterpret_cast<int64_t*>(sm_de + L);    // [L] bits[l][def]
+  if (tid == 0) { s_status = LGRECO_OK; s_mx = 0; }
+  __syncthreads();
+  for (int l = tid; l < L; l += DP_THREADS) {
+    const int f = compress ? (compress[l] != 0) : 1;
+    const int d = default_idx[l];
+    sm_flag[l] = f;
+    sm_def[l] = d;
+    choice[l] = -1;
+    if (f) {
+      if (d < 0 || d >= K) { atomicExch(&s_status, LGRECO_EINVAL); sm_de[l] = 0.0; sm_db[l] = 0; }
+      else { sm_de[l] = metric(err[(int64_t)l * K + d], flags); sm_db[l] = bits[(int64_t)l * K + d]; }
+    }
+  }
+  __syncthreads();
+  // ---- Alg.1 lines 1-2 (thread 0, layer order, from shared memory)
   if (tid == 0) {
-    int La = 0, status = LGRECO_OK;
+    int La = 0;
     double emax = 0.0;
     int64_t defb = 0;
     for (int l = 0; l < L; ++l) {
-      choice[l] = -1;
-      if (compress && !compress[l]) continue;
-      const int d = default_idx[l];
-      if (d < 0 || d >= K) { status = LGRECO_EINVAL; continue; }
+      if (!sm_flag[l]) continue;
       act[La++] = l;
-      emax = __dadd_rn(emax, metric(err[(int64_t)l * K + d], flags));
-      defb += bits[(int64_t)l * K + d];
+      emax = __dadd_rn(emax, sm_de[l]);
+      defb += sm_db[l];
     }
-    s_La = La; s_status = status; s_emax = emax; s_defbits = defb;
+    s_La = La; s_emax = emax; s_defbits = defb;
     int cb = 0;
     while ((1 << cb) < K) ++cb;
     s_cbits = cb;
   }
   __syncthreads();
   const int La = s_La;
-  // ---- validation + gcd + max plan cost (all threads)
+  const double emax = s_emax;
+  // ---- validation + gcd of costs + largest plan cost (parallel)
   uint64_t gg = 0;
   int bad = 0;
   for (int i = tid; i < La * K; i += DP_THREADS) {
@@ -239,23 +258,28 @@ k_solve_fast(const double* __restrict__ err, const int64_t* __restrict__ bits, i
   bad = __reduce_or_sync(LG_FULL, bad);
 #pragma unroll
   for (int o = 16; o; o >>= 1) gg = gcd64(gg, __shfl_xor_sync(LG_FULL, gg, o));
-  if (lane == 0) { s_g[warp] = gg; if (bad) atomicOr(&s_status, bad & 1 ? LGRECO_ENONFINITE : LGRECO_EINVAL); }
+  if (lane == 0) {
+    s_g[warp] = gg;
+    if (bad & 1) atomicExch(&s_status, LGRECO_ENONFINITE);
+    else if (bad & 2) atomicExch(&s_status, LGRECO_EINVAL);
+  }
   __syncthreads();
   if (tid == 0) {
     uint64_t g = 0;
     for (int w = 0; w < DP_THREADS / 32; ++w) g = gcd64(g, s_g[w]);
-    if (g == 0) g = 1;
-    s_g[0] = g;
-    // largest reachable plan cost in units of g
-    uint64_t mx = 0;
-    for (int a = 0; a < La; ++a) {
-      uint64_t m = 0;
-      for (int c = 0; c < K; ++c) m = max(m, (uint64_t)bits[(int64_t)act[a] * K + c] / g);
-      mx += m;
-    }
-    s_wide = (mx >= (1ull << (31 - s_cbits))) ? 1 : 0;
-    if (mx >= (1ull << (62 - s_cbits))) s_status = LGRECO_EINVAL;
-    if (s_status != LGRECO_OK && s_status != LGRECO_ENONFINITE && s_status != LGRECO_EINVAL) s_status = LGRECO_EINVAL;
+    s_g[0] = g ? g : 1;
+  }
+  __syncthreads();
+  const uint64_t g = s_g[0];
+  for (int a = tid; a < La; a += DP_THREADS) {
+    uint64_t m = 0;
+    for (int c = 0; c < K; ++c) m = max(m, (uint64_t)max((int64_t)0, bits[(int64_t)act[a] * K + c]) / g);
+    atomicAdd(&s_mx, (unsigned long long)m);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    s_wide = (s_mx >= (1ull << (31 - s_cbits))) ? 1 : 0;
+    if (s_mx >= (1ull << (62 - s_cbits)) && s_status == LGRECO_OK) s_status = LGRECO_EINVAL;
   }
   __syncthreads();
   if (s_status != LGRECO_OK || La == 0) {
@@ -267,12 +291,17 @@ k_solve_fast(const double* __restrict__ err, const int64_t* __restrict__ bits, i
     }
     return;
   }
-  const double emax = s_emax;
-  const uint64_t g = s_g[0];
   const int cbits = s_cbits;
   const uint64_t cmask = (1ull << cbits) - 1;
   const bool wide = s_wide;
-  const int W1 = D + 1;
+  // ---- Alg.1 lines 3-5 for every (layer, candidate), in parallel, to the workspace
+  for (int i = tid; i < La * K; i += DP_THREADS) {
+    const int a = i / K, c = i % K;
+    const int l = act[a];
+    wdisc[i] = discretise(metric(err[(int64_t)l * K + c], flags), emax, D, flags);
+    wadd[i] = (((uint64_t)bits[(int64_t)l * K + c] / g) << cbits) | (uint64_t)c;
+  }
+  __syncthreads();
   // rows: 32-bit keys -> two rows padded with W1 INF entries in front (no bounds test);
   //       64-bit keys -> two rows with one INF sentinel at index -1 (clamped index)
   // (+ DP_THREADS tail entries: the last register cell of a thread may lie past D)
@@ -284,24 +313,19 @@ k_solve_fast(const double* __restrict__ err, const int64_t* __restrict__ bits, i
   const uint32_t INF32 = 0x7FFFFFFFu;
   const uint64_t INF64 = 1ull << 62;
   if (!wide) {
-    for (int i = tid; i < row32; i += DP_THREADS) { r32a[i] = INF32; r32b[i] = INF32; }
-    __syncthreads();
-    if (tid == 0) r32a[W1] = 0;  // virtual layer 0: DP0[0] = 0 (R18)
+    for (int i = tid; i < row32; i += DP_THREADS) { r32a[i] = (i == W1) ? 0u : INF32; r32b[i] = INF32; }
   } else {
-    for (int i = tid; i < row64; i += DP_THREADS) { r64a[i] = INF64; r64b[i] = INF64; }
-    __syncthreads();
-    if (tid == 0) r64a[1] = 0;
+    for (int i = tid; i < row64; i += DP_THREADS) { r64a[i] = (i == 1) ? 0ull : INF64; r64b[i] = INF64; }
   }
+  if (tid < K) { s_disc[0][tid] = wdisc[tid]; s_add[0][tid] = wadd[tid]; }
   __syncthreads();
   int cur_is_b = 1;
   for (int a = 0; a < La; ++a) {
-    const int l = act[a];
-    if (tid < K) {
-      const int d = discretise(metric(err[(int64_t)l * K + tid], flags), emax, D, flags);
-      s_disc[tid] = d;
-      s_add[tid] = (((uint64_t)bits[(int64_t)l * K + tid] / g) << cbits) | (uint64_t)tid;
-    }
-    __syncthreads();
+    const int sb = a & 1;
+    // prefetch the next layer's candidate row (published by the barrier below)
+    int32_t nd = -1;
+    uint64_t na = 0;
+    if (tid < K && a + 1 < La) { nd = wdisc[(a + 1) * K + tid]; na = wadd[(a + 1) * K + tid]; }
     uint8_t* pdrow = PD + (int64_t)a * W1;
     if (!wide) {
       const uint32_t* prev = (cur_is_b ? r32a : r32b) + W1;  // index e-d >= -W1 is padded
@@ -310,9 +334,9 @@ k_solve_fast(const double* __restrict__ err, const int64_t* __restrict__ bits, i
 #pragma unroll
       for (int i = 0; i < CPT; ++i) best[i] = 0xFFFFFFFFu;
       for (int c = 0; c < K; ++c) {
-        const int d = s_disc[c];
+        const int d = s_disc[sb][c];
         if (d < 0) continue;
-        const uint32_t ak = (uint32_t)s_add[c];
+        const uint32_t ak = (uint32_t)s_add[sb][c];
         const uint32_t* pv = prev - d + tid;
 #pragma unroll
         for (int i = 0; i < CPT; ++i) best[i] = min(best[i], pv[i * DP_THREADS] + ak);
@@ -333,9 +357,9 @@ k_solve_fast(const double* __restrict__ err, const int64_t* __restrict__ bits, i
 #pragma unroll
       for (int i = 0; i < CPT; ++i) best[i] = ~0ull;
       for (int c = 0; c < K; ++c) {
-        const int d = s_disc[c];
+        const int d = s_disc[sb][c];
         if (d < 0) continue;
-        const uint64_t ak = s_add[c];
+        const uint64_t ak = s_add[sb][c];
 #pragma unroll
         for (int i = 0; i < CPT; ++i) {
           const int idx = max(tid + i * DP_THREADS - d, -1);
@@ -352,6 +376,7 @@ k_solve_fast(const double* __restrict__ err, const int64_t* __restrict__ bits, i
         }
       }
     }
+    if (tid < K) { s_disc[sb ^ 1][tid] = nd; s_add[sb ^ 1][tid] = na; }
     cur_is_b ^= 1;
     __syncthreads();
   }
@@ -372,6 +397,13 @@ k_solve_fast(const double* __restrict__ err, const int64_t* __restrict__ bits, i
   }
   if (lane == 0) { s_redk[warp] = bk; s_rede[warp] = be; }
   __syncthreads();
+  // stage the discretised table in shared memory for the serial backtrack
+  int32_t* sdisc_all = reinterpret_cast<int32_t*>(smem_raw);
+  const bool disc_in_smem = (size_t)La * K * 4 <= (size_t)4 * (wide ? 2 * row64 * 2 : 2 * row32);
+  if (disc_in_smem)
+    for (int i = tid; i < La * K; i += DP_THREADS) sdisc_all[i] = wdisc[i];
+  __syncthreads();
+  const int32_t* bdisc = disc_in_smem ? sdisc_all : wdisc;
   // ---- lines 24-27 backtrack + R20 (thread 0)
   if (tid == 0) {
     bk = ~0ull; be = 0x7fffffff;
@@ -383,47 +415,59 @@ k_solve_fast(const double* __restrict__ err, const int64_t* __restrict__ bits, i
     } else {
       int e = be;
       for (int a = La - 1; a >= 0; --a) {
-        const int l = act[a];
         const int c = PD[(int64_t)a * W1 + e];
-        choice[l] = c;
-        e -= discretise(metric(err[(int64_t)l * K + c], flags), emax, D, flags);
+        choice[act[a]] = c;
+        e -= bdisc[a * K + c];
       }
+    }
+    s_La = used_default;
+  }
+  __syncthreads();
+  // R20 check and the summary (parallel gathers, ordered fp64 sum by thread 0)
+  double* sm_ce = reinterpret_cast<double*>(smem_raw);         // [La] metric(err[choice])
+  int64_t* sm_cb = reinterpret_cast<int64_t*>(sm_ce + La);    // [La] bits[choice]
+  int used_default = s_La;
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int a = tid; a < La; a += DP_THREADS) {
+      const int l = act[a];
+      const int c = used_default ? default_idx[l] : choice[l];
+      sm_ce[a] = metric(err[(int64_t)l * K + c], flags);
+      sm_cb[a] = bits[(int64_t)l * K + c];
+    }
+    __syncthreads();
+    if (tid == 0) {
       int64_t pb = 0;
       double pe = 0.0;
-      for (int a = 0; a < La; ++a) {
-        const int l = act[a];
-        pb += bits[(int64_t)l * K + choice[l]];
-        pe = __dadd_rn(pe, metric(err[(int64_t)l * K + choice[l]], flags));
+      for (int a = 0; a < La; ++a) { pb += sm_cb[a]; pe = __dadd_rn(pe, sm_ce[a]); }
+      if (!used_default && (pb > s_defbits || pe > emax)) {
+        s_La = 1;  // fall back; recompute the summary for the defaults
+      } else {
+        lgreco_solve_info inf = {};
+        inf.emax = emax;
+        inf.total_err = pe;
+        inf.total_bits = pb;
+        inf.default_bits = s_defbits;
+        inf.used_default = used_default;
+        inf.n_active = La;
+        inf.status = LGRECO_OK;
+        *info = inf;
+        s_La = -1;  // done
       }
-      if (pb > s_defbits || pe > emax) used_default = 1;
     }
-    if (used_default)
-      for (int a = 0; a < La; ++a) choice[act[a]] = default_idx[act[a]];
-    int64_t tb = 0;
-    double te = 0.0;
-    for (int a = 0; a < La; ++a) {
-      const int l = act[a];
-      tb += bits[(int64_t)l * K + choice[l]];
-      te = __dadd_rn(te, metric(err[(int64_t)l * K + choice[l]], flags));
-    }
-    lgreco_solve_info inf = {};
-    inf.emax = emax;
-    inf.total_err = te;
-    inf.total_bits = tb;
-    inf.default_bits = s_defbits;
-    inf.used_default = used_default;
-    inf.n_active = La;
-    inf.status = LGRECO_OK;
-    *info = inf;
+    __syncthreads();
+    if (s_La < 0) break;
+    used_default = 1;
+    for (int a = tid; a < La; a += DP_THREADS) choice[act[a]] = default_idx[act[a]];
+    __syncthreads();
   }
 }
 
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 size_t solve_workspace_bytes(int L, int K, int D) {
-  (void)K;
   return align_up((size_t)L * (D + 1)) + align_up(sizeof(int32_t) * (size_t)(L + 1)) +
-         align_up(sizeof(int64_t) * 2 * (size_t)(D + 1));
+         align_up(sizeof(int64_t) * 2 * (size_t)(D + 1)) + align_up(sizeof(int32_t) * (size_t)L * K) +
+         align_up(sizeof(uint64_t) * (size_t)L * K);
 }
 
 cudaError_t launch_solve(const SolveArgs& a, void* ws, cudaStream_t st) {
@@ -432,18 +476,23 @@ cudaError_t launch_solve(const SolveArgs& a, void* ws, cudaStream_t st) {
   int32_t* act = reinterpret_cast<int32_t*>(base + align_up((size_t)a.L * (a.D + 1)));
   int64_t* grows = reinterpret_cast<int64_t*>(base + align_up((size_t)a.L * (a.D + 1)) +
                                               align_up(sizeof(int32_t) * (size_t)(a.L + 1)));
+  int32_t* wdisc = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(grows) +
+                                              align_up(sizeof(int64_t) * 2 * (size_t)(a.D + 1)));
+  uint64_t* wadd = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(wdisc) +
+                                               align_up(sizeof(int32_t) * (size_t)a.L * a.K));
   const int W1 = a.D + 1;
   const int cpt = (W1 + DP_THREADS - 1) / DP_THREADS;
   // fast path: two padded 32-bit rows or two 64-bit rows in smem (see k_solve_fast)
   const size_t fast_smem = std::max((size_t)8 * (2 * W1 + DP_THREADS), (size_t)16 * (W1 + 1 + DP_THREADS));
-  if (cpt <= 12 && fast_smem <= 200 * 1024) {
+  // the prelude stages 24 bytes per layer in the same shared memory
+  if (cpt <= 12 && fast_smem <= 200 * 1024 && (size_t)24 * a.L + 64 <= fast_smem) {
     cudaError_t e = cudaSuccess;
 #define LG_SF(C)                                                                                       \
   case C:                                                                                              \
     e = cudaFuncSetAttribute(k_solve_fast<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
     if (e != cudaSuccess) return e;                                                                    \
     k_solve_fast<C><<<1, DP_THREADS, fast_smem, st>>>(a.err, a.bits, a.L, a.K, a.default_idx, a.compress, a.D, \
-                                                     a.flags, a.choice, a.info, pd, act);              \
+                                                     a.flags, a.choice, a.info, pd, act, wdisc, wadd); \
     break;
     switch (cpt) { LG_SF(1) LG_SF(2) LG_SF(3) LG_SF(4) LG_SF(5) LG_SF(6) LG_SF(7) LG_SF(8) LG_SF(9) LG_SF(10)
                    LG_SF(11) LG_SF(12) }

@@ -48,6 +48,35 @@ cudaError_t launch_qreduce(const QReduceArgs& a, cudaStream_t st);
 cudaError_t launch_philox(const uint32_t* ctr, uint32_t k0, uint32_t k1, int64_t n, uint32_t* out,
                           cudaStream_t st);
 
+// TopK (topk.cu) -----------------------------------------------------------------
+struct TChunk { int32_t cidx; int32_t n; int64_t first; };  // cidx: compressed-layer (or layer) index
+struct TQ {  // one radix-select query (layer, density)
+  int64_t k, r;          // kept count; residual rank inside the current bin
+  int32_t b1, s1, c2, s2; // level-1 bin / slot, level-2 sub-bin / slot
+  uint32_t T; int32_t bad;  // threshold key; non-finite input seen
+  double below, sse;     // sum x^2 strictly below the current bin; final dropped energy
+};
+struct TPlan { int64_t pay_off; int64_t k; };
+struct TkArgs {
+  const DevLayer* layers; const int32_t* clayer; int nC;
+  const TChunk* chunks; int nchunks; const int32_t* cchunk0;
+  uint32_t* cnt1; unsigned long long* sum1; uint32_t* cnt2; unsigned long long* sum2; uint32_t* cnt3;
+  int32_t* n1; int32_t* n2; int32_t* sl1; uint32_t* sl2;
+  TQ* q; const int64_t* kq; uint2* ccnt; ulonglong2* coff; const TPlan* tplan; unsigned* flag;
+};
+cudaError_t launch_topk_select(const float* g, const float* e, const TkArgs& a, int nq, double* err, int64_t* bits,
+                               int K, cudaStream_t st, int64_t* launches);
+cudaError_t launch_topk_lossless_rows(const DevLayer* layers, int L, int K, double* err, int64_t* bits, cudaStream_t st);
+cudaError_t launch_topk_compact(const float* g, float* ef, uint8_t* payload, float* out, const TkArgs& a,
+                                cudaStream_t st);
+cudaError_t launch_lossless_pack(const float* g, float* ef, uint8_t* payload, float* out, const DevLayer* layers,
+                                 const TChunk* chunks, int nchunks, const TPlan* tplan, unsigned* flag,
+                                 cudaStream_t st);
+cudaError_t launch_topk_combine(const uint8_t* gathered, int64_t S, int W, float* out, const DevLayer* layers,
+                                const TChunk* all_chunks, int nall, const int32_t* clayer,
+                                int nC, const int64_t* kpre, int64_t ktotal, const TPlan* tplan, cudaStream_t st,
+                                int64_t* launches);
+
 // Algorithm 1 DP (dp.cu)
 struct SolveArgs {
   const double* err; const int64_t* bits; int L; int K;

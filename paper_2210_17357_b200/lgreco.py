@@ -63,6 +63,8 @@ _SIGS = {
     "lgreco_qsgd_pack": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _U32, _U64, _VP]),
     "lgreco_qsgd_reduce": (C.c_int, [_VP, _VP, _I32, _I64, _I64, _VP, _VP, _U64, _VP]),
     "lgreco_qsgd_unpack": (C.c_int, [_VP, _VP, _VP, _VP, _VP]),
+    "lgreco_topk_pack": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _VP]),
+    "lgreco_topk_combine": (C.c_int, [_VP, _VP, _I32, _VP, _VP, _VP]),
     "lgreco_debug_philox": (C.c_int, [_VP, _U32, _U32, _I64, _VP, _VP]),
 }
 EXPORTED = tuple(_SIGS)
@@ -187,6 +189,15 @@ class Context:
     def qsgd_unpack(self, choice, payload, out, stream=None):
         _check(lib().lgreco_qsgd_unpack(self.h, _i32(choice), _ptr(payload), _ptr(out), _stream(stream)),
                "qsgd_unpack")
+
+
+    def topk_pack(self, choice, g, ef, payload, out, stream=None):
+        _check(lib().lgreco_topk_pack(self.h, _i32(choice), _ptr(g), _ptr(ef), _ptr(payload), _ptr(out),
+                                      _stream(stream)), "topk_pack")
+
+    def topk_combine(self, choice, W, gathered, out, stream=None):
+        _check(lib().lgreco_topk_combine(self.h, _i32(choice), W, _ptr(gathered), _ptr(out), _stream(stream)),
+               "topk_combine")
 
 
 def solve_workspace_bytes(L, K, D) -> int:
