@@ -209,7 +209,7 @@ k_solve_fast(const double* __restrict__ err, const int64_t* __restrict__ bits, i
   // ---- prelude, parallel: stage flags/defaults in smem (row area is free yet)
   int32_t* sm_flag = reinterpret_cast<int32_t*>(smem_raw);   // [L]
   int32_t* sm_def = sm_flag + L;                             // [L]
-  double* sm_de = reinterpret_cast<double*>(sm_def + L + (L & 1));  // [L] metric(err[l][def])
+  double* sm_de = reinterpret_cast<double*>(sm_def + L);  // [L] metric(err[l][def]) (8L bytes in: aligned)
   int64_t* sm_db = reinterpret_cast<int64_t*>(sm_de + L);    // [L] bits[l][def]
   if (tid == 0) { s_status = LGRECO_OK; s_mx = 0; }
   __syncthreads();
