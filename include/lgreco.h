@@ -187,6 +187,27 @@ int lgreco_topk_pack(lgreco_ctx* ctx, const int32_t* h_choice, const float* d_g,
 int lgreco_topk_combine(lgreco_ctx* ctx, const int32_t* h_choice, int32_t W, const uint8_t* d_gathered,
                         float* d_out, void* stream);
 
+/* PowerSGD stages (K7, R12).  Factor buffers use per-layer slots sized for the
+ * largest candidate rank: P slots hold m x r (column-major) per compressed matrix
+ * layer, Q slots k x r; lgreco_psgd_sizes returns the slot-area sizes (elements). */
+int lgreco_psgd_sizes(lgreco_ctx* ctx, int64_t* h_p_elems, int64_t* h_q_elems);
+/* P_w = M_w Q_ws (Q_ws re-initialised from Philox stream 2 at `step` where the rank
+ * changed) into d_P. */
+int lgreco_psgd_p(lgreco_ctx* ctx, const int32_t* h_choice, const float* d_g, const float* d_ef, float* d_P,
+                  uint64_t step, void* stream);
+/* Phat = orthonormalise(d_Psum / W) (kept in ctx); Q_w = M_w^T Phat into d_Q. */
+int lgreco_psgd_q(lgreco_ctx* ctx, const int32_t* h_choice, const float* d_g, const float* d_ef,
+                  const float* d_Psum, int32_t W, float* d_Q, void* stream);
+/* Q_ws = d_Qsum / W; d_out = Phat Q_ws^T (matrix layers); d_ef <- x - d_out. */
+int lgreco_psgd_out(lgreco_ctx* ctx, const int32_t* h_choice, const float* d_g, float* d_ef,
+                    const float* d_Qsum, int32_t W, float* d_out, void* stream);
+/* Raw layers (vectors, lossless-equivalent ranks): payload = x (S = lgreco_payload_bytes),
+ * e' = 0, d_out = x (nullable each); combine: d_out = ordered mean of W raw payloads. */
+int lgreco_psgd_raw_pack(lgreco_ctx* ctx, const int32_t* h_choice, const float* d_g, float* d_ef,
+                         uint8_t* d_payload, float* d_out, void* stream);
+int lgreco_psgd_raw_combine(lgreco_ctx* ctx, const int32_t* h_choice, int32_t W, const uint8_t* d_gathered,
+                            float* d_out, void* stream);
+
 /* Debug: Philox4x32-10 of n counters (d_ctr: n*4 u32, key) -> d_out n*4 u32. */
 int lgreco_debug_philox(const uint32_t* d_ctr, uint32_t key0, uint32_t key1, int64_t n,
                         uint32_t* d_out, void* stream);

@@ -149,10 +149,6 @@ int lgreco_ctx_create(lgreco_ctx** out, const lgreco_layer* layers, int32_t L, c
     }
     end = ly.offset + ly.numel;
   }
-  if (cand->family == LGRECO_POWERSGD) {
-    lg_set_error("family %d not available in this build", cand->family);
-    return LGRECO_EUNSUPPORTED;
-  }
   cudaStream_t st = (cudaStream_t)stream;
   lgreco_ctx* c = new lgreco_ctx();
   c->L = L; c->rank = rank; c->world = world;
@@ -239,6 +235,11 @@ int lgreco_ctx_create(lgreco_ctx** out, const lgreco_layer* layers, int32_t L, c
     const int s = topk_init(c, st);
     if (s != LGRECO_OK) return fail(s);
   }
+  if (c->family == LGRECO_POWERSGD) {
+    if (c->power_steps < 1) { lg_set_error("power_steps must be >= 1"); return fail(LGRECO_EINVAL); }
+    const int s = psgd_init(c, st);
+    if (s != LGRECO_OK) return fail(s);
+  }
   if (world > 1) {
     if (!nccl_unique_id) { lg_set_error("world > 1 needs an ncclUniqueId"); return fail(LGRECO_EINVAL); }
     ncclUniqueId id;
@@ -257,6 +258,7 @@ int lgreco_ctx_create(lgreco_ctx** out, const lgreco_layer* layers, int32_t L, c
 void lgreco_ctx_destroy(lgreco_ctx* c) {
   if (!c) return;
   topk_destroy(c);
+  psgd_destroy(c);
   if (c->comm) ncclCommDestroy(c->comm);
   cudaFree(c->d_layers); cudaFree(c->d_bucket0); cudaFree(c->d_cand_s); cudaFree(c->d_params);
   cudaFree(c->d_chunks); cudaFree(c->d_chunks_all); cudaFree(c->d_layer_chunk0); cudaFree(c->d_partial); cudaFree(c->d_flag);
@@ -296,6 +298,7 @@ int lgreco_profile(lgreco_ctx* c, const float* d_g, const float* d_ef, uint64_t 
     return LGRECO_OK;
   }
   if (c->family == LGRECO_TOPK) return topk_profile(c, d_g, d_ef, d_err, d_bits, st);
+  if (c->family == LGRECO_POWERSGD) return psgd_profile(c, d_g, d_ef, step, d_err, d_bits, st);
   lg_set_error("profile: family %d unsupported", c->family);
   return LGRECO_EUNSUPPORTED;
 }
@@ -327,6 +330,7 @@ int lgreco_plan_broadcast(lgreco_ctx* c, int32_t* d_choice, void* stream) {
 int64_t lgreco_payload_bytes(lgreco_ctx* c, const int32_t* h_choice) {
   if (!c || !h_choice) return LGRECO_EINVAL;
   if (c->family == LGRECO_TOPK) return topk_payload_bytes(c, h_choice);
+  if (c->family == LGRECO_POWERSGD) return psgd_payload_bytes(c, h_choice);
   std::vector<lg::DevPlan> plan;
   int64_t S = 0;
   int s = qsgd_layout(c, h_choice, plan, S);
@@ -390,6 +394,7 @@ int lgreco_compress_allreduce(lgreco_ctx* c, const int32_t* h_choice, const floa
   if (!c || !h_choice || !d_g || !d_out) { lg_set_error("null argument"); return LGRECO_EINVAL; }
   cudaStream_t st = (cudaStream_t)stream;
   if (c->family == LGRECO_TOPK) return topk_compress_allreduce(c, h_choice, d_g, d_ef, d_out, st);
+  if (c->family == LGRECO_POWERSGD) return psgd_compress_allreduce(c, h_choice, d_g, d_ef, d_out, step, st);
   if (c->family != LGRECO_QSGD) { lg_set_error("family unsupported"); return LGRECO_EUNSUPPORTED; }
   if (c->world == 1)  // stage 2 skipped (R13): fused pack + EF + decode, nothing leaves the GPU
     return lgreco_qsgd_pack(c, h_choice, d_g, d_ef, nullptr, d_out, 0u, step, stream);
@@ -429,6 +434,43 @@ int lgreco_topk_combine(lgreco_ctx* c, const int32_t* h_choice, int32_t W, const
   if (!c || !h_choice || W < 1 || !d_gathered || !d_out) return LGRECO_EINVAL;
   if (c->family != LGRECO_TOPK) return LGRECO_EUNSUPPORTED;
   return topk_combine(c, h_choice, W, d_gathered, d_out, (cudaStream_t)stream);
+}
+
+int lgreco_psgd_sizes(lgreco_ctx* c, int64_t* h_p_elems, int64_t* h_q_elems) {
+  if (!c || c->family != LGRECO_POWERSGD || !h_p_elems || !h_q_elems) return LGRECO_EINVAL;
+  *h_p_elems = psgd_sizes(c, 0);
+  *h_q_elems = psgd_sizes(c, 1);
+  return LGRECO_OK;
+}
+
+int lgreco_psgd_p(lgreco_ctx* c, const int32_t* h_choice, const float* d_g, const float* d_ef, float* d_P,
+                  uint64_t step, void* stream) {
+  if (!c || !h_choice || !d_g || !d_P || c->family != LGRECO_POWERSGD) return LGRECO_EINVAL;
+  return psgd_p(c, h_choice, d_g, d_ef, d_P, step, (cudaStream_t)stream);
+}
+
+int lgreco_psgd_q(lgreco_ctx* c, const int32_t* h_choice, const float* d_g, const float* d_ef, const float* d_Psum,
+                  int32_t W, float* d_Q, void* stream) {
+  if (!c || !h_choice || !d_g || !d_Psum || !d_Q || W < 1 || c->family != LGRECO_POWERSGD) return LGRECO_EINVAL;
+  return psgd_q(c, h_choice, d_g, d_ef, d_Psum, W, d_Q, (cudaStream_t)stream);
+}
+
+int lgreco_psgd_out(lgreco_ctx* c, const int32_t* h_choice, const float* d_g, float* d_ef, const float* d_Qsum,
+                    int32_t W, float* d_out, void* stream) {
+  if (!c || !h_choice || !d_g || !d_Qsum || W < 1 || c->family != LGRECO_POWERSGD) return LGRECO_EINVAL;
+  return psgd_out(c, h_choice, d_g, d_ef, d_Qsum, W, d_out, (cudaStream_t)stream);
+}
+
+int lgreco_psgd_raw_pack(lgreco_ctx* c, const int32_t* h_choice, const float* d_g, float* d_ef, uint8_t* d_payload,
+                         float* d_out, void* stream) {
+  if (!c || !h_choice || !d_g || c->family != LGRECO_POWERSGD) return LGRECO_EINVAL;
+  return psgd_raw_pack(c, h_choice, d_g, d_ef, d_payload, d_out, (cudaStream_t)stream);
+}
+
+int lgreco_psgd_raw_combine(lgreco_ctx* c, const int32_t* h_choice, int32_t W, const uint8_t* d_gathered,
+                            float* d_out, void* stream) {
+  if (!c || !h_choice || W < 1 || !d_gathered || !d_out || c->family != LGRECO_POWERSGD) return LGRECO_EINVAL;
+  return psgd_raw_combine(c, h_choice, W, d_gathered, d_out, (cudaStream_t)stream);
 }
 
 int lgreco_debug_philox(const uint32_t* d_ctr, uint32_t key0, uint32_t key1, int64_t n, uint32_t* d_out, void* stream) {

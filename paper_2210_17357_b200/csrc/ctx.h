@@ -83,5 +83,22 @@ int topk_combine(lgreco_ctx* c, const int32_t* choice, int W, const uint8_t* gat
 int topk_compress_allreduce(lgreco_ctx* c, const int32_t* choice, const float* g, float* ef, float* out,
                             cudaStream_t st);
 int64_t topk_payload_bytes(lgreco_ctx* c, const int32_t* choice);
+int psgd_init(lgreco_ctx* c, cudaStream_t st);
+void psgd_destroy(lgreco_ctx* c);
+int psgd_profile(lgreco_ctx* c, const float* g, const float* e, uint64_t step, double* err, int64_t* bits,
+                 cudaStream_t st);
+int64_t psgd_payload_bytes(lgreco_ctx* c, const int32_t* choice);
+int psgd_p(lgreco_ctx* c, const int32_t* choice, const float* g, const float* e, float* d_P, uint64_t step,
+           cudaStream_t st);
+int psgd_q(lgreco_ctx* c, const int32_t* choice, const float* g, const float* e, const float* d_Psum, int W,
+           float* d_Q, cudaStream_t st);
+int psgd_out(lgreco_ctx* c, const int32_t* choice, const float* g, float* ef, const float* d_Qsum, int W, float* out,
+             cudaStream_t st);
+int psgd_raw_pack(lgreco_ctx* c, const int32_t* choice, const float* g, float* ef, uint8_t* payload, float* out,
+                  cudaStream_t st);
+int psgd_raw_combine(lgreco_ctx* c, const int32_t* choice, int W, const uint8_t* gathered, float* out, cudaStream_t st);
+int psgd_compress_allreduce(lgreco_ctx* c, const int32_t* choice, const float* g, float* ef, float* out,
+                            uint64_t step, cudaStream_t st);
+int64_t psgd_sizes(lgreco_ctx* c, int which);
 
 

@@ -427,6 +427,10 @@ k_solve_fast(const double* __restrict__ err, const int64_t* __restrict__ bits, i
   double* sm_ce = reinterpret_cast<double*>(smem_raw);         // [La] metric(err[choice])
   int64_t* sm_cb = reinterpret_cast<int64_t*>(sm_ce + La);    // [La] bits[choice]
   int used_default = s_La;
+  if (used_default) {
+    for (int a = tid; a < La; a += DP_THREADS) choice[act[a]] = default_idx[act[a]];
+    __syncthreads();
+  }
   for (int pass = 0; pass < 2; ++pass) {
     for (int a = tid; a < La; a += DP_THREADS) {
       const int l = act[a];

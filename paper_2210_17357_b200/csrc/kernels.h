@@ -77,6 +77,38 @@ cudaError_t launch_topk_combine(const uint8_t* gathered, int64_t S, int W, float
                                 int nC, const int64_t* kpre, int64_t ktotal, const TPlan* tplan, cudaStream_t st,
                                 int64_t* launches);
 
+// PowerSGD (psgd.cu) ---------------------------------------------------------------
+struct PLayer {        // one compressed matrix layer in a grouped launch
+  int64_t moff;        // element offset of M (m x k row-major) in the flat gradient
+  int32_t m, k, r;     // view and the rank of this launch
+  int32_t layer;       // layer index in the table
+  int64_t poff, qoff, goff;  // offsets into P (m x r), Q (k x r) col-major, G (r x r)
+  int64_t qstride;     // elements between split partials of Q
+  int32_t nsplit, pad;
+};
+struct PTile { int32_t ci, split, i0, i1, c0, pad; };  // row tile (i0) or column tile (c0, rows [i0,i1))
+struct RawSeg { int64_t off, n, pay_off; };            // raw (uncompressed) segment of the gradient
+struct PsArgs {
+  const float* g; const float* e; const PLayer* pl; int nC;
+  const PTile* rtiles; int n_rtiles; const PTile* ctiles; int n_ctiles; int rmax;
+};
+cudaError_t launch_ps_initq(const PsArgs& a, float* Q, uint32_t k0, uint32_t k1, uint32_t step, const int32_t* only,
+                            cudaStream_t st);
+cudaError_t launch_ps_mq(const PsArgs& a, const float* Q, float* P, double* nrm_part, cudaStream_t st);
+cudaError_t launch_ps_orth(const PsArgs& a, const float* P, float scale, double* G, float* Ph, cudaStream_t st);
+cudaError_t launch_ps_mtp(const PsArgs& a, const float* Ph, float* part, float* Q, float scale, cudaStream_t st);
+cudaError_t launch_ps_mtp_scale(const PsArgs& a, const float* src, float* dst, float scale, cudaStream_t st);
+cudaError_t launch_ps_err(const PsArgs& a, const double* nrm_part, const int32_t* rtile0, const float* Ph,
+                          const float* Q, const int32_t* ranks, int K, double* err, int64_t* bits, double* nrm,
+                          int32_t* need, double* dpart, cudaStream_t st);
+cudaError_t launch_ps_lossless_rows(const DevLayer* layers, int L, int K, const int32_t* ismat, double* err,
+                                    int64_t* bits, cudaStream_t st);
+cudaError_t launch_ps_out(const PsArgs& a, float* ef, float* out, const float* Ph, const float* Q, cudaStream_t st);
+cudaError_t launch_ps_raw_pack(const float* g, float* ef, uint8_t* payload, float* out, const RawSeg* segs, int nseg,
+                               unsigned* flag, cudaStream_t st);
+cudaError_t launch_ps_raw_mean(const uint8_t* gathered, int64_t S, int W, float* out, const RawSeg* segs, int nseg,
+                               cudaStream_t st);
+
 // Algorithm 1 DP (dp.cu)
 struct SolveArgs {
   const double* err; const int64_t* bits; int L; int K;

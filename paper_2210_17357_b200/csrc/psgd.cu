@@ -1,0 +1,532 @@
+// psgd.cu -- PowerSGD on sm_100a: the power-iteration contractions P = M Q and
+// Q = M^T P, fp64 Cholesky-QR orthogonalisation, profile error and the
+// compressed reconstruction with error feedback.
+//
+//   K3 profile (a4): per matrix layer (view m x k, R11),
+//      one run at r_max of `steps` power steps from Q0 (Philox stream 2); every
+//      smaller candidate rank is the prefix of that run (pinned prefix property);
+//      err_r^2 = ||M||^2 - sum_{j<r} ||q_j||^2 (P orthonormal, Q = M^T P), with a
+//      direct fp64 ||M - P_r Q_r^T||_F fallback where err_r < 0.01 ||M||.
+//   K7 compress (a8-a10, R12): P = M Q_ws -> (all-reduce) -> orthogonalise ->
+//      Q = M^T P -> (all-reduce) -> out = P Q^T, e = x - out, Q_ws <- Q.
+//
+// The M operand is never materialised: x = fl(fl(g + e) + 0) is formed while the
+// tile is staged in shared memory.  Orthogonalisation: the oracle's modified
+// Gram-Schmidt and Cholesky-QR return the same Q factor (unique QR with a
+// positive diagonal) up to O(kappa^2 eps_64) -- far below the 1e-5 parity bar.
+#include <math.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace lg {
+
+constexpr int PS_THREADS = 256;
+constexpr int PS_TM = 64;   // rows per MQ tile / cols per MtP tile
+constexpr int PS_TK = 32;   // reduction depth staged per iteration
+
+__device__ __forceinline__ float xval(const float* __restrict__ g, const float* __restrict__ e, int64_t i) {
+  return canon(__ldg(g + i), e ? __ldg(e + i) : 0.f);
+}
+
+// ---------------------------------------------------------------------------
+// Q0 init (Philox stream 2): Q[j*k + c] = 2u - 1, ctr = ((j*k+c)>>2, layer, step, 2)
+// ---------------------------------------------------------------------------
+__global__ void k_ps_initq(const PLayer* __restrict__ pl, int nC, float* __restrict__ Q, uint32_t k0, uint32_t k1,
+                           uint32_t step, const int32_t* __restrict__ only /*nullable: init only flagged*/) {
+  const int ci = blockIdx.y;
+  if (ci >= nC) return;
+  const PLayer p = pl[ci];
+  if (only && !only[ci]) return;
+  const int64_t n = (int64_t)p.k * p.r;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    const U4 w = philox10((uint32_t)(t >> 2), (uint32_t)p.layer, step, 2u, k0, k1);
+    const uint32_t sel = (t & 3) == 0 ? w.x : (t & 3) == 1 ? w.y : (t & 3) == 2 ? w.z : w.w;
+    Q[p.qoff + t] = __fsub_rn(__fmul_rn(2.0f, word_u(sel)), 1.0f);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// P = M Q  (grouped over layers; tile = 64 rows x r <= RMAX; column-major P, Q)
+// also accumulates ||M||^2 of the tile (fp64) when nrm != nullptr
+// ---------------------------------------------------------------------------
+template <int RMAX>
+__global__ void __launch_bounds__(PS_THREADS)
+k_ps_mq(const float* __restrict__ g, const float* __restrict__ e, const PLayer* __restrict__ pl,
+        const PTile* __restrict__ tiles, const float* __restrict__ Q, float* __restrict__ P,
+        double* __restrict__ nrm_part) {
+  constexpr int CPT = RMAX / 16;  // output columns per thread
+  __shared__ float Ms[PS_TM][PS_TK + 1];
+  __shared__ float Qs[PS_TK][RMAX];
+  __shared__ double red[PS_THREADS / 32];
+  const PTile tl = tiles[blockIdx.x];
+  const PLayer p = pl[tl.ci];
+  const int tid = threadIdx.x;
+  const int ty = tid >> 4, tx = tid & 15;  // 16 x 16 threads: 4 rows x CPT cols each
+  const int r = p.r;
+  float acc[4][CPT];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < CPT; ++b) acc[a][b] = 0.f;
+  double nsq = 0.0;
+  const int rows = min(PS_TM, p.m - tl.i0);
+  for (int c0 = 0; c0 < p.k; c0 += PS_TK) {
+    // stage M tile (64 x 32) and Q tile (32 x r)
+    for (int t = tid; t < PS_TM * PS_TK; t += PS_THREADS) {
+      const int rr = t / PS_TK, cc = t % PS_TK;
+      float v = 0.f;
+      if (rr < rows && c0 + cc < p.k) v = xval(g, e, p.moff + (int64_t)(tl.i0 + rr) * p.k + c0 + cc);
+      Ms[rr][cc] = v;
+      if (nrm_part) nsq += (double)v * (double)v;
+    }
+    for (int t = tid; t < PS_TK * RMAX; t += PS_THREADS) {
+      const int j = t / PS_TK, cc = t % PS_TK;
+      Qs[cc][j] = (j < r && c0 + cc < p.k) ? Q[p.qoff + (int64_t)j * p.k + c0 + cc] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int cc = 0; cc < PS_TK; ++cc) {
+      float mv[4], qv[CPT];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) mv[a] = Ms[ty + 16 * a][cc];
+#pragma unroll
+      for (int b = 0; b < CPT; ++b) qv[b] = Qs[cc][tx + 16 * b];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < CPT; ++b) acc[a][b] = __fmaf_rn(mv[a], qv[b], acc[a][b]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < CPT; ++b) {
+      const int i = ty + 16 * a, j = tx + 16 * b;
+      if (i < rows && j < r) P[p.poff + (int64_t)j * p.m + tl.i0 + i] = acc[a][b];
+    }
+  if (nrm_part) {
+    nsq = warp_sum_d(nsq);
+    if ((tid & 31) == 0) red[tid >> 5] = nsq;
+    __syncthreads();
+    if (tid == 0) {
+      double s = 0.0;
+      for (int w = 0; w < PS_THREADS / 32; ++w) s += red[w];
+      nrm_part[blockIdx.x] = s;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// partial Q = M^T P over a row split: tile = 64 columns x r; partial[split][j*k + c]
+// ---------------------------------------------------------------------------
+template <int RMAX>
+__global__ void __launch_bounds__(PS_THREADS)
+k_ps_mtp(const float* __restrict__ g, const float* __restrict__ e, const PLayer* __restrict__ pl,
+         const PTile* __restrict__ tiles, const float* __restrict__ Ph, float* __restrict__ part) {
+  constexpr int CPT = RMAX / 16;
+  __shared__ float Ms[PS_TK][PS_TM + 1];
+  __shared__ float Ps[PS_TK][RMAX];
+  const PTile tl = tiles[blockIdx.x];
+  const PLayer p = pl[tl.ci];
+  const int tid = threadIdx.x;
+  const int ty = tid >> 4, tx = tid & 15;
+  const int r = p.r;
+  const int cols = min(PS_TM, p.k - tl.c0);
+  float acc[4][CPT];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < CPT; ++b) acc[a][b] = 0.f;
+  for (int i0 = tl.i0; i0 < tl.i1; i0 += PS_TK) {
+    for (int t = tid; t < PS_TK * PS_TM; t += PS_THREADS) {
+      const int rr = t / PS_TM, cc = t % PS_TM;
+      Ms[rr][cc] = (i0 + rr < tl.i1 && cc < cols) ? xval(g, e, p.moff + (int64_t)(i0 + rr) * p.k + tl.c0 + cc) : 0.f;
+    }
+    for (int t = tid; t < PS_TK * RMAX; t += PS_THREADS) {
+      const int j = t / PS_TK, rr = t % PS_TK;
+      Ps[rr][j] = (j < r && i0 + rr < tl.i1) ? Ph[p.poff + (int64_t)j * p.m + i0 + rr] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int rr = 0; rr < PS_TK; ++rr) {
+      float mv[4], pv[CPT];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) mv[a] = Ms[rr][ty + 16 * a];
+#pragma unroll
+      for (int b = 0; b < CPT; ++b) pv[b] = Ps[rr][tx + 16 * b];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < CPT; ++b) acc[a][b] = __fmaf_rn(mv[a], pv[b], acc[a][b]);
+    }
+    __syncthreads();
+  }
+  float* out = part + (int64_t)tl.split * p.qstride + p.qoff;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < CPT; ++b) {
+      const int c = ty + 16 * a, j = tx + 16 * b;
+      if (c < cols && j < r) out[(int64_t)j * p.k + tl.c0 + c] = acc[a][b];
+    }
+}
+
+// Q = scale * sum_{split} partial (fixed order)
+__global__ void k_ps_reduce(const PLayer* __restrict__ pl, int nC, const float* __restrict__ part,
+                            float* __restrict__ Q, float scale) {
+  const int ci = blockIdx.y;
+  if (ci >= nC) return;
+  const PLayer p = pl[ci];
+  const int64_t n = (int64_t)p.k * p.r;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    float s = part[p.qoff + t];
+    for (int sp = 1; sp < p.nsplit; ++sp) s = __fadd_rn(s, part[(int64_t)sp * p.qstride + p.qoff + t]);
+    Q[p.qoff + t] = __fmul_rn(s, scale);
+  }
+}
+
+// Qdst = fl(scale * Qsrc) over each layer's k x r block
+__global__ void k_ps_scale(const PLayer* __restrict__ pl, int nC, const float* __restrict__ src, float* __restrict__ dst,
+                           float scale) {
+  const int ci = blockIdx.y;
+  if (ci >= nC) return;
+  const PLayer p = pl[ci];
+  const int64_t n = (int64_t)p.k * p.r;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x)
+    dst[p.qoff + t] = __fmul_rn(src[p.qoff + t], scale);
+}
+
+// ---------------------------------------------------------------------------
+// Gram matrix G = Pbar^T Pbar (fp64), Pbar = fl(scale * P); one block per layer
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(PS_THREADS)
+k_ps_gram(const PLayer* __restrict__ pl, const float* __restrict__ P, float scale, double* __restrict__ G) {
+  const PLayer p = pl[blockIdx.x];
+  const int r = p.r;
+  // thread handles entries (a, b), a <= b, strided
+  const int npairs = r * (r + 1) / 2;
+  for (int t = threadIdx.x; t < npairs; t += PS_THREADS) {
+    int a = 0, rem = t;
+    while (rem >= r - a) { rem -= r - a; ++a; }
+    const int b = a + rem;
+    const float* pa = P + p.poff + (int64_t)a * p.m;
+    const float* pb = P + p.poff + (int64_t)b * p.m;
+    double s = 0.0;
+    for (int i = 0; i < p.m; ++i) {
+      const double x = (double)__fmul_rn(pa[i], scale), y = (double)__fmul_rn(pb[i], scale);
+      s = fma(x, y, s);
+    }
+    G[p.goff + a * r + b] = s;
+    G[p.goff + b * r + a] = s;
+  }
+}
+
+// Cholesky G = R^T R (R upper, positive diagonal) in smem, then Phat rows:
+// phat R = pbar (forward substitution per row).  A pivot <= 1e-24 * G[j][j]
+// (or G[j][j] == 0) marks column j as zero, like MGS's zero column.
+__global__ void __launch_bounds__(PS_THREADS)
+k_ps_cholsolve(const PLayer* __restrict__ pl, const PTile* __restrict__ tiles, const double* __restrict__ G,
+               const float* __restrict__ P, float scale, float* __restrict__ Ph) {
+  __shared__ double Rm[64][65];
+  __shared__ int zero[64];
+  const PTile tl = tiles[blockIdx.x];
+  const PLayer p = pl[tl.ci];
+  const int r = p.r;
+  for (int t = threadIdx.x; t < r * r; t += PS_THREADS) Rm[t / r][t % r] = G[p.goff + t];
+  __syncthreads();
+  if (threadIdx.x < 32) {  // one warp: right-looking Cholesky on the upper triangle
+    for (int j = 0; j < r; ++j) {
+      const double gjj = G[p.goff + j * r + j];
+      double d = Rm[j][j];
+      const bool z = !(d > 1e-24 * gjj) || gjj == 0.0;
+      d = z ? 0.0 : sqrt(d);
+      __syncwarp();
+      if (threadIdx.x == 0) { Rm[j][j] = d; zero[j] = z; }
+      __syncwarp();
+      for (int b = j + 1 + threadIdx.x; b < r; b += 32) Rm[j][b] = z ? 0.0 : Rm[j][b] / d;
+      __syncwarp();
+      for (int a = j + 1; a < r; ++a)
+        for (int b = a + threadIdx.x; b < r; b += 32) Rm[a][b] -= Rm[j][a] * Rm[j][b];
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  const int rows = min(PS_TM, p.m - tl.i0);
+  for (int i = threadIdx.x; i < rows; i += PS_THREADS) {
+    double ph[64];
+    for (int j = 0; j < r; ++j) {
+      double s = (double)__fmul_rn(P[p.poff + (int64_t)j * p.m + tl.i0 + i], scale);
+      for (int t = 0; t < j; ++t) s -= ph[t] * Rm[t][j];
+      ph[j] = zero[j] ? 0.0 : s / Rm[j][j];
+    }
+    for (int j = 0; j < r; ++j) Ph[p.poff + (int64_t)j * p.m + tl.i0 + i] = (float)ph[j];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// profile error from the identity; flags layers that need the direct form
+// ---------------------------------------------------------------------------
+__global__ void k_ps_err_identity(const PLayer* __restrict__ pl, int nC, const double* __restrict__ nrm_part,
+                                  const int32_t* __restrict__ tile0, const float* __restrict__ Q,
+                                  const int32_t* __restrict__ ranks, int K, double* __restrict__ err,
+                                  int64_t* __restrict__ bits, double* __restrict__ nrm, int32_t* __restrict__ need_direct) {
+  const int ci = blockIdx.x;
+  if (ci >= nC) return;
+  const PLayer p = pl[ci];
+  __shared__ double qn[64];
+  __shared__ double s_nrm;
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int t = tile0[ci]; t < tile0[ci + 1]; ++t) s += nrm_part[t];
+    s_nrm = s;
+    nrm[ci] = s;
+  }
+  for (int j = threadIdx.x; j < p.r; j += blockDim.x) {
+    double s = 0.0;
+    for (int c = 0; c < p.k; ++c) {
+      const double v = Q[p.qoff + (int64_t)j * p.k + c];
+      s = fma(v, v, s);
+    }
+    qn[j] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int need = 0;
+    for (int t = 0; t < K; ++t) {
+      const int r = ranks[t];
+      const int64_t m = p.m, k = p.k;
+      if ((int64_t)r * (m + k) >= m * k) {  // lossless-equivalent (R11)
+        err[(int64_t)p.layer * K + t] = 0.0;
+        bits[(int64_t)p.layer * K + t] = 32 * m * k;
+        continue;
+      }
+      double s = 0.0;
+      for (int j = 0; j < r; ++j) s += qn[j];
+      const double e2 = s_nrm - s;
+      const double ev = e2 > 0.0 ? sqrt(e2) : 0.0;
+      err[(int64_t)p.layer * K + t] = ev;
+      bits[(int64_t)p.layer * K + t] = 32 * (int64_t)r * (m + k);
+      if (!(ev >= 0.01 * sqrt(s_nrm))) need = 1;
+    }
+    need_direct[ci] = need;
+  }
+}
+
+// direct ||M - P_r Q_r^T||_F^2 for candidate ranks [t0, t0+8) of flagged layers (fp64)
+__global__ void __launch_bounds__(PS_THREADS)
+k_ps_err_direct(const float* __restrict__ g, const float* __restrict__ e, const PLayer* __restrict__ pl,
+                const PTile* __restrict__ tiles, const float* __restrict__ Ph, const float* __restrict__ Q,
+                const int32_t* __restrict__ ranks, int K, const int32_t* __restrict__ need, double* __restrict__ part) {
+  const PTile tl = tiles[blockIdx.x];
+  const PLayer p = pl[tl.ci];
+  if (!need[tl.ci]) return;
+  __shared__ double red[PS_THREADS / 32][8];
+  const int t0 = blockIdx.y * 8;
+  double acc[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+  const int rows = min(PS_TM, p.m - tl.i0);
+  for (int64_t el = threadIdx.x; el < (int64_t)rows * p.k; el += PS_THREADS) {
+    const int i = tl.i0 + (int)(el / p.k), c = (int)(el % p.k);
+    const double x = (double)xval(g, e, p.moff + (int64_t)i * p.k + c);
+    double rec = 0.0;
+    int j = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int t = t0 + q;
+      if (t >= K) break;
+      const int r = min(ranks[t], p.r);
+      for (; j < r; ++j) rec = fma((double)Ph[p.poff + (int64_t)j * p.m + i], (double)Q[p.qoff + (int64_t)j * p.k + c], rec);
+      const double d = x - rec;
+      acc[q] = fma(d, d, acc[q]);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const double v = warp_sum_d(acc[q]);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][q] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 8) {
+    double s = 0.0;
+    for (int w = 0; w < PS_THREADS / 32; ++w) s += red[w][threadIdx.x];
+    part[((int64_t)blockIdx.x) * ((K + 7) / 8 * 8) + t0 + threadIdx.x] = s;
+  }
+}
+
+__global__ void k_ps_err_direct_final(const PLayer* __restrict__ pl, int nC, const int32_t* __restrict__ tile0,
+                                      const int32_t* __restrict__ ranks, int K, const int32_t* __restrict__ need,
+                                      const double* __restrict__ part, double* __restrict__ err) {
+  const int ci = blockIdx.x;
+  if (ci >= nC || !need[ci]) return;
+  const PLayer p = pl[ci];
+  const int KP = (K + 7) / 8 * 8;
+  for (int t = threadIdx.x; t < K; t += blockDim.x) {
+    const int64_t m = p.m, k = p.k;
+    if ((int64_t)ranks[t] * (m + k) >= m * k) continue;
+    double s = 0.0;
+    for (int b = tile0[ci]; b < tile0[ci + 1]; ++b) s += part[(int64_t)b * KP + t];
+    err[(int64_t)p.layer * K + t] = sqrt(s);
+  }
+}
+
+// lossless / vector layers of the profile table: err 0, bits 32 n
+__global__ void k_ps_lossless_rows(const DevLayer* __restrict__ layers, int L, int K, const int32_t* __restrict__ ismat,
+                                   double* __restrict__ err, int64_t* __restrict__ bits) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)L * K; i += (int64_t)gridDim.x * blockDim.x) {
+    const int l = (int)(i / K);
+    if (!ismat[l]) { err[i] = 0.0; bits[i] = 32 * layers[l].numel; }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// compress output: out = Phat Q^T, e' = x - out (fused EF), one tile of rows
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(PS_THREADS)
+k_ps_out(const float* __restrict__ g, float* __restrict__ ef, float* __restrict__ out, const PLayer* __restrict__ pl,
+         const PTile* __restrict__ tiles, const float* __restrict__ Ph, const float* __restrict__ Q) {
+  const PTile tl = tiles[blockIdx.x];
+  const PLayer p = pl[tl.ci];
+  __shared__ float Prow[PS_TM][64];
+  const int rows = min(PS_TM, p.m - tl.i0);
+  for (int t = threadIdx.x; t < PS_TM * 64; t += PS_THREADS) {
+    const int i = t % PS_TM, j = t / PS_TM;
+    Prow[i][j] = (i < rows && j < p.r) ? Ph[p.poff + (int64_t)j * p.m + tl.i0 + i] : 0.f;
+  }
+  __syncthreads();
+  for (int64_t el = threadIdx.x; el < (int64_t)rows * p.k; el += PS_THREADS) {
+    const int i = (int)(el / p.k), c = (int)(el % p.k);
+    const int64_t idx = p.moff + (int64_t)(tl.i0 + i) * p.k + c;
+    float s = 0.f;
+    for (int j = 0; j < p.r; ++j) s = __fmaf_rn(Prow[i][j], Q[p.qoff + (int64_t)j * p.k + c], s);
+    const float x = canon(__ldg(g + idx), ef ? ef[idx] : 0.f);
+    if (out) out[idx] = s;
+    if (ef) ef[idx] = __fsub_rn(x, s);
+  }
+}
+
+// raw layers (vectors, lossless-equivalent ranks): payload = x, e' = 0, out = x (W=1)
+__global__ void __launch_bounds__(PS_THREADS)
+k_ps_raw_pack(const float* __restrict__ g, float* __restrict__ ef, uint8_t* __restrict__ payload, float* __restrict__ out,
+              const RawSeg* __restrict__ segs, unsigned* __restrict__ flag) {
+  const RawSeg s = segs[blockIdx.x];
+  float* raw = payload ? reinterpret_cast<float*>(payload + s.pay_off) : nullptr;
+  float bad = 0.f;
+  for (int64_t i = threadIdx.x; i < s.n; i += PS_THREADS) {
+    const int64_t idx = s.off + i;
+    const float x = canon(__ldg(g + idx), ef ? ef[idx] : 0.f);
+    bad = __fadd_rn(bad, __fmul_rn(x, 0.f));
+    if (raw) raw[i] = x;
+    if (out) out[idx] = x;
+    if (ef) ef[idx] = 0.f;
+  }
+  if (!isfinite(bad)) atomicOr(flag, 1u);
+}
+
+// raw layers after the all-gather: out = (ordered sum over ranks) * fl(1/W)
+__global__ void __launch_bounds__(PS_THREADS)
+k_ps_raw_mean(const uint8_t* __restrict__ gathered, int64_t S, int W, float* __restrict__ out,
+              const RawSeg* __restrict__ segs) {
+  const RawSeg s = segs[blockIdx.x];
+  const float invW = __fdiv_rn(1.0f, (float)W);
+  for (int64_t i = threadIdx.x; i < s.n; i += PS_THREADS) {
+    float v = 0.f;
+    for (int w = 0; w < W; ++w) {
+      const float x = __ldg(reinterpret_cast<const float*>(gathered + w * S + s.pay_off) + i);
+      v = (w == 0) ? x : __fadd_rn(v, x);
+    }
+    out[s.off + i] = __fmul_rn(v, invW);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+template <int RMAX>
+static void mq_launch(const PsArgs& a, const float* Q, float* P, double* nrm_part, cudaStream_t st) {
+  k_ps_mq<RMAX><<<a.n_rtiles, PS_THREADS, 0, st>>>(a.g, a.e, a.pl, a.rtiles, Q, P, nrm_part);
+}
+template <int RMAX>
+static void mtp_launch(const PsArgs& a, const float* Ph, float* part, cudaStream_t st) {
+  k_ps_mtp<RMAX><<<a.n_ctiles, PS_THREADS, 0, st>>>(a.g, a.e, a.pl, a.ctiles, Ph, part);
+}
+
+cudaError_t launch_ps_initq(const PsArgs& a, float* Q, uint32_t k0, uint32_t k1, uint32_t step, const int32_t* only,
+                            cudaStream_t st) {
+  if (a.nC == 0) return cudaSuccess;
+  k_ps_initq<<<dim3(64, a.nC), 256, 0, st>>>(a.pl, a.nC, Q, k0, k1, step, only);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ps_mq(const PsArgs& a, const float* Q, float* P, double* nrm_part, cudaStream_t st) {
+  if (a.n_rtiles == 0) return cudaSuccess;
+  if (a.rmax <= 16) mq_launch<16>(a, Q, P, nrm_part, st);
+  else if (a.rmax <= 32) mq_launch<32>(a, Q, P, nrm_part, st);
+  else mq_launch<64>(a, Q, P, nrm_part, st);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ps_orth(const PsArgs& a, const float* P, float scale, double* G, float* Ph, cudaStream_t st) {
+  if (a.nC == 0) return cudaSuccess;
+  k_ps_gram<<<a.nC, PS_THREADS, 0, st>>>(a.pl, P, scale, G);
+  k_ps_cholsolve<<<a.n_rtiles, PS_THREADS, 0, st>>>(a.pl, a.rtiles, G, P, scale, Ph);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ps_mtp(const PsArgs& a, const float* Ph, float* part, float* Q, float scale, cudaStream_t st) {
+  if (a.n_ctiles == 0) return cudaSuccess;
+  if (a.rmax <= 16) mtp_launch<16>(a, Ph, part, st);
+  else if (a.rmax <= 32) mtp_launch<32>(a, Ph, part, st);
+  else mtp_launch<64>(a, Ph, part, st);
+  k_ps_reduce<<<dim3(32, a.nC), 256, 0, st>>>(a.pl, a.nC, part, Q, scale);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ps_mtp_scale(const PsArgs& a, const float* src, float* dst, float scale, cudaStream_t st) {
+  if (a.nC == 0) return cudaSuccess;
+  k_ps_scale<<<dim3(32, a.nC), 256, 0, st>>>(a.pl, a.nC, src, dst, scale);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ps_err(const PsArgs& a, const double* nrm_part, const int32_t* rtile0, const float* Ph,
+                          const float* Q, const int32_t* ranks, int K, double* err, int64_t* bits, double* nrm,
+                          int32_t* need, double* dpart, cudaStream_t st) {
+  if (a.nC == 0) return cudaSuccess;
+  k_ps_err_identity<<<a.nC, 64, 0, st>>>(a.pl, a.nC, nrm_part, rtile0, Q, ranks, K, err, bits, nrm, need);
+  k_ps_err_direct<<<dim3(a.n_rtiles, (K + 7) / 8), PS_THREADS, 0, st>>>(a.g, a.e, a.pl, a.rtiles, Ph, Q, ranks, K,
+                                                                         need, dpart);
+  k_ps_err_direct_final<<<a.nC, 128, 0, st>>>(a.pl, a.nC, rtile0, ranks, K, need, dpart, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ps_lossless_rows(const DevLayer* layers, int L, int K, const int32_t* ismat, double* err,
+                                    int64_t* bits, cudaStream_t st) {
+  k_ps_lossless_rows<<<64, 256, 0, st>>>(layers, L, K, ismat, err, bits);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ps_out(const PsArgs& a, float* ef, float* out, const float* Ph, const float* Q, cudaStream_t st) {
+  if (a.n_rtiles == 0) return cudaSuccess;
+  k_ps_out<<<a.n_rtiles, PS_THREADS, 0, st>>>(a.g, ef, out, a.pl, a.rtiles, Ph, Q);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ps_raw_pack(const float* g, float* ef, uint8_t* payload, float* out, const RawSeg* segs, int nseg,
+                               unsigned* flag, cudaStream_t st) {
+  if (nseg == 0) return cudaSuccess;
+  k_ps_raw_pack<<<nseg, PS_THREADS, 0, st>>>(g, ef, payload, out, segs, flag);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ps_raw_mean(const uint8_t* gathered, int64_t S, int W, float* out, const RawSeg* segs, int nseg,
+                               cudaStream_t st) {
+  if (nseg == 0) return cudaSuccess;
+  k_ps_raw_mean<<<nseg, PS_THREADS, 0, st>>>(gathered, S, W, out, segs);
+  return cudaGetLastError();
+}
+
+}  // namespace lg

@@ -65,6 +65,12 @@ _SIGS = {
     "lgreco_qsgd_unpack": (C.c_int, [_VP, _VP, _VP, _VP, _VP]),
     "lgreco_topk_pack": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _VP]),
     "lgreco_topk_combine": (C.c_int, [_VP, _VP, _I32, _VP, _VP, _VP]),
+    "lgreco_psgd_sizes": (C.c_int, [_VP, _VP, _VP]),
+    "lgreco_psgd_p": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _U64, _VP]),
+    "lgreco_psgd_q": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _I32, _VP, _VP]),
+    "lgreco_psgd_out": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _I32, _VP, _VP]),
+    "lgreco_psgd_raw_pack": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _VP]),
+    "lgreco_psgd_raw_combine": (C.c_int, [_VP, _VP, _I32, _VP, _VP, _VP]),
     "lgreco_debug_philox": (C.c_int, [_VP, _U32, _U32, _I64, _VP, _VP]),
 }
 EXPORTED = tuple(_SIGS)
@@ -198,6 +204,31 @@ class Context:
     def topk_combine(self, choice, W, gathered, out, stream=None):
         _check(lib().lgreco_topk_combine(self.h, _i32(choice), W, _ptr(gathered), _ptr(out), _stream(stream)),
                "topk_combine")
+
+
+    def psgd_sizes(self):
+        p, q = C.c_int64(), C.c_int64()
+        _check(lib().lgreco_psgd_sizes(self.h, C.byref(p), C.byref(q)), "psgd_sizes")
+        return p.value, q.value
+
+    def psgd_p(self, choice, g, ef, P, step, stream=None):
+        _check(lib().lgreco_psgd_p(self.h, _i32(choice), _ptr(g), _ptr(ef), _ptr(P), step, _stream(stream)), "psgd_p")
+
+    def psgd_q(self, choice, g, ef, Psum, W, Q, stream=None):
+        _check(lib().lgreco_psgd_q(self.h, _i32(choice), _ptr(g), _ptr(ef), _ptr(Psum), W, _ptr(Q), _stream(stream)),
+               "psgd_q")
+
+    def psgd_out(self, choice, g, ef, Qsum, W, out, stream=None):
+        _check(lib().lgreco_psgd_out(self.h, _i32(choice), _ptr(g), _ptr(ef), _ptr(Qsum), W, _ptr(out),
+                                     _stream(stream)), "psgd_out")
+
+    def psgd_raw_pack(self, choice, g, ef, payload, out, stream=None):
+        _check(lib().lgreco_psgd_raw_pack(self.h, _i32(choice), _ptr(g), _ptr(ef), _ptr(payload), _ptr(out),
+                                          _stream(stream)), "psgd_raw_pack")
+
+    def psgd_raw_combine(self, choice, W, gathered, out, stream=None):
+        _check(lib().lgreco_psgd_raw_combine(self.h, _i32(choice), W, _ptr(gathered), _ptr(out), _stream(stream)),
+               "psgd_raw_combine")
 
 
 def solve_workspace_bytes(L, K, D) -> int:
