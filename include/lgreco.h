@@ -159,6 +159,13 @@ int64_t lgreco_payload_bytes(lgreco_ctx* ctx, const int32_t* h_choice);
 int lgreco_shard_bounds(lgreco_ctx* ctx, const int32_t* h_choice, int32_t W,
                         int64_t* h_rec_bounds, int64_t* h_byte_bounds);
 
+/* Host-only (no device, no ctx): payload bytes S of plan h_choice and, for QSGD,
+ * the W byte-balanced shard bounds (R13) -- every rank computes the same bounds.
+ * TopK/PowerSGD: S = bytes of the pair arrays / raw layers; bounds (0..0, S). */
+int lgreco_plan_layout(const lgreco_layer* layers, int32_t L, const lgreco_candidates* cand,
+                       const int32_t* h_choice, int32_t W, int64_t* h_S, int64_t* h_rec_bounds,
+                       int64_t* h_byte_bounds);
+
 /* QSGD stage 1 (K5): pack x = d_g + d_ef for rank field `rank` into d_payload
  * (S bytes, record layout R7), update d_ef (nullable), write decoded values to
  * d_dec (nullable). */

@@ -403,6 +403,50 @@ int ref_qsgd_allreduce(const ref_layer* layers, int32_t L, const int32_t* lbits,
     return st;
 }
 
+/* Owner side of the exchange for one shard (R13): records [r0, r1) whose stage-1
+ * bytes from the W ranks sit rank-major in recv (W x shard_bytes, shard starting at
+ * byte0).  Writes the stage-2 records at their payload offsets in pay2. */
+int ref_qsgd_reduce_shard(const ref_layer* layers, int32_t L, const int32_t* lbits, int32_t B, uint64_t seed,
+                          uint64_t step, int32_t W, const uint8_t* recv, int64_t r0, int64_t r1, int64_t byte0,
+                          int64_t shard_bytes, uint8_t* pay2) {
+    int64_t* bs = (int64_t*)malloc(sizeof(int64_t) * (L + 1));
+    int64_t* bo = (int64_t*)malloc(sizeof(int64_t) * (L + 1));
+    ref_layout(layers, L, lbits, B, bs, bo);
+    float invW = 1.0f / (float)W;
+    float* tmp = (float*)malloc(sizeof(float) * B);
+    float* acc = (float*)malloc(sizeof(float) * B);
+    float* dec2 = (float*)malloc(sizeof(float) * B);
+    float* u = (float*)malloc(sizeof(float) * B);
+    uint32_t* q = (uint32_t*)malloc(sizeof(uint32_t) * B);
+    int st = REF_OK;
+    for (int l = 0; l < L && st == REF_OK; l++) {
+        int64_t n = layers[l].numel;
+        for (int64_t j = 0; j < bs[l + 1] - bs[l] && st == REF_OK; j++) {
+            int64_t r = bs[l] + j;
+            if (r < r0 || r >= r1) continue;
+            int32_t nv = (int32_t)((n - j * B) < B ? (n - j * B) : B);
+            int64_t roff = bo[l] + (lbits[l] > 0 ? j * rec_bytes_full(lbits[l], B) : j * 4 * (int64_t)B);
+            for (int w = 0; w < W; w++) {
+                const uint8_t* src = recv + (int64_t)w * shard_bytes + (roff - byte0);
+                if (lbits[l] > 0) unpack_record(src, nv, lbits[l], B, tmp);
+                else memcpy(tmp, src, sizeof(float) * nv);
+                for (int i = 0; i < nv; i++) acc[i] = (w == 0) ? tmp[i] : acc[i] + tmp[i];
+            }
+            for (int i = 0; i < nv; i++) acc[i] = acc[i] * invW;
+            if (lbits[l] > 0) {
+                float mn, unit;
+                ref_bucket_uniforms(seed, 0xFFFFFFFFu, step, 1u, r, B, nv, u);
+                st = ref_quantize_bucket(acc, nv, lbits[l], u, q, dec2, &mn, &unit);
+                if (st == REF_OK) pack_record(pay2 + roff, q, nv, lbits[l], B, mn, unit);
+            } else {
+                memcpy(pay2 + roff, acc, sizeof(float) * nv);
+            }
+        }
+    }
+    free(tmp); free(acc); free(dec2); free(u); free(q); free(bs); free(bo);
+    return st;
+}
+
 /* ------------------------------------------------------------------------ */
 /* TopK (R8-R10).                                                             */
 /* ------------------------------------------------------------------------ */

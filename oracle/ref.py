@@ -175,6 +175,14 @@ def qsgd_allreduce(layers, lbits, g_ranks, e_ranks, B=128, seed=0, step=0):
     return out, es, [p1[w * S:(w + 1) * S] for w in range(W)], p2[:S]
 
 
+def qsgd_reduce_shard(layers, lbits, B, seed, step, W, recv, r0, r1, byte0, shard_bytes, pay2):
+    recv = np.ascontiguousarray(recv, dtype=np.uint8)
+    st = lib().ref_qsgd_reduce_shard(_layers(layers), C.c_int32(len(layers)), _p(_i32(lbits)), C.c_int32(B),
+                                     C.c_uint64(seed), C.c_uint64(step), C.c_int32(W), _p(recv), C.c_int64(r0),
+                                     C.c_int64(r1), C.c_int64(byte0), C.c_int64(shard_bytes), _p(pay2))
+    _check(st, "qsgd_reduce_shard")
+
+
 # ---------------------------------------------------------------------- TopK
 def topk_k(n, ppm):
     return int(lib().ref_topk_k(C.c_int64(n), C.c_int32(ppm)))

@@ -473,6 +473,57 @@ int lgreco_psgd_raw_combine(lgreco_ctx* c, const int32_t* h_choice, int32_t W, c
   return psgd_raw_combine(c, h_choice, W, d_gathered, d_out, (cudaStream_t)stream);
 }
 
+int lgreco_plan_layout(const lgreco_layer* layers, int32_t L, const lgreco_candidates* cand, const int32_t* h_choice,
+                       int32_t W, int64_t* h_S, int64_t* h_rec_bounds, int64_t* h_byte_bounds) {
+  if (!layers || L <= 0 || !cand || !cand->params || !h_choice || W < 1 || !h_S) return LGRECO_EINVAL;
+  lgreco_ctx c;  // host-only view: no device state is touched
+  c.L = L; c.K = cand->K; c.family = cand->family;
+  c.B = cand->family == LGRECO_QSGD ? cand->qbucket : 128;
+  if (c.B < 128 || c.B % 128) return LGRECO_EINVAL;
+  c.layers.assign(layers, layers + L);
+  c.params.assign(cand->params, cand->params + cand->K);
+  c.bucket0.resize(L + 1);
+  int64_t gb = 0;
+  for (int l = 0; l < L; ++l) { c.bucket0[l] = gb; gb += (layers[l].numel + c.B - 1) / c.B; }
+  c.bucket0[L] = gb;
+  c.R = gb;
+  int64_t S = 0;
+  if (cand->family == LGRECO_QSGD) {
+    std::vector<lg::DevPlan> plan;
+    LG_TRY(qsgd_layout(&c, h_choice, plan, S));
+    std::vector<int64_t> rb, bb;
+    shard_bounds(&c, plan, S, W, rb, bb);
+    if (h_rec_bounds) memcpy(h_rec_bounds, rb.data(), sizeof(int64_t) * (W + 1));
+    if (h_byte_bounds) memcpy(h_byte_bounds, bb.data(), sizeof(int64_t) * (W + 1));
+  } else {
+    for (int l = 0; l < L; ++l) {
+      const lgreco_layer& ly = layers[l];
+      int64_t bytes = 4 * ly.numel;
+      if (ly.compress) {
+        const int j = h_choice[l];
+        if (j < 0 || j >= cand->K) return LGRECO_EINVAL;
+        const int32_t prm = cand->params[j];
+        if (cand->family == LGRECO_TOPK) {
+          int64_t k = ((int64_t)prm * ly.numel + 999999) / 1000000;
+          k = std::max<int64_t>(1, std::min<int64_t>(k, ly.numel));
+          bytes = 8 * k;
+        } else if (ly.rows > 0 && (int64_t)prm * (ly.rows + ly.cols) < ly.numel) {
+          bytes = 0;  // low-rank factors travel through the all-reduces
+        }
+      }
+      S += bytes;
+      S = (S + 15) & ~(int64_t)15;
+    }
+    if (h_rec_bounds || h_byte_bounds)
+      for (int j = 0; j <= W; ++j) {
+        if (h_rec_bounds) h_rec_bounds[j] = 0;
+        if (h_byte_bounds) h_byte_bounds[j] = j == W ? S : 0;
+      }
+  }
+  *h_S = S;
+  return LGRECO_OK;
+}
+
 int lgreco_debug_philox(const uint32_t* d_ctr, uint32_t key0, uint32_t key1, int64_t n, uint32_t* d_out, void* stream) {
   cudaError_t e = lg::launch_philox(d_ctr, key0, key1, n, d_out, (cudaStream_t)stream);
   if (e != cudaSuccess) { lg_set_error("philox: %s", cudaGetErrorString(e)); return LGRECO_ECUDA; }

@@ -65,6 +65,7 @@ _SIGS = {
     "lgreco_qsgd_unpack": (C.c_int, [_VP, _VP, _VP, _VP, _VP]),
     "lgreco_topk_pack": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _VP]),
     "lgreco_topk_combine": (C.c_int, [_VP, _VP, _I32, _VP, _VP, _VP]),
+    "lgreco_plan_layout": (C.c_int, [_VP, _I32, _VP, _VP, _I32, _VP, _VP, _VP]),
     "lgreco_psgd_sizes": (C.c_int, [_VP, _VP, _VP]),
     "lgreco_psgd_p": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _U64, _VP]),
     "lgreco_psgd_q": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _I32, _VP, _VP]),
@@ -229,6 +230,20 @@ class Context:
     def psgd_raw_combine(self, choice, W, gathered, out, stream=None):
         _check(lib().lgreco_psgd_raw_combine(self.h, _i32(choice), W, _ptr(gathered), _ptr(out), _stream(stream)),
                "psgd_raw_combine")
+
+
+def plan_layout(layers, family, params, choice, W, qbucket=128):
+    """Host-only payload layout / shard bounds (no GPU needed)."""
+    L = len(layers)
+    arr = (Layer * L)(*[Layer(l.offset, l.numel, l.rows, l.cols, l.compress) for l in layers])
+    pa = _i32(params)
+    cand = Candidates(family, len(params), C.cast(pa, C.POINTER(C.c_int32)), qbucket, 5, 0)
+    S = C.c_int64()
+    rb = (C.c_int64 * (W + 1))()
+    bb = (C.c_int64 * (W + 1))()
+    _check(lib().lgreco_plan_layout(C.cast(arr, C.c_void_p), L, C.cast(C.pointer(cand), C.c_void_p), _i32(choice), W,
+                                    C.byref(S), rb, bb), "plan_layout")
+    return S.value, list(rb), list(bb)
 
 
 def solve_workspace_bytes(L, K, D) -> int:
