@@ -644,10 +644,17 @@ static void mat_mtp(const double* M, int64_t m, int64_t k, int32_t r, const doub
             Q[j * k + c] = s;
         }
 }
-/* Modified Gram-Schmidt on the columns of P (in place); zero-norm column stays 0. */
+/* Modified Gram-Schmidt on the columns of P (in place).  A column whose norm after
+ * the projections is <= 1e-12 of its norm before them is numerically dependent on the
+ * previous columns and is set to 0 (R11: "a column with norm 0 stays 0", read in
+ * floating point; without the relative test fp64 round-off would be normalised into a
+ * spurious, non-orthogonal direction). */
 void ref_mgs(double* P, int64_t m, int32_t r) {
     for (int j = 0; j < r; j++) {
         double* pj = P + (int64_t)j * m;
+        double n0 = 0.0;
+        for (int64_t t = 0; t < m; t++) n0 += pj[t] * pj[t];
+        n0 = sqrt(n0);
         for (int i = 0; i < j; i++) {
             const double* pi = P + (int64_t)i * m;
             double d = 0.0;
@@ -657,7 +664,8 @@ void ref_mgs(double* P, int64_t m, int32_t r) {
         double nrm = 0.0;
         for (int64_t t = 0; t < m; t++) nrm += pj[t] * pj[t];
         nrm = sqrt(nrm);
-        for (int64_t t = 0; t < m; t++) pj[t] = nrm > 0.0 ? pj[t] / nrm : 0.0;
+        int zero = !(nrm > 1e-12 * n0);
+        for (int64_t t = 0; t < m; t++) pj[t] = zero ? 0.0 : pj[t] / nrm;
     }
 }
 

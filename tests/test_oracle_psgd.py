@@ -142,3 +142,15 @@ def test_exchange_w1_and_mean(ref):
     s = (xs[0][600:610] + xs[1][600:610]).astype(np.float32)
     s = (s + xs[2][600:610]).astype(np.float32)
     assert np.array_equal(out[600:610], (s * np.float32(1 / 3)).astype(np.float32))
+
+
+def test_rank_deficient_dependent_columns_dropped(ref):
+    # exactly rank-2 M: with r > 2 the extra power-iteration columns are numerically
+    # dependent; they are dropped (zero), so err_r stays at the exact value 0
+    rng = np.random.default_rng(0)
+    M = (rng.standard_normal((50, 2)) @ rng.standard_normal((2, 40))).astype(np.float32).astype(np.float64)
+    for r in (2, 4, 8):
+        P, Q = ref.psgd_power(M, ref.psgd_init_q(1, 0, 0, 40, r), 5)
+        assert ref.psgd_err(M, P, Q) <= 1e-12 * np.linalg.norm(M)
+        if r > 2:
+            assert not P[:, 2:].any()
