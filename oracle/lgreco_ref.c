@@ -644,23 +644,25 @@ static void mat_mtp(const double* M, int64_t m, int64_t k, int32_t r, const doub
             Q[j * k + c] = s;
         }
 }
-/* Modified Gram-Schmidt on the columns of P (in place).  A column whose norm after
- * the projections is <= 1e-12 of its norm before them is numerically dependent on the
- * previous columns and is set to 0 (R11: "a column with norm 0 stays 0", read in
- * floating point; without the relative test fp64 round-off would be normalised into a
- * spurious, non-orthogonal direction). */
+/* Modified Gram-Schmidt with one reorthogonalisation sweep ("twice is enough") on
+ * the columns of P (in place).  A column whose norm after the projections is <= 1e-12
+ * of its norm before them is numerically dependent on the previous columns and is
+ * set to 0 (R11: "a column with norm 0 stays 0", read in floating point).  A single
+ * MGS sweep loses orthogonality on nearly dependent columns (tests/test_oracle_psgd.py
+ * rank-deficient pin); the second sweep restores it to round-off. */
 void ref_mgs(double* P, int64_t m, int32_t r) {
     for (int j = 0; j < r; j++) {
         double* pj = P + (int64_t)j * m;
         double n0 = 0.0;
         for (int64_t t = 0; t < m; t++) n0 += pj[t] * pj[t];
         n0 = sqrt(n0);
-        for (int i = 0; i < j; i++) {
-            const double* pi = P + (int64_t)i * m;
-            double d = 0.0;
-            for (int64_t t = 0; t < m; t++) d += pi[t] * pj[t];
-            for (int64_t t = 0; t < m; t++) pj[t] -= d * pi[t];
-        }
+        for (int sweep = 0; sweep < 2; sweep++)
+            for (int i = 0; i < j; i++) {
+                const double* pi = P + (int64_t)i * m;
+                double d = 0.0;
+                for (int64_t t = 0; t < m; t++) d += pi[t] * pj[t];
+                for (int64_t t = 0; t < m; t++) pj[t] -= d * pi[t];
+            }
         double nrm = 0.0;
         for (int64_t t = 0; t < m; t++) nrm += pj[t] * pj[t];
         nrm = sqrt(nrm);

@@ -205,7 +205,7 @@ int psgd_profile(lgreco_ctx* c, const float* g, const float* e, uint64_t step, d
     LG_LAUNCH(c, lg::launch_ps_mq(a, p->Qprof, p->P, s == 0 ? p->nrm_part : nullptr, st));
     LG_LAUNCH(c, lg::launch_ps_orth(a, p->P, 1.0f, p->G, p->Ph, st));
     LG_LAUNCH(c, lg::launch_ps_mtp(a, p->Ph, p->part, p->Qprof, 1.0f, st));
-    c->launches += 5;
+    c->launches += 7;
   }
   LG_LAUNCH(c, lg::launch_ps_err(a, p->nrm_part, p->d_rtile0_prof, p->Ph, p->Qprof, p->d_ranks, c->K, err, bits,
                                  p->nrm, p->need, p->dpart, st));
@@ -333,7 +333,7 @@ int psgd_q(lgreco_ctx* c, const int32_t* choice, const float* g, const float* e,
   const float invW = 1.0f / (float)W;
   LG_LAUNCH(c, lg::launch_ps_orth(a, d_Psum ? d_Psum : p->P, invW, p->G, p->Ph, st));
   LG_LAUNCH(c, lg::launch_ps_mtp(a, p->Ph, p->part, d_Q ? d_Q : p->Qn, 1.0f, st));
-  c->launches += 4;
+  c->launches += 6;
   return LGRECO_OK;
 }
 

@@ -230,7 +230,7 @@ k_ps_gram(const PLayer* __restrict__ pl, const float* __restrict__ P, float scal
 // (or G[j][j] == 0) marks column j as zero, like MGS's zero column.
 __global__ void __launch_bounds__(PS_THREADS)
 k_ps_cholsolve(const PLayer* __restrict__ pl, const PTile* __restrict__ tiles, const double* __restrict__ G,
-               const float* __restrict__ P, float scale, float* __restrict__ Ph) {
+               const float* P, float scale, float* Ph) {  // P may alias Ph (row-local)
   __shared__ double Rm[64][65];
   __shared__ int zero[64];
   const PTile tl = tiles[blockIdx.x];
@@ -472,8 +472,12 @@ cudaError_t launch_ps_mq(const PsArgs& a, const float* Q, float* P, double* nrm_
 
 cudaError_t launch_ps_orth(const PsArgs& a, const float* P, float scale, double* G, float* Ph, cudaStream_t st) {
   if (a.nC == 0) return cudaSuccess;
+  // Cholesky-QR twice (CholQR2): the second pass restores orthogonality to round-off
+  // when P is ill-conditioned (nearly dependent power-iteration columns)
   k_ps_gram<<<a.nC, PS_THREADS, 0, st>>>(a.pl, P, scale, G);
   k_ps_cholsolve<<<a.n_rtiles, PS_THREADS, 0, st>>>(a.pl, a.rtiles, G, P, scale, Ph);
+  k_ps_gram<<<a.nC, PS_THREADS, 0, st>>>(a.pl, Ph, 1.0f, G);
+  k_ps_cholsolve<<<a.n_rtiles, PS_THREADS, 0, st>>>(a.pl, a.rtiles, G, Ph, 1.0f, Ph);
   return cudaGetLastError();
 }
 
