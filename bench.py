@@ -73,21 +73,40 @@ class ClockSampler:
         self._thr = None
 
     def _run(self):
-        import pynvml as N
         try:
+            import pynvml as N
             N.nvmlInit()
             h = N.nvmlDeviceGetHandleByIndex(self.idx)
             self.max_mhz = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
-            bits = {k: getattr(N, v) for k, v in self.REASONS.items()}
+            bits = {k: getattr(N, v, 0) for k, v in self.REASONS.items()}
+            get_reasons = getattr(N, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                N.nvmlDeviceGetCurrentClocksThrottleReasons
             while not self._stop.is_set():
                 self.sm.append(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM))
-                r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                r = get_reasons(h)
                 for k, bit in bits.items():
-                    if r & bit:
+                    if bit and (r & bit):
                         self.reasons.add(k)
                 self._stop.wait(0.002)
-        except Exception as ex:  # no NVML: report nothing rather than guess
-            self.err = str(ex)
+        except Exception as ex:  # fall back to nvidia-smi polling
+            self.err = f"nvml: {ex}"
+            import subprocess
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip().split(",")
+                    self.sm.append(float(out[0]))
+                    self.max_mhz = float(out[1])
+                    for n, v in zip(names, out[2:]):
+                        if v.strip().lower() == "active":
+                            self.reasons.add(n)
+                except Exception as ex2:
+                    self.err += f"; smi: {ex2}"
+                    break
 
     def start(self):
         import threading
@@ -99,9 +118,10 @@ class ClockSampler:
         if self._thr:
             self._thr.join(timeout=5)
         if not self.sm:
-            return None
+            return {"error": getattr(self, "err", "no samples")}
         return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
-                "samples": len(self.sm), "source": "nvml, 2 ms, timed region"}
+                "samples": len(self.sm), "source": "nvml 2 ms" if not hasattr(self, "err") else "nvidia-smi",
+                "min_mhz": min(self.sm)}
 
 
 # ---------------------------------------------------------------------- our arm
@@ -249,10 +269,89 @@ def run_ours(args):
         }
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline_full()
-        print(json.dumps(line), flush=True)
     ctx.close()
+    if not args.no_extras:
+        ex = run_extras(dev, rank, world, stream, l2_flush, nccl_dist=(world > 1))
+        if rank == 0:
+            line["extras"] = ex
+    if rank == 0:
+        print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_extras(dev, rank, world, stream, l2_flush, nccl_dist):
+    """Secondary rows measured the same way (device-timed step, L2 flushed), on
+    device-generated seeded inputs (per-layer sigma log-uniform, Gaussian): C2 PowerSGD,
+    C3 TopK, C5 QSGD.  Reported as extras; the headline line is C4."""
+    import torch
+    import torch.distributed as dist
+    from paper_2210_17357_b200 import lgreco
+    specs = [("C2", lgreco.POWERSGD, W.PSGD_RANKS_C2, 2, "ResNet-18 CIFAR-10 PowerSGD r{1,2,4,8,16}"),
+             ("C3", lgreco.TOPK, W.TOPK_PPM_C3, 9, "Transformer-XL TopK 0.1%..10%"),
+             ("C5", lgreco.QSGD, W.QSGD_BITS, 2, "GPT-2-medium-like QSGD 2..8 bits")]
+    res = {}
+    for name, fam, params, dflt_i, desc in specs:
+        layers = W.config_layers(name)
+        N = W.total_numel(layers)
+        L, K = len(layers), len(params)
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(0x5EED + rank)
+        sig = torch.zeros(N, device=dev)
+        for l in layers:
+            sig[l.offset:l.offset + l.numel] = 10.0 ** (-4 + 3 * torch.rand(1, generator=gen, device=dev))
+        g = torch.randn(N, generator=gen, device=dev) * sig
+        ef = torch.randn(N, generator=gen, device=dev) * sig * 0.1
+        del sig
+        out = torch.empty_like(g)
+        err = torch.empty(L, K, dtype=torch.float64, device=dev)
+        bits = torch.empty(L, K, dtype=torch.int64, device=dev)
+        dflt = torch.full((L,), dflt_i, dtype=torch.int32, device=dev)
+        comp = torch.tensor([l.compress for l in layers], dtype=torch.int32, device=dev)
+        ch_d = torch.empty(L, dtype=torch.int32, device=dev)
+        info = torch.empty(48, dtype=torch.uint8, device=dev)
+        ws = torch.empty(lgreco.solve_workspace_bytes(L, K, D_BINS), dtype=torch.uint8, device=dev)
+        ch_h = torch.empty(L, dtype=torch.int32).pin_memory()
+        nid = None
+        if world > 1:
+            obj = [lgreco.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            nid = obj[0]
+        ctx = lgreco.Context(layers, fam, params, qbucket=128, seed=SEED, rank=rank, world=world, nccl_id=nid)
+        t = {"profile": [], "solve": [], "compress_allreduce": [], "step": []}
+        for s in range(7):
+            if s >= 2:
+                l2_flush.zero_()
+            m = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            m[0].record(stream)
+            ctx.profile(g, ef, s, err, bits)
+            m[1].record(stream)
+            lgreco.solve(err, bits, dflt, comp, D=D_BINS, choice=ch_d, info=info, workspace=ws)
+            ctx.plan_broadcast(ch_d)
+            m[2].record(stream)
+            ch_h.copy_(ch_d, non_blocking=True)
+            stream.synchronize()
+            ctx.compress_allreduce(ch_h.tolist(), g, ef, out, s)
+            m[3].record(stream)
+            torch.cuda.synchronize()
+            if s >= 2:
+                t["profile"].append(m[0].elapsed_time(m[1]))
+                t["solve"].append(m[1].elapsed_time(m[2]))
+                t["compress_allreduce"].append(m[2].elapsed_time(m[3]))
+                t["step"].append(m[0].elapsed_time(m[3]))
+        ctx.check()
+        ctx.close()
+        st = {k: sum(v) / len(v) for k, v in t.items()}
+        if world > 1:
+            tt = torch.tensor([st[k] for k in ("step", "profile", "solve", "compress_allreduce")], device=dev,
+                              dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            st = dict(zip(("step", "profile", "solve", "compress_allreduce"), tt.tolist()))
+        res[name] = {"workload": desc, "n": N, "gbs": round(world * 4.0 * N / (st["step"] * 1e-3) / 1e9, 2),
+                     "stage_ms": {k: round(v, 4) for k, v in st.items()}, "steps": 5}
+        del g, ef, out
+        torch.cuda.empty_cache()
+    return res
 
 
 def _ncu_traffic():
@@ -335,6 +434,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the C2/C3/C5 secondary measurements")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

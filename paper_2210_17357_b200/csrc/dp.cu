@@ -187,7 +187,7 @@ __device__ __forceinline__ uint64_t gcd64(uint64_t a, uint64_t b) {
   return a;
 }
 
-template <int CPT>
+template <int CPT, int KT>
 __global__ void __launch_bounds__(DP_THREADS, 1)
 k_solve_fast(const double* __restrict__ err, const int64_t* __restrict__ bits, int L, int K,
              const int32_t* __restrict__ default_idx, const int32_t* __restrict__ compress, int D, uint32_t flags,
@@ -278,7 +278,7 @@ k_solve_fast(const double* __restrict__ err, const int64_t* __restrict__ bits, i
   }
   __syncthreads();
   if (tid == 0) {
-    s_wide = (s_mx >= (1ull << (31 - s_cbits))) ? 1 : 0;
+    s_wide = (s_mx >= (1ull << (30 - s_cbits))) ? 1 : 0;  // 32-bit keys < 2^30 < INF32
     if (s_mx >= (1ull << (62 - s_cbits)) && s_status == LGRECO_OK) s_status = LGRECO_EINVAL;
   }
   __syncthreads();
@@ -310,7 +310,7 @@ k_solve_fast(const double* __restrict__ err, const int64_t* __restrict__ bits, i
   uint32_t* r32b = r32a + row32;
   uint64_t* r64a = reinterpret_cast<uint64_t*>(smem_raw);
   uint64_t* r64b = r64a + row64;
-  const uint32_t INF32 = 0x7FFFFFFFu;
+  const uint32_t INF32 = 0x7FFFFF00u;  // > every 32-bit key; INF32 + addend < 2^32
   const uint64_t INF64 = 1ull << 62;
   if (!wide) {
     for (int i = tid; i < row32; i += DP_THREADS) { r32a[i] = (i == W1) ? 0u : INF32; r32b[i] = INF32; }
@@ -333,21 +333,37 @@ k_solve_fast(const double* __restrict__ err, const int64_t* __restrict__ bits, i
       uint32_t best[CPT];
 #pragma unroll
       for (int i = 0; i < CPT; ++i) best[i] = 0xFFFFFFFFu;
-      for (int c = 0; c < K; ++c) {
-        const int d = s_disc[sb][c];
-        if (d < 0) continue;
-        const uint32_t ak = (uint32_t)s_add[sb][c];
-        const uint32_t* pv = prev - d + tid;
+      if (KT > 0) {
+        // compile-time candidate bound: every prev[] read is an LDS with an immediate offset
 #pragma unroll
-        for (int i = 0; i < CPT; ++i) best[i] = min(best[i], pv[i * DP_THREADS] + ak);
+        for (int c = 0; c < (KT > 0 ? KT : 1); ++c) {
+          if (c < K) {
+            const int d = s_disc[sb][c];
+            if (d >= 0) {
+              const uint32_t ak = (uint32_t)s_add[sb][c];
+              const uint32_t* pv = prev - d + tid;
+#pragma unroll
+              for (int i = 0; i < CPT; ++i) best[i] = min(best[i], pv[i * DP_THREADS] + ak);
+            }
+          }
+        }
+      } else {
+        for (int c = 0; c < K; ++c) {
+          const int d = s_disc[sb][c];
+          if (d < 0) continue;
+          const uint32_t ak = (uint32_t)s_add[sb][c];
+          const uint32_t* pv = prev - d + tid;
+#pragma unroll
+          for (int i = 0; i < CPT; ++i) best[i] = min(best[i], pv[i * DP_THREADS] + ak);
+        }
       }
 #pragma unroll
       for (int i = 0; i < CPT; ++i) {
         const int e = tid + i * DP_THREADS;
         if (e < W1) {
           const uint32_t k = best[i];
-          cur[e] = (k >= INF32) ? INF32 : (k & ~(uint32_t)cmask);
-          pdrow[e] = (uint8_t)((k >= INF32) ? 0 : (k & (uint32_t)cmask));
+          cur[e] = min(k, INF32) & ~(uint32_t)cmask;  // unreachable stays >= INF32
+          pdrow[e] = (uint8_t)(k & (uint32_t)cmask);   // read only on the backtrack path
         }
       }
     } else {
@@ -491,12 +507,16 @@ cudaError_t launch_solve(const SolveArgs& a, void* ws, cudaStream_t st) {
   // the prelude stages 24 bytes per layer in the same shared memory
   if (cpt <= 12 && fast_smem <= 200 * 1024 && (size_t)24 * a.L + 64 <= fast_smem) {
     cudaError_t e = cudaSuccess;
-#define LG_SF(C)                                                                                       \
-  case C:                                                                                              \
-    e = cudaFuncSetAttribute(k_solve_fast<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); \
-    if (e != cudaSuccess) return e;                                                                    \
-    k_solve_fast<C><<<1, DP_THREADS, fast_smem, st>>>(a.err, a.bits, a.L, a.K, a.default_idx, a.compress, a.D, \
-                                                     a.flags, a.choice, a.info, pd, act, wdisc, wadd); \
+#define LG_SF2(C, KT)                                                                                      \
+  {                                                                                                          \
+    e = cudaFuncSetAttribute(k_solve_fast<C, KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);  \
+    if (e != cudaSuccess) return e;                                                                          \
+    k_solve_fast<C, KT><<<1, DP_THREADS, fast_smem, st>>>(a.err, a.bits, a.L, a.K, a.default_idx, a.compress, \
+                                                          a.D, a.flags, a.choice, a.info, pd, act, wdisc, wadd); \
+  }
+#define LG_SF(C)                                       \
+  case C:                                              \
+    if (a.K <= 8) LG_SF2(C, 8) else if (a.K <= 16) LG_SF2(C, 16) else LG_SF2(C, 0) \
     break;
     switch (cpt) { LG_SF(1) LG_SF(2) LG_SF(3) LG_SF(4) LG_SF(5) LG_SF(6) LG_SF(7) LG_SF(8) LG_SF(9) LG_SF(10)
                    LG_SF(11) LG_SF(12) }
