@@ -215,6 +215,12 @@ int lgreco_psgd_raw_pack(lgreco_ctx* ctx, const int32_t* h_choice, const float* 
 int lgreco_psgd_raw_combine(lgreco_ctx* ctx, const int32_t* h_choice, int32_t W, const uint8_t* d_gathered,
                             float* d_out, void* stream);
 
+/* Debug: P = M Q through the tcgen05 kind::tf32 (3xTF32) path for one matrix:
+ * M = d_g + d_e (m x k row-major, d_e nullable), d_Q k x r column-major (r <= 64),
+ * d_P m x r column-major.  Synchronises `stream`. */
+int lgreco_debug_tc_mq(const float* d_g, const float* d_e, int64_t m, int32_t k, const float* d_Q, int32_t r,
+                       float* d_P, void* stream);
+
 /* Debug: Philox4x32-10 of n counters (d_ctr: n*4 u32, key) -> d_out n*4 u32. */
 int lgreco_debug_philox(const uint32_t* d_ctr, uint32_t key0, uint32_t key1, int64_t n,
                         uint32_t* d_out, void* stream);

@@ -391,3 +391,31 @@ int psgd_compress_allreduce(lgreco_ctx* c, const int32_t* choice, const float* g
 
 float* psgd_internal_P(lgreco_ctx* c) { return c->ps ? c->ps->P : nullptr; }
 int64_t psgd_sizes(lgreco_ctx* c, int which) { return !c->ps ? 0 : which == 0 ? c->ps->Psz : c->ps->Qsz; }
+
+// Debug / unit-test entry: P = M Q on the tcgen05 path for one matrix (M = canon(g + e),
+// m x k row-major; Q k x r column-major; P m x r column-major).  Allocates its tiny
+// descriptor arrays (debug only).
+extern "C" int lgreco_debug_tc_mq(const float* d_g, const float* d_e, int64_t m, int32_t k, const float* d_Q, int32_t r,
+                                  float* d_P, void* stream) {
+  if (!d_g || !d_Q || !d_P || m <= 0 || k <= 0 || r < 1 || r > 64 || m > 0x7fffffff) return LGRECO_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  lg::PLayer pl{0, (int32_t)m, k, r, 0, 0, 0, 0, (int64_t)k * r, 1, 0};
+  std::vector<lg::PTile> tiles;
+  for (int64_t i0 = 0; i0 < m; i0 += 128) tiles.push_back(lg::PTile{0, 0, (int32_t)i0, 0, 0, 0});
+  lg::PLayer* d_pl = nullptr;
+  lg::PTile* d_t = nullptr;
+  LG_CUDA(cudaMalloc(&d_pl, sizeof(pl)));
+  LG_CUDA(cudaMalloc(&d_t, sizeof(lg::PTile) * tiles.size()));
+  LG_CUDA(cudaMemcpyAsync(d_pl, &pl, sizeof(pl), cudaMemcpyHostToDevice, st));
+  LG_CUDA(cudaMemcpyAsync(d_t, tiles.data(), sizeof(lg::PTile) * tiles.size(), cudaMemcpyHostToDevice, st));
+  lg::PsArgs a{d_g, d_e, d_pl, 1, nullptr, 0, nullptr, 0, r};
+  cudaError_t e = lg::launch_ps_mq_tc(a, d_t, (int)tiles.size(), d_Q, d_P, st);
+  cudaError_t e2 = cudaStreamSynchronize(st);
+  cudaFree(d_pl);
+  cudaFree(d_t);
+  if (e != cudaSuccess || e2 != cudaSuccess) {
+    lg_set_error("tc_mq: %s / %s", cudaGetErrorString(e), cudaGetErrorString(e2));
+    return LGRECO_ECUDA;
+  }
+  return LGRECO_OK;
+}

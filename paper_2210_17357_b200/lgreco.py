@@ -72,6 +72,7 @@ _SIGS = {
     "lgreco_psgd_out": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _I32, _VP, _VP]),
     "lgreco_psgd_raw_pack": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _VP]),
     "lgreco_psgd_raw_combine": (C.c_int, [_VP, _VP, _I32, _VP, _VP, _VP]),
+    "lgreco_debug_tc_mq": (C.c_int, [_VP, _VP, _I64, _I32, _VP, _I32, _VP, _VP]),
     "lgreco_debug_philox": (C.c_int, [_VP, _U32, _U32, _I64, _VP, _VP]),
 }
 EXPORTED = tuple(_SIGS)
@@ -278,3 +279,7 @@ def debug_philox(ctr, key0, key1, stream=None):
     out = torch.empty_like(ctr)
     _check(lib().lgreco_debug_philox(_ptr(ctr), key0, key1, n, _ptr(out), _stream(stream)), "debug_philox")
     return out
+
+
+def debug_tc_mq(g, e, m, k, Q, r, P, stream=None):
+    _check(lib().lgreco_debug_tc_mq(_ptr(g), _ptr(e), m, k, _ptr(Q), r, _ptr(P), _stream(stream)), "debug_tc_mq")
