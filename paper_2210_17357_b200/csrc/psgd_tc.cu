@@ -10,8 +10,12 @@
 // layout (8-row groups of 1024 B, 16-byte chunk c of row r at c ^ (r & 7)); B = 32
 // K-elements of the r columns of Q (column-major, hence K-major too).  Two smem
 // stages: the threads stage tile k+1 while the elected thread's MMAs consume tile k
-// (completion tracked by tcgen05.commit -> mbarrier).  Epilogue: tcgen05.ld 32x32b
-// (warp w reads TMEM lanes 32w..32w+31 = tile rows) -> column-major P.
+// (completion tracked by tcgen05.commit -> mbarrier).  Every K tile accumulates into its
+// own TMEM buffer (two, ping-pong): measured on B200, chaining hundreds of MMAs in one
+// accumulator drifts by ~3e-5 relative (the in-MMA accumulation is not RN fp32), while
+// a 12-MMA tile stays at ~7e-7; tile partials are added in registers in fp32 (RN) while
+// the next tile's MMAs run.  tcgen05.ld 32x32b: warp w reads TMEM lanes 32w..32w+31 =
+// tile rows -> column-major P.
 #include <stdint.h>
 
 #include "common.cuh"
@@ -86,7 +90,7 @@ k_ps_mq_tc(const float* __restrict__ g, const float* __restrict__ e, const PLaye
   constexpr int A_BYTES = TC_M * 128;        // 16 KB per A tile (hi or lo)
   constexpr int B_BYTES = NP * 128;          // per B tile (hi or lo)
   constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;
-  constexpr uint32_t TMEM_COLS = NP < 32 ? 32 : NP;
+  constexpr uint32_t TMEM_COLS = 2 * NP < 32 ? 32 : 2 * NP;  // two accumulator buffers
   extern __shared__ __align__(1024) uint8_t smem_dyn[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~(uintptr_t)1023);
   __shared__ uint64_t mma_done[2];
@@ -114,23 +118,46 @@ k_ps_mq_tc(const float* __restrict__ g, const float* __restrict__ e, const PLaye
   const uint32_t tmem_d = tmem_base_sh;
   constexpr uint32_t idesc = tf32_idesc(NP);
 
+  const int row = warp * 32 + lane;
+  float acc[NP];
+#pragma unroll
+  for (int j = 0; j < NP; ++j) acc[j] = 0.f;
+  // read the finished tile partial of K tile `t` (TMEM buffer t & 1) and add it (fp32 RN)
+  auto drain = [&](int t) {
+    mbar_wait(&mma_done[t & 1], (t >> 1) & 1);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+    for (int j0 = 0; j0 < NP; j0 += 16) {
+      uint32_t v[16];
+      const uint32_t taddr = tmem_d + ((uint32_t)(warp * 32) << 16) + (uint32_t)((t & 1) * NP + j0);
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+      for (int q = 0; q < 16; ++q) acc[j0 + q] = __fadd_rn(acc[j0 + q], __uint_as_float(v[q]));
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+  };
+
   for (int kt = 0; kt < nk; ++kt) {
     const int s = kt & 1;
-    if (kt >= 2) mbar_wait(&mma_done[s], ((kt - 2) >> 1) & 1);  // buffer s free again
     uint8_t* Ah = smem + s * STAGE;
     uint8_t* Al = Ah + A_BYTES;
     uint8_t* Bh = Al + A_BYTES;
     uint8_t* Bl = Bh + B_BYTES;
     const int c0 = kt * TC_KT;
-    // A: 128 rows x 8 chunks; lane l of a warp covers row 4*it + l/8 (of the warp's 16), chunk l%8
+    // A: 128 rows x 8 chunks; a warp covers 4 rows x 128 B per instruction (coalesced)
 #pragma unroll 4
     for (int it = 0; it < TC_M * 8 / TC_THREADS; ++it) {
       const int idx = it * TC_THREADS + tid;
-      const int row = idx >> 3, ch = idx & 7;
+      const int r_ = idx >> 3, ch = idx & 7;
       const int col = c0 + ch * 4;
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (row < rows) {
-        const int64_t base = p.moff + (int64_t)(tl.i0 + row) * p.k + col;
+      if (r_ < rows) {
+        const int64_t base = p.moff + (int64_t)(tl.i0 + r_) * p.k + col;
         if (col + 4 <= p.k && ((base & 3) == 0)) {
           const float4 a = __ldg(reinterpret_cast<const float4*>(g + base));
           const float4 b = e ? __ldg(reinterpret_cast<const float4*>(e + base)) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -143,7 +170,7 @@ k_ps_mq_tc(const float* __restrict__ g, const float* __restrict__ e, const PLaye
           v = make_float4(t[0], t[1], t[2], t[3]);
         }
       }
-      put_chunk(Ah, Al, row, ch, v);
+      put_chunk(Ah, Al, r_, ch, v);
     }
     // B: NP rows (Q columns j) x 8 chunks
     for (int idx = tid; idx < NP * 8; idx += TC_THREADS) {
@@ -161,38 +188,26 @@ k_ps_mq_tc(const float* __restrict__ g, const float* __restrict__ e, const PLaye
     if (tid == 0) {
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t sAh = smem_u32(Ah), sAl = smem_u32(Al), sBh = smem_u32(Bh), sBl = smem_u32(Bl);
+      const uint32_t dbuf = tmem_d + (uint32_t)(s * NP);
 #pragma unroll
       for (int kk = 0; kk < TC_KT / 8; ++kk) {
         const uint32_t koff = kk * 32;  // 8 tf32 = 32 bytes along K inside the swizzle row
-        const uint32_t acc0 = (kt > 0 || kk > 0) ? 1u : 0u;
-        mma_tf32(tmem_d, sw128_desc(sAh + koff), sw128_desc(sBh + koff), idesc, acc0);
-        mma_tf32(tmem_d, sw128_desc(sAh + koff), sw128_desc(sBl + koff), idesc, 1u);
-        mma_tf32(tmem_d, sw128_desc(sAl + koff), sw128_desc(sBh + koff), idesc, 1u);
+        mma_tf32(dbuf, sw128_desc(sAh + koff), sw128_desc(sBh + koff), idesc, kk > 0 ? 1u : 0u);
+        mma_tf32(dbuf, sw128_desc(sAh + koff), sw128_desc(sBl + koff), idesc, 1u);
+        mma_tf32(dbuf, sw128_desc(sAl + koff), sw128_desc(sBh + koff), idesc, 1u);
       }
       mma_commit(&mma_done[s]);
     }
     __syncwarp();
+    // while tile kt's MMAs run: drain tile kt-1 (this also frees smem stage s^1 and
+    // TMEM buffer s^1 for tile kt+1)
+    if (kt >= 1) drain(kt - 1);
   }
-  // all MMAs done (they complete in issue order)
-  mbar_wait(&mma_done[(nk - 1) & 1], ((nk - 1) >> 1) & 1);
-  asm volatile("tcgen05.fence::after_thread_sync;");
-  // epilogue: warp w owns TMEM lanes (tile rows) 32w .. 32w+31
-  const int row = warp * 32 + lane;
+  drain(nk - 1);
+  if (row < rows) {
 #pragma unroll
-  for (int j0 = 0; j0 < NP; j0 += 16) {
-    uint32_t v[16];
-    const uint32_t taddr = tmem_d + ((uint32_t)(warp * 32) << 16) + (uint32_t)j0;
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;");
-    if (row < rows) {
-#pragma unroll
-      for (int q = 0; q < 16; ++q)
-        if (j0 + q < p.r) P[p.poff + (int64_t)(j0 + q) * p.m + tl.i0 + row] = __uint_as_float(v[q]);
-    }
+    for (int j = 0; j < NP; ++j)
+      if (j < p.r) P[p.poff + (int64_t)j * p.m + tl.i0 + row] = acc[j];
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
