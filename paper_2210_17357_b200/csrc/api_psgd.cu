@@ -13,8 +13,8 @@ struct Psgd {
   int Rmax = 0;
   // profile launch config
   lg::PLayer* d_pl_prof = nullptr;
-  lg::PTile *d_rt_prof = nullptr, *d_ct_prof = nullptr;
-  int n_prof = 0, nrt_prof = 0, nct_prof = 0, rmax_prof = 0;
+  lg::PTile *d_rt_prof = nullptr, *d_ct_prof = nullptr, *d_rt128_prof = nullptr, *d_ct128_prof = nullptr;
+  int n_prof = 0, nrt_prof = 0, nct_prof = 0, rmax_prof = 0, nrt128_prof = 0, nct128_prof = 0;
   int32_t* d_rtile0_prof = nullptr;
   int32_t* d_ranks = nullptr;
   int32_t* d_ismat = nullptr;
@@ -23,8 +23,8 @@ struct Psgd {
   bool plan_valid = false;
   std::vector<int32_t> cur_rank;    // rank currently held in Q_ws per matrix layer (0: none)
   lg::PLayer* d_pl_c = nullptr;
-  lg::PTile *d_rt_c = nullptr, *d_ct_c = nullptr;
-  int n_c = 0, nrt_c = 0, nct_c = 0, rmax_c = 0;
+  lg::PTile *d_rt_c = nullptr, *d_ct_c = nullptr, *d_rt128_c = nullptr, *d_ct128_c = nullptr;
+  int n_c = 0, nrt_c = 0, nct_c = 0, rmax_c = 0, nrt128_c = 0, nct128_c = 0;
   int32_t* d_initflag = nullptr;
   bool need_init = false;
   lg::RawSeg* d_raw = nullptr;
@@ -50,9 +50,10 @@ static constexpr int64_t RAW_CHUNK = 16384;
 
 // Build PLayer + tiles for the ranks `r` (per matrix layer; 0 = skip)
 static void ps_config(lgreco_ctx* c, const std::vector<int32_t>& r, std::vector<lg::PLayer>& pl,
-                      std::vector<lg::PTile>& rt, std::vector<lg::PTile>& ct, std::vector<int32_t>& rt0, int& rmax) {
+                      std::vector<lg::PTile>& rt, std::vector<lg::PTile>& ct, std::vector<int32_t>& rt0, int& rmax,
+                      std::vector<lg::PTile>& rt128, std::vector<lg::PTile>& ct128) {
   Psgd* p = c->ps;
-  pl.clear(); rt.clear(); ct.clear(); rt0.clear();
+  pl.clear(); rt.clear(); ct.clear(); rt0.clear(); rt128.clear(); ct128.clear();
   rmax = 0;
   for (int i = 0; i < p->nM; ++i) {
     if (r[i] <= 0) continue;
@@ -64,9 +65,11 @@ static void ps_config(lgreco_ctx* c, const std::vector<int32_t>& r, std::vector<
     rmax = std::max(rmax, r[i]);
     rt0.push_back((int32_t)rt.size());
     for (int i0 = 0; i0 < ly.rows; i0 += PS_TM) rt.push_back(lg::PTile{ci, 0, i0, 0, 0, 0});
+    for (int i0 = 0; i0 < ly.rows; i0 += 128) rt128.push_back(lg::PTile{ci, 0, i0, 0, 0, 0});
     for (int s = 0; s < nsplit; ++s) {
       const int i0 = (int)(s * PS_SPLIT_ROWS), i1 = (int)std::min<int64_t>(ly.rows, (s + 1) * PS_SPLIT_ROWS);
       for (int c0 = 0; c0 < ly.cols; c0 += PS_TM) ct.push_back(lg::PTile{ci, s, i0, i1, c0, 0});
+      for (int c0 = 0; c0 < ly.cols; c0 += 128) ct128.push_back(lg::PTile{ci, s, i0, i1, c0, 0});
     }
   }
   rt0.push_back((int32_t)rt.size());
@@ -109,10 +112,11 @@ int psgd_init(lgreco_ctx* c, cudaStream_t st) {
   p->cur_rank.assign(p->nM, 0);
   p->raw_cap = raw_cap;
   std::vector<lg::PLayer> pl;
-  std::vector<lg::PTile> rt, ct;
+  std::vector<lg::PTile> rt, ct, rt128, ct128;
   std::vector<int32_t> rt0;
-  ps_config(c, p->rprof, pl, rt, ct, rt0, p->rmax_prof);
+  ps_config(c, p->rprof, pl, rt, ct, rt0, p->rmax_prof, rt128, ct128);
   p->n_prof = (int)pl.size(); p->nrt_prof = (int)rt.size(); p->nct_prof = (int)ct.size();
+  p->nrt128_prof = (int)rt128.size(); p->nct128_prof = (int)ct128.size();
   const size_t KP = (size_t)((K + 7) / 8 * 8);
   // compress configs can use at most all matrix layers / tiles of the profile shapes
   size_t max_rt = 0, max_ct = 0, max_raw = 0;
@@ -122,7 +126,7 @@ int psgd_init(lgreco_ctx* c, cudaStream_t st) {
     max_ct += (size_t)((ly.rows + PS_SPLIT_ROWS - 1) / PS_SPLIT_ROWS) * ((ly.cols + PS_TM - 1) / PS_TM);
   }
   for (int l = 0; l < L; ++l) max_raw += (c->layers[l].numel + RAW_CHUNK - 1) / RAW_CHUNK;
-  p->stage_bytes = sizeof(lg::PLayer) * std::max(1, p->nM) + sizeof(lg::PTile) * (max_rt + max_ct + 2) +
+  p->stage_bytes = sizeof(lg::PLayer) * std::max(1, p->nM) + sizeof(lg::PTile) * 2 * (max_rt + max_ct + 2) +
                    sizeof(int32_t) * std::max(1, p->nM) + sizeof(lg::RawSeg) * (max_raw + 1) + 64;
 #define PS_ALLOC(ptr, bytes)                                                                \
   if (cudaMalloc((void**)&(ptr), std::max<size_t>((size_t)(bytes), 16)) != cudaSuccess) {  \
@@ -132,12 +136,16 @@ int psgd_init(lgreco_ctx* c, cudaStream_t st) {
   PS_ALLOC(p->d_pl_prof, sizeof(lg::PLayer) * std::max<size_t>(1, pl.size()));
   PS_ALLOC(p->d_rt_prof, sizeof(lg::PTile) * std::max<size_t>(1, rt.size()));
   PS_ALLOC(p->d_ct_prof, sizeof(lg::PTile) * std::max<size_t>(1, ct.size()));
+  PS_ALLOC(p->d_rt128_prof, sizeof(lg::PTile) * std::max<size_t>(1, rt128.size()));
+  PS_ALLOC(p->d_ct128_prof, sizeof(lg::PTile) * std::max<size_t>(1, ct128.size()));
   PS_ALLOC(p->d_rtile0_prof, sizeof(int32_t) * rt0.size());
   PS_ALLOC(p->d_ranks, sizeof(int32_t) * K);
   PS_ALLOC(p->d_ismat, sizeof(int32_t) * L);
   PS_ALLOC(p->d_pl_c, sizeof(lg::PLayer) * std::max(1, p->nM));
   PS_ALLOC(p->d_rt_c, sizeof(lg::PTile) * std::max<size_t>(1, max_rt));
   PS_ALLOC(p->d_ct_c, sizeof(lg::PTile) * std::max<size_t>(1, max_ct));
+  PS_ALLOC(p->d_rt128_c, sizeof(lg::PTile) * std::max<size_t>(1, max_rt));
+  PS_ALLOC(p->d_ct128_c, sizeof(lg::PTile) * std::max<size_t>(1, max_ct));
   PS_ALLOC(p->d_initflag, sizeof(int32_t) * std::max(1, p->nM));
   PS_ALLOC(p->d_raw, sizeof(lg::RawSeg) * (max_raw + 1));
   PS_ALLOC(p->P, sizeof(float) * p->Psz);
@@ -161,6 +169,10 @@ int psgd_init(lgreco_ctx* c, cudaStream_t st) {
   if (!pl.empty()) LG_CUDA(cudaMemcpyAsync(p->d_pl_prof, pl.data(), sizeof(lg::PLayer) * pl.size(), cudaMemcpyHostToDevice, st));
   if (!rt.empty()) LG_CUDA(cudaMemcpyAsync(p->d_rt_prof, rt.data(), sizeof(lg::PTile) * rt.size(), cudaMemcpyHostToDevice, st));
   if (!ct.empty()) LG_CUDA(cudaMemcpyAsync(p->d_ct_prof, ct.data(), sizeof(lg::PTile) * ct.size(), cudaMemcpyHostToDevice, st));
+  if (!rt128.empty())
+    LG_CUDA(cudaMemcpyAsync(p->d_rt128_prof, rt128.data(), sizeof(lg::PTile) * rt128.size(), cudaMemcpyHostToDevice, st));
+  if (!ct128.empty())
+    LG_CUDA(cudaMemcpyAsync(p->d_ct128_prof, ct128.data(), sizeof(lg::PTile) * ct128.size(), cudaMemcpyHostToDevice, st));
   LG_CUDA(cudaMemcpyAsync(p->d_rtile0_prof, rt0.data(), sizeof(int32_t) * rt0.size(), cudaMemcpyHostToDevice, st));
   LG_CUDA(cudaMemcpyAsync(p->d_ranks, c->params.data(), sizeof(int32_t) * K, cudaMemcpyHostToDevice, st));
   LG_CUDA(cudaMemcpyAsync(p->d_ismat, ismat.data(), sizeof(int32_t) * L, cudaMemcpyHostToDevice, st));
@@ -172,6 +184,7 @@ void psgd_destroy(lgreco_ctx* c) {
   Psgd* p = c->ps;
   if (!p) return;
   cudaFree(p->d_pl_prof); cudaFree(p->d_rt_prof); cudaFree(p->d_ct_prof); cudaFree(p->d_rtile0_prof);
+  cudaFree(p->d_rt128_prof); cudaFree(p->d_ct128_prof); cudaFree(p->d_rt128_c); cudaFree(p->d_ct128_c);
   cudaFree(p->d_ranks); cudaFree(p->d_ismat); cudaFree(p->d_pl_c); cudaFree(p->d_rt_c); cudaFree(p->d_ct_c);
   cudaFree(p->d_initflag); cudaFree(p->d_raw); cudaFree(p->P); cudaFree(p->Ph); cudaFree(p->Qprof);
   cudaFree(p->Qws); cudaFree(p->Qn); cudaFree(p->part); cudaFree(p->G); cudaFree(p->nrm_part); cudaFree(p->nrm);
@@ -184,11 +197,13 @@ void psgd_destroy(lgreco_ctx* c) {
 
 static lg::PsArgs ps_args_prof(lgreco_ctx* c, const float* g, const float* e) {
   Psgd* p = c->ps;
-  return lg::PsArgs{g, e, p->d_pl_prof, p->n_prof, p->d_rt_prof, p->nrt_prof, p->d_ct_prof, p->nct_prof, p->rmax_prof};
+  return lg::PsArgs{g, e, p->d_pl_prof, p->n_prof, p->d_rt_prof, p->nrt_prof, p->d_ct_prof, p->nct_prof, p->rmax_prof,
+                    p->d_rt128_prof, p->nrt128_prof, p->d_ct128_prof, p->nct128_prof};
 }
 static lg::PsArgs ps_args_c(lgreco_ctx* c, const float* g, const float* e) {
   Psgd* p = c->ps;
-  return lg::PsArgs{g, e, p->d_pl_c, p->n_c, p->d_rt_c, p->nrt_c, p->d_ct_c, p->nct_c, p->rmax_c};
+  return lg::PsArgs{g, e, p->d_pl_c, p->n_c, p->d_rt_c, p->nrt_c, p->d_ct_c, p->nct_c, p->rmax_c,
+                    p->d_rt128_c, p->nrt128_c, p->d_ct128_c, p->nct128_c};
 }
 
 int psgd_profile(lgreco_ctx* c, const float* g, const float* e, uint64_t step, double* err, int64_t* bits,
@@ -241,10 +256,10 @@ static int psgd_set_plan(lgreco_ctx* c, const int32_t* choice, cudaStream_t st) 
       return LGRECO_EINVAL;
     }
   std::vector<lg::PLayer> pl;
-  std::vector<lg::PTile> rt, ct;
+  std::vector<lg::PTile> rt, ct, rt128, ct128;
   std::vector<int32_t> rt0;
   int rmax = 0;
-  ps_config(c, r, pl, rt, ct, rt0, rmax);
+  ps_config(c, r, pl, rt, ct, rt0, rmax, rt128, ct128);
   // init flags follow the compress config order (layers with r > 0)
   int ci = 0;
   bool any_init = false;
@@ -272,15 +287,22 @@ static int psgd_set_plan(lgreco_ctx* c, const int32_t* choice, cudaStream_t st) 
   const size_t o_pl = put(pl.data(), sizeof(lg::PLayer) * pl.size());
   const size_t o_rt = put(rt.data(), sizeof(lg::PTile) * rt.size());
   const size_t o_ct = put(ct.data(), sizeof(lg::PTile) * ct.size());
+  const size_t o_rt2 = put(rt128.data(), sizeof(lg::PTile) * rt128.size());
+  const size_t o_ct2 = put(ct128.data(), sizeof(lg::PTile) * ct128.size());
   const size_t o_if = put(initf.data(), sizeof(int32_t) * initf.size());
   const size_t o_sg = put(segs.data(), sizeof(lg::RawSeg) * segs.size());
   if (!pl.empty()) LG_CUDA(cudaMemcpyAsync(p->d_pl_c, h + o_pl, sizeof(lg::PLayer) * pl.size(), cudaMemcpyHostToDevice, st));
   if (!rt.empty()) LG_CUDA(cudaMemcpyAsync(p->d_rt_c, h + o_rt, sizeof(lg::PTile) * rt.size(), cudaMemcpyHostToDevice, st));
   if (!ct.empty()) LG_CUDA(cudaMemcpyAsync(p->d_ct_c, h + o_ct, sizeof(lg::PTile) * ct.size(), cudaMemcpyHostToDevice, st));
+  if (!rt128.empty())
+    LG_CUDA(cudaMemcpyAsync(p->d_rt128_c, h + o_rt2, sizeof(lg::PTile) * rt128.size(), cudaMemcpyHostToDevice, st));
+  if (!ct128.empty())
+    LG_CUDA(cudaMemcpyAsync(p->d_ct128_c, h + o_ct2, sizeof(lg::PTile) * ct128.size(), cudaMemcpyHostToDevice, st));
   LG_CUDA(cudaMemcpyAsync(p->d_initflag, h + o_if, sizeof(int32_t) * initf.size(), cudaMemcpyHostToDevice, st));
   if (!segs.empty()) LG_CUDA(cudaMemcpyAsync(p->d_raw, h + o_sg, sizeof(lg::RawSeg) * segs.size(), cudaMemcpyHostToDevice, st));
   LG_CUDA(cudaEventRecord(p->evt, st));
   p->n_c = (int)pl.size(); p->nrt_c = (int)rt.size(); p->nct_c = (int)ct.size(); p->rmax_c = rmax;
+  p->nrt128_c = (int)rt128.size(); p->nct128_c = (int)ct128.size();
   p->nraw = (int)segs.size();
   p->Sraw = off;
   p->need_init = any_init;
@@ -408,7 +430,7 @@ extern "C" int lgreco_debug_tc_mq(const float* d_g, const float* d_e, int64_t m,
   LG_CUDA(cudaMalloc(&d_t, sizeof(lg::PTile) * tiles.size()));
   LG_CUDA(cudaMemcpyAsync(d_pl, &pl, sizeof(pl), cudaMemcpyHostToDevice, st));
   LG_CUDA(cudaMemcpyAsync(d_t, tiles.data(), sizeof(lg::PTile) * tiles.size(), cudaMemcpyHostToDevice, st));
-  lg::PsArgs a{d_g, d_e, d_pl, 1, nullptr, 0, nullptr, 0, r};
+  lg::PsArgs a{d_g, d_e, d_pl, 1, nullptr, 0, nullptr, 0, r, nullptr, 0, nullptr, 0};
   cudaError_t e = lg::launch_ps_mq_tc(a, d_t, (int)tiles.size(), d_Q, d_P, st);
   cudaError_t e2 = cudaStreamSynchronize(st);
   cudaFree(d_pl);

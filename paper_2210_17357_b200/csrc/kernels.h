@@ -91,6 +91,7 @@ struct RawSeg { int64_t off, n, pay_off; };            // raw (uncompressed) seg
 struct PsArgs {
   const float* g; const float* e; const PLayer* pl; int nC;
   const PTile* rtiles; int n_rtiles; const PTile* ctiles; int n_ctiles; int rmax;
+  const PTile* rt128; int n_rt128; const PTile* ct128; int n_ct128;  // tensor-core tiles (128 rows / cols)
 };
 cudaError_t launch_ps_initq(const PsArgs& a, float* Q, uint32_t k0, uint32_t k1, uint32_t step, const int32_t* only,
                             cudaStream_t st);
@@ -99,6 +100,8 @@ cudaError_t launch_ps_orth(const PsArgs& a, const float* P, float scale, double*
 cudaError_t launch_ps_mtp(const PsArgs& a, const float* Ph, float* part, float* Q, float scale, cudaStream_t st);
 cudaError_t launch_ps_mq_tc(const PsArgs& a, const PTile* tiles128, int ntiles, const float* Q, float* P,
                             cudaStream_t st);
+cudaError_t launch_ps_mtp_tc(const PsArgs& a, const PTile* ctiles128, int ntiles, const float* Ph, float* part,
+                             cudaStream_t st);
 cudaError_t launch_ps_mtp_scale(const PsArgs& a, const float* src, float* dst, float scale, cudaStream_t st);
 cudaError_t launch_ps_err(const PsArgs& a, const double* nrm_part, const int32_t* rtile0, const float* Ph,
                           const float* Q, const int32_t* ranks, int K, double* err, int64_t* bits, double* nrm,

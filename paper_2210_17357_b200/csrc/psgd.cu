@@ -451,7 +451,7 @@ static void mq_launch(const PsArgs& a, const float* Q, float* P, double* nrm_par
   k_ps_mq<RMAX><<<a.n_rtiles, PS_THREADS, 0, st>>>(a.g, a.e, a.pl, a.rtiles, Q, P, nrm_part);
 }
 template <int RMAX>
-static void mtp_launch(const PsArgs& a, const float* Ph, float* part, cudaStream_t st) {
+[[maybe_unused]] static void mtp_launch(const PsArgs& a, const float* Ph, float* part, cudaStream_t st) {
   k_ps_mtp<RMAX><<<a.n_ctiles, PS_THREADS, 0, st>>>(a.g, a.e, a.pl, a.ctiles, Ph, part);
 }
 
@@ -464,10 +464,13 @@ cudaError_t launch_ps_initq(const PsArgs& a, float* Q, uint32_t k0, uint32_t k1,
 
 cudaError_t launch_ps_mq(const PsArgs& a, const float* Q, float* P, double* nrm_part, cudaStream_t st) {
   if (a.n_rtiles == 0) return cudaSuccess;
-  if (a.rmax <= 16) mq_launch<16>(a, Q, P, nrm_part, st);
-  else if (a.rmax <= 32) mq_launch<32>(a, Q, P, nrm_part, st);
-  else mq_launch<64>(a, Q, P, nrm_part, st);
-  return cudaGetLastError();
+  if (nrm_part) {  // ||M||^2 partials (first profile step) come with the SIMT kernel
+    if (a.rmax <= 16) mq_launch<16>(a, Q, P, nrm_part, st);
+    else if (a.rmax <= 32) mq_launch<32>(a, Q, P, nrm_part, st);
+    else mq_launch<64>(a, Q, P, nrm_part, st);
+    return cudaGetLastError();
+  }
+  return launch_ps_mq_tc(a, a.rt128, a.n_rt128, Q, P, st);
 }
 
 cudaError_t launch_ps_orth(const PsArgs& a, const float* P, float scale, double* G, float* Ph, cudaStream_t st) {
@@ -483,9 +486,8 @@ cudaError_t launch_ps_orth(const PsArgs& a, const float* P, float scale, double*
 
 cudaError_t launch_ps_mtp(const PsArgs& a, const float* Ph, float* part, float* Q, float scale, cudaStream_t st) {
   if (a.n_ctiles == 0) return cudaSuccess;
-  if (a.rmax <= 16) mtp_launch<16>(a, Ph, part, st);
-  else if (a.rmax <= 32) mtp_launch<32>(a, Ph, part, st);
-  else mtp_launch<64>(a, Ph, part, st);
+  cudaError_t e = launch_ps_mtp_tc(a, a.ct128, a.n_ct128, Ph, part, st);
+  if (e != cudaSuccess) return e;
   k_ps_reduce<<<dim3(32, a.nC), 256, 0, st>>>(a.pl, a.nC, part, Q, scale);
   return cudaGetLastError();
 }

@@ -42,9 +42,22 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   return d;
 }
 
-// instruction descriptor: kind::tf32, D f32, A/B tf32 K-major, M = 128, N
-__host__ __device__ constexpr uint32_t tf32_idesc(int N) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(TC_M >> 4) << 24);
+// SW128 MN-major smem descriptor: 32-element (128 B) MN rows, MN groups LBO apart,
+// 8-row K groups SBO apart
+__device__ __forceinline__ uint64_t sw128_mn_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+// instruction descriptor: kind::tf32, D f32, A/B tf32, B K-major, A K- or MN-major, M = 128, N
+__host__ __device__ constexpr uint32_t tf32_idesc(int N, bool a_mn = false) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((a_mn ? 1u : 0u) << 15) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(TC_M >> 4) << 24);
 }
 
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
@@ -82,11 +95,16 @@ __device__ __forceinline__ void put_chunk(uint8_t* hi_tile, uint8_t* lo_tile, in
                  __float_as_uint(__fsub_rn(v.z, __uint_as_float(h2))), __float_as_uint(__fsub_rn(v.w, __uint_as_float(h3))));
 }
 
-// NP: N padded to a multiple of 16 (16, 32, 64); grouped over layers via row tiles of 128
-template <int NP>
+// NP: N padded to a multiple of 16 (16, 32, 64); grouped over layers.
+// TRANS = false: P = M Q   -- tile = 128 rows of M, K runs over the k columns,
+//                             A = M rows (K-major), B = Q columns, out P[j*m + i]
+// TRANS = true:  Q = M^T P -- tile = 128 columns of M, K runs over rows [i0, i1),
+//                             A = M^T staged from M rows as an MN-major operand,
+//                             B = P columns, out partial[split][j*k + c]
+template <int NP, bool TRANS>
 __global__ void __launch_bounds__(TC_THREADS, 1)
-k_ps_mq_tc(const float* __restrict__ g, const float* __restrict__ e, const PLayer* __restrict__ pl,
-           const PTile* __restrict__ tiles, const float* __restrict__ Q, float* __restrict__ P) {
+k_ps_tc(const float* __restrict__ g, const float* __restrict__ e, const PLayer* __restrict__ pl,
+        const PTile* __restrict__ tiles, const float* __restrict__ Bsrc, float* __restrict__ out) {
   constexpr int A_BYTES = TC_M * 128;        // 16 KB per A tile (hi or lo)
   constexpr int B_BYTES = NP * 128;          // per B tile (hi or lo)
   constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;
@@ -99,8 +117,11 @@ k_ps_mq_tc(const float* __restrict__ g, const float* __restrict__ e, const PLaye
   const PTile tl = tiles[blockIdx.x];
   const PLayer p = pl[tl.ci];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int rows = min(TC_M, p.m - tl.i0);
-  const int nk = (p.k + TC_KT - 1) / TC_KT;
+  // tile extent along the MMA M dimension, and the K range
+  const int rows = TRANS ? min(TC_M, p.k - tl.c0) : min(TC_M, p.m - tl.i0);
+  const int kbeg = TRANS ? tl.i0 : 0;
+  const int kend = TRANS ? tl.i1 : p.k;
+  const int nk = (kend - kbeg + TC_KT - 1) / TC_KT;
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
@@ -116,7 +137,7 @@ k_ps_mq_tc(const float* __restrict__ g, const float* __restrict__ e, const PLaye
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem_d = tmem_base_sh;
-  constexpr uint32_t idesc = tf32_idesc(NP);
+  constexpr uint32_t idesc = tf32_idesc(NP, TRANS);
 
   const int row = warp * 32 + lane;
   float acc[NP];
@@ -148,40 +169,78 @@ k_ps_mq_tc(const float* __restrict__ g, const float* __restrict__ e, const PLaye
     uint8_t* Al = Ah + A_BYTES;
     uint8_t* Bh = Al + A_BYTES;
     uint8_t* Bl = Bh + B_BYTES;
-    const int c0 = kt * TC_KT;
-    // A: 128 rows x 8 chunks; a warp covers 4 rows x 128 B per instruction (coalesced)
+    const int k0 = kbeg + kt * TC_KT;
+    if (!TRANS) {
+      // A: 128 rows x 8 chunks; a warp covers 4 rows x 128 B per instruction (coalesced)
 #pragma unroll 4
-    for (int it = 0; it < TC_M * 8 / TC_THREADS; ++it) {
-      const int idx = it * TC_THREADS + tid;
-      const int r_ = idx >> 3, ch = idx & 7;
-      const int col = c0 + ch * 4;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (r_ < rows) {
-        const int64_t base = p.moff + (int64_t)(tl.i0 + r_) * p.k + col;
-        if (col + 4 <= p.k && ((base & 3) == 0)) {
-          const float4 a = __ldg(reinterpret_cast<const float4*>(g + base));
-          const float4 b = e ? __ldg(reinterpret_cast<const float4*>(e + base)) : make_float4(0.f, 0.f, 0.f, 0.f);
-          v = make_float4(canon(a.x, b.x), canon(a.y, b.y), canon(a.z, b.z), canon(a.w, b.w));
-        } else {
-          float t[4];
+      for (int it = 0; it < TC_M * 8 / TC_THREADS; ++it) {
+        const int idx = it * TC_THREADS + tid;
+        const int r_ = idx >> 3, ch = idx & 7;
+        const int col = k0 + ch * 4;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (r_ < rows) {
+          const int64_t base = p.moff + (int64_t)(tl.i0 + r_) * p.k + col;
+          if (col + 4 <= kend && ((base & 3) == 0)) {
+            const float4 a = __ldg(reinterpret_cast<const float4*>(g + base));
+            const float4 b = e ? __ldg(reinterpret_cast<const float4*>(e + base)) : make_float4(0.f, 0.f, 0.f, 0.f);
+            v = make_float4(canon(a.x, b.x), canon(a.y, b.y), canon(a.z, b.z), canon(a.w, b.w));
+          } else {
+            float t[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            t[q] = (col + q < p.k) ? canon(__ldg(g + base + q), e ? __ldg(e + base + q) : 0.f) : 0.f;
-          v = make_float4(t[0], t[1], t[2], t[3]);
+            for (int q = 0; q < 4; ++q)
+              t[q] = (col + q < kend) ? canon(__ldg(g + base + q), e ? __ldg(e + base + q) : 0.f) : 0.f;
+            v = make_float4(t[0], t[1], t[2], t[3]);
+          }
         }
+        put_chunk(Ah, Al, r_, ch, v);
       }
-      put_chunk(Ah, Al, r_, ch, v);
-    }
-    // B: NP rows (Q columns j) x 8 chunks
-    for (int idx = tid; idx < NP * 8; idx += TC_THREADS) {
-      const int j = idx >> 3, ch = idx & 7;
-      const int col = c0 + ch * 4;
-      float t[4] = {0.f, 0.f, 0.f, 0.f};
-      if (j < p.r) {
+    } else {
+      // A^T: 32 K-rows (rows i of M) x 128 M-elements (columns c), MN-major:
+      // offset = (c/32)*4096 + (kr/8)*1024 + (kr%8)*128 + (((c%32)/4) ^ (kr%8))*16
+#pragma unroll 4
+      for (int it = 0; it < TC_KT * 32 / TC_THREADS; ++it) {
+        const int idx = it * TC_THREADS + tid;
+        const int kr = idx >> 5, cq = idx & 31;  // K row, 16-byte chunk along c (4 columns)
+        const int i = k0 + kr, c = tl.c0 + cq * 4;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (i < kend) {
+          const int64_t base = p.moff + (int64_t)i * p.k + c;
+          if (c + 4 <= tl.c0 + rows && ((base & 3) == 0)) {
+            const float4 a = __ldg(reinterpret_cast<const float4*>(g + base));
+            const float4 b = e ? __ldg(reinterpret_cast<const float4*>(e + base)) : make_float4(0.f, 0.f, 0.f, 0.f);
+            v = make_float4(canon(a.x, b.x), canon(a.y, b.y), canon(a.z, b.z), canon(a.w, b.w));
+          } else {
+            float t[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) t[q] = (col + q < p.k) ? Q[p.qoff + (int64_t)j * p.k + col + q] : 0.f;
+            for (int q = 0; q < 4; ++q)
+              t[q] = (c + q < tl.c0 + rows) ? canon(__ldg(g + base + q), e ? __ldg(e + base + q) : 0.f) : 0.f;
+            v = make_float4(t[0], t[1], t[2], t[3]);
+          }
+        }
+        const int mg = cq >> 3, ch = cq & 7;
+        const uint32_t off = (uint32_t)mg * 4096u + (uint32_t)(kr >> 3) * 1024u + (uint32_t)(kr & 7) * 128u +
+                             (uint32_t)((ch ^ (kr & 7)) << 4);
+        const uint32_t h0 = tf32_hi(v.x), h1 = tf32_hi(v.y), h2 = tf32_hi(v.z), h3 = tf32_hi(v.w);
+        *reinterpret_cast<uint4*>(Ah + off) = make_uint4(h0, h1, h2, h3);
+        *reinterpret_cast<uint4*>(Al + off) = make_uint4(
+            __float_as_uint(__fsub_rn(v.x, __uint_as_float(h0))), __float_as_uint(__fsub_rn(v.y, __uint_as_float(h1))),
+            __float_as_uint(__fsub_rn(v.z, __uint_as_float(h2))), __float_as_uint(__fsub_rn(v.w, __uint_as_float(h3))));
       }
-      put_chunk(Bh, Bl, j, ch, make_float4(t[0], t[1], t[2], t[3]));
+    }
+    // B: NP rows (columns j of Q, resp. of P) x 8 chunks along K
+    {
+      const int64_t bld = TRANS ? (int64_t)p.m : (int64_t)p.k;   // column length of Bsrc
+      const int64_t boff = TRANS ? p.poff : p.qoff;
+      for (int idx = tid; idx < NP * 8; idx += TC_THREADS) {
+        const int j = idx >> 3, ch = idx & 7;
+        const int col = k0 + ch * 4;
+        float t[4] = {0.f, 0.f, 0.f, 0.f};
+        if (j < p.r) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) t[q] = (col + q < kend) ? Bsrc[boff + (int64_t)j * bld + col + q] : 0.f;
+        }
+        put_chunk(Bh, Bl, j, ch, make_float4(t[0], t[1], t[2], t[3]));
+      }
     }
     asm volatile("fence.proxy.async.shared::cta;");
     __syncthreads();
@@ -192,9 +251,11 @@ k_ps_mq_tc(const float* __restrict__ g, const float* __restrict__ e, const PLaye
 #pragma unroll
       for (int kk = 0; kk < TC_KT / 8; ++kk) {
         const uint32_t koff = kk * 32;  // 8 tf32 = 32 bytes along K inside the swizzle row
-        mma_tf32(dbuf, sw128_desc(sAh + koff), sw128_desc(sBh + koff), idesc, kk > 0 ? 1u : 0u);
-        mma_tf32(dbuf, sw128_desc(sAh + koff), sw128_desc(sBl + koff), idesc, 1u);
-        mma_tf32(dbuf, sw128_desc(sAl + koff), sw128_desc(sBh + koff), idesc, 1u);
+        const uint64_t dAh = TRANS ? sw128_mn_desc(sAh + kk * 1024, 4096, 1024) : sw128_desc(sAh + koff);
+        const uint64_t dAl = TRANS ? sw128_mn_desc(sAl + kk * 1024, 4096, 1024) : sw128_desc(sAl + koff);
+        mma_tf32(dbuf, dAh, sw128_desc(sBh + koff), idesc, kk > 0 ? 1u : 0u);
+        mma_tf32(dbuf, dAh, sw128_desc(sBl + koff), idesc, 1u);
+        mma_tf32(dbuf, dAl, sw128_desc(sBh + koff), idesc, 1u);
       }
       mma_commit(&mma_done[s]);
     }
@@ -205,9 +266,16 @@ k_ps_mq_tc(const float* __restrict__ g, const float* __restrict__ e, const PLaye
   }
   drain(nk - 1);
   if (row < rows) {
+    if (!TRANS) {
 #pragma unroll
-    for (int j = 0; j < NP; ++j)
-      if (j < p.r) P[p.poff + (int64_t)j * p.m + tl.i0 + row] = acc[j];
+      for (int j = 0; j < NP; ++j)
+        if (j < p.r) out[p.poff + (int64_t)j * p.m + tl.i0 + row] = acc[j];
+    } else {
+      float* o = out + (int64_t)tl.split * p.qstride + p.qoff;
+#pragma unroll
+      for (int j = 0; j < NP; ++j)
+        if (j < p.r) o[(int64_t)j * p.k + tl.c0 + row] = acc[j];
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
@@ -215,23 +283,31 @@ k_ps_mq_tc(const float* __restrict__ g, const float* __restrict__ e, const PLaye
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "r"(TMEM_COLS));
 }
 
-template <int NP>
-static cudaError_t mq_tc_launch(const PsArgs& a, const PTile* tiles128, int ntiles, const float* Q, float* P,
-                                cudaStream_t st) {
+template <int NP, bool TRANS>
+static cudaError_t tc_launch(const PsArgs& a, const PTile* tiles, int ntiles, const float* B, float* out,
+                             cudaStream_t st) {
   constexpr int STAGE = 2 * TC_M * 128 + 2 * NP * 128;
   const int smem = 2 * STAGE + 1024;
-  cudaError_t e = cudaFuncSetAttribute(k_ps_mq_tc<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = cudaFuncSetAttribute(k_ps_tc<NP, TRANS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  k_ps_mq_tc<NP><<<ntiles, TC_THREADS, smem, st>>>(a.g, a.e, a.pl, tiles128, Q, P);
+  k_ps_tc<NP, TRANS><<<ntiles, TC_THREADS, smem, st>>>(a.g, a.e, a.pl, tiles, B, out);
   return cudaGetLastError();
 }
 
 cudaError_t launch_ps_mq_tc(const PsArgs& a, const PTile* tiles128, int ntiles, const float* Q, float* P,
                             cudaStream_t st) {
   if (ntiles == 0) return cudaSuccess;
-  if (a.rmax <= 16) return mq_tc_launch<16>(a, tiles128, ntiles, Q, P, st);
-  if (a.rmax <= 32) return mq_tc_launch<32>(a, tiles128, ntiles, Q, P, st);
-  return mq_tc_launch<64>(a, tiles128, ntiles, Q, P, st);
+  if (a.rmax <= 16) return tc_launch<16, false>(a, tiles128, ntiles, Q, P, st);
+  if (a.rmax <= 32) return tc_launch<32, false>(a, tiles128, ntiles, Q, P, st);
+  return tc_launch<64, false>(a, tiles128, ntiles, Q, P, st);
+}
+
+cudaError_t launch_ps_mtp_tc(const PsArgs& a, const PTile* ctiles128, int ntiles, const float* Ph, float* part,
+                             cudaStream_t st) {
+  if (ntiles == 0) return cudaSuccess;
+  if (a.rmax <= 16) return tc_launch<16, true>(a, ctiles128, ntiles, Ph, part, st);
+  if (a.rmax <= 32) return tc_launch<32, true>(a, ctiles128, ntiles, Ph, part, st);
+  return tc_launch<64, true>(a, ctiles128, ntiles, Ph, part, st);
 }
 
 }  // namespace lg
