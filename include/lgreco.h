@@ -221,6 +221,11 @@ int lgreco_psgd_raw_combine(lgreco_ctx* ctx, const int32_t* h_choice, int32_t W,
 int lgreco_debug_tc_mq(const float* d_g, const float* d_e, int64_t m, int32_t k, const float* d_Q, int32_t r,
                        float* d_P, void* stream);
 
+/* Debug: Q = M^T P through the tcgen05 path (A operand MN-major): d_P m x r and d_Q
+ * k x r column-major.  Synchronises `stream`. */
+int lgreco_debug_tc_mtp(const float* d_g, const float* d_e, int64_t m, int32_t k, const float* d_P, int32_t r,
+                        float* d_Q, void* stream);
+
 /* Debug: Philox4x32-10 of n counters (d_ctr: n*4 u32, key) -> d_out n*4 u32. */
 int lgreco_debug_philox(const uint32_t* d_ctr, uint32_t key0, uint32_t key1, int64_t n,
                         uint32_t* d_out, void* stream);

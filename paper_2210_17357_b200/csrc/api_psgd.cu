@@ -441,3 +441,30 @@ extern "C" int lgreco_debug_tc_mq(const float* d_g, const float* d_e, int64_t m,
   }
   return LGRECO_OK;
 }
+
+// Debug / unit-test entry: Q = M^T P on the tcgen05 path for one matrix (one row split):
+// M = canon(g + e) m x k row-major, P m x r column-major, Q k x r column-major.
+extern "C" int lgreco_debug_tc_mtp(const float* d_g, const float* d_e, int64_t m, int32_t k, const float* d_P, int32_t r,
+                                   float* d_Q, void* stream) {
+  if (!d_g || !d_P || !d_Q || m <= 0 || k <= 0 || r < 1 || r > 64 || m > 0x7fffffff) return LGRECO_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  lg::PLayer pl{0, (int32_t)m, k, r, 0, 0, 0, 0, (int64_t)k * r, 1, 0};
+  std::vector<lg::PTile> tiles;
+  for (int c0 = 0; c0 < k; c0 += 128) tiles.push_back(lg::PTile{0, 0, 0, (int32_t)m, c0, 0});
+  lg::PLayer* d_pl = nullptr;
+  lg::PTile* d_t = nullptr;
+  LG_CUDA(cudaMalloc(&d_pl, sizeof(pl)));
+  LG_CUDA(cudaMalloc(&d_t, sizeof(lg::PTile) * tiles.size()));
+  LG_CUDA(cudaMemcpyAsync(d_pl, &pl, sizeof(pl), cudaMemcpyHostToDevice, st));
+  LG_CUDA(cudaMemcpyAsync(d_t, tiles.data(), sizeof(lg::PTile) * tiles.size(), cudaMemcpyHostToDevice, st));
+  lg::PsArgs a{d_g, d_e, d_pl, 1, nullptr, 0, nullptr, 0, r, nullptr, 0, nullptr, 0};
+  cudaError_t e = lg::launch_ps_mtp_tc(a, d_t, (int)tiles.size(), d_P, d_Q, st);
+  cudaError_t e2 = cudaStreamSynchronize(st);
+  cudaFree(d_pl);
+  cudaFree(d_t);
+  if (e != cudaSuccess || e2 != cudaSuccess) {
+    lg_set_error("tc_mtp: %s / %s", cudaGetErrorString(e), cudaGetErrorString(e2));
+    return LGRECO_ECUDA;
+  }
+  return LGRECO_OK;
+}

@@ -73,6 +73,7 @@ _SIGS = {
     "lgreco_psgd_raw_pack": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _VP]),
     "lgreco_psgd_raw_combine": (C.c_int, [_VP, _VP, _I32, _VP, _VP, _VP]),
     "lgreco_debug_tc_mq": (C.c_int, [_VP, _VP, _I64, _I32, _VP, _I32, _VP, _VP]),
+    "lgreco_debug_tc_mtp": (C.c_int, [_VP, _VP, _I64, _I32, _VP, _I32, _VP, _VP]),
     "lgreco_debug_philox": (C.c_int, [_VP, _U32, _U32, _I64, _VP, _VP]),
 }
 EXPORTED = tuple(_SIGS)
@@ -283,3 +284,7 @@ def debug_philox(ctr, key0, key1, stream=None):
 
 def debug_tc_mq(g, e, m, k, Q, r, P, stream=None):
     _check(lib().lgreco_debug_tc_mq(_ptr(g), _ptr(e), m, k, _ptr(Q), r, _ptr(P), _stream(stream)), "debug_tc_mq")
+
+
+def debug_tc_mtp(g, e, m, k, P, r, Q, stream=None):
+    _check(lib().lgreco_debug_tc_mtp(_ptr(g), _ptr(e), m, k, _ptr(P), r, _ptr(Q), _stream(stream)), "debug_tc_mtp")

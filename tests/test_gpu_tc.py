@@ -23,3 +23,20 @@ def test_tc_mq(m, k, r):
     got = P.cpu().numpy().reshape(r, m).T
     rel = np.linalg.norm(got - ref) / np.linalg.norm(ref)
     assert rel < 2e-6, rel
+
+
+@pytest.mark.parametrize("m,k,r", [(32, 128, 16), (300, 1000, 16), (1000, 257, 32), (512, 4608, 64), (2048, 77, 4)])
+def test_tc_mtp(m, k, r):
+    from paper_2210_17357_b200 import lgreco
+    rng = np.random.default_rng(m * 3 + k + r)
+    g = rng.standard_normal((m, k)).astype(np.float32)
+    e = (rng.standard_normal((m, k)) * 0.1).astype(np.float32)
+    P = rng.uniform(-1, 1, (r, m)).astype(np.float32)  # column-major m x r
+    Q = torch.zeros(r * k, dtype=torch.float32, device="cuda")
+    lgreco.debug_tc_mtp(torch.from_numpy(g.ravel()).cuda(), torch.from_numpy(e.ravel()).cuda(), m, k,
+                        torch.from_numpy(P.ravel()).cuda(), r, Q)
+    x = ((g + e) + np.float32(0)).astype(np.float64)
+    ref = x.T @ P.astype(np.float64).T  # k x r
+    got = Q.cpu().numpy().reshape(r, k).T
+    rel = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+    assert rel < 2e-6, rel
