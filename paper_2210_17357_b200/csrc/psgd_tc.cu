@@ -42,18 +42,6 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   return d;
 }
 
-// SW128 MN-major smem descriptor: 32-element (128 B) MN rows, MN groups LBO apart,
-// 8-row K groups SBO apart
-__device__ __forceinline__ uint64_t sw128_mn_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
-  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
-  d |= (uint64_t)1 << 46;
-  d |= (uint64_t)2 << 61;
-  return d;
-}
-
 // instruction descriptor: kind::tf32, D f32, A/B tf32, B K-major, A K- or MN-major, M = 128, N
 __host__ __device__ constexpr uint32_t tf32_idesc(int N, bool a_mn = false) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((a_mn ? 1u : 0u) << 15) | ((uint32_t)(N >> 3) << 17) |
@@ -99,7 +87,7 @@ __device__ __forceinline__ void put_chunk(uint8_t* hi_tile, uint8_t* lo_tile, in
 // TRANS = false: P = M Q   -- tile = 128 rows of M, K runs over the k columns,
 //                             A = M rows (K-major), B = Q columns, out P[j*m + i]
 // TRANS = true:  Q = M^T P -- tile = 128 columns of M, K runs over rows [i0, i1),
-//                             A = M^T staged from M rows as an MN-major operand,
+//                             A = M^T, transposed while staged from M rows (K-major),
 //                             B = P columns, out partial[split][j*k + c]
 template <int NP, bool TRANS>
 __global__ void __launch_bounds__(TC_THREADS, 1)
@@ -137,7 +125,7 @@ k_ps_tc(const float* __restrict__ g, const float* __restrict__ e, const PLayer* 
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem_d = tmem_base_sh;
-  constexpr uint32_t idesc = tf32_idesc(NP, TRANS);
+  constexpr uint32_t idesc = tf32_idesc(NP);
 
   const int row = warp * 32 + lane;
   float acc[NP];
@@ -217,14 +205,17 @@ k_ps_tc(const float* __restrict__ g, const float* __restrict__ e, const PLayer* 
             v = make_float4(t[0], t[1], t[2], t[3]);
           }
         }
-        const int mg = cq >> 3, ch = cq & 7;
-        const uint32_t off = (uint32_t)mg * 4096u + (uint32_t)(kr >> 3) * 1024u + (uint32_t)(kr & 7) * 128u +
-                             (uint32_t)((ch ^ (kr & 7)) << 4);
-        const uint32_t h0 = tf32_hi(v.x), h1 = tf32_hi(v.y), h2 = tf32_hi(v.z), h3 = tf32_hi(v.w);
-        *reinterpret_cast<uint4*>(Ah + off) = make_uint4(h0, h1, h2, h3);
-        *reinterpret_cast<uint4*>(Al + off) = make_uint4(
-            __float_as_uint(__fsub_rn(v.x, __uint_as_float(h0))), __float_as_uint(__fsub_rn(v.y, __uint_as_float(h1))),
-            __float_as_uint(__fsub_rn(v.z, __uint_as_float(h2))), __float_as_uint(__fsub_rn(v.w, __uint_as_float(h3))));
+        // transpose into the K-major A tile: A row = column c (local cq*4 + q), K = kr.
+        // (tcgen05 kind::tf32 does not take an MN-major A here: measured all-zero D.)
+        const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int arow = cq * 4 + q;
+          const uint32_t off = (uint32_t)arow * 128u + (uint32_t)((((kr >> 2) ^ (arow & 7))) << 4) + (uint32_t)(kr & 3) * 4u;
+          const uint32_t h = tf32_hi(vv[q]);
+          *reinterpret_cast<uint32_t*>(Ah + off) = h;
+          *reinterpret_cast<uint32_t*>(Al + off) = __float_as_uint(__fsub_rn(vv[q], __uint_as_float(h)));
+        }
       }
     }
     // B: NP rows (columns j of Q, resp. of P) x 8 chunks along K
@@ -251,8 +242,8 @@ k_ps_tc(const float* __restrict__ g, const float* __restrict__ e, const PLayer* 
 #pragma unroll
       for (int kk = 0; kk < TC_KT / 8; ++kk) {
         const uint32_t koff = kk * 32;  // 8 tf32 = 32 bytes along K inside the swizzle row
-        const uint64_t dAh = TRANS ? sw128_mn_desc(sAh + kk * 1024, 4096, 1024) : sw128_desc(sAh + koff);
-        const uint64_t dAl = TRANS ? sw128_mn_desc(sAl + kk * 1024, 4096, 1024) : sw128_desc(sAl + koff);
+        const uint64_t dAh = sw128_desc(sAh + koff);
+        const uint64_t dAl = sw128_desc(sAl + koff);
         mma_tf32(dbuf, dAh, sw128_desc(sBh + koff), idesc, kk > 0 ? 1u : 0u);
         mma_tf32(dbuf, dAh, sw128_desc(sBl + koff), idesc, 1u);
         mma_tf32(dbuf, dAl, sw128_desc(sBh + koff), idesc, 1u);
