@@ -158,6 +158,7 @@ int psgd_init(lgreco_ctx* c, cudaStream_t st) {
   PS_ALLOC(p->nrm_part, sizeof(double) * std::max<size_t>(1, max_rt));
   PS_ALLOC(p->nrm, sizeof(double) * std::max(1, p->nM));
   PS_ALLOC(p->dpart, sizeof(double) * std::max<size_t>(1, max_rt) * KP);
+  if (K > 128) { lg_set_error("PowerSGD: at most 128 candidate ranks"); return LGRECO_EINVAL; }
   PS_ALLOC(p->need, sizeof(int32_t) * std::max(1, p->nM));
   if (c->world > 1) {
     PS_ALLOC(p->d_raw_pay, raw_cap);
@@ -217,7 +218,7 @@ int psgd_profile(lgreco_ctx* c, const float* g, const float* e, uint64_t step, d
   LG_LAUNCH(c, lg::launch_ps_initq(a, p->Qprof, k0, k1, (uint32_t)step, nullptr, st));
   c->launches += 1;
   for (int s = 0; s < c->power_steps; ++s) {
-    LG_LAUNCH(c, lg::launch_ps_mq(a, p->Qprof, p->P, s == 0 ? p->nrm_part : nullptr, st));
+    LG_LAUNCH(c, lg::launch_ps_mq(a, p->Qprof, p->P, nullptr, st));
     LG_LAUNCH(c, lg::launch_ps_orth(a, p->P, 1.0f, p->G, p->Ph, st));
     LG_LAUNCH(c, lg::launch_ps_mtp(a, p->Ph, p->part, p->Qprof, 1.0f, st));
     c->launches += 7;

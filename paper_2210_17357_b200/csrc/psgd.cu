@@ -5,8 +5,8 @@
 //   K3 profile (a4): per matrix layer (view m x k, R11),
 //      one run at r_max of `steps` power steps from Q0 (Philox stream 2); every
 //      smaller candidate rank is the prefix of that run (pinned prefix property);
-//      err_r^2 = ||M||^2 - sum_{j<r} ||q_j||^2 (P orthonormal, Q = M^T P), with a
-//      direct fp64 ||M - P_r Q_r^T||_F fallback where err_r < 0.01 ||M||.
+//      err_r = ||M - P_r Q_r^T||_F computed directly in fp64 from the fp32 factors
+//      (first-order insensitive to factor errors; see k_ps_err_direct).
 //   K7 compress (a8-a10, R12): P = M Q_ws -> (all-reduce) -> orthogonalise ->
 //      Q = M^T P -> (all-reduce) -> out = P Q^T, e = x - out, Q_ws <- Q.
 //
@@ -308,53 +308,62 @@ __global__ void k_ps_err_identity(const PLayer* __restrict__ pl, int nC, const d
       for (int j = 0; j < r; ++j) s += qn[j];
       const double e2 = s_nrm - s;
       const double ev = e2 > 0.0 ? sqrt(e2) : 0.0;
-      err[(int64_t)p.layer * K + t] = ev;
+      err[(int64_t)p.layer * K + t] = ev;  // overwritten by the direct form below
       bits[(int64_t)p.layer * K + t] = 32 * (int64_t)r * (m + k);
-      if (!(ev >= 0.01 * sqrt(s_nrm))) need = 1;
+      need = 1;
     }
     need_direct[ci] = need;
   }
 }
 
-// direct ||M - P_r Q_r^T||_F^2 for candidate ranks [t0, t0+8) of flagged layers (fp64)
+// direct ||M - P_r Q_r^T||_F^2 for every candidate rank, fp64.  The residual of the
+// reconstruction is first-order insensitive to errors in Q (P^T (M - P Q^T) = 0), so the
+// tensor-core factors give err_r to ~1e-9 here, while the identity
+// ||M||^2 - sum ||q_j||^2 would amplify them by (||M|| / err)^2.
+// One warp walks its elements; at each candidate rank the warp-reduced d^2 goes to a
+// per-warp shared-memory slot; per-block partials are summed in fixed order later.
+constexpr int PS_KMAX = 128;
 __global__ void __launch_bounds__(PS_THREADS)
 k_ps_err_direct(const float* __restrict__ g, const float* __restrict__ e, const PLayer* __restrict__ pl,
                 const PTile* __restrict__ tiles, const float* __restrict__ Ph, const float* __restrict__ Q,
                 const int32_t* __restrict__ ranks, int K, const int32_t* __restrict__ need, double* __restrict__ part) {
+  __shared__ double acc[PS_THREADS / 32][PS_KMAX];
+  __shared__ int32_t srank[PS_KMAX];
   const PTile tl = tiles[blockIdx.x];
   const PLayer p = pl[tl.ci];
-  if (!need[tl.ci]) return;
-  __shared__ double red[PS_THREADS / 32][8];
-  const int t0 = blockIdx.y * 8;
-  double acc[8];
-#pragma unroll
-  for (int q = 0; q < 8; ++q) acc[q] = 0.0;
-  const int rows = min(PS_TM, p.m - tl.i0);
-  for (int64_t el = threadIdx.x; el < (int64_t)rows * p.k; el += PS_THREADS) {
-    const int i = tl.i0 + (int)(el / p.k), c = (int)(el % p.k);
-    const double x = (double)xval(g, e, p.moff + (int64_t)i * p.k + c);
-    double rec = 0.0;
-    int j = 0;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int t = t0 + q;
-      if (t >= K) break;
-      const int r = min(ranks[t], p.r);
-      for (; j < r; ++j) rec = fma((double)Ph[p.poff + (int64_t)j * p.m + i], (double)Q[p.qoff + (int64_t)j * p.k + c], rec);
-      const double d = x - rec;
-      acc[q] = fma(d, d, acc[q]);
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const double v = warp_sum_d(acc[q]);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][q] = v;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int t = threadIdx.x; t < PS_KMAX; t += PS_THREADS) {
+    srank[t] = (t < K) ? ranks[t] : 0x7fffffff;
+    for (int w = 0; w < PS_THREADS / 32; ++w) acc[w][t] = 0.0;
   }
   __syncthreads();
-  if (threadIdx.x < 8) {
-    double s = 0.0;
-    for (int w = 0; w < PS_THREADS / 32; ++w) s += red[w][threadIdx.x];
-    part[((int64_t)blockIdx.x) * ((K + 7) / 8 * 8) + t0 + threadIdx.x] = s;
+  if (need[tl.ci]) {
+    const int rows = min(PS_TM, p.m - tl.i0);
+    const int64_t nel = (int64_t)rows * p.k;
+    for (int64_t base = (int64_t)warp * 32; base < nel; base += PS_THREADS) {
+      const int64_t el = base + lane;
+      const bool valid = el < nel;
+      const int i = tl.i0 + (int)(valid ? el / p.k : 0), c = (int)(valid ? el % p.k : 0);
+      const double x = valid ? (double)xval(g, e, p.moff + (int64_t)i * p.k + c) : 0.0;
+      double rec = 0.0;
+      int t = 0;
+      while (t < K && srank[t] <= 0) ++t;
+      for (int j = 0; j < p.r && t < K; ++j) {
+        if (valid) rec = fma((double)Ph[p.poff + (int64_t)j * p.m + i], (double)Q[p.qoff + (int64_t)j * p.k + c], rec);
+        while (t < K && srank[t] == j + 1) {  // candidate t uses the first j+1 columns
+          const double d = valid ? x - rec : 0.0;
+          const double v = warp_sum_d(d * d);
+          if (lane == 0) acc[warp][t] += v;
+          ++t;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < K; t += PS_THREADS) {
+    double s2 = 0.0;
+    for (int w = 0; w < PS_THREADS / 32; ++w) s2 += acc[w][t];
+    part[(int64_t)blockIdx.x * K + t] = s2;
   }
 }
 
@@ -364,12 +373,11 @@ __global__ void k_ps_err_direct_final(const PLayer* __restrict__ pl, int nC, con
   const int ci = blockIdx.x;
   if (ci >= nC || !need[ci]) return;
   const PLayer p = pl[ci];
-  const int KP = (K + 7) / 8 * 8;
   for (int t = threadIdx.x; t < K; t += blockDim.x) {
     const int64_t m = p.m, k = p.k;
     if ((int64_t)ranks[t] * (m + k) >= m * k) continue;
     double s = 0.0;
-    for (int b = tile0[ci]; b < tile0[ci + 1]; ++b) s += part[(int64_t)b * KP + t];
+    for (int b = tile0[ci]; b < tile0[ci + 1]; ++b) s += part[(int64_t)b * K + t];
     err[(int64_t)p.layer * K + t] = sqrt(s);
   }
 }
@@ -464,7 +472,7 @@ cudaError_t launch_ps_initq(const PsArgs& a, float* Q, uint32_t k0, uint32_t k1,
 
 cudaError_t launch_ps_mq(const PsArgs& a, const float* Q, float* P, double* nrm_part, cudaStream_t st) {
   if (a.n_rtiles == 0) return cudaSuccess;
-  if (nrm_part) {  // ||M||^2 partials (first profile step) come with the SIMT kernel
+  if (nrm_part) {  // ||M||^2 partials requested: SIMT kernel
     if (a.rmax <= 16) mq_launch<16>(a, Q, P, nrm_part, st);
     else if (a.rmax <= 32) mq_launch<32>(a, Q, P, nrm_part, st);
     else mq_launch<64>(a, Q, P, nrm_part, st);
@@ -503,8 +511,8 @@ cudaError_t launch_ps_err(const PsArgs& a, const double* nrm_part, const int32_t
                           int32_t* need, double* dpart, cudaStream_t st) {
   if (a.nC == 0) return cudaSuccess;
   k_ps_err_identity<<<a.nC, 64, 0, st>>>(a.pl, a.nC, nrm_part, rtile0, Q, ranks, K, err, bits, nrm, need);
-  k_ps_err_direct<<<dim3(a.n_rtiles, (K + 7) / 8), PS_THREADS, 0, st>>>(a.g, a.e, a.pl, a.rtiles, Ph, Q, ranks, K,
-                                                                         need, dpart);
+  if (K > PS_KMAX) return cudaErrorInvalidValue;
+  k_ps_err_direct<<<a.n_rtiles, PS_THREADS, 0, st>>>(a.g, a.e, a.pl, a.rtiles, Ph, Q, ranks, K, need, dpart);
   k_ps_err_direct_final<<<a.nC, 128, 0, st>>>(a.pl, a.nC, rtile0, ranks, K, need, dpart, err);
   return cudaGetLastError();
 }
