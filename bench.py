@@ -175,11 +175,10 @@ def run_ours(args):
         lgreco.solve(err, bits, dflt, comp, D=D_BINS, choice=choice_d, info=info_d, workspace=ws)
         ctx.plan_broadcast(choice_d)
         if marks: marks[2].record(stream)
-        choice_h.copy_(choice_d, non_blocking=True)
-        stream.synchronize()  # the plan is host-side state of the comm engine (NCCL counts)
+        # plan consumed on the device at W = 1 (no host round trip); copied to the host
+        # inside the library when the exchange needs the shard sizes (W > 1)
+        ctx.compress_allreduce_dev(choice_d, g, ef, out, s)
         if marks: marks[3].record(stream)
-        ctx.compress_allreduce(choice_h.tolist(), g, ef, out, s)
-        if marks: marks[4].record(stream)
 
     for s in range(args.warmup):
         step(s)
@@ -194,16 +193,18 @@ def run_ours(args):
     torch.cuda.synchronize()
     clocks.start()
     t_wall0 = time.perf_counter()
+    all_marks = []
     for s in range(args.steps):
         l2_flush.zero_()  # flush L2 between timed steps (outside the timed events)
-        marks = [ev() for _ in range(5)]
-        step(args.warmup + s, marks)
-        torch.cuda.synchronize()
-        times["step"].append(marks[0].elapsed_time(marks[4]))
+        marks = [ev() for _ in range(4)]
+        step(args.warmup + s, marks)  # enqueued without host synchronisation (W = 1)
+        all_marks.append(marks)
+    torch.cuda.synchronize()
+    for marks in all_marks:
+        times["step"].append(marks[0].elapsed_time(marks[3]))
         times["profile"].append(marks[0].elapsed_time(marks[1]))
         times["solve"].append(marks[1].elapsed_time(marks[2]))
-        times["compress_allreduce"].append(marks[3].elapsed_time(marks[4]))
-    torch.cuda.synchronize()
+        times["compress_allreduce"].append(marks[2].elapsed_time(marks[3]))
     if world > 1:
         dist.barrier()
     wall = time.perf_counter() - t_wall0
@@ -225,6 +226,7 @@ def run_ours(args):
     out_host = torch.empty(N, dtype=torch.float32).pin_memory()
     e2e_ms = []
     ef.copy_(e0)
+    pairs = []
     for s in range(max(1, args.steps)):
         l2_flush.zero_()
         a, b = ev(), ev()
@@ -233,8 +235,9 @@ def run_ours(args):
         step(s)
         out_host.copy_(out, non_blocking=True)
         b.record(stream)
-        torch.cuda.synchronize()
-        e2e_ms.append(a.elapsed_time(b))
+        pairs.append((a, b))
+    torch.cuda.synchronize()
+    e2e_ms = [a.elapsed_time(b) for a, b in pairs]
     e2e = sum(e2e_ms) / len(e2e_ms)
     if world > 1:
         t = torch.tensor([e2e], device=dev, dtype=torch.float64)
@@ -311,7 +314,6 @@ def run_extras(dev, rank, world, stream, l2_flush, nccl_dist):
         ch_d = torch.empty(L, dtype=torch.int32, device=dev)
         info = torch.empty(48, dtype=torch.uint8, device=dev)
         ws = torch.empty(lgreco.solve_workspace_bytes(L, K, D_BINS), dtype=torch.uint8, device=dev)
-        ch_h = torch.empty(L, dtype=torch.int32).pin_memory()
         nid = None
         if world > 1:
             obj = [lgreco.nccl_unique_id() if rank == 0 else None]
@@ -319,6 +321,7 @@ def run_extras(dev, rank, world, stream, l2_flush, nccl_dist):
             nid = obj[0]
         ctx = lgreco.Context(layers, fam, params, qbucket=128, seed=SEED, rank=rank, world=world, nccl_id=nid)
         t = {"profile": [], "solve": [], "compress_allreduce": [], "step": []}
+        allm = []
         for s in range(7):
             if s >= 2:
                 l2_flush.zero_()
@@ -329,16 +332,16 @@ def run_extras(dev, rank, world, stream, l2_flush, nccl_dist):
             lgreco.solve(err, bits, dflt, comp, D=D_BINS, choice=ch_d, info=info, workspace=ws)
             ctx.plan_broadcast(ch_d)
             m[2].record(stream)
-            ch_h.copy_(ch_d, non_blocking=True)
-            stream.synchronize()
-            ctx.compress_allreduce(ch_h.tolist(), g, ef, out, s)
+            ctx.compress_allreduce_dev(ch_d, g, ef, out, s)
             m[3].record(stream)
-            torch.cuda.synchronize()
             if s >= 2:
-                t["profile"].append(m[0].elapsed_time(m[1]))
-                t["solve"].append(m[1].elapsed_time(m[2]))
-                t["compress_allreduce"].append(m[2].elapsed_time(m[3]))
-                t["step"].append(m[0].elapsed_time(m[3]))
+                allm.append(m)
+        torch.cuda.synchronize()
+        for m in allm:
+            t["profile"].append(m[0].elapsed_time(m[1]))
+            t["solve"].append(m[1].elapsed_time(m[2]))
+            t["compress_allreduce"].append(m[2].elapsed_time(m[3]))
+            t["step"].append(m[0].elapsed_time(m[3]))
         ctx.check()
         ctx.close()
         st = {k: sum(v) / len(v) for k, v in t.items()}

@@ -148,6 +148,14 @@ int lgreco_plan_broadcast(lgreco_ctx* ctx, int32_t* d_choice, void* stream);
 int lgreco_compress_allreduce(lgreco_ctx* ctx, const int32_t* h_choice, const float* d_g,
                               float* d_ef, float* d_out, uint64_t step, void* stream);
 
+/* Same as lgreco_compress_allreduce with the plan in DEVICE memory (d_choice, e.g. the
+ * lgreco_solve output).  For world == 1 QSGD / TopK the plan is consumed on the device
+ * (no host synchronisation: profile -> solve -> compress is one asynchronous stream
+ * sequence and can be captured in a CUDA graph); otherwise the plan is copied to the
+ * host (stream synchronisation) because the exchange sizes depend on it. */
+int lgreco_compress_allreduce_dev(lgreco_ctx* ctx, const int32_t* d_choice, const float* d_g, float* d_ef,
+                                  float* d_out, uint64_t step, void* stream);
+
 /* ---- stage entry points (the steps lgreco_compress_allreduce composes; used by
  * ---- the parity tests to simulate W ranks on one GPU) ------------------------ */
 

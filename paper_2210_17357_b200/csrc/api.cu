@@ -213,6 +213,7 @@ int lgreco_ctx_create(lgreco_ctx** out, const lgreco_layer* layers, int32_t L, c
   }
 #undef LG_ALLOC
   if (cudaMallocHost((void**)&c->h_plan_pinned, sizeof(lg::DevPlan) * L) != cudaSuccess) return fail(LGRECO_ENOMEM);
+  if (cudaMallocHost((void**)&c->h_choice_pinned, sizeof(int32_t) * L) != cudaSuccess) return fail(LGRECO_ENOMEM);
   if (cudaEventCreateWithFlags(&c->plan_evt, cudaEventDisableTiming) != cudaSuccess) return fail(LGRECO_ECUDA);
   cudaError_t e = cudaSuccess;
   if (e == cudaSuccess) e = cudaMemcpyAsync(c->d_layers, dl.data(), sizeof(lg::DevLayer) * L, cudaMemcpyHostToDevice, st);
@@ -264,6 +265,7 @@ void lgreco_ctx_destroy(lgreco_ctx* c) {
   cudaFree(c->d_chunks); cudaFree(c->d_chunks_all); cudaFree(c->d_layer_chunk0); cudaFree(c->d_partial); cudaFree(c->d_flag);
   cudaFree(c->d_plan); cudaFree(c->d_pay1); cudaFree(c->d_recv); cudaFree(c->d_pay2);
   if (c->h_plan_pinned) cudaFreeHost(c->h_plan_pinned);
+  if (c->h_choice_pinned) cudaFreeHost(c->h_choice_pinned);
   if (c->plan_evt) cudaEventDestroy(c->plan_evt);
   delete c;
 }
@@ -420,6 +422,32 @@ int lgreco_compress_allreduce(lgreco_ctx* c, const int32_t* h_choice, const floa
   }
   LG_NCCL(ncclGroupEnd());
   return lgreco_qsgd_unpack(c, h_choice, c->d_pay2, d_out, stream);
+}
+
+int lgreco_compress_allreduce_dev(lgreco_ctx* c, const int32_t* d_choice, const float* d_g, float* d_ef,
+                                  float* d_out, uint64_t step, void* stream) {
+  if (!c || !d_choice || !d_g || !d_out) { lg_set_error("null argument"); return LGRECO_EINVAL; }
+  cudaStream_t st = (cudaStream_t)stream;
+  if (c->world == 1 && c->family == LGRECO_QSGD) {
+    // W = 1: nothing leaves the GPU, the fused pass needs only the bits per layer
+    LG_LAUNCH(c, lg::launch_plan_qsgd_dev(d_choice, c->d_params, c->K, c->d_layers, c->L, c->d_plan, c->d_flag, st));
+    c->plan_valid = false;  // d_plan now holds a device-chosen plan
+    uint32_t k0, k1;
+    key_of(c, k0, k1);
+    lg::QPackArgs a{d_g, d_ef, nullptr, d_out, c->d_layers, c->d_plan, c->d_chunks_all, c->nchunks_all, c->B,
+                    k0, k1, 0u, (uint32_t)step, c->d_flag};
+    LG_LAUNCH(c, lg::launch_qpack(a, st));
+    c->launches += 2;
+    return LGRECO_OK;
+  }
+  if (c->world == 1 && c->family == LGRECO_TOPK) {
+    c->launches += 0;
+    return topk_compress_dev(c, d_choice, d_g, d_ef, d_out, st);
+  }
+  // the exchange needs host-side shard sizes: bring the plan to the host
+  LG_CUDA(cudaMemcpyAsync(c->h_choice_pinned, d_choice, sizeof(int32_t) * c->L, cudaMemcpyDeviceToHost, st));
+  LG_CUDA(cudaStreamSynchronize(st));
+  return lgreco_compress_allreduce(c, c->h_choice_pinned, d_g, d_ef, d_out, step, stream);
 }
 
 int lgreco_topk_pack(lgreco_ctx* c, const int32_t* h_choice, const float* d_g, float* d_ef, uint8_t* d_payload,

@@ -253,3 +253,24 @@ int topk_compress_allreduce(lgreco_ctx* c, const int32_t* choice, const float* g
   LG_NCCL(ncclAllGather(t->d_pay, t->d_gath, (size_t)t->S, ncclUint8, c->comm, st));
   return topk_combine(c, choice, c->world, t->d_gath, out, st);
 }
+
+// W == 1 fused TopK compress with the plan read on the device (no host round trip).
+int topk_compress_dev(lgreco_ctx* c, const int32_t* d_choice, const float* g, float* ef, float* out, cudaStream_t st) {
+  Topk* t = c->tk;
+  LG_LAUNCH(c, lg::launch_plan_topk_dev(d_choice, c->d_params, c->K, c->d_layers, t->d_clayer, t->nC, t->d_kplan,
+                                        c->d_flag, st));
+  t->plan_valid = false;  // d_kplan now holds a device-chosen plan
+  const lg::TkArgs a = tk_args(c, t->d_kplan);
+  c->launches += 1;
+  if (t->nC) {
+    LG_LAUNCH(c, lg::launch_topk_select(g, ef, a, 1, nullptr, nullptr, 1, st, &c->launches));
+    LG_LAUNCH(c, lg::launch_topk_compact(g, ef, nullptr, out, a, st));
+    c->launches += 3;
+  }
+  if (t->n_ll) {
+    LG_LAUNCH(c, lg::launch_lossless_pack(g, ef, nullptr, out, c->d_layers, t->d_chunks_ll, t->n_ll, t->d_tplan,
+                                          c->d_flag, st));
+    c->launches += 1;
+  }
+  return LGRECO_OK;
+}

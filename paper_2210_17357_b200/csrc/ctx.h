@@ -67,6 +67,7 @@ struct lgreco_ctx {
   uint8_t *d_pay1 = nullptr, *d_recv = nullptr, *d_pay2 = nullptr;
   int64_t pay_cap = 0;
   ncclComm_t comm = nullptr;
+  int32_t* h_choice_pinned = nullptr;  // D2H staging for lgreco_compress_allreduce_dev
   // TopK state (family == LGRECO_TOPK)
   struct Topk* tk = nullptr;
   // PowerSGD state (family == LGRECO_POWERSGD)
@@ -83,6 +84,7 @@ int topk_combine(lgreco_ctx* c, const int32_t* choice, int W, const uint8_t* gat
 int topk_compress_allreduce(lgreco_ctx* c, const int32_t* choice, const float* g, float* ef, float* out,
                             cudaStream_t st);
 int64_t topk_payload_bytes(lgreco_ctx* c, const int32_t* choice);
+int topk_compress_dev(lgreco_ctx* c, const int32_t* d_choice, const float* g, float* ef, float* out, cudaStream_t st);
 int psgd_init(lgreco_ctx* c, cudaStream_t st);
 void psgd_destroy(lgreco_ctx* c);
 int psgd_profile(lgreco_ctx* c, const float* g, const float* e, uint64_t step, double* err, int64_t* bits,

@@ -45,6 +45,8 @@ cudaError_t launch_qprofile(const QProfileArgs& a, cudaStream_t st);
 cudaError_t launch_qpack(const QPackArgs& a, cudaStream_t st);
 cudaError_t launch_qunpack(const QUnpackArgs& a, cudaStream_t st);
 cudaError_t launch_qreduce(const QReduceArgs& a, cudaStream_t st);
+cudaError_t launch_plan_qsgd_dev(const int32_t* choice, const int32_t* params, int K, const DevLayer* layers, int L,
+                                 DevPlan* plan, unsigned* flag, cudaStream_t st);
 cudaError_t launch_philox(const uint32_t* ctr, uint32_t k0, uint32_t k1, int64_t n, uint32_t* out,
                           cudaStream_t st);
 
@@ -66,6 +68,8 @@ struct TkArgs {
 };
 cudaError_t launch_topk_select(const float* g, const float* e, const TkArgs& a, int nq, double* err, int64_t* bits,
                                int K, cudaStream_t st, int64_t* launches);
+cudaError_t launch_plan_topk_dev(const int32_t* choice, const int32_t* params, int K, const DevLayer* layers,
+                                 const int32_t* clayer, int nC, int64_t* kplan, unsigned* flag, cudaStream_t st);
 cudaError_t launch_topk_lossless_rows(const DevLayer* layers, int L, int K, double* err, int64_t* bits, cudaStream_t st);
 cudaError_t launch_topk_compact(const float* g, float* ef, uint8_t* payload, float* out, const TkArgs& a,
                                 cudaStream_t st);

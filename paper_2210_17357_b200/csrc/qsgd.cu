@@ -542,6 +542,28 @@ k_qreduce(const uint8_t* __restrict__ recv, int64_t shard_bytes, int64_t byte0, 
   }
 }
 
+// device-side plan for the W == 1 fused path (no payload): bits per layer from the
+// device-resident choice (no host round trip)
+__global__ void k_plan_qsgd_dev(const int32_t* __restrict__ choice, const int32_t* __restrict__ params, int K,
+                                const DevLayer* __restrict__ layers, int L, DevPlan* __restrict__ plan,
+                                unsigned* __restrict__ flag) {
+  for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < L; l += gridDim.x * blockDim.x) {
+    int bits = 0;
+    if (layers[l].compress) {
+      int c = choice[l];
+      if (c < 0 || c >= K) { atomicOr(flag, 2u); c = 0; }
+      bits = params[c];
+    }
+    plan[l] = DevPlan{0, bits, 0};
+  }
+}
+
+cudaError_t launch_plan_qsgd_dev(const int32_t* choice, const int32_t* params, int K, const DevLayer* layers, int L,
+                                 DevPlan* plan, unsigned* flag, cudaStream_t st) {
+  k_plan_qsgd_dev<<<(L + 255) / 256, 256, 0, st>>>(choice, params, K, layers, L, plan, flag);
+  return cudaGetLastError();
+}
+
 __global__ void k_philox(const uint32_t* __restrict__ ctr, uint32_t k0, uint32_t k1, int64_t n,
                          uint32_t* __restrict__ out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

@@ -637,6 +637,27 @@ k_tk_scatter(const uint8_t* __restrict__ pay_w, int W, float* __restrict__ out, 
   }
 }
 
+// device-side k per compressed layer from the device-resident choice (W == 1 path)
+__global__ void k_plan_topk_dev(const int32_t* __restrict__ choice, const int32_t* __restrict__ params, int K,
+                                const DevLayer* __restrict__ layers, const int32_t* __restrict__ clayer, int nC,
+                                int64_t* __restrict__ kplan, unsigned* __restrict__ flag) {
+  for (int ci = blockIdx.x * blockDim.x + threadIdx.x; ci < nC; ci += gridDim.x * blockDim.x) {
+    const int l = clayer[ci];
+    int c = choice[l];
+    if (c < 0 || c >= K) { atomicOr(flag, 2u); c = 0; }
+    const int64_t n = layers[l].numel;
+    int64_t k = ((int64_t)params[c] * n + 999999) / 1000000;
+    kplan[ci] = k < 1 ? 1 : (k > n ? n : k);
+  }
+}
+
+cudaError_t launch_plan_topk_dev(const int32_t* choice, const int32_t* params, int K, const DevLayer* layers,
+                                 const int32_t* clayer, int nC, int64_t* kplan, unsigned* flag, cudaStream_t st) {
+  if (nC == 0) return cudaSuccess;
+  k_plan_topk_dev<<<(nC + 255) / 256, 256, 0, st>>>(choice, params, K, layers, clayer, nC, kplan, flag);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------

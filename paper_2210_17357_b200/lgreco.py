@@ -58,6 +58,7 @@ _SIGS = {
     "lgreco_solve": (C.c_int, [_VP, _VP, _I32, _I32, _VP, _VP, _I32, _U32, _VP, _VP, _VP, C.c_size_t, _VP]),
     "lgreco_plan_broadcast": (C.c_int, [_VP, _VP, _VP]),
     "lgreco_compress_allreduce": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _U64, _VP]),
+    "lgreco_compress_allreduce_dev": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _U64, _VP]),
     "lgreco_payload_bytes": (_I64, [_VP, _VP]),
     "lgreco_shard_bounds": (C.c_int, [_VP, _VP, _I32, _VP, _VP]),
     "lgreco_qsgd_pack": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _U32, _U64, _VP]),
@@ -164,6 +165,10 @@ class Context:
     def compress_allreduce(self, choice, g, ef, out, step, stream=None):
         _check(lib().lgreco_compress_allreduce(self.h, _i32(choice), _ptr(g), _ptr(ef), _ptr(out), step,
                                                _stream(stream)), "compress_allreduce")
+
+    def compress_allreduce_dev(self, d_choice, g, ef, out, step, stream=None):
+        _check(lib().lgreco_compress_allreduce_dev(self.h, _ptr(d_choice), _ptr(g), _ptr(ef), _ptr(out), step,
+                                                   _stream(stream)), "compress_allreduce_dev")
 
     def plan_broadcast(self, d_choice, stream=None):
         _check(lib().lgreco_plan_broadcast(self.h, _ptr(d_choice), _stream(stream)), "plan_broadcast")

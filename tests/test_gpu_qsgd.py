@@ -203,3 +203,17 @@ def test_c4_full_size(lg, ref):
     out_ref, es_ref, _, _ = ref.qsgd_allreduce(layers, lbits, [g], [e], seed=0x5EED, step=0)
     assert np.array_equal(out.cpu().numpy().view(np.uint32), out_ref.view(np.uint32))
     assert np.array_equal(ed.cpu().numpy().view(np.uint32), es_ref[0].view(np.uint32))
+
+
+def test_compress_allreduce_dev_matches_host_path(lg):
+    """The device-plan entry point (no host round trip at W = 1) gives the same bytes."""
+    layers = W.config_layers("C1")
+    g, e = W.gaussian_outliers(layers, seed=12)
+    choice = [int(c) for c in np.random.default_rng(12).integers(0, len(BITS), len(layers))]
+    ctx = lg.Context(layers, lg.QSGD, BITS, seed=5)
+    gd = _dev(g)
+    e1, e2 = _dev(e), _dev(e)
+    o1, o2 = torch.empty_like(gd), torch.empty_like(gd)
+    ctx.compress_allreduce(choice, gd, e1, o1, 3)
+    ctx.compress_allreduce_dev(torch.tensor(choice, dtype=torch.int32, device="cuda"), gd, e2, o2, 3)
+    assert torch.equal(o1.view(torch.int32), o2.view(torch.int32)) and torch.equal(e1.view(torch.int32), e2.view(torch.int32))

@@ -176,3 +176,16 @@ def test_c3_sampled_full_size(lg, ref):
         sl = slice(l.offset, l.offset + l.numel)
         assert np.array_equal(oc[sl].view(np.uint32), out_ref[sl].view(np.uint32))
         assert np.array_equal(ec[sl].view(np.uint32), es_ref[0][sl].view(np.uint32))
+
+
+def test_compress_allreduce_dev_matches_host_path(lg):
+    layers = _layers()
+    g, e = _data(layers, 21)
+    choice = [3 if l.compress else -1 for l in layers]
+    ctx = lg.Context(layers, lg.TOPK, PPM)
+    gd = _dev(g)
+    e1, e2 = _dev(e), _dev(e)
+    o1, o2 = torch.empty_like(gd), torch.empty_like(gd)
+    ctx.compress_allreduce(choice, gd, e1, o1, 0)
+    ctx.compress_allreduce_dev(torch.tensor(choice, dtype=torch.int32, device="cuda"), gd, e2, o2, 0)
+    assert torch.equal(o1.view(torch.int32), o2.view(torch.int32)) and torch.equal(e1.view(torch.int32), e2.view(torch.int32))
