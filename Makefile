@@ -15,9 +15,18 @@ ORACLE  := oracle/liblgreco_ref.so
 
 all: $(LIB) $(ORACLE)
 
-$(LIB): $(SRCS) $(HDRS)
-	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRCS) -L$(NCCL)/lib -l:libnccl.so.2 \
-	    -Xlinker -rpath=$(NCCL)/lib -Xlinker -rpath=$(CUDART) 2> build/ptxas.log || (cat build/ptxas.log; false)
+OBJS    := $(patsubst $(PKG)/csrc/%.cu,build/obj/%.o,$(SRCS))
+
+# one object per translation unit (parallel with make -j); the ptxas -v report of
+# every unit is concatenated into build/ptxas.log
+build/obj/%.o: $(PKG)/csrc/%.cu $(HDRS)
+	@mkdir -p build/obj
+	$(NVCC) $(NVFLAGS) -c -o $@ $< 2> build/obj/$*.ptxas.log || (cat build/obj/$*.ptxas.log; false)
+
+$(LIB): $(OBJS)
+	$(NVCC) $(ARCH) -cudart shared -shared -o $@ $(OBJS) -L$(NCCL)/lib -l:libnccl.so.2 \
+	    -Xlinker -rpath=$(NCCL)/lib -Xlinker -rpath=$(CUDART)
+	cat build/obj/*.ptxas.log > build/ptxas.log
 
 $(ORACLE): oracle/lgreco_ref.c
 	gcc -O2 -ffp-contract=off -fno-fast-math -fPIC -shared -o $@ $< -lm
@@ -25,4 +34,15 @@ $(ORACLE): oracle/lgreco_ref.c
 clean:
 	rm -f $(LIB) $(ORACLE)
 
-.PHONY: all clean
+.PHONY: all clean timing
+
+# diagnostic build: k_solve_fast prints its phase cycle counts (scripts/dp_timing.py)
+build/obj/dp_timing.o: $(PKG)/csrc/dp.cu $(HDRS)
+	@mkdir -p build/obj
+	$(NVCC) $(NVFLAGS) -DLG_DP_TIMING -c -o $@ $< 2> /dev/null
+
+build/liblgreco_timing.so: $(filter-out build/obj/dp.o,$(OBJS)) build/obj/dp_timing.o
+	$(NVCC) $(ARCH) -cudart shared -shared -o $@ $^ -L$(NCCL)/lib -l:libnccl.so.2 \
+	    -Xlinker -rpath=$(NCCL)/lib -Xlinker -rpath=$(CUDART)
+
+timing: build/liblgreco_timing.so

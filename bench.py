@@ -72,55 +72,71 @@ class ClockSampler:
         self._stop = threading.Event()
         self._thr = None
 
+    def _nvml(self):
+        import pynvml as N
+        N.nvmlInit()
+        h = N.nvmlDeviceGetHandleByIndex(self.idx)
+        self.max_mhz = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+        bits = {k: getattr(N, v, 0) for k, v in self.REASONS.items()}
+        get_reasons = getattr(N, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            N.nvmlDeviceGetCurrentClocksThrottleReasons
+
+        def sample():
+            self.sm.append(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM))
+            r = get_reasons(h)
+            for k, bit in bits.items():
+                if bit and (r & bit):
+                    self.reasons.add(k)
+        return sample
+
     def _run(self):
         try:
-            import pynvml as N
-            N.nvmlInit()
-            h = N.nvmlDeviceGetHandleByIndex(self.idx)
-            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
-            bits = {k: getattr(N, v, 0) for k, v in self.REASONS.items()}
-            get_reasons = getattr(N, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
-                N.nvmlDeviceGetCurrentClocksThrottleReasons
             while not self._stop.is_set():
-                self.sm.append(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM))
-                r = get_reasons(h)
-                for k, bit in bits.items():
-                    if bit and (r & bit):
-                        self.reasons.add(k)
-                self._stop.wait(0.002)
-        except Exception as ex:  # fall back to nvidia-smi polling
+                self._sample()
+                self._stop.wait(0.001)
+        except Exception as ex:
             self.err = f"nvml: {ex}"
-            import subprocess
-            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
-            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-            while not self._stop.is_set():
-                try:
-                    out = subprocess.run(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                         timeout=5).stdout.strip().split(",")
-                    self.sm.append(float(out[0]))
-                    self.max_mhz = float(out[1])
-                    for n, v in zip(names, out[2:]):
-                        if v.strip().lower() == "active":
-                            self.reasons.add(n)
-                except Exception as ex2:
-                    self.err += f"; smi: {ex2}"
-                    break
+
+    def _smi(self):
+        import subprocess
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        out = subprocess.run(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={q}", "--format=csv,noheader,nounits"],
+                             capture_output=True, text=True, timeout=5).stdout.strip().split(",")
+        self.sm.append(float(out[0]))
+        self.max_mhz = float(out[1])
+        for n, v in zip(names, out[2:]):
+            if v.strip().lower() == "active":
+                self.reasons.add(n)
 
     def start(self):
+        """Called right before the timed region: NVML is initialised here (outside the
+        region) so the sampling thread is already polling when the first step launches."""
         import threading
+        try:
+            self._sample = self._nvml()
+            self.source = "nvml ~1 ms"
+        except Exception as ex:
+            self.err = f"nvml: {ex}"
+            self._sample = self._smi
+            self.source = "nvidia-smi"
         self._thr = threading.Thread(target=self._run, daemon=True)
         self._thr.start()
 
     def stop(self):
+        """Called right after the timed region's closing synchronize (one final sample)."""
         self._stop.set()
         if self._thr:
             self._thr.join(timeout=5)
+        try:
+            self._sample()
+        except Exception as ex:
+            self.err = getattr(self, "err", "") + f"; final sample: {ex}"
         if not self.sm:
             return {"error": getattr(self, "err", "no samples")}
         return {"sm_mhz": statistics.median(self.sm), "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
-                "samples": len(self.sm), "source": "nvml 2 ms" if not hasattr(self, "err") else "nvidia-smi",
+                "samples": len(self.sm), "source": self.source,
                 "min_mhz": min(self.sm)}
 
 

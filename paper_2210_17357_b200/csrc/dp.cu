@@ -10,6 +10,7 @@
 // memory, PD (one byte per cell) in global memory.
 #include <math.h>
 #include <stdint.h>
+#include <stdio.h>
 
 #include <algorithm>
 
@@ -175,17 +176,45 @@ k_solve_generic(const double* __restrict__ err, const int64_t* __restrict__ bits
 
 
 // ---------------------------------------------------------------------------
-// Fast path: cells in registers, packed (value << cbits | c) keys.
-// Costs are divided by g = gcd of all active costs (an exact order-preserving
-// rescale), so the DP runs on 32-bit keys whenever the largest possible plan
-// cost fits in 31 - cbits bits, else on 64-bit keys.  min() over packed keys
-// picks the smallest cost and, among equal costs, the first candidate in list
-// order -- exactly Alg.1's strict-< update in candidate order (R19).
+// Fast path: cells in registers, packed (value << kb | c) keys.
+// Costs are divided by g = the largest power of two dividing every active cost (an
+// exact order- and sum-preserving rescale: one OR-reduction, a shift per cost).  min() over packed keys picks the smallest cost and, among equal costs,
+// the first candidate in list order -- exactly Alg.1's strict-< update in candidate
+// order (R19).  32-bit keys (one LDS + one VIADDMNMX, DPX add-min, per cell and
+// candidate) whenever the largest plan cost fits 30 - kb bits:
+//   K <= 16 (KT > 0): kb = ceil(log2 K), key = value << kb | c;
+//   K > 16 (KT = 0):  candidates in groups of 16, kb = 4, key = value << 4 | (c % 16);
+//                     the min over a group is merged into the running best by value
+//                     with strict < (earlier group wins ties), the group kept aside.
+// Otherwise 64-bit keys value << cbits | c.
+//
+// A warp owns 32*CPT consecutive cells; row arrays carry 32*CPT INF cells in front.
+// A candidate shift d > wbase + 32*CPT (the warp's whole window below cell 0) is
+// clamped to wbase + 32*CPT, so every read lands in the row or in the INF pad.
+// PD is stored thread-major, one 16-byte word per thread and layer (byte i =
+// register i): PD byte of (layer a, cell e) = PD[a*16384 + tid(e)*16 + i(e)].
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ uint64_t gcd64(uint64_t a, uint64_t b) {
-  while (b) { const uint64_t t = a % b; a = b; b = t; }
-  return a;
+constexpr int PD_ROW = DP_THREADS * 16;
+
+// Cell e lives in warp w = e / (32*CPT), register i = (e % (32*CPT)) / 32, lane e % 32:
+// a warp owns one contiguous range of 32*CPT cells (so a warp wholly outside the
+// reachable band skips its row at once).
+template <int CPT>
+__device__ __forceinline__ int pd_byte(const uint8_t* PD, int a, int e) {
+  const int w = e / (32 * CPT), r = e - w * (32 * CPT);
+  return __ldcg(PD + (int64_t)a * PD_ROW + (w * 32 + (r & 31)) * 16 + (r >> 5));  // L2 (written this kernel)
 }
+
+// byte p of x replaced by the low byte of y
+__device__ __forceinline__ uint32_t put_byte(uint32_t x, uint32_t y, int p) {
+  return __byte_perm(x, y, p == 0 ? 0x3214 : p == 1 ? 0x3240 : p == 2 ? 0x3410 : 0x4210);
+}
+
+#ifdef LG_DP_TIMING
+#define LG_T(i) do { if (tid == 0) tstamp[i] = clock64(); } while (0)
+#else
+#define LG_T(i) do { } while (0)
+#endif
 
 template <int CPT, int KT>
 __global__ void __launch_bounds__(DP_THREADS, 1)
@@ -193,9 +222,11 @@ k_solve_fast(const double* __restrict__ err, const int64_t* __restrict__ bits, i
              const int32_t* __restrict__ default_idx, const int32_t* __restrict__ compress, int D, uint32_t flags,
              int32_t* __restrict__ choice, lgreco_solve_info* __restrict__ info, uint8_t* __restrict__ PD,
              int32_t* __restrict__ act, int32_t* __restrict__ wdisc, uint64_t* __restrict__ wadd) {
+  static_assert(CPT >= 1 && CPT <= 16, "PD word holds 16 cells");
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ int32_t s_disc[2][256];
-  __shared__ uint64_t s_add[2][256];
+  __shared__ __align__(16) uint2 s_cand[2][256];  // {disc, 32-bit key addend} per candidate, double-buffered
+  __shared__ uint64_t s_add[2][256];  // 64-bit key addend
+  __shared__ int2 s_band[2];
   __shared__ int s_La, s_status, s_wide, s_cbits;
   __shared__ double s_emax;
   __shared__ int64_t s_defbits;
@@ -205,83 +236,128 @@ k_solve_fast(const double* __restrict__ err, const int64_t* __restrict__ bits, i
   __shared__ int s_rede[DP_THREADS / 32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int W1 = D + 1;
+#ifdef LG_DP_TIMING
+  long long tstamp[10];
+  long long t_ldg = 0, t_rest = 0;
+  int n_rounds = 0;
+#endif
+  LG_T(0);
 
   // ---- prelude, parallel: stage flags/defaults in smem (row area is free yet)
   int32_t* sm_flag = reinterpret_cast<int32_t*>(smem_raw);   // [L]
-  int32_t* sm_def = sm_flag + L;                             // [L]
-  double* sm_de = reinterpret_cast<double*>(sm_def + L);  // [L] metric(err[l][def]) (8L bytes in: aligned)
-  int64_t* sm_db = reinterpret_cast<int64_t*>(sm_de + L);    // [L] bits[l][def]
+  int32_t* sm_act = sm_flag + L;                             // [L] compacted active layer ids
+  double* sm_de = reinterpret_cast<double*>(sm_act + L);     // [L] metric(err[l][def]), by layer (8L bytes in)
+  double* sm_dea = sm_de + L;                                // [L] the same, compacted
   if (tid == 0) { s_status = LGRECO_OK; s_mx = 0; }
   __syncthreads();
+  int64_t db_part = 0;
+  int bad_def = 0;
   for (int l = tid; l < L; l += DP_THREADS) {
     const int f = compress ? (compress[l] != 0) : 1;
     const int d = default_idx[l];
     sm_flag[l] = f;
-    sm_def[l] = d;
     choice[l] = -1;
     if (f) {
-      if (d < 0 || d >= K) { atomicExch(&s_status, LGRECO_EINVAL); sm_de[l] = 0.0; sm_db[l] = 0; }
-      else { sm_de[l] = metric(err[(int64_t)l * K + d], flags); sm_db[l] = bits[(int64_t)l * K + d]; }
+      if (d < 0 || d >= K) { bad_def = 1; sm_de[l] = 0.0; }
+      else { sm_de[l] = metric(err[(int64_t)l * K + d], flags); db_part += bits[(int64_t)l * K + d]; }
     }
   }
+  if (__any_sync(LG_FULL, bad_def) && lane == 0) atomicExch(&s_status, LGRECO_EINVAL);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) db_part += __shfl_xor_sync(LG_FULL, db_part, o);
+  if (lane == 0) s_redk[warp] = (uint64_t)db_part;
   __syncthreads();
-  // ---- Alg.1 lines 1-2 (thread 0, layer order, from shared memory)
-  if (tid == 0) {
+  // ---- Alg.1 lines 1-2 (warp 0): ordered compaction by ballot, Emax in layer order
+  if (warp == 0) {
     int La = 0;
-    double emax = 0.0;
-    int64_t defb = 0;
-    for (int l = 0; l < L; ++l) {
-      if (!sm_flag[l]) continue;
-      act[La++] = l;
-      emax = __dadd_rn(emax, sm_de[l]);
-      defb += sm_db[l];
+    for (int base = 0; base < L; base += 32) {
+      const int l = base + lane;
+      const int f = (l < L) ? sm_flag[l] : 0;
+      const unsigned m = __ballot_sync(LG_FULL, f);
+      if (f) {
+        const int pos = La + __popc(m & ((1u << lane) - 1u));
+        sm_act[pos] = l;
+        act[pos] = l;
+        sm_dea[pos] = sm_de[l];
+      }
+      La += __popc(m);
     }
-    s_La = La; s_emax = emax; s_defbits = defb;
-    int cb = 0;
-    while ((1 << cb) < K) ++cb;
-    s_cbits = cb;
+    __syncwarp();
+    if (lane == 0) {
+      double emax = 0.0;
+      int a = 0;
+      for (; a + 4 <= La; a += 4) {  // loads hoisted, the fp64 chain stays in layer order
+        const double v0 = sm_dea[a], v1 = sm_dea[a + 1], v2 = sm_dea[a + 2], v3 = sm_dea[a + 3];
+        emax = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(emax, v0), v1), v2), v3);
+      }
+      for (; a < La; ++a) emax = __dadd_rn(emax, sm_dea[a]);
+      int64_t defb = 0;
+      for (int w = 0; w < DP_THREADS / 32; ++w) defb += (int64_t)s_redk[w];
+      s_La = La; s_emax = emax; s_defbits = defb;
+      int cb = 0;
+      while ((1 << cb) < K) ++cb;
+      s_cbits = cb;
+    }
   }
   __syncthreads();
+  LG_T(1);
   const int La = s_La;
   const double emax = s_emax;
-  // ---- validation + gcd of costs + largest plan cost (parallel)
-  uint64_t gg = 0;
+  // ---- one pass over every (layer, candidate): validation, Alg.1 lines 3-5 (discretise
+  //      to the workspace), OR of the costs, per-layer largest cost (for the key width)
+  uint64_t gg = 0, mx_part = 0;
   int bad = 0;
-  for (int i = tid; i < La * K; i += DP_THREADS) {
-    const int l = act[i / K];
-    const double v = err[(int64_t)l * K + (i % K)];
-    const int64_t b = bits[(int64_t)l * K + (i % K)];
-    if (!isfinite(v) || v < 0.0) bad |= 1;
-    if (b < 0) bad |= 2;
-    gg = gcd64(gg, (uint64_t)(b < 0 ? 0 : b));
+  for (int a = warp; a < La; a += DP_THREADS / 32) {
+    const int l = sm_act[a];
+    uint64_t m = 0;
+    for (int c = lane; c < K; c += 32) {
+      const double v = err[(int64_t)l * K + c];
+      const int64_t b = bits[(int64_t)l * K + c];
+      if (!isfinite(v) || v < 0.0) bad |= 1;
+      if (b < 0) bad |= 2;
+      const uint64_t ub = (uint64_t)(b < 0 ? 0 : b);
+      gg |= ub;
+      m = max(m, ub);
+      wdisc[a * K + c] = discretise(metric(v, flags), emax, D, flags);
+      wadd[a * K + c] = ub;  // raw cost; keyed (cost/g << cbits | c) when staged per layer
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(LG_FULL, m, o));
+    mx_part += m;  // sum_a max_c cost (lane-replicated)
   }
   bad = __reduce_or_sync(LG_FULL, bad);
 #pragma unroll
-  for (int o = 16; o; o >>= 1) gg = gcd64(gg, __shfl_xor_sync(LG_FULL, gg, o));
+  for (int o = 16; o; o >>= 1) gg |= __shfl_xor_sync(LG_FULL, gg, o);
   if (lane == 0) {
     s_g[warp] = gg;
+    s_redk[warp] = mx_part;
     if (bad & 1) atomicExch(&s_status, LGRECO_ENONFINITE);
     else if (bad & 2) atomicExch(&s_status, LGRECO_EINVAL);
   }
   __syncthreads();
-  if (tid == 0) {
-    uint64_t g = 0;
-    for (int w = 0; w < DP_THREADS / 32; ++w) g = gcd64(g, s_g[w]);
-    s_g[0] = g ? g : 1;
+  if (warp == 0) {
+    uint64_t g = s_g[lane];
+    unsigned long long mxs = s_redk[lane];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      g |= __shfl_xor_sync(LG_FULL, g, o);
+      mxs += __shfl_xor_sync(LG_FULL, mxs, o);
+    }
+    if (lane == 0) {
+      g = g ? (g & (~g + 1)) : 1;  // lowest set bit of the OR = 2^min ctz(cost)
+      s_g[0] = g;
+      // every cost is a multiple of g, so sum_a max_c cost/g = (sum_a max_c cost)/g exactly
+      const uint64_t mx = mxs >> (__ffsll((long long)g) - 1);
+      const int kb = (KT > 0) ? s_cbits : 4;
+      s_wide = (mx >= (1ull << (30 - kb))) ? 1 : 0;  // 32-bit keys < 2^30 < INF32
+      if (mx >= (1ull << (62 - s_cbits)) && s_status == LGRECO_OK) s_status = LGRECO_EINVAL;
+    }
   }
   __syncthreads();
   const uint64_t g = s_g[0];
-  for (int a = tid; a < La; a += DP_THREADS) {
-    uint64_t m = 0;
-    for (int c = 0; c < K; ++c) m = max(m, (uint64_t)max((int64_t)0, bits[(int64_t)act[a] * K + c]) / g);
-    atomicAdd(&s_mx, (unsigned long long)m);
-  }
-  __syncthreads();
-  if (tid == 0) {
-    s_wide = (s_mx >= (1ull << (30 - s_cbits))) ? 1 : 0;  // 32-bit keys < 2^30 < INF32
-    if (s_mx >= (1ull << (62 - s_cbits)) && s_status == LGRECO_OK) s_status = LGRECO_EINVAL;
-  }
-  __syncthreads();
+  const int gsh = __ffsll((long long)g) - 1;
+  const int cbits = s_cbits;
+  LG_T(2);
   if (s_status != LGRECO_OK || La == 0) {
     if (tid == 0) {
       lgreco_solve_info inf = {};
@@ -291,118 +367,166 @@ k_solve_fast(const double* __restrict__ err, const int64_t* __restrict__ bits, i
     }
     return;
   }
-  const int cbits = s_cbits;
-  const uint64_t cmask = (1ull << cbits) - 1;
   const bool wide = s_wide;
-  // ---- Alg.1 lines 3-5 for every (layer, candidate), in parallel, to the workspace
-  for (int i = tid; i < La * K; i += DP_THREADS) {
-    const int a = i / K, c = i % K;
-    const int l = act[a];
-    wdisc[i] = discretise(metric(err[(int64_t)l * K + c], flags), emax, D, flags);
-    wadd[i] = (((uint64_t)bits[(int64_t)l * K + c] / g) << cbits) | (uint64_t)c;
-  }
-  __syncthreads();
-  // rows: 32-bit keys -> two rows padded with W1 INF entries in front (no bounds test);
-  //       64-bit keys -> two rows with one INF sentinel at index -1 (clamped index)
-  // (+ DP_THREADS tail entries: the last register cell of a thread may lie past D)
-  const int row32 = 2 * W1 + DP_THREADS, row64 = W1 + 1 + DP_THREADS;
+  const int kb = wide ? cbits : ((KT > 0) ? cbits : 4);  // key bits below the value
+  const uint64_t kmask = (1ull << kb) - 1;
+  const int pdmask = (!wide && KT == 0) ? 0xFF : (int)((1u << cbits) - 1u);  // PD byte -> c
+  auto keyed = [&](uint64_t ub, int c) -> uint64_t {
+    return ((ub >> gsh) << kb) | (uint64_t)(c & (int)kmask);
+  };
+  // two rows of 32*CPT INF pad cells + CPT*1024 cells (cells past D are computed
+  // too; a cell <= D never reads one)
+  constexpr int PAD = 32 * CPT;
+  const int row = PAD + CPT * DP_THREADS;
   uint32_t* r32a = reinterpret_cast<uint32_t*>(smem_raw);
-  uint32_t* r32b = r32a + row32;
+  uint32_t* r32b = r32a + row;
   uint64_t* r64a = reinterpret_cast<uint64_t*>(smem_raw);
-  uint64_t* r64b = r64a + row64;
+  uint64_t* r64b = r64a + row;
   const uint32_t INF32 = 0x7FFFFF00u;  // > every 32-bit key; INF32 + addend < 2^32
   const uint64_t INF64 = 1ull << 62;
   if (!wide) {
-    for (int i = tid; i < row32; i += DP_THREADS) { r32a[i] = (i == W1) ? 0u : INF32; r32b[i] = INF32; }
+    for (int i = tid; i < row; i += DP_THREADS) { r32a[i] = (i == PAD) ? 0u : INF32; r32b[i] = INF32; }
   } else {
-    for (int i = tid; i < row64; i += DP_THREADS) { r64a[i] = (i == 1) ? 0ull : INF64; r64b[i] = INF64; }
+    for (int i = tid; i < row; i += DP_THREADS) { r64a[i] = (i == PAD) ? 0ull : INF64; r64b[i] = INF64; }
   }
-  if (tid < K) { s_disc[0][tid] = wdisc[tid]; s_add[0][tid] = wadd[tid]; }
+  // Reachable band: a cell e of row a is finite only if lo_a <= e <= hi_a, with lo/hi the
+  // running sums of the smallest/largest admissible disc (exact: every path to e sums
+  // one admissible disc per layer).  A warp whose cells lie wholly outside the band
+  // skips the row (its cells reset to INF).  Tracked for K <= 32 (warp 0).
+  const bool track_band = K <= 32;
+  int lo = 0, hi = 0;  // band of the virtual layer 0 (warp 0 lanes keep it)
+  // Candidates of active layer a (lanes c < K loaded d, ub earlier) into slot, and the
+  // band update.  Inadmissible candidates (disc < 0) and the padding up to KT become
+  // {disc 0, addend INF}: they never win a min, so the inner loop has no branches.
+  const int KP = (KT > 0) ? KT : K;
+  auto stage = [&](int32_t d, uint64_t ub, int slot, int& blo, int& bhi) {
+    if (tid < KP) {
+      const bool ok = tid < K && d >= 0;
+      const uint64_t k = ok ? keyed(ub, tid) : 0;
+      s_cand[slot][tid] = make_uint2(ok ? (uint32_t)d : 0u, ok ? (uint32_t)k : INF32);
+      s_add[slot][tid] = ok ? k : INF64;
+    }
+    if (track_band && warp == 0) {
+      const unsigned ok = (tid < K && d >= 0) ? 1u : 0u;
+      const unsigned mn = __reduce_min_sync(LG_FULL, ok ? (unsigned)d : 0x7fffffffu);
+      const unsigned mxd = __reduce_max_sync(LG_FULL, ok ? (unsigned)d : 0u);
+      const bool any = __any_sync(LG_FULL, ok);
+      blo = any ? min(blo + (int)mn, 0x3fffffff) : 0x3fffffff;
+      bhi = any ? min(bhi + (int)mxd, D) : -1;
+      if (lane == 0) s_band[slot] = make_int2(blo, bhi);
+    }
+  };
+  if (!track_band && tid == 0) { s_band[0] = make_int2(0, D); s_band[1] = make_int2(0, D); }
+  {
+    const int32_t d0 = (tid < K) ? wdisc[tid] : -1;
+    const uint64_t u0 = (tid < K) ? wadd[tid] : 0;
+    stage(d0, u0, 0, lo, hi);
+  }
   __syncthreads();
+  LG_T(3);
   int cur_is_b = 1;
+  const int wbase = warp * (32 * CPT);
+  const int dclamp = wbase + PAD;  // shifts beyond this read only INF (whole window < 0)
   for (int a = 0; a < La; ++a) {
     const int sb = a & 1;
-    // prefetch the next layer's candidate row (published by the barrier below)
+    const int2 band = s_band[sb];
+    // prefetch the next layer's candidates (staged after this row, before the barrier)
     int32_t nd = -1;
-    uint64_t na = 0;
-    if (tid < K && a + 1 < La) { nd = wdisc[(a + 1) * K + tid]; na = wadd[(a + 1) * K + tid]; }
-    uint8_t* pdrow = PD + (int64_t)a * W1;
+    uint64_t nub = 0;
+    if (tid < K && a + 1 < La) { nd = wdisc[(a + 1) * K + tid]; nub = wadd[(a + 1) * K + tid]; }
+    uint32_t pdw[4] = {0u, 0u, 0u, 0u};
+    const bool live = (wbase + 32 * CPT - 1 >= band.x) && (wbase <= band.y);  // warp-uniform
     if (!wide) {
-      const uint32_t* prev = (cur_is_b ? r32a : r32b) + W1;  // index e-d >= -W1 is padded
-      uint32_t* cur = (cur_is_b ? r32b : r32a) + W1;
-      uint32_t best[CPT];
+      const uint32_t* prev = (cur_is_b ? r32a : r32b) + PAD + wbase + lane;
+      uint32_t* cur = (cur_is_b ? r32b : r32a) + PAD + wbase + lane;
+      if (live) {
+        uint32_t best[CPT];
+        if (KT > 0) {
+          // compile-time candidate count: every prev[] read is an LDS with an immediate offset
 #pragma unroll
-      for (int i = 0; i < CPT; ++i) best[i] = 0xFFFFFFFFu;
-      if (KT > 0) {
-        // compile-time candidate bound: every prev[] read is an LDS with an immediate offset
+          for (int c = 0; c < (KT > 0 ? KT : 2); c += 2) {
+            const uint4 q = *reinterpret_cast<const uint4*>(&s_cand[sb][c]);
+            const uint32_t* pv = prev - min((int)q.x, dclamp);
 #pragma unroll
-        for (int c = 0; c < (KT > 0 ? KT : 1); ++c) {
-          if (c < K) {
-            const int d = s_disc[sb][c];
-            if (d >= 0) {
-              const uint32_t ak = (uint32_t)s_add[sb][c];
-              const uint32_t* pv = prev - d + tid;
+            for (int i = 0; i < CPT; ++i)
+              best[i] = (c == 0) ? pv[i * 32] + q.y : __viaddmin_u32(pv[i * 32], q.y, best[i]);
+            if (c + 1 < KT) {
+              const uint32_t* pw = prev - min((int)q.z, dclamp);
 #pragma unroll
-              for (int i = 0; i < CPT; ++i) best[i] = min(best[i], pv[i * DP_THREADS] + ak);
+              for (int i = 0; i < CPT; ++i) best[i] = __viaddmin_u32(pw[i * 32], q.w, best[i]);
             }
+          }
+#pragma unroll
+          for (int i = 0; i < CPT; ++i) {
+            const uint32_t k = best[i];
+            cur[i * 32] = min(k, INF32) & ~(uint32_t)kmask;  // unreachable stays >= INF32
+            pdw[i >> 2] = put_byte(pdw[i >> 2], k, i & 3);   // low bits = candidate (backtrack only)
+          }
+        } else {
+          uint32_t bgrp[CPT];
+#pragma unroll
+          for (int i = 0; i < CPT; ++i) { best[i] = 0xFFFFFFFFu; bgrp[i] = 0; }
+          for (int c0 = 0; c0 < K; c0 += 16) {
+            const int cn = min(16, K - c0);
+            uint32_t gk[CPT];
+#pragma unroll
+            for (int i = 0; i < CPT; ++i) gk[i] = 0xFFFFFFFFu;
+            for (int c = 0; c < cn; ++c) {
+              const uint2 cd = s_cand[sb][c0 + c];
+              const uint32_t* pv = prev - min((int)cd.x, dclamp);
+#pragma unroll
+              for (int i = 0; i < CPT; ++i) gk[i] = __viaddmin_u32(pv[i * 32], cd.y, gk[i]);
+            }
+#pragma unroll
+            for (int i = 0; i < CPT; ++i)
+              if ((gk[i] & ~15u) < (best[i] & ~15u)) { best[i] = gk[i]; bgrp[i] = (uint32_t)c0; }
+          }
+#pragma unroll
+          for (int i = 0; i < CPT; ++i) {
+            const uint32_t k = best[i];
+            cur[i * 32] = min(k, INF32) & ~15u;
+            pdw[i >> 2] = put_byte(pdw[i >> 2], bgrp[i] + (k & 15u), i & 3);
           }
         }
       } else {
-        for (int c = 0; c < K; ++c) {
-          const int d = s_disc[sb][c];
-          if (d < 0) continue;
-          const uint32_t ak = (uint32_t)s_add[sb][c];
-          const uint32_t* pv = prev - d + tid;
 #pragma unroll
-          for (int i = 0; i < CPT; ++i) best[i] = min(best[i], pv[i * DP_THREADS] + ak);
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < CPT; ++i) {
-        const int e = tid + i * DP_THREADS;
-        if (e < W1) {
-          const uint32_t k = best[i];
-          cur[e] = min(k, INF32) & ~(uint32_t)cmask;  // unreachable stays >= INF32
-          pdrow[e] = (uint8_t)(k & (uint32_t)cmask);   // read only on the backtrack path
-        }
+        for (int i = 0; i < CPT; ++i) cur[i * 32] = INF32;
       }
     } else {
-      const uint64_t* prev = (cur_is_b ? r64a : r64b) + 1;  // index -1 is the INF sentinel
-      uint64_t* cur = (cur_is_b ? r64b : r64a) + 1;
+      const uint64_t* prev = (cur_is_b ? r64a : r64b) + PAD + wbase + lane;
+      uint64_t* cur = (cur_is_b ? r64b : r64a) + PAD + wbase + lane;
       uint64_t best[CPT];
 #pragma unroll
       for (int i = 0; i < CPT; ++i) best[i] = ~0ull;
-      for (int c = 0; c < K; ++c) {
-        const int d = s_disc[sb][c];
-        if (d < 0) continue;
-        const uint64_t ak = s_add[sb][c];
+      if (live) {
+        for (int c = 0; c < KP; ++c) {
+          const uint64_t* pv = prev - min((int)s_cand[sb][c].x, dclamp);
+          const uint64_t ak = s_add[sb][c];
 #pragma unroll
-        for (int i = 0; i < CPT; ++i) {
-          const int idx = max(tid + i * DP_THREADS - d, -1);
-          best[i] = min(best[i], prev[idx] + ak);
+          for (int i = 0; i < CPT; ++i) best[i] = min(best[i], pv[i * 32] + ak);
         }
       }
 #pragma unroll
       for (int i = 0; i < CPT; ++i) {
-        const int e = tid + i * DP_THREADS;
-        if (e < W1) {
-          const uint64_t k = best[i];
-          cur[e] = (k >= INF64) ? INF64 : (k & ~cmask);
-          pdrow[e] = (uint8_t)((k >= INF64) ? 0 : (k & cmask));
-        }
+        const uint64_t k = best[i];
+        cur[i * 32] = (k >= INF64) ? INF64 : (k & ~kmask);
+        pdw[i >> 2] = put_byte(pdw[i >> 2], (uint32_t)k, i & 3);
       }
     }
-    if (tid < K) { s_disc[sb ^ 1][tid] = nd; s_add[sb ^ 1][tid] = na; }
+    if (live)
+      *reinterpret_cast<uint4*>(PD + (int64_t)a * PD_ROW + tid * 16) = make_uint4(pdw[0], pdw[1], pdw[2], pdw[3]);
+    if (a + 1 < La) stage(nd, nub, sb ^ 1, lo, hi);
     cur_is_b ^= 1;
     __syncthreads();
   }
+  LG_T(4);
   // ---- line 23: argmin of the last row, smallest e on ties
   uint64_t bk = ~0ull;
   int be = 0x7fffffff;
   for (int e = tid; e < W1; e += DP_THREADS) {
     uint64_t v;
-    if (!wide) { const uint32_t x = ((cur_is_b ? r32a : r32b) + W1)[e]; v = (x >= INF32) ? ~0ull : x; }
-    else { const uint64_t x = ((cur_is_b ? r64a : r64b) + 1)[e]; v = (x >= INF64) ? ~0ull : x; }
+    if (!wide) { const uint32_t x = ((cur_is_b ? r32a : r32b) + PAD)[e]; v = (x >= INF32) ? ~0ull : x; }
+    else { const uint64_t x = ((cur_is_b ? r64a : r64b) + PAD)[e]; v = (x >= INF64) ? ~0ull : x; }
     if (v < bk) { bk = v; be = e; }
   }
 #pragma unroll
@@ -413,32 +537,124 @@ k_solve_fast(const double* __restrict__ err, const int64_t* __restrict__ bits, i
   }
   if (lane == 0) { s_redk[warp] = bk; s_rede[warp] = be; }
   __syncthreads();
-  // stage the discretised table in shared memory for the serial backtrack
+  LG_T(7);
+  // stage the discretised table and the active list in shared memory for the backtrack
   int32_t* sdisc_all = reinterpret_cast<int32_t*>(smem_raw);
-  const bool disc_in_smem = (size_t)La * K * 4 <= (size_t)4 * (wide ? 2 * row64 * 2 : 2 * row32);
-  if (disc_in_smem)
+  const size_t rows_bytes = (size_t)16 * row;  // allocated for two 64-bit rows
+  const bool disc_in_smem = (size_t)(La * K + 2 * La) * 4 <= rows_bytes;
+  if (disc_in_smem) {
     for (int i = tid; i < La * K; i += DP_THREADS) sdisc_all[i] = wdisc[i];
+    for (int i = tid; i < La; i += DP_THREADS) sdisc_all[La * K + i] = act[i];
+  }
   __syncthreads();
+  LG_T(8);
   const int32_t* bdisc = disc_in_smem ? sdisc_all : wdisc;
-  // ---- lines 24-27 backtrack + R20 (thread 0)
-  if (tid == 0) {
-    bk = ~0ull; be = 0x7fffffff;
-    for (int w = 0; w < DP_THREADS / 32; ++w)
-      if (s_redk[w] < bk || (s_redk[w] == bk && s_rede[w] < be)) { bk = s_redk[w]; be = s_rede[w]; }
-    int used_default = 0;
-    if (bk == ~0ull) {
-      used_default = 1;
-    } else {
-      int e = be;
-      for (int a = La - 1; a >= 0; --a) {
-        const int c = PD[(int64_t)a * W1 + e];
-        choice[act[a]] = c;
+  int32_t* bch = disc_in_smem ? sdisc_all + La * K + La : nullptr;  // chosen c per active layer
+  // ---- lines 24-27 backtrack (warp 0).  Speculative: one PD round trip resolves up to
+  //      three layers.  Entry 0 is PD(a, e); entry 1+c1 is PD(a-1, e - disc[a][c1]);
+  //      entry 1+K+c1*K+c2 is PD(a-2, e - disc[a][c1] - disc[a-1][c2]); two entries
+  //      per lane.  The disc rows are loaded before e is known.
+  if (warp == 0) {
+    uint64_t k = s_redk[lane];
+    int ee = s_rede[lane];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const uint64_t ov = __shfl_xor_sync(LG_FULL, k, o);
+      const int oe = __shfl_xor_sync(LG_FULL, ee, o);
+      if (ov < k || (ov == k && oe < ee)) { k = ov; ee = oe; }
+    }
+    const int used_default = (k == ~0ull);
+    const int cm = pdmask;
+    auto put = [&](int a, int c) {
+      if (lane == 0) {
+        if (bch) bch[a] = c;
+        else choice[act[a]] = c;
+      }
+    };
+    if (!used_default) {
+      const int depth = (K < 32 && 1 + K + K * K <= 64) ? 3 : ((K < 32) ? 2 : 1);
+      // per lane slot r: level and candidate pair of entry j = lane + 32 r
+      int lev[2], c1s[2], c2s[2];
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int j = lane + 32 * r;
+        lev[r] = -1; c1s[r] = 0; c2s[r] = 0;
+        if (j == 0) lev[r] = 0;
+        else if (depth >= 2 && j <= K) { lev[r] = 1; c1s[r] = j - 1; }
+        else if (depth >= 3 && j < 1 + K + K * K) { lev[r] = 2; c1s[r] = (j - 1 - K) / K; c2s[r] = (j - 1 - K) % K; }
+      }
+      int e = ee, a = La - 1;
+      // the disc rows of a round do not depend on e: the next round's are loaded
+      // (and its speculative offsets formed) while this round's PD loads are in flight
+      auto disc_rows = [&](int ar, int& da, int& db, int& dc, int* off) {
+        da = (lane < K) ? bdisc[ar * K + lane] : 0;
+        db = (lane < K) ? bdisc[(ar - 1) * K + lane] : 0;
+        dc = (lane < K && depth >= 3) ? bdisc[(ar - 2) * K + lane] : 0;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const int d1 = __shfl_sync(LG_FULL, da, c1s[r]);
+          const int d2 = __shfl_sync(LG_FULL, db, c2s[r]);
+          off[r] = (lev[r] == 0) ? 0 : (lev[r] == 1) ? ((d1 >= 0) ? d1 : -1)
+                 : (lev[r] == 2) ? ((d1 >= 0 && d2 >= 0) ? d1 + d2 : -1) : -1;
+        }
+      };
+      if (depth > 1 && a >= depth - 1) {
+        int da, db, dc, off[2];
+        disc_rows(a, da, db, dc, off);
+        for (;;) {
+          int v[2];
+#ifdef LG_DP_TIMING
+          const long long tq0 = clock64();
+#endif
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            v[r] = 0;
+            if (off[r] >= 0 && e - off[r] >= 0) v[r] = pd_byte<CPT>(PD, a - lev[r], e - off[r]);
+          }
+          const int an = a - depth;
+          int nda = 0, ndb = 0, ndc = 0, noff[2] = {-1, -1};
+          if (an >= depth - 1) disc_rows(an, nda, ndb, ndc, noff);
+#ifdef LG_DP_TIMING
+          {
+            const int vv = __shfl_sync(LG_FULL, v[0] + v[1], 0);
+            const long long tq1 = clock64();
+            t_ldg += tq1 - tq0 + (vv & 0);
+            ++n_rounds;
+          }
+#endif
+          auto val = [&](int j) {
+            const int x0 = __shfl_sync(LG_FULL, v[0], j & 31), x1 = __shfl_sync(LG_FULL, v[1], j & 31);
+            return (j < 32 ? x0 : x1) & cm;
+          };
+          const int c0 = val(0);
+          const int c1 = val(1 + c0);
+          put(a, c0);
+          put(a - 1, c1);
+          int de = __shfl_sync(LG_FULL, da, c0) + __shfl_sync(LG_FULL, db, c1);
+          if (depth >= 3) {
+            const int c2 = val(1 + K + c0 * K + c1);
+            put(a - 2, c2);
+            de += __shfl_sync(LG_FULL, dc, c2);
+          }
+          e -= de;
+          a = an;
+          if (a < depth - 1) break;
+          da = nda; db = ndb; dc = ndc; off[0] = noff[0]; off[1] = noff[1];
+        }
+      }
+      for (; a >= 0; --a) {
+        const int c = pd_byte<CPT>(PD, a, e) & cm;
+        put(a, c);
         e -= bdisc[a * K + c];
       }
     }
-    s_La = used_default;
+    if (lane == 0) s_La = used_default;
   }
   __syncthreads();
+  if (bch && !s_La)
+    for (int a = tid; a < La; a += DP_THREADS) choice[bdisc[La * K + a]] = bch[a];
+  __syncthreads();
+  LG_T(5);
   // R20 check and the summary (parallel gathers, ordered fp64 sum by thread 0)
   double* sm_ce = reinterpret_cast<double*>(smem_raw);         // [La] metric(err[choice])
   int64_t* sm_cb = reinterpret_cast<int64_t*>(sm_ce + La);    // [La] bits[choice]
@@ -458,7 +674,13 @@ k_solve_fast(const double* __restrict__ err, const int64_t* __restrict__ bits, i
     if (tid == 0) {
       int64_t pb = 0;
       double pe = 0.0;
-      for (int a = 0; a < La; ++a) { pb += sm_cb[a]; pe = __dadd_rn(pe, sm_ce[a]); }
+      int a = 0;
+      for (; a + 4 <= La; a += 4) {
+        const double v0 = sm_ce[a], v1 = sm_ce[a + 1], v2 = sm_ce[a + 2], v3 = sm_ce[a + 3];
+        pb += sm_cb[a] + sm_cb[a + 1] + sm_cb[a + 2] + sm_cb[a + 3];
+        pe = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(pe, v0), v1), v2), v3);
+      }
+      for (; a < La; ++a) { pb += sm_cb[a]; pe = __dadd_rn(pe, sm_ce[a]); }
       if (!used_default && (pb > s_defbits || pe > emax)) {
         s_La = 1;  // fall back; recompute the summary for the defaults
       } else {
@@ -480,12 +702,21 @@ k_solve_fast(const double* __restrict__ err, const int64_t* __restrict__ bits, i
     for (int a = tid; a < La; a += DP_THREADS) choice[act[a]] = default_idx[act[a]];
     __syncthreads();
   }
+  LG_T(6);
+#ifdef LG_DP_TIMING
+  if (tid == 0)
+    printf("dp timing (cycles): prelude %lld gcd/disc %lld rows %lld loop %lld (%lld/layer) argmin %lld stage %lld "
+           "back %lld (rounds %d, ldg %lld/round) summary %lld\n",
+           tstamp[1] - tstamp[0], tstamp[2] - tstamp[1], tstamp[3] - tstamp[2], tstamp[4] - tstamp[3],
+           (tstamp[4] - tstamp[3]) / (La ? La : 1), tstamp[7] - tstamp[4], tstamp[8] - tstamp[7],
+           tstamp[5] - tstamp[8], n_rounds, n_rounds ? t_ldg / n_rounds : 0LL, tstamp[6] - tstamp[5]);
+#endif
 }
 
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 size_t solve_workspace_bytes(int L, int K, int D) {
-  return align_up((size_t)L * (D + 1)) + align_up(sizeof(int32_t) * (size_t)(L + 1)) +
+  return align_up((size_t)L * std::max(D + 1, PD_ROW)) + align_up(sizeof(int32_t) * (size_t)(L + 1)) +
          align_up(sizeof(int64_t) * 2 * (size_t)(D + 1)) + align_up(sizeof(int32_t) * (size_t)L * K) +
          align_up(sizeof(uint64_t) * (size_t)L * K);
 }
@@ -493,8 +724,9 @@ size_t solve_workspace_bytes(int L, int K, int D) {
 cudaError_t launch_solve(const SolveArgs& a, void* ws, cudaStream_t st) {
   uint8_t* base = static_cast<uint8_t*>(ws);
   uint8_t* pd = base;
-  int32_t* act = reinterpret_cast<int32_t*>(base + align_up((size_t)a.L * (a.D + 1)));
-  int64_t* grows = reinterpret_cast<int64_t*>(base + align_up((size_t)a.L * (a.D + 1)) +
+  const size_t pd_bytes = align_up((size_t)a.L * std::max(a.D + 1, PD_ROW));
+  int32_t* act = reinterpret_cast<int32_t*>(base + pd_bytes);
+  int64_t* grows = reinterpret_cast<int64_t*>(base + pd_bytes +
                                               align_up(sizeof(int32_t) * (size_t)(a.L + 1)));
   int32_t* wdisc = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(grows) +
                                               align_up(sizeof(int64_t) * 2 * (size_t)(a.D + 1)));
@@ -503,9 +735,9 @@ cudaError_t launch_solve(const SolveArgs& a, void* ws, cudaStream_t st) {
   const int W1 = a.D + 1;
   const int cpt = (W1 + DP_THREADS - 1) / DP_THREADS;
   // fast path: two padded 32-bit rows or two 64-bit rows in smem (see k_solve_fast)
-  const size_t fast_smem = std::max((size_t)8 * (2 * W1 + DP_THREADS), (size_t)16 * (W1 + 1 + DP_THREADS));
+  const size_t fast_smem = (size_t)16 * (32 * cpt + cpt * DP_THREADS);  // two 64-bit rows (>= two 32-bit rows)
   // the prelude stages 24 bytes per layer in the same shared memory
-  if (cpt <= 12 && fast_smem <= 200 * 1024 && (size_t)24 * a.L + 64 <= fast_smem) {
+  if (cpt <= 16 && fast_smem <= 200 * 1024 && (size_t)24 * a.L + 64 <= fast_smem) {
     cudaError_t e = cudaSuccess;
 #define LG_SF2(C, KT)                                                                                      \
   {                                                                                                          \
@@ -516,10 +748,11 @@ cudaError_t launch_solve(const SolveArgs& a, void* ws, cudaStream_t st) {
   }
 #define LG_SF(C)                                       \
   case C:                                              \
-    if (a.K <= 8) LG_SF2(C, 8) else if (a.K <= 16) LG_SF2(C, 16) else LG_SF2(C, 0) \
+    if (C == 10 && a.K == 5) LG_SF2(C, (C == 10 ? 5 : 8)) else if (C == 10 && a.K == 7) LG_SF2(C, (C == 10 ? 7 : 8)) \
+    else if (a.K <= 8) LG_SF2(C, 8) else if (a.K <= 16) LG_SF2(C, 16) else LG_SF2(C, 0) \
     break;
     switch (cpt) { LG_SF(1) LG_SF(2) LG_SF(3) LG_SF(4) LG_SF(5) LG_SF(6) LG_SF(7) LG_SF(8) LG_SF(9) LG_SF(10)
-                   LG_SF(11) LG_SF(12) }
+                   LG_SF(11) LG_SF(12) LG_SF(13) LG_SF(14) LG_SF(15) LG_SF(16) }
 #undef LG_SF
     return cudaGetLastError();
   }

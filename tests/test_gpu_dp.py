@@ -16,8 +16,8 @@ def lg():
 
 
 def _run(lg, err, bits, dflt, compress, D, flags):
-    e = torch.from_numpy(np.ascontiguousarray(err)).cuda()
-    b = torch.from_numpy(np.ascontiguousarray(bits)).cuda()
+    e = torch.from_numpy(np.array(err, dtype=np.float64, order="C", copy=True)).cuda()
+    b = torch.from_numpy(np.array(bits, dtype=np.int64, order="C", copy=True)).cuda()
     d = torch.from_numpy(np.asarray(dflt, np.int32)).cuda()
     c = None if compress is None else torch.from_numpy(np.asarray(compress, np.int32)).cuda()
     choice, info = lg.solve(e, b, d, c, D=D, flags=flags)
@@ -78,3 +78,27 @@ def test_worked_example(lg):
     bits = np.array([[100, 60, 20], [120, 100, 40]], np.int64)
     c, info = _run(lg, err, bits, [1, 1], None, 300, 0)
     assert list(c) == [2, 0] and info.total_bits == 140
+
+
+@pytest.mark.parametrize("K", [1, 3, 5, 7, 8, 12, 16, 17, 33, 100])
+def test_narrow_keys_ties_and_bands(lg, ref, K):
+    """Small costs (32-bit keys: the K <= 16 unrolled path, the grouped K > 16 path),
+    quantised errors so that many (layer, candidate) pairs tie in both disc and cost
+    (tie-breaks R19), and a few inadmissible candidates (disc > D, R17) so that the
+    reachable band is ragged."""
+    rng = np.random.default_rng(100 + K)
+    for D in (100, 5000, 10000, 12000):
+        L = int(rng.integers(20, 160))
+        err = np.sort(rng.integers(0, 6, (L, K)).astype(np.float64) * rng.choice([0.5, 1.0, 2.0], (L, 1)), 1)[:, ::-1]
+        err = err.copy()  # a fresh C-ordered array (the reversed view has negative strides)
+        err[rng.random((L, K)) < 0.03] = 1e6  # disc > D -> skipped
+        bits = np.sort(rng.integers(1, 40, (L, K)), 1).astype(np.int64) * 64
+        dflt = np.full(L, K - 1, np.int32)  # the default must stay admissible
+        err[:, K - 1] = np.minimum(err[:, K - 1], 1.0)
+        comp = (rng.random(L) < 0.85).astype(np.int32)
+        st, c_ref, i_ref = ref.solve(err, bits, dflt, comp, D=D)
+        c_gpu, i_gpu = _run(lg, err, bits, dflt, comp, D, 0)
+        assert st == 0 and i_gpu.status == 0
+        assert list(c_gpu) == list(c_ref), (K, D)
+        assert (i_gpu.total_bits, i_gpu.used_default) == (i_ref.total_bits, i_ref.used_default)
+        assert i_gpu.emax == i_ref.emax and i_gpu.total_err == i_ref.total_err
