@@ -14,8 +14,9 @@ struct Psgd {
   // profile launch config
   lg::PLayer* d_pl_prof = nullptr;
   lg::PTile *d_rt_prof = nullptr, *d_ct_prof = nullptr, *d_rt128_prof = nullptr, *d_ct128_prof = nullptr;
-  int n_prof = 0, nrt_prof = 0, nct_prof = 0, rmax_prof = 0, nrt128_prof = 0, nct128_prof = 0;
-  int32_t* d_rtile0_prof = nullptr;
+  lg::PTile* d_et_prof = nullptr;
+  int n_prof = 0, nrt_prof = 0, nct_prof = 0, rmax_prof = 0, nrt128_prof = 0, nct128_prof = 0, net_prof = 0;
+  int32_t* d_et0_prof = nullptr;
   int32_t* d_ranks = nullptr;
   int32_t* d_ismat = nullptr;
   // compress launch config (per plan)
@@ -23,8 +24,8 @@ struct Psgd {
   bool plan_valid = false;
   std::vector<int32_t> cur_rank;    // rank currently held in Q_ws per matrix layer (0: none)
   lg::PLayer* d_pl_c = nullptr;
-  lg::PTile *d_rt_c = nullptr, *d_ct_c = nullptr, *d_rt128_c = nullptr, *d_ct128_c = nullptr;
-  int n_c = 0, nrt_c = 0, nct_c = 0, rmax_c = 0, nrt128_c = 0, nct128_c = 0;
+  lg::PTile *d_rt_c = nullptr, *d_ct_c = nullptr, *d_rt128_c = nullptr, *d_ct128_c = nullptr, *d_et_c = nullptr;
+  int n_c = 0, nrt_c = 0, nct_c = 0, rmax_c = 0, nrt128_c = 0, nct128_c = 0, net_c = 0;
   int32_t* d_initflag = nullptr;
   bool need_init = false;
   lg::RawSeg* d_raw = nullptr;
@@ -35,9 +36,10 @@ struct Psgd {
   cudaEvent_t evt = nullptr;
   // buffers
   float *P = nullptr, *Ph = nullptr, *Qprof = nullptr, *Qws = nullptr, *Qn = nullptr, *part = nullptr;
-  double *G = nullptr, *nrm_part = nullptr, *nrm = nullptr, *dpart = nullptr;
-  int32_t* need = nullptr;
-  int max_split = 1;
+  float* Ppart = nullptr;  // split-K partials of M Q
+  double *G = nullptr, *epart = nullptr;
+  int max_split = 1, max_ks = 1;
+  int nb_max = 1;  // distinct candidate ranks <= 64 (error boundary slots)
   uint8_t *d_raw_pay = nullptr, *d_raw_gath = nullptr;
   int64_t raw_cap = 0;
 };
@@ -45,34 +47,45 @@ struct Psgd {
 static bool ps_lossless(int64_t m, int64_t k, int64_t r) { return r * (m + k) >= m * k; }
 
 static constexpr int PS_TM = 64;
-static constexpr int64_t PS_SPLIT_ROWS = 2048;
+static constexpr int64_t PS_SPLIT_ROWS = 256;   // M^T P: rows per split (8 K tiles per CTA)
+static constexpr int64_t PS_SPLIT_COLS = 256;   // M Q: K columns per split (8 K tiles per CTA)
+static constexpr int PE_ROWS = 64, PE_COLS = 256, PE_SLOTS = 64;  // element tiles (psgd.cu)
+static int64_t ps_nks(int64_t k) { return std::max<int64_t>(1, (k + PS_SPLIT_COLS - 1) / PS_SPLIT_COLS); }
+static int64_t ps_net(int64_t m, int64_t k) { return ((m + PE_ROWS - 1) / PE_ROWS) * ((k + PE_COLS - 1) / PE_COLS); }
 static constexpr int64_t RAW_CHUNK = 16384;
 
 // Build PLayer + tiles for the ranks `r` (per matrix layer; 0 = skip)
 static void ps_config(lgreco_ctx* c, const std::vector<int32_t>& r, std::vector<lg::PLayer>& pl,
-                      std::vector<lg::PTile>& rt, std::vector<lg::PTile>& ct, std::vector<int32_t>& rt0, int& rmax,
-                      std::vector<lg::PTile>& rt128, std::vector<lg::PTile>& ct128) {
+                      std::vector<lg::PTile>& rt, std::vector<lg::PTile>& ct, std::vector<int32_t>& et0, int& rmax,
+                      std::vector<lg::PTile>& rt128, std::vector<lg::PTile>& ct128, std::vector<lg::PTile>& et) {
   Psgd* p = c->ps;
-  pl.clear(); rt.clear(); ct.clear(); rt0.clear(); rt128.clear(); ct128.clear();
+  pl.clear(); rt.clear(); ct.clear(); et0.clear(); rt128.clear(); ct128.clear(); et.clear();
   rmax = 0;
   for (int i = 0; i < p->nM; ++i) {
     if (r[i] <= 0) continue;
     const lgreco_layer& ly = c->layers[p->mlayer[i]];
     const int ci = (int)pl.size();
     const int nsplit = (int)std::max<int64_t>(1, (ly.rows + PS_SPLIT_ROWS - 1) / PS_SPLIT_ROWS);
+    const int nks = (int)ps_nks(ly.cols);
     pl.push_back(lg::PLayer{ly.offset, ly.rows, ly.cols, r[i], p->mlayer[i], p->poff[i], p->qoff[i], p->goff[i],
-                            p->Qsz, nsplit, 0});
+                            p->Qsz, p->Psz, nsplit, nks});
     rmax = std::max(rmax, r[i]);
-    rt0.push_back((int32_t)rt.size());
+    et0.push_back((int32_t)et.size());
     for (int i0 = 0; i0 < ly.rows; i0 += PS_TM) rt.push_back(lg::PTile{ci, 0, i0, 0, 0, 0});
-    for (int i0 = 0; i0 < ly.rows; i0 += 128) rt128.push_back(lg::PTile{ci, 0, i0, 0, 0, 0});
+    for (int i0 = 0; i0 < ly.rows; i0 += 128)
+      for (int s = 0; s < nks; ++s) {
+        const int c0 = (int)(s * PS_SPLIT_COLS), c1 = (int)std::min<int64_t>(ly.cols, (s + 1) * PS_SPLIT_COLS);
+        rt128.push_back(lg::PTile{ci, s, i0, c1, c0, 0});
+      }
     for (int s = 0; s < nsplit; ++s) {
       const int i0 = (int)(s * PS_SPLIT_ROWS), i1 = (int)std::min<int64_t>(ly.rows, (s + 1) * PS_SPLIT_ROWS);
       for (int c0 = 0; c0 < ly.cols; c0 += PS_TM) ct.push_back(lg::PTile{ci, s, i0, i1, c0, 0});
       for (int c0 = 0; c0 < ly.cols; c0 += 128) ct128.push_back(lg::PTile{ci, s, i0, i1, c0, 0});
     }
+    for (int i0 = 0; i0 < ly.rows; i0 += PE_ROWS)
+      for (int c0 = 0; c0 < ly.cols; c0 += PE_COLS) et.push_back(lg::PTile{ci, 0, i0, 0, c0, 0});
   }
-  rt0.push_back((int32_t)rt.size());
+  et0.push_back((int32_t)et.size());
 }
 
 int psgd_init(lgreco_ctx* c, cudaStream_t st) {
@@ -104,30 +117,40 @@ int psgd_init(lgreco_ctx* c, cudaStream_t st) {
       p->Gsz += (int64_t)rm * rm;
       p->Rmax = std::max(p->Rmax, rm);
       p->max_split = std::max<int>(p->max_split, (int)((ly.rows + PS_SPLIT_ROWS - 1) / PS_SPLIT_ROWS));
+      p->max_ks = std::max<int>(p->max_ks, (int)ps_nks(ly.cols));
       ismat[l] = rp > 0;
     }
     raw_cap += 4 * ly.numel + 16;
   }
   p->nM = (int)p->mlayer.size();
   p->cur_rank.assign(p->nM, 0);
+  {
+    std::vector<int32_t> rs;
+    for (int j = 0; j < K; ++j)
+      if (c->params[j] >= 1 && c->params[j] <= 64) rs.push_back(c->params[j]);
+    std::sort(rs.begin(), rs.end());
+    p->nb_max = std::max<int>(1, (int)(std::unique(rs.begin(), rs.end()) - rs.begin()));
+  }
   p->raw_cap = raw_cap;
   std::vector<lg::PLayer> pl;
-  std::vector<lg::PTile> rt, ct, rt128, ct128;
-  std::vector<int32_t> rt0;
-  ps_config(c, p->rprof, pl, rt, ct, rt0, p->rmax_prof, rt128, ct128);
+  std::vector<lg::PTile> rt, ct, rt128, ct128, et;
+  std::vector<int32_t> et0;
+  ps_config(c, p->rprof, pl, rt, ct, et0, p->rmax_prof, rt128, ct128, et);
   p->n_prof = (int)pl.size(); p->nrt_prof = (int)rt.size(); p->nct_prof = (int)ct.size();
-  p->nrt128_prof = (int)rt128.size(); p->nct128_prof = (int)ct128.size();
-  const size_t KP = (size_t)((K + 7) / 8 * 8);
+  p->nrt128_prof = (int)rt128.size(); p->nct128_prof = (int)ct128.size(); p->net_prof = (int)et.size();
   // compress configs can use at most all matrix layers / tiles of the profile shapes
-  size_t max_rt = 0, max_ct = 0, max_raw = 0;
+  size_t max_rt = 0, max_ct = 0, max_rt128 = 0, max_et = 0, max_raw = 0;
   for (int i = 0; i < p->nM; ++i) {
     const lgreco_layer& ly = c->layers[p->mlayer[i]];
     max_rt += (ly.rows + PS_TM - 1) / PS_TM;
     max_ct += (size_t)((ly.rows + PS_SPLIT_ROWS - 1) / PS_SPLIT_ROWS) * ((ly.cols + PS_TM - 1) / PS_TM);
+    max_rt128 += (size_t)((ly.rows + 127) / 128) * ps_nks(ly.cols);
+    max_et += (size_t)ps_net(ly.rows, ly.cols);
   }
   for (int l = 0; l < L; ++l) max_raw += (c->layers[l].numel + RAW_CHUNK - 1) / RAW_CHUNK;
-  p->stage_bytes = sizeof(lg::PLayer) * std::max(1, p->nM) + sizeof(lg::PTile) * 2 * (max_rt + max_ct + 2) +
-                   sizeof(int32_t) * std::max(1, p->nM) + sizeof(lg::RawSeg) * (max_raw + 1) + 64;
+  p->stage_bytes = sizeof(lg::PLayer) * std::max(1, p->nM) +
+                   sizeof(lg::PTile) * (max_rt + 2 * max_ct + max_rt128 + max_et + 8) +
+                   sizeof(int32_t) * (2 * (size_t)std::max(1, p->nM) + 2) + sizeof(lg::RawSeg) * (max_raw + 1) + 256;
 #define PS_ALLOC(ptr, bytes)                                                                \
   if (cudaMalloc((void**)&(ptr), std::max<size_t>((size_t)(bytes), 16)) != cudaSuccess) {  \
     lg_set_error("cudaMalloc %zu bytes failed (psgd)", (size_t)(bytes));                    \
@@ -138,13 +161,15 @@ int psgd_init(lgreco_ctx* c, cudaStream_t st) {
   PS_ALLOC(p->d_ct_prof, sizeof(lg::PTile) * std::max<size_t>(1, ct.size()));
   PS_ALLOC(p->d_rt128_prof, sizeof(lg::PTile) * std::max<size_t>(1, rt128.size()));
   PS_ALLOC(p->d_ct128_prof, sizeof(lg::PTile) * std::max<size_t>(1, ct128.size()));
-  PS_ALLOC(p->d_rtile0_prof, sizeof(int32_t) * rt0.size());
+  PS_ALLOC(p->d_et_prof, sizeof(lg::PTile) * std::max<size_t>(1, et.size()));
+  PS_ALLOC(p->d_et0_prof, sizeof(int32_t) * et0.size());
   PS_ALLOC(p->d_ranks, sizeof(int32_t) * K);
   PS_ALLOC(p->d_ismat, sizeof(int32_t) * L);
   PS_ALLOC(p->d_pl_c, sizeof(lg::PLayer) * std::max(1, p->nM));
   PS_ALLOC(p->d_rt_c, sizeof(lg::PTile) * std::max<size_t>(1, max_rt));
   PS_ALLOC(p->d_ct_c, sizeof(lg::PTile) * std::max<size_t>(1, max_ct));
-  PS_ALLOC(p->d_rt128_c, sizeof(lg::PTile) * std::max<size_t>(1, max_rt));
+  PS_ALLOC(p->d_rt128_c, sizeof(lg::PTile) * std::max<size_t>(1, max_rt128));
+  PS_ALLOC(p->d_et_c, sizeof(lg::PTile) * std::max<size_t>(1, max_et));
   PS_ALLOC(p->d_ct128_c, sizeof(lg::PTile) * std::max<size_t>(1, max_ct));
   PS_ALLOC(p->d_initflag, sizeof(int32_t) * std::max(1, p->nM));
   PS_ALLOC(p->d_raw, sizeof(lg::RawSeg) * (max_raw + 1));
@@ -154,12 +179,10 @@ int psgd_init(lgreco_ctx* c, cudaStream_t st) {
   PS_ALLOC(p->Qws, sizeof(float) * p->Qsz);
   PS_ALLOC(p->Qn, sizeof(float) * p->Qsz);
   PS_ALLOC(p->part, sizeof(float) * p->Qsz * p->max_split);
+  PS_ALLOC(p->Ppart, sizeof(float) * p->Psz * p->max_ks);
   PS_ALLOC(p->G, sizeof(double) * p->Gsz);
-  PS_ALLOC(p->nrm_part, sizeof(double) * std::max<size_t>(1, max_rt));
-  PS_ALLOC(p->nrm, sizeof(double) * std::max(1, p->nM));
-  PS_ALLOC(p->dpart, sizeof(double) * std::max<size_t>(1, max_rt) * KP);
+  PS_ALLOC(p->epart, sizeof(double) * std::max<size_t>(1, et.size()) * PE_SLOTS);
   if (K > 128) { lg_set_error("PowerSGD: at most 128 candidate ranks"); return LGRECO_EINVAL; }
-  PS_ALLOC(p->need, sizeof(int32_t) * std::max(1, p->nM));
   if (c->world > 1) {
     PS_ALLOC(p->d_raw_pay, raw_cap);
     PS_ALLOC(p->d_raw_gath, raw_cap * c->world);
@@ -174,7 +197,8 @@ int psgd_init(lgreco_ctx* c, cudaStream_t st) {
     LG_CUDA(cudaMemcpyAsync(p->d_rt128_prof, rt128.data(), sizeof(lg::PTile) * rt128.size(), cudaMemcpyHostToDevice, st));
   if (!ct128.empty())
     LG_CUDA(cudaMemcpyAsync(p->d_ct128_prof, ct128.data(), sizeof(lg::PTile) * ct128.size(), cudaMemcpyHostToDevice, st));
-  LG_CUDA(cudaMemcpyAsync(p->d_rtile0_prof, rt0.data(), sizeof(int32_t) * rt0.size(), cudaMemcpyHostToDevice, st));
+  if (!et.empty()) LG_CUDA(cudaMemcpyAsync(p->d_et_prof, et.data(), sizeof(lg::PTile) * et.size(), cudaMemcpyHostToDevice, st));
+  LG_CUDA(cudaMemcpyAsync(p->d_et0_prof, et0.data(), sizeof(int32_t) * et0.size(), cudaMemcpyHostToDevice, st));
   LG_CUDA(cudaMemcpyAsync(p->d_ranks, c->params.data(), sizeof(int32_t) * K, cudaMemcpyHostToDevice, st));
   LG_CUDA(cudaMemcpyAsync(p->d_ismat, ismat.data(), sizeof(int32_t) * L, cudaMemcpyHostToDevice, st));
   LG_CUDA(cudaStreamSynchronize(st));
@@ -184,12 +208,13 @@ int psgd_init(lgreco_ctx* c, cudaStream_t st) {
 void psgd_destroy(lgreco_ctx* c) {
   Psgd* p = c->ps;
   if (!p) return;
-  cudaFree(p->d_pl_prof); cudaFree(p->d_rt_prof); cudaFree(p->d_ct_prof); cudaFree(p->d_rtile0_prof);
+  cudaFree(p->d_pl_prof); cudaFree(p->d_rt_prof); cudaFree(p->d_ct_prof); cudaFree(p->d_et_prof);
+  cudaFree(p->d_et0_prof); cudaFree(p->d_et_c); cudaFree(p->Ppart); cudaFree(p->epart);
   cudaFree(p->d_rt128_prof); cudaFree(p->d_ct128_prof); cudaFree(p->d_rt128_c); cudaFree(p->d_ct128_c);
   cudaFree(p->d_ranks); cudaFree(p->d_ismat); cudaFree(p->d_pl_c); cudaFree(p->d_rt_c); cudaFree(p->d_ct_c);
   cudaFree(p->d_initflag); cudaFree(p->d_raw); cudaFree(p->P); cudaFree(p->Ph); cudaFree(p->Qprof);
-  cudaFree(p->Qws); cudaFree(p->Qn); cudaFree(p->part); cudaFree(p->G); cudaFree(p->nrm_part); cudaFree(p->nrm);
-  cudaFree(p->dpart); cudaFree(p->need); cudaFree(p->d_raw_pay); cudaFree(p->d_raw_gath);
+  cudaFree(p->Qws); cudaFree(p->Qn); cudaFree(p->part); cudaFree(p->G);
+  cudaFree(p->d_raw_pay); cudaFree(p->d_raw_gath);
   if (p->h_stage) cudaFreeHost(p->h_stage);
   if (p->evt) cudaEventDestroy(p->evt);
   delete p;
@@ -199,12 +224,13 @@ void psgd_destroy(lgreco_ctx* c) {
 static lg::PsArgs ps_args_prof(lgreco_ctx* c, const float* g, const float* e) {
   Psgd* p = c->ps;
   return lg::PsArgs{g, e, p->d_pl_prof, p->n_prof, p->d_rt_prof, p->nrt_prof, p->d_ct_prof, p->nct_prof, p->rmax_prof,
-                    p->d_rt128_prof, p->nrt128_prof, p->d_ct128_prof, p->nct128_prof};
+                    p->d_rt128_prof, p->nrt128_prof, p->d_ct128_prof, p->nct128_prof,
+                    p->d_et_prof, p->net_prof, p->d_et0_prof};
 }
 static lg::PsArgs ps_args_c(lgreco_ctx* c, const float* g, const float* e) {
   Psgd* p = c->ps;
   return lg::PsArgs{g, e, p->d_pl_c, p->n_c, p->d_rt_c, p->nrt_c, p->d_ct_c, p->nct_c, p->rmax_c,
-                    p->d_rt128_c, p->nrt128_c, p->d_ct128_c, p->nct128_c};
+                    p->d_rt128_c, p->nrt128_c, p->d_ct128_c, p->nct128_c, p->d_et_c, p->net_c, nullptr};
 }
 
 int psgd_profile(lgreco_ctx* c, const float* g, const float* e, uint64_t step, double* err, int64_t* bits,
@@ -218,14 +244,13 @@ int psgd_profile(lgreco_ctx* c, const float* g, const float* e, uint64_t step, d
   LG_LAUNCH(c, lg::launch_ps_initq(a, p->Qprof, k0, k1, (uint32_t)step, nullptr, st));
   c->launches += 1;
   for (int s = 0; s < c->power_steps; ++s) {
-    LG_LAUNCH(c, lg::launch_ps_mq(a, p->Qprof, p->P, nullptr, st));
+    LG_LAUNCH(c, lg::launch_ps_mq(a, p->Qprof, p->P, p->Ppart, st));
     LG_LAUNCH(c, lg::launch_ps_orth(a, p->P, 1.0f, p->G, p->Ph, st));
     LG_LAUNCH(c, lg::launch_ps_mtp(a, p->Ph, p->part, p->Qprof, 1.0f, st));
-    c->launches += 7;
+    c->launches += 10;  // mq 2 + orth 6 + mtp 2
   }
-  LG_LAUNCH(c, lg::launch_ps_err(a, p->nrm_part, p->d_rtile0_prof, p->Ph, p->Qprof, p->d_ranks, c->K, err, bits,
-                                 p->nrm, p->need, p->dpart, st));
-  c->launches += 3;
+  LG_LAUNCH(c, lg::launch_ps_err(a, p->Ph, p->Qprof, p->d_ranks, c->K, p->nb_max, err, bits, p->epart, st));
+  c->launches += 2;
   return LGRECO_OK;
 }
 
@@ -257,10 +282,10 @@ static int psgd_set_plan(lgreco_ctx* c, const int32_t* choice, cudaStream_t st) 
       return LGRECO_EINVAL;
     }
   std::vector<lg::PLayer> pl;
-  std::vector<lg::PTile> rt, ct, rt128, ct128;
-  std::vector<int32_t> rt0;
+  std::vector<lg::PTile> rt, ct, rt128, ct128, et;
+  std::vector<int32_t> et0;
   int rmax = 0;
-  ps_config(c, r, pl, rt, ct, rt0, rmax, rt128, ct128);
+  ps_config(c, r, pl, rt, ct, et0, rmax, rt128, ct128, et);
   // init flags follow the compress config order (layers with r > 0)
   int ci = 0;
   bool any_init = false;
@@ -290,6 +315,7 @@ static int psgd_set_plan(lgreco_ctx* c, const int32_t* choice, cudaStream_t st) 
   const size_t o_ct = put(ct.data(), sizeof(lg::PTile) * ct.size());
   const size_t o_rt2 = put(rt128.data(), sizeof(lg::PTile) * rt128.size());
   const size_t o_ct2 = put(ct128.data(), sizeof(lg::PTile) * ct128.size());
+  const size_t o_et = put(et.data(), sizeof(lg::PTile) * et.size());
   const size_t o_if = put(initf.data(), sizeof(int32_t) * initf.size());
   const size_t o_sg = put(segs.data(), sizeof(lg::RawSeg) * segs.size());
   if (!pl.empty()) LG_CUDA(cudaMemcpyAsync(p->d_pl_c, h + o_pl, sizeof(lg::PLayer) * pl.size(), cudaMemcpyHostToDevice, st));
@@ -299,11 +325,12 @@ static int psgd_set_plan(lgreco_ctx* c, const int32_t* choice, cudaStream_t st) 
     LG_CUDA(cudaMemcpyAsync(p->d_rt128_c, h + o_rt2, sizeof(lg::PTile) * rt128.size(), cudaMemcpyHostToDevice, st));
   if (!ct128.empty())
     LG_CUDA(cudaMemcpyAsync(p->d_ct128_c, h + o_ct2, sizeof(lg::PTile) * ct128.size(), cudaMemcpyHostToDevice, st));
+  if (!et.empty()) LG_CUDA(cudaMemcpyAsync(p->d_et_c, h + o_et, sizeof(lg::PTile) * et.size(), cudaMemcpyHostToDevice, st));
   LG_CUDA(cudaMemcpyAsync(p->d_initflag, h + o_if, sizeof(int32_t) * initf.size(), cudaMemcpyHostToDevice, st));
   if (!segs.empty()) LG_CUDA(cudaMemcpyAsync(p->d_raw, h + o_sg, sizeof(lg::RawSeg) * segs.size(), cudaMemcpyHostToDevice, st));
   LG_CUDA(cudaEventRecord(p->evt, st));
   p->n_c = (int)pl.size(); p->nrt_c = (int)rt.size(); p->nct_c = (int)ct.size(); p->rmax_c = rmax;
-  p->nrt128_c = (int)rt128.size(); p->nct128_c = (int)ct128.size();
+  p->nrt128_c = (int)rt128.size(); p->nct128_c = (int)ct128.size(); p->net_c = (int)et.size();
   p->nraw = (int)segs.size();
   p->Sraw = off;
   p->need_init = any_init;
@@ -342,8 +369,8 @@ int psgd_p(lgreco_ctx* c, const int32_t* choice, const float* g, const float* e,
     c->launches += 1;
     p->need_init = false;
   }
-  LG_LAUNCH(c, lg::launch_ps_mq(a, p->Qws, d_P ? d_P : p->P, nullptr, st));
-  c->launches += 1;
+  LG_LAUNCH(c, lg::launch_ps_mq(a, p->Qws, d_P ? d_P : p->P, p->Ppart, st));
+  c->launches += 2;
   return LGRECO_OK;
 }
 
@@ -356,7 +383,7 @@ int psgd_q(lgreco_ctx* c, const int32_t* choice, const float* g, const float* e,
   const float invW = 1.0f / (float)W;
   LG_LAUNCH(c, lg::launch_ps_orth(a, d_Psum ? d_Psum : p->P, invW, p->G, p->Ph, st));
   LG_LAUNCH(c, lg::launch_ps_mtp(a, p->Ph, p->part, d_Q ? d_Q : p->Qn, 1.0f, st));
-  c->launches += 6;
+  c->launches += 8;  // orth 6 + mtp 2
   return LGRECO_OK;
 }
 
@@ -422,16 +449,16 @@ extern "C" int lgreco_debug_tc_mq(const float* d_g, const float* d_e, int64_t m,
                                   float* d_P, void* stream) {
   if (!d_g || !d_Q || !d_P || m <= 0 || k <= 0 || r < 1 || r > 64 || m > 0x7fffffff) return LGRECO_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
-  lg::PLayer pl{0, (int32_t)m, k, r, 0, 0, 0, 0, (int64_t)k * r, 1, 0};
-  std::vector<lg::PTile> tiles;
-  for (int64_t i0 = 0; i0 < m; i0 += 128) tiles.push_back(lg::PTile{0, 0, (int32_t)i0, 0, 0, 0});
+  lg::PLayer pl{0, (int32_t)m, k, r, 0, 0, 0, 0, (int64_t)k * r, m * r, 1, 1};
+  std::vector<lg::PTile> tiles;  // one K split: P written directly
+  for (int64_t i0 = 0; i0 < m; i0 += 128) tiles.push_back(lg::PTile{0, 0, (int32_t)i0, k, 0, 0});
   lg::PLayer* d_pl = nullptr;
   lg::PTile* d_t = nullptr;
   LG_CUDA(cudaMalloc(&d_pl, sizeof(pl)));
   LG_CUDA(cudaMalloc(&d_t, sizeof(lg::PTile) * tiles.size()));
   LG_CUDA(cudaMemcpyAsync(d_pl, &pl, sizeof(pl), cudaMemcpyHostToDevice, st));
   LG_CUDA(cudaMemcpyAsync(d_t, tiles.data(), sizeof(lg::PTile) * tiles.size(), cudaMemcpyHostToDevice, st));
-  lg::PsArgs a{d_g, d_e, d_pl, 1, nullptr, 0, nullptr, 0, r, nullptr, 0, nullptr, 0};
+  lg::PsArgs a{d_g, d_e, d_pl, 1, nullptr, 0, nullptr, 0, r, nullptr, 0, nullptr, 0, nullptr, 0, nullptr};
   cudaError_t e = lg::launch_ps_mq_tc(a, d_t, (int)tiles.size(), d_Q, d_P, st);
   cudaError_t e2 = cudaStreamSynchronize(st);
   cudaFree(d_pl);
@@ -449,7 +476,7 @@ extern "C" int lgreco_debug_tc_mtp(const float* d_g, const float* d_e, int64_t m
                                    float* d_Q, void* stream) {
   if (!d_g || !d_P || !d_Q || m <= 0 || k <= 0 || r < 1 || r > 64 || m > 0x7fffffff) return LGRECO_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
-  lg::PLayer pl{0, (int32_t)m, k, r, 0, 0, 0, 0, (int64_t)k * r, 1, 0};
+  lg::PLayer pl{0, (int32_t)m, k, r, 0, 0, 0, 0, (int64_t)k * r, m * r, 1, 1};
   std::vector<lg::PTile> tiles;
   for (int c0 = 0; c0 < k; c0 += 128) tiles.push_back(lg::PTile{0, 0, 0, (int32_t)m, c0, 0});
   lg::PLayer* d_pl = nullptr;
@@ -458,7 +485,7 @@ extern "C" int lgreco_debug_tc_mtp(const float* d_g, const float* d_e, int64_t m
   LG_CUDA(cudaMalloc(&d_t, sizeof(lg::PTile) * tiles.size()));
   LG_CUDA(cudaMemcpyAsync(d_pl, &pl, sizeof(pl), cudaMemcpyHostToDevice, st));
   LG_CUDA(cudaMemcpyAsync(d_t, tiles.data(), sizeof(lg::PTile) * tiles.size(), cudaMemcpyHostToDevice, st));
-  lg::PsArgs a{d_g, d_e, d_pl, 1, nullptr, 0, nullptr, 0, r, nullptr, 0, nullptr, 0};
+  lg::PsArgs a{d_g, d_e, d_pl, 1, nullptr, 0, nullptr, 0, r, nullptr, 0, nullptr, 0, nullptr, 0, nullptr};
   cudaError_t e = lg::launch_ps_mtp_tc(a, d_t, (int)tiles.size(), d_P, d_Q, st);
   cudaError_t e2 = cudaStreamSynchronize(st);
   cudaFree(d_pl);

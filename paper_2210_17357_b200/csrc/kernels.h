@@ -87,29 +87,34 @@ struct PLayer {        // one compressed matrix layer in a grouped launch
   int32_t m, k, r;     // view and the rank of this launch
   int32_t layer;       // layer index in the table
   int64_t poff, qoff, goff;  // offsets into P (m x r), Q (k x r) col-major, G (r x r)
-  int64_t qstride;     // elements between split partials of Q
-  int32_t nsplit, pad;
+  int64_t qstride;     // elements between split partials of Q (M^T P row splits)
+  int64_t pstride;     // elements between split partials of P (M Q column splits)
+  int32_t nsplit;      // row splits of M^T P
+  int32_t nks;         // column (K) splits of M Q
 };
-struct PTile { int32_t ci, split, i0, i1, c0, pad; };  // row tile (i0) or column tile (c0, rows [i0,i1))
+// tile of a grouped launch: MQ tensor-core tile (rows i0.., K columns [c0, i1), split);
+// MtP tile (columns c0.., rows [i0, i1), split); row tile (i0); element tile (i0, c0)
+struct PTile { int32_t ci, split, i0, i1, c0, pad; };
 struct RawSeg { int64_t off, n, pay_off; };            // raw (uncompressed) segment of the gradient
 struct PsArgs {
   const float* g; const float* e; const PLayer* pl; int nC;
   const PTile* rtiles; int n_rtiles; const PTile* ctiles; int n_ctiles; int rmax;
   const PTile* rt128; int n_rt128; const PTile* ct128; int n_ct128;  // tensor-core tiles (128 rows / cols)
+  const PTile* etiles; int n_etiles; const int32_t* etile0;           // element tiles (64 rows x 256 cols)
 };
 cudaError_t launch_ps_initq(const PsArgs& a, float* Q, uint32_t k0, uint32_t k1, uint32_t step, const int32_t* only,
                             cudaStream_t st);
-cudaError_t launch_ps_mq(const PsArgs& a, const float* Q, float* P, double* nrm_part, cudaStream_t st);
+cudaError_t launch_ps_mq(const PsArgs& a, const float* Q, float* P, float* Ppart, cudaStream_t st);
 cudaError_t launch_ps_orth(const PsArgs& a, const float* P, float scale, double* G, float* Ph, cudaStream_t st);
 cudaError_t launch_ps_mtp(const PsArgs& a, const float* Ph, float* part, float* Q, float scale, cudaStream_t st);
 cudaError_t launch_ps_mq_tc(const PsArgs& a, const PTile* tiles128, int ntiles, const float* Q, float* P,
                             cudaStream_t st);
+cudaError_t launch_ps_preduce(const PsArgs& a, const float* part, float* P, cudaStream_t st);
 cudaError_t launch_ps_mtp_tc(const PsArgs& a, const PTile* ctiles128, int ntiles, const float* Ph, float* part,
                              cudaStream_t st);
 cudaError_t launch_ps_mtp_scale(const PsArgs& a, const float* src, float* dst, float scale, cudaStream_t st);
-cudaError_t launch_ps_err(const PsArgs& a, const double* nrm_part, const int32_t* rtile0, const float* Ph,
-                          const float* Q, const int32_t* ranks, int K, double* err, int64_t* bits, double* nrm,
-                          int32_t* need, double* dpart, cudaStream_t st);
+cudaError_t launch_ps_err(const PsArgs& a, const float* Ph, const float* Q, const int32_t* ranks, int K, int nbmax,
+                          double* err, int64_t* bits, double* epart, cudaStream_t st);
 cudaError_t launch_ps_lossless_rows(const DevLayer* layers, int L, int K, const int32_t* ismat, double* err,
                                     int64_t* bits, cudaStream_t st);
 cudaError_t launch_ps_out(const PsArgs& a, float* ef, float* out, const float* Ph, const float* Q, cudaStream_t st);

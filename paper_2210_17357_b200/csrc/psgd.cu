@@ -6,7 +6,7 @@
 //      one run at r_max of `steps` power steps from Q0 (Philox stream 2); every
 //      smaller candidate rank is the prefix of that run (pinned prefix property);
 //      err_r = ||M - P_r Q_r^T||_F computed directly in fp64 from the fp32 factors
-//      (first-order insensitive to factor errors; see k_ps_err_direct).
+//      (first-order insensitive to factor errors; see k_ps_err_cols).
 //   K7 compress (a8-a10, R12): P = M Q_ws -> (all-reduce) -> orthogonalise ->
 //      Q = M^T P -> (all-reduce) -> out = P Q^T, e = x - out, Q_ws <- Q.
 //
@@ -24,8 +24,7 @@
 namespace lg {
 
 constexpr int PS_THREADS = 256;
-constexpr int PS_TM = 64;   // rows per MQ tile / cols per MtP tile
-constexpr int PS_TK = 32;   // reduction depth staged per iteration
+constexpr int PS_TM = 64;   // rows per Cholesky-solve tile
 
 __device__ __forceinline__ float xval(const float* __restrict__ g, const float* __restrict__ e, int64_t i) {
   return canon(__ldg(g + i), e ? __ldg(e + i) : 0.f);
@@ -46,133 +45,6 @@ __global__ void k_ps_initq(const PLayer* __restrict__ pl, int nC, float* __restr
     const uint32_t sel = (t & 3) == 0 ? w.x : (t & 3) == 1 ? w.y : (t & 3) == 2 ? w.z : w.w;
     Q[p.qoff + t] = __fsub_rn(__fmul_rn(2.0f, word_u(sel)), 1.0f);
   }
-}
-
-// ---------------------------------------------------------------------------
-// P = M Q  (grouped over layers; tile = 64 rows x r <= RMAX; column-major P, Q)
-// also accumulates ||M||^2 of the tile (fp64) when nrm != nullptr
-// ---------------------------------------------------------------------------
-template <int RMAX>
-__global__ void __launch_bounds__(PS_THREADS)
-k_ps_mq(const float* __restrict__ g, const float* __restrict__ e, const PLayer* __restrict__ pl,
-        const PTile* __restrict__ tiles, const float* __restrict__ Q, float* __restrict__ P,
-        double* __restrict__ nrm_part) {
-  constexpr int CPT = RMAX / 16;  // output columns per thread
-  __shared__ float Ms[PS_TM][PS_TK + 1];
-  __shared__ float Qs[PS_TK][RMAX];
-  __shared__ double red[PS_THREADS / 32];
-  const PTile tl = tiles[blockIdx.x];
-  const PLayer p = pl[tl.ci];
-  const int tid = threadIdx.x;
-  const int ty = tid >> 4, tx = tid & 15;  // 16 x 16 threads: 4 rows x CPT cols each
-  const int r = p.r;
-  float acc[4][CPT];
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < CPT; ++b) acc[a][b] = 0.f;
-  double nsq = 0.0;
-  const int rows = min(PS_TM, p.m - tl.i0);
-  for (int c0 = 0; c0 < p.k; c0 += PS_TK) {
-    // stage M tile (64 x 32) and Q tile (32 x r)
-    for (int t = tid; t < PS_TM * PS_TK; t += PS_THREADS) {
-      const int rr = t / PS_TK, cc = t % PS_TK;
-      float v = 0.f;
-      if (rr < rows && c0 + cc < p.k) v = xval(g, e, p.moff + (int64_t)(tl.i0 + rr) * p.k + c0 + cc);
-      Ms[rr][cc] = v;
-      if (nrm_part) nsq += (double)v * (double)v;
-    }
-    for (int t = tid; t < PS_TK * RMAX; t += PS_THREADS) {
-      const int j = t / PS_TK, cc = t % PS_TK;
-      Qs[cc][j] = (j < r && c0 + cc < p.k) ? Q[p.qoff + (int64_t)j * p.k + c0 + cc] : 0.f;
-    }
-    __syncthreads();
-#pragma unroll 8
-    for (int cc = 0; cc < PS_TK; ++cc) {
-      float mv[4], qv[CPT];
-#pragma unroll
-      for (int a = 0; a < 4; ++a) mv[a] = Ms[ty + 16 * a][cc];
-#pragma unroll
-      for (int b = 0; b < CPT; ++b) qv[b] = Qs[cc][tx + 16 * b];
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < CPT; ++b) acc[a][b] = __fmaf_rn(mv[a], qv[b], acc[a][b]);
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < CPT; ++b) {
-      const int i = ty + 16 * a, j = tx + 16 * b;
-      if (i < rows && j < r) P[p.poff + (int64_t)j * p.m + tl.i0 + i] = acc[a][b];
-    }
-  if (nrm_part) {
-    nsq = warp_sum_d(nsq);
-    if ((tid & 31) == 0) red[tid >> 5] = nsq;
-    __syncthreads();
-    if (tid == 0) {
-      double s = 0.0;
-      for (int w = 0; w < PS_THREADS / 32; ++w) s += red[w];
-      nrm_part[blockIdx.x] = s;
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// partial Q = M^T P over a row split: tile = 64 columns x r; partial[split][j*k + c]
-// ---------------------------------------------------------------------------
-template <int RMAX>
-__global__ void __launch_bounds__(PS_THREADS)
-k_ps_mtp(const float* __restrict__ g, const float* __restrict__ e, const PLayer* __restrict__ pl,
-         const PTile* __restrict__ tiles, const float* __restrict__ Ph, float* __restrict__ part) {
-  constexpr int CPT = RMAX / 16;
-  __shared__ float Ms[PS_TK][PS_TM + 1];
-  __shared__ float Ps[PS_TK][RMAX];
-  const PTile tl = tiles[blockIdx.x];
-  const PLayer p = pl[tl.ci];
-  const int tid = threadIdx.x;
-  const int ty = tid >> 4, tx = tid & 15;
-  const int r = p.r;
-  const int cols = min(PS_TM, p.k - tl.c0);
-  float acc[4][CPT];
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < CPT; ++b) acc[a][b] = 0.f;
-  for (int i0 = tl.i0; i0 < tl.i1; i0 += PS_TK) {
-    for (int t = tid; t < PS_TK * PS_TM; t += PS_THREADS) {
-      const int rr = t / PS_TM, cc = t % PS_TM;
-      Ms[rr][cc] = (i0 + rr < tl.i1 && cc < cols) ? xval(g, e, p.moff + (int64_t)(i0 + rr) * p.k + tl.c0 + cc) : 0.f;
-    }
-    for (int t = tid; t < PS_TK * RMAX; t += PS_THREADS) {
-      const int j = t / PS_TK, rr = t % PS_TK;
-      Ps[rr][j] = (j < r && i0 + rr < tl.i1) ? Ph[p.poff + (int64_t)j * p.m + i0 + rr] : 0.f;
-    }
-    __syncthreads();
-#pragma unroll 8
-    for (int rr = 0; rr < PS_TK; ++rr) {
-      float mv[4], pv[CPT];
-#pragma unroll
-      for (int a = 0; a < 4; ++a) mv[a] = Ms[rr][ty + 16 * a];
-#pragma unroll
-      for (int b = 0; b < CPT; ++b) pv[b] = Ps[rr][tx + 16 * b];
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < CPT; ++b) acc[a][b] = __fmaf_rn(mv[a], pv[b], acc[a][b]);
-    }
-    __syncthreads();
-  }
-  float* out = part + (int64_t)tl.split * p.qstride + p.qoff;
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < CPT; ++b) {
-      const int c = ty + 16 * a, j = tx + 16 * b;
-      if (c < cols && j < r) out[(int64_t)j * p.k + tl.c0 + c] = acc[a][b];
-    }
 }
 
 // Q = scale * sum_{split} partial (fixed order)
@@ -205,180 +77,211 @@ __global__ void k_ps_scale(const PLayer* __restrict__ pl, int nC, const float* _
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(PS_THREADS)
 k_ps_gram(const PLayer* __restrict__ pl, const float* __restrict__ P, float scale, double* __restrict__ G) {
+  // one warp per entry (a, b), a <= b: lanes stride the rows, fixed shuffle tree
   const PLayer p = pl[blockIdx.x];
-  const int r = p.r;
-  // thread handles entries (a, b), a <= b, strided
+  const int r = p.r, lane = threadIdx.x & 31;
   const int npairs = r * (r + 1) / 2;
-  for (int t = threadIdx.x; t < npairs; t += PS_THREADS) {
+  for (int t = blockIdx.y * (PS_THREADS / 32) + (threadIdx.x >> 5); t < npairs; t += gridDim.y * (PS_THREADS / 32)) {
     int a = 0, rem = t;
     while (rem >= r - a) { rem -= r - a; ++a; }
     const int b = a + rem;
     const float* pa = P + p.poff + (int64_t)a * p.m;
     const float* pb = P + p.poff + (int64_t)b * p.m;
     double s = 0.0;
-    for (int i = 0; i < p.m; ++i) {
+    for (int i = lane; i < p.m; i += 32) {
       const double x = (double)__fmul_rn(pa[i], scale), y = (double)__fmul_rn(pb[i], scale);
       s = fma(x, y, s);
     }
-    G[p.goff + a * r + b] = s;
-    G[p.goff + b * r + a] = s;
+    s = warp_sum_d(s);
+    if (lane == 0) {
+      G[p.goff + a * r + b] = s;
+      G[p.goff + b * r + a] = s;
+    }
   }
 }
 
-// Cholesky G = R^T R (R upper, positive diagonal) in smem, then Phat rows:
-// phat R = pbar (forward substitution per row).  A pivot <= 1e-24 * G[j][j]
-// (or G[j][j] == 0) marks column j as zero, like MGS's zero column.
-__global__ void __launch_bounds__(PS_THREADS)
-k_ps_cholsolve(const PLayer* __restrict__ pl, const PTile* __restrict__ tiles, const double* __restrict__ G,
+// Cholesky G = R^T R (R upper, positive diagonal), once per layer (one warp; the
+// trailing update of step j spreads its (a, b) pairs over the lanes).  A pivot
+// <= 1e-24 * G[j][j] (or G[j][j] == 0) marks column j as zero, like MGS's zero column.
+// R overwrites G (upper triangle; the diagonal entry of a zero column is 0).
+template <int RMAX>
+__global__ void __launch_bounds__(32)
+k_ps_chol(const PLayer* __restrict__ pl, double* __restrict__ G) {
+  __shared__ double Rm[RMAX][RMAX + 1];
+  __shared__ double gdiag[RMAX];
+  const PLayer p = pl[blockIdx.x];
+  const int r = p.r, lane = threadIdx.x;
+  for (int t = lane; t < r * r; t += 32) {
+    const double v = G[p.goff + t];
+    Rm[t / r][t % r] = v;
+    if (t / r == t % r) gdiag[t / r] = v;
+  }
+  __syncwarp();
+  for (int j = 0; j < r; ++j) {
+    double d = Rm[j][j];
+    const bool z = !(d > 1e-24 * gdiag[j]) || gdiag[j] == 0.0;
+    d = z ? 0.0 : sqrt(d);
+    for (int b = j + 1 + lane; b < r; b += 32) Rm[j][b] = z ? 0.0 : Rm[j][b] / d;
+    __syncwarp();
+    if (lane == 0) Rm[j][j] = d;
+    // trailing update over the pairs a <= b of rows/cols j+1 .. r-1
+    const int n = r - j - 1;
+    for (int t = lane; t < n * (n + 1) / 2; t += 32) {
+      int a = 0, rem = t;
+      while (rem >= n - a) { rem -= n - a; ++a; }
+      const int aa = j + 1 + a, bb = aa + rem;
+      Rm[aa][bb] -= Rm[j][aa] * Rm[j][bb];
+    }
+    __syncwarp();
+  }
+  for (int t = lane; t < r * r; t += 32) {
+    const int a = t / r, b = t % r;
+    G[p.goff + t] = (b >= a) ? Rm[a][b] : 0.0;
+  }
+}
+
+// Phat rows: phat R = pbar (forward substitution per row, registers, unrolled), with R
+// from k_ps_chol; column j is zero where R[j][j] == 0.
+template <int RMAX>
+__global__ void __launch_bounds__(PS_TM)
+k_ps_cholsolve(const PLayer* __restrict__ pl, const PTile* __restrict__ tiles, const double* __restrict__ R,
                const float* P, float scale, float* Ph) {  // P may alias Ph (row-local)
-  __shared__ double Rm[64][65];
-  __shared__ int zero[64];
+  __shared__ double Rm[RMAX][RMAX + 1];
   const PTile tl = tiles[blockIdx.x];
   const PLayer p = pl[tl.ci];
   const int r = p.r;
-  for (int t = threadIdx.x; t < r * r; t += PS_THREADS) Rm[t / r][t % r] = G[p.goff + t];
+  for (int t = threadIdx.x; t < r * r; t += PS_TM) Rm[t / r][t % r] = R[p.goff + t];
   __syncthreads();
-  if (threadIdx.x < 32) {  // one warp: right-looking Cholesky on the upper triangle
-    for (int j = 0; j < r; ++j) {
-      const double gjj = G[p.goff + j * r + j];
-      double d = Rm[j][j];
-      const bool z = !(d > 1e-24 * gjj) || gjj == 0.0;
-      d = z ? 0.0 : sqrt(d);
-      __syncwarp();
-      if (threadIdx.x == 0) { Rm[j][j] = d; zero[j] = z; }
-      __syncwarp();
-      for (int b = j + 1 + threadIdx.x; b < r; b += 32) Rm[j][b] = z ? 0.0 : Rm[j][b] / d;
-      __syncwarp();
-      for (int a = j + 1; a < r; ++a)
-        for (int b = a + threadIdx.x; b < r; b += 32) Rm[a][b] -= Rm[j][a] * Rm[j][b];
-      __syncwarp();
-    }
-  }
-  __syncthreads();
-  const int rows = min(PS_TM, p.m - tl.i0);
-  for (int i = threadIdx.x; i < rows; i += PS_THREADS) {
-    double ph[64];
-    for (int j = 0; j < r; ++j) {
-      double s = (double)__fmul_rn(P[p.poff + (int64_t)j * p.m + tl.i0 + i], scale);
+  const int i = threadIdx.x;
+  if (i >= min(PS_TM, p.m - tl.i0)) return;
+  double ph[RMAX];
+  float pin[RMAX];
+#pragma unroll
+  for (int j = 0; j < RMAX; ++j) pin[j] = (j < r) ? P[p.poff + (int64_t)j * p.m + tl.i0 + i] : 0.f;
+#pragma unroll
+  for (int j = 0; j < RMAX; ++j) {
+    if (j < r) {
+      double s = (double)__fmul_rn(pin[j], scale);
+#pragma unroll
       for (int t = 0; t < j; ++t) s -= ph[t] * Rm[t][j];
-      ph[j] = zero[j] ? 0.0 : s / Rm[j][j];
+      ph[j] = (Rm[j][j] == 0.0) ? 0.0 : s / Rm[j][j];
+    } else {
+      ph[j] = 0.0;
     }
-    for (int j = 0; j < r; ++j) Ph[p.poff + (int64_t)j * p.m + tl.i0 + i] = (float)ph[j];
   }
+#pragma unroll
+  for (int j = 0; j < RMAX; ++j)
+    if (j < r) Ph[p.poff + (int64_t)j * p.m + tl.i0 + i] = (float)ph[j];
 }
 
 // ---------------------------------------------------------------------------
-// profile error from the identity; flags layers that need the direct form
+// profile error, direct: err_r^2 = ||M - P_r Q_r^T||_F^2 in fp64 for every candidate
+// rank r (the first r columns of the r_max run).  The residual is first-order
+// insensitive to errors in the factors (P^T (M - P Q^T) = 0), so tensor-core factors
+// give err_r to ~1e-9, while the identity ||M||^2 - sum ||q_j||^2 would amplify them
+// by (||M|| / err)^2.
+// Element tile = 64 rows x 256 columns: thread = column c (coalesced x loads), its
+// Q row in fp64 registers, the tile's P rows in shared memory (fp64, broadcast).  A
+// running fp64 reconstruction over j; at every candidate boundary j + 1 = r the
+// square of the residual goes to the thread's shared-memory slot of that boundary.
+// Per tile and boundary: fixed-order block sum -> part[tile][slot]; per layer the
+// tiles are summed in order by k_ps_err_final.
 // ---------------------------------------------------------------------------
-__global__ void k_ps_err_identity(const PLayer* __restrict__ pl, int nC, const double* __restrict__ nrm_part,
-                                  const int32_t* __restrict__ tile0, const float* __restrict__ Q,
-                                  const int32_t* __restrict__ ranks, int K, double* __restrict__ err,
-                                  int64_t* __restrict__ bits, double* __restrict__ nrm, int32_t* __restrict__ need_direct) {
-  const int ci = blockIdx.x;
-  if (ci >= nC) return;
-  const PLayer p = pl[ci];
-  __shared__ double qn[64];
-  __shared__ double s_nrm;
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int t = tile0[ci]; t < tile0[ci + 1]; ++t) s += nrm_part[t];
-    s_nrm = s;
-    nrm[ci] = s;
+constexpr int PE_ROWS = 64, PE_COLS = 256, PE_SLOTS = 64;
+
+__device__ __forceinline__ uint64_t ps_boundaries(const PLayer& p, const int32_t* ranks, int K) {
+  uint64_t bm = 0;
+  for (int t = 0; t < K; ++t) {
+    const int r = ranks[t];
+    if (r >= 1 && r <= p.r && (int64_t)r * ((int64_t)p.m + p.k) < (int64_t)p.m * p.k) bm |= 1ull << (r - 1);
   }
-  for (int j = threadIdx.x; j < p.r; j += blockDim.x) {
-    double s = 0.0;
-    for (int c = 0; c < p.k; ++c) {
-      const double v = Q[p.qoff + (int64_t)j * p.k + c];
-      s = fma(v, v, s);
-    }
-    qn[j] = s;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int need = 0;
-    for (int t = 0; t < K; ++t) {
-      const int r = ranks[t];
-      const int64_t m = p.m, k = p.k;
-      if ((int64_t)r * (m + k) >= m * k) {  // lossless-equivalent (R11)
-        err[(int64_t)p.layer * K + t] = 0.0;
-        bits[(int64_t)p.layer * K + t] = 32 * m * k;
-        continue;
-      }
-      double s = 0.0;
-      for (int j = 0; j < r; ++j) s += qn[j];
-      const double e2 = s_nrm - s;
-      const double ev = e2 > 0.0 ? sqrt(e2) : 0.0;
-      err[(int64_t)p.layer * K + t] = ev;  // overwritten by the direct form below
-      bits[(int64_t)p.layer * K + t] = 32 * (int64_t)r * (m + k);
-      need = 1;
-    }
-    need_direct[ci] = need;
-  }
+  return bm;
 }
 
-// direct ||M - P_r Q_r^T||_F^2 for every candidate rank, fp64.  The residual of the
-// reconstruction is first-order insensitive to errors in Q (P^T (M - P Q^T) = 0), so the
-// tensor-core factors give err_r to ~1e-9 here, while the identity
-// ||M||^2 - sum ||q_j||^2 would amplify them by (||M|| / err)^2.
-// One warp walks its elements; at each candidate rank the warp-reduced d^2 goes to a
-// per-warp shared-memory slot; per-block partials are summed in fixed order later.
-constexpr int PS_KMAX = 128;
-__global__ void __launch_bounds__(PS_THREADS)
-k_ps_err_direct(const float* __restrict__ g, const float* __restrict__ e, const PLayer* __restrict__ pl,
-                const PTile* __restrict__ tiles, const float* __restrict__ Ph, const float* __restrict__ Q,
-                const int32_t* __restrict__ ranks, int K, const int32_t* __restrict__ need, double* __restrict__ part) {
-  __shared__ double acc[PS_THREADS / 32][PS_KMAX];
-  __shared__ int32_t srank[PS_KMAX];
+template <int RMAX>
+__global__ void __launch_bounds__(PE_COLS)
+k_ps_err_cols(const float* __restrict__ g, const float* __restrict__ e, const PLayer* __restrict__ pl,
+              const PTile* __restrict__ tiles, const float* __restrict__ Ph, const float* __restrict__ Q,
+              const int32_t* __restrict__ ranks, int K, double* __restrict__ part) {
+  extern __shared__ double s_acc[];  // [nb][PE_COLS]
+  __shared__ double Ps[PE_ROWS][RMAX];
+  __shared__ unsigned long long s_bm;
   const PTile tl = tiles[blockIdx.x];
   const PLayer p = pl[tl.ci];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int t = threadIdx.x; t < PS_KMAX; t += PS_THREADS) {
-    srank[t] = (t < K) ? ranks[t] : 0x7fffffff;
-    for (int w = 0; w < PS_THREADS / 32; ++w) acc[w][t] = 0.0;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_bm = ps_boundaries(p, ranks, K);
+  const int rows = min(PE_ROWS, p.m - tl.i0);
+  for (int t = tid; t < PE_ROWS * RMAX; t += PE_COLS) {
+    const int i = t / RMAX, j = t % RMAX;
+    Ps[i][j] = (i < rows && j < p.r) ? (double)Ph[p.poff + (int64_t)j * p.m + tl.i0 + i] : 0.0;
   }
   __syncthreads();
-  if (need[tl.ci]) {
-    const int rows = min(PS_TM, p.m - tl.i0);
-    const int64_t nel = (int64_t)rows * p.k;
-    for (int64_t base = (int64_t)warp * 32; base < nel; base += PS_THREADS) {
-      const int64_t el = base + lane;
-      const bool valid = el < nel;
-      const int i = tl.i0 + (int)(valid ? el / p.k : 0), c = (int)(valid ? el % p.k : 0);
-      const double x = valid ? (double)xval(g, e, p.moff + (int64_t)i * p.k + c) : 0.0;
+  const uint64_t bm = s_bm;
+  const int nb = __popcll(bm);
+  for (int b = 0; b < nb; ++b) s_acc[b * PE_COLS + tid] = 0.0;
+  const int c = tl.c0 + tid;
+  if (c < p.k) {
+    double qd[RMAX];
+#pragma unroll
+    for (int j = 0; j < RMAX; ++j) qd[j] = (j < p.r) ? (double)Q[p.qoff + (int64_t)j * p.k + c] : 0.0;
+    const float* gx = g + p.moff + (int64_t)tl.i0 * p.k + c;
+    const float* ex = e ? e + p.moff + (int64_t)tl.i0 * p.k + c : nullptr;
+    for (int i = 0; i < rows; ++i) {
+      const double x = (double)canon(__ldg(gx + (int64_t)i * p.k), ex ? __ldg(ex + (int64_t)i * p.k) : 0.f);
       double rec = 0.0;
-      int t = 0;
-      while (t < K && srank[t] <= 0) ++t;
-      for (int j = 0; j < p.r && t < K; ++j) {
-        if (valid) rec = fma((double)Ph[p.poff + (int64_t)j * p.m + i], (double)Q[p.qoff + (int64_t)j * p.k + c], rec);
-        while (t < K && srank[t] == j + 1) {  // candidate t uses the first j+1 columns
-          const double d = valid ? x - rec : 0.0;
-          const double v = warp_sum_d(d * d);
-          if (lane == 0) acc[warp][t] += v;
-          ++t;
+      int b = 0;
+#pragma unroll
+      for (int j = 0; j < RMAX; ++j) {
+        if (j < p.r) {
+          rec = fma(Ps[i][j], qd[j], rec);
+          if ((bm >> j) & 1) {
+            const double d = x - rec;
+            s_acc[b * PE_COLS + tid] = fma(d, d, s_acc[b * PE_COLS + tid]);
+            ++b;
+          }
         }
       }
     }
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < K; t += PS_THREADS) {
-    double s2 = 0.0;
-    for (int w = 0; w < PS_THREADS / 32; ++w) s2 += acc[w][t];
-    part[(int64_t)blockIdx.x * K + t] = s2;
+  for (int b = warp; b < nb; b += PE_COLS / 32) {
+    double v = 0.0;
+#pragma unroll
+    for (int q = 0; q < PE_COLS / 32; ++q) v += s_acc[b * PE_COLS + q * 32 + lane];
+    v = warp_sum_d(v);
+    if (lane == 0) part[(int64_t)blockIdx.x * PE_SLOTS + b] = v;
   }
 }
 
-__global__ void k_ps_err_direct_final(const PLayer* __restrict__ pl, int nC, const int32_t* __restrict__ tile0,
-                                      const int32_t* __restrict__ ranks, int K, const int32_t* __restrict__ need,
-                                      const double* __restrict__ part, double* __restrict__ err) {
+// per layer: bits / lossless rows of the table, then err_r = sqrt(sum over the layer's
+// element tiles of the boundary slot of r); one warp per candidate, lanes stride the
+// tiles, fixed shuffle tree (deterministic)
+__global__ void k_ps_err_final(const PLayer* __restrict__ pl, int nC, const int32_t* __restrict__ tile0,
+                               const int32_t* __restrict__ ranks, int K, const double* __restrict__ part,
+                               double* __restrict__ err, int64_t* __restrict__ bits) {
   const int ci = blockIdx.x;
-  if (ci >= nC || !need[ci]) return;
+  if (ci >= nC) return;
   const PLayer p = pl[ci];
-  for (int t = threadIdx.x; t < K; t += blockDim.x) {
+  const uint64_t bm = ps_boundaries(p, ranks, K);
+  const int lane = threadIdx.x & 31;
+  for (int t = threadIdx.x >> 5; t < K; t += blockDim.x >> 5) {
+    const int r = ranks[t];
     const int64_t m = p.m, k = p.k;
-    if ((int64_t)ranks[t] * (m + k) >= m * k) continue;
+    if ((int64_t)r * (m + k) >= m * k) {  // lossless-equivalent (R11)
+      if (lane == 0) {
+        err[(int64_t)p.layer * K + t] = 0.0;
+        bits[(int64_t)p.layer * K + t] = 32 * m * k;
+      }
+      continue;
+    }
+    const int slot = __popcll(bm & ((1ull << (r - 1)) - 1ull));
     double s = 0.0;
-    for (int b = tile0[ci]; b < tile0[ci + 1]; ++b) s += part[(int64_t)b * K + t];
-    err[(int64_t)p.layer * K + t] = sqrt(s);
+    for (int b = tile0[ci] + lane; b < tile0[ci + 1]; b += 32) s += part[(int64_t)b * PE_SLOTS + slot];
+    s = warp_sum_d(s);
+    if (lane == 0) {
+      err[(int64_t)p.layer * K + t] = sqrt(s);
+      bits[(int64_t)p.layer * K + t] = 32 * (int64_t)r * (m + k);
+    }
   }
 }
 
@@ -392,28 +295,54 @@ __global__ void k_ps_lossless_rows(const DevLayer* __restrict__ layers, int L, i
 }
 
 // ---------------------------------------------------------------------------
-// compress output: out = Phat Q^T, e' = x - out (fused EF), one tile of rows
+// compress output: out = Phat Q^T (fp32, j ascending from 0), e' = x - out (fused EF).
+// Element tile 64 x 256: thread = column (coalesced), its Q row in registers, the
+// tile's Phat rows in shared memory.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(PS_THREADS)
-k_ps_out(const float* __restrict__ g, float* __restrict__ ef, float* __restrict__ out, const PLayer* __restrict__ pl,
-         const PTile* __restrict__ tiles, const float* __restrict__ Ph, const float* __restrict__ Q) {
+template <int RMAX>
+__global__ void __launch_bounds__(PE_COLS)
+k_ps_out_cols(const float* __restrict__ g, float* __restrict__ ef, float* __restrict__ out,
+              const PLayer* __restrict__ pl, const PTile* __restrict__ tiles, const float* __restrict__ Ph,
+              const float* __restrict__ Q) {
+  __shared__ float Ps[PE_ROWS][RMAX];
   const PTile tl = tiles[blockIdx.x];
   const PLayer p = pl[tl.ci];
-  __shared__ float Prow[PS_TM][64];
-  const int rows = min(PS_TM, p.m - tl.i0);
-  for (int t = threadIdx.x; t < PS_TM * 64; t += PS_THREADS) {
-    const int i = t % PS_TM, j = t / PS_TM;
-    Prow[i][j] = (i < rows && j < p.r) ? Ph[p.poff + (int64_t)j * p.m + tl.i0 + i] : 0.f;
+  const int tid = threadIdx.x;
+  const int rows = min(PE_ROWS, p.m - tl.i0);
+  for (int t = tid; t < PE_ROWS * RMAX; t += PE_COLS) {
+    const int i = t / RMAX, j = t % RMAX;
+    Ps[i][j] = (i < rows && j < p.r) ? Ph[p.poff + (int64_t)j * p.m + tl.i0 + i] : 0.f;
   }
   __syncthreads();
-  for (int64_t el = threadIdx.x; el < (int64_t)rows * p.k; el += PS_THREADS) {
-    const int i = (int)(el / p.k), c = (int)(el % p.k);
-    const int64_t idx = p.moff + (int64_t)(tl.i0 + i) * p.k + c;
+  const int c = tl.c0 + tid;
+  if (c >= p.k) return;
+  float qv[RMAX];
+#pragma unroll
+  for (int j = 0; j < RMAX; ++j) qv[j] = (j < p.r) ? Q[p.qoff + (int64_t)j * p.k + c] : 0.f;
+  const int64_t base = p.moff + (int64_t)tl.i0 * p.k + c;
+  for (int i = 0; i < rows; ++i) {
+    const int64_t idx = base + (int64_t)i * p.k;
     float s = 0.f;
-    for (int j = 0; j < p.r; ++j) s = __fmaf_rn(Prow[i][j], Q[p.qoff + (int64_t)j * p.k + c], s);
+#pragma unroll
+    for (int j = 0; j < RMAX; ++j)
+      if (j < p.r) s = __fmaf_rn(Ps[i][j], qv[j], s);
     const float x = canon(__ldg(g + idx), ef ? ef[idx] : 0.f);
     if (out) out[idx] = s;
     if (ef) ef[idx] = __fsub_rn(x, s);
+  }
+}
+
+// P = sum over the K splits of M Q (fixed order)
+__global__ void k_ps_preduce(const PLayer* __restrict__ pl, int nC, const float* __restrict__ part,
+                             float* __restrict__ P) {
+  const int ci = blockIdx.y;
+  if (ci >= nC) return;
+  const PLayer p = pl[ci];
+  const int64_t n = (int64_t)p.m * p.r;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    float s = part[p.poff + t];
+    for (int sp = 1; sp < p.nks; ++sp) s = __fadd_rn(s, part[(int64_t)sp * p.pstride + p.poff + t]);
+    P[p.poff + t] = s;
   }
 }
 
@@ -454,15 +383,6 @@ k_ps_raw_mean(const uint8_t* __restrict__ gathered, int64_t S, int W, float* __r
 // ---------------------------------------------------------------------------
 // launchers
 // ---------------------------------------------------------------------------
-template <int RMAX>
-static void mq_launch(const PsArgs& a, const float* Q, float* P, double* nrm_part, cudaStream_t st) {
-  k_ps_mq<RMAX><<<a.n_rtiles, PS_THREADS, 0, st>>>(a.g, a.e, a.pl, a.rtiles, Q, P, nrm_part);
-}
-template <int RMAX>
-[[maybe_unused]] static void mtp_launch(const PsArgs& a, const float* Ph, float* part, cudaStream_t st) {
-  k_ps_mtp<RMAX><<<a.n_ctiles, PS_THREADS, 0, st>>>(a.g, a.e, a.pl, a.ctiles, Ph, part);
-}
-
 cudaError_t launch_ps_initq(const PsArgs& a, float* Q, uint32_t k0, uint32_t k1, uint32_t step, const int32_t* only,
                             cudaStream_t st) {
   if (a.nC == 0) return cudaSuccess;
@@ -470,25 +390,34 @@ cudaError_t launch_ps_initq(const PsArgs& a, float* Q, uint32_t k0, uint32_t k1,
   return cudaGetLastError();
 }
 
-cudaError_t launch_ps_mq(const PsArgs& a, const float* Q, float* P, double* nrm_part, cudaStream_t st) {
-  if (a.n_rtiles == 0) return cudaSuccess;
-  if (nrm_part) {  // ||M||^2 partials requested: SIMT kernel
-    if (a.rmax <= 16) mq_launch<16>(a, Q, P, nrm_part, st);
-    else if (a.rmax <= 32) mq_launch<32>(a, Q, P, nrm_part, st);
-    else mq_launch<64>(a, Q, P, nrm_part, st);
-    return cudaGetLastError();
-  }
-  return launch_ps_mq_tc(a, a.rt128, a.n_rt128, Q, P, st);
+cudaError_t launch_ps_mq(const PsArgs& a, const float* Q, float* P, float* Ppart, cudaStream_t st) {
+  if (a.n_rt128 == 0) return cudaSuccess;
+  cudaError_t e = launch_ps_mq_tc(a, a.rt128, a.n_rt128, Q, Ppart, st);  // split-K partials
+  if (e != cudaSuccess) return e;
+  return launch_ps_preduce(a, Ppart, P, st);
 }
 
 cudaError_t launch_ps_orth(const PsArgs& a, const float* P, float scale, double* G, float* Ph, cudaStream_t st) {
   if (a.nC == 0) return cudaSuccess;
   // Cholesky-QR twice (CholQR2): the second pass restores orthogonality to round-off
   // when P is ill-conditioned (nearly dependent power-iteration columns)
-  k_ps_gram<<<a.nC, PS_THREADS, 0, st>>>(a.pl, P, scale, G);
-  k_ps_cholsolve<<<a.n_rtiles, PS_THREADS, 0, st>>>(a.pl, a.rtiles, G, P, scale, Ph);
-  k_ps_gram<<<a.nC, PS_THREADS, 0, st>>>(a.pl, Ph, 1.0f, G);
-  k_ps_cholsolve<<<a.n_rtiles, PS_THREADS, 0, st>>>(a.pl, a.rtiles, G, Ph, 1.0f, Ph);
+  const dim3 gg(a.nC, (a.rmax * (a.rmax + 1) / 2 + PS_THREADS / 32 - 1) / (PS_THREADS / 32));
+  auto solve = [&](const float* src, float sc) {
+    if (a.rmax <= 16) {
+      k_ps_chol<16><<<a.nC, 32, 0, st>>>(a.pl, G);
+      k_ps_cholsolve<16><<<a.n_rtiles, PS_TM, 0, st>>>(a.pl, a.rtiles, G, src, sc, Ph);
+    } else if (a.rmax <= 32) {
+      k_ps_chol<32><<<a.nC, 32, 0, st>>>(a.pl, G);
+      k_ps_cholsolve<32><<<a.n_rtiles, PS_TM, 0, st>>>(a.pl, a.rtiles, G, src, sc, Ph);
+    } else {
+      k_ps_chol<64><<<a.nC, 32, 0, st>>>(a.pl, G);
+      k_ps_cholsolve<64><<<a.n_rtiles, PS_TM, 0, st>>>(a.pl, a.rtiles, G, src, sc, Ph);
+    }
+  };
+  k_ps_gram<<<gg, PS_THREADS, 0, st>>>(a.pl, P, scale, G);
+  solve(P, scale);
+  k_ps_gram<<<gg, PS_THREADS, 0, st>>>(a.pl, Ph, 1.0f, G);
+  solve(Ph, 1.0f);
   return cudaGetLastError();
 }
 
@@ -506,14 +435,26 @@ cudaError_t launch_ps_mtp_scale(const PsArgs& a, const float* src, float* dst, f
   return cudaGetLastError();
 }
 
-cudaError_t launch_ps_err(const PsArgs& a, const double* nrm_part, const int32_t* rtile0, const float* Ph,
-                          const float* Q, const int32_t* ranks, int K, double* err, int64_t* bits, double* nrm,
-                          int32_t* need, double* dpart, cudaStream_t st) {
+cudaError_t launch_ps_err(const PsArgs& a, const float* Ph, const float* Q, const int32_t* ranks, int K, int nbmax,
+                          double* err, int64_t* bits, double* epart, cudaStream_t st) {
   if (a.nC == 0) return cudaSuccess;
-  k_ps_err_identity<<<a.nC, 64, 0, st>>>(a.pl, a.nC, nrm_part, rtile0, Q, ranks, K, err, bits, nrm, need);
-  if (K > PS_KMAX) return cudaErrorInvalidValue;
-  k_ps_err_direct<<<a.n_rtiles, PS_THREADS, 0, st>>>(a.g, a.e, a.pl, a.rtiles, Ph, Q, ranks, K, need, dpart);
-  k_ps_err_direct_final<<<a.nC, 128, 0, st>>>(a.pl, a.nC, rtile0, ranks, K, need, dpart, err);
+  if (nbmax < 1 || nbmax > PE_SLOTS) return cudaErrorInvalidValue;
+  if (a.n_etiles > 0) {
+    const size_t smem = sizeof(double) * nbmax * PE_COLS;  // one slot per distinct candidate rank
+    cudaError_t e = cudaSuccess;
+    if (a.rmax <= 16) {
+      e = cudaFuncSetAttribute(k_ps_err_cols<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      k_ps_err_cols<16><<<a.n_etiles, PE_COLS, smem, st>>>(a.g, a.e, a.pl, a.etiles, Ph, Q, ranks, K, epart);
+    } else if (a.rmax <= 32) {
+      e = cudaFuncSetAttribute(k_ps_err_cols<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      k_ps_err_cols<32><<<a.n_etiles, PE_COLS, smem, st>>>(a.g, a.e, a.pl, a.etiles, Ph, Q, ranks, K, epart);
+    } else {
+      e = cudaFuncSetAttribute(k_ps_err_cols<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      k_ps_err_cols<64><<<a.n_etiles, PE_COLS, smem, st>>>(a.g, a.e, a.pl, a.etiles, Ph, Q, ranks, K, epart);
+    }
+    if (e != cudaSuccess) return e;
+  }
+  k_ps_err_final<<<a.nC, 256, 0, st>>>(a.pl, a.nC, a.etile0, ranks, K, epart, err, bits);
   return cudaGetLastError();
 }
 
@@ -524,8 +465,16 @@ cudaError_t launch_ps_lossless_rows(const DevLayer* layers, int L, int K, const 
 }
 
 cudaError_t launch_ps_out(const PsArgs& a, float* ef, float* out, const float* Ph, const float* Q, cudaStream_t st) {
-  if (a.n_rtiles == 0) return cudaSuccess;
-  k_ps_out<<<a.n_rtiles, PS_THREADS, 0, st>>>(a.g, ef, out, a.pl, a.rtiles, Ph, Q);
+  if (a.n_etiles == 0) return cudaSuccess;
+  if (a.rmax <= 16) k_ps_out_cols<16><<<a.n_etiles, PE_COLS, 0, st>>>(a.g, ef, out, a.pl, a.etiles, Ph, Q);
+  else if (a.rmax <= 32) k_ps_out_cols<32><<<a.n_etiles, PE_COLS, 0, st>>>(a.g, ef, out, a.pl, a.etiles, Ph, Q);
+  else k_ps_out_cols<64><<<a.n_etiles, PE_COLS, 0, st>>>(a.g, ef, out, a.pl, a.etiles, Ph, Q);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ps_preduce(const PsArgs& a, const float* part, float* P, cudaStream_t st) {
+  if (a.nC == 0) return cudaSuccess;
+  k_ps_preduce<<<dim3(16, a.nC), 256, 0, st>>>(a.pl, a.nC, part, P);
   return cudaGetLastError();
 }
 

@@ -18,6 +18,8 @@
 // tile rows -> column-major P.
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -25,7 +27,7 @@ namespace lg {
 
 constexpr int TC_M = 128;      // rows per tile (UMMA_M)
 constexpr int TC_KT = 32;      // K elements per stage (one 128-byte swizzle row)
-constexpr int TC_THREADS = 128;
+constexpr int TC_THREADS = 256;  // 8 warps: warps w and w+4 share TMEM lanes 32*(w%4), split columns
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -83,33 +85,77 @@ __device__ __forceinline__ void put_chunk(uint8_t* hi_tile, uint8_t* lo_tile, in
                  __float_as_uint(__fsub_rn(v.z, __uint_as_float(h2))), __float_as_uint(__fsub_rn(v.w, __uint_as_float(h3))));
 }
 
+// async global -> shared copies (LDGSTS): 16 bytes (zero-filled past src_bytes) or 4 bytes
+__device__ __forceinline__ void cp16(void* dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp4(void* dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+
 // NP: N padded to a multiple of 16 (16, 32, 64); grouped over layers.
-// TRANS = false: P = M Q   -- tile = 128 rows of M, K runs over the k columns,
-//                             A = M rows (K-major), B = Q columns, out P[j*m + i]
+// TRANS = false: P = M Q   -- tile = 128 rows of M, K runs over the columns [c0, i1) of
+//                             split `split` (split-K: enough CTAs to cover the SMs),
+//                             A = M rows (K-major), B = Q columns,
+//                             out partial[split][j*m + i] (summed by k_ps_preduce)
 // TRANS = true:  Q = M^T P -- tile = 128 columns of M, K runs over rows [i0, i1),
 //                             A = M^T, transposed while staged from M rows (K-major),
 //                             B = P columns, out partial[split][j*k + c]
+// Pipeline: the raw g, e and B slices of K tiles kt+1 .. kt+RS-1 are in flight (cp.async,
+// RS-stage ring) while tile kt is converted (x = canon(g + e), hi/lo split, swizzle)
+// into the A/B operand stage (kt & 1) and tile kt - 1's MMAs run.
+
+template <int NP, bool TRANS>
+struct TcSmem {
+  static constexpr int RAW_X = TC_M * TC_KT * 4;     // 16 KB: 128 x 32 floats of g (or e)
+  static constexpr int RAW_B = NP * TC_KT * 4;       // NP x 32 floats of Q (or P)
+  static constexpr int RAW = 2 * RAW_X + RAW_B;
+  static constexpr int A_BYTES = TC_M * 128;         // 16 KB per A tile (hi or lo)
+  static constexpr int B_BYTES = NP * 128;           // per B tile (hi or lo)
+  static constexpr int OPS = 2 * A_BYTES + 2 * B_BYTES;
+  static constexpr int RS = (2 * OPS + 4 * RAW + 1024 <= 220 * 1024) ? 4 : 3;  // raw ring stages (RS-1 in flight)
+  static constexpr int TOTAL = 2 * OPS + RS * RAW + 1024;
+};
+
+// Persistent: gridDim.x CTAs (<= one per SM) walk the tiles t = blockIdx.x + q*gridDim.x;
+// the (tile, K tile) steps of a CTA form one continuous pipeline, so the copies of the
+// next tile are in flight while the last K tiles of the current one are multiplied.
 template <int NP, bool TRANS>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 k_ps_tc(const float* __restrict__ g, const float* __restrict__ e, const PLayer* __restrict__ pl,
-        const PTile* __restrict__ tiles, const float* __restrict__ Bsrc, float* __restrict__ out) {
-  constexpr int A_BYTES = TC_M * 128;        // 16 KB per A tile (hi or lo)
-  constexpr int B_BYTES = NP * 128;          // per B tile (hi or lo)
-  constexpr int STAGE = 2 * A_BYTES + 2 * B_BYTES;
+        const PTile* __restrict__ tiles, int ntiles, const float* __restrict__ Bsrc, float* __restrict__ out) {
+  using SM = TcSmem<NP, TRANS>;
   constexpr uint32_t TMEM_COLS = 2 * NP < 32 ? 32 : 2 * NP;  // two accumulator buffers
   extern __shared__ __align__(1024) uint8_t smem_dyn[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_dyn) + 1023) & ~(uintptr_t)1023);
+  // 1024-byte aligned base, as an offset from the shared array (keeps the shared
+  // address space: LDS/STS rather than generic LD/ST)
+  uint8_t* smem = smem_dyn + ((1024u - (smem_u32(smem_dyn) & 1023u)) & 1023u);
+  uint8_t* raw0 = smem + 2 * SM::OPS;
   __shared__ uint64_t mma_done[2];
   __shared__ uint32_t tmem_base_sh;
-
-  const PTile tl = tiles[blockIdx.x];
-  const PLayer p = pl[tl.ci];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  // tile extent along the MMA M dimension, and the K range
-  const int rows = TRANS ? min(TC_M, p.k - tl.c0) : min(TC_M, p.m - tl.i0);
-  const int kbeg = TRANS ? tl.i0 : 0;
-  const int kend = TRANS ? tl.i1 : p.k;
-  const int nk = (kend - kbeg + TC_KT - 1) / TC_KT;
+
+  // tile geometry: rows along the MMA M dimension, K range [kbeg, kend)
+  struct TileG {
+    PTile tl;
+    PLayer p;
+    int rows, kbeg, kend, nk;
+  };
+  auto geo = [&](int t) {
+    TileG G;
+    G.tl = tiles[t];
+    G.p = pl[G.tl.ci];
+    G.rows = TRANS ? min(TC_M, G.p.k - G.tl.c0) : min(TC_M, G.p.m - G.tl.i0);
+    G.kbeg = TRANS ? G.tl.i0 : G.tl.c0;
+    G.kend = G.tl.i1;
+    G.nk = (G.kend - G.kbeg + TC_KT - 1) / TC_KT;
+    return G;
+  };
+  int nsteps = 0;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) nsteps += geo(t).nk;
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
@@ -121,91 +167,164 @@ k_ps_tc(const float* __restrict__ g, const float* __restrict__ e, const PLayer* 
     mbar_init(&mma_done[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
+
+  constexpr int TC_RS = SM::RS;
+  // issue cursor: the raw copies of step s (tile ti, K tile kti) into ring slot s % TC_RS
+  int ti = blockIdx.x, kti = 0;
+  TileG gi = geo(min(ti, ntiles - 1));
+  auto issue = [&](int step) {
+    uint8_t* rg = raw0 + (step % TC_RS) * SM::RAW;
+    uint8_t* re = rg + SM::RAW_X;
+    uint8_t* rb = re + SM::RAW_X;
+    const PLayer& p = gi.p;
+    const PTile& tl = gi.tl;
+    const int k0 = gi.kbeg + kti * TC_KT, kend = gi.kend, rows = gi.rows;
+    const bool a16 = ((p.moff & 3) == 0) && ((p.k & 3) == 0);
+    const int64_t bld = TRANS ? (int64_t)p.m : (int64_t)p.k;  // column length of Bsrc
+    const int64_t boff = TRANS ? p.poff : p.qoff;
+    const bool b16 = ((boff & 3) == 0) && ((bld & 3) == 0);
+    // X: 128 x 32 floats as 1024 16-byte chunks; MQ: [row][kchunk], MtP: [krow][cchunk]
+#pragma unroll
+    for (int it = 0; it < TC_M * TC_KT / 4 / TC_THREADS; ++it) {
+      const int idx = it * TC_THREADS + tid;
+      int64_t xi;  // flat element index of the chunk's first element
+      int nval;    // valid elements in the chunk
+      if (!TRANS) {
+        const int r_ = idx >> 3, ch = idx & 7, col = k0 + ch * 4;
+        nval = (r_ < rows) ? max(0, min(4, kend - col)) : 0;
+        xi = p.moff + (int64_t)(tl.i0 + min(r_, rows - 1)) * p.k + col;
+      } else {
+        const int kr = idx >> 5, cq = idx & 31, i = k0 + kr, c = tl.c0 + cq * 4;
+        nval = (i < kend) ? max(0, min(4, tl.c0 + rows - c)) : 0;
+        xi = p.moff + (int64_t)min(i, kend - 1) * p.k + c;
+      }
+      // raw slot: MQ chunk idx; MtP chunk (kr, cq) at cq*32 + (kr ^ cq) (XOR swizzle: the
+      // copies along cq and the transposing reads along kr are both conflict-free)
+      const int slot = TRANS ? ((idx & 31) * 32 + ((idx >> 5) ^ (idx & 31))) : idx;
+      if (a16) {
+        cp16(rg + slot * 16, g + xi, 4 * nval);
+        if (e) cp16(re + slot * 16, e + xi, 4 * nval);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          cp4(rg + slot * 16 + 4 * q, g + xi + (q < nval ? q : 0), q < nval ? 4 : 0);
+          if (e) cp4(re + slot * 16 + 4 * q, e + xi + (q < nval ? q : 0), q < nval ? 4 : 0);
+        }
+      }
+    }
+    // B: NP columns x 32 K elements as NP*8 chunks [j][kchunk]
+    for (int idx = tid; idx < NP * 8; idx += TC_THREADS) {
+      const int j = idx >> 3, ch = idx & 7, col = k0 + ch * 4;
+      const int nval = (j < p.r) ? max(0, min(4, kend - col)) : 0;
+      const float* src = Bsrc + boff + (int64_t)min(j, p.r - 1) * bld + col;
+      if (b16) {
+        cp16(rb + idx * 16, src, 4 * nval);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) cp4(rb + idx * 16 + 4 * q, src + (q < nval ? q : 0), q < nval ? 4 : 0);
+      }
+    }
+    if (++kti >= gi.nk) {
+      kti = 0;
+      ti += gridDim.x;
+      if (ti < ntiles) gi = geo(ti);
+    }
+  };
+
+  // prologue: steps 0 .. RS-2 in flight (one commit group per step, empty ones too)
+#pragma unroll
+  for (int s = 0; s < TC_RS - 1; ++s) {
+    if (s < nsteps) issue(s);
+    cp_commit();
+  }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem_d = tmem_base_sh;
   constexpr uint32_t idesc = tf32_idesc(NP);
 
-  const int row = warp * 32 + lane;
-  float acc[NP];
+  // accumulator rows = TMEM lanes 32*(warp%4) + lane; columns [half*NP/2, half*NP/2 + NP/2)
+  constexpr int NH = NP / 2;
+  const int row = (warp & 3) * 32 + lane, half = warp >> 2;
+  float acc[NH];
 #pragma unroll
-  for (int j = 0; j < NP; ++j) acc[j] = 0.f;
-  // read the finished tile partial of K tile `t` (TMEM buffer t & 1) and add it (fp32 RN)
+  for (int j = 0; j < NH; ++j) acc[j] = 0.f;
+  // drain cursor: step s-1 belongs to tile td, K tile ktd
+  int td = blockIdx.x, ktd = 0, nkd = (td < ntiles) ? geo(td).nk : 0;
+  // add the finished partial of step t (TMEM buffer t & 1); at the tile's last K tile
+  // write the tile's output and restart the accumulator
   auto drain = [&](int t) {
     mbar_wait(&mma_done[t & 1], (t >> 1) & 1);
     asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
-    for (int j0 = 0; j0 < NP; j0 += 16) {
-      uint32_t v[16];
-      const uint32_t taddr = tmem_d + ((uint32_t)(warp * 32) << 16) + (uint32_t)((t & 1) * NP + j0);
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-          : "r"(taddr));
+    for (int j0 = 0; j0 < NH; j0 += 8) {
+      uint32_t v[8];
+      const uint32_t taddr =
+          tmem_d + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)((t & 1) * NP + half * NH + j0);
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                   : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                   : "r"(taddr));
       asm volatile("tcgen05.wait::ld.sync.aligned;");
 #pragma unroll
-      for (int q = 0; q < 16; ++q) acc[j0 + q] = __fadd_rn(acc[j0 + q], __uint_as_float(v[q]));
+      for (int q = 0; q < 8; ++q) acc[j0 + q] = __fadd_rn(acc[j0 + q], __uint_as_float(v[q]));
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
+    if (++ktd >= nkd) {
+      const TileG G = geo(td);
+      if (row < G.rows) {
+        if (!TRANS) {
+          float* o = out + (int64_t)G.tl.split * G.p.pstride + G.p.poff;
+#pragma unroll
+          for (int q = 0; q < NH; ++q) {
+            const int j = half * NH + q;
+            if (j < G.p.r) o[(int64_t)j * G.p.m + G.tl.i0 + row] = acc[q];
+          }
+        } else {
+          float* o = out + (int64_t)G.tl.split * G.p.qstride + G.p.qoff;
+#pragma unroll
+          for (int q = 0; q < NH; ++q) {
+            const int j = half * NH + q;
+            if (j < G.p.r) o[(int64_t)j * G.p.k + G.tl.c0 + row] = acc[q];
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < NH; ++j) acc[j] = 0.f;
+      ktd = 0;
+      td += gridDim.x;
+      nkd = (td < ntiles) ? geo(td).nk : 0;
+    }
   };
 
-  for (int kt = 0; kt < nk; ++kt) {
-    const int s = kt & 1;
-    uint8_t* Ah = smem + s * STAGE;
-    uint8_t* Al = Ah + A_BYTES;
-    uint8_t* Bh = Al + A_BYTES;
-    uint8_t* Bl = Bh + B_BYTES;
-    const int k0 = kbeg + kt * TC_KT;
-    if (!TRANS) {
-      // A: 128 rows x 8 chunks; a warp covers 4 rows x 128 B per instruction (coalesced)
-#pragma unroll 4
-      for (int it = 0; it < TC_M * 8 / TC_THREADS; ++it) {
-        const int idx = it * TC_THREADS + tid;
-        const int r_ = idx >> 3, ch = idx & 7;
-        const int col = k0 + ch * 4;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (r_ < rows) {
-          const int64_t base = p.moff + (int64_t)(tl.i0 + r_) * p.k + col;
-          if (col + 4 <= kend && ((base & 3) == 0)) {
-            const float4 a = __ldg(reinterpret_cast<const float4*>(g + base));
-            const float4 b = e ? __ldg(reinterpret_cast<const float4*>(e + base)) : make_float4(0.f, 0.f, 0.f, 0.f);
-            v = make_float4(canon(a.x, b.x), canon(a.y, b.y), canon(a.z, b.z), canon(a.w, b.w));
-          } else {
-            float t[4];
+  for (int s = 0; s < nsteps; ++s) {
+    // keep TC_RS - 1 steps in flight; wait for step s (this thread's copies), then a
+    // barrier makes every thread's copies of step s visible
+    if (s + TC_RS - 1 < nsteps) issue(s + TC_RS - 1);
+    cp_commit();
+    cp_wait<TC_RS - 1>();
+    __syncthreads();
+    const uint8_t* rg = raw0 + (s % TC_RS) * SM::RAW;
+    const uint8_t* re = rg + SM::RAW_X;
+    const uint8_t* rb = re + SM::RAW_X;
+    const int sb = s & 1;
+    uint8_t* Ah = smem + sb * SM::OPS;
+    uint8_t* Al = Ah + SM::A_BYTES;
+    uint8_t* Bh = Al + SM::A_BYTES;
+    uint8_t* Bl = Bh + SM::B_BYTES;
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-              t[q] = (col + q < kend) ? canon(__ldg(g + base + q), e ? __ldg(e + base + q) : 0.f) : 0.f;
-            v = make_float4(t[0], t[1], t[2], t[3]);
-          }
-        }
-        put_chunk(Ah, Al, r_, ch, v);
-      }
-    } else {
-      // A^T: 32 K-rows (rows i of M) x 128 M-elements (columns c), MN-major:
-      // offset = (c/32)*4096 + (kr/8)*1024 + (kr%8)*128 + (((c%32)/4) ^ (kr%8))*16
-#pragma unroll 4
-      for (int it = 0; it < TC_KT * 32 / TC_THREADS; ++it) {
-        const int idx = it * TC_THREADS + tid;
-        const int kr = idx >> 5, cq = idx & 31;  // K row, 16-byte chunk along c (4 columns)
-        const int i = k0 + kr, c = tl.c0 + cq * 4;
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (i < kend) {
-          const int64_t base = p.moff + (int64_t)i * p.k + c;
-          if (c + 4 <= tl.c0 + rows && ((base & 3) == 0)) {
-            const float4 a = __ldg(reinterpret_cast<const float4*>(g + base));
-            const float4 b = e ? __ldg(reinterpret_cast<const float4*>(e + base)) : make_float4(0.f, 0.f, 0.f, 0.f);
-            v = make_float4(canon(a.x, b.x), canon(a.y, b.y), canon(a.z, b.z), canon(a.w, b.w));
-          } else {
-            float t[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              t[q] = (c + q < tl.c0 + rows) ? canon(__ldg(g + base + q), e ? __ldg(e + base + q) : 0.f) : 0.f;
-            v = make_float4(t[0], t[1], t[2], t[3]);
-          }
-        }
-        // transpose into the K-major A tile: A row = column c (local cq*4 + q), K = kr.
+    for (int it = 0; it < TC_M * TC_KT / 4 / TC_THREADS; ++it) {
+      const int idx = it * TC_THREADS + tid;
+      // MtP: lanes walk kr (K rows) for one cq, so the transposed 4-byte stores below
+      // hit 32 distinct banks
+      const int kr = idx & 31, cq = idx >> 5;
+      const int slot = TRANS ? (cq * 32 + (kr ^ cq)) : idx;
+      const float4 a = *reinterpret_cast<const float4*>(rg + slot * 16);
+      const float4 b = e ? *reinterpret_cast<const float4*>(re + slot * 16) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 v = make_float4(canon(a.x, b.x), canon(a.y, b.y), canon(a.z, b.z), canon(a.w, b.w));
+      if (!TRANS) {
+        put_chunk(Ah, Al, idx >> 3, idx & 7, v);
+      } else {
+        // transpose into the K-major A tile: A row = column (local cq*4 + q), K = kr.
         // (tcgen05 kind::tf32 does not take an MN-major A here: measured all-zero D.)
         const float vv[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
@@ -218,27 +337,14 @@ k_ps_tc(const float* __restrict__ g, const float* __restrict__ e, const PLayer* 
         }
       }
     }
-    // B: NP rows (columns j of Q, resp. of P) x 8 chunks along K
-    {
-      const int64_t bld = TRANS ? (int64_t)p.m : (int64_t)p.k;   // column length of Bsrc
-      const int64_t boff = TRANS ? p.poff : p.qoff;
-      for (int idx = tid; idx < NP * 8; idx += TC_THREADS) {
-        const int j = idx >> 3, ch = idx & 7;
-        const int col = k0 + ch * 4;
-        float t[4] = {0.f, 0.f, 0.f, 0.f};
-        if (j < p.r) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) t[q] = (col + q < kend) ? Bsrc[boff + (int64_t)j * bld + col + q] : 0.f;
-        }
-        put_chunk(Bh, Bl, j, ch, make_float4(t[0], t[1], t[2], t[3]));
-      }
-    }
+    for (int idx = tid; idx < NP * 8; idx += TC_THREADS)
+      put_chunk(Bh, Bl, idx >> 3, idx & 7, *reinterpret_cast<const float4*>(rb + idx * 16));
     asm volatile("fence.proxy.async.shared::cta;");
     __syncthreads();
     if (tid == 0) {
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t sAh = smem_u32(Ah), sAl = smem_u32(Al), sBh = smem_u32(Bh), sBl = smem_u32(Bl);
-      const uint32_t dbuf = tmem_d + (uint32_t)(s * NP);
+      const uint32_t dbuf = tmem_d + (uint32_t)(sb * NP);
 #pragma unroll
       for (int kk = 0; kk < TC_KT / 8; ++kk) {
         const uint32_t koff = kk * 32;  // 8 tf32 = 32 bytes along K inside the swizzle row
@@ -248,26 +354,15 @@ k_ps_tc(const float* __restrict__ g, const float* __restrict__ e, const PLayer* 
         mma_tf32(dbuf, dAh, sw128_desc(sBl + koff), idesc, 1u);
         mma_tf32(dbuf, dAl, sw128_desc(sBh + koff), idesc, 1u);
       }
-      mma_commit(&mma_done[s]);
+      mma_commit(&mma_done[sb]);
     }
     __syncwarp();
-    // while tile kt's MMAs run: drain tile kt-1 (this also frees smem stage s^1 and
-    // TMEM buffer s^1 for tile kt+1)
-    if (kt >= 1) drain(kt - 1);
+    // while step s's MMAs run: drain step s-1 (this also frees operand stage s^1 and
+    // TMEM buffer s^1 for step s+1)
+    if (s >= 1) drain(s - 1);
   }
-  drain(nk - 1);
-  if (row < rows) {
-    if (!TRANS) {
-#pragma unroll
-      for (int j = 0; j < NP; ++j)
-        if (j < p.r) out[p.poff + (int64_t)j * p.m + tl.i0 + row] = acc[j];
-    } else {
-      float* o = out + (int64_t)tl.split * p.qstride + p.qoff;
-#pragma unroll
-      for (int j = 0; j < NP; ++j)
-        if (j < p.r) o[(int64_t)j * p.k + tl.c0 + row] = acc[j];
-    }
-  }
+  cp_wait<0>();
+  if (nsteps > 0) drain(nsteps - 1);
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (warp == 0)
@@ -277,11 +372,17 @@ k_ps_tc(const float* __restrict__ g, const float* __restrict__ e, const PLayer* 
 template <int NP, bool TRANS>
 static cudaError_t tc_launch(const PsArgs& a, const PTile* tiles, int ntiles, const float* B, float* out,
                              cudaStream_t st) {
-  constexpr int STAGE = 2 * TC_M * 128 + 2 * NP * 128;
-  const int smem = 2 * STAGE + 1024;
+  const int smem = TcSmem<NP, TRANS>::TOTAL;
   cudaError_t e = cudaFuncSetAttribute(k_ps_tc<NP, TRANS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  k_ps_tc<NP, TRANS><<<ntiles, TC_THREADS, smem, st>>>(a.g, a.e, a.pl, tiles, B, out);
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (nsm <= 0) nsm = 148;
+  }
+  k_ps_tc<NP, TRANS><<<std::min(ntiles, nsm), TC_THREADS, smem, st>>>(a.g, a.e, a.pl, tiles, ntiles, B, out);
   return cudaGetLastError();
 }
 
