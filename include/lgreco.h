@@ -106,6 +106,17 @@ int lgreco_ctx_check(lgreco_ctx* ctx, void* stream);
 /* Number of kernels this ctx has launched (evidence counter). */
 int64_t lgreco_ctx_launches(lgreco_ctx* ctx);
 
+/* Measurement hook (bench.py roofline): while enabled (enable != 0), every
+ * lgreco_profile call of a QSGD ctx records a CUDA event pair on its stream
+ * immediately around the K1 launch (k_qprofile, the dominant kernel).  Costs one
+ * event pair per call; off by default.  Returns LGRECO_EINVAL for a null ctx. */
+int lgreco_ctx_timing(lgreco_ctx* ctx, int32_t enable);
+
+/* Synchronises the recorded event pairs, writes their summed elapsed time (ms) to
+ * *total_ms and their number to *count, then releases them.  LGRECO_ECUDA if an
+ * event failed (the sum then covers the others). */
+int lgreco_ctx_kernel_ms(lgreco_ctx* ctx, double* total_ms, int64_t* count);
+
 /* (a2-a4) Profile: for every layer l and candidate j, d_err[l*K+j] = the L2 norm of
  * x_l - decompress(compress(x_l, c^j)) and d_bits[l*K+j] = its transmitted size in
  * bits ("simulate the compression/decompression ... without

@@ -285,6 +285,32 @@ int lgreco_ctx_check(lgreco_ctx* c, void* stream) {
 
 int64_t lgreco_ctx_launches(lgreco_ctx* c) { return c ? c->launches : -1; }
 
+int lgreco_ctx_timing(lgreco_ctx* c, int32_t enable) {
+  if (!c) { lg_set_error("null ctx"); return LGRECO_EINVAL; }
+  c->timing = enable != 0;
+  return LGRECO_OK;
+}
+
+int lgreco_ctx_kernel_ms(lgreco_ctx* c, double* total_ms, int64_t* count) {
+  if (!c || !total_ms || !count) { lg_set_error("null argument"); return LGRECO_EINVAL; }
+  double t = 0.0;
+  int rc = LGRECO_OK;
+  for (auto& pr : c->tev) {
+    float ms = 0.f;
+    if (cudaEventSynchronize(pr.second) != cudaSuccess || cudaEventElapsedTime(&ms, pr.first, pr.second) != cudaSuccess) {
+      lg_set_error("kernel timing event: %s", cudaGetErrorString(cudaGetLastError()));
+      rc = LGRECO_ECUDA;
+    }
+    t += ms;
+    cudaEventDestroy(pr.first);
+    cudaEventDestroy(pr.second);
+  }
+  *total_ms = t;
+  *count = (int64_t)c->tev.size();
+  c->tev.clear();
+  return rc;
+}
+
 int lgreco_profile(lgreco_ctx* c, const float* d_g, const float* d_ef, uint64_t step, double* d_err,
                    int64_t* d_bits, void* stream) {
   if (!c || !d_g || !d_err || !d_bits) { lg_set_error("null argument"); return LGRECO_EINVAL; }
@@ -295,6 +321,14 @@ int lgreco_profile(lgreco_ctx* c, const float* d_g, const float* d_ef, uint64_t 
     lg::QProfileArgs a{d_g, d_ef, c->d_layers, c->L, c->d_chunks, c->nchunks, c->d_layer_chunk0,
                        c->B, c->cs, c->d_params, c->K, k0, k1, (uint32_t)c->rank, (uint32_t)step,
                        c->d_partial, d_err, d_bits};
+    if (c->timing && c->nchunks > 0) {
+      cudaEvent_t e0, e1;
+      LG_CUDA(cudaEventCreate(&e0));
+      LG_CUDA(cudaEventCreate(&e1));
+      c->tev.emplace_back(e0, e1);
+      a.ev0 = e0;
+      a.ev1 = e1;
+    }
     LG_LAUNCH(c, lg::launch_qprofile(a, st));
     c->launches += (c->nchunks > 0) + 1;
     return LGRECO_OK;

@@ -41,6 +41,9 @@ struct lgreco_ctx {
   std::vector<int64_t> bucket0;  // L+1
   int64_t N = 0, R = 0;
   int64_t launches = 0;
+  // optional per-launch CUDA events around the family's dominant profile kernel
+  bool timing = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tev;
   // device tables
   lg::DevLayer* d_layers = nullptr;
   int64_t* d_bucket0 = nullptr;

@@ -22,6 +22,7 @@ struct QProfileArgs {
   int B; CandS cs; const int32_t* params; int K;
   uint32_t k0, k1, rankfield, step;
   double* partial; double* err; int64_t* bits;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // when set: recorded around the K1 launch
 };
 
 struct QPackArgs {

@@ -577,6 +577,7 @@ __global__ void k_philox(const uint32_t* __restrict__ ctr, uint32_t k0, uint32_t
 // ---------------------------------------------------------------------------
 cudaError_t launch_qprofile(const QProfileArgs& a, cudaStream_t st) {
   if (a.nchunks > 0) {
+    if (a.ev0) cudaEventRecord(a.ev0, st);
 #define LG_QP(KT)                                                                          \
   k_qprofile<KT><<<a.nchunks, QP_THREADS, 0, st>>>(a.g, a.e, a.layers, a.chunks, a.B, a.cs, a.K, \
                                                     a.k0, a.k1, a.rankfield, a.step, a.partial)
@@ -591,6 +592,7 @@ cudaError_t launch_qprofile(const QProfileArgs& a, cudaStream_t st) {
         else LG_QP(16);
     }
 #undef LG_QP
+    if (a.ev1) cudaEventRecord(a.ev1, st);
   }
   k_qprofile_reduce<<<a.L, 256, 0, st>>>(a.layers, a.layer_chunk0, a.partial, a.params, a.K, a.B, a.err, a.bits);
   return cudaGetLastError();

@@ -53,6 +53,8 @@ _SIGS = {
     "lgreco_ctx_destroy": (None, [_VP]),
     "lgreco_ctx_check": (C.c_int, [_VP, _VP]),
     "lgreco_ctx_launches": (_I64, [_VP]),
+    "lgreco_ctx_timing": (_I32, [_VP, _I32]),
+    "lgreco_ctx_kernel_ms": (_I32, [_VP, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     "lgreco_profile": (C.c_int, [_VP, _VP, _VP, _U64, _VP, _VP, _VP]),
     "lgreco_solve_workspace_bytes": (C.c_size_t, [_I32, _I32, _I32]),
     "lgreco_solve": (C.c_int, [_VP, _VP, _I32, _I32, _VP, _VP, _I32, _U32, _VP, _VP, _VP, C.c_size_t, _VP]),
@@ -178,6 +180,16 @@ class Context:
 
     def launches(self) -> int:
         return int(lib().lgreco_ctx_launches(self.h))
+
+    def timing(self, enable=True):
+        """Record CUDA events around the dominant profile kernel (QSGD K1) per call."""
+        _check(lib().lgreco_ctx_timing(self.h, 1 if enable else 0), "timing")
+
+    def kernel_ms(self):
+        """(total ms, launches) of the recorded dominant-kernel launches; clears them."""
+        t, n = C.c_double(0.0), C.c_int64(0)
+        _check(lib().lgreco_ctx_kernel_ms(self.h, C.byref(t), C.byref(n)), "kernel_ms")
+        return t.value, n.value
 
     # ---- stages ----------------------------------------------------------------
     def payload_bytes(self, choice) -> int:

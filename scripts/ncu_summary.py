@@ -76,19 +76,27 @@ def main():
                     f"{int(d.get('inst_executed', 0))} | {int(d.get('registers', 0))} | "
                     f"{', '.join(f'{k} {v}' for k, v in d['top_stalls'].items())} |\n")
     if len(sys.argv) > 3:  # launch list -> per-kernel share of device time
-        tot, per = 0.0, {}
-        for r in csv.DictReader(open(sys.argv[3])):
+        lines = open(sys.argv[3]).read().splitlines()
+        start = next(i for i, l in enumerate(lines) if l.startswith('"ID"'))
+        tot, ours, per, cnt = 0.0, 0.0, {}, {}
+        for r in csv.DictReader(io.StringIO("\n".join(lines[start:]))):
             if r.get("Metric Name") != "gpu__time_duration.sum":
                 continue
             name = r["Kernel Name"].split("(")[0]
             v = float(r["Metric Value"].replace(",", ""))
             per[name] = per.get(name, 0.0) + v
+            cnt[name] = cnt.get(name, 0) + 1
             tot += v
+            if "lg::" in name:
+                ours += v
         with open(out + "_launches.md", "w") as f:
-            f.write("Launch list (ncu gpu__time_duration.sum, --clock-control none; cold-cache, serialised: "
-                    "compare shares, not absolutes)\n\n| kernel | total ns | share |\n|---|---|---|\n")
+            f.write("Launch list (ncu --metrics gpu__time_duration.sum --clock-control none; cold-cache, serialised: "
+                    "compare shares, not absolutes).  `share` = of all device time in the list; `share_lg` = of the "
+                    "library's own kernels (lg::*), i.e. of the hot path without the bench's L2-flush memsets and "
+                    "input fills.\n\n| kernel | launches | total us | mean us | share | share_lg |\n|---|---|---|---|---|---|\n")
             for k, v in sorted(per.items(), key=lambda x: -x[1]):
-                f.write(f"| {k} | {v:.0f} | {v / tot:.3f} |\n")
+                sl = f"{v / ours:.3f}" if "lg::" in k and ours else "-"
+                f.write(f"| {k} | {cnt[k]} | {v / 1e3:.1f} | {v / 1e3 / cnt[k]:.1f} | {v / tot:.3f} | {sl} |\n")
 
 
 if __name__ == "__main__":
