@@ -56,6 +56,12 @@ struct lgreco_ctx {
   lg::CandS cs{};
   int32_t* d_layer_chunk0 = nullptr;
   double* d_partial = nullptr;
+  // K1 at B = 128: persistent warps over 32-bucket chunks of the compressed layers
+  lg::ProfChunk* d_qchunks = nullptr;
+  int nqchunks = 0;
+  int32_t* d_layer_qchunk0 = nullptr;
+  int nqwarps = 0;
+  unsigned* d_ticket = nullptr;
   unsigned* d_flag = nullptr;
   // plan
   std::vector<int32_t> plan_choice;

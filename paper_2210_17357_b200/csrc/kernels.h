@@ -13,7 +13,8 @@ struct ProfChunk {
   int64_t first;  // first bucket index within the layer
 };
 
-struct CandS { float s[16]; };  // s_j = 2^{b_j} - 1, passed by value (constant bank)
+struct CandS { float s[16]; };
+  // s_j = 2^{b_j} - 1, passed by value (constant bank)
 
 struct QProfileArgs {
   const float* g; const float* e;
@@ -23,6 +24,10 @@ struct QProfileArgs {
   uint32_t k0, k1, rankfield, step;
   double* partial; double* err; int64_t* bits;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // when set: recorded around the K1 launch
+  // B == 128: persistent quad kernel over 32-bucket chunks (qchunks, per-layer
+  // layer_qchunk0[L+1]), nqwarps resident warps, ticket[2] zeroed counters
+  const ProfChunk* qchunks = nullptr; int nqchunks = 0; const int32_t* layer_qchunk0 = nullptr;
+  int nqwarps = 0; unsigned* ticket = nullptr; int ptr_aligned = 0;
 };
 
 struct QPackArgs {

@@ -115,10 +115,11 @@ __device__ __forceinline__ void uniforms4(uint32_t c0, uint32_t rankfield, uint3
 // ---------------------------------------------------------------------------
 // K1 profile
 // ---------------------------------------------------------------------------
-// Quantise 4 elements with every candidate and accumulate the lane's SSE (fp32).
+// Quantise 4 elements with every candidate and accumulate the lane's SSE (fp32, of
+// d * S: see bucket_scale).
 template <int KT>
 __device__ __forceinline__ void prof_candidates(const float* x, float mn, const float* u, float my_inv,
-                                                float my_unit, const CandS& cs, int K, float* acc) {
+                                                float my_unit, const CandS& cs, int K, float S, float* acc) {
   float tt[4];
 #pragma unroll
   for (int s = 0; s < 4; ++s) tt[s] = __fsub_rn(x[s], mn);
@@ -131,7 +132,7 @@ __device__ __forceinline__ void prof_candidates(const float* x, float mn, const 
 #pragma unroll
       for (int s = 0; s < 4; ++s) {
         const float q = qcode(tt[s], inv, u[s], cs.s[j]);
-        const float d = __fsub_rn(x[s], __fmaf_rn(q, unit, mn));
+        const float d = __fmul_rn(__fsub_rn(x[s], __fmaf_rn(q, unit, mn)), S);
         sse = __fmaf_rn(d, d, sse);
       }
       acc[j] = __fadd_rn(acc[j], sse);
@@ -139,8 +140,60 @@ __device__ __forceinline__ void prof_candidates(const float* x, float mn, const 
   }
 }
 
+// Fast-path candidate loop (full aligned buckets of 128, 8 lanes per bucket, 16
+// elements per lane).  q is the pinned code (R6) computed as
+//   q = min(ceil(RU(v - u)), s),  v = RN(t * inv),
+// which equals min(floor(v) + [u < v - floor(v)], s) exactly: for real r = v - u in
+// (n-1, n], RU(r) lies in (n-1, n] because every integer below 2^24 is a float, so
+// ceil(RU(r)) = ceil(r) = floor(v) + [u < frac(v)] (u = frac(v) gives floor(v)).  The
+// ceil is RU(w + (2^23 + 1)) - (2^23 + 1), exact for w in (-1, 2^23 - 1).  v - u is
+// formed as one FFMA.RU of the integer word (w >> 8) with -2^-24 (the product is
+// exact).  dec = fmaf(q, unit, mn) and d = x - dec are the pinned decode, so the SSE is
+// that of the realised reconstruction.
+template <int KT, bool SCALED>
+__device__ __forceinline__ void prof_cand16(const float* x, float mn, uint32_t c0, uint32_t rankfield, uint32_t step,
+                                            uint32_t k0, uint32_t k1, const float* inv, const float* unit,
+                                            const CandS& cs, float S, float* acc) {
+  constexpr float MAGIC = 8388609.0f;  // 2^23 + 1
+#pragma unroll
+  for (int j = 0; j < KT; ++j) acc[j] = 0.f;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const U4 r = philox10(c0 + 8 * i, rankfield, step, 0u, k0, k1);
+    const float uw[4] = {__uint2float_rn(r.x >> 8), __uint2float_rn(r.y >> 8), __uint2float_rn(r.z >> 8),
+                         __uint2float_rn(r.w >> 8)};
+#pragma unroll
+    for (int j = 0; j < KT; ++j) {
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        const float xv = x[4 * i + s];
+        const float v = __fmul_rn(__fsub_rn(xv, mn), inv[j]);
+        const float w = __fmaf_ru(uw[s], -5.9604644775390625e-08f, v);
+        const float q = fminf(__fsub_rn(__fadd_ru(w, MAGIC), MAGIC), cs.s[j]);
+        float d = __fsub_rn(xv, __fmaf_rn(q, unit[j], mn));
+        if (SCALED) d = __fmul_rn(d, S);  // exact power-of-two rescale: d^2 stays normal
+        acc[j] = __fmaf_rn(d, d, acc[j]);
+      }
+    }
+  }
+}
+
+// Per-bucket rescale of the error terms.  d = x - dec is exact-as-rounded; its square
+// in fp32 underflows (or loses bits as a subnormal) once |d| < 2^-63, which the fp64
+// oracle does not.  Buckets with range < 2^-20 therefore square d * 2^k (k = 127 -
+// biased exponent of the range, so range * 2^k is in [1, 2)) and add the fp32 sum times
+// 2^-2k in fp64.  Other buckets: k = 0.
+__device__ __forceinline__ bool bucket_scale(float mn, float mx, float& S, double& S2inv) {
+  const int eb = (int)((__float_as_uint(__fsub_rn(mx, mn)) >> 23) & 0xffu);
+  if (eb >= 107) { S = 1.f; S2inv = 1.0; return false; }
+  const int k = 127 - eb;  // 21..127
+  S = __uint_as_float((uint32_t)(127 + k) << 23);
+  S2inv = __longlong_as_double((long long)(1023 - 2 * k) << 52);
+  return true;
+}
+
 template <int KT>
-__global__ void __launch_bounds__(QP_THREADS, 4)
+__global__ void __launch_bounds__(QP_THREADS, 3)
 k_qprofile(const float* __restrict__ g, const float* __restrict__ e, const DevLayer* __restrict__ layers,
            const ProfChunk* __restrict__ chunks, int B, const CandS cs, int K, uint32_t k0, uint32_t k1,
            uint32_t rankfield, uint32_t step, double* __restrict__ partial) {
@@ -151,27 +204,75 @@ k_qprofile(const float* __restrict__ g, const float* __restrict__ e, const DevLa
   const bool fast_layer = ((ly.offset & 3) == 0) && B == 128;
   const int M = B >> 7;
   const float my_s = (lane < K) ? cs.s[lane] : 1.f;
-  float acc[KT];
+  double acc[KT];
 #pragma unroll
-  for (int j = 0; j < KT; ++j) acc[j] = 0.f;
+  for (int j = 0; j < KT; ++j) acc[j] = 0.0;
 
-  for (int bi = warp; bi < ch.nbk; bi += QP_WARPS) {
+  int bi = warp;
+  if (fast_layer) {
+    // ---- fast path: full aligned buckets of 128; lane group grp (8 lanes) owns one
+    //      bucket, lane l8 holds elements 32i + 4*l8 + s (i, s < 4) = Philox counter
+    //      gb*32 + 8i + l8, words s (R3).  Per-candidate inv/unit computed by lane j of
+    //      the group and kept in registers for the bucket's 16 elements.
+    const int grp = lane >> 3, l8 = lane & 7;
+    const float gs = (l8 < K) ? cs.s[l8] : 1.f;
+    const float gs2 = (KT > 8 && l8 + 8 < K) ? cs.s[(l8 + 8) & 15] : 1.f;
+    const int64_t nfull = min((int64_t)ch.nbk, ly.numel / 128 - ch.first);
+    for (int b0 = warp * 4; b0 < nfull; b0 += QP_WARPS * 4) {
+      const int bq = b0 + grp;
+      const bool valid = bq < nfull;
+      const int64_t jb = ch.first + (valid ? bq : b0);
+      const int64_t base = ly.offset + jb * 128 + 4 * l8;
+      float x[16];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float4 a = ld4(g + base + 32 * i);
+        if (e) {
+          const float4 c = ld4(e + base + 32 * i);
+          x[4 * i] = __fadd_rn(a.x, c.x); x[4 * i + 1] = __fadd_rn(a.y, c.y);
+          x[4 * i + 2] = __fadd_rn(a.z, c.z); x[4 * i + 3] = __fadd_rn(a.w, c.w);
+        } else {
+          x[4 * i] = a.x; x[4 * i + 1] = a.y; x[4 * i + 2] = a.z; x[4 * i + 3] = a.w;
+        }
+      }
+      // (the +0 of canon() only turns -0 into +0, which changes no error: omitted here)
+      float mn = fmin_nan(x[0], x[1]), mx = fmax_nan(x[0], x[1]);
+#pragma unroll
+      for (int s = 2; s < 16; ++s) { mn = fmin_nan(mn, x[s]); mx = fmax_nan(mx, x[s]); }
+#pragma unroll
+      for (int o = 4; o; o >>= 1) {
+        mn = fmin_nan(mn, __shfl_xor_sync(LG_FULL, mn, o));
+        mx = fmax_nan(mx, __shfl_xor_sync(LG_FULL, mx, o));
+      }
+      float my_inv, my_unit, my_inv2 = 0.f, my_unit2 = 0.f;
+      qparams(mn, mx, gs, my_inv, my_unit);
+      if (KT > 8) qparams(mn, mx, gs2, my_inv2, my_unit2);
+      float inv[KT], unit[KT];
+#pragma unroll
+      for (int j = 0; j < KT; ++j) {
+        inv[j] = __shfl_sync(LG_FULL, j < 8 ? my_inv : my_inv2, (lane & ~7) + (j & 7));
+        unit[j] = __shfl_sync(LG_FULL, j < 8 ? my_unit : my_unit2, (lane & ~7) + (j & 7));
+      }
+      const uint32_t c0 = (uint32_t)((ly.bucket0 + jb) * 32 + l8);
+      float S;
+      double S2inv;
+      const bool small = bucket_scale(mn, mx, S, S2inv);
+      float a2[KT];
+      if (__any_sync(LG_FULL, small)) prof_cand16<KT, true>(x, mn, c0, rankfield, step, k0, k1, inv, unit, cs, S, a2);
+      else prof_cand16<KT, false>(x, mn, c0, rankfield, step, k0, k1, inv, unit, cs, 1.f, a2);
+      if (valid) {
+#pragma unroll
+        for (int j = 0; j < KT; ++j) acc[j] = __dadd_rn(acc[j], __dmul_rn((double)a2[j], S2inv));
+      }
+    }
+    // ragged last bucket of the layer (if in this chunk): the generic path, warp 0
+    bi = (nfull < ch.nbk && warp == 0) ? (int)nfull : ch.nbk;
+  }
+  for (; bi < ch.nbk; bi += QP_WARPS) {
     const int64_t jb = ch.first + bi;
     const int64_t gb = ly.bucket0 + jb;
     const int64_t e0 = jb * (int64_t)B;
-    if (fast_layer && e0 + 128 <= ly.numel) {
-      // ---- fast path: one full, aligned bucket of 128
-      const int64_t base = ly.offset + e0 + 4 * lane;
-      const X4 xs = canon4(ld4(g + base), e ? ld4(e + base) : make_float4(0.f, 0.f, 0.f, 0.f));
-      float mn = fmin_nan(fmin_nan(xs.v[0], xs.v[1]), fmin_nan(xs.v[2], xs.v[3]));
-      float mx = fmax_nan(fmax_nan(xs.v[0], xs.v[1]), fmax_nan(xs.v[2], xs.v[3]));
-      warp_minmax_nan(mn, mx);
-      float my_inv, my_unit;
-      qparams(mn, mx, my_s, my_inv, my_unit);
-      float u[4];
-      uniforms4((uint32_t)(gb * 32 + lane), rankfield, step, 0u, k0, k1, u);
-      prof_candidates<KT>(xs.v, mn, u, my_inv, my_unit, cs, K, acc);
-    } else {
+    {
       // ---- generic path: ragged / misaligned / B > 128
       const bool aligned = (ly.offset & 3) == 0;
       float mn = INFINITY, mx = -INFINITY;
@@ -187,6 +288,12 @@ k_qprofile(const float* __restrict__ g, const float* __restrict__ e, const DevLa
       warp_minmax_nan(mn, mx);
       float my_inv, my_unit;
       qparams(mn, mx, my_s, my_inv, my_unit);
+      float S;
+      double S2inv;
+      bucket_scale(mn, mx, S, S2inv);
+      float a2[KT];
+#pragma unroll
+      for (int j = 0; j < KT; ++j) a2[j] = 0.f;
       for (int t = 0; t < M; ++t) {
         const int64_t i0 = e0 + 128 * t + 4 * lane;
         const int nv = (int)max((int64_t)0, min((int64_t)4, ly.numel - i0));
@@ -195,15 +302,17 @@ k_qprofile(const float* __restrict__ g, const float* __restrict__ e, const DevLa
         uniforms4((uint32_t)(gb * (B >> 2) + 32 * t + lane), rankfield, step, 0u, k0, k1, u);
 #pragma unroll
         for (int s = 0; s < 4; ++s) x[s] = (s < nv) ? xs.v[s] : mn;  // invalid -> d = 0
-        prof_candidates<KT>(x, mn, u, my_inv, my_unit, cs, K, acc);
+        prof_candidates<KT>(x, mn, u, my_inv, my_unit, cs, K, S, a2);
       }
+#pragma unroll
+      for (int j = 0; j < KT; ++j) acc[j] = __dadd_rn(acc[j], __dmul_rn((double)a2[j], S2inv));
     }
   }
   // ---- deterministic block reduction (fp64)
 #pragma unroll
   for (int j = 0; j < KT; ++j) {
     if (j < K) {
-      const double v = warp_sum_d((double)acc[j]);
+      const double v = warp_sum_d(acc[j]);
       if (lane == 0) red[warp][j] = v;
     }
   }
@@ -216,35 +325,303 @@ k_qprofile(const float* __restrict__ g, const float* __restrict__ e, const DevLa
   }
 }
 
-// K1b: per layer, fixed-order tree over its chunks' partials.
-__global__ void __launch_bounds__(256)
+// ---------------------------------------------------------------------------
+// K1 (B = 128): persistent warps over chunks of <= 32 buckets of one layer, handed
+// out dynamically (one global ticket counter; a warp holds its next chunk while
+// computing the current one).  A chunk is walked in "quads" of 4 consecutive buckets
+// (one per 8-lane group), staged into shared memory by the bulk-copy engine
+// (cp.async.bulk, TMA 1-D) with an mbarrier per stage: while a warp computes quad q,
+// the next quad (of this chunk or of its next chunk) is in flight.  Each chunk's fp64
+// SSE goes to its own partial slot, so K1b's fixed-order per-layer sum is
+// deterministic whatever warp took the chunk.  Dynamic hand-out balances the warps of
+// an SM (the issue arbiter favours high warp ids, so static equal ranges leave a
+// tail of low-id warps).  Quads of misaligned layers or with a ragged bucket are
+// loaded directly (masked).  The last warp to finish resets the counter, so the
+// launch is stream- and graph-replay safe.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t sm_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void bar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sm_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sm_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred done;\n\t"
+      "QW_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+      "@!done bra QW_%=;\n\t}\n" ::"r"(sm_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   sm_addr(dst)),
+               "l"(src), "r"(bytes), "r"(sm_addr(bar))
+               : "memory");
+}
+
+template <int KT>
+__global__ void __launch_bounds__(QP_THREADS, 3)
+k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const DevLayer* __restrict__ layers,
+             const ProfChunk* __restrict__ qchunks, int nqc, unsigned* __restrict__ ticket, const CandS cs, int K,
+             uint32_t k0, uint32_t k1, uint32_t rankfield, uint32_t step, int ptr_aligned,
+             double* __restrict__ partial) {
+  extern __shared__ __align__(128) unsigned char qsm[];
+  __shared__ __align__(8) uint64_t bars[QP_WARPS][2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int grp = lane >> 3, l8 = lane & 7;
+  // stage b of this warp: g at qsm + (2 warp + b) 4096 bytes, e 2048 bytes after it
+  auto stage_g = [&](int b) { return reinterpret_cast<float*>(qsm + (size_t)(warp * 2 + b) * 4096); };
+  auto grab = [&]() -> int {
+    unsigned v = 0;
+    if (lane == 0) v = atomicAdd(&ticket[0], 1u);
+    return (int)__shfl_sync(LG_FULL, v, 0);
+  };
+  auto finish = [&]() {  // after this warp's failing grab
+    if (lane == 0 && atomicAdd(&ticket[1], 1u) == gridDim.x * QP_WARPS - 1u) {
+      atomicExch(&ticket[0], 0u);
+      atomicExch(&ticket[1], 0u);
+    }
+  };
+  int c = grab();
+  if (c >= nqc) { finish(); return; }
+  if (lane == 0) {
+    bar_init(&bars[warp][0], 1);
+    bar_init(&bars[warp][1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const bool pal = ptr_aligned != 0;
+  const uint32_t tx = e ? 4096u : 2048u;
+  float gs = 1.f, gs2 = 1.f;  // s of candidates l8 and l8 + 8 (select chain: no local copy of cs)
+#pragma unroll
+  for (int j = 0; j < KT; ++j) {
+    if (j < K && j == l8) gs = cs.s[j];
+    if (j < K && j == l8 + 8) gs2 = cs.s[j];
+  }
+  // current chunk: layer offset, numel (< 2^31), first bucket (global), first bucket in
+  // the layer, bucket count
+  int64_t ly_off, ly_b0;
+  int ly_n, ch_first, ch_nbk;
+  auto load_chunk = [&](int ci) {
+    const ProfChunk ch = qchunks[ci];
+    ly_off = layers[ch.layer].offset;
+    ly_b0 = layers[ch.layer].bucket0;
+    ly_n = (int)layers[ch.layer].numel;
+    ch_first = (int)ch.first;
+    ch_nbk = ch.nbk;
+  };
+  // bulk copies of the quad whose first bucket (in its layer) is fb, into stage b
+  // (lane 0), when regular (aligned layer and pointers, 4 full buckets)
+  auto issue = [&](int64_t off, int n, int fb, int b) -> bool {
+    if (!(pal && (off & 3) == 0 && (fb + 4) * 128 <= n)) return false;
+    if (lane == 0) {
+      const int64_t o = off + (int64_t)fb * 128;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier generic reads of the stage
+      bar_expect_tx(&bars[warp][b], tx);
+      bulk_g2s(stage_g(b), g + o, 2048u, &bars[warp][b]);
+      if (e) bulk_g2s(stage_g(b) + 512, e + o, 2048u, &bars[warp][b]);
+    }
+    return true;
+  };
+  load_chunk(c);
+  int cn = grab();
+  uint32_t phase = 0u;  // bit b: parity of stage b's next completion
+  int b = 0;
+  bool inflight = issue(ly_off, ly_n, ch_first, 0);
+  double acc[KT];
+#pragma unroll
+  for (int j = 0; j < KT; ++j) acc[j] = 0.0;
+
+  for (;;) {
+    const int nq = (ch_nbk + 3) >> 2;
+    for (int k = 0; k < nq; ++k, b ^= 1) {
+      const bool cur_regular = inflight;
+      // prefetch the next quad into the other stage (its previous contents were consumed
+      // in the previous iteration; __syncwarp orders those reads before the copy)
+      __syncwarp();
+      if (k + 1 < nq) {
+        inflight = issue(ly_off, ly_n, ch_first + 4 * (k + 1), b ^ 1);
+      } else if (cn < nqc) {
+        const ProfChunk nc = qchunks[cn];
+        inflight = issue(layers[nc.layer].offset, (int)layers[nc.layer].numel, (int)nc.first, b ^ 1);
+      } else {
+        inflight = false;
+      }
+      const int jb = ch_first + 4 * k + grp;  // bucket within the layer
+      const bool valid = 4 * k + grp < ch_nbk;
+      float x[16];
+      if (cur_regular) {
+        bar_wait(&bars[warp][b], (phase >> b) & 1u);
+        phase ^= 1u << b;
+        const float* sg = stage_g(b) + grp * 128 + 4 * l8;
+        const float* se = sg + 512;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float4 a = *reinterpret_cast<const float4*>(sg + 32 * i);
+          if (e) {
+            const float4 f = *reinterpret_cast<const float4*>(se + 32 * i);
+            x[4 * i] = __fadd_rn(a.x, f.x); x[4 * i + 1] = __fadd_rn(a.y, f.y);
+            x[4 * i + 2] = __fadd_rn(a.z, f.z); x[4 * i + 3] = __fadd_rn(a.w, f.w);
+          } else {
+            x[4 * i] = a.x; x[4 * i + 1] = a.y; x[4 * i + 2] = a.z; x[4 * i + 3] = a.w;
+          }
+        }
+      } else {
+        // masked direct loads: element 32i + 4*l8 + s of bucket jb
+        const int base = jb * 128 + 4 * l8;
+        const float* gl = g + ly_off;
+        const float* el = e ? e + ly_off : nullptr;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+#pragma unroll
+          for (int s2 = 0; s2 < 4; ++s2) {
+            const int idx = base + 32 * i + s2;
+            const bool ok = valid && idx < ly_n;
+            float v = 0.f;
+            if (ok) {
+              v = __ldg(gl + idx);
+              if (el) v = __fadd_rn(v, __ldg(el + idx));
+            }
+            x[4 * i + s2] = v;
+          }
+        }
+      }
+      // (the +0 of canon() only turns -0 into +0, which changes no error: omitted here)
+      float mn, mx;
+      if (cur_regular) {
+        mn = fmin_nan(x[0], x[1]); mx = fmax_nan(x[0], x[1]);
+#pragma unroll
+        for (int s2 = 2; s2 < 16; ++s2) { mn = fmin_nan(mn, x[s2]); mx = fmax_nan(mx, x[s2]); }
+      } else {
+        mn = INFINITY; mx = -INFINITY;
+#pragma unroll
+        for (int s2 = 0; s2 < 16; ++s2) {
+          const int idx = jb * 128 + 4 * l8 + 32 * (s2 >> 2) + (s2 & 3);
+          if (valid && idx < ly_n) { mn = fmin_nan(mn, x[s2]); mx = fmax_nan(mx, x[s2]); }
+        }
+      }
+#pragma unroll
+      for (int o = 4; o; o >>= 1) {
+        mn = fmin_nan(mn, __shfl_xor_sync(LG_FULL, mn, o));
+        mx = fmax_nan(mx, __shfl_xor_sync(LG_FULL, mx, o));
+      }
+      if (!cur_regular) {
+#pragma unroll
+        for (int s2 = 0; s2 < 16; ++s2) {
+          const int idx = jb * 128 + 4 * l8 + 32 * (s2 >> 2) + (s2 & 3);
+          if (!(valid && idx < ly_n)) x[s2] = mn;  // invalid -> t = 0, q = 0, d = 0
+        }
+      }
+      float my_inv, my_unit, my_inv2 = 0.f, my_unit2 = 0.f;
+      qparams(mn, mx, gs, my_inv, my_unit);
+      if (KT > 8) qparams(mn, mx, gs2, my_inv2, my_unit2);
+      float inv[KT], unit[KT];
+#pragma unroll
+      for (int j = 0; j < KT; ++j) {
+        inv[j] = __shfl_sync(LG_FULL, j < 8 ? my_inv : my_inv2, (lane & ~7) + (j & 7));
+        unit[j] = __shfl_sync(LG_FULL, j < 8 ? my_unit : my_unit2, (lane & ~7) + (j & 7));
+      }
+      const uint32_t c0 = (uint32_t)((ly_b0 + jb) * 32 + l8);
+      float S;
+      double S2inv;
+      const bool small = bucket_scale(mn, mx, S, S2inv);
+      float a2[KT];
+      if (__any_sync(LG_FULL, small)) prof_cand16<KT, true>(x, mn, c0, rankfield, step, k0, k1, inv, unit, cs, S, a2);
+      else prof_cand16<KT, false>(x, mn, c0, rankfield, step, k0, k1, inv, unit, cs, 1.f, a2);
+      if (valid) {
+#pragma unroll
+        for (int j = 0; j < KT; ++j) acc[j] = __dadd_rn(acc[j], __dmul_rn((double)a2[j], S2inv));
+      }
+    }
+    // chunk done: fixed-order warp reduction into its slot
+    if (KT <= 8) {
+      // transpose-reduce: after the xor-16/8/4 halvings lane L holds value 4*bit4 +
+      // 2*bit3 + bit2 of L summed over its 8-lane class, xor-2/1 finish the sum
+      double v8[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v8[j] = (j < KT) ? acc[j] : 0.0;
+#pragma unroll
+      for (int h = 4; h >= 1; h >>= 1) {
+        const int o = 4 * h;  // xor 16, 8, 4
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int i = 0; i < h; ++i) {
+          const double send = up ? v8[i] : v8[i + h];
+          const double keep = up ? v8[i + h] : v8[i];
+          v8[i] = __dadd_rn(keep, __shfl_xor_sync(LG_FULL, send, o));
+        }
+      }
+      double t = __dadd_rn(v8[0], __shfl_xor_sync(LG_FULL, v8[0], 2));
+      t = __dadd_rn(t, __shfl_xor_sync(LG_FULL, t, 1));
+      const int j = lane >> 2;
+      if ((lane & 3) == 0 && j < K) partial[(int64_t)c * K + j] = t;
+    } else {
+#pragma unroll
+      for (int j = 0; j < KT; ++j) {
+        if (j < K) {
+          const double v = warp_sum_d(acc[j]);
+          if (lane == 0) partial[(int64_t)c * K + j] = v;
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < KT; ++j) acc[j] = 0.0;
+    if (cn >= nqc) break;
+    c = cn;
+    load_chunk(c);
+    cn = grab();
+  }
+  finish();
+}
+
+// K1b: per layer, fixed-order sum of its chunks' partials (all K values of a chunk row
+// per thread, rows strided over 512 threads, then a fixed warp tree and a fixed sum
+// over warps), sqrt.
+constexpr int QR_THREADS = 512;
+__global__ void __launch_bounds__(QR_THREADS)
 k_qprofile_reduce(const DevLayer* __restrict__ layers, const int32_t* __restrict__ layer_chunk0,
                   const double* __restrict__ partial, const int32_t* __restrict__ params, int K, int B,
                   double* __restrict__ err, int64_t* __restrict__ bits) {
-  __shared__ double sm[256];
+  __shared__ double sm[16][QR_THREADS / 32];
   const int l = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const DevLayer ly = layers[l];
   const int c0 = layer_chunk0[l], c1 = layer_chunk0[l + 1];
   const int64_t nb = (ly.numel + B - 1) / B;
-  for (int j = 0; j < K; ++j) {
+  double a[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) a[j] = 0.0;
+  for (int c = c0 + threadIdx.x; c < c1; c += QR_THREADS) {
+    const double* row = partial + (int64_t)c * K;
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (j < K) a[j] += __ldg(row + j);
+  }
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    if (j < K) {
+      const double v = warp_sum_d(a[j]);
+      if (lane == 0) sm[j][warp] = v;
+    }
+  }
+  __syncthreads();
+  const int j = threadIdx.x;
+  if (j < K) {
     double s = 0.0;
-    for (int c = c0 + threadIdx.x; c < c1; c += blockDim.x) s += partial[(int64_t)c * K + j];
-    sm[threadIdx.x] = s;
-    __syncthreads();
-    for (int o = 128; o; o >>= 1) {
-      if (threadIdx.x < o) sm[threadIdx.x] += sm[threadIdx.x + o];
-      __syncthreads();
+#pragma unroll
+    for (int w = 0; w < QR_THREADS / 32; ++w) s += sm[j][w];
+    if (ly.compress) {
+      err[(int64_t)l * K + j] = sqrt(s);
+      bits[(int64_t)l * K + j] = nb * ((int64_t)B * params[j] + 64);
+    } else {
+      err[(int64_t)l * K + j] = 0.0;
+      bits[(int64_t)l * K + j] = 32 * ly.numel;
     }
-    if (threadIdx.x == 0) {
-      if (ly.compress) {
-        err[(int64_t)l * K + j] = sqrt(sm[0]);
-        bits[(int64_t)l * K + j] = nb * ((int64_t)B * params[j] + 64);
-      } else {
-        err[(int64_t)l * K + j] = 0.0;
-        bits[(int64_t)l * K + j] = 32 * ly.numel;
-      }
-    }
-    __syncthreads();
   }
 }
 
@@ -576,25 +953,49 @@ __global__ void k_philox(const uint32_t* __restrict__ ctr, uint32_t k0, uint32_t
 // launchers
 // ---------------------------------------------------------------------------
 cudaError_t launch_qprofile(const QProfileArgs& a, cudaStream_t st) {
+  const bool quads = a.B == 128 && a.nqwarps > 0 && a.nqchunks > 0;
   if (a.nchunks > 0) {
     if (a.ev0) cudaEventRecord(a.ev0, st);
+    if (quads) {
+      const size_t smem = (size_t)QP_WARPS * 2 * 4096;
+      const int grid = a.nqwarps / QP_WARPS;
+#define LG_QQ(KT)                                                                                              \
+  {                                                                                                            \
+    cudaError_t e = cudaFuncSetAttribute(k_qprofile_q<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    if (e != cudaSuccess) return e;                                                                            \
+    k_qprofile_q<KT><<<grid, QP_THREADS, smem, st>>>(a.g, a.e, a.layers, a.qchunks, a.nqchunks, a.ticket, a.cs, a.K, \
+                                                    a.k0, a.k1, a.rankfield, a.step, a.ptr_aligned, a.partial);  \
+  }
+      switch (a.K) {
+        case 4: LG_QQ(4); break;
+        case 5: LG_QQ(5); break;
+        case 6: LG_QQ(6); break;
+        case 7: LG_QQ(7); break;
+        case 8: LG_QQ(8); break;
+        default:
+          if (a.K < 4) LG_QQ(4) else LG_QQ(16)
+      }
+#undef LG_QQ
+    } else {
 #define LG_QP(KT)                                                                          \
   k_qprofile<KT><<<a.nchunks, QP_THREADS, 0, st>>>(a.g, a.e, a.layers, a.chunks, a.B, a.cs, a.K, \
                                                     a.k0, a.k1, a.rankfield, a.step, a.partial)
-    switch (a.K) {
-      case 4: LG_QP(4); break;
-      case 5: LG_QP(5); break;
-      case 6: LG_QP(6); break;
-      case 7: LG_QP(7); break;
-      case 8: LG_QP(8); break;
-      default:
-        if (a.K < 4) LG_QP(4);
-        else LG_QP(16);
-    }
+      switch (a.K) {
+        case 4: LG_QP(4); break;
+        case 5: LG_QP(5); break;
+        case 6: LG_QP(6); break;
+        case 7: LG_QP(7); break;
+        case 8: LG_QP(8); break;
+        default:
+          if (a.K < 4) LG_QP(4);
+          else LG_QP(16);
+      }
 #undef LG_QP
+    }
     if (a.ev1) cudaEventRecord(a.ev1, st);
   }
-  k_qprofile_reduce<<<a.L, 256, 0, st>>>(a.layers, a.layer_chunk0, a.partial, a.params, a.K, a.B, a.err, a.bits);
+  k_qprofile_reduce<<<a.L, QR_THREADS, 0, st>>>(a.layers, quads ? a.layer_qchunk0 : a.layer_chunk0, a.partial, a.params, a.K,
+                                         a.B, a.err, a.bits);
   return cudaGetLastError();
 }
 

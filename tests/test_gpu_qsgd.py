@@ -217,3 +217,78 @@ def test_compress_allreduce_dev_matches_host_path(lg):
     ctx.compress_allreduce(choice, gd, e1, o1, 3)
     ctx.compress_allreduce_dev(torch.tensor(choice, dtype=torch.int32, device="cuda"), gd, e2, o2, 3)
     assert torch.equal(o1.view(torch.int32), o2.view(torch.int32)) and torch.equal(e1.view(torch.int32), e2.view(torch.int32))
+
+
+def _adversarial_buckets(seed=21):
+    """One-bucket layers (128 elements, 16-byte aligned offsets: the K1 fast path) whose
+    codes are easy to get wrong, so that ONE wrong stochastic-rounding decision moves the
+    layer's error by far more than the 1e-5 tolerance:
+      - large offset, tiny range (x = 1000 + N(0, 1e-3)): t = x - mn exact, dec rounds coarsely;
+      - on-grid values of one candidate (v exactly integral, frac = 0);
+      - ranges r with fl32(r * fl32(s/r)) > s for some s: the maximum element gives v > s,
+        so the clamp min(., s) decides (R6);
+      - a near-subnormal range (inv = s/range overflows: constant-bucket rule, R5);
+      - repeated maxima/minima and exact zeros."""
+    rng = np.random.default_rng(seed)
+    f32 = np.float32
+    blocks = []
+    for _ in range(12):
+        blocks.append((f32(1000.0) + rng.normal(0, 1e-3, 128).astype(f32)).astype(f32))
+    for b in BITS:
+        s = f32(2 ** b - 1)
+        unit = f32(rng.uniform(1e-4, 1e-1))
+        mn = f32(rng.normal(0, 1))
+        k = rng.integers(0, int(s) + 1, 128).astype(f32)
+        k[0], k[1] = 0, s
+        blocks.append((mn + k * unit).astype(f32))
+    found = 0
+    while found < 16:
+        r = f32(rng.uniform(1e-3, 10.0))
+        hit = [b for b in BITS if f32(r * f32(f32(2 ** b - 1) / r)) > f32(2 ** b - 1)]
+        if not hit:
+            continue
+        x = (rng.uniform(0, 1, 128) * r).astype(f32)
+        x[:6] = r
+        x[6] = f32(0.0)
+        if found % 2:
+            x = -x  # mn = -r: t = x - mn
+        blocks.append(x.astype(f32))
+        found += 1
+    tiny = np.zeros(128, f32)
+    tiny[::3] = f32(1e-44)
+    blocks.append(tiny)
+    blocks.append(np.concatenate([np.full(64, f32(-2.5)), np.full(64, f32(3.0))]).astype(f32))
+    g = np.concatenate(blocks).astype(f32)
+    layers = [W.Layer(128 * i, 128, 0, 0, 1) for i in range(len(blocks))]
+    return layers, g
+
+
+def _dev_shifted(a):
+    """Device copy whose data pointer is 4 bytes past a 16-byte boundary (the K1
+    bulk-copy path must fall back to masked direct loads)."""
+    buf = torch.empty(a.size + 1, dtype=torch.float32, device="cuda")
+    v = buf[1:]
+    v.copy_(torch.from_numpy(np.ascontiguousarray(a)))
+    return v
+
+
+@pytest.mark.parametrize("with_ef,shifted", [(False, False), (True, False), (True, True)])
+def test_profile_parity_adversarial_buckets(lg, ref, with_ef, shifted):
+    """Per-bucket exactness of the fused profile's codes (fast path) against the oracle."""
+    layers, g = _adversarial_buckets()
+    e = None
+    if with_ef:
+        e = np.zeros_like(g)  # x = g + 0: exercises the EF add without moving the values
+    seed, step = 0xC0FFEE, 11
+    ctx = lg.Context(layers, lg.QSGD, BITS, seed=seed)
+    L, K = len(layers), len(BITS)
+    err = torch.empty(L, K, dtype=torch.float64, device="cuda")
+    bits = torch.empty(L, K, dtype=torch.int64, device="cuda")
+    mk = _dev_shifted if shifted else _dev
+    ctx.profile(mk(g), None if e is None else mk(e), step, err, bits)
+    ref_err, ref_bits = ref.qsgd_profile(layers, g, e, BITS, seed=seed, step=step)
+    assert np.array_equal(bits.cpu().numpy(), ref_bits)
+    ge = err.cpu().numpy()
+    assert np.all((ref_err == 0) == (ge == 0))
+    rel = np.abs(ge - ref_err) / np.maximum(ref_err, 1e-300)
+    assert rel.max() <= 1e-5, (rel.max(), np.unravel_index(rel.argmax(), rel.shape))
