@@ -11,6 +11,7 @@
 #include <math.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include <algorithm>
 
@@ -713,25 +714,729 @@ k_solve_fast(const double* __restrict__ err, const int64_t* __restrict__ bits, i
 #endif
 }
 
+// ---------------------------------------------------------------------------
+// Cluster path: the row recursion of Alg.1 (lines 13-22) spread over a thread-block
+// cluster of NC CTAs (one per SM).  A single SM is bound by shared-memory bandwidth
+// (one 4-byte LDS per cell and candidate: 10,001 x 7 x 4 B / 128 B/clk ~ 2.2 K cycles
+// per row); NC SMs each own a contiguous slice of S cells and keep a full-length copy
+// of the two rows.  Cell e of row a reads row a-1 at e - d (d >= 0), i.e. only cells
+// at or below e, so CTA r needs, besides its own slice, the cells [r S - maxd, r S) of
+// lower CTAs, where maxd is the largest admissible disc of the next layer (exact: no
+// read of row a+1 reaches further down).  Every warp pushes the cells of its slice that
+// a higher CTA will read straight from its registers into that CTA's copy of the row
+// (st.shared::cluster), then one cluster barrier (release/acquire) per row publishes
+// them; the same barrier orders the reuse of the double-buffered rows (no CTA writes
+// row a+2 before every CTA has finished reading row a).  Keys, tie-breaks, the band
+// skip and the PD bytes are those of k_solve_fast; the argmin is reduced per CTA and
+// gathered in rank 0 over DSMEM; rank 0 backtracks through PD (global, L2).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t cl_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cl_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cl_map(const void* p, uint32_t rank) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(p));
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cl_st(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void cl_st(uint32_t addr, uint64_t v) {
+  asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
+}
+
+constexpr int CL_MAX = 8;  // CTAs per cluster (portable maximum)
+
+template <int CPT>
+__device__ __forceinline__ void pd_store(uint8_t* dst, const uint32_t* w) {
+  if (CPT == 1) *dst = (uint8_t)w[0];
+  else if (CPT == 2) *reinterpret_cast<uint16_t*>(dst) = (uint16_t)w[0];
+  else if (CPT == 4) *reinterpret_cast<uint32_t*>(dst) = w[0];
+  else if (CPT == 8) *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
+  else *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+template <int CPT, int KT>
+__global__ void __launch_bounds__(DP_THREADS, 1)
+k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int L, int K,
+           const int32_t* __restrict__ default_idx, const int32_t* __restrict__ compress, int D, uint32_t flags,
+           int32_t* __restrict__ choice, lgreco_solve_info* __restrict__ info, uint8_t* __restrict__ PD,
+           int32_t* __restrict__ act, int32_t* __restrict__ wdisc, uint64_t* __restrict__ wadd,
+           int32_t* __restrict__ wmaxd) {
+  static_assert(KT > 0 && KT <= 16 && (CPT == 1 || CPT == 2 || CPT == 4 || CPT == 8 || CPT == 16), "cluster DP");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ __align__(16) uint2 s_cand[2][(KT + 2) & ~1];  // even stride: 16-byte pair reads
+  __shared__ uint64_t s_add[2][KT];
+  __shared__ int2 s_band[2];
+  __shared__ int s_La, s_status, s_wide, s_cbits;
+  __shared__ double s_emax;
+  __shared__ int64_t s_defbits;
+  __shared__ uint64_t s_g[32];
+  __shared__ uint64_t s_redk[32];
+  __shared__ int s_rede[32];
+  __shared__ uint64_t s_clk[CL_MAX];
+  __shared__ int s_cle[CL_MAX];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int NT = blockDim.x, NW = NT >> 5;
+  const uint32_t rank = cl_rank(), NC = gridDim.x;
+  const int S = NW * 32 * CPT;     // cells per CTA
+  const int cbase = (int)rank * S; // first cell of this CTA
+#ifdef LG_DP_TIMING
+  long long tstamp[10] = {0};
+  long long t_push = 0, t_c = 0, t_p = 0, t_s = 0, t_cl = 0;
+#endif
+  LG_T(0);
+
+  // ---- prelude (every CTA, identical): flags/defaults, active list, Emax (layer order)
+  int32_t* sm_flag = reinterpret_cast<int32_t*>(smem_raw);
+  int32_t* sm_act = sm_flag + L;
+  double* sm_de = reinterpret_cast<double*>(sm_act + L);
+  double* sm_dea = sm_de + L;
+  if (tid == 0) s_status = LGRECO_OK;
+  if (tid < 32) { s_redk[tid] = 0; s_g[tid] = 0; }
+  __syncthreads();
+  int64_t db_part = 0;
+  int bad_def = 0;
+  for (int l = tid; l < L; l += NT) {
+    const int f = compress ? (compress[l] != 0) : 1;
+    const int d = default_idx[l];
+    sm_flag[l] = f;
+    if (rank == 0) choice[l] = -1;
+    if (f) {
+      if (d < 0 || d >= K) { bad_def = 1; sm_de[l] = 0.0; }
+      else { sm_de[l] = metric(err[(int64_t)l * K + d], flags); db_part += bits[(int64_t)l * K + d]; }
+    }
+  }
+  if (__any_sync(LG_FULL, bad_def) && lane == 0) atomicExch(&s_status, LGRECO_EINVAL);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) db_part += __shfl_xor_sync(LG_FULL, db_part, o);
+  if (lane == 0) s_redk[warp] = (uint64_t)db_part;
+  __syncthreads();
+  if (warp == 0) {
+    int La = 0;
+    for (int base = 0; base < L; base += 32) {
+      const int l = base + lane;
+      const int f = (l < L) ? sm_flag[l] : 0;
+      const unsigned m = __ballot_sync(LG_FULL, f);
+      if (f) {
+        const int pos = La + __popc(m & ((1u << lane) - 1u));
+        sm_act[pos] = l;
+        if (rank == 0) act[pos] = l;
+        sm_dea[pos] = sm_de[l];
+      }
+      La += __popc(m);
+    }
+    __syncwarp();
+    if (lane == 0) {
+      double emax = 0.0;
+      int a = 0;
+      for (; a + 4 <= La; a += 4) {
+        const double v0 = sm_dea[a], v1 = sm_dea[a + 1], v2 = sm_dea[a + 2], v3 = sm_dea[a + 3];
+        emax = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(emax, v0), v1), v2), v3);
+      }
+      for (; a < La; ++a) emax = __dadd_rn(emax, sm_dea[a]);
+      int64_t defb = 0;
+      for (int w = 0; w < NW; ++w) defb += (int64_t)s_redk[w];
+      s_La = La; s_emax = emax; s_defbits = defb;
+      int cb = 0;
+      while ((1 << cb) < K) ++cb;
+      s_cbits = cb;
+    }
+  }
+  __syncthreads();
+  const int La = s_La;
+  const double emax = s_emax;
+  // ---- validation, discretisation (Alg.1 lines 3-5) into this CTA's shared memory
+  //      (tail region after the two rows; identical in every CTA), OR of the costs,
+  //      sum of per-layer max cost, per-layer max admissible disc
+  constexpr int PAD = 32 * CPT;
+  const int row = PAD + (int)NC * S;
+  uint64_t* my_wadd = reinterpret_cast<uint64_t*>(smem_raw + (size_t)16 * row);  // [La*K] raw costs
+  int32_t* my_wdisc = reinterpret_cast<int32_t*>(my_wadd + (size_t)La * K);        // [La*K]
+  int32_t* my_wmaxd = my_wdisc + (size_t)La * K;                                   // [La+1]
+  uint64_t gg = 0, mx_part = 0;
+  int bad = 0;
+  if (tid == 0) my_wmaxd[La] = 0;
+  for (int a = warp; a < La; a += NW) {
+    const int l = sm_act[a];
+    uint64_t m = 0;
+    int dm = 0;
+    for (int c = lane; c < K; c += 32) {
+      const double v = err[(int64_t)l * K + c];
+      const int64_t b = bits[(int64_t)l * K + c];
+      if (!isfinite(v) || v < 0.0) bad |= 1;
+      if (b < 0) bad |= 2;
+      const uint64_t ub = (uint64_t)(b < 0 ? 0 : b);
+      gg |= ub;
+      m = max(m, ub);
+      const int dd = discretise(metric(v, flags), emax, D, flags);
+      dm = max(dm, dd);
+      my_wdisc[a * K + c] = dd;
+      my_wadd[a * K + c] = ub;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      m = max(m, __shfl_xor_sync(LG_FULL, m, o));
+      dm = max(dm, __shfl_xor_sync(LG_FULL, dm, o));
+    }
+    mx_part += m;
+    if (lane == 0) my_wmaxd[a] = dm;
+  }
+  bad = __reduce_or_sync(LG_FULL, bad);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) gg |= __shfl_xor_sync(LG_FULL, gg, o);
+  if (lane == 0) {
+    s_g[warp] = gg;
+    s_redk[warp] = mx_part;
+    if (bad & 1) atomicExch(&s_status, LGRECO_ENONFINITE);
+    else if (bad & 2) atomicExch(&s_status, LGRECO_EINVAL);
+  }
+  __syncthreads();
+  if (warp == 0) {
+    uint64_t g = (lane < NW) ? s_g[lane] : 0;
+    unsigned long long mxs = (lane < NW) ? s_redk[lane] : 0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      g |= __shfl_xor_sync(LG_FULL, g, o);
+      mxs += __shfl_xor_sync(LG_FULL, mxs, o);
+    }
+    if (lane == 0) {
+      g = g ? (g & (~g + 1)) : 1;
+      s_g[0] = g;
+      const uint64_t mx = mxs >> (__ffsll((long long)g) - 1);
+      s_wide = (mx >= (1ull << (30 - s_cbits))) ? 1 : 0;
+      if (mx >= (1ull << (62 - s_cbits)) && s_status == LGRECO_OK) s_status = LGRECO_EINVAL;
+    }
+  }
+  __syncthreads();
+  const uint64_t g = s_g[0];
+  const int gsh = __ffsll((long long)g) - 1;
+  const int cbits = s_cbits;
+  if (s_status != LGRECO_OK || La == 0) {  // identical in every CTA: no cluster barrier is pending
+    if (rank == 0 && tid == 0) {
+      lgreco_solve_info inf = {};
+      inf.n_active = La;
+      inf.status = s_status;
+      *info = inf;
+    }
+    return;
+  }
+  const bool wide = s_wide;
+  const int kb = cbits;
+  const uint64_t kmask = (1ull << kb) - 1;
+  const int pdmask = (int)((1u << cbits) - 1u);
+  auto keyed = [&](uint64_t ub, int c) -> uint64_t { return ((ub >> gsh) << kb) | (uint64_t)(c & (int)kmask); };
+  // two full-length rows (PAD INF cells + NC*S cells), in every CTA
+  uint32_t* r32a = reinterpret_cast<uint32_t*>(smem_raw);
+  uint32_t* r32b = r32a + row;
+  uint64_t* r64a = reinterpret_cast<uint64_t*>(smem_raw);
+  uint64_t* r64b = r64a + row;
+  const uint32_t INF32 = 0x7FFFFF00u;
+  const uint64_t INF64 = 1ull << 62;
+  // per-layer candidate tables for the whole recursion, staged once: {disc, 32-bit
+  // key} pairs (inadmissible and padding candidates = {0, INF}: they never win, so
+  // the inner loop has no branches), 64-bit keys, and the reachable band [lo, hi]
+  constexpr int KP2 = (KT + 2) & ~1;
+  uint2* cand_all = reinterpret_cast<uint2*>(
+      (reinterpret_cast<uintptr_t>(my_wmaxd + La + 1) + 15) & ~static_cast<uintptr_t>(15));  // [La][KP2], 16-B aligned
+  uint64_t* add_all = reinterpret_cast<uint64_t*>(cand_all + (size_t)La * KP2);  // [La][KT]
+  int2* band_all = reinterpret_cast<int2*>(add_all + (size_t)La * KT);          // [La]
+  for (int i = tid; i < La * KP2; i += NT) {
+    const int aa = i / KP2, c = i - aa * KP2;
+    const int32_t d = (c < K) ? my_wdisc[aa * K + c] : -1;
+    const bool ok = c < K && d >= 0;
+    const uint64_t k = ok ? keyed(my_wadd[aa * K + c], c) : 0;
+    cand_all[i] = make_uint2(ok ? (uint32_t)d : 0u, ok ? (uint32_t)k : INF32);
+    if (c < KT) add_all[aa * KT + c] = ok ? k : INF64;
+  }
+  __syncthreads();  // the prelude's shared staging (front of smem) is dead from here
+  // bands: running sums of the smallest / largest admissible disc (exact reachable
+  // set bounds).  Warp 0 scans the layers 32 at a time; a layer with no admissible
+  // candidate empties every later band (lo = INF).
+  if (warp == 0) {
+    long long slo = 0;
+    int shi = 0;
+    bool dead = false;
+    for (int base = 0; base < La; base += 32) {
+      const int aa = base + lane;
+      int mn = 0, mxd = 0;
+      bool any = true;
+      if (aa < La) {
+        int m1 = 0x7fffffff, m2 = -1;
+        for (int c = 0; c < K; ++c) {
+          const int d = my_wdisc[aa * K + c];
+          if (d >= 0) { m1 = min(m1, d); m2 = max(m2, d); }
+        }
+        any = m2 >= 0;
+        mn = any ? m1 : 0;
+        mxd = any ? m2 : 0;
+      }
+      long long plo = mn;
+      int phi = mxd;
+      unsigned dead_m = __ballot_sync(LG_FULL, !any);
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long t1 = __shfl_up_sync(LG_FULL, plo, o);
+        const int t2 = __shfl_up_sync(LG_FULL, phi, o);
+        if (lane >= o) { plo += t1; phi = min(phi + t2, D); }
+      }
+      const bool dead_here = dead || (dead_m & ((2u << lane) - 1u)) != 0;
+      if (aa < La) {
+        const long long lo_v = slo + plo;
+        band_all[aa] = make_int2(dead_here ? 0x3fffffff : (int)min(lo_v, 0x3fffffffll), min(shi + phi, D));
+      }
+      slo += __shfl_sync(LG_FULL, plo, 31);
+      shi = min(shi + __shfl_sync(LG_FULL, phi, 31), D);
+      dead = dead || dead_m != 0;
+    }
+  }
+  if (!wide) {
+    for (int i = tid; i < row; i += NT) { r32a[i] = (i == PAD) ? 0u : INF32; r32b[i] = INF32; }
+  } else {
+    for (int i = tid; i < row; i += NT) { r64a[i] = (i == PAD) ? 0ull : INF64; r64b[i] = INF64; }
+  }
+  // s_bar[p]: completion of the remote cells of rows with parity p (st.async complete_tx)
+  __shared__ __align__(8) uint64_t s_bar[2];
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&s_bar[0])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&s_bar[1])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  LG_T(1);
+  cl_sync();  // every CTA's rows and barriers initialised before any remote push lands
+  LG_T(2);
+  int cur_is_b = 1;
+  uint32_t bph = 0u;  // bit p: parity of s_bar[p]'s next phase
+  const int wbase = cbase + warp * (32 * CPT);
+  const int dclamp = wbase + PAD;
+  const int64_t PDR = (int64_t)NC * NT * CPT;  // PD bytes per layer
+  const int gtid = (int)rank * NT + tid;
+  const uint32_t vb = wide ? 8u : 4u;
+  // row a's candidate pairs, band and max shift, loaded during row a-1 (off the
+  // critical path of the row)
+  uint4 cq[KP2 / 2];
+#pragma unroll
+  for (int c = 0; c < KP2 / 2; ++c) cq[c] = reinterpret_cast<const uint4*>(cand_all)[c];
+  int2 band = band_all[0];
+  int maxd = my_wmaxd[1];
+  for (int a = 0; a < La; ++a) {
+    const int sb = a & 1;
+    // cells of row a this CTA receives: [cbase - maxd, cbase) (clipped at 0)
+    if (tid == 0) {
+      const uint32_t bytes = (uint32_t)min(maxd, cbase) * vb;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                       (uint32_t)__cvta_generic_to_shared(&s_bar[sb])),
+                   "r"(bytes)
+                   : "memory");
+    }
+#ifdef LG_DP_TIMING
+    const long long tr0 = clock64();
+#endif
+    const uint2* cnd = cand_all + (size_t)a * KP2;
+    uint32_t pdw[4] = {0u, 0u, 0u, 0u};
+    const bool live = (wbase + 32 * CPT - 1 >= band.x) && (wbase <= band.y);
+    // highest CTA that reads any cell of this warp in the next row
+    int rtop = min((int)NC - 1, (wbase + 32 * CPT - 1 + maxd) / S);
+#ifdef LG_DP_TIMING
+    if (flags & (1u << 30)) rtop = -1;  // diagnostic only: no pushes (wrong result)
+#endif
+    if (!wide) {
+      const uint32_t* prev = (cur_is_b ? r32a : r32b) + PAD + wbase + lane;
+      uint32_t* cur = (cur_is_b ? r32b : r32a) + PAD + wbase + lane;
+      uint32_t best[CPT];
+      if (live) {
+#pragma unroll
+        for (int c = 0; c < KT; c += 2) {
+          const uint4 q = cq[c >> 1];
+          const uint32_t* pv = prev - min((int)q.x, dclamp);
+#pragma unroll
+          for (int i = 0; i < CPT; ++i)
+            best[i] = (c == 0) ? pv[i * 32] + q.y : __viaddmin_u32(pv[i * 32], q.y, best[i]);
+          if (c + 1 < KT) {
+            const uint32_t* pw = prev - min((int)q.z, dclamp);
+#pragma unroll
+            for (int i = 0; i < CPT; ++i) best[i] = __viaddmin_u32(pw[i * 32], q.w, best[i]);
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < CPT; ++i) {
+          const uint32_t k = best[i];
+          best[i] = min(k, INF32) & ~(uint32_t)kmask;
+          pdw[i >> 2] = put_byte(pdw[i >> 2], k, i & 3);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < CPT; ++i) best[i] = INF32;
+      }
+#pragma unroll
+      for (int i = 0; i < CPT; ++i) cur[i * 32] = best[i];
+#ifdef LG_DP_TIMING
+      t_c += clock64() - tr0 + (best[0] & 0);
+#endif
+      for (int r2 = (int)rank + 1; r2 <= rtop; ++r2) {  // warp-uniform bounds
+        const int need = r2 * S - maxd;                   // r2 reads cells >= need
+        const uint32_t rbar = cl_map(&s_bar[sb], (uint32_t)r2);
+#pragma unroll
+        for (int i = 0; i < CPT; ++i)
+          if (wbase + 32 * i + lane >= need)
+            asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(
+                             cl_map(cur + i * 32, (uint32_t)r2)),
+                         "r"(best[i]), "r"(rbar)
+                         : "memory");
+      }
+    } else {
+      const uint64_t* prev = (cur_is_b ? r64a : r64b) + PAD + wbase + lane;
+      uint64_t* cur = (cur_is_b ? r64b : r64a) + PAD + wbase + lane;
+      const uint64_t* add = add_all + (size_t)a * KT;
+      uint64_t best[CPT];
+#pragma unroll
+      for (int i = 0; i < CPT; ++i) best[i] = ~0ull;
+      if (live) {
+        for (int c = 0; c < KT; ++c) {
+          const uint64_t* pv = prev - min((int)cnd[c].x, dclamp);
+          const uint64_t ak = add[c];
+#pragma unroll
+          for (int i = 0; i < CPT; ++i) best[i] = min(best[i], pv[i * 32] + ak);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < CPT; ++i) {
+        const uint64_t k = best[i];
+        best[i] = (k >= INF64) ? INF64 : (k & ~kmask);
+        pdw[i >> 2] = put_byte(pdw[i >> 2], (uint32_t)k, i & 3);
+        cur[i * 32] = best[i];
+      }
+      for (int r2 = (int)rank + 1; r2 <= rtop; ++r2) {
+        const int need = r2 * S - maxd;
+        const uint32_t rbar = cl_map(&s_bar[sb], (uint32_t)r2);
+#pragma unroll
+        for (int i = 0; i < CPT; ++i)
+          if (wbase + 32 * i + lane >= need)
+            asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(
+                             cl_map(cur + i * 32, (uint32_t)r2)),
+                         "l"(best[i]), "r"(rbar)
+                         : "memory");
+      }
+    }
+    cur_is_b ^= 1;
+    if (a + 1 < La) {
+      const uint4* nq = reinterpret_cast<const uint4*>(cand_all + (size_t)(a + 1) * KP2);
+#pragma unroll
+      for (int c = 0; c < KP2 / 2; ++c) cq[c] = nq[c];
+      band = band_all[a + 1];
+      maxd = my_wmaxd[a + 2];
+    }
+#ifdef LG_DP_TIMING
+    const long long tp0 = clock64();
+    t_p += tp0 - tr0;
+#endif
+    // local cells of row a visible to every warp of this CTA
+    __syncthreads();
+#ifdef LG_DP_TIMING
+    const long long ts1 = clock64();
+    t_s += ts1 - tp0;
+#endif
+    // back-pressure only (no CTA runs a row ahead, so no push lands in a row buffer a
+    // peer still reads); the data itself is ordered by the st.async -> mbarrier path
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+    if (live) pd_store<CPT>(PD + (int64_t)a * PDR + (int64_t)gtid * CPT, pdw);
+    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+#ifdef LG_DP_TIMING
+    t_cl += clock64() - ts1;
+#endif
+    // remote cells of row a landed
+    {
+      const uint32_t ba = (uint32_t)__cvta_generic_to_shared(&s_bar[sb]);
+      const uint32_t par = (bph >> sb) & 1u;
+      asm volatile(
+          "{\n\t.reg .pred done;\n\t"
+          "DPW_%=:\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+          "@!done bra DPW_%=;\n\t}\n" ::"r"(ba),
+          "r"(par)
+          : "memory");
+      bph ^= 1u << sb;
+    }
+#ifdef LG_DP_TIMING
+    t_push += clock64() - tp0;
+#endif
+  }
+  LG_T(3);
+  // ---- line 23: argmin of the last row over this CTA's cells, gathered in rank 0
+  {
+    uint64_t bk = ~0ull;
+    int be = 0x7fffffff;
+    for (int el = tid; el < S; el += NT) {
+      const int e = cbase + el;
+      if (e > D) break;
+      uint64_t v;
+      if (!wide) { const uint32_t x = ((cur_is_b ? r32a : r32b) + PAD)[e]; v = (x >= INF32) ? ~0ull : x; }
+      else { const uint64_t x = ((cur_is_b ? r64a : r64b) + PAD)[e]; v = (x >= INF64) ? ~0ull : x; }
+      if (v < bk) { bk = v; be = e; }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const uint64_t ov = __shfl_xor_sync(LG_FULL, bk, o);
+      const int oe = __shfl_xor_sync(LG_FULL, be, o);
+      if (ov < bk || (ov == bk && oe < be)) { bk = ov; be = oe; }
+    }
+    if (lane == 0) { s_redk[warp] = bk; s_rede[warp] = be; }
+    __syncthreads();
+    if (warp == 0) {
+      bk = (lane < NW) ? s_redk[lane] : ~0ull;
+      be = (lane < NW) ? s_rede[lane] : 0x7fffffff;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const uint64_t ov = __shfl_xor_sync(LG_FULL, bk, o);
+        const int oe = __shfl_xor_sync(LG_FULL, be, o);
+        if (ov < bk || (ov == bk && oe < be)) { bk = ov; be = oe; }
+      }
+      if (lane == 0) {
+        cl_st(cl_map(&s_clk[rank], 0), bk);
+        cl_st(cl_map(&s_cle[rank], 0), (uint32_t)be);
+      }
+    }
+  }
+  cl_sync();  // PD (global) and the gathered argmins visible; peers may exit after this
+  LG_T(4);
+  if (rank != 0) return;
+  // ---- rank 0: backtrack (lines 24-27) through PD, R20 check and summary
+  const int32_t* bdisc = my_wdisc;  // the discretised table (shared memory)
+  int32_t* bch = reinterpret_cast<int32_t*>(smem_raw);  // [La] chosen c per active layer (rows are dead)
+  __syncthreads();
+  // PD byte of (layer a, cell e): CTA r = e / S, warp w, register i, lane
+  auto pd_at = [&](int a, int e) -> int {
+    const int r = e / S, el = e - r * S;
+    const int w = el / (32 * CPT), rr = el - w * (32 * CPT);
+    const int T = r * NT + w * 32 + (rr & 31);
+    return __ldcg(PD + (int64_t)a * PDR + (int64_t)T * CPT + (rr >> 5));
+  };
+  if (warp == 0) {
+    uint64_t k = (lane < (int)NC) ? s_clk[lane] : ~0ull;
+    int ee = (lane < (int)NC) ? s_cle[lane] : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const uint64_t ov = __shfl_xor_sync(LG_FULL, k, o);
+      const int oe = __shfl_xor_sync(LG_FULL, ee, o);
+      if (ov < k || (ov == k && oe < ee)) { k = ov; ee = oe; }
+    }
+    const int used_default = (k == ~0ull);
+    const int cm = pdmask;
+    auto put = [&](int a, int c) {
+      if (lane == 0) bch[a] = c;
+    };
+    if (!used_default) {
+      const int depth = (K < 32 && 1 + K + K * K <= 64) ? 3 : ((K < 32) ? 2 : 1);
+      int lev[2], c1s[2], c2s[2];
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int j = lane + 32 * r;
+        lev[r] = -1; c1s[r] = 0; c2s[r] = 0;
+        if (j == 0) lev[r] = 0;
+        else if (depth >= 2 && j <= K) { lev[r] = 1; c1s[r] = j - 1; }
+        else if (depth >= 3 && j < 1 + K + K * K) { lev[r] = 2; c1s[r] = (j - 1 - K) / K; c2s[r] = (j - 1 - K) % K; }
+      }
+      int e = ee, a = La - 1;
+      auto disc_rows = [&](int ar, int& da, int& db, int& dc, int* off) {
+        da = (lane < K) ? bdisc[ar * K + lane] : 0;
+        db = (lane < K) ? bdisc[(ar - 1) * K + lane] : 0;
+        dc = (lane < K && depth >= 3) ? bdisc[(ar - 2) * K + lane] : 0;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const int d1 = __shfl_sync(LG_FULL, da, c1s[r]);
+          const int d2 = __shfl_sync(LG_FULL, db, c2s[r]);
+          off[r] = (lev[r] == 0) ? 0 : (lev[r] == 1) ? ((d1 >= 0) ? d1 : -1)
+                 : (lev[r] == 2) ? ((d1 >= 0 && d2 >= 0) ? d1 + d2 : -1) : -1;
+        }
+      };
+      if (depth > 1 && a >= depth - 1) {
+        int da, db, dc, off[2];
+        disc_rows(a, da, db, dc, off);
+        for (;;) {
+          int v[2];
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            v[r] = 0;
+            if (off[r] >= 0 && e - off[r] >= 0) v[r] = pd_at(a - lev[r], e - off[r]);
+          }
+          const int an = a - depth;
+          int nda = 0, ndb = 0, ndc = 0, noff[2] = {-1, -1};
+          if (an >= depth - 1) disc_rows(an, nda, ndb, ndc, noff);
+          auto val = [&](int j) {
+            const int x0 = __shfl_sync(LG_FULL, v[0], j & 31), x1 = __shfl_sync(LG_FULL, v[1], j & 31);
+            return (j < 32 ? x0 : x1) & cm;
+          };
+          const int c0 = val(0);
+          const int c1 = val(1 + c0);
+          put(a, c0);
+          put(a - 1, c1);
+          int de = __shfl_sync(LG_FULL, da, c0) + __shfl_sync(LG_FULL, db, c1);
+          if (depth >= 3) {
+            const int c2 = val(1 + K + c0 * K + c1);
+            put(a - 2, c2);
+            de += __shfl_sync(LG_FULL, dc, c2);
+          }
+          e -= de;
+          a = an;
+          if (a < depth - 1) break;
+          da = nda; db = ndb; dc = ndc; off[0] = noff[0]; off[1] = noff[1];
+        }
+      }
+      for (; a >= 0; --a) {
+        const int c = pd_at(a, e) & cm;
+        put(a, c);
+        e -= bdisc[a * K + c];
+      }
+    }
+    if (lane == 0) s_La = used_default;
+  }
+  __syncthreads();
+  if (!s_La)
+    for (int a = tid; a < La; a += NT) choice[act[a]] = bch[a];
+  __syncthreads();
+  double* sm_ce = reinterpret_cast<double*>(smem_raw);
+  int64_t* sm_cb = reinterpret_cast<int64_t*>(sm_ce + La);
+  int used_default = s_La;
+  if (used_default) {
+    for (int a = tid; a < La; a += NT) choice[act[a]] = default_idx[act[a]];
+    __syncthreads();
+  }
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int a = tid; a < La; a += NT) {
+      const int l = act[a];
+      const int c = used_default ? default_idx[l] : choice[l];
+      sm_ce[a] = metric(err[(int64_t)l * K + c], flags);
+      sm_cb[a] = bits[(int64_t)l * K + c];
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int64_t pb = 0;
+      double pe = 0.0;
+      int a = 0;
+      for (; a + 4 <= La; a += 4) {
+        const double v0 = sm_ce[a], v1 = sm_ce[a + 1], v2 = sm_ce[a + 2], v3 = sm_ce[a + 3];
+        pb += sm_cb[a] + sm_cb[a + 1] + sm_cb[a + 2] + sm_cb[a + 3];
+        pe = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(pe, v0), v1), v2), v3);
+      }
+      for (; a < La; ++a) { pb += sm_cb[a]; pe = __dadd_rn(pe, sm_ce[a]); }
+      if (!used_default && (pb > s_defbits || pe > emax)) {
+        s_La = 1;
+      } else {
+        lgreco_solve_info inf = {};
+        inf.emax = emax;
+        inf.total_err = pe;
+        inf.total_bits = pb;
+        inf.default_bits = s_defbits;
+        inf.used_default = used_default;
+        inf.n_active = La;
+        inf.status = LGRECO_OK;
+        *info = inf;
+        s_La = -1;
+      }
+    }
+    __syncthreads();
+    if (s_La < 0) break;
+    used_default = 1;
+    for (int a = tid; a < La; a += NT) choice[act[a]] = default_idx[act[a]];
+    __syncthreads();
+  }
+#ifdef LG_DP_TIMING
+  LG_T(5);
+  if (tid == 0)
+    printf("dp cluster timing (cycles, rank 0): prelude %lld init %lld rows %lld (%lld/layer: compute %lld push %lld "
+           "syncthreads %lld cluster %lld all-waits %lld) argmin %lld back+summary %lld\n", tstamp[1] - tstamp[0],
+           tstamp[2] - tstamp[1], tstamp[3] - tstamp[2], (tstamp[3] - tstamp[2]) / (La ? La : 1), t_c / La,
+           (t_p - t_c) / La, t_s / La, t_cl / La, t_push / (La ? La : 1), tstamp[4] - tstamp[3], tstamp[5] - tstamp[4]);
+#endif
+}
+
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 size_t solve_workspace_bytes(int L, int K, int D) {
-  return align_up((size_t)L * std::max(D + 1, PD_ROW)) + align_up(sizeof(int32_t) * (size_t)(L + 1)) +
-         align_up(sizeof(int64_t) * 2 * (size_t)(D + 1)) + align_up(sizeof(int32_t) * (size_t)L * K) +
-         align_up(sizeof(uint64_t) * (size_t)L * K);
+  return align_up((size_t)L * std::max(D + 1 + CL_MAX * 32 * 8, PD_ROW)) + align_up(sizeof(int32_t) * (size_t)(L + 1)) +
+         align_up(sizeof(int64_t) * 2 * (size_t)(D + 1)) + align_up(sizeof(int32_t) * (size_t)L * K * CL_MAX) +
+         align_up(sizeof(uint64_t) * (size_t)L * K * CL_MAX) + align_up(sizeof(int32_t) * (size_t)(L + 1) * CL_MAX);
+}
+
+// Cluster launch (k_solve_cl) when the shapes fit: K <= 16, CPT in {2, 4, 8}, two
+// 64-bit full-length rows within 200 KB of shared memory, and an 8-CTA cluster of that
+// size can be resident.  Returns cudaErrorNotSupported (nothing launched) otherwise.
+static cudaError_t launch_solve_cluster(const SolveArgs& a, uint8_t* pd, int32_t* act, int32_t* wdisc, uint64_t* wadd,
+                                        int32_t* wmaxd, cudaStream_t st) {
+  if (a.K < 1 || a.K > 16) return cudaErrorNotSupported;
+  int NC = CL_MAX;
+  if (const char* env = getenv("LGRECO_DP_NC")) NC = std::max(2, std::min(CL_MAX, atoi(env)));
+  int cpt = 2;
+  while (cpt <= 8 && (int64_t)NC * DP_THREADS * cpt < (int64_t)a.D + 1) cpt *= 2;
+  if (const char* env = getenv("LGRECO_DP_CPT")) cpt = std::max(cpt, atoi(env));
+  if (cpt > 8) return cudaErrorNotSupported;
+  const int nw = (int)(((int64_t)a.D + 1 + NC * 32 * cpt - 1) / (NC * 32 * cpt));
+  const int nt = nw * 32;
+  const int S = nt * cpt;
+  // two 64-bit rows, then the per-layer tables: costs (8 B), disc (4 B), max disc (4 B),
+  // candidate pairs (8 B x KP2), 64-bit keys (8 B x KT), band (8 B)
+  const int kt0 = a.K <= 4 ? 4 : a.K == 5 ? 5 : a.K <= 7 ? 7 : a.K <= 8 ? 8 : 16;
+  const size_t smem = (size_t)16 * (32 * cpt + (size_t)NC * S) + (size_t)12 * a.L * a.K + (size_t)4 * (a.L + 4) + 16 +
+                      (size_t)a.L * (8 * ((kt0 + 2) & ~1) + 8 * kt0 + 8);
+  if (smem > 220 * 1024 || (size_t)24 * a.L + 64 > (size_t)16 * (32 * cpt + (size_t)NC * S)) return cudaErrorNotSupported;
+  const int kt = a.K <= 4 ? 4 : a.K == 5 ? 5 : a.K <= 7 ? 7 : a.K <= 8 ? 8 : 16;
+  void (*fn)(const double*, const int64_t*, int, int, const int32_t*, const int32_t*, int, uint32_t, int32_t*,
+             lgreco_solve_info*, uint8_t*, int32_t*, int32_t*, uint64_t*, int32_t*) = nullptr;
+#define LG_CL(C, KT) if (cpt == C && kt == KT) fn = k_solve_cl<C, KT>;
+#define LG_CL_K(C) LG_CL(C, 4) LG_CL(C, 5) LG_CL(C, 7) LG_CL(C, 8) LG_CL(C, 16)
+  LG_CL_K(2) LG_CL_K(4) LG_CL_K(8)
+#undef LG_CL_K
+#undef LG_CL
+  if (!fn) return cudaErrorNotSupported;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) { cudaGetLastError(); return cudaErrorNotSupported; }
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = NC;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(NC, 1, 1);
+  cfg.blockDim = dim3(nt, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int nclusters = 0;
+  e = cudaOccupancyMaxActiveClusters(&nclusters, (const void*)fn, &cfg);
+  if (e != cudaSuccess || nclusters < 1) {
+    if (getenv("LGRECO_DEBUG")) fprintf(stderr, "lgreco: cluster occupancy %d (%s)\n", nclusters, cudaGetErrorString(e));
+    cudaGetLastError();
+    return cudaErrorNotSupported;
+  }
+  return cudaLaunchKernelEx(&cfg, fn, a.err, a.bits, a.L, a.K, a.default_idx, a.compress, a.D, a.flags, a.choice,
+                            a.info, pd, act, wdisc, wadd, wmaxd);
 }
 
 cudaError_t launch_solve(const SolveArgs& a, void* ws, cudaStream_t st) {
   uint8_t* base = static_cast<uint8_t*>(ws);
   uint8_t* pd = base;
-  const size_t pd_bytes = align_up((size_t)a.L * std::max(a.D + 1, PD_ROW));
+  const size_t pd_bytes = align_up((size_t)a.L * std::max(a.D + 1 + CL_MAX * 32 * 8, PD_ROW));
   int32_t* act = reinterpret_cast<int32_t*>(base + pd_bytes);
   int64_t* grows = reinterpret_cast<int64_t*>(base + pd_bytes +
                                               align_up(sizeof(int32_t) * (size_t)(a.L + 1)));
   int32_t* wdisc = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(grows) +
                                               align_up(sizeof(int64_t) * 2 * (size_t)(a.D + 1)));
   uint64_t* wadd = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(wdisc) +
-                                               align_up(sizeof(int32_t) * (size_t)a.L * a.K));
+                                               align_up(sizeof(int32_t) * (size_t)a.L * a.K * CL_MAX));
+  int32_t* wmaxd = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(wadd) +
+                                              align_up(sizeof(uint64_t) * (size_t)a.L * a.K * CL_MAX));
+  if (!(a.flags & LGRECO_SOLVE_SINGLE_CTA)) {
+    const cudaError_t ce = launch_solve_cluster(a, pd, act, wdisc, wadd, wmaxd, st);
+    if (ce != cudaErrorNotSupported) return ce;
+    if (getenv("LGRECO_DEBUG")) fprintf(stderr, "lgreco: cluster solve not used (L=%d K=%d D=%d)\n", a.L, a.K, a.D);
+  }
   const int W1 = a.D + 1;
   const int cpt = (W1 + DP_THREADS - 1) / DP_THREADS;
   // fast path: two padded 32-bit rows or two 64-bit rows in smem (see k_solve_fast)

@@ -16,8 +16,12 @@ if len(sys.argv) > 1 and sys.argv[1] == "timing":
 
 dev = torch.device("cuda:0")
 D = 10000
+if os.environ.get("DP_ONLY_C4"):
+    pass
 specs = [("C4", lgreco.QSGD, W.QSGD_BITS, 2), ("C5", lgreco.QSGD, W.QSGD_BITS, 2),
          ("C3", lgreco.TOPK, W.TOPK_PPM_C3, 9), ("C2", lgreco.POWERSGD, W.PSGD_RANKS_C2, 2)]
+if os.environ.get("DP_ONLY_C4"):
+    specs = specs[:1]
 for name, fam, params, di in specs:
     layers = W.config_layers(name)
     N = W.total_numel(layers)
@@ -35,17 +39,19 @@ for name, fam, params, di in specs:
     ch = torch.empty(L, dtype=torch.int32, device=dev)
     info = torch.empty(48, dtype=torch.uint8, device=dev)
     ws = torch.empty(lgreco.solve_workspace_bytes(L, K, D), dtype=torch.uint8, device=dev)
-    ts = []
-    for it in range(6):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        lgreco.solve(err, bits, dflt, comp, D=D, choice=ch, info=info, workspace=ws)
-        b.record()
-        torch.cuda.synchronize()
-        ts.append(a.elapsed_time(b))
-    inf = lgreco.read_info(info)
-    print(f"{name}: L={L} La={inf.n_active} K={K} solve ms {min(ts[1:]):.4f} (all {[round(t, 4) for t in ts]}) "
-          f"used_default={inf.used_default} bits {inf.total_bits}/{inf.default_bits}", flush=True)
+    for fl in ((0, 4) if not os.environ.get('DP_NOPUSH') else (1 << 30,)):  # 4 = LGRECO_SOLVE_SINGLE_CTA
+        ts = []
+        for it in range(6):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            lgreco.solve(err, bits, dflt, comp, D=D, flags=fl, choice=ch, info=info, workspace=ws)
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        inf = lgreco.read_info(info)
+        print(f"{name}: flags={fl} L={L} La={inf.n_active} K={K} solve ms {min(ts[1:]):.4f} "
+              f"(all {[round(t, 4) for t in ts]}) used_default={inf.used_default} "
+              f"bits {inf.total_bits}/{inf.default_bits} choice {ch[:8].tolist()}", flush=True)
     ctx.close()
     del g, ef
     torch.cuda.empty_cache()

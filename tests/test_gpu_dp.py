@@ -33,8 +33,10 @@ def _table(rng, L, K, zero_frac=0.0):
     return err, bits
 
 
-@pytest.mark.parametrize("flags", [0, 1, 2, 3])
+@pytest.mark.parametrize("flags", [0, 1, 2, 3, 4, 7])
 def test_random_tables(lg, ref, flags):
+    """flags bit 2 (LGRECO_SOLVE_SINGLE_CTA) selects the one-CTA kernel, otherwise the
+    8-CTA cluster kernel runs (K <= 16): both must reproduce the oracle exactly."""
     rng = np.random.default_rng(flags)
     for trial in range(40):
         L = int(rng.integers(1, 30))
@@ -43,7 +45,7 @@ def test_random_tables(lg, ref, flags):
         err, bits = _table(rng, L, K, zero_frac=0.2 if trial % 4 == 0 else 0.0)
         dflt = rng.integers(0, K, L).astype(np.int32)
         comp = (rng.random(L) < 0.8).astype(np.int32) if trial % 3 == 0 else None
-        st, c_ref, i_ref = ref.solve(err, bits, dflt, comp, D=D, flags=flags)
+        st, c_ref, i_ref = ref.solve(err, bits, dflt, comp, D=D, flags=flags & 3)
         c_gpu, i_gpu = _run(lg, err, bits, dflt, comp, D, flags)
         assert st == 0 and i_gpu.status == 0
         assert list(c_gpu) == list(c_ref)
