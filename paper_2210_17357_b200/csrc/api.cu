@@ -182,7 +182,7 @@ int lgreco_ctx_create(lgreco_ctx** out, const lgreco_layer* layers, int32_t L, c
   c->nchunks = (int)chunks.size();
   c->nchunks_all = (int)chunks_all.size();
   // K1 (B = 128): chunks of <= 4 buckets (one quad) of the compressed layers, handed
-  // out to the resident warps (3 CTAs of 8 warps per SM) by a ticket counter: the
+  // out to the resident warps (occupancy x SMs CTAs of 8 warps) by a ticket counter: the
   // fine grain keeps every warp busy to the end (a quad is ~1/14 of a warp's share)
   std::vector<lg::ProfChunk> qchunks;
   std::vector<int32_t> lqc0(L + 1, 0);
@@ -196,7 +196,7 @@ int lgreco_ctx_create(lgreco_ctx** out, const lgreco_layer* layers, int32_t L, c
     lqc0[L] = (int32_t)qchunks.size();
     int nsm = 148, dev = 0;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    c->nqwarps = nsm * 3 * 8;
+    c->nqwarps = nsm * 4 * 8;  // upper bound; the launcher sizes the grid by the kernel's occupancy
     c->nqchunks = (int)qchunks.size();
   }
   std::vector<float> cs(c->K);

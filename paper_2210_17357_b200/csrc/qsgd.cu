@@ -20,6 +20,8 @@
 // misaligned layers and B > 128 take the generic path.
 #include <math.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -27,6 +29,9 @@ namespace lg {
 
 constexpr int QP_THREADS = 256;
 constexpr int QP_WARPS = QP_THREADS / 32;
+#ifndef QP_XU_CEIL
+#define QP_XU_CEIL 7  // candidates of the K1 fast path whose ceil runs on the XU pipe
+#endif
 
 // ---------------------------------------------------------------------------
 // small helpers
@@ -169,7 +174,11 @@ __device__ __forceinline__ void prof_cand16(const float* x, float mn, uint32_t c
         const float xv = x[4 * i + s];
         const float v = __fmul_rn(__fsub_rn(xv, mn), inv[j]);
         const float w = __fmaf_ru(uw[s], -5.9604644775390625e-08f, v);
-        const float q = fminf(__fsub_rn(__fadd_ru(w, MAGIC), MAGIC), cs.s[j]);
+        // ceil(w): the last QP_XU_CEIL candidates use FRND.CEIL on the conversion
+        // pipe (idle otherwise), the others the two-FADD magic on the FMA pipe (the
+        // kernel's bottleneck): both are exact; -0 from FRND changes no error
+        const float cw = (j >= KT - QP_XU_CEIL) ? ceilf(w) : __fsub_rn(__fadd_ru(w, MAGIC), MAGIC);
+        const float q = fminf(cw, cs.s[j]);
         float d = __fsub_rn(xv, __fmaf_rn(q, unit[j], mn));
         if (SCALED) d = __fmul_rn(d, S);  // exact power-of-two rescale: d^2 stays normal
         acc[j] = __fmaf_rn(d, d, acc[j]);
@@ -364,8 +373,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                : "memory");
 }
 
+#ifndef QP_MINB
+#define QP_MINB 3  // resident CTAs per SM of the K1 fast kernel (register budget 65536 / (256 * QP_MINB))
+#endif
 template <int KT>
-__global__ void __launch_bounds__(QP_THREADS, 3)
+__global__ void __launch_bounds__(QP_THREADS, QP_MINB)
 k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const DevLayer* __restrict__ layers,
              const ProfChunk* __restrict__ qchunks, int nqc, unsigned* __restrict__ ticket, const CandS cs, int K,
              uint32_t k0, uint32_t k1, uint32_t rankfield, uint32_t step, int ptr_aligned,
@@ -958,11 +970,15 @@ cudaError_t launch_qprofile(const QProfileArgs& a, cudaStream_t st) {
     if (a.ev0) cudaEventRecord(a.ev0, st);
     if (quads) {
       const size_t smem = (size_t)QP_WARPS * 2 * 4096;
-      const int grid = a.nqwarps / QP_WARPS;
+      const int nsm = a.nqwarps / (QP_WARPS * 4);  // nqwarps = SMs x 4 CTAs x 8 warps (an upper bound)
 #define LG_QQ(KT)                                                                                              \
   {                                                                                                            \
     cudaError_t e = cudaFuncSetAttribute(k_qprofile_q<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
     if (e != cudaSuccess) return e;                                                                            \
+    static int occ = 0;                                                                                        \
+    if (occ == 0 && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_qprofile_q<KT>, QP_THREADS, smem) != \
+                     cudaSuccess || occ < 1)) occ = 1;                                                          \
+    const int grid = std::max(1, std::min(a.nqwarps / QP_WARPS, nsm * occ));                                    \
     k_qprofile_q<KT><<<grid, QP_THREADS, smem, st>>>(a.g, a.e, a.layers, a.qchunks, a.nqchunks, a.ticket, a.cs, a.K, \
                                                     a.k0, a.k1, a.rankfield, a.step, a.ptr_aligned, a.partial);  \
   }

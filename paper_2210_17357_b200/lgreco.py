@@ -13,7 +13,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblgreco.so")
+LIB_PATH = os.environ.get("LGRECO_LIB") or os.path.join(_HERE, "liblgreco.so")  # override: diagnostics only
 
 OK, EINVAL, ENONFINITE, EINFEASIBLE, ECUDA, ENCCL, ENOMEM, EUNSUPPORTED = 0, -1, -2, -3, -4, -5, -6, -7
 QSGD, TOPK, POWERSGD = 0, 1, 2

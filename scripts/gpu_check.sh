@@ -10,7 +10,7 @@ timeout 600 python bench.py --steps ${BENCH_STEPS:-50} --warmup 5 > gpurun_out/b
 if [ -z "$NO_NCU" ]; then
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
   python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-extras > gpurun_out/bench_ncu.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_qprofile|k_qpack|k_solve|k_qunpack" -s 6 -c 3 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_qprofile_q|k_qpack|k_solve_cl|k_qprofile_reduce" -s 8 -c 4 \
   -o gpurun_out/prof_full -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-extras > gpurun_out/ncu_full.log 2>&1
 fi
 echo done
