@@ -769,11 +769,11 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
            int32_t* __restrict__ choice, lgreco_solve_info* __restrict__ info, uint8_t* __restrict__ PD,
            int32_t* __restrict__ act, int32_t* __restrict__ wdisc, uint64_t* __restrict__ wadd,
            int32_t* __restrict__ wmaxd) {
-  static_assert(KT > 0 && KT <= 16 && (CPT == 1 || CPT == 2 || CPT == 4 || CPT == 8 || CPT == 16), "cluster DP");
+  static_assert(KT >= 0 && KT <= 16 && (CPT == 1 || CPT == 2 || CPT == 4 || CPT == 8 || CPT == 16), "cluster DP");
+  // KT > 0: K <= KT candidates, tables of the whole recursion in shared memory;
+  // KT == 0: K <= 256 candidates in groups of 16 (k_solve_fast's grouped keys), tables
+  // in global memory (this CTA's copy of the workspace), staged per row
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ __align__(16) uint2 s_cand[2][(KT + 2) & ~1];  // even stride: 16-byte pair reads
-  __shared__ uint64_t s_add[2][KT];
-  __shared__ int2 s_band[2];
   __shared__ int s_La, s_status, s_wide, s_cbits;
   __shared__ double s_emax;
   __shared__ int64_t s_defbits;
@@ -857,9 +857,19 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
   //      sum of per-layer max cost, per-layer max admissible disc
   constexpr int PAD = 32 * CPT;
   const int row = PAD + (int)NC * S;
-  uint64_t* my_wadd = reinterpret_cast<uint64_t*>(smem_raw + (size_t)16 * row);  // [La*K] raw costs
-  int32_t* my_wdisc = reinterpret_cast<int32_t*>(my_wadd + (size_t)La * K);        // [La*K]
-  int32_t* my_wmaxd = my_wdisc + (size_t)La * K;                                   // [La+1]
+  unsigned char* tail = smem_raw + (size_t)16 * row;
+  uint64_t* my_wadd;  // [La*K] raw costs
+  int32_t* my_wdisc;  // [La*K] discretised errors
+  int32_t* my_wmaxd;  // [La+1] largest admissible disc per layer (0 past the end)
+  if constexpr (KT > 0) {
+    my_wadd = reinterpret_cast<uint64_t*>(tail);
+    my_wdisc = reinterpret_cast<int32_t*>(my_wadd + (size_t)La * K);
+    my_wmaxd = my_wdisc + (size_t)La * K;
+  } else {
+    my_wadd = wadd + (size_t)rank * L * K;
+    my_wdisc = wdisc + (size_t)rank * L * K;
+    my_wmaxd = reinterpret_cast<int32_t*>(tail);
+  }
   uint64_t gg = 0, mx_part = 0;
   int bad = 0;
   if (tid == 0) my_wmaxd[La] = 0;
@@ -910,7 +920,7 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
       g = g ? (g & (~g + 1)) : 1;
       s_g[0] = g;
       const uint64_t mx = mxs >> (__ffsll((long long)g) - 1);
-      s_wide = (mx >= (1ull << (30 - s_cbits))) ? 1 : 0;
+      s_wide = (mx >= (1ull << (30 - ((KT > 0) ? s_cbits : 4)))) ? 1 : 0;
       if (mx >= (1ull << (62 - s_cbits)) && s_status == LGRECO_OK) s_status = LGRECO_EINVAL;
     }
   }
@@ -928,9 +938,9 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
     return;
   }
   const bool wide = s_wide;
-  const int kb = cbits;
+  const int kb = (wide || KT > 0) ? cbits : 4;  // key bits below the value
   const uint64_t kmask = (1ull << kb) - 1;
-  const int pdmask = (int)((1u << cbits) - 1u);
+  const int pdmask = (!wide && KT == 0) ? 0xFF : (int)((1u << cbits) - 1u);  // PD byte -> c
   auto keyed = [&](uint64_t ub, int c) -> uint64_t { return ((ub >> gsh) << kb) | (uint64_t)(c & (int)kmask); };
   // two full-length rows (PAD INF cells + NC*S cells), in every CTA
   uint32_t* r32a = reinterpret_cast<uint32_t*>(smem_raw);
@@ -945,9 +955,9 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
   constexpr int KP2 = (KT + 2) & ~1;
   uint2* cand_all = reinterpret_cast<uint2*>(
       (reinterpret_cast<uintptr_t>(my_wmaxd + La + 1) + 15) & ~static_cast<uintptr_t>(15));  // [La][KP2], 16-B aligned
-  uint64_t* add_all = reinterpret_cast<uint64_t*>(cand_all + (size_t)La * KP2);  // [La][KT]
+  uint64_t* add_all = reinterpret_cast<uint64_t*>(cand_all + (size_t)La * (KT > 0 ? KP2 : 0));  // [La][KT]
   int2* band_all = reinterpret_cast<int2*>(add_all + (size_t)La * KT);          // [La]
-  for (int i = tid; i < La * KP2; i += NT) {
+  for (int i = tid; KT > 0 && i < La * KP2; i += NT) {
     const int aa = i / KP2, c = i - aa * KP2;
     const int32_t d = (c < K) ? my_wdisc[aa * K + c] : -1;
     const bool ok = c < K && d >= 0;
@@ -1008,6 +1018,18 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&s_bar[1])));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  // KT == 0: the candidates of row a staged in s_ck/s_ak[a & 1] (keyed as above)
+  __shared__ __align__(16) uint2 s_ck[2][KT > 0 ? 2 : 256];
+  __shared__ uint64_t s_ak[2][KT > 0 ? 1 : 256];
+  auto stage0 = [&](int32_t d, uint64_t ub, int slot) {
+    if (tid < K) {
+      const bool ok = d >= 0;
+      const uint64_t k = ok ? keyed(ub, tid) : 0;
+      s_ck[slot][tid] = make_uint2(ok ? (uint32_t)d : 0u, ok ? (uint32_t)k : INF32);
+      s_ak[slot][tid] = ok ? k : INF64;
+    }
+  };
+  if (KT == 0) stage0((tid < K) ? my_wdisc[tid] : -1, (tid < K) ? my_wadd[tid] : 0, 0);
   LG_T(1);
   cl_sync();  // every CTA's rows and barriers initialised before any remote push lands
   LG_T(2);
@@ -1022,7 +1044,7 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
   // critical path of the row)
   uint4 cq[KP2 / 2];
 #pragma unroll
-  for (int c = 0; c < KP2 / 2; ++c) cq[c] = reinterpret_cast<const uint4*>(cand_all)[c];
+  for (int c = 0; c < KP2 / 2; ++c) cq[c] = (KT > 0) ? reinterpret_cast<const uint4*>(cand_all)[c] : make_uint4(0, 0, 0, 0);
   int2 band = band_all[0];
   int maxd = my_wmaxd[1];
   for (int a = 0; a < La; ++a) {
@@ -1039,6 +1061,9 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
     const long long tr0 = clock64();
 #endif
     const uint2* cnd = cand_all + (size_t)a * KP2;
+    int32_t nd = -1;  // KT == 0: next layer's candidate tid, staged after this row
+    uint64_t nub = 0;
+    if (KT == 0 && tid < K && a + 1 < La) { nd = my_wdisc[(a + 1) * K + tid]; nub = my_wadd[(a + 1) * K + tid]; }
     uint32_t pdw[4] = {0u, 0u, 0u, 0u};
     const bool live = (wbase + 32 * CPT - 1 >= band.x) && (wbase <= band.y);
     // highest CTA that reads any cell of this warp in the next row
@@ -1050,7 +1075,32 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
       const uint32_t* prev = (cur_is_b ? r32a : r32b) + PAD + wbase + lane;
       uint32_t* cur = (cur_is_b ? r32b : r32a) + PAD + wbase + lane;
       uint32_t best[CPT];
-      if (live) {
+      if (live && KT == 0) {
+        uint32_t bgrp[CPT];
+#pragma unroll
+        for (int i = 0; i < CPT; ++i) { best[i] = 0xFFFFFFFFu; bgrp[i] = 0; }
+        for (int c0 = 0; c0 < K; c0 += 16) {
+          const int cn = min(16, K - c0);
+          uint32_t gk[CPT];
+#pragma unroll
+          for (int i = 0; i < CPT; ++i) gk[i] = 0xFFFFFFFFu;
+          for (int c = 0; c < cn; ++c) {
+            const uint2 cd = s_ck[sb][c0 + c];
+            const uint32_t* pv = prev - min((int)cd.x, dclamp);
+#pragma unroll
+            for (int i = 0; i < CPT; ++i) gk[i] = __viaddmin_u32(pv[i * 32], cd.y, gk[i]);
+          }
+#pragma unroll
+          for (int i = 0; i < CPT; ++i)
+            if ((gk[i] & ~15u) < (best[i] & ~15u)) { best[i] = gk[i]; bgrp[i] = (uint32_t)c0; }
+        }
+#pragma unroll
+        for (int i = 0; i < CPT; ++i) {
+          const uint32_t k = best[i];
+          best[i] = min(k, INF32) & ~15u;
+          pdw[i >> 2] = put_byte(pdw[i >> 2], bgrp[i] + (k & 15u), i & 3);
+        }
+      } else if (live) {
 #pragma unroll
         for (int c = 0; c < KT; c += 2) {
           const uint4 q = cq[c >> 1];
@@ -1098,9 +1148,9 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
 #pragma unroll
       for (int i = 0; i < CPT; ++i) best[i] = ~0ull;
       if (live) {
-        for (int c = 0; c < KT; ++c) {
-          const uint64_t* pv = prev - min((int)cnd[c].x, dclamp);
-          const uint64_t ak = add[c];
+        for (int c = 0; c < (KT > 0 ? KT : K); ++c) {
+          const uint64_t* pv = prev - min((int)(KT > 0 ? cnd[c].x : s_ck[sb][c].x), dclamp);
+          const uint64_t ak = (KT > 0) ? add[c] : s_ak[sb][c];
 #pragma unroll
           for (int i = 0; i < CPT; ++i) best[i] = min(best[i], pv[i * 32] + ak);
         }
@@ -1125,10 +1175,11 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
       }
     }
     cur_is_b ^= 1;
+    if (KT == 0 && a + 1 < La) stage0(nd, nub, sb ^ 1);  // slot last read in row a-1
     if (a + 1 < La) {
       const uint4* nq = reinterpret_cast<const uint4*>(cand_all + (size_t)(a + 1) * KP2);
 #pragma unroll
-      for (int c = 0; c < KP2 / 2; ++c) cq[c] = nq[c];
+      for (int c = 0; c < KP2 / 2; ++c) if (KT > 0) cq[c] = nq[c];
       band = band_all[a + 1];
       maxd = my_wmaxd[a + 2];
     }
@@ -1369,27 +1420,29 @@ size_t solve_workspace_bytes(int L, int K, int D) {
 // size can be resident.  Returns cudaErrorNotSupported (nothing launched) otherwise.
 static cudaError_t launch_solve_cluster(const SolveArgs& a, uint8_t* pd, int32_t* act, int32_t* wdisc, uint64_t* wadd,
                                         int32_t* wmaxd, cudaStream_t st) {
-  if (a.K < 1 || a.K > 16) return cudaErrorNotSupported;
+  if (a.K < 1 || a.K > 256) return cudaErrorNotSupported;
   int NC = CL_MAX;
   if (const char* env = getenv("LGRECO_DP_NC")) NC = std::max(2, std::min(CL_MAX, atoi(env)));
   int cpt = 2;
   while (cpt <= 8 && (int64_t)NC * DP_THREADS * cpt < (int64_t)a.D + 1) cpt *= 2;
   if (const char* env = getenv("LGRECO_DP_CPT")) cpt = std::max(cpt, atoi(env));
   if (cpt > 8) return cudaErrorNotSupported;
-  const int nw = (int)(((int64_t)a.D + 1 + NC * 32 * cpt - 1) / (NC * 32 * cpt));
+  // (KT == 0 stages one candidate per thread: at least K threads)
+  const int nw = std::max((int)(((int64_t)a.D + 1 + NC * 32 * cpt - 1) / (NC * 32 * cpt)), (a.K + 31) / 32);
   const int nt = nw * 32;
   const int S = nt * cpt;
   // two 64-bit rows, then the per-layer tables: costs (8 B), disc (4 B), max disc (4 B),
   // candidate pairs (8 B x KP2), 64-bit keys (8 B x KT), band (8 B)
-  const int kt0 = a.K <= 4 ? 4 : a.K == 5 ? 5 : a.K <= 7 ? 7 : a.K <= 8 ? 8 : 16;
-  const size_t smem = (size_t)16 * (32 * cpt + (size_t)NC * S) + (size_t)12 * a.L * a.K + (size_t)4 * (a.L + 4) + 16 +
-                      (size_t)a.L * (8 * ((kt0 + 2) & ~1) + 8 * kt0 + 8);
+  const int kt0 = a.K <= 4 ? 4 : a.K == 5 ? 5 : a.K <= 7 ? 7 : a.K <= 8 ? 8 : a.K <= 16 ? 16 : 0;
+  // KT == 0: only the max-disc and band tables live in shared memory
+  const size_t smem = (size_t)16 * (32 * cpt + (size_t)NC * S) + (size_t)4 * (a.L + 4) + 16 + (size_t)8 * a.L +
+                      (kt0 > 0 ? (size_t)12 * a.L * a.K + (size_t)a.L * (8 * ((kt0 + 2) & ~1) + 8 * kt0) : 0);
   if (smem > 220 * 1024 || (size_t)24 * a.L + 64 > (size_t)16 * (32 * cpt + (size_t)NC * S)) return cudaErrorNotSupported;
-  const int kt = a.K <= 4 ? 4 : a.K == 5 ? 5 : a.K <= 7 ? 7 : a.K <= 8 ? 8 : 16;
+  const int kt = kt0;
   void (*fn)(const double*, const int64_t*, int, int, const int32_t*, const int32_t*, int, uint32_t, int32_t*,
              lgreco_solve_info*, uint8_t*, int32_t*, int32_t*, uint64_t*, int32_t*) = nullptr;
 #define LG_CL(C, KT) if (cpt == C && kt == KT) fn = k_solve_cl<C, KT>;
-#define LG_CL_K(C) LG_CL(C, 4) LG_CL(C, 5) LG_CL(C, 7) LG_CL(C, 8) LG_CL(C, 16)
+#define LG_CL_K(C) LG_CL(C, 4) LG_CL(C, 5) LG_CL(C, 7) LG_CL(C, 8) LG_CL(C, 16) LG_CL(C, 0)
   LG_CL_K(2) LG_CL_K(4) LG_CL_K(8)
 #undef LG_CL_K
 #undef LG_CL

@@ -591,42 +591,40 @@ k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const Dev
   finish();
 }
 
-// K1b: per layer, fixed-order sum of its chunks' partials (all K values of a chunk row
-// per thread, rows strided over 512 threads, then a fixed warp tree and a fixed sum
-// over warps), sqrt.
-constexpr int QR_THREADS = 512;
+// K1b: per layer, fixed-order sum of its chunks' partials, sqrt.  The layer's rows
+// [c0, c1) x K are one contiguous run of doubles; thread t < T = K floor(1024/K) sums
+// the elements t, t + T, ... (all of candidate t mod K; coalesced, 4 loads in flight),
+// then thread j < K adds the T/K thread sums of candidate j in thread order.
+constexpr int QR_THREADS = 1024;
 __global__ void __launch_bounds__(QR_THREADS)
 k_qprofile_reduce(const DevLayer* __restrict__ layers, const int32_t* __restrict__ layer_chunk0,
                   const double* __restrict__ partial, const int32_t* __restrict__ params, int K, int B,
                   double* __restrict__ err, int64_t* __restrict__ bits) {
-  __shared__ double sm[16][QR_THREADS / 32];
+  __shared__ double sm[QR_THREADS];
   const int l = blockIdx.x;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const DevLayer ly = layers[l];
   const int c0 = layer_chunk0[l], c1 = layer_chunk0[l + 1];
   const int64_t nb = (ly.numel + B - 1) / B;
-  double a[16];
-#pragma unroll
-  for (int j = 0; j < 16; ++j) a[j] = 0.0;
-  for (int c = c0 + threadIdx.x; c < c1; c += QR_THREADS) {
-    const double* row = partial + (int64_t)c * K;
-#pragma unroll
-    for (int j = 0; j < 16; ++j)
-      if (j < K) a[j] += __ldg(row + j);
-  }
-#pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    if (j < K) {
-      const double v = warp_sum_d(a[j]);
-      if (lane == 0) sm[j][warp] = v;
+  const int T = K * (QR_THREADS / K);
+  const int t = threadIdx.x;
+  const double* base = partial + (int64_t)c0 * K;
+  const int64_t n = (int64_t)(c1 - c0) * K;
+  double acc = 0.0;
+  if (t < T) {
+    int64_t i = t;
+    for (; i + 3 * (int64_t)T < n; i += 4 * (int64_t)T) {
+      const double v0 = __ldg(base + i), v1 = __ldg(base + i + T), v2 = __ldg(base + i + 2 * T),
+                   v3 = __ldg(base + i + 3 * T);
+      acc += v0; acc += v1; acc += v2; acc += v3;
     }
+    for (; i < n; i += T) acc += __ldg(base + i);
   }
+  sm[t] = acc;
   __syncthreads();
-  const int j = threadIdx.x;
+  const int j = t;
   if (j < K) {
     double s = 0.0;
-#pragma unroll
-    for (int w = 0; w < QR_THREADS / 32; ++w) s += sm[j][w];
+    for (int u = j; u < T; u += K) s += sm[u];
     if (ly.compress) {
       err[(int64_t)l * K + j] = sqrt(s);
       bits[(int64_t)l * K + j] = nb * ((int64_t)B * params[j] + 64);

@@ -82,8 +82,9 @@ def test_worked_example(lg):
     assert list(c) == [2, 0] and info.total_bits == 140
 
 
+@pytest.mark.parametrize("single", [False, True])
 @pytest.mark.parametrize("K", [1, 3, 5, 7, 8, 12, 16, 17, 33, 100])
-def test_narrow_keys_ties_and_bands(lg, ref, K):
+def test_narrow_keys_ties_and_bands(lg, ref, K, single):
     """Small costs (32-bit keys: the K <= 16 unrolled path, the grouped K > 16 path),
     quantised errors so that many (layer, candidate) pairs tie in both disc and cost
     (tie-breaks R19), and a few inadmissible candidates (disc > D, R17) so that the
@@ -99,7 +100,7 @@ def test_narrow_keys_ties_and_bands(lg, ref, K):
         err[:, K - 1] = np.minimum(err[:, K - 1], 1.0)
         comp = (rng.random(L) < 0.85).astype(np.int32)
         st, c_ref, i_ref = ref.solve(err, bits, dflt, comp, D=D)
-        c_gpu, i_gpu = _run(lg, err, bits, dflt, comp, D, 0)
+        c_gpu, i_gpu = _run(lg, err, bits, dflt, comp, D, 4 if single else 0)
         assert st == 0 and i_gpu.status == 0
         assert list(c_gpu) == list(c_ref), (K, D)
         assert (i_gpu.total_bits, i_gpu.used_default) == (i_ref.total_bits, i_ref.used_default)
