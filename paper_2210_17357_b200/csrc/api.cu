@@ -184,14 +184,16 @@ int lgreco_ctx_create(lgreco_ctx** out, const lgreco_layer* layers, int32_t L, c
   // K1 (B = 128): chunks of <= 4 buckets (one quad) of the compressed layers, handed
   // out to the resident warps (occupancy x SMs CTAs of 8 warps) by a ticket counter: the
   // fine grain keeps every warp busy to the end (a quad is ~1/14 of a warp's share)
-  std::vector<lg::ProfChunk> qchunks;
+  std::vector<lg::QInfo> qchunks;
   std::vector<int32_t> lqc0(L + 1, 0);
   if (c->B == 128) {
     for (int l = 0; l < L; ++l) {
       lqc0[l] = (int32_t)qchunks.size();
       if (!layers[l].compress) continue;
       const int64_t nb = (layers[l].numel + 127) / 128;
-      for (int64_t j = 0; j < nb; j += 4) qchunks.push_back(lg::ProfChunk{l, (int32_t)std::min<int64_t>(4, nb - j), j});
+      for (int64_t j = 0; j < nb; j += 4)
+        qchunks.push_back(lg::QInfo{layers[l].offset + 128 * j, (uint32_t)(c->bucket0[l] + j),
+                                    (int32_t)std::min<int64_t>(512, layers[l].numel - 128 * j)});
     }
     lqc0[L] = (int32_t)qchunks.size();
     int nsm = 148, dev = 0;
@@ -222,9 +224,9 @@ int lgreco_ctx_create(lgreco_ctx** out, const lgreco_layer* layers, int32_t L, c
   LG_ALLOC(c->d_chunks_all, sizeof(lg::ProfChunk) * std::max(1, c->nchunks_all));
   LG_ALLOC(c->d_layer_chunk0, sizeof(int32_t) * (L + 1));
   LG_ALLOC(c->d_partial, sizeof(double) * (size_t)std::max(1, std::max(c->nchunks, c->nqchunks)) * c->K);
-  LG_ALLOC(c->d_qchunks, sizeof(lg::ProfChunk) * std::max(1, c->nqchunks));
+  LG_ALLOC(c->d_qinfo, sizeof(lg::QInfo) * std::max(1, c->nqchunks));
   LG_ALLOC(c->d_layer_qchunk0, sizeof(int32_t) * (L + 1));
-  LG_ALLOC(c->d_ticket, 2 * sizeof(unsigned));
+  LG_ALLOC(c->d_ticket, 17 * 64 * sizeof(unsigned));  // K1 part counters + done counter, 256 B apart
   LG_ALLOC(c->d_flag, sizeof(unsigned));
   LG_ALLOC(c->d_plan, sizeof(lg::DevPlan) * L);
   if (world > 1 && c->family == LGRECO_QSGD) {
@@ -248,9 +250,9 @@ int lgreco_ctx_create(lgreco_ctx** out, const lgreco_layer* layers, int32_t L, c
                         cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = cudaMemcpyAsync(c->d_layer_chunk0, lc0.data(), sizeof(int32_t) * (L + 1), cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess && c->nqchunks)
-    e = cudaMemcpyAsync(c->d_qchunks, qchunks.data(), sizeof(lg::ProfChunk) * c->nqchunks, cudaMemcpyHostToDevice, st);
+    e = cudaMemcpyAsync(c->d_qinfo, qchunks.data(), sizeof(lg::QInfo) * c->nqchunks, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = cudaMemcpyAsync(c->d_layer_qchunk0, lqc0.data(), sizeof(int32_t) * (L + 1), cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess) e = cudaMemsetAsync(c->d_ticket, 0, 2 * sizeof(unsigned), st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(c->d_ticket, 0, 17 * 64 * sizeof(unsigned), st);
   if (e == cudaSuccess) e = cudaMemsetAsync(c->d_flag, 0, sizeof(unsigned), st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) {
@@ -288,7 +290,7 @@ void lgreco_ctx_destroy(lgreco_ctx* c) {
   if (c->comm) ncclCommDestroy(c->comm);
   cudaFree(c->d_layers); cudaFree(c->d_bucket0); cudaFree(c->d_cand_s); cudaFree(c->d_params);
   cudaFree(c->d_chunks); cudaFree(c->d_chunks_all); cudaFree(c->d_layer_chunk0); cudaFree(c->d_partial);
-  cudaFree(c->d_qchunks); cudaFree(c->d_layer_qchunk0); cudaFree(c->d_ticket); cudaFree(c->d_flag);
+  cudaFree(c->d_qinfo); cudaFree(c->d_layer_qchunk0); cudaFree(c->d_ticket); cudaFree(c->d_flag);
   cudaFree(c->d_plan); cudaFree(c->d_pay1); cudaFree(c->d_recv); cudaFree(c->d_pay2);
   if (c->h_plan_pinned) cudaFreeHost(c->h_plan_pinned);
   if (c->h_choice_pinned) cudaFreeHost(c->h_choice_pinned);
@@ -347,7 +349,7 @@ int lgreco_profile(lgreco_ctx* c, const float* d_g, const float* d_ef, uint64_t 
     lg::QProfileArgs a{d_g, d_ef, c->d_layers, c->L, c->d_chunks, c->nchunks, c->d_layer_chunk0,
                        c->B, c->cs, c->d_params, c->K, k0, k1, (uint32_t)c->rank, (uint32_t)step,
                        c->d_partial, d_err, d_bits};
-    a.qchunks = c->d_qchunks; a.nqchunks = c->nqchunks; a.layer_qchunk0 = c->d_layer_qchunk0;
+    a.qinfo = c->d_qinfo; a.nqchunks = c->nqchunks; a.layer_qchunk0 = c->d_layer_qchunk0;
     a.nqwarps = c->nqwarps; a.ticket = c->d_ticket;
     a.ptr_aligned = ((reinterpret_cast<uintptr_t>(d_g) | reinterpret_cast<uintptr_t>(d_ef)) & 15) == 0;
     if (c->timing && c->nchunks > 0) {

@@ -57,7 +57,7 @@ struct lgreco_ctx {
   int32_t* d_layer_chunk0 = nullptr;
   double* d_partial = nullptr;
   // K1 at B = 128: persistent warps over 32-bucket chunks of the compressed layers
-  lg::ProfChunk* d_qchunks = nullptr;
+  lg::QInfo* d_qinfo = nullptr;
   int nqchunks = 0;
   int32_t* d_layer_qchunk0 = nullptr;
   int nqwarps = 0;

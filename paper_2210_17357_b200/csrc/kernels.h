@@ -14,6 +14,11 @@ struct ProfChunk {
 };
 
 struct CandS { float s[16]; };
+
+// K1 (B = 128) work unit: one quad (4 buckets of one layer): flat element offset of its
+// first element, global index of its first bucket (Philox counter base, mod 2^32),
+// number of valid elements (512 unless the layer ends inside the quad).
+struct QInfo { int64_t elem0; uint32_t gb0; int32_t nvalid; };
   // s_j = 2^{b_j} - 1, passed by value (constant bank)
 
 struct QProfileArgs {
@@ -26,7 +31,7 @@ struct QProfileArgs {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // when set: recorded around the K1 launch
   // B == 128: persistent quad kernel over 32-bucket chunks (qchunks, per-layer
   // layer_qchunk0[L+1]), nqwarps resident warps, ticket[2] zeroed counters
-  const ProfChunk* qchunks = nullptr; int nqchunks = 0; const int32_t* layer_qchunk0 = nullptr;
+  const QInfo* qinfo = nullptr; int nqchunks = 0; const int32_t* layer_qchunk0 = nullptr;
   int nqwarps = 0; unsigned* ticket = nullptr; int ptr_aligned = 0;
 };
 

@@ -373,33 +373,50 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                : "memory");
 }
 
+constexpr int QP_NPART = 16;  // K1 ticket counters (parts of the quad range), 256 B apart
 #ifndef QP_MINB
 #define QP_MINB 3  // resident CTAs per SM of the K1 fast kernel (register budget 65536 / (256 * QP_MINB))
 #endif
 template <int KT>
 __global__ void __launch_bounds__(QP_THREADS, QP_MINB)
-k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const DevLayer* __restrict__ layers,
-             const ProfChunk* __restrict__ qchunks, int nqc, unsigned* __restrict__ ticket, const CandS cs, int K,
-             uint32_t k0, uint32_t k1, uint32_t rankfield, uint32_t step, int ptr_aligned,
-             double* __restrict__ partial) {
+k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const QInfo* __restrict__ qinfo, int nqc,
+             unsigned* __restrict__ ticket, const CandS cs, int K, uint32_t k0, uint32_t k1, uint32_t rankfield,
+             uint32_t step, int ptr_aligned, double* __restrict__ partial) {
   extern __shared__ __align__(128) unsigned char qsm[];
   __shared__ __align__(8) uint64_t bars[QP_WARPS][2];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int grp = lane >> 3, l8 = lane & 7;
   // stage b of this warp: g at qsm + (2 warp + b) 4096 bytes, e 2048 bytes after it
   auto stage_g = [&](int b) { return reinterpret_cast<float*>(qsm + (size_t)(warp * 2 + b) * 4096); };
-  auto grab = [&]() -> int {
+  // Work hand-out: the quads are split into QP_NPART contiguous parts, each with its own
+  // ticket counter (one hot address would serialise ~50K atomics in one L2 slice);
+  // a warp starts on part (global warp id mod QP_NPART) and moves on when its part is
+  // exhausted.  Grabs are split: lane 0 issues the atomic, the broadcast (which waits
+  // for it) happens one quad later, so the atomic's latency hides behind a quad.
+  const int gw = blockIdx.x * QP_WARPS + warp;
+  int part = gw % QP_NPART, tried = 0;
+  auto plo = [&](int p) -> int { return (int)(((int64_t)nqc * p) / QP_NPART); };
+  auto grab_issue = [&]() -> unsigned {
     unsigned v = 0;
-    if (lane == 0) v = atomicAdd(&ticket[0], 1u);
-    return (int)__shfl_sync(LG_FULL, v, 0);
+    if (lane == 0) v = atomicAdd(&ticket[part * 64], 1u);
+    return v;
   };
-  auto finish = [&]() {  // after this warp's failing grab
-    if (lane == 0 && atomicAdd(&ticket[1], 1u) == gridDim.x * QP_WARPS - 1u) {
-      atomicExch(&ticket[0], 0u);
-      atomicExch(&ticket[1], 0u);
+  auto resolve = [&](unsigned v) -> int {
+    int q = plo(part) + (int)__shfl_sync(LG_FULL, v, 0);
+    while (q >= plo(part + 1)) {  // part exhausted: next part (synchronously; rare)
+      if (++tried >= QP_NPART) return nqc;
+      part = (part + 1) % QP_NPART;
+      q = plo(part) + (int)__shfl_sync(LG_FULL, grab_issue(), 0);
+    }
+    return q;
+  };
+  auto finish = [&]() {  // after this warp found every part exhausted
+    if (lane == 0 && atomicAdd(&ticket[QP_NPART * 64], 1u) == gridDim.x * QP_WARPS - 1u) {
+      for (int p2 = 0; p2 <= QP_NPART; ++p2) atomicExch(&ticket[p2 * 64], 0u);
     }
   };
-  int c = grab();
+  auto load_info = [&](int ci) -> QInfo { return (ci < nqc) ? qinfo[ci] : QInfo{0, 0u, 0}; };
+  int c = resolve(grab_issue());
   if (c >= nqc) { finish(); return; }
   if (lane == 0) {
     bar_init(&bars[warp][0], 1);
@@ -415,57 +432,41 @@ k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const Dev
     if (j < K && j == l8) gs = cs.s[j];
     if (j < K && j == l8 + 8) gs2 = cs.s[j];
   }
-  // current chunk: layer offset, numel (< 2^31), first bucket (global), first bucket in
-  // the layer, bucket count
-  int64_t ly_off, ly_b0;
-  int ly_n, ch_first, ch_nbk;
-  auto load_chunk = [&](int ci) {
-    const ProfChunk ch = qchunks[ci];
-    ly_off = layers[ch.layer].offset;
-    ly_b0 = layers[ch.layer].bucket0;
-    ly_n = (int)layers[ch.layer].numel;
-    ch_first = (int)ch.first;
-    ch_nbk = ch.nbk;
-  };
-  // bulk copies of the quad whose first bucket (in its layer) is fb, into stage b
-  // (lane 0), when regular (aligned layer and pointers, 4 full buckets)
-  auto issue = [&](int64_t off, int n, int fb, int b) -> bool {
-    if (!(pal && (off & 3) == 0 && (fb + 4) * 128 <= n)) return false;
+  // bulk copies of quad `in` into stage b (lane 0) when regular: aligned, 4 full buckets
+  auto issue = [&](const QInfo& in, int b) -> bool {
+    if (!(pal && (in.elem0 & 3) == 0 && in.nvalid == 512)) return false;
     if (lane == 0) {
-      const int64_t o = off + (int64_t)fb * 128;
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier generic reads of the stage
       bar_expect_tx(&bars[warp][b], tx);
-      bulk_g2s(stage_g(b), g + o, 2048u, &bars[warp][b]);
-      if (e) bulk_g2s(stage_g(b) + 512, e + o, 2048u, &bars[warp][b]);
+      bulk_g2s(stage_g(b), g + in.elem0, 2048u, &bars[warp][b]);
+      if (e) bulk_g2s(stage_g(b) + 512, e + in.elem0, 2048u, &bars[warp][b]);
     }
     return true;
   };
-  load_chunk(c);
-  int cn = grab();
+  // queue: c (computing), nA (its quad prefetched during c), nB (info load in flight)
+  int nA = resolve(grab_issue());
+  bool failed = nA >= nqc;
+  int nB = nqc;
+  if (!failed) { nB = resolve(grab_issue()); failed = nB >= nqc; }
+  QInfo ic = qinfo[c], ia = load_info(nA), ibq = load_info(nB);
   uint32_t phase = 0u;  // bit b: parity of stage b's next completion
   int b = 0;
-  bool inflight = issue(ly_off, ly_n, ch_first, 0);
+  bool inflight = issue(ic, 0);
   double acc[KT];
 #pragma unroll
   for (int j = 0; j < KT; ++j) acc[j] = 0.0;
 
   for (;;) {
-    const int nq = (ch_nbk + 3) >> 2;
-    for (int k = 0; k < nq; ++k, b ^= 1) {
+    unsigned raw = 0;
+    const bool pend = !failed;
+    if (pend) raw = grab_issue();
+    {
       const bool cur_regular = inflight;
-      // prefetch the next quad into the other stage (its previous contents were consumed
-      // in the previous iteration; __syncwarp orders those reads before the copy)
+      // prefetch quad nA into the other stage (its previous contents were consumed in
+      // the previous iteration; __syncwarp orders those reads before the copy)
       __syncwarp();
-      if (k + 1 < nq) {
-        inflight = issue(ly_off, ly_n, ch_first + 4 * (k + 1), b ^ 1);
-      } else if (cn < nqc) {
-        const ProfChunk nc = qchunks[cn];
-        inflight = issue(layers[nc.layer].offset, (int)layers[nc.layer].numel, (int)nc.first, b ^ 1);
-      } else {
-        inflight = false;
-      }
-      const int jb = ch_first + 4 * k + grp;  // bucket within the layer
-      const bool valid = 4 * k + grp < ch_nbk;
+      const bool next_inflight = (nA < nqc) ? issue(ia, b ^ 1) : false;
+      const bool valid = grp * 128 < ic.nvalid;
       float x[16];
       if (cur_regular) {
         bar_wait(&bars[warp][b], (phase >> b) & 1u);
@@ -484,16 +485,16 @@ k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const Dev
           }
         }
       } else {
-        // masked direct loads: element 32i + 4*l8 + s of bucket jb
-        const int base = jb * 128 + 4 * l8;
-        const float* gl = g + ly_off;
-        const float* el = e ? e + ly_off : nullptr;
+        // masked direct loads: element 32i + 4*l8 + s of bucket grp of the quad
+        const int base = grp * 128 + 4 * l8;
+        const float* gl = g + ic.elem0;
+        const float* el = e ? e + ic.elem0 : nullptr;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
 #pragma unroll
           for (int s2 = 0; s2 < 4; ++s2) {
             const int idx = base + 32 * i + s2;
-            const bool ok = valid && idx < ly_n;
+            const bool ok = idx < ic.nvalid;
             float v = 0.f;
             if (ok) {
               v = __ldg(gl + idx);
@@ -513,8 +514,8 @@ k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const Dev
         mn = INFINITY; mx = -INFINITY;
 #pragma unroll
         for (int s2 = 0; s2 < 16; ++s2) {
-          const int idx = jb * 128 + 4 * l8 + 32 * (s2 >> 2) + (s2 & 3);
-          if (valid && idx < ly_n) { mn = fmin_nan(mn, x[s2]); mx = fmax_nan(mx, x[s2]); }
+          const int idx = grp * 128 + 4 * l8 + 32 * (s2 >> 2) + (s2 & 3);
+          if (idx < ic.nvalid) { mn = fmin_nan(mn, x[s2]); mx = fmax_nan(mx, x[s2]); }
         }
       }
 #pragma unroll
@@ -525,8 +526,8 @@ k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const Dev
       if (!cur_regular) {
 #pragma unroll
         for (int s2 = 0; s2 < 16; ++s2) {
-          const int idx = jb * 128 + 4 * l8 + 32 * (s2 >> 2) + (s2 & 3);
-          if (!(valid && idx < ly_n)) x[s2] = mn;  // invalid -> t = 0, q = 0, d = 0
+          const int idx = grp * 128 + 4 * l8 + 32 * (s2 >> 2) + (s2 & 3);
+          if (!(idx < ic.nvalid)) x[s2] = mn;  // invalid -> t = 0, q = 0, d = 0
         }
       }
       float my_inv, my_unit, my_inv2 = 0.f, my_unit2 = 0.f;
@@ -538,7 +539,7 @@ k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const Dev
         inv[j] = __shfl_sync(LG_FULL, j < 8 ? my_inv : my_inv2, (lane & ~7) + (j & 7));
         unit[j] = __shfl_sync(LG_FULL, j < 8 ? my_unit : my_unit2, (lane & ~7) + (j & 7));
       }
-      const uint32_t c0 = (uint32_t)((ly_b0 + jb) * 32 + l8);
+      const uint32_t c0 = (ic.gb0 + (uint32_t)grp) * 32u + (uint32_t)l8;
       float S;
       double S2inv;
       const bool small = bucket_scale(mn, mx, S, S2inv);
@@ -549,6 +550,8 @@ k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const Dev
 #pragma unroll
         for (int j = 0; j < KT; ++j) acc[j] = __dadd_rn(acc[j], __dmul_rn((double)a2[j], S2inv));
       }
+      inflight = next_inflight;
+      b ^= 1;
     }
     // chunk done: fixed-order warp reduction into its slot
     if (KT <= 8) {
@@ -583,10 +586,11 @@ k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const Dev
     }
 #pragma unroll
     for (int j = 0; j < KT; ++j) acc[j] = 0.0;
-    if (cn >= nqc) break;
-    c = cn;
-    load_chunk(c);
-    cn = grab();
+    if (nA >= nqc) break;
+    c = nA; ic = ia;
+    nA = nB; ia = ibq;
+    if (pend) { nB = resolve(raw); failed = nB >= nqc; ibq = load_info(nB); }
+    else nB = nqc;
   }
   finish();
 }
@@ -977,8 +981,8 @@ cudaError_t launch_qprofile(const QProfileArgs& a, cudaStream_t st) {
     if (occ == 0 && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_qprofile_q<KT>, QP_THREADS, smem) != \
                      cudaSuccess || occ < 1)) occ = 1;                                                          \
     const int grid = std::max(1, std::min(a.nqwarps / QP_WARPS, nsm * occ));                                    \
-    k_qprofile_q<KT><<<grid, QP_THREADS, smem, st>>>(a.g, a.e, a.layers, a.qchunks, a.nqchunks, a.ticket, a.cs, a.K, \
-                                                    a.k0, a.k1, a.rankfield, a.step, a.ptr_aligned, a.partial);  \
+    k_qprofile_q<KT><<<grid, QP_THREADS, smem, st>>>(a.g, a.e, a.qinfo, a.nqchunks, a.ticket, a.cs, a.K, a.k0,  \
+                                                    a.k1, a.rankfield, a.step, a.ptr_aligned, a.partial);        \
   }
       switch (a.K) {
         case 4: LG_QQ(4); break;
