@@ -32,10 +32,11 @@ from paper_2210_17357_b200 import workloads as W  # noqa: E402
 METRIC = "gradient GB/s profile+solve+compress+allreduce"
 WORKLOAD = "C4 ResNet-50/ImageNet gradient (25,557,032 fp32), QSGD bits 2..8 default 4, bucket 128, D=10000"
 D_BINS = 10000
-# K1 algorithmic lane-ops per compressed element: per candidate
-# 9 (t*inv, floor, frac, u<f, +step, min s, fma dec, x-dec, fma d^2) x 7 candidates = 63,
-# shared 23 (g+e, +0, x-mn, 2 min/max, Philox4x32-10 15 per element, u = 3)
-K1_OPS_PER_ELEM = 86
+# K1 algorithmic lane-ops per compressed element, counted on the
+# cheapest exact form of the pinned sequence R6: per candidate 7 (v = t*inv, w = RU(v - u),
+# ceil, min s, fma dec, x - dec, fma d^2) x 7 candidates = 49; per element 21 (g + e,
+# x - mn, 2 min/max, Philox4x32-10 15 per element, u word shift + convert 2)
+K1_OPS_PER_ELEM = 70
 SEED = 0x5EED
 
 
