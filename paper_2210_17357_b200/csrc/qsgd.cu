@@ -373,6 +373,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                : "memory");
 }
 
+#ifndef QK_UNROLL
+#define QK_UNROLL 4  // K5 fast path: buckets per warp iteration (loads in flight)
+#endif
 constexpr int QP_NPART = 16;  // K1 ticket counters (parts of the quad range), 256 B apart
 #ifndef QP_MINB
 #define QP_MINB 3  // resident CTAs per SM of the K1 fast kernel (register budget 65536 / (256 * QP_MINB))
@@ -743,22 +746,27 @@ k_qpack(const float* __restrict__ g, float* __restrict__ ef, uint8_t* __restrict
   const float s_b = (float)((1u << b) - 1u);
   const bool fast_layer = aligned && B == 128;
   int bi = warp;
-  // ---- fast path, two buckets per iteration for memory-level parallelism
+  // ---- fast path, QK_UNROLL buckets per iteration (all loads issued first) for
+  //      memory-level parallelism
   if (fast_layer) {
-    for (; bi + QP_WARPS < ch.nbk; bi += 2 * QP_WARPS) {
-      const int64_t jbA = ch.first + bi, jbB = jbA + QP_WARPS;
-      if ((jbB + 1) * 128 > ly.numel) break;  // B bucket not full: finish in the loop below
-      const int64_t baseA = ly.offset + jbA * 128 + 4 * lane, baseB = ly.offset + jbB * 128 + 4 * lane;
-      const float4 gA = ld4(g + baseA), gB = ld4(g + baseB);
-      const float4 eA = ef ? ld4(ef + baseA) : make_float4(0.f, 0.f, 0.f, 0.f);
-      const float4 eB = ef ? ld4(ef + baseB) : make_float4(0.f, 0.f, 0.f, 0.f);
-      const X4 xA = canon4(gA, eA), xB = canon4(gB, eB);
-      pack_bucket_fast(xA, b, ly.bucket0 + jbA, rankfield, step, k0, k1, lane,
-                       payload ? payload + pl.pay_off + jbA * (int64_t)pl.rec_bytes : nullptr, ef, dec_out,
-                       baseA, bad);
-      pack_bucket_fast(xB, b, ly.bucket0 + jbB, rankfield, step, k0, k1, lane,
-                       payload ? payload + pl.pay_off + jbB * (int64_t)pl.rec_bytes : nullptr, ef, dec_out,
-                       baseB, bad);
+    constexpr int U = QK_UNROLL;
+    for (; bi + (U - 1) * QP_WARPS < ch.nbk; bi += U * QP_WARPS) {
+      const int64_t jb0 = ch.first + bi;
+      if ((jb0 + (U - 1) * QP_WARPS + 1) * 128 > ly.numel) break;  // last bucket not full: loop below
+      X4 xs[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t base = ly.offset + (jb0 + u * QP_WARPS) * 128 + 4 * lane;
+        xs[u] = canon4(ld4(g + base), ef ? ld4(ef + base) : make_float4(0.f, 0.f, 0.f, 0.f));
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t jb = jb0 + u * QP_WARPS;
+        const int64_t base = ly.offset + jb * 128 + 4 * lane;
+        pack_bucket_fast(xs[u], b, ly.bucket0 + jb, rankfield, step, k0, k1, lane,
+                         payload ? payload + pl.pay_off + jb * (int64_t)pl.rec_bytes : nullptr, ef, dec_out,
+                         base, bad);
+      }
     }
   }
   for (; bi < ch.nbk; bi += QP_WARPS) {
