@@ -798,6 +798,16 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
   int32_t* sm_act = sm_flag + L;
   double* sm_de = reinterpret_cast<double*>(sm_act + L);
   double* sm_dea = sm_de + L;
+  // the whole (err, bits) table in one global round trip (every later prelude read is
+  // shared memory) when it fits in front of the rows' space
+  constexpr int PADC = 32 * CPT;
+  const bool pre = (size_t)(24 + 16 * K) * L + 64 <= (size_t)16 * (PADC + (int)NC * S);
+  double* sm_err = sm_dea + L;
+  int64_t* sm_bits = reinterpret_cast<int64_t*>(sm_err + (pre ? (size_t)L * K : 0));
+  if (pre)
+    for (int i = tid; i < L * K; i += NT) { sm_err[i] = __ldg(err + i); sm_bits[i] = __ldg(bits + i); }
+  const double* t_err = pre ? sm_err : err;
+  const int64_t* t_bits = pre ? sm_bits : bits;
   if (tid == 0) s_status = LGRECO_OK;
   if (tid < 32) { s_redk[tid] = 0; s_g[tid] = 0; }
   __syncthreads();
@@ -810,7 +820,7 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
     if (rank == 0) choice[l] = -1;
     if (f) {
       if (d < 0 || d >= K) { bad_def = 1; sm_de[l] = 0.0; }
-      else { sm_de[l] = metric(err[(int64_t)l * K + d], flags); db_part += bits[(int64_t)l * K + d]; }
+      else { sm_de[l] = metric(t_err[(int64_t)l * K + d], flags); db_part += t_bits[(int64_t)l * K + d]; }
     }
   }
   if (__any_sync(LG_FULL, bad_def) && lane == 0) atomicExch(&s_status, LGRECO_EINVAL);
@@ -818,6 +828,7 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
   for (int o = 16; o; o >>= 1) db_part += __shfl_xor_sync(LG_FULL, db_part, o);
   if (lane == 0) s_redk[warp] = (uint64_t)db_part;
   __syncthreads();
+  LG_T(6);
   if (warp == 0) {
     int La = 0;
     for (int base = 0; base < L; base += 32) {
@@ -852,6 +863,7 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
   __syncthreads();
   const int La = s_La;
   const double emax = s_emax;
+  LG_T(7);
   // ---- validation, discretisation (Alg.1 lines 3-5) into this CTA's shared memory
   //      (tail region after the two rows; identical in every CTA), OR of the costs,
   //      sum of per-layer max cost, per-layer max admissible disc
@@ -878,8 +890,8 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
     uint64_t m = 0;
     int dm = 0;
     for (int c = lane; c < K; c += 32) {
-      const double v = err[(int64_t)l * K + c];
-      const int64_t b = bits[(int64_t)l * K + c];
+      const double v = t_err[(int64_t)l * K + c];
+      const int64_t b = t_bits[(int64_t)l * K + c];
       if (!isfinite(v) || v < 0.0) bad |= 1;
       if (b < 0) bad |= 2;
       const uint64_t ub = (uint64_t)(b < 0 ? 0 : b);
@@ -899,6 +911,7 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
     if (lane == 0) my_wmaxd[a] = dm;
   }
   bad = __reduce_or_sync(LG_FULL, bad);
+  LG_T(8);
 #pragma unroll
   for (int o = 16; o; o >>= 1) gg |= __shfl_xor_sync(LG_FULL, gg, o);
   if (lane == 0) {
@@ -966,6 +979,7 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
     if (c < KT) add_all[aa * KT + c] = ok ? k : INF64;
   }
   __syncthreads();  // the prelude's shared staging (front of smem) is dead from here
+  LG_T(9);
   // bands: running sums of the smallest / largest admissible disc (exact reachable
   // set bounds).  Warp 0 scans the layers 32 at a time; a layer with no admissible
   // candidate empties every later band (lo = INF).
@@ -1399,6 +1413,9 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
   }
 #ifdef LG_DP_TIMING
   LG_T(5);
+  if (tid == 0)
+    printf("dp cluster prelude phases: flags %lld compact+emax %lld disc %lld gcd+cand %lld\n", tstamp[6] - tstamp[0],
+           tstamp[7] - tstamp[6], tstamp[8] - tstamp[7], tstamp[9] - tstamp[8]);
   if (tid == 0)
     printf("dp cluster timing (cycles, rank 0): prelude %lld init %lld rows %lld (%lld/layer: compute %lld push %lld "
            "syncthreads %lld cluster %lld all-waits %lld) argmin %lld back+summary %lld\n", tstamp[1] - tstamp[0],

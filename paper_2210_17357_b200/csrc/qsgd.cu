@@ -619,19 +619,25 @@ k_qprofile_reduce(const DevLayer* __restrict__ layers, const int32_t* __restrict
   double acc = 0.0;
   if (t < T) {
     int64_t i = t;
-    for (; i + 3 * (int64_t)T < n; i += 4 * (int64_t)T) {
-      const double v0 = __ldg(base + i), v1 = __ldg(base + i + T), v2 = __ldg(base + i + 2 * T),
-                   v3 = __ldg(base + i + 3 * T);
-      acc += v0; acc += v1; acc += v2; acc += v3;
+    for (; i + 7 * (int64_t)T < n; i += 8 * (int64_t)T) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = __ldg(base + i + u * (int64_t)T);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc += v[u];
     }
     for (; i < n; i += T) acc += __ldg(base + i);
   }
   sm[t] = acc;
   __syncthreads();
-  const int j = t;
-  if (j < K) {
+  // warp w sums candidate j = w, w + 32, ...: lanes take the T/K thread sums in a fixed
+  // strided order, then a fixed xor tree
+  const int lane = t & 31, w = t >> 5;
+  for (int j = w; j < K; j += QR_THREADS / 32) {
     double s = 0.0;
-    for (int u = j; u < T; u += K) s += sm[u];
+    for (int u = lane; u < T / K; u += 32) s += sm[j + K * u];
+    s = warp_sum_d(s);
+    if (lane != 0) continue;
     if (ly.compress) {
       err[(int64_t)l * K + j] = sqrt(s);
       bits[(int64_t)l * K + j] = nb * ((int64_t)B * params[j] + 64);
