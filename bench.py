@@ -358,6 +358,9 @@ def run_extras(dev, rank, world, stream, l2_flush, nccl_dist):
     specs = [("C2", lgreco.POWERSGD, W.PSGD_RANKS_C2, 2, "ResNet-18 CIFAR-10 PowerSGD r{1,2,4,8,16}"),
              ("C3", lgreco.TOPK, W.TOPK_PPM_C3, 9, "Transformer-XL TopK 0.1%..10%"),
              ("C5", lgreco.QSGD, W.QSGD_BITS, 2, "GPT-2-medium-like QSGD 2..8 bits")]
+    only = os.environ.get("LG_EXTRAS")  # diagnostics: comma list of config names to run
+    if only:
+        specs = [sp for sp in specs if sp[0] in only.split(",")]
     res = {}
     for name, fam, params, dflt_i, desc in specs:
         layers = W.config_layers(name)

@@ -78,29 +78,49 @@ __device__ __forceinline__ uint32_t warp_sum_u32(uint32_t v) {
 // ---------------------------------------------------------------------------
 // P1: level-1 histogram (counts + fixed-point x^2 sums), CTA-private, two copies
 // ---------------------------------------------------------------------------
+// Per-lane update of the CTA-private level-1 histogram: the count and, with WS, the
+// fixed-point M^2 >> 16 (< 2^32) as two 16-bit halves in 32-bit counters (a copy sees
+// <= TK_CHUNK/2 = 2^13 keys: each half-sum < 2^29) -- 32-bit shared atomics are ~4x
+// faster than 64-bit ones here.  (Warp aggregation by match.any + redux was measured
+// 4.7x slower on C3.)
+template <bool WS>
+__device__ __forceinline__ void h1_add(uint32_t* scnt, uint32_t* shi, uint32_t* slo, uint32_t b, uint32_t key,
+                                       bool active) {
+  if (!active) return;
+  atomicAdd(&scnt[b], 1u);
+  if (WS) {
+    const uint32_t v = (uint32_t)fx_sq(key);
+    atomicAdd(&shi[b], v >> 16);
+    atomicAdd(&slo[b], v & 0xFFFFu);
+  }
+}
+
+template <bool WS>
 __global__ void __launch_bounds__(TK_THREADS)
 k_tk_pass1(const float* __restrict__ g, const float* __restrict__ e, TkArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
-  uint32_t* scnt = reinterpret_cast<uint32_t*>(smem);                               // [2][2048]
-  unsigned long long* ssum = reinterpret_cast<unsigned long long*>(smem + 2 * 2048 * 4);  // [2][2048]
-  for (int i = threadIdx.x; i < 2 * 2048; i += TK_THREADS) { scnt[i] = 0; ssum[i] = 0; }
+  uint32_t* scnt = reinterpret_cast<uint32_t*>(smem);  // [2][2048]
+  uint32_t* shi = scnt + 2 * 2048;                      // [2][2048] (WS)
+  uint32_t* slo = shi + 2 * 2048;                       // [2][2048] (WS)
+  for (int i = threadIdx.x; i < 2 * 2048; i += TK_THREADS) { scnt[i] = 0; if (WS) { shi[i] = 0; slo[i] = 0; } }
   __syncthreads();
   const TChunk ch = a.chunks[blockIdx.x];
   const DevLayer ly = a.layers[a.clayer[ch.cidx]];
   const int cp = (threadIdx.x >> 7) & 1;
   uint32_t zc = 0, bad = 0;
+  uint32_t* mc = scnt + cp * 2048;
+  uint32_t* mh = shi + cp * 2048;
+  uint32_t* ml = slo + cp * 2048;
   for_chunk(g, e, ly, ch, [&](int64_t, float x) {
     const uint32_t key = tkey(x);
     if (key == 0) { ++zc; return; }
-    const uint32_t b = key >> 20;
     bad |= (key >= 0x7F800000u);
-    atomicAdd(&scnt[cp * 2048 + b], 1u);
-    atomicAdd(&ssum[cp * 2048 + b], fx_sq(key));
+    h1_add<WS>(mc, mh, ml, key >> 20, key, true);
   });
   zc = warp_sum_u32(zc);
   bad = __reduce_or_sync(LG_FULL, bad);
   if ((threadIdx.x & 31) == 0) {
-    if (zc) atomicAdd(&scnt[cp * 2048], zc);
+    if (zc) atomicAdd(&mc[0], zc);
     if (bad) atomicOr(a.flag, 1u);
   }
   __syncthreads();
@@ -110,8 +130,11 @@ k_tk_pass1(const float* __restrict__ g, const float* __restrict__ e, TkArgs a) {
     const uint32_t c = scnt[b] + scnt[2048 + b];
     if (c) {
       atomicAdd(gc + b, c);
-      const unsigned long long s = ssum[b] + ssum[2048 + b];
-      if (s) atomicAdd(gs + b, s);
+      if (WS) {
+        const unsigned long long s2 = (((unsigned long long)shi[b] + shi[2048 + b]) << 16) +
+                                      (unsigned long long)slo[b] + slo[2048 + b];
+        if (s2) atomicAdd(gs + b, s2);
+      }
     }
   }
 }
@@ -210,6 +233,7 @@ k_tk_select1(TkArgs a, int nq) {
 // ---------------------------------------------------------------------------
 // P2: level-2 histograms of the boundary level-1 bins
 // ---------------------------------------------------------------------------
+template <bool WS>
 __global__ void __launch_bounds__(TK_THREADS)
 k_tk_pass2(const float* __restrict__ g, const float* __restrict__ e, TkArgs a, int nq) {
   __shared__ uint8_t tbl[2048];
@@ -231,7 +255,7 @@ k_tk_pass2(const float* __restrict__ g, const float* __restrict__ e, TkArgs a, i
     if (key == 0) { ++zc; return; }
     const int64_t idx = (int64_t)s * 1024 + ((key >> 10) & 1023u);
     atomicAdd(c2 + idx, 1u);
-    atomicAdd(s2 + idx, fx_sq(key));
+    if (WS) atomicAdd(s2 + idx, fx_sq(key));
   });
   zc = warp_sum_u32(zc);
   if ((threadIdx.x & 31) == 0 && zc) atomicAdd(c2 + (int64_t)tbl[0] * 1024, zc);
@@ -665,18 +689,21 @@ cudaError_t launch_topk_select(const float* g, const float* e, const TkArgs& a, 
                                int K, cudaStream_t st, int64_t* launches) {
   if (a.nC == 0 || a.nchunks == 0) return cudaSuccess;
   cudaError_t r = cudaMemsetAsync(a.cnt1, 0, sizeof(uint32_t) * 2048 * (size_t)a.nC, st);
-  if (r == cudaSuccess) r = cudaMemsetAsync(a.sum1, 0, sizeof(unsigned long long) * 2048 * (size_t)a.nC, st);
+  if (r == cudaSuccess && err) r = cudaMemsetAsync(a.sum1, 0, sizeof(unsigned long long) * 2048 * (size_t)a.nC, st);
   if (r != cudaSuccess) return r;
-  const size_t sm1 = 2 * 2048 * (4 + 8);
+  const bool ws = err != nullptr;  // the compress select needs no energy sums
+  const size_t sm1 = 2 * 2048 * (ws ? 12 : 4);
   static bool attr = false;
   if (!attr) {
-    r = cudaFuncSetAttribute(k_tk_pass1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
+    r = cudaFuncSetAttribute(k_tk_pass1<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * 2048 * 12));
     if (r != cudaSuccess) return r;
     attr = true;
   }
-  k_tk_pass1<<<a.nchunks, TK_THREADS, sm1, st>>>(g, e, a);
+  if (ws) k_tk_pass1<true><<<a.nchunks, TK_THREADS, sm1, st>>>(g, e, a);
+  else k_tk_pass1<false><<<a.nchunks, TK_THREADS, sm1, st>>>(g, e, a);
   k_tk_select1<<<a.nC, TK_THREADS, 0, st>>>(a, nq);
-  k_tk_pass2<<<a.nchunks, TK_THREADS, 0, st>>>(g, e, a, nq);
+  if (ws) k_tk_pass2<true><<<a.nchunks, TK_THREADS, 0, st>>>(g, e, a, nq);
+  else k_tk_pass2<false><<<a.nchunks, TK_THREADS, 0, st>>>(g, e, a, nq);
   k_tk_select2<<<a.nC, TK_THREADS, 0, st>>>(a, nq);
   k_tk_pass3<<<a.nchunks, TK_THREADS, 0, st>>>(g, e, a, nq);
   k_tk_select3<<<a.nC, TK_THREADS, 0, st>>>(a, nq, err, bits, K);
