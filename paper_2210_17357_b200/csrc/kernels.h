@@ -76,7 +76,9 @@ struct TkArgs {
   uint32_t* cnt1; unsigned long long* sum1; uint32_t* cnt2; unsigned long long* sum2; uint32_t* cnt3;
   int32_t* n1; int32_t* n2; int32_t* sl1; uint32_t* sl2;
   TQ* q; const int64_t* kq; uint2* ccnt; ulonglong2* coff; const TPlan* tplan; unsigned* flag;
+  uint32_t* ckeys; int32_t* ckn;  // per chunk: keys of its boundary level-1 bins (pass2 -> pass3), count
 };
+constexpr int TK_CKCAP = 2048;  // compacted boundary keys kept per 16384-element chunk
 cudaError_t launch_topk_select(const float* g, const float* e, const TkArgs& a, int nq, double* err, int64_t* bits,
                                int K, cudaStream_t st, int64_t* launches);
 cudaError_t launch_plan_topk_dev(const int32_t* choice, const int32_t* params, int K, const DevLayer* layers,

@@ -247,11 +247,18 @@ k_tk_pass2(const float* __restrict__ g, const float* __restrict__ e, TkArgs a, i
   __syncthreads();
   uint32_t* c2 = a.cnt2 + (int64_t)c * nq * 1024;
   unsigned long long* s2 = a.sum2 + (int64_t)c * nq * 1024;
+  __shared__ int s_kn;
+  if (threadIdx.x == 0) s_kn = 0;
+  __syncthreads();
+  uint32_t* ck = a.ckeys + (int64_t)blockIdx.x * TK_CKCAP;
   uint32_t zc = 0;
   for_chunk(g, e, ly, ch, [&](int64_t, float x) {
     const uint32_t key = tkey(x);
     const uint32_t s = tbl[key >> 20];
     if (s == 0xFF) return;
+    // keep the key for pass 3 (order-free counting): no re-read of the chunk there
+    const int pos = atomicAdd(&s_kn, 1);
+    if (pos < TK_CKCAP) ck[pos] = key;
     if (key == 0) { ++zc; return; }
     const int64_t idx = (int64_t)s * 1024 + ((key >> 10) & 1023u);
     atomicAdd(c2 + idx, 1u);
@@ -259,6 +266,8 @@ k_tk_pass2(const float* __restrict__ g, const float* __restrict__ e, TkArgs a, i
   });
   zc = warp_sum_u32(zc);
   if ((threadIdx.x & 31) == 0 && zc) atomicAdd(c2 + (int64_t)tbl[0] * 1024, zc);
+  __syncthreads();
+  if (threadIdx.x == 0) a.ckn[blockIdx.x] = s_kn;  // > TK_CKCAP: pass 3 rescans the chunk
 }
 
 // scan a 1024-bin count histogram from the top with one warp: returns the bin holding
@@ -380,8 +389,7 @@ k_tk_pass3(const float* __restrict__ g, const float* __restrict__ e, TkArgs a, i
   __syncthreads();
   uint32_t* c3 = a.cnt3 + (int64_t)c * nq * 1024;
   uint32_t zc = 0;
-  for_chunk(g, e, ly, ch, [&](int64_t, float x) {
-    const uint32_t key = tkey(x);
+  auto count = [&](uint32_t key) {
     if (tbl[key >> 20] == 0xFF) return;
     const uint32_t p = key >> 10;
     int lo = 0, hi = n2 - 1;
@@ -392,7 +400,14 @@ k_tk_pass3(const float* __restrict__ g, const float* __restrict__ e, TkArgs a, i
     if (pre[lo] != p) return;
     if (key == 0) { ++zc; return; }
     atomicAdd(c3 + (int64_t)lo * 1024 + (key & 1023u), 1u);
-  });
+  };
+  const int kn = a.ckn[blockIdx.x];
+  if (kn <= TK_CKCAP) {  // the chunk's boundary keys, compacted by pass 2
+    const uint32_t* ck = a.ckeys + (int64_t)blockIdx.x * TK_CKCAP;
+    for (int i = threadIdx.x; i < kn; i += TK_THREADS) count(ck[i]);
+  } else {
+    for_chunk(g, e, ly, ch, [&](int64_t, float x) { count(tkey(x)); });
+  }
   zc = warp_sum_u32(zc);
   if ((threadIdx.x & 31) == 0 && zc && n2 > 0 && pre[0] == 0) atomicAdd(c3, zc);
 }
