@@ -186,6 +186,8 @@ int lgreco_ctx_create(lgreco_ctx** out, const lgreco_layer* layers, int32_t L, c
   // fine grain keeps every warp busy to the end (a quad is ~1/14 of a warp's share)
   std::vector<lg::QInfo> qchunks;
   std::vector<int32_t> lqc0(L + 1, 0);
+  std::vector<lg::QSeg> qsegs;
+  std::vector<int32_t> lqs0(L + 1, 0);
   if (c->B == 128) {
     for (int l = 0; l < L; ++l) {
       lqc0[l] = (int32_t)qchunks.size();
@@ -196,6 +198,14 @@ int lgreco_ctx_create(lgreco_ctx** out, const lgreco_layer* layers, int32_t L, c
                                     (int32_t)std::min<int64_t>(512, layers[l].numel - 128 * j)});
     }
     lqc0[L] = (int32_t)qchunks.size();
+    for (int l = 0; l < L; ++l) {
+      lqs0[l] = (int32_t)qsegs.size();
+      const int r0 = lqc0[l], r1 = lqc0[l + 1];
+      if (r1 == r0) qsegs.push_back(lg::QSeg{l, r0, 0, 0});
+      for (int r = r0; r < r1; r += 256) qsegs.push_back(lg::QSeg{l, r, std::min(256, r1 - r), 0});
+    }
+    lqs0[L] = (int32_t)qsegs.size();
+    c->nqseg = (int)qsegs.size();
     int nsm = 148, dev = 0;
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     c->nqwarps = nsm * 4 * 8;  // upper bound; the launcher sizes the grid by the kernel's occupancy
@@ -226,7 +236,11 @@ int lgreco_ctx_create(lgreco_ctx** out, const lgreco_layer* layers, int32_t L, c
   LG_ALLOC(c->d_partial, sizeof(double) * (size_t)std::max(1, std::max(c->nchunks, c->nqchunks)) * c->K);
   LG_ALLOC(c->d_qinfo, sizeof(lg::QInfo) * std::max(1, c->nqchunks));
   LG_ALLOC(c->d_layer_qchunk0, sizeof(int32_t) * (L + 1));
-  LG_ALLOC(c->d_ticket, 17 * 64 * sizeof(unsigned));  // K1 part counters + done counter, 256 B apart
+  LG_ALLOC(c->d_ticket, 17 * 64 * sizeof(unsigned));
+  LG_ALLOC(c->d_qseg, sizeof(lg::QSeg) * std::max(1, c->nqseg));
+  LG_ALLOC(c->d_lqseg0, sizeof(int32_t) * (L + 1));
+  LG_ALLOC(c->d_segsum, sizeof(double) * std::max(1, c->nqseg) * c->K);
+  LG_ALLOC(c->d_ldone, sizeof(unsigned) * L);  // K1 part counters + done counter, 256 B apart
   LG_ALLOC(c->d_flag, sizeof(unsigned));
   LG_ALLOC(c->d_plan, sizeof(lg::DevPlan) * L);
   if (world > 1 && c->family == LGRECO_QSGD) {
@@ -253,6 +267,10 @@ int lgreco_ctx_create(lgreco_ctx** out, const lgreco_layer* layers, int32_t L, c
     e = cudaMemcpyAsync(c->d_qinfo, qchunks.data(), sizeof(lg::QInfo) * c->nqchunks, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = cudaMemcpyAsync(c->d_layer_qchunk0, lqc0.data(), sizeof(int32_t) * (L + 1), cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(c->d_ticket, 0, 17 * 64 * sizeof(unsigned), st);
+  if (e == cudaSuccess && c->nqseg)
+    e = cudaMemcpyAsync(c->d_qseg, qsegs.data(), sizeof(lg::QSeg) * c->nqseg, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(c->d_lqseg0, lqs0.data(), sizeof(int32_t) * (L + 1), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(c->d_ldone, 0, sizeof(unsigned) * L, st);
   if (e == cudaSuccess) e = cudaMemsetAsync(c->d_flag, 0, sizeof(unsigned), st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) {
@@ -290,7 +308,8 @@ void lgreco_ctx_destroy(lgreco_ctx* c) {
   if (c->comm) ncclCommDestroy(c->comm);
   cudaFree(c->d_layers); cudaFree(c->d_bucket0); cudaFree(c->d_cand_s); cudaFree(c->d_params);
   cudaFree(c->d_chunks); cudaFree(c->d_chunks_all); cudaFree(c->d_layer_chunk0); cudaFree(c->d_partial);
-  cudaFree(c->d_qinfo); cudaFree(c->d_layer_qchunk0); cudaFree(c->d_ticket); cudaFree(c->d_flag);
+  cudaFree(c->d_qinfo); cudaFree(c->d_layer_qchunk0); cudaFree(c->d_ticket);
+  cudaFree(c->d_qseg); cudaFree(c->d_lqseg0); cudaFree(c->d_segsum); cudaFree(c->d_ldone); cudaFree(c->d_flag);
   cudaFree(c->d_plan); cudaFree(c->d_pay1); cudaFree(c->d_recv); cudaFree(c->d_pay2);
   if (c->h_plan_pinned) cudaFreeHost(c->h_plan_pinned);
   if (c->h_choice_pinned) cudaFreeHost(c->h_choice_pinned);
@@ -351,6 +370,7 @@ int lgreco_profile(lgreco_ctx* c, const float* d_g, const float* d_ef, uint64_t 
                        c->d_partial, d_err, d_bits};
     a.qinfo = c->d_qinfo; a.nqchunks = c->nqchunks; a.layer_qchunk0 = c->d_layer_qchunk0;
     a.nqwarps = c->nqwarps; a.ticket = c->d_ticket;
+    a.segs = c->d_qseg; a.nseg = c->nqseg; a.lseg0 = c->d_lqseg0; a.segsum = c->d_segsum; a.ldone = c->d_ldone;
     a.ptr_aligned = ((reinterpret_cast<uintptr_t>(d_g) | reinterpret_cast<uintptr_t>(d_ef)) & 15) == 0;
     if (c->timing && c->nchunks > 0) {
       cudaEvent_t e0, e1;

@@ -62,6 +62,11 @@ struct lgreco_ctx {
   int32_t* d_layer_qchunk0 = nullptr;
   int nqwarps = 0;
   unsigned* d_ticket = nullptr;
+  lg::QSeg* d_qseg = nullptr;    // K1b segments (<= 256 quad rows of one layer)
+  int nqseg = 0;
+  int32_t* d_lqseg0 = nullptr;   // per-layer first segment [L+1]
+  double* d_segsum = nullptr;    // [nqseg][K]
+  unsigned* d_ldone = nullptr;   // per-layer finished-segment counters [L]
   unsigned* d_flag = nullptr;
   // plan
   std::vector<int32_t> plan_choice;

@@ -1464,8 +1464,20 @@ static cudaError_t launch_solve_cluster(const SolveArgs& a, uint8_t* pd, int32_t
 #undef LG_CL_K
 #undef LG_CL
   if (!fn) return cudaErrorNotSupported;
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) { cudaGetLastError(); return cudaErrorNotSupported; }
+  // attribute + cluster-occupancy checks are host-side driver calls (tens of us): done
+  // once per (kernel, shared memory, block) configuration and cached
+  struct CfgKey { const void* fn; size_t smem; int nt, nc; int ok; };
+  static CfgKey cache[16];
+  static int ncache = 0;
+  int cached = -1;
+  for (int i = 0; i < ncache; ++i)
+    if (cache[i].fn == (const void*)fn && cache[i].smem == smem && cache[i].nt == nt && cache[i].nc == NC) cached = i;
+  if (cached >= 0 && !cache[cached].ok) return cudaErrorNotSupported;
+  cudaError_t e = cudaSuccess;
+  if (cached < 0) {  // the attribute is the kernel's maximum: set to the largest size this path uses
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    if (e != cudaSuccess) { cudaGetLastError(); return cudaErrorNotSupported; }
+  }
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1478,12 +1490,16 @@ static cudaError_t launch_solve_cluster(const SolveArgs& a, uint8_t* pd, int32_t
   cfg.stream = st;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  int nclusters = 0;
-  e = cudaOccupancyMaxActiveClusters(&nclusters, (const void*)fn, &cfg);
-  if (e != cudaSuccess || nclusters < 1) {
-    if (getenv("LGRECO_DEBUG")) fprintf(stderr, "lgreco: cluster occupancy %d (%s)\n", nclusters, cudaGetErrorString(e));
-    cudaGetLastError();
-    return cudaErrorNotSupported;
+  if (cached < 0) {
+    int nclusters = 0;
+    e = cudaOccupancyMaxActiveClusters(&nclusters, (const void*)fn, &cfg);
+    const int ok = (e == cudaSuccess && nclusters >= 1) ? 1 : 0;
+    if (ncache < 16) cache[ncache++] = CfgKey{(const void*)fn, smem, nt, NC, ok};
+    if (!ok) {
+      if (getenv("LGRECO_DEBUG")) fprintf(stderr, "lgreco: cluster occupancy %d (%s)\n", nclusters, cudaGetErrorString(e));
+      cudaGetLastError();
+      return cudaErrorNotSupported;
+    }
   }
   return cudaLaunchKernelEx(&cfg, fn, a.err, a.bits, a.L, a.K, a.default_idx, a.compress, a.D, a.flags, a.choice,
                             a.info, pd, act, wdisc, wadd, wmaxd);

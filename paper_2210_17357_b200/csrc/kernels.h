@@ -19,6 +19,8 @@ struct CandS { float s[16]; };
 // first element, global index of its first bucket (Philox counter base, mod 2^32),
 // number of valid elements (512 unless the layer ends inside the quad).
 struct QInfo { int64_t elem0; uint32_t gb0; int32_t nvalid; };
+// K1b segment: <= 256 consecutive quad rows of one layer
+struct QSeg { int32_t layer, row0, nrows, pad; };
   // s_j = 2^{b_j} - 1, passed by value (constant bank)
 
 struct QProfileArgs {
@@ -33,6 +35,8 @@ struct QProfileArgs {
   // layer_qchunk0[L+1]), nqwarps resident warps, ticket[2] zeroed counters
   const QInfo* qinfo = nullptr; int nqchunks = 0; const int32_t* layer_qchunk0 = nullptr;
   int nqwarps = 0; unsigned* ticket = nullptr; int ptr_aligned = 0;
+  const QSeg* segs = nullptr; int nseg = 0; const int32_t* lseg0 = nullptr; double* segsum = nullptr;
+  unsigned* ldone = nullptr;
 };
 
 struct QPackArgs {

@@ -598,53 +598,90 @@ k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const QIn
   finish();
 }
 
-// K1b: per layer, fixed-order sum of its chunks' partials, sqrt.  The layer's rows
-// [c0, c1) x K are one contiguous run of doubles; thread t < T = K floor(1024/K) sums
-// the elements t, t + T, ... (all of candidate t mod K; coalesced, 4 loads in flight),
-// then thread j < K adds the T/K thread sums of candidate j in thread order.
-constexpr int QR_THREADS = 1024;
-__global__ void __launch_bounds__(QR_THREADS)
-k_qprofile_reduce(const DevLayer* __restrict__ layers, const int32_t* __restrict__ layer_chunk0,
-                  const double* __restrict__ partial, const int32_t* __restrict__ params, int K, int B,
-                  double* __restrict__ err, int64_t* __restrict__ bits) {
-  __shared__ double sm[QR_THREADS];
+// K1b: per layer, fixed-order sum of its quads' partial rows, sqrt.  One CTA per segment
+// of <= QR_ROWS rows of one layer (layers without rows get one empty segment): thread t
+// loads row seg0 + t (K contiguous doubles), a fixed shared-memory tree per candidate
+// gives the segment sum; the layer's last segment to finish (counter per layer, reset
+// by that CTA) adds the segment sums in segment order and writes err/bits.
+constexpr int QR_ROWS = 256;
+__global__ void __launch_bounds__(QR_ROWS)
+k_qprofile_reduce(const DevLayer* __restrict__ layers, const QSeg* __restrict__ segs, const int32_t* __restrict__ lseg0,
+                  const double* __restrict__ partial, double* __restrict__ segsum, unsigned* __restrict__ ldone,
+                  const int32_t* __restrict__ params, int K, int B, double* __restrict__ err, int64_t* __restrict__ bits) {
+  __shared__ double sm[16][QR_ROWS];
+  __shared__ bool s_last;
+  const QSeg sg = segs[blockIdx.x];
+  const int l = sg.layer, t = threadIdx.x;
+  const DevLayer ly = layers[l];
+  const double* row = partial + (int64_t)(sg.row0 + t) * K;
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    if (j < K) sm[j][t] = (t < sg.nrows) ? __ldg(row + j) : 0.0;
+  __syncthreads();
+#pragma unroll
+  for (int o = QR_ROWS / 2; o; o >>= 1) {
+    if (t < o) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (j < K) sm[j][t] += sm[j][t + o];
+    }
+    __syncthreads();
+  }
+  if (t < K) segsum[(int64_t)blockIdx.x * K + t] = sm[t][0];
+  __syncthreads();
+  if (t == 0) {
+    __threadfence();
+    const int s0 = lseg0[l], s1 = lseg0[l + 1];
+    s_last = atomicAdd(&ldone[l], 1u) == (unsigned)(s1 - s0 - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const int s0 = lseg0[l], s1 = lseg0[l + 1];
+  const int64_t nb = (ly.numel + B - 1) / B;
+  if (t < K) {
+    double s = 0.0;
+    for (int q = s0; q < s1; ++q) s += __ldcg(segsum + (int64_t)q * K + t);
+    if (ly.compress) {
+      err[(int64_t)l * K + t] = sqrt(s);
+      bits[(int64_t)l * K + t] = nb * ((int64_t)B * params[t] + 64);
+    } else {
+      err[(int64_t)l * K + t] = 0.0;
+      bits[(int64_t)l * K + t] = 32 * ly.numel;
+    }
+  }
+  if (t == 0) ldone[l] = 0u;  // stream-ordered reuse by the next launch
+}
+
+// Per-layer reduction of the B > 128 kernel's chunk partials (k_qprofile).
+__global__ void __launch_bounds__(256)
+k_qprofile_reduce_chunks(const DevLayer* __restrict__ layers, const int32_t* __restrict__ layer_chunk0,
+                         const double* __restrict__ partial, const int32_t* __restrict__ params, int K, int B,
+                         double* __restrict__ err, int64_t* __restrict__ bits) {
+  __shared__ double sm[256];
   const int l = blockIdx.x;
   const DevLayer ly = layers[l];
   const int c0 = layer_chunk0[l], c1 = layer_chunk0[l + 1];
   const int64_t nb = (ly.numel + B - 1) / B;
-  const int T = K * (QR_THREADS / K);
-  const int t = threadIdx.x;
-  const double* base = partial + (int64_t)c0 * K;
-  const int64_t n = (int64_t)(c1 - c0) * K;
-  double acc = 0.0;
-  if (t < T) {
-    int64_t i = t;
-    for (; i + 7 * (int64_t)T < n; i += 8 * (int64_t)T) {
-      double v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = __ldg(base + i + u * (int64_t)T);
-#pragma unroll
-      for (int u = 0; u < 8; ++u) acc += v[u];
-    }
-    for (; i < n; i += T) acc += __ldg(base + i);
-  }
-  sm[t] = acc;
-  __syncthreads();
-  // warp w sums candidate j = w, w + 32, ...: lanes take the T/K thread sums in a fixed
-  // strided order, then a fixed xor tree
-  const int lane = t & 31, w = t >> 5;
-  for (int j = w; j < K; j += QR_THREADS / 32) {
+  for (int j = 0; j < K; ++j) {
     double s = 0.0;
-    for (int u = lane; u < T / K; u += 32) s += sm[j + K * u];
-    s = warp_sum_d(s);
-    if (lane != 0) continue;
-    if (ly.compress) {
-      err[(int64_t)l * K + j] = sqrt(s);
-      bits[(int64_t)l * K + j] = nb * ((int64_t)B * params[j] + 64);
-    } else {
-      err[(int64_t)l * K + j] = 0.0;
-      bits[(int64_t)l * K + j] = 32 * ly.numel;
+    for (int c = c0 + threadIdx.x; c < c1; c += blockDim.x) s += partial[(int64_t)c * K + j];
+    sm[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = 128; o; o >>= 1) {
+      if (threadIdx.x < o) sm[threadIdx.x] += sm[threadIdx.x + o];
+      __syncthreads();
     }
+    if (threadIdx.x == 0) {
+      if (ly.compress) {
+        err[(int64_t)l * K + j] = sqrt(sm[0]);
+        bits[(int64_t)l * K + j] = nb * ((int64_t)B * params[j] + 64);
+      } else {
+        err[(int64_t)l * K + j] = 0.0;
+        bits[(int64_t)l * K + j] = 32 * ly.numel;
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -989,9 +1026,11 @@ cudaError_t launch_qprofile(const QProfileArgs& a, cudaStream_t st) {
       const int nsm = a.nqwarps / (QP_WARPS * 4);  // nqwarps = SMs x 4 CTAs x 8 warps (an upper bound)
 #define LG_QQ(KT)                                                                                              \
   {                                                                                                            \
-    cudaError_t e = cudaFuncSetAttribute(k_qprofile_q<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
-    if (e != cudaSuccess) return e;                                                                            \
     static int occ = 0;                                                                                        \
+    if (occ == 0) {                                                                                            \
+      cudaError_t e = cudaFuncSetAttribute(k_qprofile_q<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+      if (e != cudaSuccess) return e;                                                                          \
+    }                                                                                                          \
     if (occ == 0 && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_qprofile_q<KT>, QP_THREADS, smem) != \
                      cudaSuccess || occ < 1)) occ = 1;                                                          \
     const int grid = std::max(1, std::min(a.nqwarps / QP_WARPS, nsm * occ));                                    \
@@ -1026,8 +1065,12 @@ cudaError_t launch_qprofile(const QProfileArgs& a, cudaStream_t st) {
     }
     if (a.ev1) cudaEventRecord(a.ev1, st);
   }
-  k_qprofile_reduce<<<a.L, QR_THREADS, 0, st>>>(a.layers, quads ? a.layer_qchunk0 : a.layer_chunk0, a.partial, a.params, a.K,
-                                         a.B, a.err, a.bits);
+  if (quads)
+    k_qprofile_reduce<<<a.nseg, QR_ROWS, 0, st>>>(a.layers, a.segs, a.lseg0, a.partial, a.segsum, a.ldone, a.params,
+                                                  a.K, a.B, a.err, a.bits);
+  else
+    k_qprofile_reduce_chunks<<<a.L, 256, 0, st>>>(a.layers, a.layer_chunk0, a.partial, a.params, a.K, a.B, a.err,
+                                                  a.bits);
   return cudaGetLastError();
 }
 
