@@ -125,7 +125,8 @@ int lgreco_ctx_kernel_ms(lgreco_ctx* ctx, double* total_ms, int64_t* count);
  * accumulated-gradient mode).  The EF buffer is read, never written.  `step`
  * selects the Philox counter (QSGD: the same uniforms the compress call of this
  * step draws, R6).  Lossless layers: err 0, bits 32*numel.
- * d_err: L*K doubles, d_bits: L*K int64, row-major by layer. */
+ * d_err: L*K doubles, d_bits: L*K int64, row-major by layer.  QSGD accepts any 4-byte
+ * aligned d_g / d_ef; TopK and PowerSGD need 16-byte aligned base pointers (EINVAL). */
 int lgreco_profile(lgreco_ctx* ctx, const float* d_g, const float* d_ef, uint64_t step,
                    double* d_err, int64_t* d_bits, void* stream);
 
@@ -156,7 +157,8 @@ int lgreco_plan_broadcast(lgreco_ctx* ctx, int32_t* d_choice, void* stream);
  * QSGD: pack -> all-to-all of byte-balanced bucket shards -> ordered dequantise-
  * sum-requantise on the owner -> all-gather -> decode (R13).  TopK: select ->
  * all-gather (idx,val) -> ordered sparse sum (R10).  PowerSGD: P=MQ, all-reduce,
- * orthogonalise, Q=M^T P, all-reduce, out = P Q^T (R12). */
+ * orthogonalise, Q=M^T P, all-reduce, out = P Q^T (R12).  d_g, d_ef and d_out must be
+ * 16-byte aligned (cudaMalloc / torch allocations are); LGRECO_EINVAL otherwise. */
 int lgreco_compress_allreduce(lgreco_ctx* ctx, const int32_t* h_choice, const float* d_g,
                               float* d_ef, float* d_out, uint64_t step, void* stream);
 

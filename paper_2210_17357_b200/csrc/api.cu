@@ -358,6 +358,18 @@ int lgreco_ctx_kernel_ms(lgreco_ctx* c, double* total_ms, int64_t* count) {
   return rc;
 }
 
+// Base pointers of the fp32 gradient-sized buffers must be 16-byte aligned for the
+// 128-bit (and bulk-copy) paths of every kernel except the QSGD profile (which falls
+// back to masked loads).  Argument error otherwise (include/lgreco.h).
+static int check_align16(const char* what, const void* a, const void* b = nullptr, const void* d = nullptr) {
+  const uintptr_t m = reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b) | reinterpret_cast<uintptr_t>(d);
+  if (m & 15) {
+    lg_set_error("%s: gradient / EF / output base pointers must be 16-byte aligned", what);
+    return LGRECO_EINVAL;
+  }
+  return LGRECO_OK;
+}
+
 int lgreco_profile(lgreco_ctx* c, const float* d_g, const float* d_ef, uint64_t step, double* d_err,
                    int64_t* d_bits, void* stream) {
   if (!c || !d_g || !d_err || !d_bits) { lg_set_error("null argument"); return LGRECO_EINVAL; }
@@ -384,6 +396,7 @@ int lgreco_profile(lgreco_ctx* c, const float* d_g, const float* d_ef, uint64_t 
     c->launches += (c->nchunks > 0) + 1;
     return LGRECO_OK;
   }
+  LG_TRY(check_align16("profile", d_g, d_ef));  // (QSGD above handles any 4-byte alignment)
   if (c->family == LGRECO_TOPK) return topk_profile(c, d_g, d_ef, d_err, d_bits, st);
   if (c->family == LGRECO_POWERSGD) return psgd_profile(c, d_g, d_ef, step, d_err, d_bits, st);
   lg_set_error("profile: family %d unsupported", c->family);
@@ -436,10 +449,12 @@ int lgreco_shard_bounds(lgreco_ctx* c, const int32_t* h_choice, int32_t W, int64
   return LGRECO_OK;
 }
 
+
 int lgreco_qsgd_pack(lgreco_ctx* c, const int32_t* h_choice, const float* d_g, float* d_ef, uint8_t* d_payload,
                      float* d_dec, uint32_t rank, uint64_t step, void* stream) {
   if (!c || !h_choice || !d_g) return LGRECO_EINVAL;
   if (c->family != LGRECO_QSGD) return LGRECO_EUNSUPPORTED;
+  LG_TRY(check_align16("qsgd_pack", d_g, d_ef, d_dec));
   cudaStream_t st = (cudaStream_t)stream;
   LG_TRY(set_plan(c, h_choice, st));
   uint32_t k0, k1;
@@ -468,6 +483,7 @@ int lgreco_qsgd_reduce(lgreco_ctx* c, const int32_t* h_choice, int32_t W, int64_
 
 int lgreco_qsgd_unpack(lgreco_ctx* c, const int32_t* h_choice, const uint8_t* d_payload, float* d_out, void* stream) {
   if (!c || !h_choice || !d_payload || !d_out) return LGRECO_EINVAL;
+  LG_TRY(check_align16("qsgd_unpack", d_out));
   cudaStream_t st = (cudaStream_t)stream;
   LG_TRY(set_plan(c, h_choice, st));
   lg::QUnpackArgs a{d_payload, d_out, c->d_layers, c->d_plan, c->d_chunks_all, c->nchunks_all, c->B};
@@ -479,6 +495,7 @@ int lgreco_qsgd_unpack(lgreco_ctx* c, const int32_t* h_choice, const uint8_t* d_
 int lgreco_compress_allreduce(lgreco_ctx* c, const int32_t* h_choice, const float* d_g, float* d_ef, float* d_out,
                               uint64_t step, void* stream) {
   if (!c || !h_choice || !d_g || !d_out) { lg_set_error("null argument"); return LGRECO_EINVAL; }
+  LG_TRY(check_align16("compress_allreduce", d_g, d_ef, d_out));
   cudaStream_t st = (cudaStream_t)stream;
   if (c->family == LGRECO_TOPK) return topk_compress_allreduce(c, h_choice, d_g, d_ef, d_out, st);
   if (c->family == LGRECO_POWERSGD) return psgd_compress_allreduce(c, h_choice, d_g, d_ef, d_out, step, st);
@@ -512,6 +529,7 @@ int lgreco_compress_allreduce(lgreco_ctx* c, const int32_t* h_choice, const floa
 int lgreco_compress_allreduce_dev(lgreco_ctx* c, const int32_t* d_choice, const float* d_g, float* d_ef,
                                   float* d_out, uint64_t step, void* stream) {
   if (!c || !d_choice || !d_g || !d_out) { lg_set_error("null argument"); return LGRECO_EINVAL; }
+  LG_TRY(check_align16("compress_allreduce_dev", d_g, d_ef, d_out));
   cudaStream_t st = (cudaStream_t)stream;
   if (c->world == 1 && c->family == LGRECO_QSGD) {
     // W = 1: nothing leaves the GPU, the fused pass needs only the bits per layer

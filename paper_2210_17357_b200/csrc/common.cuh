@@ -85,6 +85,28 @@ __device__ __forceinline__ int find_layer(const int64_t* b0, int L, int64_t gb) 
   return lo;
 }
 
+// Programmatic dependent launch (PDL): a kernel launched with launch_pdl may be
+// scheduled while its predecessor in the stream drains; it must call pdl_wait() before
+// touching anything the predecessor writes (griddepcontrol.wait returns once the
+// predecessor grid has completed and its memory is visible).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 }  // namespace lg
 
 // host-side error helpers ------------------------------------------------------

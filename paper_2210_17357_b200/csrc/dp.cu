@@ -792,6 +792,7 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
   long long t_push = 0, t_c = 0, t_p = 0, t_s = 0, t_cl = 0;
 #endif
   LG_T(0);
+  pdl_wait();  // the error / size tables of the profile
 
   // ---- prelude (every CTA, identical): flags/defaults, active list, Emax (layer order)
   int32_t* sm_flag = reinterpret_cast<int32_t*>(smem_raw);
@@ -1479,17 +1480,19 @@ static cudaError_t launch_solve_cluster(const SolveArgs& a, uint8_t* pd, int32_t
     if (e != cudaSuccess) { cudaGetLastError(); return cudaErrorNotSupported; }
   }
   cudaLaunchConfig_t cfg = {};
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = NC;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL: k_solve_cl waits in-kernel
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.gridDim = dim3(NC, 1, 1);
   cfg.blockDim = dim3(nt, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 1;  // (occupancy query without PDL)
   if (cached < 0) {
     int nclusters = 0;
     e = cudaOccupancyMaxActiveClusters(&nclusters, (const void*)fn, &cfg);
@@ -1501,6 +1504,7 @@ static cudaError_t launch_solve_cluster(const SolveArgs& a, uint8_t* pd, int32_t
       return cudaErrorNotSupported;
     }
   }
+  cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, fn, a.err, a.bits, a.L, a.K, a.default_idx, a.compress, a.D, a.flags, a.choice,
                             a.info, pd, act, wdisc, wadd, wmaxd);
 }

@@ -610,6 +610,7 @@ k_qprofile_reduce(const DevLayer* __restrict__ layers, const QSeg* __restrict__ 
                   const int32_t* __restrict__ params, int K, int B, double* __restrict__ err, int64_t* __restrict__ bits) {
   __shared__ double sm[16][QR_ROWS];
   __shared__ bool s_last;
+  pdl_wait();  // K1's partial rows
   const QSeg sg = segs[blockIdx.x];
   const int l = sg.layer, t = threadIdx.x;
   const DevLayer ly = layers[l];
@@ -763,6 +764,7 @@ k_qpack(const float* __restrict__ g, float* __restrict__ ef, uint8_t* __restrict
         float* __restrict__ dec_out, const DevLayer* __restrict__ layers, const DevPlan* __restrict__ plan,
         const ProfChunk* __restrict__ chunks, int B, uint32_t k0, uint32_t k1, uint32_t rankfield,
         uint32_t step, unsigned* __restrict__ flag) {
+  pdl_wait();  // the plan (k_plan_qsgd_dev) and the EF of the previous step
   const ProfChunk ch = chunks[blockIdx.x];
   const DevLayer ly = layers[ch.layer];
   const DevPlan pl = plan[ch.layer];
@@ -989,6 +991,7 @@ k_qreduce(const uint8_t* __restrict__ recv, int64_t shard_bytes, int64_t byte0, 
 __global__ void k_plan_qsgd_dev(const int32_t* __restrict__ choice, const int32_t* __restrict__ params, int K,
                                 const DevLayer* __restrict__ layers, int L, DevPlan* __restrict__ plan,
                                 unsigned* __restrict__ flag) {
+  pdl_wait();  // the solve's choice
   for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < L; l += gridDim.x * blockDim.x) {
     int bits = 0;
     if (layers[l].compress) {
@@ -1002,7 +1005,9 @@ __global__ void k_plan_qsgd_dev(const int32_t* __restrict__ choice, const int32_
 
 cudaError_t launch_plan_qsgd_dev(const int32_t* choice, const int32_t* params, int K, const DevLayer* layers, int L,
                                  DevPlan* plan, unsigned* flag, cudaStream_t st) {
-  k_plan_qsgd_dev<<<(L + 255) / 256, 256, 0, st>>>(choice, params, K, layers, L, plan, flag);
+  const cudaError_t e = launch_pdl(k_plan_qsgd_dev, dim3((L + 255) / 256), dim3(256), 0, st, choice, params, K, layers,
+                                   L, plan, flag);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
@@ -1065,9 +1070,11 @@ cudaError_t launch_qprofile(const QProfileArgs& a, cudaStream_t st) {
     }
     if (a.ev1) cudaEventRecord(a.ev1, st);
   }
-  if (quads)
-    k_qprofile_reduce<<<a.nseg, QR_ROWS, 0, st>>>(a.layers, a.segs, a.lseg0, a.partial, a.segsum, a.ldone, a.params,
-                                                  a.K, a.B, a.err, a.bits);
+  if (quads) {
+    const cudaError_t e = launch_pdl(k_qprofile_reduce, dim3(a.nseg), dim3(QR_ROWS), 0, st, a.layers, a.segs, a.lseg0,
+                                     a.partial, a.segsum, a.ldone, a.params, a.K, a.B, a.err, a.bits);
+    if (e != cudaSuccess) return e;
+  }
   else
     k_qprofile_reduce_chunks<<<a.L, 256, 0, st>>>(a.layers, a.layer_chunk0, a.partial, a.params, a.K, a.B, a.err,
                                                   a.bits);
@@ -1076,8 +1083,9 @@ cudaError_t launch_qprofile(const QProfileArgs& a, cudaStream_t st) {
 
 cudaError_t launch_qpack(const QPackArgs& a, cudaStream_t st) {
   if (a.nchunks == 0) return cudaSuccess;
-  k_qpack<<<a.nchunks, QP_THREADS, 0, st>>>(a.g, a.ef, a.payload, a.dec, a.layers, a.plan, a.chunks, a.B, a.k0,
-                                            a.k1, a.rankfield, a.step, a.flag);
+  const cudaError_t e = launch_pdl(k_qpack, dim3(a.nchunks), dim3(QP_THREADS), 0, st, a.g, a.ef, a.payload, a.dec,
+                                   a.layers, a.plan, a.chunks, a.B, a.k0, a.k1, a.rankfield, a.step, a.flag);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

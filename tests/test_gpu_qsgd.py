@@ -292,3 +292,19 @@ def test_profile_parity_adversarial_buckets(lg, ref, with_ef, shifted):
     assert np.all((ref_err == 0) == (ge == 0))
     rel = np.abs(ge - ref_err) / np.maximum(ref_err, 1e-300)
     assert rel.max() <= 1e-5, (rel.max(), np.unravel_index(rel.argmax(), rel.shape))
+
+
+def test_misaligned_buffers_rejected(lg):
+    """Compress entry points need 16-byte aligned g / e / out (EINVAL, no launch); the
+    QSGD profile accepts them (masked loads, covered by the adversarial test)."""
+    layers = W.config_layers("C1")[:3]
+    N = W.total_numel(layers)
+    g, e = W.gaussian_outliers(layers, seed=2)
+    ctx = lg.Context(layers, lg.QSGD, BITS, seed=1)
+    gs, es = _dev_shifted(g), _dev_shifted(e)
+    out = torch.empty(N, dtype=torch.float32, device="cuda")
+    with pytest.raises(lg.LGrecoError) as ex:
+        ctx.compress_allreduce([2] * len(layers), gs, es, out, 0)
+    assert ex.value.status == lg.EINVAL
+    ctx.check()
+    ctx.close()
