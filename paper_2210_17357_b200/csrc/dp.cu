@@ -1451,11 +1451,16 @@ static cudaError_t launch_solve_cluster(const SolveArgs& a, uint8_t* pd, int32_t
   const int S = nt * cpt;
   // two 64-bit rows, then the per-layer tables: costs (8 B), disc (4 B), max disc (4 B),
   // candidate pairs (8 B x KP2), 64-bit keys (8 B x KT), band (8 B)
-  const int kt0 = a.K <= 4 ? 4 : a.K == 5 ? 5 : a.K <= 7 ? 7 : a.K <= 8 ? 8 : a.K <= 16 ? 16 : 0;
+  int kt0 = a.K <= 4 ? 4 : a.K == 5 ? 5 : a.K <= 7 ? 7 : a.K <= 8 ? 8 : a.K <= 16 ? 16 : 0;
+  const size_t rows_b = (size_t)16 * (32 * cpt + (size_t)NC * S);
   // KT == 0: only the max-disc and band tables live in shared memory
-  const size_t smem = (size_t)16 * (32 * cpt + (size_t)NC * S) + (size_t)4 * (a.L + 4) + 16 + (size_t)8 * a.L +
-                      (kt0 > 0 ? (size_t)12 * a.L * a.K + (size_t)a.L * (8 * ((kt0 + 2) & ~1) + 8 * kt0) : 0);
-  if (smem > 220 * 1024 || (size_t)24 * a.L + 64 > (size_t)16 * (32 * cpt + (size_t)NC * S)) return cudaErrorNotSupported;
+  auto smem_of = [&](int k) {
+    return rows_b + (size_t)4 * (a.L + 4) + 16 + (size_t)8 * a.L +
+           (k > 0 ? (size_t)12 * a.L * a.K + (size_t)a.L * (8 * ((k + 2) & ~1) + 8 * k) : 0);
+  };
+  if (kt0 > 0 && smem_of(kt0) > 220 * 1024) kt0 = 0;  // many layers: per-row staged tables (grouped keys)
+  const size_t smem = smem_of(kt0);
+  if (smem > 220 * 1024 || (size_t)24 * a.L + 64 > rows_b) return cudaErrorNotSupported;
   const int kt = kt0;
   void (*fn)(const double*, const int64_t*, int, int, const int32_t*, const int32_t*, int, uint32_t, int32_t*,
              lgreco_solve_info*, uint8_t*, int32_t*, int32_t*, uint64_t*, int32_t*) = nullptr;
@@ -1475,9 +1480,20 @@ static cudaError_t launch_solve_cluster(const SolveArgs& a, uint8_t* pd, int32_t
     if (cache[i].fn == (const void*)fn && cache[i].smem == smem && cache[i].nt == nt && cache[i].nc == NC) cached = i;
   if (cached >= 0 && !cache[cached].ok) return cudaErrorNotSupported;
   cudaError_t e = cudaSuccess;
-  if (cached < 0) {  // the attribute is the kernel's maximum: set to the largest size this path uses
-    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    if (e != cudaSuccess) { cudaGetLastError(); return cudaErrorNotSupported; }
+  if (cached < 0) {
+    // the attribute is the kernel's maximum dynamic size: only ever raised (a launch of a
+    // smaller configuration must not lower it under a cached larger one)
+    struct FnMax { const void* fn; size_t smem; };
+    static FnMax fmax[32];
+    static int nfmax = 0;
+    int fi = -1;
+    for (int i = 0; i < nfmax; ++i) if (fmax[i].fn == (const void*)fn) fi = i;
+    if (fi < 0 || fmax[fi].smem < smem) {
+      e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) { cudaGetLastError(); return cudaErrorNotSupported; }
+      if (fi < 0 && nfmax < 32) fmax[nfmax++] = FnMax{(const void*)fn, smem};
+      else if (fi >= 0) fmax[fi].smem = smem;
+    }
   }
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[2];
