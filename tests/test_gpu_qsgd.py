@@ -308,3 +308,36 @@ def test_misaligned_buffers_rejected(lg):
     assert ex.value.status == lg.EINVAL
     ctx.check()
     ctx.close()
+
+
+def test_c5_sampled_full_size(lg, ref):
+    """C5 (GPT-2-medium-like, 354.8M fp32, 292 tensors) at full size in the bench launch
+    configuration (every >= 2-D tensor compressed): the profile rows of sampled layers
+    -- the 50257x1024 token embedding, first / middle / last blocks and a ragged-size
+    vector -- against the oracle, which recomputes only those layers (the others are
+    marked lossless on its side; global bucket numbering is unchanged, R3)."""
+    layers = W.config_layers("C5")
+    N = W.total_numel(layers)
+    comp_idx = [i for i, l in enumerate(layers) if l.compress]
+    big = max(comp_idx, key=lambda i: layers[i].numel)
+    sample = sorted({big, comp_idx[1], comp_idx[len(comp_idx) // 2], comp_idx[-1]})
+    rng = np.random.default_rng(55)
+    g = np.zeros(N, np.float32)
+    e = np.zeros(N, np.float32)
+    for i in sample:
+        l = layers[i]
+        s = 10.0 ** rng.uniform(-4, -1)
+        g[l.offset:l.offset + l.numel] = (rng.standard_normal(l.numel) * s).astype(np.float32)
+        e[l.offset:l.offset + l.numel] = (rng.standard_normal(l.numel) * 0.1 * s).astype(np.float32)
+    ctx = lg.Context(layers, lg.QSGD, BITS, seed=0x5EED)
+    L, K = len(layers), len(BITS)
+    err = torch.empty(L, K, dtype=torch.float64, device="cuda")
+    bits = torch.empty(L, K, dtype=torch.int64, device="cuda")
+    ctx.profile(_dev(g), _dev(e), 3, err, bits)
+    sub = [W.Layer(l.offset, l.numel, l.rows, l.cols, 1 if i in sample else 0) for i, l in enumerate(layers)]
+    ref_err, ref_bits = ref.qsgd_profile(sub, g, e, BITS, seed=0x5EED, step=3)
+    ge, gb = err.cpu().numpy(), bits.cpu().numpy()
+    for i in sample:
+        assert np.array_equal(gb[i], ref_bits[i])
+        assert (np.abs(ge[i] - ref_err[i]) / np.maximum(ref_err[i], 1e-300)).max() <= 1e-5, i
+    ctx.close()
