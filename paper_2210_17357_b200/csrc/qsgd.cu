@@ -608,27 +608,30 @@ __global__ void __launch_bounds__(QR_ROWS)
 k_qprofile_reduce(const DevLayer* __restrict__ layers, const QSeg* __restrict__ segs, const int32_t* __restrict__ lseg0,
                   const double* __restrict__ partial, double* __restrict__ segsum, unsigned* __restrict__ ldone,
                   const int32_t* __restrict__ params, int K, int B, double* __restrict__ err, int64_t* __restrict__ bits) {
-  __shared__ double sm[16][QR_ROWS];
+  __shared__ double sm[16][QR_ROWS / 32];
   __shared__ bool s_last;
   pdl_wait();  // K1's partial rows
   const QSeg sg = segs[blockIdx.x];
-  const int l = sg.layer, t = threadIdx.x;
+  const int l = sg.layer, t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const DevLayer ly = layers[l];
   const double* row = partial + (int64_t)(sg.row0 + t) * K;
+  double v[16];
 #pragma unroll
-  for (int j = 0; j < 16; ++j)
-    if (j < K) sm[j][t] = (t < sg.nrows) ? __ldg(row + j) : 0.0;
-  __syncthreads();
+  for (int j = 0; j < 16; ++j) v[j] = (j < K && t < sg.nrows) ? __ldg(row + j) : 0.0;
 #pragma unroll
-  for (int o = QR_ROWS / 2; o; o >>= 1) {
-    if (t < o) {
-#pragma unroll
-      for (int j = 0; j < 16; ++j)
-        if (j < K) sm[j][t] += sm[j][t + o];
+  for (int j = 0; j < 16; ++j) {
+    if (j < K) {
+      const double w = warp_sum_d(v[j]);  // fixed xor tree
+      if (lane == 0) sm[j][warp] = w;
     }
-    __syncthreads();
   }
-  if (t < K) segsum[(int64_t)blockIdx.x * K + t] = sm[t][0];
+  __syncthreads();
+  if (t < K) {
+    double s2 = 0.0;
+#pragma unroll
+    for (int w = 0; w < QR_ROWS / 32; ++w) s2 += sm[t][w];
+    segsum[(int64_t)blockIdx.x * K + t] = s2;
+  }
   __syncthreads();
   if (t == 0) {
     __threadfence();
