@@ -124,13 +124,12 @@ k_ps_chol(const PLayer* __restrict__ pl, double* __restrict__ G) {
     for (int b = j + 1 + lane; b < r; b += 32) Rm[j][b] = z ? 0.0 : Rm[j][b] / d;
     __syncwarp();
     if (lane == 0) Rm[j][j] = d;
-    // trailing update over the pairs a <= b of rows/cols j+1 .. r-1
-    const int n = r - j - 1;
-    for (int t = lane; t < n * (n + 1) / 2; t += 32) {
-      int a = 0, rem = t;
-      while (rem >= n - a) { rem -= n - a; ++a; }
-      const int aa = j + 1 + a, bb = aa + rem;
-      Rm[aa][bb] -= Rm[j][aa] * Rm[j][bb];
+    // trailing update over the pairs a <= b of rows/cols j+1 .. r-1: lane owns column b
+    // (RMAX <= 64: at most two columns per lane), rows a ascending -- the same
+    // operation and rounding per entry as the pair loop, without index decoding
+    for (int bb = j + 1 + lane; bb < r; bb += 32) {
+      const double rb = Rm[j][bb];
+      for (int aa = j + 1; aa <= bb; ++aa) Rm[aa][bb] = fma(-Rm[j][aa], rb, Rm[aa][bb]);
     }
     __syncwarp();
   }
