@@ -341,3 +341,45 @@ def test_c5_sampled_full_size(lg, ref):
         assert np.array_equal(gb[i], ref_bits[i])
         assert (np.abs(ge[i] - ref_err[i]) / np.maximum(ref_err[i], 1e-300)).max() <= 1e-5, i
     ctx.close()
+
+
+def test_device_chain_without_sync_matches_synced(lg):
+    """profile -> solve -> compress_allreduce_dev chained on one stream with no host
+    synchronisation (the PDL-launched kernels wait in-kernel for their producers) gives
+    bitwise the same plans, EF and outputs over several steps as the same calls with a
+    device synchronisation after each."""
+    layers = W.config_layers("C4")
+    g, e = W.gaussian_outliers(layers, seed=21)
+    L, K = len(layers), len(BITS)
+    comp = torch.tensor([l.compress for l in layers], dtype=torch.int32, device="cuda")
+    dflt = torch.full((L,), BITS.index(4), dtype=torch.int32, device="cuda")
+
+    def run(sync):
+        ctx = lg.Context(layers, lg.QSGD, BITS, seed=9)
+        gd, ed = _dev(g), _dev(e)
+        out = torch.empty_like(gd)
+        err = torch.empty(L, K, dtype=torch.float64, device="cuda")
+        bits = torch.empty(L, K, dtype=torch.int64, device="cuda")
+        ch = torch.empty(L, dtype=torch.int32, device="cuda")
+        info = torch.empty(48, dtype=torch.uint8, device="cuda")
+        ws = torch.empty(lg.solve_workspace_bytes(L, K, 10000), dtype=torch.uint8, device="cuda")
+        outs = []
+        for s in range(4):
+            ctx.profile(gd, ed, s, err, bits)
+            if sync: torch.cuda.synchronize()
+            lg.solve(err, bits, dflt, comp, D=10000, choice=ch, info=info, workspace=ws)
+            if sync: torch.cuda.synchronize()
+            ctx.compress_allreduce_dev(ch, gd, ed, out, s)
+            if sync: torch.cuda.synchronize()
+            outs.append((ch.clone(), out.clone()))
+        torch.cuda.synchronize()
+        ctx.check()
+        ctx.close()
+        return outs, ed
+
+    a, ea = run(False)
+    b, eb = run(True)
+    for (c1, o1), (c2, o2) in zip(a, b):
+        assert torch.equal(c1, c2)
+        assert torch.equal(o1.view(torch.int32), o2.view(torch.int32))
+    assert torch.equal(ea.view(torch.int32), eb.view(torch.int32))
