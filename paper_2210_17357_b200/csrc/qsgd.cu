@@ -419,6 +419,7 @@ k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const QIn
     }
   };
   auto load_info = [&](int ci) -> QInfo { return (ci < nqc) ? qinfo[ci] : QInfo{0, 0u, 0}; };
+  pdl_wait();  // g / e (and the ticket reset) of the preceding kernels
   int c = resolve(grab_issue());
   if (c >= nqc) { finish(); return; }
   if (lane == 0) {
@@ -1042,8 +1043,10 @@ cudaError_t launch_qprofile(const QProfileArgs& a, cudaStream_t st) {
     if (occ == 0 && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_qprofile_q<KT>, QP_THREADS, smem) != \
                      cudaSuccess || occ < 1)) occ = 1;                                                          \
     const int grid = std::max(1, std::min(a.nqwarps / QP_WARPS, nsm * occ));                                    \
-    k_qprofile_q<KT><<<grid, QP_THREADS, smem, st>>>(a.g, a.e, a.qinfo, a.nqchunks, a.ticket, a.cs, a.K, a.k0,  \
-                                                    a.k1, a.rankfield, a.step, a.ptr_aligned, a.partial);        \
+    const cudaError_t e2 = launch_pdl(k_qprofile_q<KT>, dim3(grid), dim3(QP_THREADS), smem, st, a.g, a.e,       \
+                                      a.qinfo, a.nqchunks, a.ticket, a.cs, a.K, a.k0, a.k1, a.rankfield, a.step,   \
+                                      a.ptr_aligned, a.partial);                                                 \
+    if (e2 != cudaSuccess) return e2;                                                                            \
   }
       switch (a.K) {
         case 4: LG_QQ(4); break;
