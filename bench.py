@@ -318,7 +318,7 @@ def run_ours(args):
             # with the plan fixed), which is what runs between replans
             "plan_fixed_gbs": round(world * 4.0 * N / (stage["compress_allreduce"] * 1e-3) / 1e9, 2),
             "stage_ms": {k: round(v, 4) for k, v in stage.items()},
-            "roofline": {"bound": "alu", "kernel": "k_qprofile (K1)", "achieved": round(k1_tops, 3),
+            "roofline": {"bound": "alu", "kernel": "k_qprofile_q (K1)", "achieved": round(k1_tops, 3),
                          "peak": round(alu_peak, 3), "unit": "T lane-op/s", "frac": round(k1_tops / alu_peak, 4),
                          "traffic": traffic, "peak_source": f"derived: {nsm} SMs x 4 SMSP x 32 lanes x {sm_mhz:.0f} MHz",
                          "kernel_ms": round(k1_ms, 4), "launches_timed": k1_n,
