@@ -146,6 +146,16 @@ int lgreco_solve(const double* d_err, const int64_t* d_bits, int32_t L, int32_t 
                  uint32_t flags, int32_t* d_choice, lgreco_solve_info* d_info,
                  void* d_workspace, size_t workspace_bytes, void* stream);
 
+/* Weighted objective ("minimize sum size(l, c^l) *
+ * T(l)" and PAPER.md:680-682 bucket priorities "multiplying the size of each layer by the
+ * index of the bucket"): d_out[l*K + c] = d_bits[l*K + c] * d_weight[l] (int64, exact) for
+ * lgreco_solve to minimise.  A negative weight or a product that overflows int64 writes
+ * -1 (lgreco_solve then reports LGRECO_EINVAL).  Real-valued coefficients T(l) are
+ * quantised by the caller (paper_2210_17357_b200/objectives.py).  All pointers DEVICE:
+ * d_bits, d_out L*K, d_weight L; d_out may alias d_bits. */
+int lgreco_weight_costs(const int64_t* d_bits, const int64_t* d_weight, int32_t L, int32_t K,
+                        int64_t* d_out, void* stream);
+
 /* (a7) Plan agreement: broadcast d_choice (L int32) from rank 0.
  * No-op when world == 1. */
 int lgreco_plan_broadcast(lgreco_ctx* ctx, int32_t* d_choice, void* stream);

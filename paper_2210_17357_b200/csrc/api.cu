@@ -403,6 +403,13 @@ int lgreco_profile(lgreco_ctx* c, const float* d_g, const float* d_ef, uint64_t 
   return LGRECO_EUNSUPPORTED;
 }
 
+int lgreco_weight_costs(const int64_t* d_bits, const int64_t* d_weight, int32_t L, int32_t K, int64_t* d_out,
+                        void* stream) {
+  if (!d_bits || !d_weight || !d_out || L < 0 || K <= 0) { lg_set_error("weight_costs: bad argument"); return LGRECO_EINVAL; }
+  LG_CUDA(lg::launch_weight_costs(d_bits, d_weight, L, K, d_out, (cudaStream_t)stream));
+  return LGRECO_OK;
+}
+
 size_t lgreco_solve_workspace_bytes(int32_t L, int32_t K, int32_t D) {
   if (L < 0 || K <= 0 || D <= 0) return 0;
   return lg::solve_workspace_bytes(L, K, D);

@@ -1425,6 +1425,30 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
 #endif
 }
 
+// Weighted costs (NEXT-1): out = bits * w[l], exact in int64; -1 on a negative input or
+// overflow (lgreco_solve rejects negative costs with LGRECO_EINVAL).
+__global__ void k_weight_costs(const int64_t* __restrict__ bits, const int64_t* __restrict__ w, int L, int K,
+                               int64_t* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (int64_t)L * K;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = bits[i], x = w[i / K];
+    int64_t r = -1;
+    if (b >= 0 && x >= 0) {
+      const unsigned long long hi = __umul64hi((unsigned long long)b, (unsigned long long)x);
+      const unsigned long long lo = (unsigned long long)b * (unsigned long long)x;
+      if (hi == 0 && lo <= (unsigned long long)INT64_MAX) r = (int64_t)lo;
+    }
+    out[i] = r;
+  }
+}
+
+cudaError_t launch_weight_costs(const int64_t* bits, const int64_t* w, int L, int K, int64_t* out, cudaStream_t st) {
+  const int64_t n = (int64_t)L * K;
+  if (n <= 0) return cudaSuccess;
+  k_weight_costs<<<(unsigned)std::min<int64_t>((n + 255) / 256, 1024), 256, 0, st>>>(bits, w, L, K, out);
+  return cudaGetLastError();
+}
+
 static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
 size_t solve_workspace_bytes(int L, int K, int D) {

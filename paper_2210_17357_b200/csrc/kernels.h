@@ -148,6 +148,7 @@ struct SolveArgs {
   uint8_t* pd; int32_t* act;  // workspace: L*(D+1) bytes, L ints
 };
 size_t solve_workspace_bytes(int L, int K, int D);
+cudaError_t launch_weight_costs(const int64_t* bits, const int64_t* w, int L, int K, int64_t* out, cudaStream_t st);
 cudaError_t launch_solve(const SolveArgs& a, void* workspace, cudaStream_t st);
 
 }  // namespace lg

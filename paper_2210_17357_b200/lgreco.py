@@ -58,6 +58,7 @@ _SIGS = {
     "lgreco_profile": (C.c_int, [_VP, _VP, _VP, _U64, _VP, _VP, _VP]),
     "lgreco_solve_workspace_bytes": (C.c_size_t, [_I32, _I32, _I32]),
     "lgreco_solve": (C.c_int, [_VP, _VP, _I32, _I32, _VP, _VP, _I32, _U32, _VP, _VP, _VP, C.c_size_t, _VP]),
+    "lgreco_weight_costs": (C.c_int, [_VP, _VP, _I32, _I32, _VP, _VP]),
     "lgreco_plan_broadcast": (C.c_int, [_VP, _VP, _VP]),
     "lgreco_compress_allreduce": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _U64, _VP]),
     "lgreco_compress_allreduce_dev": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _U64, _VP]),
@@ -285,6 +286,15 @@ def solve(err, bits, default_idx, compress=None, D=10000, flags=0, choice=None, 
                               _ptr(choice), _ptr(info), _ptr(workspace), workspace.numel(), _stream(stream)),
            "solve")
     return choice, info
+
+
+def weight_costs(bits, weight, out=None, stream=None):
+    """Device: out[l, c] = bits[l, c] * weight[l] (int64 cuda tensors; -1 on overflow)."""
+    L, K = bits.shape
+    if out is None:
+        out = torch.empty_like(bits)
+    _check(lib().lgreco_weight_costs(_ptr(bits), _ptr(weight), L, K, _ptr(out), _stream(stream)), "weight_costs")
+    return out
 
 
 def read_info(info_tensor) -> SolveInfo:

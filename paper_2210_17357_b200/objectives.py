@@ -1,0 +1,55 @@
+"""Per-layer weights for the time-weighted objective and the bucket priorities
+(SURVEY.md 8(f) NEXT-1).  Host-side planning helpers: they produce the integer weight
+vector that `lgreco.weight_costs` multiplies into the size table on the device before
+`lgreco.solve` (the DP itself is unchanged; only its cost table is).
+
+  PAPER.md:350-356  minimize sum_l size(l, c^l) * T(l)  s.t.  sum_l error(l, c^l) <= Emax,
+                    T(b) the per-bucket coefficients of a linear regression of measured
+                    synchronisation time on the transmitted bucket sizes.
+  PAPER.md:680-682  bucket prioritisation: "multiplying the size of each layer by the
+                    index of the bucket the layer is communicated in".
+"""
+import numpy as np
+
+
+def ddp_buckets(layers, bucket_bytes=25 * 2 ** 20, first_bucket_bytes=2 ** 20, elem_bytes=4):
+    """Bucket index (0 = transmitted first) of every layer, PyTorch-DDP style: gradients
+    become ready in reverse layer order (backward), so buckets are filled from the last
+    layer backwards; the first bucket is capped at `first_bucket_bytes`, the others at
+    `bucket_bytes`; a layer larger than the cap gets a bucket of its own."""
+    out = [0] * len(layers)
+    b, fill, cap = 0, 0, first_bucket_bytes
+    for i in reversed(range(len(layers))):
+        nbytes = layers[i].numel * elem_bytes
+        if fill > 0 and fill + nbytes > cap:
+            b, fill, cap = b + 1, 0, bucket_bytes
+        out[i] = b
+        fill += nbytes
+    return out
+
+
+def bucket_priority_weights(layers, **kw):
+    """weight of a layer = 1-based index of the bucket it is sent in."""
+    return np.array([b + 1 for b in ddp_buckets(layers, **kw)], dtype=np.int64)
+
+
+def fit_bucket_time(sizes, times, intercept=True):
+    """least-squares linear model time ~ sum_b sizes[:, b] * T(b) (+ c)
+    over measured samples.  sizes: (S, nb) transmitted bytes (or bits) per bucket,
+    times: (S,) synchronisation times.  Returns (T (nb,), c)."""
+    A = np.asarray(sizes, dtype=np.float64)
+    y = np.asarray(times, dtype=np.float64)
+    if intercept:
+        A = np.hstack([A, np.ones((A.shape[0], 1))])
+    coef, *_ = np.linalg.lstsq(A, y, rcond=None)
+    return (coef[:-1], float(coef[-1])) if intercept else (coef, 0.0)
+
+
+def time_weights(layers, T, buckets=None, scale=2 ** 16):
+    """Integer weights w_l = max(1, round(scale * T(bucket(l)) / max_b T(b))) -- the DP needs
+    exact integer costs; `scale` sets the resolution of the quantised coefficients."""
+    T = np.asarray(T, dtype=np.float64)
+    if buckets is None:
+        buckets = ddp_buckets(layers)
+    tmax = float(T.max()) if T.size and T.max() > 0 else 1.0
+    return np.array([max(1, int(round(scale * max(T[b], 0.0) / tmax))) for b in buckets], dtype=np.int64)

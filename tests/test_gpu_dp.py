@@ -105,3 +105,28 @@ def test_narrow_keys_ties_and_bands(lg, ref, K, single):
         assert list(c_gpu) == list(c_ref), (K, D)
         assert (i_gpu.total_bits, i_gpu.used_default) == (i_ref.total_bits, i_ref.used_default)
         assert i_gpu.emax == i_ref.emax and i_gpu.total_err == i_ref.total_err
+
+
+def test_weighted_costs_and_solve(lg, ref):
+    """NEXT-1: the device product bits * w is exact (-1 on
+    overflow or a negative input), and the solve on it reproduces the oracle's weighted
+    plan (C4-sized table, DDP bucket-priority weights)."""
+    from paper_2210_17357_b200 import objectives as O
+    layers = W.config_layers("C4")
+    L, K = len(layers), 7
+    rng = np.random.default_rng(77)
+    err, bits = _table(rng, L, K)
+    w = O.bucket_priority_weights(layers)
+    b_d = torch.from_numpy(bits).cuda()
+    w_d = torch.from_numpy(w).cuda()
+    wb = lg.weight_costs(b_d, w_d).cpu().numpy()
+    assert np.array_equal(wb, bits * w[:, None])
+    # overflow and negative inputs -> -1
+    big = torch.tensor([[2 ** 62, 5], [-3, 7]], dtype=torch.int64, device="cuda")
+    ww = torch.tensor([4, -1], dtype=torch.int64, device="cuda")
+    assert lg.weight_costs(big, ww).cpu().tolist() == [[-1, 20], [-1, -1]]
+    comp = np.array([l.compress for l in layers], np.int32)
+    dflt = np.full(L, 2, np.int32)
+    st, c_ref, i_ref = ref.solve(err, bits * w[:, None], dflt, comp, D=10000)
+    c_gpu, i_gpu = _run(lg, err, wb, dflt, comp, 10000, 0)
+    assert list(c_gpu) == list(c_ref) and i_gpu.total_bits == i_ref.total_bits
