@@ -2,6 +2,7 @@
 PY      ?= python
 SITE    := $(shell $(PY) -c "import sysconfig;print(sysconfig.get_paths()['purelib'])")
 NCCL    := $(SITE)/nvidia/nccl
+CUSOLVER := $(SITE)/nvidia/cusolver
 CUDART  := $(SITE)/nvidia/cuda_runtime/lib
 NVCC    ?= nvcc
 ARCH    := -gencode arch=compute_100a,code=sm_100a
@@ -25,7 +26,8 @@ build/obj/%.o: $(PKG)/csrc/%.cu $(HDRS)
 
 $(LIB): $(OBJS)
 	$(NVCC) $(ARCH) -cudart shared -shared -o $@ $(OBJS) -L$(NCCL)/lib -l:libnccl.so.2 \
-	    -Xlinker -rpath=$(NCCL)/lib -Xlinker -rpath=$(CUDART)
+	    -L$(CUSOLVER)/lib -l:libcusolver.so.11 \
+	    -Xlinker -rpath=$(NCCL)/lib -Xlinker -rpath=$(CUDART) -Xlinker -rpath=$(CUSOLVER)/lib
 	cat build/obj/*.ptxas.log > build/ptxas.log
 
 $(ORACLE): oracle/lgreco_ref.c
@@ -43,6 +45,7 @@ build/obj/dp_timing.o: $(PKG)/csrc/dp.cu $(HDRS)
 
 build/liblgreco_timing.so: $(filter-out build/obj/dp.o,$(OBJS)) build/obj/dp_timing.o
 	$(NVCC) $(ARCH) -cudart shared -shared -o $@ $^ -L$(NCCL)/lib -l:libnccl.so.2 \
-	    -Xlinker -rpath=$(NCCL)/lib -Xlinker -rpath=$(CUDART)
+	    -L$(CUSOLVER)/lib -l:libcusolver.so.11 \
+	    -Xlinker -rpath=$(NCCL)/lib -Xlinker -rpath=$(CUDART) -Xlinker -rpath=$(CUSOLVER)/lib
 
 timing: build/liblgreco_timing.so

@@ -130,6 +130,17 @@ int lgreco_ctx_kernel_ms(lgreco_ctx* ctx, double* total_ms, int64_t* count);
 int lgreco_profile(lgreco_ctx* ctx, const float* d_g, const float* d_ef, uint64_t step,
                    double* d_err, int64_t* d_bits, void* stream);
 
+/* (a4, NEXT-2) PowerSGD profile by singular values: for every layer l
+ * and candidate rank r, d_err[l*K+j] = sqrt(sum_{i > r} sigma_i^2) of the m x k view of
+ * x = d_g + d_ef (the optimal rank-r error, Eckart-Young), d_bits as lgreco_profile
+ * (32 r (m + k), or 32 numel for lossless candidates / layers).  Squared singular
+ * values = eigenvalues of the fp64 Gram matrix of the smaller side (cuSOLVER dsyevd,
+ * values only); the paper's choice when the rank range is large.  PowerSGD ctx only
+ * (LGRECO_EUNSUPPORTED otherwise); may synchronise the stream (cuSOLVER).  d_g / d_ef
+ * 4-byte aligned; d_err L*K doubles, d_bits L*K int64. */
+int lgreco_psgd_profile_svd(lgreco_ctx* ctx, const float* d_g, const float* d_ef, double* d_err,
+                            int64_t* d_bits, void* stream);
+
 /* Device workspace bytes lgreco_solve needs for (L, K, D). */
 size_t lgreco_solve_workspace_bytes(int32_t L, int32_t K, int32_t D);
 

@@ -283,6 +283,33 @@ def psgd_profile(layers, g, e, ranks, steps=5, seed=0, step=0):
     return err, bits
 
 
+def psgd_svd_profile(layers, g, e, ranks):
+    """NEXT-2: e_r = sqrt(sum_{i > r} sigma_i^2) of the m x k view of
+    x = fl32(fl32(g + e) + 0) (R2, R11), singular values by LAPACK (numpy, fp64); lossless
+    candidates r (m + k) >= m k and vector / uncompressed layers: err 0, bits 32 n."""
+    g = np.asarray(g, np.float32)
+    x = g if e is None else (g + np.asarray(e, np.float32)).astype(np.float32)
+    x = (x + np.float32(0)).astype(np.float32)
+    L, K = len(layers), len(ranks)
+    err = np.zeros((L, K), np.float64)
+    bits = np.zeros((L, K), np.int64)
+    for l, ly in enumerate(layers):
+        bits[l, :] = 32 * ly.numel
+        if not ly.compress or ly.rows <= 0:
+            continue
+        m, k = int(ly.rows), int(ly.cols)
+        lossy = [not psgd_lossless(m, k, r) for r in ranks]
+        if not any(lossy):
+            continue
+        M = x[ly.offset:ly.offset + ly.numel].astype(np.float64).reshape(m, k)
+        sv = np.linalg.svd(M, compute_uv=False)  # descending
+        for j, r in enumerate(ranks):
+            if lossy[j]:
+                err[l, j] = float(np.sqrt(np.sum(sv[r:] ** 2)))
+                bits[l, j] = 32 * r * (m + k)
+    return err, bits
+
+
 def psgd_lossless(m, k, r):
     return r * (m + k) >= m * k
 

@@ -302,6 +302,7 @@ int lgreco_ctx_create(lgreco_ctx** out, const lgreco_layer* layers, int32_t L, c
 }
 
 void lgreco_ctx_destroy(lgreco_ctx* c) {
+  if (c) svd_destroy(c);
   if (!c) return;
   topk_destroy(c);
   psgd_destroy(c);

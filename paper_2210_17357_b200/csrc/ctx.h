@@ -86,6 +86,8 @@ struct lgreco_ctx {
   struct Topk* tk = nullptr;
   // PowerSGD state (family == LGRECO_POWERSGD)
   struct Psgd* ps = nullptr;
+  // SVD-profile workspace (svd.cu, created on first use)
+  void* svd = nullptr;
 };
 
 // family-specific parts (api_topk.cu, api_psgd.cu)
@@ -116,5 +118,6 @@ int psgd_raw_combine(lgreco_ctx* c, const int32_t* choice, int W, const uint8_t*
 int psgd_compress_allreduce(lgreco_ctx* c, const int32_t* choice, const float* g, float* ef, float* out,
                             uint64_t step, cudaStream_t st);
 int64_t psgd_sizes(lgreco_ctx* c, int which);
+void svd_destroy(lgreco_ctx* c);
 
 

@@ -59,6 +59,7 @@ _SIGS = {
     "lgreco_solve_workspace_bytes": (C.c_size_t, [_I32, _I32, _I32]),
     "lgreco_solve": (C.c_int, [_VP, _VP, _I32, _I32, _VP, _VP, _I32, _U32, _VP, _VP, _VP, C.c_size_t, _VP]),
     "lgreco_weight_costs": (C.c_int, [_VP, _VP, _I32, _I32, _VP, _VP]),
+    "lgreco_psgd_profile_svd": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP]),
     "lgreco_plan_broadcast": (C.c_int, [_VP, _VP, _VP]),
     "lgreco_compress_allreduce": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _U64, _VP]),
     "lgreco_compress_allreduce_dev": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _U64, _VP]),
@@ -164,6 +165,11 @@ class Context:
     def profile(self, g, ef, step, err, bits, stream=None):
         _check(lib().lgreco_profile(self.h, _ptr(g), _ptr(ef), step, _ptr(err), _ptr(bits), _stream(stream)),
                "profile")
+
+    def profile_svd(self, g, ef, err, bits, stream=None):
+        """PowerSGD errors of every candidate rank from the singular values (NEXT-2)."""
+        _check(lib().lgreco_psgd_profile_svd(self.h, _ptr(g), _ptr(ef), _ptr(err), _ptr(bits), _stream(stream)),
+               "psgd_profile_svd")
 
     def compress_allreduce(self, choice, g, ef, out, step, stream=None):
         _check(lib().lgreco_compress_allreduce(self.h, _i32(choice), _ptr(g), _ptr(ef), _ptr(out), step,

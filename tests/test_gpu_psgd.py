@@ -165,3 +165,38 @@ def test_compress_allreduce_w1(lg, ref):
     assert _rel(out.cpu().numpy(), out_ref) <= 1e-5
     assert _rel(ed.cpu().numpy(), es_ref[0]) <= 1e-5
     ctx.check()
+
+
+@pytest.mark.parametrize("cfg", ["C2", "tall"])
+def test_profile_svd_parity(lg, ref, cfg):
+    """NEXT-2: errors of every candidate rank from the singular values (fp64 Gram of the
+    smaller side + cuSOLVER eigenvalues) vs the oracle's LAPACK SVD; bits identical."""
+    if cfg == "C2":
+        layers = W.config_layers("C2")
+        g, _ = W.low_rank_plus_noise(layers, seed=8)
+        e = (np.random.default_rng(8).standard_normal(g.size) * 1e-4).astype(np.float32)
+    else:  # m > k (Gram of the columns), a wide one, a vector, an uncompressed matrix
+        shapes = [(3000, 40, 1), (40, 700, 1), (1, 333, 0), (300, 200, 0), (257, 129, 1)]
+        layers, off = [], 0
+        for m, k, c in shapes:
+            layers.append(W.Layer(off, m * k, m, k, c) if m > 1 else W.Layer(off, k, 0, 0, c))
+            off += m * k
+        rng = np.random.default_rng(9)
+        g = np.zeros(off, np.float32)
+        for l in layers:
+            if l.rows > 0:
+                A = rng.standard_normal((l.rows, 8)) @ rng.standard_normal((8, l.cols))
+                g[l.offset:l.offset + l.numel] = (A + 0.1 * rng.standard_normal((l.rows, l.cols))).astype(np.float32).ravel()
+        e = (rng.standard_normal(off) * 1e-3).astype(np.float32)
+    ranks = W.PSGD_RANKS_C2
+    ctx = lg.Context(layers, lg.POWERSGD, ranks, seed=3)
+    L, K = len(layers), len(ranks)
+    err = torch.empty(L, K, dtype=torch.float64, device="cuda")
+    bits = torch.empty(L, K, dtype=torch.int64, device="cuda")
+    ctx.profile_svd(_dev(g), _dev(e), err, bits)
+    r_err, r_bits = ref.psgd_svd_profile(layers, g, e, ranks)
+    assert np.array_equal(bits.cpu().numpy(), r_bits)
+    ge = err.cpu().numpy()
+    assert np.all((r_err == 0) == (ge == 0))
+    assert (np.abs(ge - r_err) / np.maximum(r_err, 1e-300)).max() <= 1e-6
+    ctx.close()
