@@ -1,0 +1,115 @@
+"""NEXT-3: L-GreCo as a PyTorch DDP communication hook (PAPER.md:312-314
+"accumulate the gradients ... the designated worker computes the errors ... runs the
+dynamic programming ... and broadcasts the mapping", PAPER.md:343 buckets).
+
+Per DDP bucket (its parameters form the layer table, >= 2-D tensors compressed, R8):
+  * warm-up steps: plain all-reduce of the bucket (the paper's uncompressed warm-up),
+    the local gradient accumulated into G;
+  * at every replan boundary (end of the warm-up, then every `replan_every` steps):
+    lgreco_profile on the accumulated G (paper mode: no EF, R2), lgreco_solve, the plan
+    broadcast from rank 0 (R21), G reset;
+  * other steps: lgreco_compress_allreduce_dev with the current plan and the bucket's
+    error-feedback buffer -- the compressed exchange and decode -- and G += g.
+Every compute step runs in the library's kernels on the current stream; this module is
+orchestration only (bucket bookkeeping, which call when).
+
+Usage:
+    state = LGrecoHook(lgreco.QSGD, workloads.QSGD_BITS, default_idx=2)
+    ddp_model.register_comm_hook(state, LGrecoHook.hook)
+"""
+import torch
+import torch.distributed as dist
+
+from . import lgreco
+from . import workloads as W
+
+
+class _Bucket:
+    def __init__(self, owner, layers, device):
+        self.layers = layers
+        L, K = len(layers), owner.K
+        n = W.total_numel(layers)
+        nid = None
+        if owner.world > 1:
+            obj = [lgreco.nccl_unique_id() if owner.rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0, group=owner.pg)
+            nid = obj[0]
+        self.ctx = lgreco.Context(layers, owner.family, owner.params, qbucket=owner.qbucket, seed=owner.seed,
+                                  rank=owner.rank, world=owner.world, nccl_id=nid)
+        self.ef = torch.zeros(n, dtype=torch.float32, device=device)
+        self.G = torch.zeros(n, dtype=torch.float32, device=device)
+        self.out = torch.empty(n, dtype=torch.float32, device=device)
+        self.err = torch.empty(L, K, dtype=torch.float64, device=device)
+        self.bits = torch.empty(L, K, dtype=torch.int64, device=device)
+        self.dflt = torch.full((L,), owner.default_idx, dtype=torch.int32, device=device)
+        self.comp = torch.tensor([l.compress for l in layers], dtype=torch.int32, device=device)
+        self.choice = torch.full((L,), owner.default_idx, dtype=torch.int32, device=device)
+        self.info = torch.empty(48, dtype=torch.uint8, device=device)
+        self.ws = torch.empty(lgreco.solve_workspace_bytes(L, K, owner.D), dtype=torch.uint8, device=device)
+        self.calls = 0
+        self.planned = False
+
+
+class LGrecoHook:
+    def __init__(self, family, params, default_idx, *, warmup_steps=10, replan_every=100, D=10000, seed=0x5EED,
+                 qbucket=128, flags=0, process_group=None, record=False):
+        self.family, self.params = family, [int(p) for p in params]
+        self.K = len(self.params)
+        self.default_idx = int(default_idx)
+        self.warmup, self.replan_every = int(warmup_steps), int(replan_every)
+        self.D, self.seed, self.qbucket, self.flags = int(D), int(seed), int(qbucket), int(flags)
+        self.pg = process_group
+        self.world = dist.get_world_size(process_group)
+        self.rank = dist.get_rank(process_group)
+        self.buckets: dict[tuple, _Bucket] = {}
+        self.record = record
+        self.last = {}  # bucket index -> (g, ef_before, choice, step) when record=True
+
+    def _state(self, bucket):
+        shapes = tuple(tuple(p.shape) for p in bucket.parameters())
+        key = (bucket.index(), shapes)
+        st = self.buckets.get(key)
+        if st is None:  # new bucket layout (DDP rebuilds its buckets after the first step)
+            layers = W.layer_table([(None, s) for s in shapes])
+            st = _Bucket(self, layers, bucket.buffer().device)
+            self.buckets[key] = st
+        return st
+
+    def _replan(self, st):
+        """Profile the accumulated gradient (paper mode), solve, agree on rank 0's plan."""
+        st.ctx.profile(st.G, None, st.calls, st.err, st.bits)
+        lgreco.solve(st.err, st.bits, st.dflt, st.comp, D=self.D, flags=self.flags, choice=st.choice, info=st.info,
+                     workspace=st.ws)
+        st.ctx.plan_broadcast(st.choice)
+        st.G.zero_()
+        st.planned = True
+
+    @staticmethod
+    def hook(state: "LGrecoHook", bucket: dist.GradBucket) -> torch.futures.Future[torch.Tensor]:
+        st = state._state(bucket)
+        g = bucket.buffer()
+        st.calls += 1
+        step = st.calls
+        if step <= state.warmup or not st.planned:
+            st.G.add_(g)
+            if step >= state.warmup:
+                state._replan(st)
+            fut = dist.all_reduce(g, group=state.pg, async_op=True).get_future()
+            world = state.world
+            return fut.then(lambda f: f.value()[0].div_(world))
+        rec = (g.clone(), st.ef.clone(), st.choice.clone(), step) if state.record else None
+        st.G.add_(g)
+        st.ctx.compress_allreduce_dev(st.choice, g, st.ef, st.out, step)
+        g.copy_(st.out)
+        if rec is not None:
+            state.last[bucket.index()] = rec + (st.out.clone(), st.layers)
+        if (step - state.warmup) % state.replan_every == 0:
+            state._replan(st)
+        fut = torch.futures.Future()
+        fut.set_result(g)
+        return fut
+
+    def close(self):
+        for st in self.buckets.values():
+            st.ctx.close()
+        self.buckets.clear()
