@@ -167,6 +167,12 @@ int lgreco_solve(const double* d_err, const int64_t* d_bits, int32_t L, int32_t 
 int lgreco_weight_costs(const int64_t* d_bits, const int64_t* d_weight, int32_t L, int32_t K,
                         int64_t* d_out, void* stream);
 
+/* Per-layer gradient norms (the Accordion-style default schedule,
+ * PAPER.md:596 "used these parameters as the default set of parameters in L-GreCo"):
+ * d_norm[l] = sqrt(sum_i x_i^2) over layer l of x = d_g (+ d_ef, nullable), fp64,
+ * fixed-order (deterministic).  d_norm: L doubles (DEVICE). */
+int lgreco_layer_norms(lgreco_ctx* ctx, const float* d_g, const float* d_ef, double* d_norm, void* stream);
+
 /* (a7) Plan agreement: broadcast d_choice (L int32) from rank 0.
  * No-op when world == 1. */
 int lgreco_plan_broadcast(lgreco_ctx* ctx, int32_t* d_choice, void* stream);

@@ -115,7 +115,36 @@ __global__ void k_svd_rows_init(const DevLayer* __restrict__ layers, int L, int 
   }
 }
 
+// per-layer sum of squares: one CTA per layer, fixed strided order + fixed tree
+__global__ void __launch_bounds__(256)
+k_layer_norms(const float* __restrict__ g, const float* __restrict__ e, const DevLayer* __restrict__ layers,
+              double* __restrict__ norm) {
+  __shared__ double sm[256];
+  const DevLayer ly = layers[blockIdx.x];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < ly.numel; i += 256) {
+    const float x = __fadd_rn(__fadd_rn(g[ly.offset + i], e ? e[ly.offset + i] : 0.f), 0.f);
+    s = fma((double)x, (double)x, s);
+  }
+  sm[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = 128; o; o >>= 1) {
+    if (threadIdx.x < o) sm[threadIdx.x] += sm[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) norm[blockIdx.x] = sqrt(sm[0]);
+}
+
 }  // namespace lg
+
+extern "C" int lgreco_layer_norms(lgreco_ctx* c, const float* d_g, const float* d_ef, double* d_norm, void* stream) {
+  if (!c || !d_g || !d_norm) { lg_set_error("null argument"); return LGRECO_EINVAL; }
+  if (c->L == 0) return LGRECO_OK;
+  lg::k_layer_norms<<<c->L, 256, 0, (cudaStream_t)stream>>>(d_g, d_ef, c->d_layers, d_norm);
+  LG_CUDA(cudaGetLastError());
+  c->launches += 1;
+  return LGRECO_OK;
+}
 
 struct SvdWs {
   cusolverDnHandle_t h = nullptr;

@@ -60,6 +60,7 @@ _SIGS = {
     "lgreco_solve": (C.c_int, [_VP, _VP, _I32, _I32, _VP, _VP, _I32, _U32, _VP, _VP, _VP, C.c_size_t, _VP]),
     "lgreco_weight_costs": (C.c_int, [_VP, _VP, _I32, _I32, _VP, _VP]),
     "lgreco_psgd_profile_svd": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP]),
+    "lgreco_layer_norms": (C.c_int, [_VP, _VP, _VP, _VP, _VP]),
     "lgreco_plan_broadcast": (C.c_int, [_VP, _VP, _VP]),
     "lgreco_compress_allreduce": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _U64, _VP]),
     "lgreco_compress_allreduce_dev": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _U64, _VP]),
@@ -170,6 +171,10 @@ class Context:
         """PowerSGD errors of every candidate rank from the singular values (NEXT-2)."""
         _check(lib().lgreco_psgd_profile_svd(self.h, _ptr(g), _ptr(ef), _ptr(err), _ptr(bits), _stream(stream)),
                "psgd_profile_svd")
+
+    def layer_norms(self, g, ef, norm, stream=None):
+        """Per-layer L2 norms of x = g (+ ef) into the L fp64 device tensor `norm`."""
+        _check(lib().lgreco_layer_norms(self.h, _ptr(g), _ptr(ef), _ptr(norm), _stream(stream)), "layer_norms")
 
     def compress_allreduce(self, choice, g, ef, out, step, stream=None):
         _check(lib().lgreco_compress_allreduce(self.h, _i32(choice), _ptr(g), _ptr(ef), _ptr(out), step,

@@ -1,5 +1,6 @@
 """Per-layer weights for the time-weighted objective and the bucket priorities
-(SURVEY.md 8(f) NEXT-1).  Host-side planning helpers: they produce the integer weight
+(SURVEY.md 8(f) NEXT-1), Accordion-style per-layer defaults and hybrid-family candidate
+tables (NEXT-4).  Host-side planning helpers: they produce the integer weight
 vector that `lgreco.weight_costs` multiplies into the size table on the device before
 `lgreco.solve` (the DP itself is unchanged; only its cost table is).
 
@@ -53,3 +54,31 @@ def time_weights(layers, T, buckets=None, scale=2 ** 16):
         buckets = ddp_buckets(layers)
     tmax = float(T.max()) if T.size and T.max() > 0 else 1.0
     return np.array([max(1, int(round(scale * max(T[b], 0.0) / tmax))) for b in buckets], dtype=np.int64)
+
+
+def accordion_defaults(prev_norm, cur_norm, low_idx, high_idx, eta=0.5):
+    """NEXT-4: per-layer defaults from an Accordion-style schedule --
+    a layer is in a critical regime when its gradient norm changed by at least `eta`
+    relative to the previous period (|n_t - n_{t-1}| / n_{t-1} >= eta); critical layers
+    get the low-compression candidate `low_idx`, the others `high_idx`.  The result is
+    the `default_idx` of lgreco_solve (the defaults set Emax, Alg.1 line 2)."""
+    p = np.asarray(prev_norm, dtype=np.float64)
+    c = np.asarray(cur_norm, dtype=np.float64)
+    crit = np.abs(c - p) >= eta * np.abs(p)
+    return np.where(crit, low_idx, high_idx).astype(np.int32)
+
+
+def hybrid_table(errs, bits, defaults_family=0):
+    """NEXT-4 hybrid strategies ("combining different compression techniques
+    inside the same model"): candidates of several families side by side in one table,
+    so Algorithm 1 picks a (family, parameter) per layer.  errs / bits: lists of (L, K_f)
+    arrays (numpy or torch, one per family, rows aligned by layer).  Returns the
+    concatenated (err, bits) and the list of (family, index) per column."""
+    cols = [(f, j) for f, e in enumerate(errs) for j in range(e.shape[1])]
+    try:
+        import torch
+        if isinstance(errs[0], torch.Tensor):
+            return torch.cat(list(errs), 1).contiguous(), torch.cat(list(bits), 1).contiguous(), cols
+    except ImportError:  # pragma: no cover
+        pass
+    return np.concatenate(errs, 1), np.concatenate(bits, 1), cols

@@ -383,3 +383,44 @@ def test_device_chain_without_sync_matches_synced(lg):
         assert torch.equal(c1, c2)
         assert torch.equal(o1.view(torch.int32), o2.view(torch.int32))
     assert torch.equal(ea.view(torch.int32), eb.view(torch.int32))
+
+
+def test_layer_norms(lg):
+    """NEXT-4 helper: per-layer L2 norms of g + e (fp64) vs numpy on the same fp32 x."""
+    layers = W.config_layers("C1")
+    g, e = W.gaussian_outliers(layers, seed=4)
+    ctx = lg.Context(layers, lg.QSGD, BITS, seed=1)
+    nrm = torch.empty(len(layers), dtype=torch.float64, device="cuda")
+    ctx.layer_norms(_dev(g), _dev(e), nrm)
+    x = (g + e).astype(np.float32).astype(np.float64)
+    ref_n = np.array([np.sqrt(np.sum(x[l.offset:l.offset + l.numel] ** 2)) for l in layers])
+    assert np.allclose(nrm.cpu().numpy(), ref_n, rtol=1e-12)
+    ctx.close()
+
+
+def test_hybrid_qsgd_topk_plan(lg, ref):
+    """NEXT-4 hybrid: QSGD and TopK profiles of the same layers side by side in one DP
+    table (device), solved on the GPU = the oracle's plan on the same table."""
+    from paper_2210_17357_b200 import objectives as O
+    layers = W.config_layers("C1")
+    g, e = W.gaussian_outliers(layers, seed=6)
+    L = len(layers)
+    ppm = [1000, 10000, 100000]
+    cq = lg.Context(layers, lg.QSGD, BITS, seed=2)
+    ct = lg.Context(layers, lg.TOPK, ppm, seed=2)
+    gd, ed = _dev(g), _dev(e)
+    eq = torch.empty(L, len(BITS), dtype=torch.float64, device="cuda")
+    bq = torch.empty(L, len(BITS), dtype=torch.int64, device="cuda")
+    et = torch.empty(L, len(ppm), dtype=torch.float64, device="cuda")
+    bt = torch.empty(L, len(ppm), dtype=torch.int64, device="cuda")
+    cq.profile(gd, ed, 0, eq, bq)
+    ct.profile(gd, ed, 0, et, bt)
+    err, bits, cols = O.hybrid_table([eq, et], [bq, bt])
+    dflt = torch.full((L,), BITS.index(4), dtype=torch.int32, device="cuda")
+    choice, info = lg.solve(err, bits, dflt, None, D=10000)
+    st, c_ref, i_ref = ref.solve(err.cpu().numpy(), bits.cpu().numpy(), dflt.cpu().numpy(), None, D=10000)
+    assert list(choice.cpu().numpy()) == list(c_ref)
+    fams = {cols[c][0] for c in c_ref}
+    assert fams <= {0, 1}
+    cq.close()
+    ct.close()

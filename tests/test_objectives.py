@@ -80,3 +80,32 @@ def test_fit_bucket_time_recovers_coefficients():
     assert np.allclose(Tf, T, rtol=1e-8) and abs(c - 4e-5) < 1e-9
     w = O.time_weights([W.Layer(0, 1, 0, 0, 1)] * 4, Tf, buckets=[0, 1, 2, 3], scale=600)
     assert list(w) == [600, 200, 100, 400]
+
+
+def test_accordion_defaults_rule():
+    prev = [1.0, 1.0, 2.0, 0.5]
+    cur = [1.6, 1.2, 0.9, 0.5]
+    # |dn| / n: 0.6, 0.2, 0.55, 0  -> critical, calm, critical, calm (eta = 0.5)
+    assert list(O.accordion_defaults(prev, cur, low_idx=4, high_idx=1, eta=0.5)) == [4, 1, 4, 1]
+
+
+def test_hybrid_table_picks_across_families(ref):
+    """Two families side by side: the DP optimum over the hybrid table is the brute-force
+    optimum over per-layer (family, parameter) choices."""
+    rng = np.random.default_rng(8)
+    for _ in range(60):
+        L = int(rng.integers(1, 5))
+        e1 = np.sort(rng.uniform(0, 1, (L, 2)), 1)[:, ::-1].copy()
+        b1 = np.sort(rng.integers(1, 500, (L, 2)), 1).astype(np.int64)
+        e2 = np.sort(rng.uniform(0, 1, (L, 2)), 1)[:, ::-1].copy()
+        b2 = np.sort(rng.integers(1, 500, (L, 2)), 1).astype(np.int64)
+        err, bits, cols = O.hybrid_table([e1, e2], [b1, b2])
+        assert err.shape == (L, 4) and cols == [(0, 0), (0, 1), (1, 0), (1, 1)]
+        dflt = np.full(L, 1, np.int32)  # family 0, second candidate
+        st, ch, info = ref.solve(err, bits, dflt, None, D=100)
+        best = _brute_weighted(err, bits, np.ones(L, np.int64), dflt, 100)
+        got = sum(int(bits[l, ch[l]]) for l in range(L))
+        if info.used_default:
+            assert got == sum(int(bits[l, 1]) for l in range(L))
+        else:
+            assert got == best
