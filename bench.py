@@ -179,13 +179,30 @@ def run_ours(args):
     choice_h = torch.empty(L, dtype=torch.int32).pin_memory()
     l2_flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
-    nccl_id = None
-    if world > 1:
-        obj = [lgreco.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
-    ctx = lgreco.Context(layers, lgreco.QSGD, W.QSGD_BITS, qbucket=128, seed=SEED, rank=rank, world=world,
-                         nccl_id=nccl_id)
+    exchange = "local"
+    ctx = None
+    if world > 1 and os.environ.get("LGRECO_EXCHANGE", "p2p") == "p2p":
+        # the product exchange: K5 stores records straight into the owners' windows over
+        # NVLink (CUDA IPC handles exchanged here), epoch flags instead of collectives
+        try:
+            ctx = lgreco.Context(layers, lgreco.QSGD, W.QSGD_BITS, qbucket=128, seed=SEED, rank=rank, world=world)
+            blobs = [None] * world
+            dist.all_gather_object(blobs, ctx.p2p_export())
+            ctx.p2p_open(blobs)
+            dist.barrier()
+            exchange = "p2p (NVLink peer stores + epoch flags)"
+        except Exception as ex:  # fall back to NCCL (reported in the JSON line)
+            print(f"# p2p exchange unavailable ({ex}); using NCCL", file=sys.stderr)
+            ctx = None
+    if ctx is None:
+        nccl_id = None
+        if world > 1:
+            obj = [lgreco.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            nccl_id = obj[0]
+            exchange = "nccl (grouped send/recv all-to-all + all-gather)"
+        ctx = lgreco.Context(layers, lgreco.QSGD, W.QSGD_BITS, qbucket=128, seed=SEED, rank=rank, world=world,
+                             nccl_id=nccl_id)
 
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
@@ -312,7 +329,8 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded Gaussian + 1% outliers, EF ~ N(0,(0.1s)^2))",
             "config": {"workload": WORKLOAD, "global_batch": None, "parallelism": f"dp{world}",
-                       "l2": "flushed (512 MiB memset) before every timed step", "family": "qsgd"},
+                       "l2": "flushed (512 MiB memset) before every timed step", "family": "qsgd",
+                       "exchange": exchange},
             "dp_solve_ms": round(stage["solve"], 4),
             # the same figure for the per-step path alone (compress + exchange
             # with the plan fixed), which is what runs between replans

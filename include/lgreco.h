@@ -174,7 +174,9 @@ int lgreco_weight_costs(const int64_t* d_bits, const int64_t* d_weight, int32_t 
 int lgreco_layer_norms(lgreco_ctx* ctx, const float* d_g, const float* d_ef, double* d_norm, void* stream);
 
 /* (a7) Plan agreement: broadcast d_choice (L int32) from rank 0.
- * No-op when world == 1. */
+ * No-op when world == 1; NCCL broadcast, or over peer memory for a ctx set up with
+ * lgreco_p2p_open / _set_peers (rank 0 stores its plan into every peer's flag area and
+ * releases an epoch word the others acquire). */
 int lgreco_plan_broadcast(lgreco_ctx* ctx, int32_t* d_choice, void* stream);
 
 /* (a8-a10) Compress with the plan h_choice (HOST, L candidate indices; ignored for
@@ -196,6 +198,26 @@ int lgreco_compress_allreduce(lgreco_ctx* ctx, const int32_t* h_choice, const fl
  * host (stream synchronisation) because the exchange sizes depend on it. */
 int lgreco_compress_allreduce_dev(lgreco_ctx* ctx, const int32_t* d_choice, const float* d_g, float* d_ef,
                                   float* d_out, uint64_t step, void* stream);
+
+/* ---- peer-memory exchange (QSGD, 1 < world <= 8, no NCCL on the data path) ----------
+ * A QSGD ctx created with world > 1 and nccl_unique_id == NULL exchanges through the
+ * peers' device memory (NVLink P2P stores; R13 unchanged: same shards, same sums, same
+ * bytes): K5 stores every stage-1 record straight into its owner's receive window, a
+ * system-scope release of a per-(stage, sender) epoch word tells the owner, the owner
+ * reduces (K8) and stores its stage-2 shard into every peer's stage-2 payload, K9
+ * decodes after the second epoch.  Setup: lgreco_p2p_export (3 CUDA IPC handles, 192
+ * bytes) on every rank, all-gather the blobs over the process group, lgreco_p2p_open
+ * (W x 192 bytes, rank order); or, for ranks simulated in one process,
+ * lgreco_p2p_local + lgreco_p2p_set_peers.  lgreco_compress_allreduce then runs the
+ * three stages (lgreco_p2p_stage 1, 2, 3); every rank must call it the same number of
+ * times (the epoch).  Errors: LGRECO_EINVAL for other families / ctxs without the
+ * buffers, LGRECO_ECUDA when an IPC handle cannot be opened. */
+int lgreco_p2p_local(lgreco_ctx* ctx, void** h_ptrs3 /* out: recv window, stage-2 payload, flags */);
+int lgreco_p2p_export(lgreco_ctx* ctx, void* h_blob /* out: 3 cudaIpcMemHandle_t */);
+int lgreco_p2p_open(lgreco_ctx* ctx, const void* h_blobs /* world x 3 handles, rank order */);
+int lgreco_p2p_set_peers(lgreco_ctx* ctx, void* const* h_recv, void* const* h_stage2, void* const* h_flags);
+int lgreco_p2p_stage(lgreco_ctx* ctx, const int32_t* h_choice, const float* d_g, float* d_ef, float* d_out,
+                     uint64_t step, int32_t stage /* 1, 2, 3 */, void* stream);
 
 /* ---- stage entry points (the steps lgreco_compress_allreduce composes; used by
  * ---- the parity tests to simulate W ranks on one GPU) ------------------------ */

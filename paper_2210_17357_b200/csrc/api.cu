@@ -286,8 +286,19 @@ int lgreco_ctx_create(lgreco_ctx** out, const lgreco_layer* layers, int32_t L, c
     const int s = psgd_init(c, st);
     if (s != LGRECO_OK) return fail(s);
   }
-  if (world > 1) {
-    if (!nccl_unique_id) { lg_set_error("world > 1 needs an ncclUniqueId"); return fail(LGRECO_EINVAL); }
+  if (world > 1 && world <= lg::P2P_MAXW && c->family == LGRECO_QSGD) {
+    const size_t fbytes = sizeof(unsigned) * (3 * lg::P2P_MAXW + (size_t)L);
+    if (cudaMalloc((void**)&c->d_flags, fbytes) != cudaSuccess || cudaMemset(c->d_flags, 0, fbytes) != cudaSuccess ||
+        cudaMalloc((void**)&c->d_p2p, sizeof(lg::P2PDev)) != cudaSuccess) {
+      lg_set_error("p2p buffers");
+      return fail(LGRECO_ENOMEM);
+    }
+  }
+  if (world > 1 && !nccl_unique_id && c->family != LGRECO_QSGD) {
+    lg_set_error("world > 1 needs an ncclUniqueId (the peer-memory exchange is QSGD only)");
+    return fail(LGRECO_EINVAL);
+  }
+  if (world > 1 && nccl_unique_id) {  // (without an id: QSGD over peer memory, lgreco_p2p_*)
     ncclUniqueId id;
     memcpy(&id, nccl_unique_id, sizeof(id));
     ncclResult_t r = ncclCommInitRank(&c->comm, world, id, rank);
@@ -303,6 +314,11 @@ int lgreco_ctx_create(lgreco_ctx** out, const lgreco_layer* layers, int32_t L, c
 
 void lgreco_ctx_destroy(lgreco_ctx* c) {
   if (c) svd_destroy(c);
+  if (c) {
+    for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
+    cudaFree(c->d_flags);
+    cudaFree(c->d_p2p);
+  }
   if (!c) return;
   topk_destroy(c);
   psgd_destroy(c);
@@ -431,6 +447,12 @@ int lgreco_solve(const double* d_err, const int64_t* d_bits, int32_t L, int32_t 
 int lgreco_plan_broadcast(lgreco_ctx* c, int32_t* d_choice, void* stream) {
   if (!c || !d_choice) return LGRECO_EINVAL;
   if (c->world == 1) return LGRECO_OK;
+  if (c->p2p) {  // over peer memory (rank 0 pushes, the others acquire)
+    LG_CUDA(lg::launch_p2p_plan(c->d_p2p, c->d_flags, c->world, c->rank, ++c->plan_epoch, d_choice, c->L,
+                                (cudaStream_t)stream));
+    return LGRECO_OK;
+  }
+  if (!c->comm) { lg_set_error("plan_broadcast: no NCCL communicator and no peers"); return LGRECO_EINVAL; }
   LG_NCCL(ncclBroadcast(d_choice, d_choice, (size_t)c->L, ncclInt32, 0, c->comm, (cudaStream_t)stream));
   return LGRECO_OK;
 }
@@ -510,6 +532,11 @@ int lgreco_compress_allreduce(lgreco_ctx* c, const int32_t* h_choice, const floa
   if (c->family != LGRECO_QSGD) { lg_set_error("family unsupported"); return LGRECO_EUNSUPPORTED; }
   if (c->world == 1)  // stage 2 skipped (R13): fused pack + EF + decode, nothing leaves the GPU
     return lgreco_qsgd_pack(c, h_choice, d_g, d_ef, nullptr, d_out, 0u, step, stream);
+  if (c->p2p) {
+    for (int sg = 1; sg <= 3; ++sg) LG_TRY(lgreco_p2p_stage(c, h_choice, d_g, d_ef, d_out, step, sg, stream));
+    return LGRECO_OK;
+  }
+  if (!c->comm) { lg_set_error("world > 1: neither an NCCL communicator nor peer buffers (lgreco_p2p_open)"); return LGRECO_EINVAL; }
   LG_TRY(lgreco_qsgd_pack(c, h_choice, d_g, d_ef, c->d_pay1, nullptr, (uint32_t)c->rank, step, stream));
   const int W = c->world, me = c->rank;
   const int64_t mine = c->byte_bounds[me + 1] - c->byte_bounds[me];
@@ -531,6 +558,102 @@ int lgreco_compress_allreduce(lgreco_ctx* c, const int32_t* h_choice, const floa
     if (bj > 0) LG_NCCL(ncclRecv(c->d_pay2 + c->byte_bounds[j], (size_t)bj, ncclUint8, j, c->comm, st));
   }
   LG_NCCL(ncclGroupEnd());
+  return lgreco_qsgd_unpack(c, h_choice, c->d_pay2, d_out, stream);
+}
+
+// ---- peer-memory exchange (QSGD, W > 1, no NCCL on the data path) -------------------
+int lgreco_p2p_local(lgreco_ctx* c, void** h_ptrs3) {
+  if (!c || !h_ptrs3 || !c->d_flags || !c->d_recv || !c->d_pay2) { lg_set_error("p2p_local: QSGD ctx with world > 1 only"); return LGRECO_EINVAL; }
+  h_ptrs3[0] = c->d_recv; h_ptrs3[1] = c->d_pay2; h_ptrs3[2] = c->d_flags;
+  return LGRECO_OK;
+}
+
+int lgreco_p2p_set_peers(lgreco_ctx* c, void* const* h_recv, void* const* h_stage2, void* const* h_flags) {
+  if (!c || !h_recv || !h_stage2 || !h_flags || !c->d_p2p || c->world > lg::P2P_MAXW) {
+    lg_set_error("p2p_set_peers: bad argument");
+    return LGRECO_EINVAL;
+  }
+  for (int j = 0; j < c->world; ++j) {
+    c->h_p2p.recv[j] = static_cast<uint8_t*>(h_recv[j]);
+    c->h_p2p.s2[j] = static_cast<uint8_t*>(h_stage2[j]);
+    c->h_p2p.flag[j] = static_cast<unsigned*>(h_flags[j]);
+  }
+  c->h_p2p.W = c->world;
+  c->h_p2p.me = c->rank;
+  // the pointers are needed before the first exchange (plan_broadcast); the shard bounds
+  // are refreshed with every plan
+  LG_CUDA(cudaMemcpy(c->d_p2p, &c->h_p2p, sizeof(lg::P2PDev), cudaMemcpyHostToDevice));
+  c->p2p = true;
+  c->plan_valid = false;  // re-upload the descriptor with the next plan
+  return LGRECO_OK;
+}
+
+int lgreco_p2p_export(lgreco_ctx* c, void* h_blob) {
+  void* p[3];
+  LG_TRY(lgreco_p2p_local(c, p));
+  if (!h_blob) return LGRECO_EINVAL;
+  for (int i = 0; i < 3; ++i)
+    LG_CUDA(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(h_blob) + i, p[i]));
+  return LGRECO_OK;
+}
+
+int lgreco_p2p_open(lgreco_ctx* c, const void* h_blobs) {
+  void* mine[3];
+  LG_TRY(lgreco_p2p_local(c, mine));
+  if (!h_blobs) return LGRECO_EINVAL;
+  void* ptrs[3][lg::P2P_MAXW];
+  const cudaIpcMemHandle_t* hs = reinterpret_cast<const cudaIpcMemHandle_t*>(h_blobs);
+  for (int j = 0; j < c->world; ++j)
+    for (int i = 0; i < 3; ++i) {
+      if (j == c->rank) { ptrs[i][j] = mine[i]; continue; }
+      void* q = nullptr;
+      LG_CUDA(cudaIpcOpenMemHandle(&q, hs[3 * j + i], cudaIpcMemLazyEnablePeerAccess));
+      c->ipc_opened.push_back(q);
+      ptrs[i][j] = q;
+    }
+  return lgreco_p2p_set_peers(c, ptrs[0], ptrs[1], ptrs[2]);
+}
+
+// Stage s of the peer-memory exchange on this rank: 1 = pack + EF with every record
+// stored straight into its owner's window, then signal; 2 = wait for all stage-1 data,
+// owner dequantise-sum-requantise (K8), push the stage-2 shard to every peer, signal;
+// 3 = wait for all stage-2 shards, decode (K9).  lgreco_compress_allreduce runs 1, 2, 3.
+int lgreco_p2p_stage(lgreco_ctx* c, const int32_t* h_choice, const float* d_g, float* d_ef, float* d_out,
+                     uint64_t step, int32_t stage, void* stream) {
+  if (!c || !c->p2p || !h_choice || stage < 1 || stage > 3) { lg_set_error("p2p_stage: bad argument / no peers"); return LGRECO_EINVAL; }
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool fresh = !c->plan_valid;
+  LG_TRY(set_plan(c, h_choice, st));
+  const int W = c->world, me = c->rank;
+  if (fresh || stage == 1) {
+    for (int j = 0; j <= W; ++j) c->h_p2p.bb[j] = c->byte_bounds[j];
+    LG_CUDA(cudaMemcpyAsync(c->d_p2p, &c->h_p2p, sizeof(lg::P2PDev), cudaMemcpyHostToDevice, st));
+  }
+  uint32_t k0, k1;
+  key_of(c, k0, k1);
+  if (stage == 1) {
+    ++c->epoch;
+    LG_TRY(check_align16("p2p_stage", d_g, d_ef, d_out));
+    lg::QPackArgs a{d_g, d_ef, nullptr, nullptr, c->d_layers, c->d_plan, c->d_chunks_all, c->nchunks_all, c->B,
+                    k0, k1, (uint32_t)me, (uint32_t)step, c->d_flag};
+    a.p2p = c->d_p2p;
+    LG_LAUNCH(c, lg::launch_qpack(a, st));
+    LG_CUDA(lg::launch_p2p_signal(c->d_p2p, 0, c->epoch, st));
+    c->launches += 2;
+    return LGRECO_OK;
+  }
+  const int64_t mine = c->byte_bounds[me + 1] - c->byte_bounds[me];
+  if (stage == 2) {
+    LG_CUDA(lg::launch_p2p_wait(c->d_flags, W, me, 0, c->epoch, st));
+    LG_TRY(lgreco_qsgd_reduce(c, h_choice, W, c->rec_bounds[me], c->rec_bounds[me + 1], c->d_recv, c->d_pay2, step,
+                              stream));
+    LG_CUDA(lg::launch_p2p_push(c->d_p2p, c->d_pay2, c->byte_bounds[me], c->byte_bounds[me] + mine, st));
+    LG_CUDA(lg::launch_p2p_signal(c->d_p2p, 1, c->epoch, st));
+    c->launches += 3;
+    return LGRECO_OK;
+  }
+  LG_CUDA(lg::launch_p2p_wait(c->d_flags, W, me, 1, c->epoch, st));
+  c->launches += 1;
   return lgreco_qsgd_unpack(c, h_choice, c->d_pay2, d_out, stream);
 }
 

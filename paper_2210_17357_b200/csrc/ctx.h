@@ -88,6 +88,14 @@ struct lgreco_ctx {
   struct Psgd* ps = nullptr;
   // SVD-profile workspace (svd.cu, created on first use)
   void* svd = nullptr;
+  // peer-memory exchange (QSGD, W > 1): peers' buffers (IPC-opened or given), flags
+  bool p2p = false;
+  unsigned* d_flags = nullptr;          // this rank's flag words [3][W] (stage, sender) + plan [L]
+  lg::P2PDev h_p2p{};                   // host copy (pointers + shard bounds of the plan)
+  lg::P2PDev* d_p2p = nullptr;
+  std::vector<void*> ipc_opened;        // to cudaIpcCloseMemHandle
+  unsigned epoch = 0;
+  unsigned plan_epoch = 0;
 };
 
 // family-specific parts (api_topk.cu, api_psgd.cu)

@@ -39,10 +39,23 @@ struct QProfileArgs {
   unsigned* ldone = nullptr;
 };
 
+// Peer-memory exchange (W <= 8 ranks): device pointers to every rank's stage-1 receive
+// window, stage-2 payload and flag words, and the shard byte bounds of the current plan.
+constexpr int P2P_MAXW = 8;
+struct P2PDev {
+  uint8_t* recv[P2P_MAXW];
+  uint8_t* s2[P2P_MAXW];
+  unsigned* flag[P2P_MAXW];   // flag[j][0..W) stage 1, [W..2W) stage 2, [2W..3W) plan (word =
+                              // sender); the plan itself at words [3*P2P_MAXW, +L)
+  int64_t bb[P2P_MAXW + 1];
+  int W, me;
+};
+
 struct QPackArgs {
   const float* g; float* ef; uint8_t* payload; float* dec;
   const DevLayer* layers; const DevPlan* plan; const ProfChunk* chunks; int nchunks; int B;
   uint32_t k0, k1, rankfield, step; unsigned* flag;
+  const P2PDev* p2p = nullptr;  // non-null: records go straight to their owner's window
 };
 
 struct QUnpackArgs {
@@ -139,6 +152,13 @@ cudaError_t launch_ps_raw_pack(const float* g, float* ef, uint8_t* payload, floa
                                unsigned* flag, cudaStream_t st);
 cudaError_t launch_ps_raw_mean(const uint8_t* gathered, int64_t S, int W, float* out, const RawSeg* segs, int nseg,
                                cudaStream_t st);
+
+// peer-memory exchange helpers (qsgd.cu)
+cudaError_t launch_p2p_signal(const P2PDev* p, int stage, unsigned epoch, cudaStream_t st);
+cudaError_t launch_p2p_wait(const unsigned* my_flags, int W, int me, int stage, unsigned epoch, cudaStream_t st);
+cudaError_t launch_p2p_push(const P2PDev* p, const uint8_t* src, int64_t b0, int64_t b1, cudaStream_t st);
+cudaError_t launch_p2p_plan(const P2PDev* p, const unsigned* my_flags, int W, int me, unsigned epoch, int32_t* choice,
+                            int L, cudaStream_t st);
 
 // Algorithm 1 DP (dp.cu)
 struct SolveArgs {

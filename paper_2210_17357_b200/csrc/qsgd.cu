@@ -763,11 +763,21 @@ __device__ __forceinline__ void pack_bucket_fast(const X4& xs, int b, int64_t gb
   if (dec_out) *reinterpret_cast<float4*>(dec_out + base) = make_float4(dec[0], dec[1], dec[2], dec[3]);
 }
 
+// Stage-1 destination of the payload byte at flat offset b: the local payload, or (peer
+// exchange) the owner's receive window, slot `me` (owner o's window holds W slots of its
+// shard size, R13) -- records never straddle a shard bound.
+__device__ __forceinline__ uint8_t* stage1_dst(uint8_t* payload, const P2PDev* __restrict__ p2p, int64_t b) {
+  if (!p2p) return payload + b;
+  int o = 0;
+  while (o + 1 < p2p->W && b >= p2p->bb[o + 1]) ++o;
+  return p2p->recv[o] + (int64_t)p2p->me * (p2p->bb[o + 1] - p2p->bb[o]) + (b - p2p->bb[o]);
+}
+
 __global__ void __launch_bounds__(QP_THREADS)
 k_qpack(const float* __restrict__ g, float* __restrict__ ef, uint8_t* __restrict__ payload,
         float* __restrict__ dec_out, const DevLayer* __restrict__ layers, const DevPlan* __restrict__ plan,
         const ProfChunk* __restrict__ chunks, int B, uint32_t k0, uint32_t k1, uint32_t rankfield,
-        uint32_t step, unsigned* __restrict__ flag) {
+        uint32_t step, unsigned* __restrict__ flag, const P2PDev* __restrict__ p2p) {
   pdl_wait();  // the plan (k_plan_qsgd_dev) and the EF of the previous step
   const ProfChunk ch = chunks[blockIdx.x];
   const DevLayer ly = layers[ch.layer];
@@ -778,13 +788,13 @@ k_qpack(const float* __restrict__ g, float* __restrict__ ef, uint8_t* __restrict
   float bad = 0.f;
   if (pl.bits == 0) {
     // lossless layer: raw x records, e' = 0 (R14, R15)
-    float* raw = payload ? reinterpret_cast<float*>(payload + pl.pay_off) : nullptr;
+    const bool rawp = payload != nullptr || p2p != nullptr;
     const int64_t i_beg = ch.first * (int64_t)B;
     const int64_t i_end = min(ly.numel, (ch.first + ch.nbk) * (int64_t)B);
     for (int64_t i = i_beg + threadIdx.x; i < i_end; i += blockDim.x) {
       const float x = canon(__ldg(g + ly.offset + i), ef ? ef[ly.offset + i] : 0.f);
       bad = __fadd_rn(bad, __fmul_rn(x, 0.f));
-      if (raw) raw[i] = x;
+      if (rawp) *reinterpret_cast<float*>(stage1_dst(payload, p2p, pl.pay_off + 4 * i)) = x;
       if (dec_out) dec_out[ly.offset + i] = x;
       if (ef) ef[ly.offset + i] = 0.f;
     }
@@ -813,7 +823,9 @@ k_qpack(const float* __restrict__ g, float* __restrict__ ef, uint8_t* __restrict
         const int64_t jb = jb0 + u * QP_WARPS;
         const int64_t base = ly.offset + jb * 128 + 4 * lane;
         pack_bucket_fast(xs[u], b, ly.bucket0 + jb, rankfield, step, k0, k1, lane,
-                         payload ? payload + pl.pay_off + jb * (int64_t)pl.rec_bytes : nullptr, ef, dec_out,
+                         (payload || p2p) ? stage1_dst(payload, p2p, pl.pay_off + jb * (int64_t)pl.rec_bytes)
+                                          : nullptr,
+                         ef, dec_out,
                          base, bad);
       }
     }
@@ -822,7 +834,7 @@ k_qpack(const float* __restrict__ g, float* __restrict__ ef, uint8_t* __restrict
     const int64_t jb = ch.first + bi;
     const int64_t gb = ly.bucket0 + jb;
     const int64_t e0 = jb * (int64_t)B;
-    uint8_t* rec = payload ? payload + pl.pay_off + jb * (int64_t)pl.rec_bytes : nullptr;
+    uint8_t* rec = (payload || p2p) ? stage1_dst(payload, p2p, pl.pay_off + jb * (int64_t)pl.rec_bytes) : nullptr;
     if (fast_layer && e0 + 128 <= ly.numel) {
       const int64_t base = ly.offset + e0 + 4 * lane;
       const X4 xs = canon4(ld4(g + base), ef ? ld4(ef + base) : make_float4(0.f, 0.f, 0.f, 0.f));
@@ -1090,7 +1102,7 @@ cudaError_t launch_qprofile(const QProfileArgs& a, cudaStream_t st) {
 cudaError_t launch_qpack(const QPackArgs& a, cudaStream_t st) {
   if (a.nchunks == 0) return cudaSuccess;
   const cudaError_t e = launch_pdl(k_qpack, dim3(a.nchunks), dim3(QP_THREADS), 0, st, a.g, a.ef, a.payload, a.dec,
-                                   a.layers, a.plan, a.chunks, a.B, a.k0, a.k1, a.rankfield, a.step, a.flag);
+                                   a.layers, a.plan, a.chunks, a.B, a.k0, a.k1, a.rankfield, a.step, a.flag, a.p2p);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
@@ -1109,6 +1121,100 @@ cudaError_t launch_qreduce(const QReduceArgs& a, cudaStream_t st) {
   const size_t smem = sizeof(int64_t) * (a.L + 1);
   k_qreduce<<<grid, QP_THREADS, smem, st>>>(a.recv, a.shard_bytes, a.byte0, a.stage2, a.layers, a.plan, a.bucket0,
                                             a.L, a.r0, a.r1, a.B, a.W, a.k0, a.k1, a.step, rpw);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Peer-memory exchange (W > 1 without NCCL): K5 stores every stage-1 record straight
+// into its owner's receive window (stage1_dst), k_p2p_signal publishes "my stage-s data
+// for you is complete" as the epoch in word (s, me) of every peer's flags (system-scope
+// fence, then a release store), k_p2p_wait spins (acquire) until all W senders'
+// words hold the epoch, k_p2p_push copies this rank's stage-2 shard into every peer's
+// stage-2 payload (16-byte stores over NVLink).  Kernel boundaries order the rest.
+// ---------------------------------------------------------------------------
+__global__ void k_p2p_signal(const P2PDev* __restrict__ p, int stage, unsigned epoch) {
+  const int o = threadIdx.x;
+  __threadfence_system();
+  if (o < p->W) {
+    unsigned* f = p->flag[o] + stage * p->W + p->me;
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(epoch) : "memory");
+  }
+}
+
+__global__ void k_p2p_wait(const unsigned* __restrict__ flags, int W, int me, int stage, unsigned epoch) {
+  const int j = threadIdx.x;
+  if (j < W) {
+    const unsigned* f = flags + stage * W + j;
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+    } while (v != epoch);
+  }
+  __syncthreads();
+  __threadfence_system();
+}
+
+__global__ void k_p2p_push(const P2PDev* __restrict__ p, const uint8_t* __restrict__ src, int64_t b0, int64_t b1) {
+  // bytes [b0, b1): unaligned head and tail byte by byte, the 16-byte-aligned body as
+  // uint4 (the peer buffers have the local buffer's alignment at every offset)
+  const int W = p->W, me = p->me;
+  const int64_t a0 = min(b1, (b0 + 15) & ~(int64_t)15);
+  const int64_t n16 = (b1 - a0) / 16;
+  const int64_t a1 = a0 + 16 * n16;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nth = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = tid; i < n16; i += nth) {
+    const uint4 v = *reinterpret_cast<const uint4*>(src + a0 + 16 * i);
+    for (int o = 0; o < W; ++o)
+      if (o != me) *reinterpret_cast<uint4*>(p->s2[o] + a0 + 16 * i) = v;
+  }
+  for (int64_t i = tid; i < (a0 - b0) + (b1 - a1); i += nth) {
+    const int64_t k = (i < a0 - b0) ? b0 + i : a1 + (i - (a0 - b0));
+    for (int o = 0; o < W; ++o)
+      if (o != me) p->s2[o][k] = src[k];
+  }
+}
+
+// Plan agreement over peer memory (R21): rank 0 stores its plan into word 3*8 + l of
+// every peer's flag area, then releases epoch word (2, 0); the others acquire it and
+// copy the plan out.
+__global__ void k_p2p_plan_push(const P2PDev* __restrict__ p, const int32_t* __restrict__ choice, int L) {
+  for (int l = blockIdx.x * blockDim.x + threadIdx.x; l < L; l += gridDim.x * blockDim.x)
+    for (int o = 1; o < p->W; ++o) p->flag[o][3 * P2P_MAXW + l] = (unsigned)choice[l];
+}
+__global__ void k_p2p_plan_pull(const unsigned* __restrict__ my_flags, int W, unsigned epoch, int32_t* choice, int L) {
+  if (threadIdx.x == 0) {
+    const unsigned* f = my_flags + 2 * W;  // word (2, sender 0)
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+    } while (v != epoch);
+  }
+  __syncthreads();
+  for (int l = threadIdx.x; l < L; l += blockDim.x) choice[l] = (int32_t)my_flags[3 * P2P_MAXW + l];
+}
+cudaError_t launch_p2p_plan(const P2PDev* p, const unsigned* my_flags, int W, int me, unsigned epoch, int32_t* choice,
+                            int L, cudaStream_t st) {
+  if (me == 0) {
+    k_p2p_plan_push<<<std::max(1, std::min(64, (L + 255) / 256)), 256, 0, st>>>(p, choice, L);
+    return launch_p2p_signal(p, 2, epoch, st);
+  }
+  k_p2p_plan_pull<<<1, 256, 0, st>>>(my_flags, W, epoch, choice, L);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_p2p_signal(const P2PDev* p, int stage, unsigned epoch, cudaStream_t st) {
+  k_p2p_signal<<<1, 32, 0, st>>>(p, stage, epoch);
+  return cudaGetLastError();
+}
+cudaError_t launch_p2p_wait(const unsigned* my_flags, int W, int me, int stage, unsigned epoch, cudaStream_t st) {
+  k_p2p_wait<<<1, 32, 0, st>>>(my_flags, W, me, stage, epoch);
+  return cudaGetLastError();
+}
+cudaError_t launch_p2p_push(const P2PDev* p, const uint8_t* src, int64_t b0, int64_t b1, cudaStream_t st) {
+  if (b1 <= b0) return cudaSuccess;
+  const int64_t n16 = (b1 - b0 + 15) / 16;
+  k_p2p_push<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((n16 + 255) / 256, 1184)), 256, 0, st>>>(p, src, b0,
+                                                                                                        b1);
   return cudaGetLastError();
 }
 

@@ -61,6 +61,11 @@ _SIGS = {
     "lgreco_weight_costs": (C.c_int, [_VP, _VP, _I32, _I32, _VP, _VP]),
     "lgreco_psgd_profile_svd": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP]),
     "lgreco_layer_norms": (C.c_int, [_VP, _VP, _VP, _VP, _VP]),
+    "lgreco_p2p_local": (C.c_int, [_VP, _VP]),
+    "lgreco_p2p_export": (C.c_int, [_VP, _VP]),
+    "lgreco_p2p_open": (C.c_int, [_VP, _VP]),
+    "lgreco_p2p_set_peers": (C.c_int, [_VP, _VP, _VP, _VP]),
+    "lgreco_p2p_stage": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _U64, _I32, _VP]),
     "lgreco_plan_broadcast": (C.c_int, [_VP, _VP, _VP]),
     "lgreco_compress_allreduce": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _U64, _VP]),
     "lgreco_compress_allreduce_dev": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _U64, _VP]),
@@ -175,6 +180,33 @@ class Context:
     def layer_norms(self, g, ef, norm, stream=None):
         """Per-layer L2 norms of x = g (+ ef) into the L fp64 device tensor `norm`."""
         _check(lib().lgreco_layer_norms(self.h, _ptr(g), _ptr(ef), _ptr(norm), _stream(stream)), "layer_norms")
+
+    # ---- peer-memory exchange (QSGD, world > 1 without NCCL) -------------------------
+    def p2p_local(self):
+        arr = (C.c_void_p * 3)()
+        _check(lib().lgreco_p2p_local(self.h, C.cast(arr, C.c_void_p)), "p2p_local")
+        return [int(v or 0) for v in arr]
+
+    def p2p_set_peers(self, recv, stage2, flags):
+        W = len(recv)
+        mk = lambda v: (C.c_void_p * W)(*[C.c_void_p(x) for x in v])  # noqa: E731
+        a, b, c = mk(recv), mk(stage2), mk(flags)
+        _check(lib().lgreco_p2p_set_peers(self.h, C.cast(a, C.c_void_p), C.cast(b, C.c_void_p), C.cast(c, C.c_void_p)),
+               "p2p_set_peers")
+
+    def p2p_export(self) -> bytes:
+        buf = C.create_string_buffer(192)
+        _check(lib().lgreco_p2p_export(self.h, C.cast(buf, C.c_void_p)), "p2p_export")
+        return buf.raw
+
+    def p2p_open(self, blobs):
+        raw = b"".join(blobs)
+        buf = C.create_string_buffer(raw, len(raw))
+        _check(lib().lgreco_p2p_open(self.h, C.cast(buf, C.c_void_p)), "p2p_open")
+
+    def p2p_stage(self, choice, g, ef, out, step, stage, stream=None):
+        _check(lib().lgreco_p2p_stage(self.h, _i32(choice), _ptr(g), _ptr(ef), _ptr(out), step, stage,
+                                      _stream(stream)), "p2p_stage")
 
     def compress_allreduce(self, choice, g, ef, out, step, stream=None):
         _check(lib().lgreco_compress_allreduce(self.h, _i32(choice), _ptr(g), _ptr(ef), _ptr(out), step,

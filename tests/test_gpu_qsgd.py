@@ -424,3 +424,51 @@ def test_hybrid_qsgd_topk_plan(lg, ref):
     assert fams <= {0, 1}
     cq.close()
     ct.close()
+
+
+@pytest.mark.parametrize("Wn", [2, 3, 4, 8])
+def test_p2p_exchange_simulated_ranks(lg, ref, Wn):
+    """Peer-memory exchange (no NCCL): W rank contexts in one process, each given the
+    others' device buffers (lgreco_p2p_set_peers); stage 1 (pack straight into the
+    owners' windows + epoch release) on every rank, then stage 2 (acquire, owner reduce,
+    push to every peer), then stage 3 (acquire, decode) -- two steps with a plan change:
+    outputs, EF and every rank's stage-2 payload bit-identical to the W-rank oracle."""
+    layers = _edge_layers()
+    seed, B = 4242, 128
+    ctxs = [lg.Context(layers, lg.QSGD, BITS, qbucket=B, seed=seed, rank=w, world=Wn) for w in range(Wn)]
+    loc = [c.p2p_local() for c in ctxs]
+    for c in ctxs:
+        c.p2p_set_peers([p[0] for p in loc], [p[1] for p in loc], [p[2] for p in loc])
+    gs, es = [], []
+    for w in range(Wn):
+        g, e = _edge_data(layers, 300 + w)
+        gs.append(g)
+        es.append(e)
+    eds = [_dev(e) for e in es]
+    es_cur = [e.copy() for e in es]
+    for step, cs in ((5, Wn), (6, Wn + 7)):
+        choice = _choice_for(layers, np.random.default_rng(cs))
+        lbits = [BITS[c] if l.compress else 0 for c, l in zip(choice, layers)]
+        out_ref, es_ref, _, p2_ref = ref.qsgd_allreduce(layers, lbits, gs, es_cur, B=B, seed=seed, step=step)
+        outs = [torch.empty(len(gs[0]), dtype=torch.float32, device="cuda") for _ in range(Wn)]
+        gds = [_dev(g) for g in gs]
+        for stage in (1, 2, 3):
+            for w in range(Wn):
+                ctxs[w].p2p_stage(choice, gds[w], eds[w], outs[w], step, stage)
+        torch.cuda.synchronize()
+        for w in range(Wn):
+            assert np.array_equal(outs[w].cpu().numpy().view(np.uint32), out_ref.view(np.uint32)), (step, w)
+            assert np.array_equal(eds[w].cpu().numpy().view(np.uint32), es_ref[w].view(np.uint32)), (step, w)
+        es_cur = [e.copy() for e in es_ref]
+    # plan agreement over peer memory: every rank proposes its own plan, rank 0's wins
+    props = [torch.tensor(_choice_for(layers, np.random.default_rng(50 + w)), dtype=torch.int32, device="cuda")
+             for w in range(Wn)]
+    want = props[0].clone()
+    for w in range(Wn):  # rank 0 pushes first (one process: launch order = dependency order)
+        ctxs[w].plan_broadcast(props[w])
+    torch.cuda.synchronize()
+    for w in range(Wn):
+        assert torch.equal(props[w], want)
+    for c in ctxs:
+        c.check()
+        c.close()
