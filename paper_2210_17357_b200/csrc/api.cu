@@ -240,7 +240,7 @@ int lgreco_ctx_create(lgreco_ctx** out, const lgreco_layer* layers, int32_t L, c
   LG_ALLOC(c->d_qseg, sizeof(lg::QSeg) * std::max(1, c->nqseg));
   LG_ALLOC(c->d_lqseg0, sizeof(int32_t) * (L + 1));
   LG_ALLOC(c->d_segsum, sizeof(double) * std::max(1, c->nqseg) * c->K);
-  LG_ALLOC(c->d_ldone, sizeof(unsigned) * L);  // K1 part counters + done counter, 256 B apart
+  LG_ALLOC(c->d_ldone, sizeof(unsigned) * L);
   LG_ALLOC(c->d_flag, sizeof(unsigned));
   LG_ALLOC(c->d_plan, sizeof(lg::DevPlan) * L);
   if (world > 1 && c->family == LGRECO_QSGD) {
@@ -677,6 +677,36 @@ int lgreco_compress_allreduce_dev(lgreco_ctx* c, const int32_t* d_choice, const 
   if (c->world == 1 && c->family == LGRECO_TOPK) {
     c->launches += 0;
     return topk_compress_dev(c, d_choice, d_g, d_ef, d_out, st);
+  }
+  if (c->p2p && c->family == LGRECO_QSGD) {
+    // W > 1 over peer memory with the plan laid out on the device: no host round trip
+    LG_CUDA(lg::launch_plan_qsgd_layout(d_choice, c->d_params, c->K, c->d_layers, c->d_bucket0, c->L, c->R, c->B,
+                                        c->d_plan, c->d_p2p, c->d_flag, st));
+    c->plan_valid = false;  // d_plan / d_p2p now hold a device-chosen plan
+    uint32_t k0, k1;
+    key_of(c, k0, k1);
+    const int W = c->world, me = c->rank;
+    ++c->epoch;
+    lg::QPackArgs a{d_g, d_ef, nullptr, nullptr, c->d_layers, c->d_plan, c->d_chunks_all, c->nchunks_all, c->B,
+                    k0, k1, (uint32_t)me, (uint32_t)step, c->d_flag};
+    a.p2p = c->d_p2p;
+    LG_LAUNCH(c, lg::launch_qpack(a, st));
+    LG_CUDA(lg::launch_p2p_signal(c->d_p2p, 0, c->epoch, st));
+    LG_CUDA(lg::launch_p2p_wait(c->d_flags, W, me, 0, c->epoch, st));
+    int nsm = 148, dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    lg::QReduceArgs r{c->d_recv, 0, 0, c->d_pay2, c->d_layers, c->d_plan, c->d_bucket0, c->L, 0, 0, c->B, W, k0, k1,
+                      (uint32_t)step};
+    r.p2p = c->d_p2p;
+    r.grid = nsm * 4;
+    LG_LAUNCH(c, lg::launch_qreduce(r, st));
+    LG_CUDA(lg::launch_p2p_push(c->d_p2p, c->d_pay2, 0, -1, st));
+    LG_CUDA(lg::launch_p2p_signal(c->d_p2p, 1, c->epoch, st));
+    LG_CUDA(lg::launch_p2p_wait(c->d_flags, W, me, 1, c->epoch, st));
+    lg::QUnpackArgs u{c->d_pay2, d_out, c->d_layers, c->d_plan, c->d_chunks_all, c->nchunks_all, c->B};
+    LG_LAUNCH(c, lg::launch_qunpack(u, st));
+    c->launches += 9;
+    return LGRECO_OK;
   }
   // the exchange needs host-side shard sizes: bring the plan to the host
   LG_CUDA(cudaMemcpyAsync(c->h_choice_pinned, d_choice, sizeof(int32_t) * c->L, cudaMemcpyDeviceToHost, st));

@@ -47,7 +47,8 @@ struct P2PDev {
   uint8_t* s2[P2P_MAXW];
   unsigned* flag[P2P_MAXW];   // flag[j][0..W) stage 1, [W..2W) stage 2, [2W..3W) plan (word =
                               // sender); the plan itself at words [3*P2P_MAXW, +L)
-  int64_t bb[P2P_MAXW + 1];
+  int64_t bb[P2P_MAXW + 1];   // shard byte bounds of the current plan (R13)
+  int64_t rb[P2P_MAXW + 1];   // shard record bounds
   int W, me;
 };
 
@@ -67,6 +68,8 @@ struct QReduceArgs {
   const uint8_t* recv; int64_t shard_bytes; int64_t byte0; uint8_t* stage2;
   const DevLayer* layers; const DevPlan* plan; const int64_t* bucket0; int L;
   int64_t r0, r1; int B; int W; uint32_t k0, k1, step;
+  const P2PDev* p2p = nullptr;  // non-null: this rank's shard (r0, r1, byte0, bytes) read on the device
+  int grid = 0;                 // with p2p: fixed grid (the shard size is not known on the host)
 };
 
 cudaError_t launch_qprofile(const QProfileArgs& a, cudaStream_t st);
@@ -159,6 +162,11 @@ cudaError_t launch_p2p_wait(const unsigned* my_flags, int W, int me, int stage, 
 cudaError_t launch_p2p_push(const P2PDev* p, const uint8_t* src, int64_t b0, int64_t b1, cudaStream_t st);
 cudaError_t launch_p2p_plan(const P2PDev* p, const unsigned* my_flags, int W, int me, unsigned epoch, int32_t* choice,
                             int L, cudaStream_t st);
+// device-side layout of a plan (W > 1 without a host round trip): DevPlan per layer
+// (payload offsets, R7) and the shard bounds (R13) into p->bb / p->rb
+cudaError_t launch_plan_qsgd_layout(const int32_t* choice, const int32_t* params, int K, const DevLayer* layers,
+                                    const int64_t* bucket0, int L, int64_t R, int B, DevPlan* plan, P2PDev* p,
+                                    unsigned* flag, cudaStream_t st);
 
 // Algorithm 1 DP (dp.cu)
 struct SolveArgs {

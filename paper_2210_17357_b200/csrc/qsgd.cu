@@ -922,14 +922,21 @@ k_qunpack(const uint8_t* __restrict__ payload, float* __restrict__ out, const De
 __global__ void __launch_bounds__(QP_THREADS)
 k_qreduce(const uint8_t* __restrict__ recv, int64_t shard_bytes, int64_t byte0, uint8_t* __restrict__ stage2,
           const DevLayer* __restrict__ layers, const DevPlan* __restrict__ plan, const int64_t* __restrict__ bucket0,
-          int L, int64_t r0, int64_t r1, int B, int W, uint32_t k0, uint32_t k1, uint32_t step, int rec_per_warp) {
+          int L, int64_t r0, int64_t r1, int B, int W, uint32_t k0, uint32_t k1, uint32_t step, int rec_per_warp,
+          const P2PDev* __restrict__ p2p) {
   extern __shared__ int64_t sb0[];
   for (int i = threadIdx.x; i <= L; i += blockDim.x) sb0[i] = bucket0[i];
+  if (p2p) {  // this rank's shard from the device-side layout
+    const int me = p2p->me;
+    r0 = p2p->rb[me]; r1 = p2p->rb[me + 1];
+    byte0 = p2p->bb[me]; shard_bytes = p2p->bb[me + 1] - p2p->bb[me];
+  }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int M = B >> 7;
   const float invW = __fdiv_rn(1.0f, (float)W);
-  const int64_t wbase = r0 + ((int64_t)blockIdx.x * QP_WARPS + warp) * rec_per_warp;
+  for (int64_t wbase = r0 + ((int64_t)blockIdx.x * QP_WARPS + warp) * rec_per_warp; wbase < r1;
+       wbase += (int64_t)gridDim.x * QP_WARPS * rec_per_warp)
   for (int ri = 0; ri < rec_per_warp; ++ri) {
     const int64_t gb = wbase + ri;
     if (gb >= r1) break;
@@ -1116,11 +1123,11 @@ cudaError_t launch_qunpack(const QUnpackArgs& a, cudaStream_t st) {
 cudaError_t launch_qreduce(const QReduceArgs& a, cudaStream_t st) {
   const int rpw = 2;
   const int64_t n = a.r1 - a.r0;
-  const int grid = (int)((n + (int64_t)QP_WARPS * rpw - 1) / ((int64_t)QP_WARPS * rpw));
+  const int grid = a.p2p ? a.grid : (int)((n + (int64_t)QP_WARPS * rpw - 1) / ((int64_t)QP_WARPS * rpw));
   if (grid == 0) return cudaSuccess;
   const size_t smem = sizeof(int64_t) * (a.L + 1);
   k_qreduce<<<grid, QP_THREADS, smem, st>>>(a.recv, a.shard_bytes, a.byte0, a.stage2, a.layers, a.plan, a.bucket0,
-                                            a.L, a.r0, a.r1, a.B, a.W, a.k0, a.k1, a.step, rpw);
+                                            a.L, a.r0, a.r1, a.B, a.W, a.k0, a.k1, a.step, rpw, a.p2p);
   return cudaGetLastError();
 }
 
@@ -1155,9 +1162,11 @@ __global__ void k_p2p_wait(const unsigned* __restrict__ flags, int W, int me, in
 }
 
 __global__ void k_p2p_push(const P2PDev* __restrict__ p, const uint8_t* __restrict__ src, int64_t b0, int64_t b1) {
-  // bytes [b0, b1): unaligned head and tail byte by byte, the 16-byte-aligned body as
-  // uint4 (the peer buffers have the local buffer's alignment at every offset)
+  // bytes [b0, b1) (b1 < 0: this rank's shard from the device-side layout): unaligned
+  // head and tail byte by byte, the 16-byte-aligned body as uint4 (the peer buffers have
+  // the local buffer's alignment at every offset)
   const int W = p->W, me = p->me;
+  if (b1 < 0) { b0 = p->bb[me]; b1 = p->bb[me + 1]; }
   const int64_t a0 = min(b1, (b0 + 15) & ~(int64_t)15);
   const int64_t n16 = (b1 - a0) / 16;
   const int64_t a1 = a0 + 16 * n16;
@@ -1202,6 +1211,77 @@ cudaError_t launch_p2p_plan(const P2PDev* p, const unsigned* my_flags, int W, in
   return cudaGetLastError();
 }
 
+// Device-side plan layout for W > 1 (R7, R13; the host's qsgd_layout + shard_bounds):
+// one CTA; per-layer sizes, a sequential 16-byte-padded prefix by thread 0 (L is a few
+// hundred), then thread j < W binary-searches the first record whose offset reaches
+// floor(j S / W).
+__global__ void k_plan_qsgd_layout(const int32_t* __restrict__ choice, const int32_t* __restrict__ params, int K,
+                                   const DevLayer* __restrict__ layers, const int64_t* __restrict__ bucket0, int L,
+                                   int64_t R, int B, DevPlan* __restrict__ plan, P2PDev* __restrict__ p,
+                                   unsigned* __restrict__ flag) {
+  pdl_wait();  // the solve's choice
+  __shared__ int64_t S_sh;
+  for (int l = threadIdx.x; l < L; l += blockDim.x) {
+    int bits = 0;
+    if (layers[l].compress) {
+      int c = choice[l];
+      if (c < 0 || c >= K) { atomicOr(flag, 2u); c = 0; }
+      bits = params[c];
+    }
+    const int32_t rb = bits > 0 ? 16 * bits * (B / 128) + 8 : 4 * B;
+    plan[l] = DevPlan{0, bits, rb};
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t off = 0;
+    for (int l = 0; l < L; ++l) {
+      const int64_t nb = bucket0[l + 1] - bucket0[l];
+      plan[l].pay_off = off;
+      off += plan[l].bits > 0 ? nb * (int64_t)plan[l].rec_bytes : 4 * layers[l].numel;
+      off = (off + 15) & ~(int64_t)15;
+    }
+    S_sh = off;
+  }
+  __syncthreads();
+  const int64_t S = S_sh;
+  const int W = p->W;
+  auto rec_off = [&](int64_t r) -> int64_t {
+    if (r >= R) return S;
+    int lo = 0, hi = L - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (bucket0[mid] <= r) lo = mid; else hi = mid - 1;
+    }
+    const DevPlan pl = plan[lo];
+    const int64_t jb = r - bucket0[lo];
+    return pl.pay_off + (pl.bits > 0 ? jb * (int64_t)pl.rec_bytes : jb * 4 * (int64_t)B);
+  };
+  const int j = threadIdx.x;
+  if (j <= W) {
+    int64_t rj = 0, bj = 0;
+    if (j == W) { rj = R; bj = S; }
+    else if (j > 0) {
+      const int64_t target = (int64_t)(((__int128)j * S) / W);
+      int64_t lo = 0, hi = R;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) / 2;
+        if (rec_off(mid) >= target) hi = mid; else lo = mid + 1;
+      }
+      rj = lo;
+      bj = rec_off(lo);
+    }
+    p->rb[j] = rj;
+    p->bb[j] = bj;
+  }
+}
+
+cudaError_t launch_plan_qsgd_layout(const int32_t* choice, const int32_t* params, int K, const DevLayer* layers,
+                                    const int64_t* bucket0, int L, int64_t R, int B, DevPlan* plan, P2PDev* p,
+                                    unsigned* flag, cudaStream_t st) {
+  return launch_pdl(k_plan_qsgd_layout, dim3(1), dim3(256), 0, st, choice, params, K, layers, bucket0, L, R, B, plan, p,
+                    flag);
+}
+
 cudaError_t launch_p2p_signal(const P2PDev* p, int stage, unsigned epoch, cudaStream_t st) {
   k_p2p_signal<<<1, 32, 0, st>>>(p, stage, epoch);
   return cudaGetLastError();
@@ -1211,8 +1291,8 @@ cudaError_t launch_p2p_wait(const unsigned* my_flags, int W, int me, int stage, 
   return cudaGetLastError();
 }
 cudaError_t launch_p2p_push(const P2PDev* p, const uint8_t* src, int64_t b0, int64_t b1, cudaStream_t st) {
-  if (b1 <= b0) return cudaSuccess;
-  const int64_t n16 = (b1 - b0 + 15) / 16;
+  if (b1 >= 0 && b1 <= b0) return cudaSuccess;
+  const int64_t n16 = b1 >= 0 ? (b1 - b0 + 15) / 16 : (int64_t)1184 * 256;  // device bounds: full grid
   k_p2p_push<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((n16 + 255) / 256, 1184)), 256, 0, st>>>(p, src, b0,
                                                                                                         b1);
   return cudaGetLastError();

@@ -472,3 +472,35 @@ def test_p2p_exchange_simulated_ranks(lg, ref, Wn):
     for c in ctxs:
         c.check()
         c.close()
+
+
+@pytest.mark.parametrize("Wn", [2, 4])
+def test_p2p_device_plan_simulated_ranks(lg, ref, Wn):
+    """The W > 1 peer-memory step with the plan laid out on the device (no host round
+    trip): W rank contexts on W streams of the one GPU, each running the whole step
+    (layout, pack into the owners' windows, epoch waits, reduce, push, decode) via
+    compress_allreduce_dev -- outputs and EF bit-identical to the W-rank oracle."""
+    layers = _edge_layers()
+    seed, B, step = 77, 128, 9
+    ctxs = [lg.Context(layers, lg.QSGD, BITS, qbucket=B, seed=seed, rank=w, world=Wn) for w in range(Wn)]
+    loc = [c.p2p_local() for c in ctxs]
+    for c in ctxs:
+        c.p2p_set_peers([p[0] for p in loc], [p[1] for p in loc], [p[2] for p in loc])
+    gs, es = zip(*[_edge_data(layers, 500 + w) for w in range(Wn)])
+    choice = _choice_for(layers, np.random.default_rng(Wn + 40))
+    lbits = [BITS[c] if l.compress else 0 for c, l in zip(choice, layers)]
+    out_ref, es_ref, _, _ = ref.qsgd_allreduce(layers, lbits, list(gs), list(es), B=B, seed=seed, step=step)
+    streams = [torch.cuda.Stream() for _ in range(Wn)]
+    gds, eds = [_dev(g) for g in gs], [_dev(e) for e in es]
+    outs = [torch.empty(len(gs[0]), dtype=torch.float32, device="cuda") for _ in range(Wn)]
+    dch = [torch.tensor(choice, dtype=torch.int32, device="cuda") for _ in range(Wn)]
+    torch.cuda.synchronize()
+    for w in range(Wn):
+        ctxs[w].compress_allreduce_dev(dch[w], gds[w], eds[w], outs[w], step, stream=streams[w])
+    torch.cuda.synchronize()
+    for w in range(Wn):
+        assert np.array_equal(outs[w].cpu().numpy().view(np.uint32), out_ref.view(np.uint32)), w
+        assert np.array_equal(eds[w].cpu().numpy().view(np.uint32), es_ref[w].view(np.uint32)), w
+    for c in ctxs:
+        c.check()
+        c.close()
