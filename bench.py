@@ -155,10 +155,18 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE {world}"
+    # (diagnostics: LG_BENCH_ONE_DEVICE=1 puts every rank on device 0 with a gloo group,
+    # to exercise the N > 1 code path -- the peer-memory exchange over CUDA IPC -- on a
+    # one-GPU box; the driver's runs never set it)
+    one_dev = os.environ.get("LG_BENCH_ONE_DEVICE") == "1"
+    local = 0 if one_dev else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if one_dev:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     stream = torch.cuda.current_stream()
 
     layers = W.config_layers("C4")
