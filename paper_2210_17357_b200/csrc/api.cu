@@ -645,9 +645,10 @@ int lgreco_p2p_stage(lgreco_ctx* c, const int32_t* h_choice, const float* d_g, f
   const int64_t mine = c->byte_bounds[me + 1] - c->byte_bounds[me];
   if (stage == 2) {
     LG_CUDA(lg::launch_p2p_wait(c->d_flags, W, me, 0, c->epoch, st));
-    LG_TRY(lgreco_qsgd_reduce(c, h_choice, W, c->rec_bounds[me], c->rec_bounds[me + 1], c->d_recv, c->d_pay2, step,
-                              stream));
-    LG_CUDA(lg::launch_p2p_push(c->d_p2p, c->d_pay2, c->byte_bounds[me], c->byte_bounds[me] + mine, st));
+    lg::QReduceArgs r{c->d_recv, mine, c->byte_bounds[me], c->d_pay2, c->d_layers, c->d_plan, c->d_bucket0, c->L,
+                      c->rec_bounds[me], c->rec_bounds[me + 1], c->B, W, k0, k1, (uint32_t)step};
+    r.p2p = c->d_p2p;  // stage-2 records stored into every peer's payload as they are produced
+    LG_LAUNCH(c, lg::launch_qreduce(r, st));
     LG_CUDA(lg::launch_p2p_signal(c->d_p2p, 1, c->epoch, st));
     c->launches += 3;
     return LGRECO_OK;
@@ -698,14 +699,14 @@ int lgreco_compress_allreduce_dev(lgreco_ctx* c, const int32_t* d_choice, const 
     lg::QReduceArgs r{c->d_recv, 0, 0, c->d_pay2, c->d_layers, c->d_plan, c->d_bucket0, c->L, 0, 0, c->B, W, k0, k1,
                       (uint32_t)step};
     r.p2p = c->d_p2p;
+    r.device_bounds = 1;
     r.grid = nsm * 4;
-    LG_LAUNCH(c, lg::launch_qreduce(r, st));
-    LG_CUDA(lg::launch_p2p_push(c->d_p2p, c->d_pay2, 0, -1, st));
+    LG_LAUNCH(c, lg::launch_qreduce(r, st));  // stores its stage-2 records into every peer's payload too
     LG_CUDA(lg::launch_p2p_signal(c->d_p2p, 1, c->epoch, st));
     LG_CUDA(lg::launch_p2p_wait(c->d_flags, W, me, 1, c->epoch, st));
     lg::QUnpackArgs u{c->d_pay2, d_out, c->d_layers, c->d_plan, c->d_chunks_all, c->nchunks_all, c->B};
     LG_LAUNCH(c, lg::launch_qunpack(u, st));
-    c->launches += 9;
+    c->launches += 8;
     return LGRECO_OK;
   }
   // the exchange needs host-side shard sizes: bring the plan to the host

@@ -68,8 +68,9 @@ struct QReduceArgs {
   const uint8_t* recv; int64_t shard_bytes; int64_t byte0; uint8_t* stage2;
   const DevLayer* layers; const DevPlan* plan; const int64_t* bucket0; int L;
   int64_t r0, r1; int B; int W; uint32_t k0, k1, step;
-  const P2PDev* p2p = nullptr;  // non-null: this rank's shard (r0, r1, byte0, bytes) read on the device
-  int grid = 0;                 // with p2p: fixed grid (the shard size is not known on the host)
+  const P2PDev* p2p = nullptr;  // non-null: stage-2 records also stored into every peer's payload
+  int device_bounds = 0;        // 1: this rank's shard (r0, r1, byte0, bytes) read from p2p on the device
+  int grid = 0;                 // with device_bounds: fixed grid (the shard size is not known on the host)
 };
 
 cudaError_t launch_qprofile(const QProfileArgs& a, cudaStream_t st);

@@ -919,18 +919,44 @@ k_qunpack(const uint8_t* __restrict__ payload, float* __restrict__ out, const De
 // ---------------------------------------------------------------------------
 // K8 owner reduce: records [r0, r1); recv = W x shard bytes (rank-major)
 // ---------------------------------------------------------------------------
+// Stage-2 store: the local payload and, over peer memory, every peer's stage-2 payload
+// at the same offset (the owner's shard reaches all ranks as it is produced).
+template <typename T>
+__device__ __forceinline__ void st2(uint8_t* stage2, const P2PDev* __restrict__ p2p, int64_t off, T v) {
+  *reinterpret_cast<T*>(stage2 + off) = v;
+  if (p2p)
+    for (int o = 0; o < p2p->W; ++o)
+      if (o != p2p->me) *reinterpret_cast<T*>(p2p->s2[o] + off) = v;
+}
+
+// pack_planes into the stage-2 payload (and the peers') at byte offset roff
+__device__ __forceinline__ void pack_planes2(uint8_t* stage2, const P2PDev* __restrict__ p2p, int64_t roff, int t,
+                                             int b, const uint32_t* q, int lane) {
+  for (int p = 0; p < b; ++p) {
+    const uint32_t w0 = __ballot_sync(LG_FULL, (q[0] >> p) & 1u);
+    const uint32_t w1 = __ballot_sync(LG_FULL, (q[1] >> p) & 1u);
+    const uint32_t w2 = __ballot_sync(LG_FULL, (q[2] >> p) & 1u);
+    const uint32_t w3 = __ballot_sync(LG_FULL, (q[3] >> p) & 1u);
+    if (lane == 0) {  // (records are 8-byte aligned: two 8-byte stores)
+      st2(stage2, p2p, roff + 4 * (int64_t)(t * b + p) * 4, make_uint2(w0, w1));
+      st2(stage2, p2p, roff + 4 * (int64_t)(t * b + p) * 4 + 8, make_uint2(w2, w3));
+    }
+  }
+}
+
 __global__ void __launch_bounds__(QP_THREADS)
 k_qreduce(const uint8_t* __restrict__ recv, int64_t shard_bytes, int64_t byte0, uint8_t* __restrict__ stage2,
           const DevLayer* __restrict__ layers, const DevPlan* __restrict__ plan, const int64_t* __restrict__ bucket0,
           int L, int64_t r0, int64_t r1, int B, int W, uint32_t k0, uint32_t k1, uint32_t step, int rec_per_warp,
-          const P2PDev* __restrict__ p2p) {
+          const P2PDev* __restrict__ p2p, int device_bounds) {
   extern __shared__ int64_t sb0[];
   for (int i = threadIdx.x; i <= L; i += blockDim.x) sb0[i] = bucket0[i];
-  if (p2p) {  // this rank's shard from the device-side layout
+  if (p2p && device_bounds) {  // this rank's shard from the device-side layout
     const int me = p2p->me;
     r0 = p2p->rb[me]; r1 = p2p->rb[me + 1];
     byte0 = p2p->bb[me]; shard_bytes = p2p->bb[me + 1] - p2p->bb[me];
   }
+  const P2PDev* p2p_out = p2p;  // stage-2 records also stored into every peer's payload
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int M = B >> 7;
@@ -957,7 +983,7 @@ k_qreduce(const uint8_t* __restrict__ recv, int64_t shard_bytes, int64_t byte0, 
             const float v = __ldg(reinterpret_cast<const float*>(recv + w * shard_bytes + bo));
             a = (w == 0) ? v : __fadd_rn(a, v);
           }
-          *reinterpret_cast<float*>(stage2 + roff + 4 * (128 * t + 4 * lane + s)) = __fmul_rn(a, invW);
+          st2(stage2, p2p_out, roff + 4 * (128 * t + 4 * lane + s), __fmul_rn(a, invW));
         }
       }
       continue;
@@ -1002,9 +1028,9 @@ k_qreduce(const uint8_t* __restrict__ recv, int64_t shard_bytes, int64_t byte0, 
           const float qf = qcode(__fsub_rn(x, mn), inv, u[s], s_b);
           q[s] = (s < nv) ? (uint32_t)qf : 0u;
         }
-        pack_planes(reinterpret_cast<uint32_t*>(stage2 + roff), t, b, q, lane);
+        pack_planes2(stage2, p2p_out, roff, t, b, q, lane);
       }
-      if (pass == 1 && lane == 0) *reinterpret_cast<float2*>(stage2 + roff + 16 * b * M) = make_float2(mn, unit);
+      if (pass == 1 && lane == 0) st2(stage2, p2p_out, roff + 16 * b * M, make_float2(mn, unit));
     }
   }
 }
@@ -1123,11 +1149,12 @@ cudaError_t launch_qunpack(const QUnpackArgs& a, cudaStream_t st) {
 cudaError_t launch_qreduce(const QReduceArgs& a, cudaStream_t st) {
   const int rpw = 2;
   const int64_t n = a.r1 - a.r0;
-  const int grid = a.p2p ? a.grid : (int)((n + (int64_t)QP_WARPS * rpw - 1) / ((int64_t)QP_WARPS * rpw));
+  const int grid = a.device_bounds ? a.grid : (int)((n + (int64_t)QP_WARPS * rpw - 1) / ((int64_t)QP_WARPS * rpw));
   if (grid == 0) return cudaSuccess;
   const size_t smem = sizeof(int64_t) * (a.L + 1);
   k_qreduce<<<grid, QP_THREADS, smem, st>>>(a.recv, a.shard_bytes, a.byte0, a.stage2, a.layers, a.plan, a.bucket0,
-                                            a.L, a.r0, a.r1, a.B, a.W, a.k0, a.k1, a.step, rpw, a.p2p);
+                                            a.L, a.r0, a.r1, a.B, a.W, a.k0, a.k1, a.step, rpw, a.p2p,
+                                            a.device_bounds);
   return cudaGetLastError();
 }
 
