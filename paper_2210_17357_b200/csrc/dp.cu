@@ -751,7 +751,7 @@ __device__ __forceinline__ void cl_st(uint32_t addr, uint64_t v) {
   asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
 }
 
-constexpr int CL_MAX = 8;  // CTAs per cluster (portable maximum)
+constexpr int CL_MAX = 16;  // CTAs per cluster (16: non-portable size; 8 is the portable maximum)
 
 template <int CPT>
 __device__ __forceinline__ void pd_store(uint8_t* dst, const uint32_t* w) {
@@ -1461,9 +1461,8 @@ size_t solve_workspace_bytes(int L, int K, int D) {
 // 64-bit full-length rows within 200 KB of shared memory, and an 8-CTA cluster of that
 // size can be resident.  Returns cudaErrorNotSupported (nothing launched) otherwise.
 static cudaError_t launch_solve_cluster(const SolveArgs& a, uint8_t* pd, int32_t* act, int32_t* wdisc, uint64_t* wadd,
-                                        int32_t* wmaxd, cudaStream_t st) {
+                                        int32_t* wmaxd, int NC, cudaStream_t st) {
   if (a.K < 1 || a.K > 256) return cudaErrorNotSupported;
-  int NC = CL_MAX;
   if (const char* env = getenv("LGRECO_DP_NC")) NC = std::max(2, std::min(CL_MAX, atoi(env)));
   int cpt = 2;
   while (cpt <= 8 && (int64_t)NC * DP_THREADS * cpt < (int64_t)a.D + 1) cpt *= 2;
@@ -1512,6 +1511,10 @@ static cudaError_t launch_solve_cluster(const SolveArgs& a, uint8_t* pd, int32_t
     static int nfmax = 0;
     int fi = -1;
     for (int i = 0; i < nfmax; ++i) if (fmax[i].fn == (const void*)fn) fi = i;
+    if (NC > 8 && cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+      cudaGetLastError();
+      return cudaErrorNotSupported;
+    }
     if (fi < 0 || fmax[fi].smem < smem) {
       e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) { cudaGetLastError(); return cudaErrorNotSupported; }
@@ -1563,7 +1566,9 @@ cudaError_t launch_solve(const SolveArgs& a, void* ws, cudaStream_t st) {
   int32_t* wmaxd = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(wadd) +
                                               align_up(sizeof(uint64_t) * (size_t)a.L * a.K * CL_MAX));
   if (!(a.flags & LGRECO_SOLVE_SINGLE_CTA)) {
-    const cudaError_t ce = launch_solve_cluster(a, pd, act, wdisc, wadd, wmaxd, st);
+    // 16 SMs when a 16-CTA cluster of this size is schedulable, else 8
+    cudaError_t ce = launch_solve_cluster(a, pd, act, wdisc, wadd, wmaxd, 16, st);
+    if (ce == cudaErrorNotSupported) ce = launch_solve_cluster(a, pd, act, wdisc, wadd, wmaxd, 8, st);
     if (ce != cudaErrorNotSupported) return ce;
     if (getenv("LGRECO_DEBUG")) fprintf(stderr, "lgreco: cluster solve not used (L=%d K=%d D=%d)\n", a.L, a.K, a.D);
   }
