@@ -751,6 +751,9 @@ __device__ __forceinline__ void cl_st(uint32_t addr, uint64_t v) {
   asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
 }
 
+#ifndef QP_DP_CPT0
+#define QP_DP_CPT0 2  // smallest cells-per-thread of the cluster solve (more warps below that)
+#endif
 constexpr int CL_MAX = 16;  // CTAs per cluster (16: non-portable size; 8 is the portable maximum)
 
 template <int CPT>
@@ -1464,9 +1467,10 @@ static cudaError_t launch_solve_cluster(const SolveArgs& a, uint8_t* pd, int32_t
                                         int32_t* wmaxd, int NC, cudaStream_t st) {
   if (a.K < 1 || a.K > 256) return cudaErrorNotSupported;
   if (const char* env = getenv("LGRECO_DP_NC")) NC = std::max(2, std::min(CL_MAX, atoi(env)));
-  int cpt = 2;
+  int cpt = 1;
+  if (const char* env = getenv("LGRECO_DP_CPT")) cpt = std::max(1, std::min(8, atoi(env)));
+  else cpt = QP_DP_CPT0;
   while (cpt <= 8 && (int64_t)NC * DP_THREADS * cpt < (int64_t)a.D + 1) cpt *= 2;
-  if (const char* env = getenv("LGRECO_DP_CPT")) cpt = std::max(cpt, atoi(env));
   if (cpt > 8) return cudaErrorNotSupported;
   // (KT == 0 stages one candidate per thread: at least K threads)
   const int nw = std::max((int)(((int64_t)a.D + 1 + NC * 32 * cpt - 1) / (NC * 32 * cpt)), (a.K + 31) / 32);
@@ -1489,7 +1493,7 @@ static cudaError_t launch_solve_cluster(const SolveArgs& a, uint8_t* pd, int32_t
              lgreco_solve_info*, uint8_t*, int32_t*, int32_t*, uint64_t*, int32_t*) = nullptr;
 #define LG_CL(C, KT) if (cpt == C && kt == KT) fn = k_solve_cl<C, KT>;
 #define LG_CL_K(C) LG_CL(C, 4) LG_CL(C, 5) LG_CL(C, 7) LG_CL(C, 8) LG_CL(C, 16) LG_CL(C, 0)
-  LG_CL_K(2) LG_CL_K(4) LG_CL_K(8)
+  LG_CL_K(1) LG_CL_K(2) LG_CL_K(4) LG_CL_K(8)
 #undef LG_CL_K
 #undef LG_CL
   if (!fn) return cudaErrorNotSupported;
