@@ -209,8 +209,10 @@ int lgreco_compress_allreduce_dev(lgreco_ctx* ctx, const int32_t* d_choice, cons
  * bytes) on every rank, all-gather the blobs over the process group, lgreco_p2p_open
  * (W x 192 bytes, rank order); or, for ranks simulated in one process,
  * lgreco_p2p_local + lgreco_p2p_set_peers.  lgreco_compress_allreduce then runs the
- * three stages (lgreco_p2p_stage 1, 2, 3); every rank must call it the same number of
- * times (the epoch).  Errors: LGRECO_EINVAL for other families / ctxs without the
+ * three stages (lgreco_p2p_stage 1, 2, 3) -- or, from lgreco_compress_allreduce_dev,
+ * the whole step with the plan laid out on the device (no host synchronisation); every
+ * rank must call it the same number of times (the epoch) with the same plan (use
+ * lgreco_plan_broadcast).  Errors: LGRECO_EINVAL for other families / ctxs without the
  * buffers, LGRECO_ECUDA when an IPC handle cannot be opened. */
 int lgreco_p2p_local(lgreco_ctx* ctx, void** h_ptrs3 /* out: recv window, stage-2 payload, flags */);
 int lgreco_p2p_export(lgreco_ctx* ctx, void* h_blob /* out: 3 cudaIpcMemHandle_t */);
