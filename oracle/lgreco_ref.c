@@ -130,13 +130,15 @@ int ref_quantize_bucket(const float* x, int32_t nvalid, int32_t bits, const floa
         } else {
             for (int i = 0; i < nvalid; i++) {
                 float t = x[i] - mn;
-                float v = t * inv;
-                float fl = floorf(v);
-                float f = v - fl;
-                float qq = fl + ((u[i] < f) ? 1.0f : 0.0f);
-                if (qq > s) qq = s;
+                /* v = t * inv taken exactly: the product of two floats has at most
+                 * 48 significant bits, so the double product is exact (R6). */
+                double v = (double)t * (double)inv;
+                double fl = floor(v);
+                double f = v - fl; /* exact: v and fl share the exponent range */
+                double qq = fl + (((double)u[i] < f) ? 1.0 : 0.0);
+                if (qq > (double)s) qq = (double)s;
                 q[i] = (uint32_t)qq;
-                dec[i] = fmaf(qq, unit, mn);
+                dec[i] = fmaf((float)qq, unit, mn);
             }
         }
     }

@@ -102,13 +102,14 @@ __device__ __forceinline__ void qparams(float mn, float mx, float s, float& inv,
   if (!isfinite(inv)) inv = 0.f;
 }
 
-// Stochastic rounding of t = x - mn (R6): q = min(floor(v) + (u < frac(v)), s).
+// Stochastic rounding of t = x - mn (R6): q = min(floor(v) + [u < frac(v)], s) with
+// v = t·inv exact.  r = t·inv - u is formed exactly inside one FFMA and rounded up once:
+// for r in (n-1, n], RU(r) stays in (n-1, n] (every integer below 2^24 is a float), so
+// ceil(RU(r)) = ceil(r) = floor(v) + [u < frac(v)] bit for bit (u = frac(v) -> floor(v)).
+// r in (-1, 0] gives q = -0: (uint32_t) and fmaf(q, unit, mn) treat it as +0 (mn != -0,
+// x is canonical).
 __device__ __forceinline__ float qcode(float t, float inv, float u, float s) {
-  const float v = __fmul_rn(t, inv);
-  const float fl = floor_pos(v);
-  const float f = __fsub_rn(v, fl);
-  const float q = __fadd_rn(fl, (u < f) ? 1.0f : 0.0f);
-  return fminf(q, s);
+  return fminf(ceilf(__fmaf_ru(t, inv, -u)), s);
 }
 
 __device__ __forceinline__ void uniforms4(uint32_t c0, uint32_t rankfield, uint32_t step, uint32_t stream,
@@ -146,14 +147,15 @@ __device__ __forceinline__ void prof_candidates(const float* x, float mn, const 
 }
 
 // Fast-path candidate loop (full aligned buckets of 128, 8 lanes per bucket, 16
-// elements per lane).  q is the pinned code (R6) computed as
-//   q = min(ceil(RU(v - u)), s),  v = RN(t * inv),
-// which equals min(floor(v) + [u < v - floor(v)], s) exactly: for real r = v - u in
-// (n-1, n], RU(r) lies in (n-1, n] because every integer below 2^24 is a float, so
-// ceil(RU(r)) = ceil(r) = floor(v) + [u < frac(v)] (u = frac(v) gives floor(v)).  The
-// ceil is RU(w + (2^23 + 1)) - (2^23 + 1), exact for w in (-1, 2^23 - 1).  v - u is
-// formed as one FFMA.RU of the integer word (w >> 8) with -2^-24 (the product is
-// exact).  dec = fmaf(q, unit, mn) and d = x - dec are the pinned decode, so the SSE is
+// elements per lane).  q is the pinned code (R6) computed as in qcode:
+//   q = min(ceil(RU(t * inv - u)), s)   (t * inv - u exact inside one FFMA.RU),
+// which equals min(floor(v) + [u < v - floor(v)], s) for the exact v = t * inv: for
+// real r = v - u in (n-1, n], RU(r) lies in (n-1, n] because every integer below 2^24
+// is a float, so ceil(RU(r)) = ceil(r) = floor(v) + [u < frac(v)] (u = frac(v) gives
+// floor(v)).  The ceil is FRND.CEIL on the conversion pipe, or RU(w + (2^23 + 1)) -
+// (2^23 + 1) on the FMA pipe (exact for w in (-1, 2^23 - 1)).  -u = (w >> 8) * -2^-24 is
+// one exact FMUL per element shared by all candidates.  dec = fmaf(q, unit, mn) and
+// d = x - dec are the pinned decode, so the SSE is
 // that of the realised reconstruction.
 template <int KT, bool SCALED>
 __device__ __forceinline__ void prof_cand16(const float* x, float mn, uint32_t c0, uint32_t rankfield, uint32_t step,
@@ -165,15 +167,18 @@ __device__ __forceinline__ void prof_cand16(const float* x, float mn, uint32_t c
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const U4 r = philox10(c0 + 8 * i, rankfield, step, 0u, k0, k1);
-    const float uw[4] = {__uint2float_rn(r.x >> 8), __uint2float_rn(r.y >> 8), __uint2float_rn(r.z >> 8),
-                         __uint2float_rn(r.w >> 8)};
+    constexpr float NEG_2M24 = -5.9604644775390625e-08f;  // -u = (w >> 8) * -2^-24, exact
+    const float nu[4] = {__fmul_rn(__uint2float_rn(r.x >> 8), NEG_2M24), __fmul_rn(__uint2float_rn(r.y >> 8), NEG_2M24),
+                         __fmul_rn(__uint2float_rn(r.z >> 8), NEG_2M24), __fmul_rn(__uint2float_rn(r.w >> 8), NEG_2M24)};
+    float t[4];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) t[s] = __fsub_rn(x[4 * i + s], mn);
 #pragma unroll
     for (int j = 0; j < KT; ++j) {
 #pragma unroll
       for (int s = 0; s < 4; ++s) {
         const float xv = x[4 * i + s];
-        const float v = __fmul_rn(__fsub_rn(xv, mn), inv[j]);
-        const float w = __fmaf_ru(uw[s], -5.9604644775390625e-08f, v);
+        const float w = __fmaf_ru(t[s], inv[j], nu[s]);  // RU(t·inv - u), one rounding (qcode)
         // ceil(w): the last QP_XU_CEIL candidates use FRND.CEIL on the conversion
         // pipe (idle otherwise), the others the two-FADD magic on the FMA pipe (the
         // kernel's bottleneck): both are exact; -0 from FRND changes no error

@@ -125,11 +125,54 @@ def test_unbiased_and_closed_form_mse(ref, bits):
     # closed form of the per-element MSE
     s = 2 ** bits - 1
     inv = np.float32(s) / np.float32(x.max() - x.min())
-    v = (x - x.min()).astype(np.float32) * inv
-    f = v.astype(np.float64) - np.floor(v)
+    v = (x - x.min()).astype(np.float32).astype(np.float64) * np.float64(inv)  # exact (R6)
+    f = v - np.floor(v)
     mse_cf = (unit ** 2 * f * (1 - f)).sum()
     mse_mc = ((decs - x) ** 2).sum(1).mean()
     assert abs(mse_mc - mse_cf) / mse_cf < 0.03
+
+
+def _rn32(r):
+    """Round a Fraction to the nearest float32, ties to even (no double rounding)."""
+    from fractions import Fraction as F
+    c = np.float32(float(r))
+    cands = [np.nextafter(c, np.float32(-np.inf)), c, np.nextafter(c, np.float32(np.inf))]
+    best = min(abs(F(float(v)) - r) for v in cands)
+    ties = [v for v in cands if abs(F(float(v)) - r) == best]
+    return ties[0] if len(ties) == 1 else [v for v in ties if (v.view(np.uint32) & 1) == 0][0]
+
+
+def test_code_is_exact_rational_rounding(ref):
+    """R6 against exact rational arithmetic (fractions.Fraction, not the oracle's
+    doubles): q = min(floor(v) + [u < frac(v)], s) with v = fl(x - mn) * fl(s / range)
+    taken exactly, dec = fl(fma(q, unit, mn)).  Inputs are chosen so that u lands on,
+    just below and just above frac(v), and v exceeds s at the maximum."""
+    from fractions import Fraction as F
+    rng = np.random.default_rng(11)
+    for trial in range(40):
+        bits = int(rng.integers(1, 9))
+        s = 2 ** bits - 1
+        x = rng.standard_normal(128).astype(np.float32) * np.float32(10.0 ** rng.integers(-6, 4))
+        mn, mx = np.float32(x.min()), np.float32(x.max())
+        rngv = np.float32(mx - mn)
+        inv = np.float32(np.float32(s) / rngv)
+        t = (x - mn).astype(np.float32)
+        vq = [F(float(ti)) * F(float(inv)) for ti in t]
+        fr = [v - (v.numerator // v.denominator) for v in vq]
+        u = rng.random(128).astype(np.float32)
+        for i in range(0, 128, 3):  # u at frac(v) rounded to float and its neighbours
+            k = (i // 3) % 3
+            ui = np.float32(float(fr[i]))
+            u[i] = [ui, np.nextafter(ui, np.float32(0)), np.nextafter(ui, np.float32(1))][k]
+            u[i] = min(u[i], np.float32(1 - 2 ** -24))
+        st, q, dec, mn_o, unit = ref.quantize_bucket(x, bits, u)
+        assert st == 0 and mn_o == mn
+        for i in range(128):
+            fl = vq[i].numerator // vq[i].denominator
+            qe = min(fl + (1 if F(float(u[i])) < fr[i] else 0), s)
+            assert q[i] == qe, (trial, i, bits)
+            de = _rn32(F(qe) * F(float(unit)) + F(float(mn)))  # one rounding of the exact fma
+            assert dec[i] == de
 
 
 def test_pow2_scale_invariance(ref):
