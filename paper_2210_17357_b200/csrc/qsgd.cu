@@ -371,6 +371,23 @@ __device__ __forceinline__ void bar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ void bar_expect_tx_a(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_wait_a(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred done;\n\t"
+      "QWA_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n\t"
+      "@!done bra QWA_%=;\n\t}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_a(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                    sm_addr(dst)),
@@ -402,7 +419,7 @@ k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const QIn
   // exhausted.  Grabs are split: lane 0 issues the atomic, the broadcast (which waits
   // for it) happens one quad later, so the atomic's latency hides behind a quad.
   const int gw = blockIdx.x * QP_WARPS + warp;
-  int part = gw % QP_NPART, tried = 0;
+  int part = gw % QP_NPART;
   auto plo = [&](int p) -> int { return (int)(((int64_t)nqc * p) / QP_NPART); };
   auto grab_issue = [&]() -> unsigned {
     unsigned v = 0;
@@ -411,9 +428,16 @@ k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const QIn
   };
   auto resolve = [&](unsigned v) -> int {
     int q = plo(part) + (int)__shfl_sync(LG_FULL, v, 0);
-    while (q >= plo(part + 1)) {  // part exhausted: next part (synchronously; rare)
-      if (++tried >= QP_NPART) return nqc;
-      part = (part + 1) % QP_NPART;
+    while (q >= plo(part + 1)) {
+      // part exhausted: lanes 0..15 read the 16 counters at once (one L2 round trip
+      // instead of one synchronous atomic per part) and the warp moves to the next part
+      // in rotation order that still has quads; none left -> done
+      bool left = false;
+      if (lane < QP_NPART) left = plo(lane) + (int)__ldcg(&ticket[lane * 64]) < plo(lane + 1);
+      const unsigned m = __ballot_sync(LG_FULL, left) & ((1u << QP_NPART) - 1u);
+      if (!m) return nqc;
+      const unsigned rot = ((m >> (part + 1)) | (m << (QP_NPART - 1 - part))) & ((1u << QP_NPART) - 1u);
+      part = (part + __ffs(rot)) % QP_NPART;
       q = plo(part) + (int)__shfl_sync(LG_FULL, grab_issue(), 0);
     }
     return q;
@@ -435,6 +459,8 @@ k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const QIn
   __syncwarp();
   const bool pal = ptr_aligned != 0;
   const uint32_t tx = e ? 4096u : 2048u;
+  const uint32_t a_bar = sm_addr(&bars[warp][0]);                      // stage b: + 8 b
+  const uint32_t a_stage = sm_addr(qsm + (size_t)warp * 2 * 4096);     // stage b: + 4096 b
   float gs = 1.f, gs2 = 1.f;  // s of candidates l8 and l8 + 8 (select chain: no local copy of cs)
 #pragma unroll
   for (int j = 0; j < KT; ++j) {
@@ -446,9 +472,9 @@ k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const QIn
     if (!(pal && (in.elem0 & 3) == 0 && in.nvalid == 512)) return false;
     if (lane == 0) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier generic reads of the stage
-      bar_expect_tx(&bars[warp][b], tx);
-      bulk_g2s(stage_g(b), g + in.elem0, 2048u, &bars[warp][b]);
-      if (e) bulk_g2s(stage_g(b) + 512, e + in.elem0, 2048u, &bars[warp][b]);
+      bar_expect_tx_a(a_bar + 8 * b, tx);
+      bulk_g2s_a(a_stage + 4096 * b, g + in.elem0, 2048u, a_bar + 8 * b);
+      if (e) bulk_g2s_a(a_stage + 4096 * b + 2048, e + in.elem0, 2048u, a_bar + 8 * b);
     }
     return true;
   };
@@ -478,7 +504,7 @@ k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const QIn
       const bool valid = grp * 128 < ic.nvalid;
       float x[16];
       if (cur_regular) {
-        bar_wait(&bars[warp][b], (phase >> b) & 1u);
+        bar_wait_a(a_bar + 8 * b, (phase >> b) & 1u);
         phase ^= 1u << b;
         const float* sg = stage_g(b) + grp * 128 + 4 * l8;
         const float* se = sg + 512;
@@ -555,36 +581,36 @@ k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const QIn
       float a2[KT];
       if (__any_sync(LG_FULL, small)) prof_cand16<KT, true>(x, mn, c0, rankfield, step, k0, k1, inv, unit, cs, S, a2);
       else prof_cand16<KT, false>(x, mn, c0, rankfield, step, k0, k1, inv, unit, cs, 1.f, a2);
-      if (valid) {
+      if (KT <= 8) {
+        // quad row, fixed order: transpose-reduce the 8 lanes of each bucket in fp32
+        // (after the xor-4/2/1 halvings lane l8 holds candidate l8's bucket SSE, from
+        // 128 fp32 squares), then x 2^-2k and the 4 buckets in fp64 (xor 8, 16)
+        float v8[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v8[j] = (j < KT) ? a2[j] : 0.f;
+#pragma unroll
+        for (int h = 4; h >= 1; h >>= 1) {
+          const bool up = (lane & h) != 0;
+#pragma unroll
+          for (int i = 0; i < h; ++i) {
+            const float send = up ? v8[i] : v8[i + h];
+            const float keep = up ? v8[i + h] : v8[i];
+            v8[i] = __fadd_rn(keep, __shfl_xor_sync(LG_FULL, send, h));
+          }
+        }
+        double t = valid ? __dmul_rn((double)v8[0], S2inv) : 0.0;
+        t = __dadd_rn(t, __shfl_xor_sync(LG_FULL, t, 8));
+        t = __dadd_rn(t, __shfl_xor_sync(LG_FULL, t, 16));
+        if (lane < K) partial[(int64_t)c * K + lane] = t;
+      } else if (valid) {
 #pragma unroll
         for (int j = 0; j < KT; ++j) acc[j] = __dadd_rn(acc[j], __dmul_rn((double)a2[j], S2inv));
       }
       inflight = next_inflight;
       b ^= 1;
     }
-    // chunk done: fixed-order warp reduction into its slot
-    if (KT <= 8) {
-      // transpose-reduce: after the xor-16/8/4 halvings lane L holds value 4*bit4 +
-      // 2*bit3 + bit2 of L summed over its 8-lane class, xor-2/1 finish the sum
-      double v8[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) v8[j] = (j < KT) ? acc[j] : 0.0;
-#pragma unroll
-      for (int h = 4; h >= 1; h >>= 1) {
-        const int o = 4 * h;  // xor 16, 8, 4
-        const bool up = (lane & o) != 0;
-#pragma unroll
-        for (int i = 0; i < h; ++i) {
-          const double send = up ? v8[i] : v8[i + h];
-          const double keep = up ? v8[i + h] : v8[i];
-          v8[i] = __dadd_rn(keep, __shfl_xor_sync(LG_FULL, send, o));
-        }
-      }
-      double t = __dadd_rn(v8[0], __shfl_xor_sync(LG_FULL, v8[0], 2));
-      t = __dadd_rn(t, __shfl_xor_sync(LG_FULL, t, 1));
-      const int j = lane >> 2;
-      if ((lane & 3) == 0 && j < K) partial[(int64_t)c * K + j] = t;
-    } else {
+    // chunk done (KT > 8): fixed-order warp reduction into its slot
+    if (KT > 8) {
 #pragma unroll
       for (int j = 0; j < KT; ++j) {
         if (j < K) {
