@@ -447,7 +447,25 @@ k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const QIn
       for (int p2 = 0; p2 <= QP_NPART; ++p2) atomicExch(&ticket[p2 * 64], 0u);
     }
   };
-  auto load_info = [&](int ci) -> QInfo { return (ci < nqc) ? qinfo[ci] : QInfo{0, 0u, 0}; };
+  // Quad descriptors travel through a 3-slot shared ring per warp (c, nA, nB), filled by
+  // lane 0 with cp.async (one commit group per descriptor), so no register holds a
+  // descriptor load in flight across the compute (that pushed K1 past its register
+  // budget: a spill store that waited on the load every quad).
+  __shared__ __align__(16) QInfo qis[QP_WARPS][3];
+  auto info_async = [&](int ci, int slot) {
+    if (lane == 0) {
+      if (ci < nqc)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(sm_addr(&qis[warp][slot])), "l"(qinfo + ci)
+                     : "memory");
+      else
+        qis[warp][slot] = QInfo{0, 0u, 0};
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+  };
+  auto info_wait1 = [&]() {  // all but the newest descriptor landed
+    if (lane == 0) asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncwarp();
+  };
   pdl_wait();  // g / e (and the ticket reset) of the preceding kernels
   int c = resolve(grab_issue());
   if (c >= nqc) { finish(); return; }
@@ -483,7 +501,13 @@ k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const QIn
   bool failed = nA >= nqc;
   int nB = nqc;
   if (!failed) { nB = resolve(grab_issue()); failed = nB >= nqc; }
-  QInfo ic = qinfo[c], ia = load_info(nA), ibq = load_info(nB);
+  int r = 0;  // ring slot of c; nA at r+1, nB at r+2 (mod 3)
+  info_async(c, 0);
+  info_async(nA, 1);
+  info_async(nB, 2);
+  if (lane == 0) asm volatile("cp.async.wait_group 2;" ::: "memory");
+  __syncwarp();
+  QInfo ic = qis[warp][0];
   uint32_t phase = 0u;  // bit b: parity of stage b's next completion
   int b = 0;
   bool inflight = issue(ic, 0);
@@ -499,8 +523,9 @@ k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const QIn
       const bool cur_regular = inflight;
       // prefetch quad nA into the other stage (its previous contents were consumed in
       // the previous iteration; __syncwarp orders those reads before the copy)
-      __syncwarp();
-      const bool next_inflight = (nA < nqc) ? issue(ia, b ^ 1) : false;
+      info_wait1();  // nA's descriptor (and c's) landed; also orders the stage reads
+      const int ra = (r == 2) ? 0 : r + 1;
+      const bool next_inflight = (nA < nqc) ? issue(qis[warp][ra], b ^ 1) : false;
       const bool valid = grp * 128 < ic.nvalid;
       float x[16];
       if (cur_regular) {
@@ -622,10 +647,14 @@ k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const QIn
 #pragma unroll
     for (int j = 0; j < KT; ++j) acc[j] = 0.0;
     if (nA >= nqc) break;
-    c = nA; ic = ia;
-    nA = nB; ia = ibq;
-    if (pend) { nB = resolve(raw); failed = nB >= nqc; ibq = load_info(nB); }
+    c = nA;
+    nA = nB;
+    const int r_old = r;  // c's slot, read (ic) before the shuffles above: free
+    r = (r == 2) ? 0 : r + 1;
+    ic = qis[warp][r];    // landed: waited for at the top of this iteration
+    if (pend) { nB = resolve(raw); failed = nB >= nqc; }
     else nB = nqc;
+    info_async(nB, r_old);
   }
   finish();
 }
