@@ -215,18 +215,22 @@ def run_ours(args):
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
     def step(s, marks=None, gin=None, gout=None):
+        """One step; marks = [begin, end] (headline pass: nothing recorded between the
+        kernels, so the library's PDL chaining is undisturbed) or [begin, after profile,
+        after solve, end] (stage pass)."""
         gin = g if gin is None else gin
         gout = out if gout is None else gout
+        staged = marks is not None and len(marks) == 4
         if marks: marks[0].record(stream)
         ctx.profile(gin, ef, s, err, bits)
-        if marks: marks[1].record(stream)
+        if staged: marks[1].record(stream)
         lgreco.solve(err, bits, dflt, comp, D=D_BINS, choice=choice_d, info=info_d, workspace=ws)
         ctx.plan_broadcast(choice_d)
-        if marks: marks[2].record(stream)
+        if staged: marks[2].record(stream)
         # plan consumed on the device at W = 1 (no host round trip); copied to the host
         # inside the library when the exchange needs the shard sizes (W > 1)
         ctx.compress_allreduce_dev(choice_d, gin, ef, gout, s)
-        if marks: marks[3].record(stream)
+        if marks: marks[-1].record(stream)
 
     for s in range(args.warmup):
         step(s)
@@ -235,9 +239,8 @@ def run_ours(args):
 
     clocks = ClockSampler(local)
     times = {"step": [], "profile": [], "solve": [], "compress_allreduce": []}
+    # ---- headline pass: K steps, events only at each step's begin and end
     launches0 = ctx.launches()
-    ctx.timing(True)  # CUDA events around K1 (the dominant kernel) on the launch stream
-    ctx.kernel_ms()   # (clears nothing recorded yet; keeps the hook's state explicit)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -246,23 +249,36 @@ def run_ours(args):
     all_marks = []
     for s in range(args.steps):
         l2_flush.zero_()  # flush L2 between timed steps (outside the timed events)
-        marks = [ev() for _ in range(4)]
+        marks = [ev() for _ in range(2)]
         step(args.warmup + s, marks)  # enqueued without host synchronisation (W = 1)
         all_marks.append(marks)
     torch.cuda.synchronize()
     for marks in all_marks:
-        times["step"].append(marks[0].elapsed_time(marks[3]))
-        times["profile"].append(marks[0].elapsed_time(marks[1]))
-        times["solve"].append(marks[1].elapsed_time(marks[2]))
-        times["compress_allreduce"].append(marks[2].elapsed_time(marks[3]))
+        times["step"].append(marks[0].elapsed_time(marks[1]))
     if world > 1:
         dist.barrier()
     wall = time.perf_counter() - t_wall0
+    launches = ctx.launches() - launches0 + args.steps  # + one solve kernel per step
+    # ---- stage pass (same K steps, not the headline): events between the stages and
+    # around K1 (the dominant kernel, `ctx.timing`) for the breakdown and the roofline
+    ctx.timing(True)
+    ctx.kernel_ms()
+    torch.cuda.synchronize()
+    all_marks = []
+    for s in range(args.steps):
+        l2_flush.zero_()
+        marks = [ev() for _ in range(4)]
+        step(args.warmup + args.steps + s, marks)
+        all_marks.append(marks)
+    torch.cuda.synchronize()
+    for marks in all_marks:
+        times["profile"].append(marks[0].elapsed_time(marks[1]))
+        times["solve"].append(marks[1].elapsed_time(marks[2]))
+        times["compress_allreduce"].append(marks[2].elapsed_time(marks[3]))
     clk = clocks.stop()
     k1_total_ms, k1_n = ctx.kernel_ms()
     ctx.timing(False)
     k1_ms = k1_total_ms / max(1, k1_n)
-    launches = ctx.launches() - launches0 + args.steps  # + one solve kernel per step
     ctx.check()
 
     ms = sum(times["step"]) / args.steps
@@ -344,6 +360,8 @@ def run_ours(args):
             # with the plan fixed), which is what runs between replans
             "plan_fixed_gbs": round(world * 4.0 * N / (stage["compress_allreduce"] * 1e-3) / 1e9, 2),
             "stage_ms": {k: round(v, 4) for k, v in stage.items()},
+            "stage_note": "step: headline pass (events at step begin/end only); profile/solve/compress: a second "
+                          "pass of K steps with events between the stages and around K1",
             "roofline": {"bound": "alu", "kernel": "k_qprofile_q (K1)", "achieved": round(k1_tops, 3),
                          "peak": round(alu_peak, 3), "unit": "T lane-op/s", "frac": round(k1_tops / alu_peak, 4),
                          "traffic": traffic, "peak_source": f"derived: {nsm} SMs x 4 SMSP x 32 lanes x {sm_mhz:.0f} MHz",
