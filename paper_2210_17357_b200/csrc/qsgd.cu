@@ -157,6 +157,99 @@ __device__ __forceinline__ void prof_candidates(const float* x, float mn, const 
 // one exact FMUL per element shared by all candidates.  dec = fmaf(q, unit, mn) and
 // d = x - dec are the pinned decode, so the SSE is
 // that of the realised reconstruction.
+#ifndef QP_F32X2
+#define QP_F32X2 1  // K1 candidate loop on the paired fp32 instructions (FFMA2 / FADD2 / FMUL2)
+#endif
+// Paired fp32 (sm_100: FFMA2/FADD2/FMUL2 -- two independent IEEE fp32 operations, each
+// rounded as its scalar form, one issue slot; a scalar operand is broadcast).
+typedef unsigned long long f2_t;
+__device__ __forceinline__ f2_t f2pk(float lo, float hi) {
+  f2_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2up(f2_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ f2_t f2fma_rp(f2_t a, f2_t b, f2_t c) {
+  f2_t r;
+  asm("fma.rp.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ f2_t f2fma(f2_t a, f2_t b, f2_t c) {
+  f2_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ f2_t f2add(f2_t a, f2_t b) {
+  f2_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2_t f2add_rp(f2_t a, f2_t b) {
+  f2_t r;
+  asm("add.rp.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ f2_t f2mul(f2_t a, f2_t b) {
+  f2_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
+// The same loop on element pairs (s = 0,1 and 2,3): per pair and candidate one FFMA2.RP
+// (w), two ceils, two FMNMX (clamp), one FFMA2 for -dec = fma(q, -unit, -mn) (exactly
+// -RN(q unit + mn): RN is symmetric), one FADD2 for d = x + (-dec) (= RN(x - dec)), one
+// FFMA2 for the square: 4 issue slots per element and candidate instead of 6, every
+// result bit-identical to the scalar form.  The SSE is kept as two fp32 partial sums
+// (even / odd elements) per candidate, added at the end.
+template <int KT, bool SCALED>
+__device__ __forceinline__ void prof_cand16x2(const float* x, float mn, uint32_t c0, uint32_t rankfield, uint32_t step,
+                                              uint32_t k0, uint32_t k1, const float* inv, const float* unit,
+                                              const CandS& cs, float S, float* acc) {
+  constexpr float MAGIC = 8388609.0f;  // 2^23 + 1
+  constexpr float NEG_2M24 = -5.9604644775390625e-08f;
+  f2_t a2[KT];
+#pragma unroll
+  for (int j = 0; j < KT; ++j) a2[j] = f2pk(0.f, 0.f);
+  const f2_t nmn = f2pk(-mn, -mn);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const U4 r = philox10(c0 + 8 * i, rankfield, step, 0u, k0, k1);
+    const f2_t nu[2] = {f2mul(f2pk(__uint2float_rn(r.x >> 8), __uint2float_rn(r.y >> 8)), f2pk(NEG_2M24, NEG_2M24)),
+                        f2mul(f2pk(__uint2float_rn(r.z >> 8), __uint2float_rn(r.w >> 8)), f2pk(NEG_2M24, NEG_2M24))};
+    const f2_t xp[2] = {f2pk(x[4 * i], x[4 * i + 1]), f2pk(x[4 * i + 2], x[4 * i + 3])};
+    const f2_t tp[2] = {f2add(xp[0], nmn), f2add(xp[1], nmn)};
+#pragma unroll
+    for (int j = 0; j < KT; ++j) {
+#pragma unroll
+      for (int p = 0; p < 2; ++p) {
+        const f2_t w = f2fma_rp(tp[p], f2pk(inv[j], inv[j]), nu[p]);
+        float q0, q1;
+        if (j >= KT - QP_XU_CEIL) {
+          float w0, w1;
+          f2up(w, w0, w1);
+          q0 = ceilf(w0);
+          q1 = ceilf(w1);
+        } else {
+          f2up(f2add(f2add_rp(w, f2pk(MAGIC, MAGIC)), f2pk(-MAGIC, -MAGIC)), q0, q1);
+        }
+        q0 = fminf(q0, cs.s[j]);
+        q1 = fminf(q1, cs.s[j]);
+        f2_t d = f2add(xp[p], f2fma(f2pk(q0, q1), f2pk(-unit[j], -unit[j]), nmn));
+        if (SCALED) d = f2mul(d, f2pk(S, S));
+        a2[j] = f2fma(d, d, a2[j]);
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < KT; ++j) {
+    float lo, hi;
+    f2up(a2[j], lo, hi);
+    acc[j] = __fadd_rn(lo, hi);
+  }
+}
+
 template <int KT, bool SCALED>
 __device__ __forceinline__ void prof_cand16(const float* x, float mn, uint32_t c0, uint32_t rankfield, uint32_t step,
                                             uint32_t k0, uint32_t k1, const float* inv, const float* unit,
@@ -272,8 +365,13 @@ k_qprofile(const float* __restrict__ g, const float* __restrict__ e, const DevLa
       double S2inv;
       const bool small = bucket_scale(mn, mx, S, S2inv);
       float a2[KT];
+#if QP_F32X2
+      if (__any_sync(LG_FULL, small)) prof_cand16x2<KT, true>(x, mn, c0, rankfield, step, k0, k1, inv, unit, cs, S, a2);
+      else prof_cand16x2<KT, false>(x, mn, c0, rankfield, step, k0, k1, inv, unit, cs, 1.f, a2);
+#else
       if (__any_sync(LG_FULL, small)) prof_cand16<KT, true>(x, mn, c0, rankfield, step, k0, k1, inv, unit, cs, S, a2);
       else prof_cand16<KT, false>(x, mn, c0, rankfield, step, k0, k1, inv, unit, cs, 1.f, a2);
+#endif
       if (valid) {
 #pragma unroll
         for (int j = 0; j < KT; ++j) acc[j] = __dadd_rn(acc[j], __dmul_rn((double)a2[j], S2inv));
@@ -604,8 +702,13 @@ k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const QIn
       double S2inv;
       const bool small = bucket_scale(mn, mx, S, S2inv);
       float a2[KT];
+#if QP_F32X2
+      if (__any_sync(LG_FULL, small)) prof_cand16x2<KT, true>(x, mn, c0, rankfield, step, k0, k1, inv, unit, cs, S, a2);
+      else prof_cand16x2<KT, false>(x, mn, c0, rankfield, step, k0, k1, inv, unit, cs, 1.f, a2);
+#else
       if (__any_sync(LG_FULL, small)) prof_cand16<KT, true>(x, mn, c0, rankfield, step, k0, k1, inv, unit, cs, S, a2);
       else prof_cand16<KT, false>(x, mn, c0, rankfield, step, k0, k1, inv, unit, cs, 1.f, a2);
+#endif
       if (KT <= 8) {
         // quad row, fixed order: transpose-reduce the 8 lanes of each bucket in fp32
         // (after the xor-4/2/1 halvings lane l8 holds candidate l8's bucket SSE, from
