@@ -46,6 +46,17 @@ __device__ __forceinline__ float fmax_nan(float a, float b) {
   asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
   return r;
 }
+// three-input forms (FMNMX3, sm_100)
+__device__ __forceinline__ float fmin3_nan(float a, float b, float c) {
+  float r;
+  asm("min.NaN.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+__device__ __forceinline__ float fmax3_nan(float a, float b, float c) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
 __device__ __forceinline__ void warp_minmax_nan(float& mn, float& mx) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
@@ -636,8 +647,8 @@ k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const QIn
           const float4 a = *reinterpret_cast<const float4*>(sg + 32 * i);
           if (e) {
             const float4 f = *reinterpret_cast<const float4*>(se + 32 * i);
-            x[4 * i] = __fadd_rn(a.x, f.x); x[4 * i + 1] = __fadd_rn(a.y, f.y);
-            x[4 * i + 2] = __fadd_rn(a.z, f.z); x[4 * i + 3] = __fadd_rn(a.w, f.w);
+            f2up(f2add(f2pk(a.x, a.y), f2pk(f.x, f.y)), x[4 * i], x[4 * i + 1]);
+            f2up(f2add(f2pk(a.z, a.w), f2pk(f.z, f.w)), x[4 * i + 2], x[4 * i + 3]);
           } else {
             x[4 * i] = a.x; x[4 * i + 1] = a.y; x[4 * i + 2] = a.z; x[4 * i + 3] = a.w;
           }
@@ -667,7 +678,7 @@ k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const QIn
       if (cur_regular) {
         mn = fmin_nan(x[0], x[1]); mx = fmax_nan(x[0], x[1]);
 #pragma unroll
-        for (int s2 = 2; s2 < 16; ++s2) { mn = fmin_nan(mn, x[s2]); mx = fmax_nan(mx, x[s2]); }
+        for (int s2 = 2; s2 < 16; s2 += 2) { mn = fmin3_nan(mn, x[s2], x[s2 + 1]); mx = fmax3_nan(mx, x[s2], x[s2 + 1]); }
       } else {
         mn = INFINITY; mx = -INFINITY;
 #pragma unroll
