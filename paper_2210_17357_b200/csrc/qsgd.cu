@@ -30,7 +30,7 @@ namespace lg {
 constexpr int QP_THREADS = 256;
 constexpr int QP_WARPS = QP_THREADS / 32;
 #ifndef QP_XU_CEIL
-#define QP_XU_CEIL 7  // candidates of the K1 fast path whose ceil runs on the XU pipe
+#define QP_XU_CEIL 5  // candidates of the K1 fast path whose ceil runs on the XU pipe (others: FADD2 magic; A/B: 0-5 equal, 7 +2 %)
 #endif
 
 // ---------------------------------------------------------------------------
