@@ -765,6 +765,12 @@ __device__ __forceinline__ void pd_store(uint8_t* dst, const uint32_t* w) {
   else *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
 }
 
+#ifndef DP_PD_CELLMAJOR
+#define DP_PD_CELLMAJOR 1
+#endif
+#ifndef DP_SUM_BCH
+#define DP_SUM_BCH 1
+#endif
 template <int CPT, int KT>
 __global__ void __launch_bounds__(DP_THREADS, 1)
 k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int L, int K,
@@ -805,11 +811,13 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
   // the whole (err, bits) table in one global round trip (every later prelude read is
   // shared memory) when it fits in front of the rows' space
   constexpr int PADC = 32 * CPT;
-  const bool pre = (size_t)(24 + 16 * K) * L + 64 <= (size_t)16 * (PADC + (int)NC * S);
+  const bool pre = (size_t)(36 + 16 * K) * L + 64 <= (size_t)16 * (PADC + (int)NC * S);
   double* sm_err = sm_dea + L;
   int64_t* sm_bits = reinterpret_cast<int64_t*>(sm_err + (pre ? (size_t)L * K : 0));
-  if (pre)
+  if (pre) {
+#pragma unroll 4
     for (int i = tid; i < L * K; i += NT) { sm_err[i] = __ldg(err + i); sm_bits[i] = __ldg(bits + i); }
+  }
   const double* t_err = pre ? sm_err : err;
   const int64_t* t_bits = pre ? sm_bits : bits;
   if (tid == 0) s_status = LGRECO_OK;
@@ -889,31 +897,31 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
   uint64_t gg = 0, mx_part = 0;
   int bad = 0;
   if (tid == 0) my_wmaxd[La] = 0;
-  for (int a = warp; a < La; a += NW) {
+  // every (layer, candidate) pair on its own thread (was: a warp per layer, K lanes
+  // busy); per-layer maxima through shared atomics (order-free: max is exact)
+  uint64_t* sm_m = reinterpret_cast<uint64_t*>(sm_bits + (pre ? (size_t)L * K : 0));  // [La]
+  int32_t* sm_dm = reinterpret_cast<int32_t*>(sm_m + L);                               // [La]
+  for (int a = tid; a < La; a += NT) { sm_m[a] = 0; sm_dm[a] = 0; }
+  __syncthreads();
+  for (int i = tid; i < La * K; i += NT) {
+    const int a = i / K, c = i - a * K;
     const int l = sm_act[a];
-    uint64_t m = 0;
-    int dm = 0;
-    for (int c = lane; c < K; c += 32) {
-      const double v = t_err[(int64_t)l * K + c];
-      const int64_t b = t_bits[(int64_t)l * K + c];
-      if (!isfinite(v) || v < 0.0) bad |= 1;
-      if (b < 0) bad |= 2;
-      const uint64_t ub = (uint64_t)(b < 0 ? 0 : b);
-      gg |= ub;
-      m = max(m, ub);
-      const int dd = discretise(metric(v, flags), emax, D, flags);
-      dm = max(dm, dd);
-      my_wdisc[a * K + c] = dd;
-      my_wadd[a * K + c] = ub;
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      m = max(m, __shfl_xor_sync(LG_FULL, m, o));
-      dm = max(dm, __shfl_xor_sync(LG_FULL, dm, o));
-    }
-    mx_part += m;
-    if (lane == 0) my_wmaxd[a] = dm;
+    const double v = t_err[(int64_t)l * K + c];
+    const int64_t b = t_bits[(int64_t)l * K + c];
+    if (!isfinite(v) || v < 0.0) bad |= 1;
+    if (b < 0) bad |= 2;
+    const uint64_t ub = (uint64_t)(b < 0 ? 0 : b);
+    gg |= ub;
+    const int dd = discretise(metric(v, flags), emax, D, flags);
+    my_wdisc[i] = dd;
+    my_wadd[i] = ub;
+    atomicMax(reinterpret_cast<unsigned long long*>(&sm_m[a]), (unsigned long long)ub);
+    atomicMax(&sm_dm[a], dd);
   }
+  __syncthreads();
+  for (int a = tid; a < La; a += NT) { mx_part += sm_m[a]; my_wmaxd[a] = sm_dm[a]; }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mx_part += __shfl_xor_sync(LG_FULL, mx_part, o);  // per-thread partials
   bad = __reduce_or_sync(LG_FULL, bad);
   LG_T(8);
 #pragma unroll
@@ -1214,7 +1222,15 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
     // back-pressure only (no CTA runs a row ahead, so no push lands in a row buffer a
     // peer still reads); the data itself is ordered by the st.async -> mbarrier path
     asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+#if DP_PD_CELLMAJOR
+    if (live) {  // cell-major PD row (byte of cell e at a * PDR + e): 32 B per warp store
+      uint8_t* dst = PD + (int64_t)a * PDR + cbase + warp * 32 * CPT + lane;
+#pragma unroll
+      for (int i = 0; i < CPT; ++i) __stcg(dst + 32 * i, (uint8_t)(pdw[i >> 2] >> (8 * (i & 3))));
+    }
+#else
     if (live) pd_store<CPT>(PD + (int64_t)a * PDR + (int64_t)gtid * CPT, pdw);
+#endif
     asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
 #ifdef LG_DP_TIMING
     t_cl += clock64() - ts1;
@@ -1279,13 +1295,17 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
   const int32_t* bdisc = my_wdisc;  // the discretised table (shared memory)
   int32_t* bch = reinterpret_cast<int32_t*>(smem_raw);  // [La] chosen c per active layer (rows are dead)
   __syncthreads();
-  // PD byte of (layer a, cell e): CTA r = e / S, warp w, register i, lane
+  // PD byte of (layer a, cell e): cell-major rows
+#if DP_PD_CELLMAJOR
+  auto pd_at = [&](int a, int e) -> int { return __ldcg(PD + (int64_t)a * PDR + e); };
+#else
   auto pd_at = [&](int a, int e) -> int {
     const int r = e / S, el = e - r * S;
     const int w = el / (32 * CPT), rr = el - w * (32 * CPT);
     const int T = r * NT + w * 32 + (rr & 31);
     return __ldcg(PD + (int64_t)a * PDR + (int64_t)T * CPT + (rr >> 5));
   };
+#endif
   if (warp == 0) {
     uint64_t k = (lane < (int)NC) ? s_clk[lane] : ~0ull;
     int ee = (lane < (int)NC) ? s_cle[lane] : 0x7fffffff;
@@ -1369,7 +1389,7 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
   if (!s_La)
     for (int a = tid; a < La; a += NT) choice[act[a]] = bch[a];
   __syncthreads();
-  double* sm_ce = reinterpret_cast<double*>(smem_raw);
+  double* sm_ce = reinterpret_cast<double*>(smem_raw + (((size_t)La * 4 + 15) & ~(size_t)15));  // after bch
   int64_t* sm_cb = reinterpret_cast<int64_t*>(sm_ce + La);
   int used_default = s_La;
   if (used_default) {
@@ -1379,7 +1399,11 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
   for (int pass = 0; pass < 2; ++pass) {
     for (int a = tid; a < La; a += NT) {
       const int l = act[a];
+#if DP_SUM_BCH
+      const int c = used_default ? default_idx[l] : bch[a];
+#else
       const int c = used_default ? default_idx[l] : choice[l];
+#endif
       sm_ce[a] = metric(err[(int64_t)l * K + c], flags);
       sm_cb[a] = bits[(int64_t)l * K + c];
     }
