@@ -1032,16 +1032,17 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
       dead = dead || dead_m != 0;
     }
   }
-  if (!wide) {
-    for (int i = tid; i < row; i += NT) { r32a[i] = (i == PAD) ? 0u : INF32; r32b[i] = INF32; }
+  if (!wide) {  // three row buffers (the 16-byte-per-cell region holds four u32 rows)
+    for (int i = tid; i < row; i += NT) { r32a[i] = (i == PAD) ? 0u : INF32; r32b[i] = INF32; r32b[row + i] = INF32; }
   } else {
     for (int i = tid; i < row; i += NT) { r64a[i] = (i == PAD) ? 0ull : INF64; r64b[i] = INF64; }
   }
-  // s_bar[p]: completion of the remote cells of rows with parity p (st.async complete_tx)
-  __shared__ __align__(8) uint64_t s_bar[2];
+  // s_bar[i]: completion of the remote cells of the row in buffer i (st.async complete_tx)
+  __shared__ __align__(8) uint64_t s_bar[3];
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&s_bar[0])));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&s_bar[1])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&s_bar[2])));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   // KT == 0: the candidates of row a staged in s_ck/s_ak[a & 1] (keyed as above)
@@ -1058,9 +1059,18 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
   if (KT == 0) stage0((tid < K) ? my_wdisc[tid] : -1, (tid < K) ? my_wadd[tid] : 0, 0);
   LG_T(1);
   cl_sync();  // every CTA's rows and barriers initialised before any remote push lands
+  if (!wide) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");  // "row -1 done"
   LG_T(2);
-  int cur_is_b = 1;
-  uint32_t bph = 0u;  // bit p: parity of s_bar[p]'s next phase
+  // Row buffers: row a in buffer bc, row a-1 in bp (row -1 = the initial row, buffer 0).
+  // Narrow keys: NB = 3 buffers, so the cluster barrier that keeps a CTA from pushing
+  // into a buffer a peer still reads is split: the wait for "every CTA finished row a-1"
+  // happens after this CTA computed row a (arrive after row a-1, wait after row a) and
+  // its latency hides behind a row; a push of row a then lands in the buffer of row
+  // a-3, last read while computing row a-2, which every CTA finished (waited for before
+  // row a).  Wide keys (64-bit rows): NB = 2 and the full barrier per row.
+  const int NB = wide ? 2 : 3;
+  int bc = 1, bp = 0;
+  uint32_t bph = 0u;  // bit i: parity of s_bar[i]'s next phase
   const int wbase = cbase + warp * (32 * CPT);
   const int dclamp = wbase + PAD;
   const int64_t PDR = (int64_t)NC * NT * CPT;  // PD bytes per layer
@@ -1074,7 +1084,8 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
   int2 band = band_all[0];
   int maxd = my_wmaxd[1];
   for (int a = 0; a < La; ++a) {
-    const int sb = a & 1;
+    const int sb = bc;     // barrier of row a's buffer
+    const int sk = a & 1;  // KT == 0 candidate staging slot of row a
     // cells of row a this CTA receives: [cbase - maxd, cbase) (clipped at 0)
     if (tid == 0) {
       const uint32_t bytes = (uint32_t)min(maxd, cbase) * vb;
@@ -1098,8 +1109,8 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
     if (flags & (1u << 30)) rtop = -1;  // diagnostic only: no pushes (wrong result)
 #endif
     if (!wide) {
-      const uint32_t* prev = (cur_is_b ? r32a : r32b) + PAD + wbase + lane;
-      uint32_t* cur = (cur_is_b ? r32b : r32a) + PAD + wbase + lane;
+      const uint32_t* prev = r32a + (size_t)bp * row + PAD + wbase + lane;
+      uint32_t* cur = r32a + (size_t)bc * row + PAD + wbase + lane;
       uint32_t best[CPT];
       if (live && KT == 0) {
         uint32_t bgrp[CPT];
@@ -1111,7 +1122,7 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
 #pragma unroll
           for (int i = 0; i < CPT; ++i) gk[i] = 0xFFFFFFFFu;
           for (int c = 0; c < cn; ++c) {
-            const uint2 cd = s_ck[sb][c0 + c];
+            const uint2 cd = s_ck[sk][c0 + c];
             const uint32_t* pv = prev - min((int)cd.x, dclamp);
 #pragma unroll
             for (int i = 0; i < CPT; ++i) gk[i] = __viaddmin_u32(pv[i * 32], cd.y, gk[i]);
@@ -1167,16 +1178,16 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
                          : "memory");
       }
     } else {
-      const uint64_t* prev = (cur_is_b ? r64a : r64b) + PAD + wbase + lane;
-      uint64_t* cur = (cur_is_b ? r64b : r64a) + PAD + wbase + lane;
+      const uint64_t* prev = r64a + (size_t)bp * row + PAD + wbase + lane;
+      uint64_t* cur = r64a + (size_t)bc * row + PAD + wbase + lane;
       const uint64_t* add = add_all + (size_t)a * KT;
       uint64_t best[CPT];
 #pragma unroll
       for (int i = 0; i < CPT; ++i) best[i] = ~0ull;
       if (live) {
         for (int c = 0; c < (KT > 0 ? KT : K); ++c) {
-          const uint64_t* pv = prev - min((int)(KT > 0 ? cnd[c].x : s_ck[sb][c].x), dclamp);
-          const uint64_t ak = (KT > 0) ? add[c] : s_ak[sb][c];
+          const uint64_t* pv = prev - min((int)(KT > 0 ? cnd[c].x : s_ck[sk][c].x), dclamp);
+          const uint64_t ak = (KT > 0) ? add[c] : s_ak[sk][c];
 #pragma unroll
           for (int i = 0; i < CPT; ++i) best[i] = min(best[i], pv[i * 32] + ak);
         }
@@ -1200,8 +1211,9 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
                          : "memory");
       }
     }
-    cur_is_b ^= 1;
-    if (KT == 0 && a + 1 < La) stage0(nd, nub, sb ^ 1);  // slot last read in row a-1
+    bp = bc;
+    bc = (bc + 1 == NB) ? 0 : bc + 1;
+    if (KT == 0 && a + 1 < La) stage0(nd, nub, sk ^ 1);  // slot last read in row a-1
     if (a + 1 < La) {
       const uint4* nq = reinterpret_cast<const uint4*>(cand_all + (size_t)(a + 1) * KP2);
 #pragma unroll
@@ -1221,6 +1233,9 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
 #endif
     // back-pressure only (no CTA runs a row ahead, so no push lands in a row buffer a
     // peer still reads); the data itself is ordered by the st.async -> mbarrier path
+    if (NB == 3) {
+      asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // every CTA finished row a-1
+    }
     asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
 #if DP_PD_CELLMAJOR
     if (live) {  // cell-major PD row (byte of cell e at a * PDR + e): 32 B per warp store
@@ -1231,7 +1246,7 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
 #else
     if (live) pd_store<CPT>(PD + (int64_t)a * PDR + (int64_t)gtid * CPT, pdw);
 #endif
-    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+    if (NB == 2) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
 #ifdef LG_DP_TIMING
     t_cl += clock64() - ts1;
 #endif
@@ -1252,6 +1267,7 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
     t_push += clock64() - tp0;
 #endif
   }
+  if (!wide) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // pairs the last arrive
   LG_T(3);
   // ---- line 23: argmin of the last row over this CTA's cells, gathered in rank 0
   {
@@ -1261,8 +1277,8 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
       const int e = cbase + el;
       if (e > D) break;
       uint64_t v;
-      if (!wide) { const uint32_t x = ((cur_is_b ? r32a : r32b) + PAD)[e]; v = (x >= INF32) ? ~0ull : x; }
-      else { const uint64_t x = ((cur_is_b ? r64a : r64b) + PAD)[e]; v = (x >= INF64) ? ~0ull : x; }
+      if (!wide) { const uint32_t x = (r32a + (size_t)bp * row + PAD)[e]; v = (x >= INF32) ? ~0ull : x; }
+      else { const uint64_t x = (r64a + (size_t)bp * row + PAD)[e]; v = (x >= INF64) ? ~0ull : x; }
       if (v < bk) { bk = v; be = e; }
     }
 #pragma unroll
