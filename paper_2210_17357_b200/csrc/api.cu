@@ -664,15 +664,17 @@ int lgreco_compress_allreduce_dev(lgreco_ctx* c, const int32_t* d_choice, const 
   LG_TRY(check_align16("compress_allreduce_dev", d_g, d_ef, d_out));
   cudaStream_t st = (cudaStream_t)stream;
   if (c->world == 1 && c->family == LGRECO_QSGD) {
-    // W = 1: nothing leaves the GPU, the fused pass needs only the bits per layer
-    LG_LAUNCH(c, lg::launch_plan_qsgd_dev(d_choice, c->d_params, c->K, c->d_layers, c->L, c->d_plan, c->d_flag, st));
-    c->plan_valid = false;  // d_plan now holds a device-chosen plan
+    // W = 1: nothing leaves the GPU, the fused pass needs only the bits per layer, which
+    // K5 reads from the device choice itself (one launch)
     uint32_t k0, k1;
     key_of(c, k0, k1);
     lg::QPackArgs a{d_g, d_ef, nullptr, d_out, c->d_layers, c->d_plan, c->d_chunks_all, c->nchunks_all, c->B,
                     k0, k1, 0u, (uint32_t)step, c->d_flag};
+    a.choice = d_choice;
+    a.params = c->d_params;
+    a.K = c->K;
     LG_LAUNCH(c, lg::launch_qpack(a, st));
-    c->launches += 2;
+    c->launches += 1;
     return LGRECO_OK;
   }
   if (c->world == 1 && c->family == LGRECO_TOPK) {

@@ -57,6 +57,9 @@ struct QPackArgs {
   const DevLayer* layers; const DevPlan* plan; const ProfChunk* chunks; int nchunks; int B;
   uint32_t k0, k1, rankfield, step; unsigned* flag;
   const P2PDev* p2p = nullptr;  // non-null: records go straight to their owner's window
+  // non-null (W = 1, no payload): bits per layer = params[choice[l]] read in the kernel
+  // itself (no plan kernel); a choice outside [0, K) sets flag bit 2 and uses 0
+  const int32_t* choice = nullptr; const int32_t* params = nullptr; int K = 0;
 };
 
 struct QUnpackArgs {

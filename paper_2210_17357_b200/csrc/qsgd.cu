@@ -951,11 +951,26 @@ __global__ void __launch_bounds__(QP_THREADS)
 k_qpack(const float* __restrict__ g, float* __restrict__ ef, uint8_t* __restrict__ payload,
         float* __restrict__ dec_out, const DevLayer* __restrict__ layers, const DevPlan* __restrict__ plan,
         const ProfChunk* __restrict__ chunks, int B, uint32_t k0, uint32_t k1, uint32_t rankfield,
-        uint32_t step, unsigned* __restrict__ flag, const P2PDev* __restrict__ p2p) {
-  pdl_wait();  // the plan (k_plan_qsgd_dev) and the EF of the previous step
+        uint32_t step, unsigned* __restrict__ flag, const P2PDev* __restrict__ p2p,
+        const int32_t* __restrict__ choice, const int32_t* __restrict__ params, int K) {
+  pdl_wait();  // the plan (k_plan_qsgd_dev, or the solve's choice) and the EF of the previous step
   const ProfChunk ch = chunks[blockIdx.x];
   const DevLayer ly = layers[ch.layer];
-  const DevPlan pl = plan[ch.layer];
+  DevPlan pl;
+  if (choice) {  // W = 1: the bits straight from the device choice (k_plan_qsgd_dev's rule)
+    int bits = 0;
+    if (ly.compress) {
+      int c = choice[ch.layer];
+      if (c < 0 || c >= K) {
+        if (threadIdx.x == 0) atomicOr(flag, 2u);
+        c = 0;
+      }
+      bits = params[c];
+    }
+    pl = DevPlan{0, bits, 0};
+  } else {
+    pl = plan[ch.layer];
+  }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int M = B >> 7;
   const bool aligned = (ly.offset & 3) == 0;
@@ -1309,7 +1324,8 @@ cudaError_t launch_qprofile(const QProfileArgs& a, cudaStream_t st) {
 cudaError_t launch_qpack(const QPackArgs& a, cudaStream_t st) {
   if (a.nchunks == 0) return cudaSuccess;
   const cudaError_t e = launch_pdl(k_qpack, dim3(a.nchunks), dim3(QP_THREADS), 0, st, a.g, a.ef, a.payload, a.dec,
-                                   a.layers, a.plan, a.chunks, a.B, a.k0, a.k1, a.rankfield, a.step, a.flag, a.p2p);
+                                   a.layers, a.plan, a.chunks, a.B, a.k0, a.k1, a.rankfield, a.step, a.flag, a.p2p,
+                                   a.choice, a.params, a.K);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
