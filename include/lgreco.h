@@ -100,8 +100,10 @@ int lgreco_ctx_create(lgreco_ctx** out, const lgreco_layer* layers, int32_t L,
                       const void* nccl_unique_id, void* stream);
 void lgreco_ctx_destroy(lgreco_ctx* ctx);
 
-/* Synchronises `stream` and returns LGRECO_ENONFINITE if any kernel saw a
- * non-finite gradient value since the last check (then clears the flag). */
+/* Synchronises `stream` and returns LGRECO_EINVAL if a device-plan entry point
+ * (lgreco_compress_allreduce_dev) met a choice outside [0, K) for a compressed
+ * layer (it used candidate 0 there), else LGRECO_ENONFINITE if any kernel saw a
+ * non-finite gradient value since the last check; either clears the flags. */
 int lgreco_ctx_check(lgreco_ctx* ctx, void* stream);
 
 /* Number of kernels this ctx has launched (evidence counter). */

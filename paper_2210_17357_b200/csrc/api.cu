@@ -341,6 +341,10 @@ int lgreco_ctx_check(lgreco_ctx* c, void* stream) {
   LG_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
   if (f) {
     LG_CUDA(cudaMemsetAsync(c->d_flag, 0, sizeof(unsigned), (cudaStream_t)stream));
+    if (f & 2u) {
+      lg_set_error("device plan: choice outside [0, K) for a compressed layer");
+      return LGRECO_EINVAL;
+    }
     lg_set_error("non-finite gradient value seen");
     return LGRECO_ENONFINITE;
   }

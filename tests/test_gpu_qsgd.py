@@ -219,6 +219,25 @@ def test_compress_allreduce_dev_matches_host_path(lg):
     assert torch.equal(o1.view(torch.int32), o2.view(torch.int32)) and torch.equal(e1.view(torch.int32), e2.view(torch.int32))
 
 
+def test_compress_allreduce_dev_bad_choice(lg):
+    """A device choice outside [0, K) on a compressed layer is reported by ctx_check as
+    EINVAL (the kernel uses candidate 0 there); a valid one afterwards checks clean."""
+    layers = W.config_layers("C1")
+    g, e = W.gaussian_outliers(layers, seed=13)
+    ctx = lg.Context(layers, lg.QSGD, BITS, seed=5)
+    gd, ed = _dev(g), _dev(e)
+    out = torch.empty_like(gd)
+    comp = [i for i, l in enumerate(layers) if l.compress]
+    bad = [0] * len(layers)
+    bad[comp[0]] = len(BITS)
+    ctx.compress_allreduce_dev(torch.tensor(bad, dtype=torch.int32, device="cuda"), gd, ed, out, 1)
+    with pytest.raises(lg.LGrecoError) as ei:
+        ctx.check()
+    assert ei.value.status == lg.EINVAL
+    ctx.compress_allreduce_dev(torch.zeros(len(layers), dtype=torch.int32, device="cuda"), gd, ed, out, 2)
+    ctx.check()
+
+
 def _adversarial_buckets(seed=21):
     """One-bucket layers (128 elements, 16-byte aligned offsets: the K1 fast path) whose
     codes are easy to get wrong, so that ONE wrong stochastic-rounding decision moves the
