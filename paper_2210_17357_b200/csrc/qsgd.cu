@@ -818,9 +818,21 @@ k_qprofile_reduce(const DevLayer* __restrict__ layers, const QSeg* __restrict__ 
   __threadfence();
   const int s0 = lseg0[l], s1 = lseg0[l + 1];
   const int64_t nb = (ly.numel + B - 1) / B;
+  // the layer's segment sums in segment order: staged a chunk at a time (one L2 round
+  // trip for up to QR_ROWS / K segments, the rows of consecutive segments being
+  // contiguous) and added in order from shared memory
+  __shared__ double sbuf[QR_ROWS];
+  const int chunk = QR_ROWS / K;
+  double s = 0.0;
+  for (int q0 = s0; q0 < s1; q0 += chunk) {
+    const int nq = min(chunk, s1 - q0);
+    if (t < nq * K) sbuf[t] = __ldcg(segsum + (int64_t)q0 * K + t);
+    __syncthreads();
+    if (t < K)
+      for (int i = 0; i < nq; ++i) s += sbuf[i * K + t];
+    __syncthreads();
+  }
   if (t < K) {
-    double s = 0.0;
-    for (int q = s0; q < s1; ++q) s += __ldcg(segsum + (int64_t)q * K + t);
     if (ly.compress) {
       err[(int64_t)l * K + t] = sqrt(s);
       bits[(int64_t)l * K + t] = nb * ((int64_t)B * params[t] + 64);
