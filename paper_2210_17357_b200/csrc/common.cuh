@@ -44,6 +44,27 @@ __device__ __forceinline__ U4 philox10(uint32_t c0, uint32_t c1, uint32_t c2, ui
   return U4{c0, c1, c2, c3};
 }
 
+// The ten round keys of Philox4x32-10 (k0 + r W0, k1 + r W1), precomputed on the host and
+// passed as a kernel parameter: the rounds then read them straight from the parameter
+// bank (a LOP3 operand) instead of re-deriving them in the loop.
+struct PhiloxRK { uint32_t k[20]; };
+__host__ __device__ inline PhiloxRK philox_rk(uint32_t k0, uint32_t k1) {
+  PhiloxRK r;
+  for (int i = 0; i < 10; ++i) { r.k[2 * i] = k0 + 0x9E3779B9u * (uint32_t)i; r.k[2 * i + 1] = k1 + 0xBB67AE85u * (uint32_t)i; }
+  return r;
+}
+__device__ __forceinline__ U4 philox10_rk(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, const PhiloxRK& rk) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t p0 = (uint64_t)0xD2511F53u * c0;
+    const uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
+    const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ rk.k[2 * r];
+    const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ rk.k[2 * r + 1];
+    c0 = n0; c1 = (uint32_t)p1; c2 = n2; c3 = (uint32_t)p0;
+  }
+  return U4{c0, c1, c2, c3};
+}
+
 // u = (w >> 8) * 2^-24 (exact)
 __device__ __forceinline__ float word_u(uint32_t w) {
   return __fmul_rn(__uint2float_rn(w >> 8), 5.9604644775390625e-08f);

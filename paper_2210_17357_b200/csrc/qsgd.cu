@@ -216,7 +216,7 @@ __device__ __forceinline__ f2_t f2mul(f2_t a, f2_t b) {
 // (even / odd elements) per candidate, added at the end.
 template <int KT, bool SCALED>
 __device__ __forceinline__ void prof_cand16x2(const float* x, float mn, uint32_t c0, uint32_t rankfield, uint32_t step,
-                                              uint32_t k0, uint32_t k1, const float* inv, const float* unit,
+                                              const PhiloxRK& rk, const float* inv, const float* unit,
                                               const CandS& cs, float S, float* acc) {
   constexpr float MAGIC = 8388609.0f;  // 2^23 + 1
   constexpr float NEG_2M24 = -5.9604644775390625e-08f;
@@ -226,7 +226,7 @@ __device__ __forceinline__ void prof_cand16x2(const float* x, float mn, uint32_t
   const f2_t nmn = f2pk(-mn, -mn);
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const U4 r = philox10(c0 + 8 * i, rankfield, step, 0u, k0, k1);
+    const U4 r = philox10_rk(c0 + 8 * i, rankfield, step, 0u, rk);
     const f2_t nu[2] = {f2mul(f2pk(__uint2float_rn(r.x >> 8), __uint2float_rn(r.y >> 8)), f2pk(NEG_2M24, NEG_2M24)),
                         f2mul(f2pk(__uint2float_rn(r.z >> 8), __uint2float_rn(r.w >> 8)), f2pk(NEG_2M24, NEG_2M24))};
     const f2_t xp[2] = {f2pk(x[4 * i], x[4 * i + 1]), f2pk(x[4 * i + 2], x[4 * i + 3])};
@@ -377,8 +377,9 @@ k_qprofile(const float* __restrict__ g, const float* __restrict__ e, const DevLa
       const bool small = bucket_scale(mn, mx, S, S2inv);
       float a2[KT];
 #if QP_F32X2
-      if (__any_sync(LG_FULL, small)) prof_cand16x2<KT, true>(x, mn, c0, rankfield, step, k0, k1, inv, unit, cs, S, a2);
-      else prof_cand16x2<KT, false>(x, mn, c0, rankfield, step, k0, k1, inv, unit, cs, 1.f, a2);
+      const PhiloxRK rk = philox_rk(k0, k1);
+      if (__any_sync(LG_FULL, small)) prof_cand16x2<KT, true>(x, mn, c0, rankfield, step, rk, inv, unit, cs, S, a2);
+      else prof_cand16x2<KT, false>(x, mn, c0, rankfield, step, rk, inv, unit, cs, 1.f, a2);
 #else
       if (__any_sync(LG_FULL, small)) prof_cand16<KT, true>(x, mn, c0, rankfield, step, k0, k1, inv, unit, cs, S, a2);
       else prof_cand16<KT, false>(x, mn, c0, rankfield, step, k0, k1, inv, unit, cs, 1.f, a2);
@@ -514,7 +515,7 @@ constexpr int QP_NPART = 16;  // K1 ticket counters (parts of the quad range), 2
 template <int KT>
 __global__ void __launch_bounds__(QP_THREADS, QP_MINB)
 k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const QInfo* __restrict__ qinfo, int nqc,
-             unsigned* __restrict__ ticket, const CandS cs, int K, uint32_t k0, uint32_t k1, uint32_t rankfield,
+             unsigned* __restrict__ ticket, const CandS cs, int K, const PhiloxRK rk, uint32_t rankfield,
              uint32_t step, int ptr_aligned, double* __restrict__ partial) {
   extern __shared__ __align__(128) unsigned char qsm[];
   __shared__ __align__(8) uint64_t bars[QP_WARPS][2];
@@ -714,8 +715,8 @@ k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const QIn
       const bool small = bucket_scale(mn, mx, S, S2inv);
       float a2[KT];
 #if QP_F32X2
-      if (__any_sync(LG_FULL, small)) prof_cand16x2<KT, true>(x, mn, c0, rankfield, step, k0, k1, inv, unit, cs, S, a2);
-      else prof_cand16x2<KT, false>(x, mn, c0, rankfield, step, k0, k1, inv, unit, cs, 1.f, a2);
+      if (__any_sync(LG_FULL, small)) prof_cand16x2<KT, true>(x, mn, c0, rankfield, step, rk, inv, unit, cs, S, a2);
+      else prof_cand16x2<KT, false>(x, mn, c0, rankfield, step, rk, inv, unit, cs, 1.f, a2);
 #else
       if (__any_sync(LG_FULL, small)) prof_cand16<KT, true>(x, mn, c0, rankfield, step, k0, k1, inv, unit, cs, S, a2);
       else prof_cand16<KT, false>(x, mn, c0, rankfield, step, k0, k1, inv, unit, cs, 1.f, a2);
@@ -1290,7 +1291,8 @@ cudaError_t launch_qprofile(const QProfileArgs& a, cudaStream_t st) {
                      cudaSuccess || occ < 1)) occ = 1;                                                          \
     const int grid = std::max(1, std::min(a.nqwarps / QP_WARPS, nsm * occ));                                    \
     const cudaError_t e2 = launch_pdl(k_qprofile_q<KT>, dim3(grid), dim3(QP_THREADS), smem, st, a.g, a.e,       \
-                                      a.qinfo, a.nqchunks, a.ticket, a.cs, a.K, a.k0, a.k1, a.rankfield, a.step,   \
+                                      a.qinfo, a.nqchunks, a.ticket, a.cs, a.K, philox_rk(a.k0, a.k1), a.rankfield, \
+                                      a.step,                                                                    \
                                       a.ptr_aligned, a.partial);                                                 \
     if (e2 != cudaSuccess) return e2;                                                                            \
   }
