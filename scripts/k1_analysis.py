@@ -45,7 +45,7 @@ def main():
                         ("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", "XU pipe"),
                         ("sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active", "LSU pipe"),
                         ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active (occupancy)"),
-                        ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput")]:
+                        ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput")]:
         print(f"| {label} | {m(name):.1f} |")
     print("\nSASS mix (executed warp instructions, top 16; per element = x32/N):\n")
     print("| opcode | warp instr | per element |")
