@@ -509,26 +509,33 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 #define QK_UNROLL 4  // K5 fast path: buckets per warp iteration (loads in flight)
 #endif
 constexpr int QP_NPART = 16;  // K1 ticket counters (parts of the quad range), 256 B apart
-#ifndef QP_MINB
-#define QP_MINB 3  // resident CTAs per SM of the K1 fast kernel (register budget 65536 / (256 * QP_MINB))
+#ifndef Q1_WARPS
+#define Q1_WARPS 8  // warps per CTA of the K1 fast kernel (each double-buffers 4 KB quads: 8 KB of shared memory)
 #endif
+#ifndef Q1_STAGES
+#define Q1_STAGES 2  // quad buffers per warp (1: the next quad is fetched once the current one is in registers)
+#endif
+#ifndef Q1_MINB
+#define Q1_MINB 3   // resident CTAs per SM of the K1 fast kernel (register budget 65536 / (32 Q1_WARPS Q1_MINB))
+#endif
+constexpr int Q1_THREADS = 32 * Q1_WARPS;
 template <int KT>
-__global__ void __launch_bounds__(QP_THREADS, QP_MINB)
+__global__ void __launch_bounds__(Q1_THREADS, Q1_MINB)
 k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const QInfo* __restrict__ qinfo, int nqc,
              unsigned* __restrict__ ticket, const CandS cs, int K, const PhiloxRK rk, uint32_t rankfield,
              uint32_t step, int ptr_aligned, double* __restrict__ partial) {
   extern __shared__ __align__(128) unsigned char qsm[];
-  __shared__ __align__(8) uint64_t bars[QP_WARPS][2];
+  __shared__ __align__(8) uint64_t bars[Q1_WARPS][2];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int grp = lane >> 3, l8 = lane & 7;
   // stage b of this warp: g at qsm + (2 warp + b) 4096 bytes, e 2048 bytes after it
-  auto stage_g = [&](int b) { return reinterpret_cast<float*>(qsm + (size_t)(warp * 2 + b) * 4096); };
+  auto stage_g = [&](int b) { return reinterpret_cast<float*>(qsm + (size_t)(warp * Q1_STAGES + b) * 4096); };
   // Work hand-out: the quads are split into QP_NPART contiguous parts, each with its own
   // ticket counter (one hot address would serialise ~50K atomics in one L2 slice);
   // a warp starts on part (global warp id mod QP_NPART) and moves on when its part is
   // exhausted.  Grabs are split: lane 0 issues the atomic, the broadcast (which waits
   // for it) happens one quad later, so the atomic's latency hides behind a quad.
-  const int gw = blockIdx.x * QP_WARPS + warp;
+  const int gw = blockIdx.x * Q1_WARPS + warp;
   int part = gw % QP_NPART;
   auto plo = [&](int p) -> int { return (int)(((int64_t)nqc * p) / QP_NPART); };
   auto grab_issue = [&]() -> unsigned {
@@ -553,7 +560,7 @@ k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const QIn
     return q;
   };
   auto finish = [&]() {  // after this warp found every part exhausted
-    if (lane == 0 && atomicAdd(&ticket[QP_NPART * 64], 1u) == gridDim.x * QP_WARPS - 1u) {
+    if (lane == 0 && atomicAdd(&ticket[QP_NPART * 64], 1u) == gridDim.x * Q1_WARPS - 1u) {
       for (int p2 = 0; p2 <= QP_NPART; ++p2) atomicExch(&ticket[p2 * 64], 0u);
     }
   };
@@ -561,7 +568,7 @@ k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const QIn
   // lane 0 with cp.async (one commit group per descriptor), so no register holds a
   // descriptor load in flight across the compute (that pushed K1 past its register
   // budget: a spill store that waited on the load every quad).
-  __shared__ __align__(16) QInfo qis[QP_WARPS][3];
+  __shared__ __align__(16) QInfo qis[Q1_WARPS][3];
   auto info_async = [&](int ci, int slot) {
     if (lane == 0) {
       if (ci < nqc)
@@ -588,7 +595,7 @@ k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const QIn
   const bool pal = ptr_aligned != 0;
   const uint32_t tx = e ? 4096u : 2048u;
   const uint32_t a_bar = sm_addr(&bars[warp][0]);                      // stage b: + 8 b
-  const uint32_t a_stage = sm_addr(qsm + (size_t)warp * 2 * 4096);     // stage b: + 4096 b
+  const uint32_t a_stage = sm_addr(qsm + (size_t)warp * Q1_STAGES * 4096);  // stage b: + 4096 b
   float gs = 1.f, gs2 = 1.f;  // s of candidates l8 and l8 + 8 (select chain: no local copy of cs)
 #pragma unroll
   for (int j = 0; j < KT; ++j) {
@@ -635,7 +642,9 @@ k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const QIn
       // the previous iteration; __syncwarp orders those reads before the copy)
       info_wait1();  // nA's descriptor (and c's) landed; also orders the stage reads
       const int ra = (r == 2) ? 0 : r + 1;
-      const bool next_inflight = (nA < nqc) ? issue(qis[warp][ra], b ^ 1) : false;
+      // two stages: prefetch quad nA into the other stage now; one stage: after the
+      // current quad has been read into registers (below)
+      bool next_inflight = (Q1_STAGES == 2 && nA < nqc) ? issue(qis[warp][ra], b ^ 1) : false;
       const bool valid = grp * 128 < ic.nvalid;
       float x[16];
       if (cur_regular) {
@@ -673,6 +682,10 @@ k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const QIn
             x[4 * i + s2] = v;
           }
         }
+      }
+      if (Q1_STAGES == 1 && nA < nqc) {  // the stage's contents are in registers now
+        __syncwarp();
+        next_inflight = issue(qis[warp][ra], 0);
       }
       // (the +0 of canon() only turns -0 into +0, which changes no error: omitted here)
       float mn, mx;
@@ -747,7 +760,7 @@ k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const QIn
         for (int j = 0; j < KT; ++j) acc[j] = __dadd_rn(acc[j], __dmul_rn((double)a2[j], S2inv));
       }
       inflight = next_inflight;
-      b ^= 1;
+      if (Q1_STAGES == 2) b ^= 1;
     }
     // chunk done (KT > 8): fixed-order warp reduction into its slot
     if (KT > 8) {
@@ -1278,8 +1291,8 @@ cudaError_t launch_qprofile(const QProfileArgs& a, cudaStream_t st) {
   if (a.nchunks > 0) {
     if (a.ev0) cudaEventRecord(a.ev0, st);
     if (quads) {
-      const size_t smem = (size_t)QP_WARPS * 2 * 4096;
-      const int nsm = a.nqwarps / (QP_WARPS * 4);  // nqwarps = SMs x 4 CTAs x 8 warps (an upper bound)
+      const size_t smem = (size_t)Q1_WARPS * Q1_STAGES * 4096;
+      const int nsm = a.nqwarps / 32;  // nqwarps = SMs x 4 CTAs x 8 warps (an upper bound)
 #define LG_QQ(KT)                                                                                              \
   {                                                                                                            \
     static int occ = 0;                                                                                        \
@@ -1287,10 +1300,10 @@ cudaError_t launch_qprofile(const QProfileArgs& a, cudaStream_t st) {
       cudaError_t e = cudaFuncSetAttribute(k_qprofile_q<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
       if (e != cudaSuccess) return e;                                                                          \
     }                                                                                                          \
-    if (occ == 0 && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_qprofile_q<KT>, QP_THREADS, smem) != \
+    if (occ == 0 && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_qprofile_q<KT>, Q1_THREADS, smem) != \
                      cudaSuccess || occ < 1)) occ = 1;                                                          \
-    const int grid = std::max(1, std::min(a.nqwarps / QP_WARPS, nsm * occ));                                    \
-    const cudaError_t e2 = launch_pdl(k_qprofile_q<KT>, dim3(grid), dim3(QP_THREADS), smem, st, a.g, a.e,       \
+    const int grid = std::max(1, std::min(a.nqwarps / Q1_WARPS, nsm * occ));                                    \
+    const cudaError_t e2 = launch_pdl(k_qprofile_q<KT>, dim3(grid), dim3(Q1_THREADS), smem, st, a.g, a.e,       \
                                       a.qinfo, a.nqchunks, a.ticket, a.cs, a.K, philox_rk(a.k0, a.k1), a.rankfield, \
                                       a.step,                                                                    \
                                       a.ptr_aligned, a.partial);                                                 \
