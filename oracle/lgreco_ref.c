@@ -25,6 +25,7 @@
  * (KATs, closed forms, brute force, textbook identities); none is "parity unpinned".
  */
 #include <math.h>
+#include <float.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -123,10 +124,14 @@ int ref_quantize_bucket(const float* x, int32_t nvalid, int32_t bits, const floa
     if (!constant) {
         float range = mx - mn;
         if (isinf(range)) return REF_ENONFINITE;
+        /* inv = RD(s / range), the largest float <= s / range (R5): from the IEEE RN
+         * quotient, stepped down when it lies above (the float products are exact in
+         * double).  Then t * inv <= s for every t <= range, so q <= s. */
         float inv = s / range;
+        if (isfinite(inv) && (double)inv * (double)range > (double)s) inv = nextafterf(inv, 0.0f);
         unit = range / s;
-        if (!isfinite(inv)) {
-            constant = 1; /* near-subnormal range: treated as constant, unit kept */
+        if (!(inv < FLT_MAX)) {
+            constant = 1; /* near-subnormal range (s / range >= FLT_MAX): treated as constant, unit kept */
         } else {
             for (int i = 0; i < nvalid; i++) {
                 float t = x[i] - mn;

@@ -103,14 +103,18 @@ __device__ __forceinline__ void store_x4(float* __restrict__ dst, int64_t base, 
   }
 }
 
-// Per-bucket quantiser parameters for s = 2^b - 1 (R5): inv = fl(s/range),
-// unit = fl(range/s); constant (mx == mn) or !finite(inv) -> inv = 0 (q = 0).
+// Per-bucket quantiser parameters for s = 2^b - 1 (R5): inv = RD(s/range) (so t·inv <= s
+// for every t <= range: the code never exceeds s), unit = RN(range/s); constant
+// (mx == mn) or s/range >= FLT_MAX (inv = FLT_MAX) -> inv = 0 (q = 0).
 __device__ __forceinline__ void qparams(float mn, float mx, float s, float& inv, float& unit) {
   if (mx == mn) { inv = 0.f; unit = 0.f; return; }
   const float range = __fsub_rn(mx, mn);
+  // RD from the RN quotient (div.rd is a slow path): step down one ulp when inv·range > s;
+  // the FMA's sign is exact (the residual is far above the subnormal range)
   inv = __fdiv_rn(s, range);
+  if (__fmaf_rn(inv, range, -s) > 0.f) inv = __int_as_float(__float_as_int(inv) - 1);
   unit = __fdiv_rn(range, s);
-  if (!isfinite(inv)) inv = 0.f;
+  if (!(inv < 3.40282347e+38f)) inv = 0.f;
 }
 
 // Stochastic rounding of t = x - mn (R6): q = min(floor(v) + [u < frac(v)], s) with
@@ -236,6 +240,7 @@ __device__ __forceinline__ void prof_cand16x2(const float* x, float mn, uint32_t
 #pragma unroll
       for (int p = 0; p < 2; ++p) {
         const f2_t w = f2fma_rp(tp[p], f2pk(inv[j], inv[j]), nu[p]);
+        // no clamp: inv = RD(s/range) makes t·inv - u <= s, so ceil <= s (R5)
         float q0, q1;
         if (j >= KT - QP_XU_CEIL) {
           float w0, w1;
@@ -245,8 +250,6 @@ __device__ __forceinline__ void prof_cand16x2(const float* x, float mn, uint32_t
         } else {
           f2up(f2add(f2add_rp(w, f2pk(MAGIC, MAGIC)), f2pk(-MAGIC, -MAGIC)), q0, q1);
         }
-        q0 = fminf(q0, cs.s[j]);
-        q1 = fminf(q1, cs.s[j]);
         f2_t d = f2add(xp[p], f2fma(f2pk(q0, q1), f2pk(-unit[j], -unit[j]), nmn));
         if (SCALED) d = f2mul(d, f2pk(S, S));
         a2[j] = f2fma(d, d, a2[j]);

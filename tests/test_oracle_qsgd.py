@@ -124,7 +124,8 @@ def test_unbiased_and_closed_form_mse(ref, bits):
     assert z.max() < 5.0  # 128 simultaneous comparisons
     # closed form of the per-element MSE
     s = 2 ** bits - 1
-    inv = np.float32(s) / np.float32(x.max() - x.min())
+    from fractions import Fraction as F
+    inv = _rd32(F(s) / F(float(np.float32(x.max() - x.min()))))  # R5: RD(s / range)
     v = (x - x.min()).astype(np.float32).astype(np.float64) * np.float64(inv)  # exact (R6)
     f = v - np.floor(v)
     mse_cf = (unit ** 2 * f * (1 - f)).sum()
@@ -142,11 +143,22 @@ def _rn32(r):
     return ties[0] if len(ties) == 1 else [v for v in ties if (v.view(np.uint32) & 1) == 0][0]
 
 
+def _rd32(r):
+    """Round a positive Fraction down to a float32 (the largest float32 <= r)."""
+    from fractions import Fraction as F
+    c = np.float32(float(r))
+    while F(float(c)) > r:
+        c = np.nextafter(c, np.float32(0))
+    while np.isfinite(np.nextafter(c, np.float32(np.inf))) and F(float(np.nextafter(c, np.float32(np.inf)))) <= r:
+        c = np.nextafter(c, np.float32(np.inf))
+    return c
+
+
 def test_code_is_exact_rational_rounding(ref):
     """R6 against exact rational arithmetic (fractions.Fraction, not the oracle's
-    doubles): q = min(floor(v) + [u < frac(v)], s) with v = fl(x - mn) * fl(s / range)
-    taken exactly, dec = fl(fma(q, unit, mn)).  Inputs are chosen so that u lands on,
-    just below and just above frac(v), and v exceeds s at the maximum."""
+    doubles): q = floor(v) + [u < frac(v)] with v = fl(x - mn) * RD(s / range) taken
+    exactly (v <= s: no clamp), dec = fl(fma(q, unit, mn)).  Inputs are chosen so that u
+    lands on, just below and just above frac(v)."""
     from fractions import Fraction as F
     rng = np.random.default_rng(11)
     for trial in range(40):
@@ -155,9 +167,10 @@ def test_code_is_exact_rational_rounding(ref):
         x = rng.standard_normal(128).astype(np.float32) * np.float32(10.0 ** rng.integers(-6, 4))
         mn, mx = np.float32(x.min()), np.float32(x.max())
         rngv = np.float32(mx - mn)
-        inv = np.float32(np.float32(s) / rngv)
+        inv = _rd32(F(s) / F(float(rngv)))  # R5: the largest float <= s / range
         t = (x - mn).astype(np.float32)
         vq = [F(float(ti)) * F(float(inv)) for ti in t]
+        assert max(vq) <= s  # so the code never needs the clamp
         fr = [v - (v.numerator // v.denominator) for v in vq]
         u = rng.random(128).astype(np.float32)
         for i in range(0, 128, 3):  # u at frac(v) rounded to float and its neighbours
