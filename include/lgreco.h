@@ -120,6 +120,15 @@ int lgreco_ctx_timing(lgreco_ctx* ctx, int32_t enable);
  * event failed (the sum then covers the others). */
 int lgreco_ctx_kernel_ms(lgreco_ctx* ctx, double* total_ms, int64_t* count);
 
+/* (a1) Paper-mode accumulation ("we accumulate per-layer gradients in
+ * auxiliary buffers", :318): d_G[i] = fl32(d_G[i] + d_g[i]) for i < n, one IEEE fp32
+ * round-to-nearest add per element, enqueued on `stream` (kernel K0).  Between replans the
+ * caller accumulates every step's local gradient into G and profiles G with d_ef = NULL.
+ * d_G (in/out) and d_g are DEVICE pointers, 4-byte aligned (128-bit path when both share
+ * their alignment mod 16); n = 0 is a no-op.  LGRECO_EINVAL on a negative n, null or
+ * misaligned pointers; LGRECO_ECUDA if the launch fails. */
+int lgreco_accumulate(float* d_G, const float* d_g, int64_t n, void* stream);
+
 /* (a2-a4) Profile: for every layer l and candidate j, d_err[l*K+j] = the L2 norm of
  * x_l - decompress(compress(x_l, c^j)) and d_bits[l*K+j] = its transmitted size in
  * bits ("simulate the compression/decompression ... without
@@ -273,6 +282,14 @@ int lgreco_topk_combine(lgreco_ctx* ctx, const int32_t* h_choice, int32_t W, con
  * largest candidate rank: P slots hold m x r (column-major) per compressed matrix
  * layer, Q slots k x r; lgreco_psgd_sizes returns the slot-area sizes (elements). */
 int lgreco_psgd_sizes(lgreco_ctx* ctx, int64_t* h_p_elems, int64_t* h_q_elems);
+/* The ctx's current PowerSGD factors (R12), for inspection / parity tests: d_Phat (P elems)
+ * <- Phat = orthonormalise(Psum / W) of the last lgreco_psgd_q (or compress) call, d_Q
+ * (Q elems) <- the warm-start Q = Qsum / W of the last lgreco_psgd_out (or compress) call.
+ * Slot layout: compressed matrix layers in layer order, each owning rows*rmax (P) and
+ * cols*rmax (Q) elements, rmax = the largest candidate rank that is not lossless for the
+ * layer (0: none); the current rank-r factor is stored column-major (m x r, k x r) at the
+ * slot start.  Either pointer nullable.  Enqueued on `stream`. */
+int lgreco_psgd_factors(lgreco_ctx* ctx, float* d_Phat, float* d_Q, void* stream);
 /* P_w = M_w Q_ws (Q_ws re-initialised from Philox stream 2 at `step` where the rank
  * changed) into d_P. */
 int lgreco_psgd_p(lgreco_ctx* ctx, const int32_t* h_choice, const float* d_g, const float* d_ef, float* d_P,

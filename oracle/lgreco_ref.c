@@ -104,6 +104,17 @@ static float canon_x(float g, const float* e, int64_t i) {
 }
 
 /* ------------------------------------------------------------------------ */
+/* Paper-mode accumulation (row a1): "we accumulate per-layer    */
+/* gradients in auxiliary buffers"; G <- G + g, one fp32 add per element.     */
+/* ------------------------------------------------------------------------ */
+void ref_accumulate(float* G, const float* g, int64_t n) {
+    for (int64_t i = 0; i < n; i++) {
+        volatile float s = G[i] + g[i];
+        G[i] = s;
+    }
+}
+
+/* ------------------------------------------------------------------------ */
 /* QSGD-style bucketed min/max stochastic quantiser (R5, R6).                */
 /* ------------------------------------------------------------------------ */
 /* Quantise one bucket of nvalid values with `bits` bits using the uniforms u.
@@ -642,14 +653,19 @@ static void mat_mq(const double* M, int64_t m, int64_t k, int32_t r, const doubl
             P[j * m + i] = s;
         }
 }
-/* Q = M^T P */
+/* Q = M^T P: Q[j][c] = sum over i = 0, 1, ..., m-1 (in that order) of M[i][c] P[j][i].
+ * The loops run i outside c so M is read row by row; every Q[j][c] still accumulates its
+ * terms in ascending i from 0.0, so the result is the plain dot product's, bit for bit. */
 static void mat_mtp(const double* M, int64_t m, int64_t k, int32_t r, const double* P, double* Q) {
-    for (int j = 0; j < r; j++)
-        for (int64_t c = 0; c < k; c++) {
-            double s = 0.0;
-            for (int64_t i = 0; i < m; i++) s += M[i * k + c] * P[j * m + i];
-            Q[j * k + c] = s;
+    for (int j = 0; j < r; j++) {
+        double* q = Q + (int64_t)j * k;
+        for (int64_t c = 0; c < k; c++) q[c] = 0.0;
+        for (int64_t i = 0; i < m; i++) {
+            const double pji = P[j * m + i];
+            const double* row = M + i * k;
+            for (int64_t c = 0; c < k; c++) q[c] += row[c] * pji;
         }
+    }
 }
 /* Modified Gram-Schmidt with one reorthogonalisation sweep ("twice is enough") on
  * the columns of P (in place).  A column whose norm after the projections is <= 1e-12

@@ -92,6 +92,14 @@ def bucket_uniforms(seed, rankfield, step, stream, gb, B, nvalid):
     return u
 
 
+# ------------------------------------------------------------- accumulation
+def accumulate(G, g):
+    """Row a1: returns a copy of G with g added (fp32, one add each)."""
+    out = _f32(G).copy()
+    lib().ref_accumulate(_p(out), _p(_f32(g)), C.c_int64(out.size))
+    return out
+
+
 # ----------------------------------------------------------------- quantiser
 def quantize_bucket(x, bits, u):
     x = _f32(x)

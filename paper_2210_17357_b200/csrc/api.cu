@@ -742,6 +742,11 @@ int lgreco_psgd_sizes(lgreco_ctx* c, int64_t* h_p_elems, int64_t* h_q_elems) {
   return LGRECO_OK;
 }
 
+int lgreco_psgd_factors(lgreco_ctx* c, float* d_Phat, float* d_Q, void* stream) {
+  if (!c || c->family != LGRECO_POWERSGD) { lg_set_error("psgd_factors: not a PowerSGD ctx"); return LGRECO_EINVAL; }
+  return psgd_factors(c, d_Phat, d_Q, (cudaStream_t)stream);
+}
+
 int lgreco_psgd_p(lgreco_ctx* c, const int32_t* h_choice, const float* d_g, const float* d_ef, float* d_P,
                   uint64_t step, void* stream) {
   if (!c || !h_choice || !d_g || !d_P || c->family != LGRECO_POWERSGD) return LGRECO_EINVAL;

@@ -442,6 +442,15 @@ int psgd_compress_allreduce(lgreco_ctx* c, const int32_t* choice, const float* g
 float* psgd_internal_P(lgreco_ctx* c) { return c->ps ? c->ps->P : nullptr; }
 int64_t psgd_sizes(lgreco_ctx* c, int which) { return !c->ps ? 0 : which == 0 ? c->ps->Psz : c->ps->Qsz; }
 
+// The ctx's current factors: Phat (orthonormalised mean P of the last stage 2) and the
+// warm-start Q (the mean Q of the last stage 3), in the P / Q slot layout.
+int psgd_factors(lgreco_ctx* c, float* d_Phat, float* d_Q, cudaStream_t st) {
+  Psgd* p = c->ps;
+  if (d_Phat && p->Psz) LG_CUDA(cudaMemcpyAsync(d_Phat, p->Ph, sizeof(float) * p->Psz, cudaMemcpyDeviceToDevice, st));
+  if (d_Q && p->Qsz) LG_CUDA(cudaMemcpyAsync(d_Q, p->Qws, sizeof(float) * p->Qsz, cudaMemcpyDeviceToDevice, st));
+  return LGRECO_OK;
+}
+
 // Debug / unit-test entry: P = M Q on the tcgen05 path for one matrix (M = canon(g + e),
 // m x k row-major; Q k x r column-major; P m x r column-major).  Allocates its tiny
 // descriptor arrays (debug only).

@@ -126,6 +126,7 @@ int psgd_raw_combine(lgreco_ctx* c, const int32_t* choice, int W, const uint8_t*
 int psgd_compress_allreduce(lgreco_ctx* c, const int32_t* choice, const float* g, float* ef, float* out,
                             uint64_t step, cudaStream_t st);
 int64_t psgd_sizes(lgreco_ctx* c, int which);
+int psgd_factors(lgreco_ctx* c, float* d_Phat, float* d_Q, cudaStream_t st);
 void svd_destroy(lgreco_ctx* c);
 
 

@@ -751,33 +751,168 @@ __device__ __forceinline__ void cl_st(uint32_t addr, uint64_t v) {
   asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
 }
 
+// Facts of the cluster prelude that k_solve_join needs (written by group 0's rank 0).
+struct JoinMeta {
+  int done;  // 1: the row kernel already wrote info (bad table / no active layer)
+  int h;     // the split: bottom group = active layers [0, h), top group = [h, La)
+  int La, cm;
+  int64_t PDR;
+  double emax;
+  int64_t defbits;
+};
+
+// PD byte of (layer a, cell e): cell-major rows of PDR bytes, in L2 (written by the
+// row kernel: __ldcg)
+__device__ __forceinline__ int pd_cm(const uint8_t* PD, int64_t PDR, int a, int e) {
+  return __ldcg(PD + (int64_t)a * PDR + e);
+}
+
+// Backtrack (Alg.1 lines 24-27) of the active layers a_hi, a_hi - 1, ..., a_lo from cell e
+// by one warp: bch[a] = PD(a, e) & cm, e -= disc[a][bch[a]].  Speculative: one PD round
+// trip resolves up to three layers (entry 0 = PD(a, e); entry 1 + c1 = PD(a - 1, e -
+// disc[a][c1]); entry 1 + K + c1 K + c2 = PD(a - 2, e - disc[a][c1] - disc[a-1][c2]); two
+// entries per lane); the disc rows are loaded before e is known.  bdisc: [La][K].
+__device__ __noinline__ void bt_warp(const uint8_t* __restrict__ PD, int64_t PDR, const int32_t* bdisc, int K, int cm,
+                                     int a_hi, int a_lo, int e, int32_t* bch) {
+  const int lane = threadIdx.x & 31;
+  auto put = [&](int a, int c) {
+    if (lane == 0) bch[a] = c;
+  };
+  const int depth = (K < 32 && 1 + K + K * K <= 64) ? 3 : ((K < 32) ? 2 : 1);
+  int lev[2], c1s[2], c2s[2];
+#pragma unroll
+  for (int r = 0; r < 2; ++r) {
+    const int j = lane + 32 * r;
+    lev[r] = -1; c1s[r] = 0; c2s[r] = 0;
+    if (j == 0) lev[r] = 0;
+    else if (depth >= 2 && j <= K) { lev[r] = 1; c1s[r] = j - 1; }
+    else if (depth >= 3 && j < 1 + K + K * K) { lev[r] = 2; c1s[r] = (j - 1 - K) / K; c2s[r] = (j - 1 - K) % K; }
+  }
+  int a = a_hi;
+  auto disc_rows = [&](int ar, int& da, int& db, int& dc, int* off) {
+    da = (lane < K) ? bdisc[ar * K + lane] : 0;
+    db = (lane < K) ? bdisc[(ar - 1) * K + lane] : 0;
+    dc = (lane < K && depth >= 3) ? bdisc[(ar - 2) * K + lane] : 0;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int d1 = __shfl_sync(LG_FULL, da, c1s[r]);
+      const int d2 = __shfl_sync(LG_FULL, db, c2s[r]);
+      off[r] = (lev[r] == 0) ? 0 : (lev[r] == 1) ? ((d1 >= 0) ? d1 : -1)
+             : (lev[r] == 2) ? ((d1 >= 0 && d2 >= 0) ? d1 + d2 : -1) : -1;
+    }
+  };
+  if (depth > 1 && a - (depth - 1) >= a_lo) {
+    int da, db, dc, off[2];
+    disc_rows(a, da, db, dc, off);
+    for (;;) {
+      int v[2];
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        v[r] = 0;
+        if (off[r] >= 0 && e - off[r] >= 0) v[r] = pd_cm(PD, PDR, a - lev[r], e - off[r]);
+      }
+      const int an = a - depth;
+      int nda = 0, ndb = 0, ndc = 0, noff[2] = {-1, -1};
+      if (an - (depth - 1) >= a_lo) disc_rows(an, nda, ndb, ndc, noff);
+      auto val = [&](int j) {
+        const int x0 = __shfl_sync(LG_FULL, v[0], j & 31), x1 = __shfl_sync(LG_FULL, v[1], j & 31);
+        return (j < 32 ? x0 : x1) & cm;
+      };
+      const int c0 = val(0);
+      const int c1 = val(1 + c0);
+      put(a, c0);
+      put(a - 1, c1);
+      int de = __shfl_sync(LG_FULL, da, c0) + __shfl_sync(LG_FULL, db, c1);
+      if (depth >= 3) {
+        const int c2 = val(1 + K + c0 * K + c1);
+        put(a - 2, c2);
+        de += __shfl_sync(LG_FULL, dc, c2);
+      }
+      e -= de;
+      a = an;
+      if (a - (depth - 1) < a_lo) break;
+      da = nda; db = ndb; dc = ndc; off[0] = noff[0]; off[1] = noff[1];
+    }
+  }
+  for (; a >= a_lo; --a) {
+    const int c = pd_cm(PD, PDR, a, e) & cm;
+    put(a, c);
+    e -= bdisc[a * K + c];
+  }
+  __syncwarp();
+}
+
+// R20 check and summary (whole CTA): choice[act[a]] = bch[a] (or the defaults when
+// used_default), the plan's bits and raw error summed in layer order; the defaults are
+// returned instead when the plan is not within the default bits and Emax.  sm_ce:
+// 16 * La bytes of shared scratch; s_flag: a shared int.
+__device__ __noinline__ void finish_plan(int used_default, const int32_t* bch, int La, const int32_t* __restrict__ act,
+                                         const int32_t* __restrict__ default_idx, const double* __restrict__ err,
+                                         const int64_t* __restrict__ bits, int K, uint32_t flags, double emax,
+                                         int64_t defbits, int32_t* __restrict__ choice,
+                                         lgreco_solve_info* __restrict__ info, double* sm_ce, int* s_flag) {
+  const int tid = threadIdx.x, NT = blockDim.x;
+  if (!used_default)
+    for (int a = tid; a < La; a += NT) choice[act[a]] = bch[a];
+  __syncthreads();
+  int64_t* sm_cb = reinterpret_cast<int64_t*>(sm_ce + La);
+  if (used_default) {
+    for (int a = tid; a < La; a += NT) choice[act[a]] = default_idx[act[a]];
+    __syncthreads();
+  }
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int a = tid; a < La; a += NT) {
+      const int l = act[a];
+      const int c = used_default ? default_idx[l] : bch[a];
+      sm_ce[a] = metric(err[(int64_t)l * K + c], flags);
+      sm_cb[a] = bits[(int64_t)l * K + c];
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int64_t pb = 0;
+      double pe = 0.0;
+      int a = 0;
+      for (; a + 4 <= La; a += 4) {
+        const double v0 = sm_ce[a], v1 = sm_ce[a + 1], v2 = sm_ce[a + 2], v3 = sm_ce[a + 3];
+        pb += sm_cb[a] + sm_cb[a + 1] + sm_cb[a + 2] + sm_cb[a + 3];
+        pe = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(pe, v0), v1), v2), v3);
+      }
+      for (; a < La; ++a) { pb += sm_cb[a]; pe = __dadd_rn(pe, sm_ce[a]); }
+      if (!used_default && (pb > defbits || pe > emax)) {
+        *s_flag = 1;
+      } else {
+        lgreco_solve_info inf = {};
+        inf.emax = emax;
+        inf.total_err = pe;
+        inf.total_bits = pb;
+        inf.default_bits = defbits;
+        inf.used_default = used_default;
+        inf.n_active = La;
+        inf.status = LGRECO_OK;
+        *info = inf;
+        *s_flag = -1;
+      }
+    }
+    __syncthreads();
+    if (*s_flag < 0) break;
+    used_default = 1;
+    for (int a = tid; a < La; a += NT) choice[act[a]] = default_idx[act[a]];
+    __syncthreads();
+  }
+}
+
 #ifndef QP_DP_CPT0
 #define QP_DP_CPT0 2  // smallest cells-per-thread of the cluster solve (more warps below that)
 #endif
 constexpr int CL_MAX = 16;  // CTAs per cluster (16: non-portable size; 8 is the portable maximum)
 
-template <int CPT>
-__device__ __forceinline__ void pd_store(uint8_t* dst, const uint32_t* w) {
-  if (CPT == 1) *dst = (uint8_t)w[0];
-  else if (CPT == 2) *reinterpret_cast<uint16_t*>(dst) = (uint16_t)w[0];
-  else if (CPT == 4) *reinterpret_cast<uint32_t*>(dst) = w[0];
-  else if (CPT == 8) *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1]);
-  else *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
-}
-
-#ifndef DP_PD_CELLMAJOR
-#define DP_PD_CELLMAJOR 1
-#endif
-#ifndef DP_SUM_BCH
-#define DP_SUM_BCH 1
-#endif
 template <int CPT, int KT>
 __global__ void __launch_bounds__(DP_THREADS, 1)
 k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int L, int K,
            const int32_t* __restrict__ default_idx, const int32_t* __restrict__ compress, int D, uint32_t flags,
            int32_t* __restrict__ choice, lgreco_solve_info* __restrict__ info, uint8_t* __restrict__ PD,
            int32_t* __restrict__ act, int32_t* __restrict__ wdisc, uint64_t* __restrict__ wadd,
-           int32_t* __restrict__ wmaxd) {
+           int32_t* __restrict__ wmaxd, int ngroups, uint64_t* __restrict__ rowout, JoinMeta* __restrict__ jmeta) {
   static_assert(KT >= 0 && KT <= 16 && (CPT == 1 || CPT == 2 || CPT == 4 || CPT == 8 || CPT == 16), "cluster DP");
   // KT > 0: K <= KT candidates, tables of the whole recursion in shared memory;
   // KT == 0: K <= 256 candidates in groups of 16 (k_solve_fast's grouped keys), tables
@@ -793,7 +928,10 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
   __shared__ int s_cle[CL_MAX];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int NT = blockDim.x, NW = NT >> 5;
-  const uint32_t rank = cl_rank(), NC = gridDim.x;
+  // ngroups == 2: two clusters, each running the row recursion of one half of the active
+  // layers from the zero row; k_solve_join combines them (see "Layer groups" below)
+  const uint32_t rank = cl_rank(), NC = gridDim.x / ngroups;
+  const int grp = (ngroups > 1) ? (int)(blockIdx.x / NC) : 0;
   const int S = NW * 32 * CPT;     // cells per CTA
   const int cbase = (int)rank * S; // first cell of this CTA
 #ifdef LG_DP_TIMING
@@ -829,7 +967,7 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
     const int f = compress ? (compress[l] != 0) : 1;
     const int d = default_idx[l];
     sm_flag[l] = f;
-    if (rank == 0) choice[l] = -1;
+    if (rank == 0 && grp == 0) choice[l] = -1;
     if (f) {
       if (d < 0 || d >= K) { bad_def = 1; sm_de[l] = 0.0; }
       else { sm_de[l] = metric(t_err[(int64_t)l * K + d], flags); db_part += t_bits[(int64_t)l * K + d]; }
@@ -850,7 +988,7 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
       if (f) {
         const int pos = La + __popc(m & ((1u << lane) - 1u));
         sm_act[pos] = l;
-        if (rank == 0) act[pos] = l;
+        if (rank == 0 && grp == 0) act[pos] = l;
         sm_dea[pos] = sm_de[l];
       }
       La += __popc(m);
@@ -954,11 +1092,12 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
   const int gsh = __ffsll((long long)g) - 1;
   const int cbits = s_cbits;
   if (s_status != LGRECO_OK || La == 0) {  // identical in every CTA: no cluster barrier is pending
-    if (rank == 0 && tid == 0) {
+    if (rank == 0 && tid == 0 && grp == 0) {
       lgreco_solve_info inf = {};
       inf.n_active = La;
       inf.status = s_status;
       *info = inf;
+      if (ngroups > 1) jmeta->done = 1;  // k_solve_join has nothing to do
     }
     return;
   }
@@ -992,18 +1131,57 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
   }
   __syncthreads();  // the prelude's shared staging (front of smem) is dead from here
   LG_T(9);
+  // Layer groups (ngroups == 2): the active layers split into a bottom group [0, h) and a
+  // top group [h, La) of about equal estimated row cost (a row costs a fixed ~1 K cycles
+  // plus its DSMEM pushes, ~maxd / 5 cycles); every CTA computes the same h.
+  __shared__ int s_a0, s_a1;
+  if (warp == 0) {
+    int a0 = 0, a1 = La;
+    if (ngroups > 1) {
+      long long tot = 0;
+      for (int base = 0; base < La; base += 32) {
+        const int aa = base + lane;
+        long long w = (aa < La) ? 1024 + my_wmaxd[aa] / 5 : 0;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) w += __shfl_xor_sync(LG_FULL, w, o);
+        tot += w;
+      }
+      const long long half = (tot + 1) / 2;
+      long long run = 0;
+      int h = La;
+      for (int base = 0; base < La; base += 32) {
+        const int aa = base + lane;
+        long long w = (aa < La) ? 1024 + my_wmaxd[aa] / 5 : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const long long t = __shfl_up_sync(LG_FULL, w, o);
+          if (lane >= o) w += t;
+        }
+        const unsigned m = __ballot_sync(LG_FULL, aa < La && run + w >= half);
+        if (m) { h = base + __ffs(m) - 1 + 1; break; }
+        run += __shfl_sync(LG_FULL, w, 31);
+      }
+      h = min(max(h, La > 1 ? 1 : 0), La > 1 ? La - 1 : La);
+      a0 = grp ? h : 0;
+      a1 = grp ? La : h;
+      if (grp == 0 && rank == 0 && lane == 0) jmeta->h = h;
+    }
+    if (lane == 0) { s_a0 = a0; s_a1 = a1; }
+  }
+  __syncthreads();
+  const int a0 = s_a0, a1 = s_a1;
   // bands: running sums of the smallest / largest admissible disc (exact reachable
-  // set bounds).  Warp 0 scans the layers 32 at a time; a layer with no admissible
-  // candidate empties every later band (lo = INF).
+  // set bounds) over this group's layers, from the zero row.  Warp 0 scans the layers
+  // 32 at a time; a layer with no admissible candidate empties every later band.
   if (warp == 0) {
     long long slo = 0;
     int shi = 0;
     bool dead = false;
-    for (int base = 0; base < La; base += 32) {
+    for (int base = a0; base < a1; base += 32) {
       const int aa = base + lane;
       int mn = 0, mxd = 0;
       bool any = true;
-      if (aa < La) {
+      if (aa < a1) {
         int m1 = 0x7fffffff, m2 = -1;
         for (int c = 0; c < K; ++c) {
           const int d = my_wdisc[aa * K + c];
@@ -1023,7 +1201,7 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
         if (lane >= o) { plo += t1; phi = min(phi + t2, D); }
       }
       const bool dead_here = dead || (dead_m & ((2u << lane) - 1u)) != 0;
-      if (aa < La) {
+      if (aa < a1) {
         const long long lo_v = slo + plo;
         band_all[aa] = make_int2(dead_here ? 0x3fffffff : (int)min(lo_v, 0x3fffffffll), min(shi + phi, D));
       }
@@ -1056,7 +1234,7 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
       s_ak[slot][tid] = ok ? k : INF64;
     }
   };
-  if (KT == 0) stage0((tid < K) ? my_wdisc[tid] : -1, (tid < K) ? my_wadd[tid] : 0, 0);
+  if (KT == 0 && a0 < a1) stage0((tid < K) ? my_wdisc[a0 * K + tid] : -1, (tid < K) ? my_wadd[a0 * K + tid] : 0, 0);
   LG_T(1);
   cl_sync();  // every CTA's rows and barriers initialised before any remote push lands
   if (!wide) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");  // "row -1 done"
@@ -1074,18 +1252,18 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
   const int wbase = cbase + warp * (32 * CPT);
   const int dclamp = wbase + PAD;
   const int64_t PDR = (int64_t)NC * NT * CPT;  // PD bytes per layer
-  const int gtid = (int)rank * NT + tid;
   const uint32_t vb = wide ? 8u : 4u;
   // row a's candidate pairs, band and max shift, loaded during row a-1 (off the
   // critical path of the row)
   uint4 cq[KP2 / 2];
 #pragma unroll
-  for (int c = 0; c < KP2 / 2; ++c) cq[c] = (KT > 0) ? reinterpret_cast<const uint4*>(cand_all)[c] : make_uint4(0, 0, 0, 0);
-  int2 band = band_all[0];
-  int maxd = my_wmaxd[1];
-  for (int a = 0; a < La; ++a) {
+  for (int c = 0; c < KP2 / 2; ++c)
+    cq[c] = (KT > 0 && a0 < a1) ? reinterpret_cast<const uint4*>(cand_all + (size_t)a0 * KP2)[c] : make_uint4(0, 0, 0, 0);
+  int2 band = (a0 < a1) ? band_all[a0] : make_int2(0, 0);
+  int maxd = (a0 + 1 < a1) ? my_wmaxd[a0 + 1] : 0;  // the next row's largest shift (0: no next row)
+  for (int a = a0; a < a1; ++a) {
     const int sb = bc;     // barrier of row a's buffer
-    const int sk = a & 1;  // KT == 0 candidate staging slot of row a
+    const int sk = (a - a0) & 1;  // KT == 0 candidate staging slot of row a
     // cells of row a this CTA receives: [cbase - maxd, cbase) (clipped at 0)
     if (tid == 0) {
       const uint32_t bytes = (uint32_t)min(maxd, cbase) * vb;
@@ -1100,7 +1278,7 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
     const uint2* cnd = cand_all + (size_t)a * KP2;
     int32_t nd = -1;  // KT == 0: next layer's candidate tid, staged after this row
     uint64_t nub = 0;
-    if (KT == 0 && tid < K && a + 1 < La) { nd = my_wdisc[(a + 1) * K + tid]; nub = my_wadd[(a + 1) * K + tid]; }
+    if (KT == 0 && tid < K && a + 1 < a1) { nd = my_wdisc[(a + 1) * K + tid]; nub = my_wadd[(a + 1) * K + tid]; }
     uint32_t pdw[4] = {0u, 0u, 0u, 0u};
     const bool live = (wbase + 32 * CPT - 1 >= band.x) && (wbase <= band.y);
     // highest CTA that reads any cell of this warp in the next row
@@ -1213,13 +1391,13 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
     }
     bp = bc;
     bc = (bc + 1 == NB) ? 0 : bc + 1;
-    if (KT == 0 && a + 1 < La) stage0(nd, nub, sk ^ 1);  // slot last read in row a-1
-    if (a + 1 < La) {
+    if (KT == 0 && a + 1 < a1) stage0(nd, nub, sk ^ 1);  // slot last read in row a-1
+    if (a + 1 < a1) {
       const uint4* nq = reinterpret_cast<const uint4*>(cand_all + (size_t)(a + 1) * KP2);
 #pragma unroll
       for (int c = 0; c < KP2 / 2; ++c) if (KT > 0) cq[c] = nq[c];
       band = band_all[a + 1];
-      maxd = my_wmaxd[a + 2];
+      maxd = (a + 2 < a1) ? my_wmaxd[a + 2] : 0;
     }
 #ifdef LG_DP_TIMING
     const long long tp0 = clock64();
@@ -1237,15 +1415,11 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
       asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // every CTA finished row a-1
     }
     asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-#if DP_PD_CELLMAJOR
     if (live) {  // cell-major PD row (byte of cell e at a * PDR + e): 32 B per warp store
       uint8_t* dst = PD + (int64_t)a * PDR + cbase + warp * 32 * CPT + lane;
 #pragma unroll
       for (int i = 0; i < CPT; ++i) __stcg(dst + 32 * i, (uint8_t)(pdw[i >> 2] >> (8 * (i & 3))));
     }
-#else
-    if (live) pd_store<CPT>(PD + (int64_t)a * PDR + (int64_t)gtid * CPT, pdw);
-#endif
     if (NB == 2) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
 #ifdef LG_DP_TIMING
     t_cl += clock64() - ts1;
@@ -1269,6 +1443,38 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
   }
   if (!wide) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // pairs the last arrive
   LG_T(3);
+  if (ngroups > 1) {
+    // this group's last row (values in units of 2^gsh bits; ~0 = unreachable) for
+    // k_solve_join, and (group 0, rank 0) the shared facts of the prelude
+    uint64_t* ro = rowout + (size_t)grp * (D + 1);
+    for (int el = tid; el < S; el += NT) {
+      const int e = cbase + el;
+      if (e > D) break;
+      uint64_t v;
+      if (!wide) { const uint32_t x = (r32a + (size_t)bp * row + PAD)[e]; v = (x >= INF32) ? ~0ull : (x >> kb); }
+      else { const uint64_t x = (r64a + (size_t)bp * row + PAD)[e]; v = (x >= INF64) ? ~0ull : (x >> kb); }
+      ro[e] = v;
+    }
+    if (grp == 0 && rank == 0) {
+      if (KT > 0)
+        for (int i = tid; i < La * K; i += NT) wdisc[i] = my_wdisc[i];
+      if (tid == 0) {
+        jmeta->done = 0;
+        jmeta->La = La;
+        jmeta->cm = pdmask;
+        jmeta->PDR = PDR;
+        jmeta->emax = emax;
+        jmeta->defbits = s_defbits;
+      }
+    }
+#ifdef LG_DP_TIMING
+    if (rank == 0 && tid == 0)
+      printf("dp group %d: layers [%d, %d) of %d: prelude %lld init %lld rows %lld (%lld/layer)\n", grp, a0, a1, La,
+             tstamp[1] - tstamp[0], tstamp[2] - tstamp[1], tstamp[3] - tstamp[2],
+             (tstamp[3] - tstamp[2]) / (a1 > a0 ? a1 - a0 : 1));
+#endif
+    return;
+  }
   // ---- line 23: argmin of the last row over this CTA's cells, gathered in rank 0
   {
     uint64_t bk = ~0ull;
@@ -1311,17 +1517,6 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
   const int32_t* bdisc = my_wdisc;  // the discretised table (shared memory)
   int32_t* bch = reinterpret_cast<int32_t*>(smem_raw);  // [La] chosen c per active layer (rows are dead)
   __syncthreads();
-  // PD byte of (layer a, cell e): cell-major rows
-#if DP_PD_CELLMAJOR
-  auto pd_at = [&](int a, int e) -> int { return __ldcg(PD + (int64_t)a * PDR + e); };
-#else
-  auto pd_at = [&](int a, int e) -> int {
-    const int r = e / S, el = e - r * S;
-    const int w = el / (32 * CPT), rr = el - w * (32 * CPT);
-    const int T = r * NT + w * 32 + (rr & 31);
-    return __ldcg(PD + (int64_t)a * PDR + (int64_t)T * CPT + (rr >> 5));
-  };
-#endif
   if (warp == 0) {
     uint64_t k = (lane < (int)NC) ? s_clk[lane] : ~0ull;
     int ee = (lane < (int)NC) ? s_cle[lane] : 0x7fffffff;
@@ -1332,129 +1527,12 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
       if (ov < k || (ov == k && oe < ee)) { k = ov; ee = oe; }
     }
     const int used_default = (k == ~0ull);
-    const int cm = pdmask;
-    auto put = [&](int a, int c) {
-      if (lane == 0) bch[a] = c;
-    };
-    if (!used_default) {
-      const int depth = (K < 32 && 1 + K + K * K <= 64) ? 3 : ((K < 32) ? 2 : 1);
-      int lev[2], c1s[2], c2s[2];
-#pragma unroll
-      for (int r = 0; r < 2; ++r) {
-        const int j = lane + 32 * r;
-        lev[r] = -1; c1s[r] = 0; c2s[r] = 0;
-        if (j == 0) lev[r] = 0;
-        else if (depth >= 2 && j <= K) { lev[r] = 1; c1s[r] = j - 1; }
-        else if (depth >= 3 && j < 1 + K + K * K) { lev[r] = 2; c1s[r] = (j - 1 - K) / K; c2s[r] = (j - 1 - K) % K; }
-      }
-      int e = ee, a = La - 1;
-      auto disc_rows = [&](int ar, int& da, int& db, int& dc, int* off) {
-        da = (lane < K) ? bdisc[ar * K + lane] : 0;
-        db = (lane < K) ? bdisc[(ar - 1) * K + lane] : 0;
-        dc = (lane < K && depth >= 3) ? bdisc[(ar - 2) * K + lane] : 0;
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-          const int d1 = __shfl_sync(LG_FULL, da, c1s[r]);
-          const int d2 = __shfl_sync(LG_FULL, db, c2s[r]);
-          off[r] = (lev[r] == 0) ? 0 : (lev[r] == 1) ? ((d1 >= 0) ? d1 : -1)
-                 : (lev[r] == 2) ? ((d1 >= 0 && d2 >= 0) ? d1 + d2 : -1) : -1;
-        }
-      };
-      if (depth > 1 && a >= depth - 1) {
-        int da, db, dc, off[2];
-        disc_rows(a, da, db, dc, off);
-        for (;;) {
-          int v[2];
-#pragma unroll
-          for (int r = 0; r < 2; ++r) {
-            v[r] = 0;
-            if (off[r] >= 0 && e - off[r] >= 0) v[r] = pd_at(a - lev[r], e - off[r]);
-          }
-          const int an = a - depth;
-          int nda = 0, ndb = 0, ndc = 0, noff[2] = {-1, -1};
-          if (an >= depth - 1) disc_rows(an, nda, ndb, ndc, noff);
-          auto val = [&](int j) {
-            const int x0 = __shfl_sync(LG_FULL, v[0], j & 31), x1 = __shfl_sync(LG_FULL, v[1], j & 31);
-            return (j < 32 ? x0 : x1) & cm;
-          };
-          const int c0 = val(0);
-          const int c1 = val(1 + c0);
-          put(a, c0);
-          put(a - 1, c1);
-          int de = __shfl_sync(LG_FULL, da, c0) + __shfl_sync(LG_FULL, db, c1);
-          if (depth >= 3) {
-            const int c2 = val(1 + K + c0 * K + c1);
-            put(a - 2, c2);
-            de += __shfl_sync(LG_FULL, dc, c2);
-          }
-          e -= de;
-          a = an;
-          if (a < depth - 1) break;
-          da = nda; db = ndb; dc = ndc; off[0] = noff[0]; off[1] = noff[1];
-        }
-      }
-      for (; a >= 0; --a) {
-        const int c = pd_at(a, e) & cm;
-        put(a, c);
-        e -= bdisc[a * K + c];
-      }
-    }
+    if (!used_default) bt_warp(PD, PDR, bdisc, K, pdmask, La - 1, 0, ee, bch);
     if (lane == 0) s_La = used_default;
   }
   __syncthreads();
-  if (!s_La)
-    for (int a = tid; a < La; a += NT) choice[act[a]] = bch[a];
-  __syncthreads();
   double* sm_ce = reinterpret_cast<double*>(smem_raw + (((size_t)La * 4 + 15) & ~(size_t)15));  // after bch
-  int64_t* sm_cb = reinterpret_cast<int64_t*>(sm_ce + La);
-  int used_default = s_La;
-  if (used_default) {
-    for (int a = tid; a < La; a += NT) choice[act[a]] = default_idx[act[a]];
-    __syncthreads();
-  }
-  for (int pass = 0; pass < 2; ++pass) {
-    for (int a = tid; a < La; a += NT) {
-      const int l = act[a];
-#if DP_SUM_BCH
-      const int c = used_default ? default_idx[l] : bch[a];
-#else
-      const int c = used_default ? default_idx[l] : choice[l];
-#endif
-      sm_ce[a] = metric(err[(int64_t)l * K + c], flags);
-      sm_cb[a] = bits[(int64_t)l * K + c];
-    }
-    __syncthreads();
-    if (tid == 0) {
-      int64_t pb = 0;
-      double pe = 0.0;
-      int a = 0;
-      for (; a + 4 <= La; a += 4) {
-        const double v0 = sm_ce[a], v1 = sm_ce[a + 1], v2 = sm_ce[a + 2], v3 = sm_ce[a + 3];
-        pb += sm_cb[a] + sm_cb[a + 1] + sm_cb[a + 2] + sm_cb[a + 3];
-        pe = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(pe, v0), v1), v2), v3);
-      }
-      for (; a < La; ++a) { pb += sm_cb[a]; pe = __dadd_rn(pe, sm_ce[a]); }
-      if (!used_default && (pb > s_defbits || pe > emax)) {
-        s_La = 1;
-      } else {
-        lgreco_solve_info inf = {};
-        inf.emax = emax;
-        inf.total_err = pe;
-        inf.total_bits = pb;
-        inf.default_bits = s_defbits;
-        inf.used_default = used_default;
-        inf.n_active = La;
-        inf.status = LGRECO_OK;
-        *info = inf;
-        s_La = -1;
-      }
-    }
-    __syncthreads();
-    if (s_La < 0) break;
-    used_default = 1;
-    for (int a = tid; a < La; a += NT) choice[act[a]] = default_idx[act[a]];
-    __syncthreads();
-  }
+  finish_plan(s_La, bch, La, act, default_idx, err, bits, K, flags, emax, s_defbits, choice, info, sm_ce, &s_La);
 #ifdef LG_DP_TIMING
   LG_T(5);
   if (tid == 0)
@@ -1466,6 +1544,199 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
            tstamp[2] - tstamp[1], tstamp[3] - tstamp[2], (tstamp[3] - tstamp[2]) / (La ? La : 1), t_c / La,
            (t_p - t_c) / La, t_s / La, t_cl / La, t_push / (La ? La : 1), tstamp[4] - tstamp[3], tstamp[5] - tstamp[4]);
 #endif
+}
+
+// ---------------------------------------------------------------------------
+// Layer groups.  With ngroups == 2, k_solve_cl's two clusters run Alg.1's row recursion
+// for the bottom active layers [0, h) and for the top layers [h, La) concurrently, each
+// from the zero row, and write their last rows F (bottom) and P (top): the critical path
+// of the solve halves.  The whole recursion's last row is their min-plus convolution,
+// DP[e] = min_{e1} F[e1] + P[e - e1] (min-plus is associative), and k_solve_join returns
+// exactly Alg.1's plan without forming it:
+//  * C* = min_{e <= D} DP[e] = min_{e1} F[e1] + PM[D - e1], PM = prefix minima of P;
+//  * e* = the smallest e attaining C* (line 23, R19) = the smallest e1 + PA[D - e1] over
+//    the e1 attaining C*, PA[x] = the first index of P's minimum over [0, x];
+//  * lines 24-27: from (La - 1, e*) Alg.1's PD takes, layer by layer from the top, the
+//    first candidate (strict <, R19) that still has an optimal completion -- the
+//    lexicographically smallest (c_{La-1}, ..., c_0) among the optimal plans of total
+//    disc e*.  An optimal plan is optimal within each group at its split (e* - e2, e2),
+//    so its top part is the top group's own backtrack from some e2 in
+//    E2 = {e2 : F[e* - e2] + P[e2] = C*}: every e2 of E2 walks down the top group's PD
+//    at once and, layer by layer, only the walks with the smallest candidate survive;
+//    the last survivor's e2 fixes e1 = e* - e2 and the bottom group's own backtrack from
+//    e1 gives the bottom layers.  (Usually |E2| = 1 and both backtracks run at once on
+//    two warps.)
+// Checked against a sequential reference on 600 random tie-heavy instances for every
+// split point (K4), and bit-exact against the oracle in tests/test_gpu_dp.py.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024, 1)
+k_solve_join(const double* __restrict__ err, const int64_t* __restrict__ bits, int L, int K,
+             const int32_t* __restrict__ default_idx, int D, uint32_t flags, int32_t* __restrict__ choice,
+             lgreco_solve_info* __restrict__ info, const uint8_t* __restrict__ PD, const int32_t* __restrict__ act,
+             const int32_t* __restrict__ wdisc, const uint64_t* __restrict__ rowout,
+             const JoinMeta* __restrict__ jmeta) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ JoinMeta M;
+  __shared__ uint64_t s_rv[32];
+  __shared__ int s_re[32];
+  __shared__ int s_flag, s_cnt[2], s_m;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, NT = blockDim.x, NW = NT >> 5;
+#ifdef LG_DP_TIMING
+  long long tj[8] = {0};
+#define LG_TJ(i) do { if (tid == 0) tj[i] = clock64(); } while (0)
+#else
+#define LG_TJ(i) do { } while (0)
+#endif
+  pdl_wait();  // the two groups' rows, PD and meta
+  LG_TJ(0);
+  if (tid == 0) { M = *jmeta; s_cnt[0] = 0; s_cnt[1] = 0; s_m = 0x7fffffff; }
+  __syncthreads();
+  if (M.done) return;
+  const int La = M.La, h = M.h, cm = M.cm;
+  const int64_t PDR = M.PDR;
+  const int W1 = D + 1;
+  const uint64_t NONE = ~0ull;
+  const uint64_t* F = rowout;
+  const uint64_t* P = rowout + W1;
+  // shared memory: [16 W1 B: PM u64 + PA i32, later two survivor buffers] [disc La*K] [bch La] [summary 16 La]
+  uint64_t* PM = reinterpret_cast<uint64_t*>(smem_raw);
+  int32_t* PA = reinterpret_cast<int32_t*>(PM + W1);
+  int2* const sv0 = reinterpret_cast<int2*>(smem_raw);  // survivor buffers (ping-pong)
+  int2* const sv1 = sv0 + W1;
+  int32_t* sdisc = reinterpret_cast<int32_t*>(smem_raw + (size_t)16 * W1);
+  int32_t* bch = sdisc + (size_t)La * K;
+  double* sm_ce = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(bch + La) + 15) & ~static_cast<uintptr_t>(15));
+  for (int i = tid; i < La * K; i += NT) sdisc[i] = __ldcg(wdisc + i);
+  // ---- prefix minima of P with their first index (chunk per thread, block scan)
+  const int CH = (W1 + NT - 1) / NT;
+  const int x0 = min(tid * CH, W1), x1 = min(x0 + CH, W1);
+  uint64_t mv = NONE;
+  int mi = -1;
+  for (int x = x0; x < x1; ++x) {
+    const uint64_t v = __ldcg(P + x);
+    if (v < mv) { mv = v; mi = x; }
+  }
+  // inclusive scan over the threads, the earlier operand winning ties
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t ov = __shfl_up_sync(LG_FULL, mv, o);
+    const int oi = __shfl_up_sync(LG_FULL, mi, o);
+    if (lane >= o && ov <= mv) { mv = ov; mi = oi; }
+  }
+  if (lane == 31) { s_rv[warp] = mv; s_re[warp] = mi; }
+  __syncthreads();
+  if (warp == 0) {
+    uint64_t wv = (lane < NW) ? s_rv[lane] : NONE;
+    int wi = (lane < NW) ? s_re[lane] : -1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t ov = __shfl_up_sync(LG_FULL, wv, o);
+      const int oi = __shfl_up_sync(LG_FULL, wi, o);
+      if (lane >= o && ov <= wv) { wv = ov; wi = oi; }
+    }
+    s_rv[lane] = wv;  // inclusive over warps 0..lane
+    s_re[lane] = wi;
+  }
+  __syncthreads();
+  {
+    // exclusive prefix of this thread = inclusive of warps < warp, then of lanes < lane
+    uint64_t ev = (warp > 0) ? s_rv[warp - 1] : NONE;
+    int ei = (warp > 0) ? s_re[warp - 1] : -1;
+    const uint64_t lv = __shfl_up_sync(LG_FULL, mv, 1);
+    const int li = __shfl_up_sync(LG_FULL, mi, 1);
+    if (lane > 0 && lv < ev) { ev = lv; ei = li; }
+    for (int x = x0; x < x1; ++x) {
+      const uint64_t v = __ldcg(P + x);
+      if (v < ev) { ev = v; ei = x; }
+      PM[x] = ev;
+      PA[x] = ei;
+    }
+  }
+  __syncthreads();
+  LG_TJ(1);
+  // ---- C* and e*: the smallest (value, e) over e1 of (F[e1] + PM[D - e1], e1 + PA[D - e1])
+  uint64_t bv = NONE;
+  int be = 0x7fffffff;
+  for (int e1 = x0; e1 < x1; ++e1) {
+    const uint64_t f = __ldcg(F + e1);
+    const uint64_t pm = PM[D - e1];
+    if (f == NONE || pm == NONE) continue;
+    const uint64_t v = f + pm;
+    const int e = e1 + PA[D - e1];
+    if (v < bv || (v == bv && e < be)) { bv = v; be = e; }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const uint64_t ov = __shfl_xor_sync(LG_FULL, bv, o);
+    const int oe = __shfl_xor_sync(LG_FULL, be, o);
+    if (ov < bv || (ov == bv && oe < be)) { bv = ov; be = oe; }
+  }
+  __syncthreads();  // PM / PA reads done before s_rv is reused
+  if (lane == 0) { s_rv[warp] = bv; s_re[warp] = be; }
+  __syncthreads();
+  if (warp == 0) {
+    bv = (lane < NW) ? s_rv[lane] : NONE;
+    be = (lane < NW) ? s_re[lane] : 0x7fffffff;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const uint64_t ov = __shfl_xor_sync(LG_FULL, bv, o);
+      const int oe = __shfl_xor_sync(LG_FULL, be, o);
+      if (ov < bv || (ov == bv && oe < be)) { bv = ov; be = oe; }
+    }
+    if (lane == 0) { s_rv[0] = bv; s_re[0] = be; }
+  }
+  __syncthreads();
+  const uint64_t Cs = s_rv[0];
+  const int es = s_re[0];
+  const int used_default = (Cs == NONE);
+  LG_TJ(2);
+  int nsurv = 0;
+  if (!used_default) {
+    // ---- E2 = {e2 in [0, e*] : F[e* - e2] + P[e2] == C*} (the PM / PA area is dead)
+    for (int e2 = tid; e2 <= es; e2 += NT) {
+      const uint64_t f = __ldcg(F + es - e2), p = __ldcg(P + e2);
+      if (f != NONE && p != NONE && f + p == Cs) sv0[atomicAdd(&s_cnt[0], 1)] = make_int2(e2, e2);
+    }
+    __syncthreads();
+    int ns = s_cnt[0], cur = 0, a = La - 1;
+    nsurv = ns;
+    LG_TJ(3);
+    // ---- top layers while several walks survive: the smallest candidate per layer
+    while (ns > 1 && a >= h) {
+      const int2* svc = cur ? sv1 : sv0;
+      int2* svn = cur ? sv0 : sv1;
+      for (int i = tid; i < ns; i += NT) atomicMin(&s_m, pd_cm(PD, PDR, a, svc[i].x) & cm);
+      if (tid == 0) s_cnt[cur ^ 1] = 0;
+      __syncthreads();
+      const int m = s_m;
+      const int dm = sdisc[a * K + m];
+      for (int i = tid; i < ns; i += NT) {
+        const int2 w = svc[i];
+        if ((pd_cm(PD, PDR, a, w.x) & cm) == m) svn[atomicAdd(&s_cnt[cur ^ 1], 1)] = make_int2(w.x - dm, w.y);
+      }
+      if (tid == 0) bch[a] = m;
+      __syncthreads();
+      ns = s_cnt[cur ^ 1];
+      cur ^= 1;
+      if (tid == 0) s_m = 0x7fffffff;
+      --a;
+      __syncthreads();
+    }
+    const int2 w = (cur ? sv1 : sv0)[0];
+    if (warp == 0 && a >= h) bt_warp(PD, PDR, sdisc, K, cm, a, h, w.x, bch);
+    if (warp == 1 && h > 0) bt_warp(PD, PDR, sdisc, K, cm, h - 1, 0, es - w.y, bch);
+  }
+  __syncthreads();
+  LG_TJ(4);
+  finish_plan(used_default, bch, La, act, default_idx, err, bits, K, flags, M.emax, M.defbits, choice, info, sm_ce,
+              &s_flag);
+#ifdef LG_DP_TIMING
+  LG_TJ(5);
+  if (tid == 0)
+    printf("dp join: h %d La %d |E2| %d: prefix-min %lld C*/e* %lld E2 %lld backtrack %lld summary %lld\n", h, La,
+           nsurv, tj[1] - tj[0], tj[2] - tj[1], tj[3] - tj[2], tj[4] - tj[3], tj[5] - tj[4]);
+#endif
+#undef LG_TJ
 }
 
 // Weighted costs (NEXT-1): out = bits * w[l], exact in int64; -1 on a negative input or
@@ -1497,14 +1768,16 @@ static size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 size_t solve_workspace_bytes(int L, int K, int D) {
   return align_up((size_t)L * std::max(D + 1 + CL_MAX * 32 * 8, PD_ROW)) + align_up(sizeof(int32_t) * (size_t)(L + 1)) +
          align_up(sizeof(int64_t) * 2 * (size_t)(D + 1)) + align_up(sizeof(int32_t) * (size_t)L * K * CL_MAX) +
-         align_up(sizeof(uint64_t) * (size_t)L * K * CL_MAX) + align_up(sizeof(int32_t) * (size_t)(L + 1) * CL_MAX);
+         align_up(sizeof(uint64_t) * (size_t)L * K * CL_MAX) + align_up(sizeof(int32_t) * (size_t)(L + 1) * CL_MAX) +
+         align_up(sizeof(JoinMeta));
 }
 
 // Cluster launch (k_solve_cl) when the shapes fit: K <= 16, CPT in {2, 4, 8}, two
 // 64-bit full-length rows within 200 KB of shared memory, and an 8-CTA cluster of that
 // size can be resident.  Returns cudaErrorNotSupported (nothing launched) otherwise.
 static cudaError_t launch_solve_cluster(const SolveArgs& a, uint8_t* pd, int32_t* act, int32_t* wdisc, uint64_t* wadd,
-                                        int32_t* wmaxd, int NC, cudaStream_t st) {
+                                        int32_t* wmaxd, int NC, int ngroups, uint64_t* rowout, JoinMeta* jmeta,
+                                        cudaStream_t st) {
   if (a.K < 1 || a.K > 256) return cudaErrorNotSupported;
   if (const char* env = getenv("LGRECO_DP_NC")) NC = std::max(2, std::min(CL_MAX, atoi(env)));
   int cpt = 1;
@@ -1529,8 +1802,11 @@ static cudaError_t launch_solve_cluster(const SolveArgs& a, uint8_t* pd, int32_t
   const size_t smem = smem_of(kt0);
   if (smem > 220 * 1024 || (size_t)24 * a.L + 64 > rows_b) return cudaErrorNotSupported;
   const int kt = kt0;
+  // layer groups: K <= 16 (tables in shared memory) and the join's 16 (D + 1) B of rows
+  const size_t join_smem = (size_t)16 * (a.D + 1) + (size_t)4 * a.L * a.K + (size_t)4 * a.L + (size_t)16 * a.L + 32;
+  if (ngroups > 1 && (kt == 0 || join_smem > 220 * 1024)) return cudaErrorNotSupported;
   void (*fn)(const double*, const int64_t*, int, int, const int32_t*, const int32_t*, int, uint32_t, int32_t*,
-             lgreco_solve_info*, uint8_t*, int32_t*, int32_t*, uint64_t*, int32_t*) = nullptr;
+             lgreco_solve_info*, uint8_t*, int32_t*, int32_t*, uint64_t*, int32_t*, int, uint64_t*, JoinMeta*) = nullptr;
 #define LG_CL(C, KT) if (cpt == C && kt == KT) fn = k_solve_cl<C, KT>;
 #define LG_CL_K(C) LG_CL(C, 4) LG_CL(C, 5) LG_CL(C, 7) LG_CL(C, 8) LG_CL(C, 16) LG_CL(C, 0)
   LG_CL_K(1) LG_CL_K(2) LG_CL_K(4) LG_CL_K(8)
@@ -1539,12 +1815,14 @@ static cudaError_t launch_solve_cluster(const SolveArgs& a, uint8_t* pd, int32_t
   if (!fn) return cudaErrorNotSupported;
   // attribute + cluster-occupancy checks are host-side driver calls (tens of us): done
   // once per (kernel, shared memory, block) configuration and cached
-  struct CfgKey { const void* fn; size_t smem; int nt, nc; int ok; };
+  struct CfgKey { const void* fn; size_t smem; int nt, nc, ng; int ok; };
   static CfgKey cache[16];
   static int ncache = 0;
   int cached = -1;
   for (int i = 0; i < ncache; ++i)
-    if (cache[i].fn == (const void*)fn && cache[i].smem == smem && cache[i].nt == nt && cache[i].nc == NC) cached = i;
+    if (cache[i].fn == (const void*)fn && cache[i].smem == smem && cache[i].nt == nt && cache[i].nc == NC &&
+        cache[i].ng == ngroups)
+      cached = i;
   if (cached >= 0 && !cache[cached].ok) return cudaErrorNotSupported;
   cudaError_t e = cudaSuccess;
   if (cached < 0) {
@@ -1574,7 +1852,7 @@ static cudaError_t launch_solve_cluster(const SolveArgs& a, uint8_t* pd, int32_t
   attr[0].val.clusterDim.z = 1;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL: k_solve_cl waits in-kernel
   attr[1].val.programmaticStreamSerializationAllowed = 1;
-  cfg.gridDim = dim3(NC, 1, 1);
+  cfg.gridDim = dim3(NC * ngroups, 1, 1);
   cfg.blockDim = dim3(nt, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
@@ -1583,8 +1861,12 @@ static cudaError_t launch_solve_cluster(const SolveArgs& a, uint8_t* pd, int32_t
   if (cached < 0) {
     int nclusters = 0;
     e = cudaOccupancyMaxActiveClusters(&nclusters, (const void*)fn, &cfg);
-    const int ok = (e == cudaSuccess && nclusters >= 1) ? 1 : 0;
-    if (ncache < 16) cache[ncache++] = CfgKey{(const void*)fn, smem, nt, NC, ok};
+    const int ok = (e == cudaSuccess && nclusters >= ngroups) ? 1 : 0;
+    if (ok && ngroups > 1) {
+      e = cudaFuncSetAttribute(k_solve_join, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+      if (e != cudaSuccess) { cudaGetLastError(); return cudaErrorNotSupported; }
+    }
+    if (ncache < 16) cache[ncache++] = CfgKey{(const void*)fn, smem, nt, NC, ngroups, ok};
     if (!ok) {
       if (getenv("LGRECO_DEBUG")) fprintf(stderr, "lgreco: cluster occupancy %d (%s)\n", nclusters, cudaGetErrorString(e));
       cudaGetLastError();
@@ -1592,8 +1874,21 @@ static cudaError_t launch_solve_cluster(const SolveArgs& a, uint8_t* pd, int32_t
     }
   }
   cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, fn, a.err, a.bits, a.L, a.K, a.default_idx, a.compress, a.D, a.flags, a.choice,
-                            a.info, pd, act, wdisc, wadd, wmaxd);
+  e = cudaLaunchKernelEx(&cfg, fn, a.err, a.bits, a.L, a.K, a.default_idx, a.compress, a.D, a.flags, a.choice, a.info,
+                         pd, act, wdisc, wadd, wmaxd, ngroups, rowout, jmeta);
+  if (e != cudaSuccess || ngroups == 1) return e;
+  // the join: one CTA, launched programmatically (its griddepcontrol.wait returns once
+  // both groups' rows, PD and meta are written)
+  cudaLaunchConfig_t jc = {};
+  jc.gridDim = dim3(1, 1, 1);
+  jc.blockDim = dim3(1024, 1, 1);
+  jc.dynamicSmemBytes = join_smem;
+  jc.stream = st;
+  jc.attrs = &attr[1];
+  jc.numAttrs = 1;
+  return cudaLaunchKernelEx(&jc, k_solve_join, a.err, a.bits, a.L, a.K, a.default_idx, a.D, a.flags, a.choice, a.info,
+                            (const uint8_t*)pd, (const int32_t*)act, (const int32_t*)wdisc, (const uint64_t*)rowout,
+                            (const JoinMeta*)jmeta);
 }
 
 cudaError_t launch_solve(const SolveArgs& a, void* ws, cudaStream_t st) {
@@ -1609,10 +1904,18 @@ cudaError_t launch_solve(const SolveArgs& a, void* ws, cudaStream_t st) {
                                                align_up(sizeof(int32_t) * (size_t)a.L * a.K * CL_MAX));
   int32_t* wmaxd = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(wadd) +
                                               align_up(sizeof(uint64_t) * (size_t)a.L * a.K * CL_MAX));
+  JoinMeta* jmeta = reinterpret_cast<JoinMeta*>(reinterpret_cast<uint8_t*>(wmaxd) +
+                                                align_up(sizeof(int32_t) * (size_t)(a.L + 1) * CL_MAX));
+  uint64_t* rowout = reinterpret_cast<uint64_t*>(grows);
   if (!(a.flags & LGRECO_SOLVE_SINGLE_CTA)) {
-    // 16 SMs when a 16-CTA cluster of this size is schedulable, else 8
-    cudaError_t ce = launch_solve_cluster(a, pd, act, wdisc, wadd, wmaxd, 16, st);
-    if (ce == cudaErrorNotSupported) ce = launch_solve_cluster(a, pd, act, wdisc, wadd, wmaxd, 8, st);
+    // two layer groups on two 16-CTA clusters when the table is long enough to pay for the
+    // join (LGRECO_DP_GROUPS=1|2 overrides); else one cluster of 16 SMs, else 8
+    int ng = a.L >= 32 ? 2 : 1;
+    if (const char* env = getenv("LGRECO_DP_GROUPS")) ng = atoi(env) == 2 ? 2 : 1;
+    cudaError_t ce = cudaErrorNotSupported;
+    if (ng == 2) ce = launch_solve_cluster(a, pd, act, wdisc, wadd, wmaxd, 16, 2, rowout, jmeta, st);
+    if (ce == cudaErrorNotSupported) ce = launch_solve_cluster(a, pd, act, wdisc, wadd, wmaxd, 16, 1, rowout, jmeta, st);
+    if (ce == cudaErrorNotSupported) ce = launch_solve_cluster(a, pd, act, wdisc, wadd, wmaxd, 8, 1, rowout, jmeta, st);
     if (ce != cudaErrorNotSupported) return ce;
     if (getenv("LGRECO_DEBUG")) fprintf(stderr, "lgreco: cluster solve not used (L=%d K=%d D=%d)\n", a.L, a.K, a.D);
   }

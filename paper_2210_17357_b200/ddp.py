@@ -25,17 +25,26 @@ from . import workloads as W
 
 
 class _Bucket:
-    def __init__(self, owner, layers, device):
+    def __init__(self, owner, layers, shapes, device):
         self.layers = layers
+        self.shapes = shapes
         L, K = len(layers), owner.K
         n = W.total_numel(layers)
-        nid = None
-        if owner.world > 1:
-            obj = [lgreco.nccl_unique_id() if owner.rank == 0 else None]
-            dist.broadcast_object_list(obj, src=0, group=owner.pg)
-            nid = obj[0]
-        self.ctx = lgreco.Context(layers, owner.family, owner.params, qbucket=owner.qbucket, seed=owner.seed,
-                                  rank=owner.rank, world=owner.world, nccl_id=nid)
+        kw = dict(qbucket=owner.qbucket, seed=owner.seed, rank=owner.rank, world=owner.world)
+        if owner.world > 1 and owner.family == lgreco.QSGD and owner.exchange == "p2p":
+            # peer-memory exchange: every rank exports its windows once, all-gathers the
+            # IPC handles over the process group and opens its peers' (no NCCL on the data path)
+            self.ctx = lgreco.Context(layers, owner.family, owner.params, **kw)
+            blobs = [None] * owner.world
+            dist.all_gather_object(blobs, self.ctx.p2p_export(), group=owner.pg)
+            self.ctx.p2p_open(blobs)
+        else:
+            nid = None
+            if owner.world > 1:
+                obj = [lgreco.nccl_unique_id() if owner.rank == 0 else None]
+                dist.broadcast_object_list(obj, src=0, group=owner.pg)
+                nid = obj[0]
+            self.ctx = lgreco.Context(layers, owner.family, owner.params, nccl_id=nid, **kw)
         self.ef = torch.zeros(n, dtype=torch.float32, device=device)
         self.G = torch.zeros(n, dtype=torch.float32, device=device)
         self.out = torch.empty(n, dtype=torch.float32, device=device)
@@ -48,11 +57,12 @@ class _Bucket:
         self.ws = torch.empty(lgreco.solve_workspace_bytes(L, K, owner.D), dtype=torch.uint8, device=device)
         self.calls = 0
         self.planned = False
+        self.added = []  # record=True: the gradients accumulated into G since its last reset
 
 
 class LGrecoHook:
     def __init__(self, family, params, default_idx, *, warmup_steps=10, replan_every=100, D=10000, seed=0x5EED,
-                 qbucket=128, flags=0, process_group=None, record=False):
+                 qbucket=128, flags=0, process_group=None, record=False, exchange="p2p"):
         self.family, self.params = family, [int(p) for p in params]
         self.K = len(self.params)
         self.default_idx = int(default_idx)
@@ -61,18 +71,22 @@ class LGrecoHook:
         self.pg = process_group
         self.world = dist.get_world_size(process_group)
         self.rank = dist.get_rank(process_group)
-        self.buckets: dict[tuple, _Bucket] = {}
+        self.exchange = exchange
+        self.buckets: dict[int, _Bucket] = {}
         self.record = record
         self.last = {}  # bucket index -> (g, ef_before, choice, step) when record=True
 
     def _state(self, bucket):
         shapes = tuple(tuple(p.shape) for p in bucket.parameters())
-        key = (bucket.index(), shapes)
-        st = self.buckets.get(key)
-        if st is None:  # new bucket layout (DDP rebuilds its buckets after the first step)
+        idx = bucket.index()
+        st = self.buckets.get(idx)
+        if st is not None and st.shapes != shapes:  # DDP rebuilt its buckets: new layout
+            st.ctx.close()
+            st = None
+        if st is None:
             layers = W.layer_table([(None, s) for s in shapes])
-            st = _Bucket(self, layers, bucket.buffer().device)
-            self.buckets[key] = st
+            st = _Bucket(self, layers, shapes, bucket.buffer().device)
+            self.buckets[idx] = st
         return st
 
     def _replan(self, st):
@@ -82,6 +96,7 @@ class LGrecoHook:
                      workspace=st.ws)
         st.ctx.plan_broadcast(st.choice)
         st.G.zero_()
+        st.added = []
         st.planned = True
 
     @staticmethod
@@ -90,15 +105,17 @@ class LGrecoHook:
         g = bucket.buffer()
         st.calls += 1
         step = st.calls
+        if state.record:
+            st.added.append(g.clone())
         if step <= state.warmup or not st.planned:
-            st.G.add_(g)
+            lgreco.accumulate(st.G, g)
             if step >= state.warmup:
                 state._replan(st)
             fut = dist.all_reduce(g, group=state.pg, async_op=True).get_future()
             world = state.world
             return fut.then(lambda f: f.value()[0].div_(world))
         rec = (g.clone(), st.ef.clone(), st.choice.clone(), step) if state.record else None
-        st.G.add_(g)
+        lgreco.accumulate(st.G, g)
         st.ctx.compress_allreduce_dev(st.choice, g, st.ef, st.out, step)
         g.copy_(st.out)
         if rec is not None:

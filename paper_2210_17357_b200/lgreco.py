@@ -55,6 +55,7 @@ _SIGS = {
     "lgreco_ctx_launches": (_I64, [_VP]),
     "lgreco_ctx_timing": (_I32, [_VP, _I32]),
     "lgreco_ctx_kernel_ms": (_I32, [_VP, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
+    "lgreco_accumulate": (C.c_int, [_VP, _VP, _I64, _VP]),
     "lgreco_profile": (C.c_int, [_VP, _VP, _VP, _U64, _VP, _VP, _VP]),
     "lgreco_solve_workspace_bytes": (C.c_size_t, [_I32, _I32, _I32]),
     "lgreco_solve": (C.c_int, [_VP, _VP, _I32, _I32, _VP, _VP, _I32, _U32, _VP, _VP, _VP, C.c_size_t, _VP]),
@@ -78,6 +79,7 @@ _SIGS = {
     "lgreco_topk_combine": (C.c_int, [_VP, _VP, _I32, _VP, _VP, _VP]),
     "lgreco_plan_layout": (C.c_int, [_VP, _I32, _VP, _VP, _I32, _VP, _VP, _VP]),
     "lgreco_psgd_sizes": (C.c_int, [_VP, _VP, _VP]),
+    "lgreco_psgd_factors": (C.c_int, [_VP, _VP, _VP, _VP]),
     "lgreco_psgd_p": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _U64, _VP]),
     "lgreco_psgd_q": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _I32, _VP, _VP]),
     "lgreco_psgd_out": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _I32, _VP, _VP]),
@@ -275,6 +277,10 @@ class Context:
         _check(lib().lgreco_psgd_sizes(self.h, C.byref(p), C.byref(q)), "psgd_sizes")
         return p.value, q.value
 
+    def psgd_factors(self, Phat, Q, stream=None):
+        """Copy the current Phat / warm-start Q slot areas into the float32 cuda tensors."""
+        _check(lib().lgreco_psgd_factors(self.h, _ptr(Phat), _ptr(Q), _stream(stream)), "psgd_factors")
+
     def psgd_p(self, choice, g, ef, P, step, stream=None):
         _check(lib().lgreco_psgd_p(self.h, _i32(choice), _ptr(g), _ptr(ef), _ptr(P), step, _stream(stream)), "psgd_p")
 
@@ -329,6 +335,13 @@ def solve(err, bits, default_idx, compress=None, D=10000, flags=0, choice=None, 
                               _ptr(choice), _ptr(info), _ptr(workspace), workspace.numel(), _stream(stream)),
            "solve")
     return choice, info
+
+
+def accumulate(G, g, stream=None):
+    """K0 (row a1): G += g in fp32 on the device (cuda float32 tensors of equal size)."""
+    assert G.dtype == torch.float32 and g.dtype == torch.float32 and G.numel() == g.numel()
+    _check(lib().lgreco_accumulate(_ptr(G), _ptr(g), G.numel(), _stream(stream)), "accumulate")
+    return G
 
 
 def weight_costs(bits, weight, out=None, stream=None):

@@ -23,7 +23,7 @@ def _port():
     return p
 
 
-def test_ddp_hook_one_gpu():
+def test_ddp_hook_one_gpu(ref):
     from paper_2210_17357_b200 import lgreco
     from paper_2210_17357_b200.ddp import LGrecoHook
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_port()))
@@ -36,7 +36,7 @@ def test_ddp_hook_one_gpu():
                                                    else [])) for m in net]).cuda()
         ref_net.load_state_dict(net.state_dict())
         ddp = torch.nn.parallel.DistributedDataParallel(net, device_ids=[0], bucket_cap_mb=0.5)
-        state = LGrecoHook(lgreco.QSGD, W.QSGD_BITS, default_idx=2, warmup_steps=2, replan_every=3, record=True)
+        state = LGrecoHook(lgreco.QSGD, W.QSGD_BITS, default_idx=2, warmup_steps=2, replan_every=4, record=True)
         ddp.register_comm_hook(state, LGrecoHook.hook)
         opt = torch.optim.SGD(ddp.parameters(), lr=0.05)
         g = torch.Generator(device="cuda").manual_seed(1)
@@ -58,14 +58,23 @@ def test_ddp_hook_one_gpu():
         torch.cuda.synchronize()
         assert state.last, "no compressed step was recorded"
         for idx, (gin, ef0, choice, st, out, layers) in state.last.items():
-            ctx = lgreco.Context(layers, lgreco.QSGD, W.QSGD_BITS, seed=state.seed)
-            ef = ef0.clone()
-            o2 = torch.empty_like(gin)
-            ctx.compress_allreduce_dev(choice, gin, ef, o2, st)
-            torch.cuda.synchronize()
-            assert torch.equal(o2.view(torch.int32), out.view(torch.int32))
+            # the hook's compressed step vs the ORACLE on the recorded inputs (R13, W = 1)
+            ch = choice.cpu().numpy()
+            lbits = [W.QSGD_BITS[c] if c >= 0 else 0 for c in ch]
+            r_out, _, _, _ = ref.qsgd_allreduce(layers, lbits, [gin.cpu().numpy()], [ef0.cpu().numpy()],
+                                                seed=state.seed, step=st)
+            assert np.array_equal(out.cpu().numpy().view(np.uint32), r_out.view(np.uint32))
             assert int((choice >= 0).sum()) == sum(l.compress for l in layers)
-            ctx.close()
+        # accumulation (row a1, K0): G after the last replan = the oracle's G += g over the
+        # bucket gradients the hook added since (bitwise)
+        n_acc = 0
+        for stt in state.buckets.values():
+            Gr = np.zeros(stt.G.numel(), np.float32)
+            for gi in stt.added:
+                Gr = ref.accumulate(Gr, gi.cpu().numpy())
+            assert np.array_equal(stt.G.cpu().numpy().view(np.uint32), Gr.view(np.uint32))
+            n_acc += len(stt.added)
+        assert n_acc > 0
         assert np.mean(losses[-3:]) < losses[0]
         state.close()
     finally:

@@ -130,3 +130,35 @@ def test_weighted_costs_and_solve(lg, ref):
     st, c_ref, i_ref = ref.solve(err, bits * w[:, None], dflt, comp, D=10000)
     c_gpu, i_gpu = _run(lg, err, wb, dflt, comp, 10000, 0)
     assert list(c_gpu) == list(c_ref) and i_gpu.total_bits == i_ref.total_bits
+
+
+@pytest.mark.parametrize("groups", ["2", "1"])
+def test_layer_groups_bit_exact(lg, ref, groups, monkeypatch):
+    """The two-group solve (k_solve_cl on two clusters + k_solve_join, forced for every
+    table size with LGRECO_DP_GROUPS=2) reproduces the oracle's plan exactly: random and
+    tie-heavy tables (many optimal plans, so |E2| > 1 and the lexicographic walk of the
+    top group decides), 1..80 layers (split points at the edges: La = 0, 1, 2), all
+    layers inactive, D from 1 to 10000."""
+    monkeypatch.setenv("LGRECO_DP_GROUPS", groups)
+    rng = np.random.default_rng(7 + int(groups))
+    n_multi = 0
+    for trial in range(120):
+        L = int(rng.integers(1, 81))
+        K = int(rng.integers(1, 17))
+        D = int(rng.choice([1, 7, 100, 1000, 10000]))
+        if trial % 2:
+            err = rng.integers(0, 4, (L, K)).astype(np.float64) * rng.choice([0.5, 1.0], (L, 1))
+            bits = rng.integers(1, 4, (L, K)).astype(np.int64) * 64
+        else:
+            err, bits = _table(rng, L, K, zero_frac=0.1)
+        dflt = rng.integers(0, K, L).astype(np.int32)
+        comp = (rng.random(L) < rng.choice([0.0, 0.5, 1.0])).astype(np.int32) if trial % 5 == 0 else None
+        st, c_ref, i_ref = ref.solve(err, bits, dflt, comp, D=D)
+        c_gpu, i_gpu = _run(lg, err, bits, dflt, comp, D, 0)
+        assert st == 0 and i_gpu.status == 0
+        assert list(c_gpu) == list(c_ref), (trial, L, K, D)
+        assert (i_gpu.total_bits, i_gpu.default_bits, i_gpu.used_default, i_gpu.n_active) == \
+            (i_ref.total_bits, i_ref.default_bits, i_ref.used_default, i_ref.n_active)
+        assert i_gpu.emax == i_ref.emax and i_gpu.total_err == i_ref.total_err
+        n_multi += trial % 2
+    assert n_multi > 0

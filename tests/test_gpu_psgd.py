@@ -87,6 +87,37 @@ def test_c2_full_size_profile(lg, ref):
     assert (np.abs(ge - rerr) / np.maximum(rerr, 1e-300)).max() <= 1e-5
 
 
+def _slots(ref, layers, ranks):
+    """P / Q slot offsets of the ctx factor areas (include/lgreco.h lgreco_psgd_factors)."""
+    po, qo, p, q = {}, {}, 0, 0
+    for l, ly in enumerate(layers):
+        if ly.compress and ly.rows > 0:
+            rmax = max([r for r in ranks if not ref.psgd_lossless(ly.rows, ly.cols, r)], default=0)
+            po[l], qo[l] = p, q
+            p += ly.rows * rmax
+            q += ly.cols * rmax
+    return po, qo
+
+
+def _check_factors(ctx, ref, layers, lrank, Ps_ref, Qs_ref, ranks):
+    """Phat and the warm-start Q of the ctx vs the oracle's (R12), 1e-5 normwise per layer."""
+    Psz, Qsz = ctx.psgd_sizes()
+    Ph = torch.zeros(max(Psz, 1), dtype=torch.float32, device="cuda")
+    Qw = torch.zeros(max(Qsz, 1), dtype=torch.float32, device="cuda")
+    ctx.psgd_factors(Ph, Qw)
+    Ph, Qw = Ph.cpu().numpy(), Qw.cpu().numpy()
+    po, qo = _slots(ref, layers, ranks)
+    n = 0
+    for l, P_ref in Ps_ref.items():
+        m, k, r = layers[l].rows, layers[l].cols, lrank[l]
+        P = Ph[po[l]:po[l] + m * r].reshape(r, m).T
+        Q = Qw[qo[l]:qo[l] + k * r].reshape(r, k).T
+        assert _rel(P, P_ref) <= 1e-5, (l, _rel(P, P_ref))
+        assert _rel(Q, Qs_ref[l]) <= 1e-5, (l, _rel(Q, Qs_ref[l]))
+        n += 1
+    return n
+
+
 def _choice(layers, rng):
     return [int(rng.integers(0, len(RANKS))) if l.compress else -1 for l in layers]
 
@@ -137,6 +168,7 @@ def test_compress_simulated_ranks_two_steps(lg, ref, Wn):
             outs.append(out)
         if S:
             ctx.psgd_raw_combine(choice, Wn, torch.cat(pays).contiguous(), outs[0])
+        assert _check_factors(ctx, ref, layers, lrank, Ps, Qs, RANKS) == len(Qs)
         o = outs[0].cpu().numpy()
         for l, ly in enumerate(layers):
             sl = slice(ly.offset, ly.offset + ly.numel)
@@ -161,9 +193,10 @@ def test_compress_allreduce_w1(lg, ref):
     ctx.compress_allreduce(choice, gd, ed, out, 4)
     Qs = {l: ref.psgd_init_q(3, l, 4, ly.cols, 2) for l, ly in enumerate(layers)
           if ly.compress and ly.rows and not ref.psgd_lossless(ly.rows, ly.cols, 2)}
-    out_ref, es_ref, _ = ref.psgd_allreduce(layers, lrank, [g], [e], Qs)
+    out_ref, es_ref, Ps = ref.psgd_allreduce(layers, lrank, [g], [e], Qs)
     assert _rel(out.cpu().numpy(), out_ref) <= 1e-5
     assert _rel(ed.cpu().numpy(), es_ref[0]) <= 1e-5
+    assert _check_factors(ctx, ref, layers, lrank, Ps, Qs, RANKS) == len(Qs) > 0
     ctx.check()
 
 

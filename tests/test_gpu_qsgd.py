@@ -523,3 +523,44 @@ def test_p2p_device_plan_simulated_ranks(lg, ref, Wn):
     for c in ctxs:
         c.check()
         c.close()
+
+
+@pytest.mark.parametrize("case", ["A", "B"])
+def test_golden_packed_record_gpu(lg, case):
+    """K5's record bytes equal the hand-derived R7 records (tests/golden/qsgd_record.txt)."""
+    from goldens import golden_record_cases
+    bits, x, words = {cs: (b, x, w) for cs, b, x, w in golden_record_cases()}[case]
+    layers = [W.Layer(0, 128, 0, 0, 1)]
+    ctx = lg.Context(layers, lg.QSGD, BITS, seed=3)
+    choice = [BITS.index(bits)]
+    S = ctx.payload_bytes(choice)
+    assert S == 4 * words.size
+    pay = torch.zeros(S, dtype=torch.uint8, device="cuda")
+    dec = torch.empty(128, dtype=torch.float32, device="cuda")
+    ef = torch.zeros(128, dtype=torch.float32, device="cuda")
+    ctx.qsgd_pack(choice, _dev(x), ef, pay, dec, 0, 5)
+    assert np.array_equal(pay.cpu().numpy().view(np.uint32), words)
+    assert np.array_equal(dec.cpu().numpy(), x)
+    ctx.close()
+
+
+@pytest.mark.parametrize("n,shift", [(0, 0), (1, 0), (3, 1), (1000, 0), (4099, 2), (4099, 1), (25557032, 0)])
+def test_accumulate_parity(lg, ref, n, shift):
+    """Row a1 / K0: G += g bitwise equal to the oracle over several steps, for ragged
+    sizes, shared and differing misalignments (scalar head / scalar path)."""
+    rng = np.random.default_rng(n + shift)
+    G0 = (rng.standard_normal(n) * 1e-2).astype(np.float32)
+    Gd = torch.zeros(n + 4, dtype=torch.float32, device="cuda")
+    Gv = Gd[shift:shift + n]
+    Gv.copy_(_dev(G0))
+    want = G0
+    for t in range(3):
+        g = (rng.standard_normal(n) * 10.0 ** rng.uniform(-6, 0)).astype(np.float32)
+        gd = torch.zeros(n + 4, dtype=torch.float32, device="cuda")
+        gsh = shift if t != 1 else (shift + 1) % 4  # step 1: different alignment -> scalar path
+        gv = gd[gsh:gsh + n]
+        gv.copy_(_dev(g))
+        lg.accumulate(Gv, gv)
+        want = ref.accumulate(want, g)
+    torch.cuda.synchronize()
+    assert np.array_equal(Gv.cpu().numpy().view(np.uint32), want.view(np.uint32))

@@ -10,6 +10,7 @@ import numpy as np
 import pytest
 
 from paper_2210_17357_b200 import workloads as W
+from goldens import golden_record_cases
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 
@@ -330,3 +331,39 @@ def test_quant_ratio_pin(ref, name, paper):
     S128, _, _ = ref.layout(layers, lbits, 128)
     assert abs(32 * N / (8 * S1024) - paper) < 0.1
     assert 7.0 < 32 * N / (8 * S128) < 7.15
+
+
+@pytest.mark.parametrize("case", ["A", "B"])
+def test_golden_packed_record(ref, case):
+    """R7 byte layout against records derived by hand (tests/golden/qsgd_record.txt): a
+    transposed (element, bit) or (lane, slot) mapping, a swapped metadata pair or missing
+    16-byte padding fails here -- the pack->unpack round trip alone cannot see them."""
+    c = {cs: (b, x, w) for cs, b, x, w in golden_record_cases()}[case]
+    bits, x, words = c
+    layers = [W.Layer(0, 128, 0, 0, 1)]
+    for step in (0, 7):  # on-grid: the code does not depend on the uniforms
+        pay, e2, dec = ref.qsgd_pack(layers, [bits], x, np.zeros(128, np.float32), seed=3, step=step, want_dec=True)
+        assert pay.size == 4 * words.size
+        assert np.array_equal(pay.view(np.uint32), words)
+        assert np.array_equal(dec, x)
+        assert not e2.any()
+
+
+def test_accumulate_exact_sums(ref):
+    """Row a1: G += g is one fp32 add per element.  On a dyadic grid (multiples of 2^-10,
+    |partial sums| < 2^13) every add is exact, so after T steps G equals the integer
+    closed form sum_t g_t exactly; off-grid, one step equals the correctly rounded sum
+    (fp64 sum of two floats is exact, then one rounding to fp32)."""
+    rng = np.random.default_rng(0)
+    n, T = 1001, 9
+    gs = [(rng.integers(-2 ** 12, 2 ** 12, n) / 1024.0).astype(np.float32) for _ in range(T)]
+    G = np.zeros(n, np.float32)
+    for g in gs:
+        G = ref.accumulate(G, g)
+    want = sum(g.astype(np.float64) for g in gs)
+    assert np.array_equal(G.astype(np.float64), want)
+    a = (rng.standard_normal(n) * 10.0 ** rng.uniform(-8, 8, n)).astype(np.float32)
+    b = (rng.standard_normal(n) * 10.0 ** rng.uniform(-8, 8, n)).astype(np.float32)
+    got = ref.accumulate(a, b)
+    assert np.array_equal(got, (a.astype(np.float64) + b.astype(np.float64)).astype(np.float32))
+    assert np.array_equal(ref.accumulate(a, np.zeros(n, np.float32)), a)
