@@ -14,14 +14,24 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <atomic>
+#include <time.h>
+#include <unistd.h>
 
 #include "common.cuh"
 #include "kernels.h"
+#include "memo.h"
 
 namespace lg {
 
 constexpr int DP_THREADS = 1024;
 constexpr int64_t DP_INF = INT64_MAX;
+
+// saturating sum of costs (the width guard: a wrapped sum would skip the EINVAL check)
+__device__ __forceinline__ unsigned long long sat_add(unsigned long long a, unsigned long long b) {
+  const unsigned long long s = a + b;
+  return s < a ? ~0ull : s;
+}
 
 __device__ __forceinline__ double metric(double v, uint32_t flags) {
   return (flags & LGRECO_METRIC_SQ) ? __dmul_rn(v, v) : v;
@@ -324,7 +334,7 @@ k_solve_fast(const double* __restrict__ err, const int64_t* __restrict__ bits, i
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(LG_FULL, m, o));
-    mx_part += m;  // sum_a max_c cost (lane-replicated)
+    mx_part = sat_add(mx_part, m);  // sum_a max_c cost (lane-replicated)
   }
   bad = __reduce_or_sync(LG_FULL, bad);
 #pragma unroll
@@ -342,7 +352,7 @@ k_solve_fast(const double* __restrict__ err, const int64_t* __restrict__ bits, i
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
       g |= __shfl_xor_sync(LG_FULL, g, o);
-      mxs += __shfl_xor_sync(LG_FULL, mxs, o);
+      mxs = sat_add(mxs, __shfl_xor_sync(LG_FULL, mxs, o));
     }
     if (lane == 0) {
       g = g ? (g & (~g + 1)) : 1;  // lowest set bit of the OR = 2^min ctz(cost)
@@ -751,15 +761,20 @@ __device__ __forceinline__ void cl_st(uint32_t addr, uint64_t v) {
   asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
 }
 
-// Facts of the cluster prelude that k_solve_join needs (written by group 0's rank 0).
+// Cross-cluster handshake of the two layer groups (workspace): group 0's CTAs publish
+// the launch's token after writing their slice of F; ns counts the top group's E2 list.
 struct JoinMeta {
-  int done;  // 1: the row kernel already wrote info (bad table / no active layer)
-  int h;     // the split: bottom group = active layers [0, h), top group = [h, La)
-  int La, cm;
-  int64_t PDR;
-  double emax;
-  int64_t defbits;
+  uint64_t tok[16];
+  int ns;
 };
+__device__ __forceinline__ void st_release_gpu(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_gpu(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
 
 // PD byte of (layer a, cell e): cell-major rows of PDR bytes, in L2 (written by the
 // row kernel: __ldcg)
@@ -852,9 +867,15 @@ __device__ __noinline__ void finish_plan(int used_default, const int32_t* bch, i
                                          int64_t defbits, int32_t* __restrict__ choice,
                                          lgreco_solve_info* __restrict__ info, double* sm_ce, int* s_flag) {
   const int tid = threadIdx.x, NT = blockDim.x;
+#ifdef LG_DP_TIMING
+  long long fp0 = clock64(), fp1 = 0, fp2 = 0, fp3 = 0;
+#endif
   if (!used_default)
     for (int a = tid; a < La; a += NT) choice[act[a]] = bch[a];
   __syncthreads();
+#ifdef LG_DP_TIMING
+  fp1 = clock64();
+#endif
   int64_t* sm_cb = reinterpret_cast<int64_t*>(sm_ce + La);
   if (used_default) {
     for (int a = tid; a < La; a += NT) choice[act[a]] = default_idx[act[a]];
@@ -868,6 +889,9 @@ __device__ __noinline__ void finish_plan(int used_default, const int32_t* bch, i
       sm_cb[a] = bits[(int64_t)l * K + c];
     }
     __syncthreads();
+#ifdef LG_DP_TIMING
+    if (pass == 0) fp2 = clock64();
+#endif
     if (tid == 0) {
       int64_t pb = 0;
       double pe = 0.0;
@@ -894,11 +918,17 @@ __device__ __noinline__ void finish_plan(int used_default, const int32_t* bch, i
       }
     }
     __syncthreads();
+#ifdef LG_DP_TIMING
+    if (pass == 0) fp3 = clock64();
+#endif
     if (*s_flag < 0) break;
     used_default = 1;
     for (int a = tid; a < La; a += NT) choice[act[a]] = default_idx[act[a]];
     __syncthreads();
   }
+#ifdef LG_DP_TIMING
+  if (tid == 0) printf("finish_plan: choice %lld gather %lld sum %lld rest %lld\n", fp1 - fp0, fp2 - fp1, fp3 - fp2, clock64() - fp3);
+#endif
 }
 
 #ifndef QP_DP_CPT0
@@ -912,7 +942,8 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
            const int32_t* __restrict__ default_idx, const int32_t* __restrict__ compress, int D, uint32_t flags,
            int32_t* __restrict__ choice, lgreco_solve_info* __restrict__ info, uint8_t* __restrict__ PD,
            int32_t* __restrict__ act, int32_t* __restrict__ wdisc, uint64_t* __restrict__ wadd,
-           int32_t* __restrict__ wmaxd, int ngroups, uint64_t* __restrict__ rowout, JoinMeta* __restrict__ jmeta) {
+           int32_t* __restrict__ wmaxd, int ngroups, uint64_t* __restrict__ rowout, JoinMeta* __restrict__ jmeta,
+           uint64_t tok) {
   static_assert(KT >= 0 && KT <= 16 && (CPT == 1 || CPT == 2 || CPT == 4 || CPT == 8 || CPT == 16), "cluster DP");
   // KT > 0: K <= KT candidates, tables of the whole recursion in shared memory;
   // KT == 0: K <= 256 candidates in groups of 16 (k_solve_fast's grouped keys), tables
@@ -935,88 +966,106 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
   const int S = NW * 32 * CPT;     // cells per CTA
   const int cbase = (int)rank * S; // first cell of this CTA
 #ifdef LG_DP_TIMING
-  long long tstamp[10] = {0};
+  long long tstamp[20] = {0};
   long long t_push = 0, t_c = 0, t_p = 0, t_s = 0, t_cl = 0;
 #endif
   LG_T(0);
   pdl_wait();  // the error / size tables of the profile
+  LG_T(10);
 
-  // ---- prelude (every CTA, identical): flags/defaults, active list, Emax (layer order)
-  int32_t* sm_flag = reinterpret_cast<int32_t*>(smem_raw);
-  int32_t* sm_act = sm_flag + L;
-  double* sm_de = reinterpret_cast<double*>(sm_act + L);
-  double* sm_dea = sm_de + L;
+  // ---- prelude (every CTA, identical).  Latency-bound: a handful of block-wide steps,
+  //      one thread per layer (or per (layer, candidate) pair) in each, no atomics on the
+  //      critical values; only Emax is a serial chain (layer order, fp64: R20).
+  int32_t* sm_act = reinterpret_cast<int32_t*>(smem_raw);
+  double* sm_dea = reinterpret_cast<double*>(sm_act + ((L + 1) & ~1));
   // the whole (err, bits) table in one global round trip (every later prelude read is
   // shared memory) when it fits in front of the rows' space
   constexpr int PADC = 32 * CPT;
-  const bool pre = (size_t)(36 + 16 * K) * L + 64 <= (size_t)16 * (PADC + (int)NC * S);
+  const bool pre = (size_t)(12 + 16 * K) * L + 64 <= (size_t)16 * (PADC + (int)NC * S);
   double* sm_err = sm_dea + L;
   int64_t* sm_bits = reinterpret_cast<int64_t*>(sm_err + (pre ? (size_t)L * K : 0));
-  if (pre) {
+  __shared__ long long s_scan[32];
+  __shared__ int s_bad;  // bit 0: non-finite or negative error, bit 1: bad default / cost, bit 2: key width
+  __shared__ unsigned long long s_or[32];
+  // block-wide inclusive sum over the threads (int64); *tot = the block's total
+  auto bscan = [&](long long v, long long* tot) -> long long {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const long long t = __shfl_up_sync(LG_FULL, v, o);
+      if (lane >= o) v += t;
+    }
+    if (lane == 31) s_scan[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+      long long x = (lane < NW) ? s_scan[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long t = __shfl_up_sync(LG_FULL, x, o);
+        if (lane >= o) x += t;
+      }
+      s_scan[lane] = x;
+    }
+    __syncthreads();
+    const long long r = v + ((warp > 0) ? s_scan[warp - 1] : 0);
+    *tot = s_scan[NW - 1];
+    __syncthreads();
+    return r;
+  };
+  // (1) the table, the flags and the defaults: one round trip
+  {
+    int fl[4], df[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int l = tid + j * NT;
+      fl[j] = (l < L) ? (compress ? (__ldg(compress + l) != 0) : 1) : 0;
+      df[j] = (l < L) ? __ldg(default_idx + l) : 0;
+    }
+    if (pre) {
 #pragma unroll 4
-    for (int i = tid; i < L * K; i += NT) { sm_err[i] = __ldg(err + i); sm_bits[i] = __ldg(bits + i); }
+      for (int i = tid; i < L * K; i += NT) { sm_err[i] = __ldg(err + i); sm_bits[i] = __ldg(bits + i); }
+    }
+    if (tid == 0) s_bad = 0;
+    __syncthreads();
+    const double* t_err0 = pre ? sm_err : err;
+    const int64_t* t_bits0 = pre ? sm_bits : bits;
+    // (2) active list (block scan of the flags, layer order), Emax terms, default bits
+    long long db = 0, base = 0;
+    int bad_def = 0;
+    for (int t0 = 0; t0 < L; t0 += NT) {
+      const int j = t0 / NT;
+      const int l = t0 + tid;
+      int f = 0, d = 0;
+      if (j < 4) { f = fl[j]; d = df[j]; }
+      else if (l < L) { f = compress ? (compress[l] != 0) : 1; d = default_idx[l]; }
+      if (l < L && rank == 0 && grp == 0) choice[l] = -1;
+      double de = 0.0;
+      if (f) {
+        if (d < 0 || d >= K) bad_def = 1;
+        else { de = metric(t_err0[(int64_t)l * K + d], flags); db += t_bits0[(int64_t)l * K + d]; }
+      }
+      long long tot;
+      const long long pos = bscan(f, &tot) - f + base;
+      if (f) {
+        sm_act[pos] = l;
+        sm_dea[pos] = de;
+        if (rank == 0 && grp == 0) act[pos] = l;
+      }
+      base += tot;
+    }
+    if (__any_sync(LG_FULL, bad_def) && lane == 0) atomicOr(&s_bad, 2);
+    long long dbt;
+    bscan(db, &dbt);  // (the inclusive value is not needed: the total)
+    if (tid == 0) { s_La = (int)base; s_defbits = dbt; }
+    __syncthreads();
   }
+  const int La = s_La;
   const double* t_err = pre ? sm_err : err;
   const int64_t* t_bits = pre ? sm_bits : bits;
-  if (tid == 0) s_status = LGRECO_OK;
-  if (tid < 32) { s_redk[tid] = 0; s_g[tid] = 0; }
-  __syncthreads();
-  int64_t db_part = 0;
-  int bad_def = 0;
-  for (int l = tid; l < L; l += NT) {
-    const int f = compress ? (compress[l] != 0) : 1;
-    const int d = default_idx[l];
-    sm_flag[l] = f;
-    if (rank == 0 && grp == 0) choice[l] = -1;
-    if (f) {
-      if (d < 0 || d >= K) { bad_def = 1; sm_de[l] = 0.0; }
-      else { sm_de[l] = metric(t_err[(int64_t)l * K + d], flags); db_part += t_bits[(int64_t)l * K + d]; }
-    }
-  }
-  if (__any_sync(LG_FULL, bad_def) && lane == 0) atomicExch(&s_status, LGRECO_EINVAL);
-#pragma unroll
-  for (int o = 16; o; o >>= 1) db_part += __shfl_xor_sync(LG_FULL, db_part, o);
-  if (lane == 0) s_redk[warp] = (uint64_t)db_part;
-  __syncthreads();
   LG_T(6);
-  if (warp == 0) {
-    int La = 0;
-    for (int base = 0; base < L; base += 32) {
-      const int l = base + lane;
-      const int f = (l < L) ? sm_flag[l] : 0;
-      const unsigned m = __ballot_sync(LG_FULL, f);
-      if (f) {
-        const int pos = La + __popc(m & ((1u << lane) - 1u));
-        sm_act[pos] = l;
-        if (rank == 0 && grp == 0) act[pos] = l;
-        sm_dea[pos] = sm_de[l];
-      }
-      La += __popc(m);
-    }
-    __syncwarp();
-    if (lane == 0) {
-      double emax = 0.0;
-      int a = 0;
-      for (; a + 4 <= La; a += 4) {
-        const double v0 = sm_dea[a], v1 = sm_dea[a + 1], v2 = sm_dea[a + 2], v3 = sm_dea[a + 3];
-        emax = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(emax, v0), v1), v2), v3);
-      }
-      for (; a < La; ++a) emax = __dadd_rn(emax, sm_dea[a]);
-      int64_t defb = 0;
-      for (int w = 0; w < NW; ++w) defb += (int64_t)s_redk[w];
-      s_La = La; s_emax = emax; s_defbits = defb;
-      int cb = 0;
-      while ((1 << cb) < K) ++cb;
-      s_cbits = cb;
-    }
-  }
-  __syncthreads();
-  const int La = s_La;
-  const double emax = s_emax;
-  LG_T(7);
-  // ---- validation, discretisation (Alg.1 lines 3-5) into this CTA's shared memory
-  //      (tail region after the two rows; identical in every CTA), OR of the costs,
-  //      sum of per-layer max cost, per-layer max admissible disc
+  // (3) Emax = sum of the defaults' errors in layer order (warp 0, lane 0: a serial fp64
+  //     chain, loads batched 8 ahead) || the other warps: per active layer the largest
+  //     cost, the OR of all costs (their lowest set bit is the exact rescale g), and the
+  //     sum of the largest costs (the key width check; saturating)
   constexpr int PAD = 32 * CPT;
   const int row = PAD + (int)NC * S;
   unsigned char* tail = smem_raw + (size_t)16 * row;
@@ -1032,72 +1081,116 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
     my_wdisc = wdisc + (size_t)rank * L * K;
     my_wmaxd = reinterpret_cast<int32_t*>(tail);
   }
-  uint64_t gg = 0, mx_part = 0;
-  int bad = 0;
-  if (tid == 0) my_wmaxd[La] = 0;
-  // every (layer, candidate) pair on its own thread (was: a warp per layer, K lanes
-  // busy); per-layer maxima through shared atomics (order-free: max is exact)
-  uint64_t* sm_m = reinterpret_cast<uint64_t*>(sm_bits + (pre ? (size_t)L * K : 0));  // [La]
-  int32_t* sm_dm = reinterpret_cast<int32_t*>(sm_m + L);                               // [La]
-  for (int a = tid; a < La; a += NT) { sm_m[a] = 0; sm_dm[a] = 0; }
-  __syncthreads();
-  for (int i = tid; i < La * K; i += NT) {
-    const int a = i / K, c = i - a * K;
-    const int l = sm_act[a];
-    const double v = t_err[(int64_t)l * K + c];
-    const int64_t b = t_bits[(int64_t)l * K + c];
-    if (!isfinite(v) || v < 0.0) bad |= 1;
-    if (b < 0) bad |= 2;
-    const uint64_t ub = (uint64_t)(b < 0 ? 0 : b);
-    gg |= ub;
-    const int dd = discretise(metric(v, flags), emax, D, flags);
-    my_wdisc[i] = dd;
-    my_wadd[i] = ub;
-    atomicMax(reinterpret_cast<unsigned long long*>(&sm_m[a]), (unsigned long long)ub);
-    atomicMax(&sm_dm[a], dd);
-  }
-  __syncthreads();
-  for (int a = tid; a < La; a += NT) { mx_part += sm_m[a]; my_wmaxd[a] = sm_dm[a]; }
+  constexpr int KP2 = (KT + 2) & ~1;
+  uint2* cand_all = reinterpret_cast<uint2*>(
+      (reinterpret_cast<uintptr_t>(my_wmaxd + La + 1) + 15) & ~static_cast<uintptr_t>(15));  // [La][KP2], 16-B aligned
+  uint64_t* add_all = reinterpret_cast<uint64_t*>(cand_all + (size_t)La * (KT > 0 ? KP2 : 0));  // [La][KT]
+  int2* band_all = reinterpret_cast<int2*>(add_all + (size_t)La * KT);          // [La]
+  {
+    uint64_t gg = 0, mxp = 0;
+    int bad = 0;
+    if (warp == 0) {
+      if (lane == 0) {
+        double emax = 0.0;
+        int a = 0;
+        for (; a + 8 <= La; a += 8) {
+          double v[8];
 #pragma unroll
-  for (int o = 16; o; o >>= 1) mx_part += __shfl_xor_sync(LG_FULL, mx_part, o);  // per-thread partials
-  bad = __reduce_or_sync(LG_FULL, bad);
-  LG_T(8);
+          for (int j = 0; j < 8; ++j) v[j] = sm_dea[a + j];
 #pragma unroll
-  for (int o = 16; o; o >>= 1) gg |= __shfl_xor_sync(LG_FULL, gg, o);
-  if (lane == 0) {
-    s_g[warp] = gg;
-    s_redk[warp] = mx_part;
-    if (bad & 1) atomicExch(&s_status, LGRECO_ENONFINITE);
-    else if (bad & 2) atomicExch(&s_status, LGRECO_EINVAL);
-  }
-  __syncthreads();
-  if (warp == 0) {
-    uint64_t g = (lane < NW) ? s_g[lane] : 0;
-    unsigned long long mxs = (lane < NW) ? s_redk[lane] : 0;
+          for (int j = 0; j < 8; ++j) emax = __dadd_rn(emax, v[j]);
+        }
+        for (; a < La; ++a) emax = __dadd_rn(emax, sm_dea[a]);
+        s_emax = emax;
+        int cb = 0;
+        while ((1 << cb) < K) ++cb;
+        s_cbits = cb;
+      }
+    }
+    if (warp > 0 || NW == 1) {  // (a one-warp CTA: warp 0 after the chain)
+      const int t1 = (NW > 1) ? tid - 32 : tid, st1 = (NW > 1) ? NT - 32 : NT;
+      for (int a = t1; a < La; a += st1) {
+        const int l = sm_act[a];
+        uint64_t m = 0;
+        for (int c = 0; c < K; ++c) {
+          const int64_t b = t_bits[(int64_t)l * K + c];
+          if (b < 0) bad |= 2;
+          const uint64_t ub = (uint64_t)(b < 0 ? 0 : b);
+          gg |= ub;
+          m = max(m, ub);
+          my_wadd[a * K + c] = ub;  // raw cost; keyed (cost/g << cbits | c) when staged per layer
+        }
+        mxp = sat_add(mxp, m);
+      }
+    }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
-      g |= __shfl_xor_sync(LG_FULL, g, o);
-      mxs += __shfl_xor_sync(LG_FULL, mxs, o);
+      gg |= __shfl_xor_sync(LG_FULL, gg, o);
+      mxp = sat_add(mxp, __shfl_xor_sync(LG_FULL, mxp, o));
     }
+    bad = __reduce_or_sync(LG_FULL, bad);
     if (lane == 0) {
-      g = g ? (g & (~g + 1)) : 1;
-      s_g[0] = g;
-      const uint64_t mx = mxs >> (__ffsll((long long)g) - 1);
-      s_wide = (mx >= (1ull << (30 - ((KT > 0) ? s_cbits : 4)))) ? 1 : 0;
-      if (mx >= (1ull << (62 - s_cbits)) && s_status == LGRECO_OK) s_status = LGRECO_EINVAL;
+      s_or[warp] = gg;
+      s_redk[warp] = mxp;
+      if (bad) atomicOr(&s_bad, bad);
     }
+    __syncthreads();
   }
-  __syncthreads();
+  const double emax = s_emax;
+  const int cbits = s_cbits;
+  LG_T(7);
+  // (4) one thread per active layer: its K discretised errors (Alg.1 lines 3-5, K
+  //     independent divisions in flight), the largest / smallest admissible disc, the
+  //     split weight; warp 0 meanwhile reduces the cost facts to g, the key width and the
+  //     width check
+  {
+    int bad = 0;
+    if (warp == 0) {
+      uint64_t g = (lane < NW) ? s_or[lane] : 0;
+      unsigned long long mxs = (lane < NW) ? s_redk[lane] : 0;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        g |= __shfl_xor_sync(LG_FULL, g, o);
+        mxs = sat_add(mxs, __shfl_xor_sync(LG_FULL, mxs, o));
+      }
+      if (lane == 0) {
+        g = g ? (g & (~g + 1)) : 1;  // lowest set bit of the OR = 2^min ctz(cost)
+        s_g[0] = g;
+        // every cost is a multiple of g, so sum_a max_c cost/g = (sum_a max_c cost)/g exactly
+        const uint64_t mx = mxs >> (__ffsll((long long)g) - 1);
+        s_wide = (mx >= (1ull << (30 - ((KT > 0) ? cbits : 4)))) ? 1 : 0;
+        if (mx >= (1ull << (62 - cbits))) atomicOr(&s_bad, 4);
+      }
+    }
+    for (int a = tid; a < La; a += NT) {
+      const int l = sm_act[a];
+      int mn = 0x7fffffff, mxd = -1;
+      for (int c = 0; c < K; ++c) {
+        const double v = t_err[(int64_t)l * K + c];
+        if (!isfinite(v) || v < 0.0) bad |= 1;
+        const int dd = discretise(metric(v, flags), emax, D, flags);
+        my_wdisc[a * K + c] = dd;
+        if (dd >= 0) { mn = min(mn, dd); mxd = max(mxd, dd); }
+      }
+      my_wmaxd[a] = max(mxd, 0);
+      band_all[a] = make_int2(mxd >= 0 ? mn : -1, max(mxd, 0));  // per-layer (min, max) admissible disc
+    }
+    if (tid == 0) my_wmaxd[La] = 0;
+    bad = __reduce_or_sync(LG_FULL, bad);
+    if (lane == 0 && bad) atomicOr(&s_bad, bad);
+    __syncthreads();
+    if (tid == 0) s_status = (s_bad & 1) ? LGRECO_ENONFINITE : (s_bad ? LGRECO_EINVAL : LGRECO_OK);
+    __syncthreads();
+  }
   const uint64_t g = s_g[0];
   const int gsh = __ffsll((long long)g) - 1;
-  const int cbits = s_cbits;
+  LG_T(8);
   if (s_status != LGRECO_OK || La == 0) {  // identical in every CTA: no cluster barrier is pending
     if (rank == 0 && tid == 0 && grp == 0) {
       lgreco_solve_info inf = {};
       inf.n_active = La;
       inf.status = s_status;
       *info = inf;
-      if (ngroups > 1) jmeta->done = 1;  // k_solve_join has nothing to do
     }
     return;
   }
@@ -1106,21 +1199,72 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
   const uint64_t kmask = (1ull << kb) - 1;
   const int pdmask = (!wide && KT == 0) ? 0xFF : (int)((1u << cbits) - 1u);  // PD byte -> c
   auto keyed = [&](uint64_t ub, int c) -> uint64_t { return ((ub >> gsh) << kb) | (uint64_t)(c & (int)kmask); };
-  // two full-length rows (PAD INF cells + NC*S cells), in every CTA
   uint32_t* r32a = reinterpret_cast<uint32_t*>(smem_raw);
   uint32_t* r32b = r32a + row;
   uint64_t* r64a = reinterpret_cast<uint64_t*>(smem_raw);
   uint64_t* r64b = r64a + row;
   const uint32_t INF32 = 0x7FFFFF00u;
   const uint64_t INF64 = 1ull << 62;
-  // per-layer candidate tables for the whole recursion, staged once: {disc, 32-bit
-  // key} pairs (inadmissible and padding candidates = {0, INF}: they never win, so
-  // the inner loop has no branches), 64-bit keys, and the reachable band [lo, hi]
-  constexpr int KP2 = (KT + 2) & ~1;
-  uint2* cand_all = reinterpret_cast<uint2*>(
-      (reinterpret_cast<uintptr_t>(my_wmaxd + La + 1) + 15) & ~static_cast<uintptr_t>(15));  // [La][KP2], 16-B aligned
-  uint64_t* add_all = reinterpret_cast<uint64_t*>(cand_all + (size_t)La * (KT > 0 ? KP2 : 0));  // [La][KT]
-  int2* band_all = reinterpret_cast<int2*>(add_all + (size_t)La * KT);          // [La]
+  // (5) the layer split (ngroups == 2: a bottom group [0, h) and a top group [h, La) of
+  //     about equal estimated row cost -- a row costs ~1.8 K cycles plus its DSMEM pushes,
+  //     ~maxd / 16 cycles, C4 measured; every CTA computes the same h), the reachable
+  //     bands of this group's layers (exact: running sums of the smallest / largest
+  //     admissible disc from the zero row, saturating at D; a layer with no admissible
+  //     candidate empties every later band), the keyed candidate pairs, the rows
+  __shared__ int s_a0, s_a1;
+  if (ngroups > 1) {
+    long long tot = 0, wsum = 0;
+    for (int t0 = 0; t0 < La; t0 += NT) wsum += (t0 + tid < La) ? 1800 + my_wmaxd[t0 + tid] / 16 : 0;
+    bscan(wsum, &tot);
+    const long long half = (tot + 1) / 2;
+    long long carry = 0;
+    for (int t0 = 0; t0 < La; t0 += NT) {
+      const int a = t0 + tid;
+      const long long w = (a < La) ? 1800 + my_wmaxd[a] / 16 : 0;
+      long long tt;
+      const long long inc = bscan(w, &tt) + carry;
+      if (a < La && inc >= half && inc - w < half) {
+        const int h = min(max(a + 1, La > 1 ? 1 : 0), La > 1 ? La - 1 : La);
+        s_a0 = grp ? h : 0;
+        s_a1 = grp ? La : h;
+      }
+      carry += tt;
+    }
+    if (tid == 0 && grp == 1 && rank == 0) jmeta->ns = 0;  // E2 list (ordered by the init cluster barrier)
+  } else if (tid == 0) {
+    s_a0 = 0;
+    s_a1 = La;
+  }
+  __syncthreads();
+  const int a0 = s_a0, a1 = s_a1;
+  LG_T(15);
+  {
+    long long clo = 0, chi = 0, cdead = 0;
+    for (int t0 = a0; t0 < a1; t0 += NT) {
+      const int a = t0 + tid;
+      const int2 mm = (a < a1) ? band_all[a] : make_int2(0, 0);
+      long long lo = (mm.x >= 0) ? mm.x : 0, hi = mm.y, dd = (mm.x < 0) ? 1 : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const long long t1 = __shfl_up_sync(LG_FULL, lo, o), t2 = __shfl_up_sync(LG_FULL, hi, o),
+                        t3 = __shfl_up_sync(LG_FULL, dd, o);
+        if (lane >= o) { lo += t1; hi += t2; dd += t3; }
+      }
+      __shared__ long long s_b3[3][32];
+      if (lane == 31) { s_b3[0][warp] = lo; s_b3[1][warp] = hi; s_b3[2][warp] = dd; }
+      __syncthreads();
+      long long plo = clo, phi = chi, pdd = cdead;
+      for (int w2 = 0; w2 < warp; ++w2) { plo += s_b3[0][w2]; phi += s_b3[1][w2]; pdd += s_b3[2][w2]; }
+      long long tlo = clo, thi = chi, tdd = cdead;
+      for (int w2 = 0; w2 < NW; ++w2) { tlo += s_b3[0][w2]; thi += s_b3[1][w2]; tdd += s_b3[2][w2]; }
+      __syncthreads();
+      if (a < a1) {
+        lo += plo; hi += phi; dd += pdd;
+        band_all[a] = make_int2(dd ? 0x3fffffff : (int)min(lo, 0x3fffffffll), (int)min(hi, (long long)D));
+      }
+      clo = tlo; chi = thi; cdead = tdd;
+    }
+  }
   for (int i = tid; KT > 0 && i < La * KP2; i += NT) {
     const int aa = i / KP2, c = i - aa * KP2;
     const int32_t d = (c < K) ? my_wdisc[aa * K + c] : -1;
@@ -1129,87 +1273,7 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
     cand_all[i] = make_uint2(ok ? (uint32_t)d : 0u, ok ? (uint32_t)k : INF32);
     if (c < KT) add_all[aa * KT + c] = ok ? k : INF64;
   }
-  __syncthreads();  // the prelude's shared staging (front of smem) is dead from here
-  LG_T(9);
-  // Layer groups (ngroups == 2): the active layers split into a bottom group [0, h) and a
-  // top group [h, La) of about equal estimated row cost (a row costs a fixed ~1 K cycles
-  // plus its DSMEM pushes, ~maxd / 5 cycles); every CTA computes the same h.
-  __shared__ int s_a0, s_a1;
-  if (warp == 0) {
-    int a0 = 0, a1 = La;
-    if (ngroups > 1) {
-      long long tot = 0;
-      for (int base = 0; base < La; base += 32) {
-        const int aa = base + lane;
-        long long w = (aa < La) ? 1024 + my_wmaxd[aa] / 5 : 0;
-#pragma unroll
-        for (int o = 16; o; o >>= 1) w += __shfl_xor_sync(LG_FULL, w, o);
-        tot += w;
-      }
-      const long long half = (tot + 1) / 2;
-      long long run = 0;
-      int h = La;
-      for (int base = 0; base < La; base += 32) {
-        const int aa = base + lane;
-        long long w = (aa < La) ? 1024 + my_wmaxd[aa] / 5 : 0;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const long long t = __shfl_up_sync(LG_FULL, w, o);
-          if (lane >= o) w += t;
-        }
-        const unsigned m = __ballot_sync(LG_FULL, aa < La && run + w >= half);
-        if (m) { h = base + __ffs(m) - 1 + 1; break; }
-        run += __shfl_sync(LG_FULL, w, 31);
-      }
-      h = min(max(h, La > 1 ? 1 : 0), La > 1 ? La - 1 : La);
-      a0 = grp ? h : 0;
-      a1 = grp ? La : h;
-      if (grp == 0 && rank == 0 && lane == 0) jmeta->h = h;
-    }
-    if (lane == 0) { s_a0 = a0; s_a1 = a1; }
-  }
-  __syncthreads();
-  const int a0 = s_a0, a1 = s_a1;
-  // bands: running sums of the smallest / largest admissible disc (exact reachable
-  // set bounds) over this group's layers, from the zero row.  Warp 0 scans the layers
-  // 32 at a time; a layer with no admissible candidate empties every later band.
-  if (warp == 0) {
-    long long slo = 0;
-    int shi = 0;
-    bool dead = false;
-    for (int base = a0; base < a1; base += 32) {
-      const int aa = base + lane;
-      int mn = 0, mxd = 0;
-      bool any = true;
-      if (aa < a1) {
-        int m1 = 0x7fffffff, m2 = -1;
-        for (int c = 0; c < K; ++c) {
-          const int d = my_wdisc[aa * K + c];
-          if (d >= 0) { m1 = min(m1, d); m2 = max(m2, d); }
-        }
-        any = m2 >= 0;
-        mn = any ? m1 : 0;
-        mxd = any ? m2 : 0;
-      }
-      long long plo = mn;
-      int phi = mxd;
-      unsigned dead_m = __ballot_sync(LG_FULL, !any);
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const long long t1 = __shfl_up_sync(LG_FULL, plo, o);
-        const int t2 = __shfl_up_sync(LG_FULL, phi, o);
-        if (lane >= o) { plo += t1; phi = min(phi + t2, D); }
-      }
-      const bool dead_here = dead || (dead_m & ((2u << lane) - 1u)) != 0;
-      if (aa < a1) {
-        const long long lo_v = slo + plo;
-        band_all[aa] = make_int2(dead_here ? 0x3fffffff : (int)min(lo_v, 0x3fffffffll), min(shi + phi, D));
-      }
-      slo += __shfl_sync(LG_FULL, plo, 31);
-      shi = min(shi + __shfl_sync(LG_FULL, phi, 31), D);
-      dead = dead || dead_m != 0;
-    }
-  }
+  LG_T(16);
   if (!wide) {  // three row buffers (the 16-byte-per-cell region holds four u32 rows)
     for (int i = tid; i < row; i += NT) { r32a[i] = (i == PAD) ? 0u : INF32; r32b[i] = INF32; r32b[row + i] = INF32; }
   } else {
@@ -1234,6 +1298,7 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
       s_ak[slot][tid] = ok ? k : INF64;
     }
   };
+  LG_T(17);
   if (KT == 0 && a0 < a1) stage0((tid < K) ? my_wdisc[a0 * K + tid] : -1, (tid < K) ? my_wadd[a0 * K + tid] : 0, 0);
   LG_T(1);
   cl_sync();  // every CTA's rows and barriers initialised before any remote push lands
@@ -1266,7 +1331,10 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
     const int sk = (a - a0) & 1;  // KT == 0 candidate staging slot of row a
     // cells of row a this CTA receives: [cbase - maxd, cbase) (clipped at 0)
     if (tid == 0) {
-      const uint32_t bytes = (uint32_t)min(maxd, cbase) * vb;
+      uint32_t bytes = (uint32_t)min(maxd, cbase) * vb;
+#ifdef LG_DP_TIMING
+      if (flags & (1u << 30)) bytes = 0;  // diagnostic: no pushes (wrong result)
+#endif
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
                        (uint32_t)__cvta_generic_to_shared(&s_bar[sb])),
                    "r"(bytes)
@@ -1444,34 +1512,221 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
   if (!wide) asm volatile("barrier.cluster.wait.aligned;" ::: "memory");  // pairs the last arrive
   LG_T(3);
   if (ngroups > 1) {
-    // this group's last row (values in units of 2^gsh bits; ~0 = unreachable) for
-    // k_solve_join, and (group 0, rank 0) the shared facts of the prelude
-    uint64_t* ro = rowout + (size_t)grp * (D + 1);
-    for (int el = tid; el < S; el += NT) {
-      const int e = cbase + el;
-      if (e > D) break;
-      uint64_t v;
-      if (!wide) { const uint32_t x = (r32a + (size_t)bp * row + PAD)[e]; v = (x >= INF32) ? ~0ull : (x >> kb); }
-      else { const uint64_t x = (r64a + (size_t)bp * row + PAD)[e]; v = (x >= INF64) ? ~0ull : (x >> kb); }
-      ro[e] = v;
-    }
-    if (grp == 0 && rank == 0) {
-      if (KT > 0)
-        for (int i = tid; i < La * K; i += NT) wdisc[i] = my_wdisc[i];
+    // ---- the join of the two layer groups (see "Layer groups" below), in the top
+    //      group's cluster: its last row P stays in its CTAs' shared memory
+    const uint64_t NONE = ~0ull;
+    auto rowv = [&](int e) -> uint64_t {  // last row's value at cell e (units of 2^gsh bits)
+      if (e > D) return NONE;
+      if (!wide) {
+        const uint32_t x = (r32a + (size_t)bp * row + PAD)[e];
+        return (x >= INF32) ? NONE : (uint64_t)(x >> kb);
+      }
+      const uint64_t x = (r64a + (size_t)bp * row + PAD)[e];
+      return (x >= INF64) ? NONE : (x >> kb);
+    };
+    uint64_t* F = rowout;                                           // group 0's last row
+    int32_t* gsurv = reinterpret_cast<int32_t*>(rowout + (D + 1));  // the E2 list
+    if (grp == 0) {
+      for (int el = tid; el < S; el += NT) {
+        const int e = cbase + el;
+        if (e > D) break;
+        __stcg(F + e, rowv(e));
+      }
+      __syncthreads();
       if (tid == 0) {
-        jmeta->done = 0;
-        jmeta->La = La;
-        jmeta->cm = pdmask;
-        jmeta->PDR = PDR;
-        jmeta->emax = emax;
-        jmeta->defbits = s_defbits;
+        __threadfence();
+        st_release_gpu(&jmeta->tok[rank], tok);  // this slice of F (and every PD row) is written
+      }
+      return;
+    }
+    // (1) prefix minima of P with their first index: a chunk of CPT cells per thread,
+    //     block scan, then the slices below this CTA's (their totals over DSMEM)
+    __shared__ uint64_t s_slv[CL_MAX];
+    __shared__ int s_sli[CL_MAX];
+    uint64_t* PMs = reinterpret_cast<uint64_t*>(smem_raw + (size_t)(wide ? 8 : 4) * bc * row);  // a free row buffer
+    int32_t* PAs = reinterpret_cast<int32_t*>(PMs + S);
+    const int c0 = tid * CPT;
+    uint64_t pv[CPT];
+    uint64_t mv = NONE;
+    int mi = -1;
+#pragma unroll
+    for (int j = 0; j < CPT; ++j) {
+      pv[j] = rowv(cbase + c0 + j);
+      if (pv[j] < mv) { mv = pv[j]; mi = cbase + c0 + j; }
+    }
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {  // inclusive scan, the earlier operand winning ties
+      const uint64_t ov = __shfl_up_sync(LG_FULL, mv, o);
+      const int oi = __shfl_up_sync(LG_FULL, mi, o);
+      if (lane >= o && ov <= mv) { mv = ov; mi = oi; }
+    }
+    if (lane == 31) { s_redk[warp] = mv; s_rede[warp] = mi; }
+    __syncthreads();
+    if (warp == 0) {
+      uint64_t wv = (lane < NW) ? s_redk[lane] : NONE;
+      int wi = (lane < NW) ? s_rede[lane] : -1;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t ov = __shfl_up_sync(LG_FULL, wv, o);
+        const int oi = __shfl_up_sync(LG_FULL, wi, o);
+        if (lane >= o && ov <= wv) { wv = ov; wi = oi; }
+      }
+      s_redk[lane] = wv;  // inclusive over warps 0..lane
+      s_rede[lane] = wi;
+      const uint64_t tv = __shfl_sync(LG_FULL, wv, NW - 1);  // the slice's minimum
+      const int ti = __shfl_sync(LG_FULL, wi, NW - 1);
+      if (lane < (int)NC) {
+        cl_st(cl_map(&s_slv[rank], (uint32_t)lane), tv);
+        cl_st(cl_map(&s_sli[rank], (uint32_t)lane), (uint32_t)ti);
       }
     }
+    cl_sync();  // the slice minima of every CTA landed; s_redk / s_rede complete
+    {
+      uint64_t cv = NONE;  // prefix over the lower slices, then the lower threads of this one
+      int ci = -1;
+      for (uint32_t r2 = 0; r2 < rank; ++r2)
+        if (s_slv[r2] < cv) { cv = s_slv[r2]; ci = s_sli[r2]; }
+      uint64_t ev = (warp > 0) ? s_redk[warp - 1] : NONE;
+      int ei = (warp > 0) ? s_rede[warp - 1] : -1;
+      const uint64_t lv = __shfl_up_sync(LG_FULL, mv, 1);
+      const int li = __shfl_up_sync(LG_FULL, mi, 1);
+      if (lane > 0 && lv < ev) { ev = lv; ei = li; }
+      if (ev < cv) { cv = ev; ci = ei; }
+#pragma unroll
+      for (int j = 0; j < CPT; ++j) {
+        if (pv[j] < cv) { cv = pv[j]; ci = cbase + c0 + j; }
+        PMs[c0 + j] = cv;
+        PAs[c0 + j] = ci;
+      }
+    }
+    // (2) group 0's F: wait for its 16 slices
+    if (tid < (int)NC)
+      while (ld_acquire_gpu(&jmeta->tok[tid]) != tok) __nanosleep(64);
+    __syncthreads();
+    LG_T(4);
+    // (3) C* = min_{e1} F[e1] + PM[D - e1] and e* = the smallest e1 + PA[D - e1] attaining
+    //     it: x = D - e1 runs over this CTA's cells (order-free: a lexicographic minimum)
+    uint64_t bv = NONE;
+    int be = 0x7fffffff;
+    {
+      uint64_t fv[CPT];
+#pragma unroll
+      for (int j = 0; j < CPT; ++j) {
+        const int x = cbase + c0 + j;
+        fv[j] = (x <= D) ? __ldcg(F + (D - x)) : NONE;
+      }
+#pragma unroll
+      for (int j = 0; j < CPT; ++j) {
+        const uint64_t pm = PMs[c0 + j];
+        if (fv[j] == NONE || pm == NONE) continue;
+        const uint64_t v = fv[j] + pm;
+        const int e = D - (cbase + c0 + j) + PAs[c0 + j];
+        if (v < bv || (v == bv && e < be)) { bv = v; be = e; }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const uint64_t ov = __shfl_xor_sync(LG_FULL, bv, o);
+      const int oe = __shfl_xor_sync(LG_FULL, be, o);
+      if (ov < bv || (ov == bv && oe < be)) { bv = ov; be = oe; }
+    }
+    __syncthreads();  // s_redk / s_rede reads of (1) done
+    if (lane == 0) { s_redk[warp] = bv; s_rede[warp] = be; }
+    __syncthreads();
+    if (warp == 0) {
+      bv = (lane < NW) ? s_redk[lane] : NONE;
+      be = (lane < NW) ? s_rede[lane] : 0x7fffffff;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const uint64_t ov = __shfl_xor_sync(LG_FULL, bv, o);
+        const int oe = __shfl_xor_sync(LG_FULL, be, o);
+        if (ov < bv || (ov == bv && oe < be)) { bv = ov; be = oe; }
+      }
+      if (lane < (int)NC) {
+        cl_st(cl_map(&s_clk[rank], (uint32_t)lane), bv);
+        cl_st(cl_map(&s_cle[rank], (uint32_t)lane), (uint32_t)be);
+      }
+    }
+    cl_sync();
+    uint64_t Cs = NONE;
+    int es = 0x7fffffff;
+    for (int r2 = 0; r2 < (int)NC; ++r2)
+      if (s_clk[r2] < Cs || (s_clk[r2] == Cs && s_cle[r2] < es)) { Cs = s_clk[r2]; es = s_cle[r2]; }
+    const int used_default = (Cs == NONE);
+    // (4) E2 = {e2 <= e* : F[e* - e2] + P[e2] == C*} over this CTA's cells (global list)
+    if (!used_default) {
+      uint64_t fv[CPT];
+#pragma unroll
+      for (int j = 0; j < CPT; ++j) {
+        const int x = cbase + c0 + j;
+        fv[j] = (x <= es && pv[j] != NONE) ? __ldcg(F + (es - x)) : NONE;
+      }
+#pragma unroll
+      for (int j = 0; j < CPT; ++j)
+        if (fv[j] != NONE && fv[j] + pv[j] == Cs) gsurv[atomicAdd(&jmeta->ns, 1)] = cbase + c0 + j;
+      __threadfence();
+    }
+    cl_sync();
+    LG_T(18);
+    if (rank != 0) return;
+    // (5) rank 0: the lexicographic walk of the top group while several E2 entries
+    //     survive, the two backtracks (one warp each), R20 check and summary
+    __shared__ int s_cnt[2], s_m;
+    int32_t* bch = reinterpret_cast<int32_t*>(smem_raw);  // [La] (the rows are dead)
+    int2* const sv0 = reinterpret_cast<int2*>(smem_raw + (((size_t)La * 4 + 15) & ~(size_t)15));
+    int2* const sv1 = sv0 + (D + 1);
+    double* sm_ce = reinterpret_cast<double*>(sv0);  // finish_plan's scratch (after the walk)
+    const int h = a0;
+    if (!used_default) {
+      const int ns0 = __ldcg(&jmeta->ns);
+      for (int i = tid; i < ns0; i += NT) { const int e2 = __ldcg(gsurv + i); sv0[i] = make_int2(e2, e2); }
+      if (tid == 0) { s_cnt[0] = ns0; s_m = 0x7fffffff; }
+      __syncthreads();
+      int ns = ns0, cur = 0, a = La - 1;
+      while (ns > 1 && a >= h) {
+        const int2* svc = cur ? sv1 : sv0;
+        int2* svn = cur ? sv0 : sv1;
+        for (int i = tid; i < ns; i += NT) atomicMin(&s_m, pd_cm(PD, PDR, a, svc[i].x) & pdmask);
+        if (tid == 0) s_cnt[cur ^ 1] = 0;
+        __syncthreads();
+        const int m = s_m;
+        const int dm = my_wdisc[a * K + m];
+        for (int i = tid; i < ns; i += NT) {
+          const int2 w = svc[i];
+          if ((pd_cm(PD, PDR, a, w.x) & pdmask) == m) svn[atomicAdd(&s_cnt[cur ^ 1], 1)] = make_int2(w.x - dm, w.y);
+        }
+        if (tid == 0) bch[a] = m;
+        __syncthreads();
+        ns = s_cnt[cur ^ 1];
+        cur ^= 1;
+        if (tid == 0) s_m = 0x7fffffff;
+        --a;
+        __syncthreads();
+      }
+      const int2 w = (cur ? sv1 : sv0)[0];
+      LG_T(19);
+      if (warp == 0 && a >= h) bt_warp(PD, PDR, my_wdisc, K, pdmask, a, h, w.x, bch);
+      if (warp == (NW > 1 ? 1 : 0) && h > 0) bt_warp(PD, PDR, my_wdisc, K, pdmask, h - 1, 0, es - w.y, bch);
+    }
+    __syncthreads();
+    LG_T(5);
+    __shared__ int s_fl;
+    finish_plan(used_default, bch, La, act, default_idx, err, bits, K, flags, emax, s_defbits, choice, info, sm_ce,
+                &s_fl);
 #ifdef LG_DP_TIMING
-    if (rank == 0 && tid == 0)
-      printf("dp group %d: layers [%d, %d) of %d: prelude %lld init %lld rows %lld (%lld/layer)\n", grp, a0, a1, La,
-             tstamp[1] - tstamp[0], tstamp[2] - tstamp[1], tstamp[3] - tstamp[2],
-             (tstamp[3] - tstamp[2]) / (a1 > a0 ? a1 - a0 : 1));
+    if (tid == 0)
+      printf("dp prelude detail: pdl %lld table+active %lld emax||costs %lld disc %lld split %lld band+cand %lld "
+             "rowinit+bars %lld sync %lld\n", tstamp[10] - tstamp[0], tstamp[6] - tstamp[10], tstamp[7] - tstamp[6],
+             tstamp[8] - tstamp[7], tstamp[15] - tstamp[8], tstamp[16] - tstamp[15], tstamp[17] - tstamp[16],
+             tstamp[2] - tstamp[17]);
+    if (tid == 0)
+      printf("dp join detail: join %lld walk-setup %lld backtrack %lld\n", tstamp[18] - tstamp[4],
+             tstamp[19] - tstamp[18], tstamp[5] - tstamp[19]);
+    if (tid == 0)
+      printf("dp group 1 (join in-cluster): layers [%d, %d) of %d: prelude %lld init %lld rows %lld (%lld/layer) "
+             "P-scan+F-wait %lld join+backtrack %lld summary %lld\n", a0, a1, La, tstamp[1] - tstamp[0],
+             tstamp[2] - tstamp[1], tstamp[3] - tstamp[2], (tstamp[3] - tstamp[2]) / (a1 > a0 ? a1 - a0 : 1),
+             tstamp[4] - tstamp[3], tstamp[5] - tstamp[4], clock64() - tstamp[5]);
 #endif
     return;
   }
@@ -1549,10 +1804,13 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
 // ---------------------------------------------------------------------------
 // Layer groups.  With ngroups == 2, k_solve_cl's two clusters run Alg.1's row recursion
 // for the bottom active layers [0, h) and for the top layers [h, La) concurrently, each
-// from the zero row, and write their last rows F (bottom) and P (top): the critical path
-// of the solve halves.  The whole recursion's last row is their min-plus convolution,
-// DP[e] = min_{e1} F[e1] + P[e - e1] (min-plus is associative), and k_solve_join returns
-// exactly Alg.1's plan without forming it:
+// from the zero row: the critical path of the solve halves.  The bottom cluster writes its
+// last row F to global memory and releases the launch's token per CTA; the top cluster
+// keeps its last row P in its CTAs' shared memory (a slice per CTA), waits for the 16
+// tokens and joins (the bottom cluster never waits, so co-scheduling is not required).
+// The whole recursion's last row is their min-plus convolution, DP[e] = min_{e1} F[e1] +
+// P[e - e1] (min-plus is associative), and the join returns exactly Alg.1's plan without
+// forming it:
 //  * C* = min_{e <= D} DP[e] = min_{e1} F[e1] + PM[D - e1], PM = prefix minima of P;
 //  * e* = the smallest e attaining C* (line 23, R19) = the smallest e1 + PA[D - e1] over
 //    the e1 attaining C*, PA[x] = the first index of P's minimum over [0, x];
@@ -1565,180 +1823,10 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
 //    at once and, layer by layer, only the walks with the smallest candidate survive;
 //    the last survivor's e2 fixes e1 = e* - e2 and the bottom group's own backtrack from
 //    e1 gives the bottom layers.  (Usually |E2| = 1 and both backtracks run at once on
-//    two warps.)
+//    two warps, PD read from L2.)
 // Checked against a sequential reference on 600 random tie-heavy instances for every
 // split point (K4), and bit-exact against the oracle in tests/test_gpu_dp.py.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(1024, 1)
-k_solve_join(const double* __restrict__ err, const int64_t* __restrict__ bits, int L, int K,
-             const int32_t* __restrict__ default_idx, int D, uint32_t flags, int32_t* __restrict__ choice,
-             lgreco_solve_info* __restrict__ info, const uint8_t* __restrict__ PD, const int32_t* __restrict__ act,
-             const int32_t* __restrict__ wdisc, const uint64_t* __restrict__ rowout,
-             const JoinMeta* __restrict__ jmeta) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ JoinMeta M;
-  __shared__ uint64_t s_rv[32];
-  __shared__ int s_re[32];
-  __shared__ int s_flag, s_cnt[2], s_m;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, NT = blockDim.x, NW = NT >> 5;
-#ifdef LG_DP_TIMING
-  long long tj[8] = {0};
-#define LG_TJ(i) do { if (tid == 0) tj[i] = clock64(); } while (0)
-#else
-#define LG_TJ(i) do { } while (0)
-#endif
-  pdl_wait();  // the two groups' rows, PD and meta
-  LG_TJ(0);
-  if (tid == 0) { M = *jmeta; s_cnt[0] = 0; s_cnt[1] = 0; s_m = 0x7fffffff; }
-  __syncthreads();
-  if (M.done) return;
-  const int La = M.La, h = M.h, cm = M.cm;
-  const int64_t PDR = M.PDR;
-  const int W1 = D + 1;
-  const uint64_t NONE = ~0ull;
-  const uint64_t* F = rowout;
-  const uint64_t* P = rowout + W1;
-  // shared memory: [16 W1 B: PM u64 + PA i32, later two survivor buffers] [disc La*K] [bch La] [summary 16 La]
-  uint64_t* PM = reinterpret_cast<uint64_t*>(smem_raw);
-  int32_t* PA = reinterpret_cast<int32_t*>(PM + W1);
-  int2* const sv0 = reinterpret_cast<int2*>(smem_raw);  // survivor buffers (ping-pong)
-  int2* const sv1 = sv0 + W1;
-  int32_t* sdisc = reinterpret_cast<int32_t*>(smem_raw + (size_t)16 * W1);
-  int32_t* bch = sdisc + (size_t)La * K;
-  double* sm_ce = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(bch + La) + 15) & ~static_cast<uintptr_t>(15));
-  for (int i = tid; i < La * K; i += NT) sdisc[i] = __ldcg(wdisc + i);
-  // ---- prefix minima of P with their first index (chunk per thread, block scan)
-  const int CH = (W1 + NT - 1) / NT;
-  const int x0 = min(tid * CH, W1), x1 = min(x0 + CH, W1);
-  uint64_t mv = NONE;
-  int mi = -1;
-  for (int x = x0; x < x1; ++x) {
-    const uint64_t v = __ldcg(P + x);
-    if (v < mv) { mv = v; mi = x; }
-  }
-  // inclusive scan over the threads, the earlier operand winning ties
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint64_t ov = __shfl_up_sync(LG_FULL, mv, o);
-    const int oi = __shfl_up_sync(LG_FULL, mi, o);
-    if (lane >= o && ov <= mv) { mv = ov; mi = oi; }
-  }
-  if (lane == 31) { s_rv[warp] = mv; s_re[warp] = mi; }
-  __syncthreads();
-  if (warp == 0) {
-    uint64_t wv = (lane < NW) ? s_rv[lane] : NONE;
-    int wi = (lane < NW) ? s_re[lane] : -1;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint64_t ov = __shfl_up_sync(LG_FULL, wv, o);
-      const int oi = __shfl_up_sync(LG_FULL, wi, o);
-      if (lane >= o && ov <= wv) { wv = ov; wi = oi; }
-    }
-    s_rv[lane] = wv;  // inclusive over warps 0..lane
-    s_re[lane] = wi;
-  }
-  __syncthreads();
-  {
-    // exclusive prefix of this thread = inclusive of warps < warp, then of lanes < lane
-    uint64_t ev = (warp > 0) ? s_rv[warp - 1] : NONE;
-    int ei = (warp > 0) ? s_re[warp - 1] : -1;
-    const uint64_t lv = __shfl_up_sync(LG_FULL, mv, 1);
-    const int li = __shfl_up_sync(LG_FULL, mi, 1);
-    if (lane > 0 && lv < ev) { ev = lv; ei = li; }
-    for (int x = x0; x < x1; ++x) {
-      const uint64_t v = __ldcg(P + x);
-      if (v < ev) { ev = v; ei = x; }
-      PM[x] = ev;
-      PA[x] = ei;
-    }
-  }
-  __syncthreads();
-  LG_TJ(1);
-  // ---- C* and e*: the smallest (value, e) over e1 of (F[e1] + PM[D - e1], e1 + PA[D - e1])
-  uint64_t bv = NONE;
-  int be = 0x7fffffff;
-  for (int e1 = x0; e1 < x1; ++e1) {
-    const uint64_t f = __ldcg(F + e1);
-    const uint64_t pm = PM[D - e1];
-    if (f == NONE || pm == NONE) continue;
-    const uint64_t v = f + pm;
-    const int e = e1 + PA[D - e1];
-    if (v < bv || (v == bv && e < be)) { bv = v; be = e; }
-  }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    const uint64_t ov = __shfl_xor_sync(LG_FULL, bv, o);
-    const int oe = __shfl_xor_sync(LG_FULL, be, o);
-    if (ov < bv || (ov == bv && oe < be)) { bv = ov; be = oe; }
-  }
-  __syncthreads();  // PM / PA reads done before s_rv is reused
-  if (lane == 0) { s_rv[warp] = bv; s_re[warp] = be; }
-  __syncthreads();
-  if (warp == 0) {
-    bv = (lane < NW) ? s_rv[lane] : NONE;
-    be = (lane < NW) ? s_re[lane] : 0x7fffffff;
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      const uint64_t ov = __shfl_xor_sync(LG_FULL, bv, o);
-      const int oe = __shfl_xor_sync(LG_FULL, be, o);
-      if (ov < bv || (ov == bv && oe < be)) { bv = ov; be = oe; }
-    }
-    if (lane == 0) { s_rv[0] = bv; s_re[0] = be; }
-  }
-  __syncthreads();
-  const uint64_t Cs = s_rv[0];
-  const int es = s_re[0];
-  const int used_default = (Cs == NONE);
-  LG_TJ(2);
-  int nsurv = 0;
-  if (!used_default) {
-    // ---- E2 = {e2 in [0, e*] : F[e* - e2] + P[e2] == C*} (the PM / PA area is dead)
-    for (int e2 = tid; e2 <= es; e2 += NT) {
-      const uint64_t f = __ldcg(F + es - e2), p = __ldcg(P + e2);
-      if (f != NONE && p != NONE && f + p == Cs) sv0[atomicAdd(&s_cnt[0], 1)] = make_int2(e2, e2);
-    }
-    __syncthreads();
-    int ns = s_cnt[0], cur = 0, a = La - 1;
-    nsurv = ns;
-    LG_TJ(3);
-    // ---- top layers while several walks survive: the smallest candidate per layer
-    while (ns > 1 && a >= h) {
-      const int2* svc = cur ? sv1 : sv0;
-      int2* svn = cur ? sv0 : sv1;
-      for (int i = tid; i < ns; i += NT) atomicMin(&s_m, pd_cm(PD, PDR, a, svc[i].x) & cm);
-      if (tid == 0) s_cnt[cur ^ 1] = 0;
-      __syncthreads();
-      const int m = s_m;
-      const int dm = sdisc[a * K + m];
-      for (int i = tid; i < ns; i += NT) {
-        const int2 w = svc[i];
-        if ((pd_cm(PD, PDR, a, w.x) & cm) == m) svn[atomicAdd(&s_cnt[cur ^ 1], 1)] = make_int2(w.x - dm, w.y);
-      }
-      if (tid == 0) bch[a] = m;
-      __syncthreads();
-      ns = s_cnt[cur ^ 1];
-      cur ^= 1;
-      if (tid == 0) s_m = 0x7fffffff;
-      --a;
-      __syncthreads();
-    }
-    const int2 w = (cur ? sv1 : sv0)[0];
-    if (warp == 0 && a >= h) bt_warp(PD, PDR, sdisc, K, cm, a, h, w.x, bch);
-    if (warp == 1 && h > 0) bt_warp(PD, PDR, sdisc, K, cm, h - 1, 0, es - w.y, bch);
-  }
-  __syncthreads();
-  LG_TJ(4);
-  finish_plan(used_default, bch, La, act, default_idx, err, bits, K, flags, M.emax, M.defbits, choice, info, sm_ce,
-              &s_flag);
-#ifdef LG_DP_TIMING
-  LG_TJ(5);
-  if (tid == 0)
-    printf("dp join: h %d La %d |E2| %d: prefix-min %lld C*/e* %lld E2 %lld backtrack %lld summary %lld\n", h, La,
-           nsurv, tj[1] - tj[0], tj[2] - tj[1], tj[3] - tj[2], tj[4] - tj[3], tj[5] - tj[4]);
-#endif
-#undef LG_TJ
-}
-
 // Weighted costs (NEXT-1): out = bits * w[l], exact in int64; -1 on a negative input or
 // overflow (lgreco_solve rejects negative costs with LGRECO_EINVAL).
 __global__ void k_weight_costs(const int64_t* __restrict__ bits, const int64_t* __restrict__ w, int L, int K,
@@ -1802,11 +1890,13 @@ static cudaError_t launch_solve_cluster(const SolveArgs& a, uint8_t* pd, int32_t
   const size_t smem = smem_of(kt0);
   if (smem > 220 * 1024 || (size_t)24 * a.L + 64 > rows_b) return cudaErrorNotSupported;
   const int kt = kt0;
-  // layer groups: K <= 16 (tables in shared memory) and the join's 16 (D + 1) B of rows
-  const size_t join_smem = (size_t)16 * (a.D + 1) + (size_t)4 * a.L * a.K + (size_t)4 * a.L + (size_t)16 * a.L + 32;
-  if (ngroups > 1 && (kt == 0 || join_smem > 220 * 1024)) return cudaErrorNotSupported;
+  // layer groups: K <= 16 (tables in shared memory); the top group's rank 0 walks the
+  // E2 list in the row space ([La] choices, two (D + 1)-entry int2 lists)
+  if (ngroups > 1 && (size_t)4 * a.L + 16 + (size_t)16 * (a.D + 1) > rows_b) return cudaErrorNotSupported;
+  if (ngroups > 1 && kt == 0) return cudaErrorNotSupported;
   void (*fn)(const double*, const int64_t*, int, int, const int32_t*, const int32_t*, int, uint32_t, int32_t*,
-             lgreco_solve_info*, uint8_t*, int32_t*, int32_t*, uint64_t*, int32_t*, int, uint64_t*, JoinMeta*) = nullptr;
+             lgreco_solve_info*, uint8_t*, int32_t*, int32_t*, uint64_t*, int32_t*, int, uint64_t*, JoinMeta*,
+             uint64_t) = nullptr;
 #define LG_CL(C, KT) if (cpt == C && kt == KT) fn = k_solve_cl<C, KT>;
 #define LG_CL_K(C) LG_CL(C, 4) LG_CL(C, 5) LG_CL(C, 7) LG_CL(C, 8) LG_CL(C, 16) LG_CL(C, 0)
   LG_CL_K(1) LG_CL_K(2) LG_CL_K(4) LG_CL_K(8)
@@ -1814,35 +1904,18 @@ static cudaError_t launch_solve_cluster(const SolveArgs& a, uint8_t* pd, int32_t
 #undef LG_CL
   if (!fn) return cudaErrorNotSupported;
   // attribute + cluster-occupancy checks are host-side driver calls (tens of us): done
-  // once per (kernel, shared memory, block) configuration and cached
-  struct CfgKey { const void* fn; size_t smem; int nt, nc, ng; int ok; };
-  static CfgKey cache[16];
-  static int ncache = 0;
-  int cached = -1;
-  for (int i = 0; i < ncache; ++i)
-    if (cache[i].fn == (const void*)fn && cache[i].smem == smem && cache[i].nt == nt && cache[i].nc == NC &&
-        cache[i].ng == ngroups)
-      cached = i;
-  if (cached >= 0 && !cache[cached].ok) return cudaErrorNotSupported;
+  // once per (device, kernel, shared memory, block) configuration and memoised (memo.h)
+  long long okm = -1;
+  const bool cached = memo_get((const void*)fn, (long long)smem, nt, NC, ngroups, &okm);
+  if (cached && !okm) return cudaErrorNotSupported;
   cudaError_t e = cudaSuccess;
-  if (cached < 0) {
-    // the attribute is the kernel's maximum dynamic size: only ever raised (a launch of a
-    // smaller configuration must not lower it under a cached larger one)
-    struct FnMax { const void* fn; size_t smem; };
-    static FnMax fmax[32];
-    static int nfmax = 0;
-    int fi = -1;
-    for (int i = 0; i < nfmax; ++i) if (fmax[i].fn == (const void*)fn) fi = i;
+  if (!cached) {
     if (NC > 8 && cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
       cudaGetLastError();
       return cudaErrorNotSupported;
     }
-    if (fi < 0 || fmax[fi].smem < smem) {
-      e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) { cudaGetLastError(); return cudaErrorNotSupported; }
-      if (fi < 0 && nfmax < 32) fmax[nfmax++] = FnMax{(const void*)fn, smem};
-      else if (fi >= 0) fmax[fi].smem = smem;
-    }
+    e = memo_smem_attr((const void*)fn, smem);
+    if (e != cudaSuccess) { cudaGetLastError(); return cudaErrorNotSupported; }
   }
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[2];
@@ -1858,15 +1931,11 @@ static cudaError_t launch_solve_cluster(const SolveArgs& a, uint8_t* pd, int32_t
   cfg.stream = st;
   cfg.attrs = attr;
   cfg.numAttrs = 1;  // (occupancy query without PDL)
-  if (cached < 0) {
+  if (!cached) {
     int nclusters = 0;
     e = cudaOccupancyMaxActiveClusters(&nclusters, (const void*)fn, &cfg);
     const int ok = (e == cudaSuccess && nclusters >= ngroups) ? 1 : 0;
-    if (ok && ngroups > 1) {
-      e = cudaFuncSetAttribute(k_solve_join, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-      if (e != cudaSuccess) { cudaGetLastError(); return cudaErrorNotSupported; }
-    }
-    if (ncache < 16) cache[ncache++] = CfgKey{(const void*)fn, smem, nt, NC, ngroups, ok};
+    memo_put((const void*)fn, (long long)smem, nt, NC, ngroups, ok);
     if (!ok) {
       if (getenv("LGRECO_DEBUG")) fprintf(stderr, "lgreco: cluster occupancy %d (%s)\n", nclusters, cudaGetErrorString(e));
       cudaGetLastError();
@@ -1874,21 +1943,11 @@ static cudaError_t launch_solve_cluster(const SolveArgs& a, uint8_t* pd, int32_t
     }
   }
   cfg.numAttrs = 2;
-  e = cudaLaunchKernelEx(&cfg, fn, a.err, a.bits, a.L, a.K, a.default_idx, a.compress, a.D, a.flags, a.choice, a.info,
-                         pd, act, wdisc, wadd, wmaxd, ngroups, rowout, jmeta);
-  if (e != cudaSuccess || ngroups == 1) return e;
-  // the join: one CTA, launched programmatically (its griddepcontrol.wait returns once
-  // both groups' rows, PD and meta are written)
-  cudaLaunchConfig_t jc = {};
-  jc.gridDim = dim3(1, 1, 1);
-  jc.blockDim = dim3(1024, 1, 1);
-  jc.dynamicSmemBytes = join_smem;
-  jc.stream = st;
-  jc.attrs = &attr[1];
-  jc.numAttrs = 1;
-  return cudaLaunchKernelEx(&jc, k_solve_join, a.err, a.bits, a.L, a.K, a.default_idx, a.D, a.flags, a.choice, a.info,
-                            (const uint8_t*)pd, (const int32_t*)act, (const int32_t*)wdisc, (const uint64_t*)rowout,
-                            (const JoinMeta*)jmeta);
+  // the launch's token (the group handshake): unique per launch in this process
+  static std::atomic<uint64_t> g_tok{0x9E3779B97F4A7C15ull ^ ((uint64_t)time(nullptr) << 24) ^ (uint64_t)getpid()};
+  const uint64_t tok = g_tok.fetch_add(2) | 1ull;
+  return cudaLaunchKernelEx(&cfg, fn, a.err, a.bits, a.L, a.K, a.default_idx, a.compress, a.D, a.flags, a.choice, a.info,
+                            pd, act, wdisc, wadd, wmaxd, ngroups, rowout, jmeta, tok);
 }
 
 cudaError_t launch_solve(const SolveArgs& a, void* ws, cudaStream_t st) {
@@ -1928,7 +1987,7 @@ cudaError_t launch_solve(const SolveArgs& a, void* ws, cudaStream_t st) {
     cudaError_t e = cudaSuccess;
 #define LG_SF2(C, KT)                                                                                      \
   {                                                                                                          \
-    e = cudaFuncSetAttribute(k_solve_fast<C, KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);  \
+    e = memo_smem_attr((const void*)k_solve_fast<C, KT>, 200 * 1024);                                     \
     if (e != cudaSuccess) return e;                                                                          \
     k_solve_fast<C, KT><<<1, DP_THREADS, fast_smem, st>>>(a.err, a.bits, a.L, a.K, a.default_idx, a.compress, \
                                                           a.D, a.flags, a.choice, a.info, pd, act, wdisc, wadd); \
@@ -1946,7 +2005,7 @@ cudaError_t launch_solve(const SolveArgs& a, void* ws, cudaStream_t st) {
   const size_t row_bytes = sizeof(int64_t) * 2 * (size_t)(a.D + 1);
   const int in_smem = row_bytes <= 200 * 1024;
   const size_t smem = in_smem ? row_bytes : 0;
-  cudaError_t e = cudaFuncSetAttribute(k_solve_generic, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(200 * 1024));
+  cudaError_t e = memo_smem_attr((const void*)k_solve_generic, 200 * 1024);
   if (e != cudaSuccess) return e;
   k_solve_generic<<<1, DP_THREADS, smem, st>>>(a.err, a.bits, a.L, a.K, a.default_idx, a.compress, a.D, a.flags,
                                                a.choice, a.info, pd, act, grows, in_smem);

@@ -22,6 +22,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "memo.h"
 
 namespace lg {
 
@@ -373,15 +374,12 @@ template <int NP, bool TRANS>
 static cudaError_t tc_launch(const PsArgs& a, const PTile* tiles, int ntiles, const float* B, float* out,
                              cudaStream_t st) {
   const int smem = TcSmem<NP, TRANS>::TOTAL;
-  cudaError_t e = cudaFuncSetAttribute(k_ps_tc<NP, TRANS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = memo_smem_attr((const void*)k_ps_tc<NP, TRANS>, smem);
   if (e != cudaSuccess) return e;
-  static int nsm = 0;
-  if (!nsm) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    if (nsm <= 0) nsm = 148;
-  }
+  int nsm = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  if (nsm <= 0) nsm = 148;
   k_ps_tc<NP, TRANS><<<std::min(ntiles, nsm), TC_THREADS, smem, st>>>(a.g, a.e, a.pl, tiles, ntiles, B, out);
   return cudaGetLastError();
 }

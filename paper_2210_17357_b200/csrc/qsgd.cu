@@ -24,6 +24,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "memo.h"
 
 namespace lg {
 
@@ -1298,13 +1299,17 @@ cudaError_t launch_qprofile(const QProfileArgs& a, cudaStream_t st) {
       const int nsm = a.nqwarps / 32;  // nqwarps = SMs x 4 CTAs x 8 warps (an upper bound)
 #define LG_QQ(KT)                                                                                              \
   {                                                                                                            \
-    static int occ = 0;                                                                                        \
-    if (occ == 0) {                                                                                            \
-      cudaError_t e = cudaFuncSetAttribute(k_qprofile_q<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    long long occm = 0;                                                                                        \
+    if (!memo_get((const void*)k_qprofile_q<KT>, (long long)smem, Q1_THREADS, 0, 0, &occm)) {               \
+      cudaError_t e = memo_smem_attr((const void*)k_qprofile_q<KT>, smem);                                     \
       if (e != cudaSuccess) return e;                                                                          \
+      int o = 0;                                                                                               \
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_qprofile_q<KT>, Q1_THREADS, smem) != cudaSuccess || \
+          o < 1) { cudaGetLastError(); o = 1; }                                                                 \
+      occm = o;                                                                                                \
+      memo_put((const void*)k_qprofile_q<KT>, (long long)smem, Q1_THREADS, 0, 0, occm);                        \
     }                                                                                                          \
-    if (occ == 0 && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_qprofile_q<KT>, Q1_THREADS, smem) != \
-                     cudaSuccess || occ < 1)) occ = 1;                                                          \
+    const int occ = (int)occm;                                                                                 \
     const int grid = std::max(1, std::min(a.nqwarps / Q1_WARPS, nsm * occ));                                    \
     const cudaError_t e2 = launch_pdl(k_qprofile_q<KT>, dim3(grid), dim3(Q1_THREADS), smem, st, a.g, a.e,       \
                                       a.qinfo, a.nqchunks, a.ticket, a.cs, a.K, philox_rk(a.k0, a.k1), a.rankfield, \

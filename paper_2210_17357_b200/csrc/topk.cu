@@ -25,6 +25,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "memo.h"
 
 namespace lg {
 
@@ -708,12 +709,8 @@ cudaError_t launch_topk_select(const float* g, const float* e, const TkArgs& a, 
   if (r != cudaSuccess) return r;
   const bool ws = err != nullptr;  // the compress select needs no energy sums
   const size_t sm1 = 2 * 2048 * (ws ? 12 : 4);
-  static bool attr = false;
-  if (!attr) {
-    r = cudaFuncSetAttribute(k_tk_pass1<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * 2048 * 12));
-    if (r != cudaSuccess) return r;
-    attr = true;
-  }
+  r = memo_smem_attr((const void*)k_tk_pass1<true>, 2 * 2048 * 12);
+  if (r != cudaSuccess) return r;
   if (ws) k_tk_pass1<true><<<a.nchunks, TK_THREADS, sm1, st>>>(g, e, a);
   else k_tk_pass1<false><<<a.nchunks, TK_THREADS, sm1, st>>>(g, e, a);
   k_tk_select1<<<a.nC, TK_THREADS, 0, st>>>(a, nq);
