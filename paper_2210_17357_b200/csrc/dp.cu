@@ -762,10 +762,9 @@ __device__ __forceinline__ void cl_st(uint32_t addr, uint64_t v) {
 }
 
 // Cross-cluster handshake of the two layer groups (workspace): group 0's CTAs publish
-// the launch's token after writing their slice of F; ns counts the top group's E2 list.
+// the launch's token after writing their slice of F.
 struct JoinMeta {
   uint64_t tok[16];
-  int ns;
 };
 __device__ __forceinline__ void st_release_gpu(uint64_t* p, uint64_t v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -892,17 +891,27 @@ __device__ __noinline__ void finish_plan(int used_default, const int32_t* bch, i
 #ifdef LG_DP_TIMING
     if (pass == 0) fp2 = clock64();
 #endif
-    if (tid == 0) {
+    if (tid < 32) {
+      // lane 0: the serial fp64 chain in layer order; 16 terms staged in registers ahead
+      // of each run of dependent adds; the int64 bits sum over the warp (order-free)
       int64_t pb = 0;
+      for (int a = tid; a < La; a += 32) pb += sm_cb[a];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) pb += __shfl_xor_sync(LG_FULL, pb, o);
       double pe = 0.0;
-      int a = 0;
-      for (; a + 4 <= La; a += 4) {
-        const double v0 = sm_ce[a], v1 = sm_ce[a + 1], v2 = sm_ce[a + 2], v3 = sm_ce[a + 3];
-        pb += sm_cb[a] + sm_cb[a + 1] + sm_cb[a + 2] + sm_cb[a + 3];
-        pe = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(pe, v0), v1), v2), v3);
+      if (tid == 0) {
+        int a = 0;
+        for (; a + 16 <= La; a += 16) {
+          double v[16];
+#pragma unroll
+          for (int q = 0; q < 16; ++q) v[q] = sm_ce[a + q];
+#pragma unroll
+          for (int q = 0; q < 16; ++q) pe = __dadd_rn(pe, v[q]);
+        }
+        for (; a < La; ++a) pe = __dadd_rn(pe, sm_ce[a]);
       }
-      for (; a < La; ++a) { pb += sm_cb[a]; pe = __dadd_rn(pe, sm_ce[a]); }
-      if (!used_default && (pb > defbits || pe > emax)) {
+      if (tid != 0) {
+      } else if (!used_default && (pb > defbits || pe > emax)) {
         *s_flag = 1;
       } else {
         lgreco_solve_info inf = {};
@@ -1212,6 +1221,7 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
   //     admissible disc from the zero row, saturating at D; a layer with no admissible
   //     candidate empties every later band), the keyed candidate pairs, the rows
   __shared__ int s_a0, s_a1;
+  __shared__ unsigned s_ns;
   if (ngroups > 1) {
     long long tot = 0, wsum = 0;
     for (int t0 = 0; t0 < La; t0 += NT) wsum += (t0 + tid < La) ? 1800 + my_wmaxd[t0 + tid] / 16 : 0;
@@ -1230,7 +1240,7 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
       }
       carry += tt;
     }
-    if (tid == 0 && grp == 1 && rank == 0) jmeta->ns = 0;  // E2 list (ordered by the init cluster barrier)
+    if (tid == 0) s_ns = 0;  // E2 list count (rank 0's is used; ordered by the init cluster barrier)
   } else if (tid == 0) {
     s_a0 = 0;
     s_a1 = La;
@@ -1525,7 +1535,6 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
       return (x >= INF64) ? NONE : (x >> kb);
     };
     uint64_t* F = rowout;                                           // group 0's last row
-    int32_t* gsurv = reinterpret_cast<int32_t*>(rowout + (D + 1));  // the E2 list
     if (grp == 0) {
       for (int el = tid; el < S; el += NT) {
         const int e = cbase + el;
@@ -1608,8 +1617,8 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
     //     it: x = D - e1 runs over this CTA's cells (order-free: a lexicographic minimum)
     uint64_t bv = NONE;
     int be = 0x7fffffff;
+    uint64_t fv[CPT];  // F[D - x] over this CTA's cells (reused by (4) when e* = D)
     {
-      uint64_t fv[CPT];
 #pragma unroll
       for (int j = 0; j < CPT; ++j) {
         const int x = cbase + c0 + j;
@@ -1653,36 +1662,48 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
     for (int r2 = 0; r2 < (int)NC; ++r2)
       if (s_clk[r2] < Cs || (s_clk[r2] == Cs && s_cle[r2] < es)) { Cs = s_clk[r2]; es = s_cle[r2]; }
     const int used_default = (Cs == NONE);
-    // (4) E2 = {e2 <= e* : F[e* - e2] + P[e2] == C*} over this CTA's cells (global list)
+    // (4) E2 = {e2 <= e* : F[e* - e2] + P[e2] == C*} over this CTA's cells, appended to
+    //     rank 0's list over DSMEM (rank 0's row space is dead from here: (3) is done)
+    int2* const sv0 = reinterpret_cast<int2*>(smem_raw + (((size_t)La * 4 + 15) & ~(size_t)15));
     if (!used_default) {
-      uint64_t fv[CPT];
+      if (es != D) {  // (e* = D, the usual case: the F window of (3))
 #pragma unroll
-      for (int j = 0; j < CPT; ++j) {
-        const int x = cbase + c0 + j;
-        fv[j] = (x <= es && pv[j] != NONE) ? __ldcg(F + (es - x)) : NONE;
+        for (int j = 0; j < CPT; ++j) {
+          const int x = cbase + c0 + j;
+          fv[j] = (x <= es && pv[j] != NONE) ? __ldcg(F + (es - x)) : NONE;
+        }
       }
 #pragma unroll
       for (int j = 0; j < CPT; ++j)
-        if (fv[j] != NONE && fv[j] + pv[j] == Cs) gsurv[atomicAdd(&jmeta->ns, 1)] = cbase + c0 + j;
-      __threadfence();
+        if (fv[j] != NONE && pv[j] != NONE && fv[j] + pv[j] == Cs) {
+          uint32_t idx;
+          asm volatile("atom.shared::cluster.add.u32 %0, [%1], 1;" : "=r"(idx) : "r"(cl_map(&s_ns, 0)) : "memory");
+          const int e2 = cbase + c0 + j;
+          asm volatile("st.shared::cluster.v2.s32 [%0], {%1, %2};" ::"r"(cl_map(sv0 + idx, 0)), "r"(e2), "r"(e2)
+                       : "memory");
+        }
     }
     cl_sync();
     LG_T(18);
+#ifdef LG_DP_TIMING
+    if ((rank == NC - 1 || rank == NC / 2) && tid == 0)
+      printf("dp group 1 rank %d per row: compute %lld push %lld syncthreads %lld cluster %lld all-waits %lld\n",
+             (int)rank, t_c / (a1 - a0), (t_p - t_c) / (a1 - a0), t_s / (a1 - a0), t_cl / (a1 - a0),
+             t_push / (a1 - a0));
+#endif
     if (rank != 0) return;
     // (5) rank 0: the lexicographic walk of the top group while several E2 entries
     //     survive, the two backtracks (one warp each), R20 check and summary
     __shared__ int s_cnt[2], s_m;
     int32_t* bch = reinterpret_cast<int32_t*>(smem_raw);  // [La] (the rows are dead)
-    int2* const sv0 = reinterpret_cast<int2*>(smem_raw + (((size_t)La * 4 + 15) & ~(size_t)15));
     int2* const sv1 = sv0 + (D + 1);
     double* sm_ce = reinterpret_cast<double*>(sv0);  // finish_plan's scratch (after the walk)
     const int h = a0;
     if (!used_default) {
-      const int ns0 = __ldcg(&jmeta->ns);
-      for (int i = tid; i < ns0; i += NT) { const int e2 = __ldcg(gsurv + i); sv0[i] = make_int2(e2, e2); }
+      const int ns0 = (int)s_ns;
+      int ns = ns0, cur = 0, a = La - 1;
       if (tid == 0) { s_cnt[0] = ns0; s_m = 0x7fffffff; }
       __syncthreads();
-      int ns = ns0, cur = 0, a = La - 1;
       while (ns > 1 && a >= h) {
         const int2* svc = cur ? sv1 : sv0;
         int2* svn = cur ? sv0 : sv1;
@@ -1720,8 +1741,10 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
              tstamp[8] - tstamp[7], tstamp[15] - tstamp[8], tstamp[16] - tstamp[15], tstamp[17] - tstamp[16],
              tstamp[2] - tstamp[17]);
     if (tid == 0)
-      printf("dp join detail: join %lld walk-setup %lld backtrack %lld\n", tstamp[18] - tstamp[4],
-             tstamp[19] - tstamp[18], tstamp[5] - tstamp[19]);
+      printf("dp join detail: join %lld walk-setup %lld backtrack %lld | per row: compute %lld push %lld "
+             "syncthreads %lld cluster %lld all-waits %lld\n", tstamp[18] - tstamp[4],
+             tstamp[19] - tstamp[18], tstamp[5] - tstamp[19], t_c / (a1 - a0), (t_p - t_c) / (a1 - a0),
+             t_s / (a1 - a0), t_cl / (a1 - a0), t_push / (a1 - a0));
     if (tid == 0)
       printf("dp group 1 (join in-cluster): layers [%d, %d) of %d: prelude %lld init %lld rows %lld (%lld/layer) "
              "P-scan+F-wait %lld join+backtrack %lld summary %lld\n", a0, a1, La, tstamp[1] - tstamp[0],
