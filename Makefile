@@ -13,8 +13,9 @@ SRCS    := $(wildcard $(PKG)/csrc/*.cu)
 HDRS    := $(wildcard $(PKG)/csrc/*.cuh) $(wildcard $(PKG)/csrc/*.h) include/lgreco.h
 LIB     := $(PKG)/liblgreco.so
 ORACLE  := oracle/liblgreco_ref.so
+ORACLE_OMP := oracle/liblgreco_ref_omp.so
 
-all: $(LIB) $(ORACLE)
+all: $(LIB) $(ORACLE) $(ORACLE_OMP)
 
 OBJS    := $(patsubst $(PKG)/csrc/%.cu,build/obj/%.o,$(SRCS))
 
@@ -33,8 +34,12 @@ $(LIB): $(OBJS)
 $(ORACLE): oracle/lgreco_ref.c
 	gcc -O2 -ffp-contract=off -fno-fast-math -fPIC -shared -o $@ $< -lm
 
+# the same oracle with its layer loops on all host cores (bench.py cpu_baseline only)
+$(ORACLE_OMP): oracle/lgreco_ref.c
+	gcc -O2 -ffp-contract=off -fno-fast-math -fPIC -fopenmp -shared -o $@ $< -lm
+
 clean:
-	rm -f $(LIB) $(ORACLE)
+	rm -f $(LIB) $(ORACLE) $(ORACLE_OMP)
 
 .PHONY: all clean timing
 

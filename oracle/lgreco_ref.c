@@ -254,21 +254,37 @@ int ref_qsgd_profile(const ref_layer* layers, int32_t L, const float* g, const f
                      const int32_t* cand_bits, int32_t K, int32_t B, uint64_t seed,
                      uint32_t rank, uint64_t step, double* err, int64_t* bits) {
     if (B <= 0 || B % 128 || B > 8192) return REF_EINVAL;
-    int64_t gb = 0;
+    /* first global bucket of every layer (the Philox counter base) */
+    int64_t* gb0 = (int64_t*)malloc(sizeof(int64_t) * (size_t)(L + 1));
+    if (!gb0) return REF_ENOMEM;
+    gb0[0] = 0;
+    for (int l = 0; l < L; l++) gb0[l + 1] = gb0[l] + nbuckets(layers[l].numel, B);
+    int status = REF_OK;
+    /* layers are independent: with -fopenmp (the oracle's OpenMP build, a timing
+     * baseline only) they run on all host cores; the arithmetic of each is unchanged */
+#pragma omp parallel for schedule(dynamic, 1)
     for (int l = 0; l < L; l++) {
-        int64_t n = layers[l].numel, nb = nbuckets(n, B);
+        int64_t n = layers[l].numel, nb = nbuckets(n, B), gb = gb0[l];
         if (!layers[l].compress) {
             for (int j = 0; j < K; j++) { err[l * K + j] = 0.0; bits[l * K + j] = 32 * n; }
-            gb += nb;
             continue;
         }
         float* xs = (float*)malloc(sizeof(float) * (size_t)n);
         float* dec = (float*)malloc(sizeof(float) * (size_t)n);
-        if (!xs || !dec) { free(xs); free(dec); return REF_ENOMEM; }
+        if (!xs || !dec) {
+            free(xs); free(dec);
+#pragma omp critical
+            status = REF_ENOMEM;
+            continue;
+        }
         for (int64_t i = 0; i < n; i++) xs[i] = canon_x(g[layers[l].offset + i], e ? e + layers[l].offset : NULL, i);
         for (int j = 0; j < K; j++) {
             int st = quantize_layer(xs, n, cand_bits[j], B, gb, seed, rank, step, 0u, NULL, dec);
-            if (st) { free(xs); free(dec); return st; }
+            if (st) {
+#pragma omp critical
+                status = st;
+                break;
+            }
             double sse = 0.0;
             for (int64_t i = 0; i < n; i++) {
                 double d = (double)xs[i] - (double)dec[i];
@@ -278,9 +294,9 @@ int ref_qsgd_profile(const ref_layer* layers, int32_t L, const float* g, const f
             bits[l * K + j] = nb * ((int64_t)B * cand_bits[j] + 64);
         }
         free(xs); free(dec);
-        gb += nb;
     }
-    return REF_OK;
+    free(gb0);
+    return status;
 }
 
 /* Stage-1 compress of one rank (a8): x = g+e; pack with lbits[l] (0 = lossless);
@@ -291,9 +307,12 @@ int ref_qsgd_pack(const ref_layer* layers, int32_t L, const int32_t* lbits, int3
     int64_t* bs = (int64_t*)malloc(sizeof(int64_t) * (L + 1));
     int64_t* bo = (int64_t*)malloc(sizeof(int64_t) * (L + 1));
     ref_layout(layers, L, lbits, B, bs, bo);
-    int st = REF_OK;
-    for (int l = 0; l < L && st == REF_OK; l++) {
+    int status = REF_OK;
+    /* layers are independent (own records, own EF range): OpenMP build only */
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int l = 0; l < L; l++) {
         int64_t n = layers[l].numel, o = layers[l].offset;
+        int st = REF_OK;
         float* xs = (float*)malloc(sizeof(float) * (size_t)n);
         float* dec = (float*)malloc(sizeof(float) * (size_t)n);
         for (int64_t i = 0; i < n; i++) xs[i] = canon_x(g[o + i], e ? e + o : NULL, i);
@@ -308,11 +327,14 @@ int ref_qsgd_pack(const ref_layer* layers, int32_t L, const int32_t* lbits, int3
                 if (e) e[o + i] = xs[i] - dec[i];
                 if (dec_out) dec_out[o + i] = dec[i];
             }
+        } else {
+#pragma omp critical
+            status = st;
         }
         free(xs); free(dec);
     }
     free(bs); free(bo);
-    return st;
+    return status;
 }
 
 /* Decode a full payload (stage 1 or stage 2) into out (a10). */
@@ -321,6 +343,7 @@ int ref_qsgd_unpack(const ref_layer* layers, int32_t L, const int32_t* lbits, in
     int64_t* bs = (int64_t*)malloc(sizeof(int64_t) * (L + 1));
     int64_t* bo = (int64_t*)malloc(sizeof(int64_t) * (L + 1));
     ref_layout(layers, L, lbits, B, bs, bo);
+#pragma omp parallel for schedule(dynamic, 1)
     for (int l = 0; l < L; l++) {
         int64_t n = layers[l].numel, o = layers[l].offset;
         if (lbits[l] > 0) {

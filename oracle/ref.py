@@ -15,16 +15,20 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "lgreco_ref.c")
 _LIB = os.path.join(_HERE, "liblgreco_ref.so")
+# the same source built with -fopenmp: layers of the QSGD profile / pack / unpack on all
+# host cores (a timing baseline for bench.py's cpu_baseline; identical results)
+_LIB_OMP = os.path.join(_HERE, "liblgreco_ref_omp.so")
 
 REF_OK, REF_EINVAL, REF_ENONFINITE, REF_EINFEASIBLE, REF_ENOMEM = 0, -1, -2, -3, -6
 METRIC_SQ, DISC_FLOOR = 1, 2
 
 
-def build(force: bool = False) -> str:
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC",
-                               "-shared", "-o", _LIB, _SRC, "-lm"])
-    return _LIB
+def build(force: bool = False, omp: bool = False) -> str:
+    out = _LIB_OMP if omp else _LIB
+    if force or not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC"] +
+                              (["-fopenmp"] if omp else []) + ["-shared", "-o", out, _SRC, "-lm"])
+    return out
 
 
 class Layer(C.Structure):
@@ -38,12 +42,20 @@ class SolveInfo(C.Structure):
 
 
 _lib = None
+_use_omp = False
+
+
+def use_openmp(on: bool) -> None:
+    """Switch the oracle to its OpenMP build (same source, layers in parallel) or back."""
+    global _lib, _use_omp
+    if on != _use_omp:
+        _use_omp, _lib = on, None
 
 
 def lib():
     global _lib
     if _lib is None:
-        _lib = C.CDLL(build())
+        _lib = C.CDLL(build(omp=_use_omp))
         _lib.ref_uniform.restype = C.c_float
         _lib.ref_layout.restype = C.c_int64
         _lib.ref_topk_k.restype = C.c_int64

@@ -367,3 +367,30 @@ def test_accumulate_exact_sums(ref):
     got = ref.accumulate(a, b)
     assert np.array_equal(got, (a.astype(np.float64) + b.astype(np.float64)).astype(np.float32))
     assert np.array_equal(ref.accumulate(a, np.zeros(n, np.float32)), a)
+
+
+def test_openmp_build_identical(ref):
+    """The oracle's OpenMP build (bench.py cpu_baseline / reference arm: layer loops on
+    all host cores) returns exactly what the single-thread build returns: profile,
+    compress + EF and the W-rank exchange, bit for bit."""
+    layers = _small_layers()
+    rng = np.random.default_rng(5)
+    N = sum(l.numel for l in layers)
+    gs = [rng.standard_normal(N).astype(np.float32) * 1e-2 for _ in range(2)]
+    es = [rng.standard_normal(N).astype(np.float32) * 1e-3 for _ in range(2)]
+    lb = [W.QSGD_BITS[i % 7] if l.compress else 0 for i, l in enumerate(layers)]
+    outs = []
+    for omp in (False, True):
+        ref.use_openmp(omp)
+        try:
+            p = ref.qsgd_profile(layers, gs[0], es[0], W.QSGD_BITS, seed=3, step=1)
+            r = ref.qsgd_allreduce(layers, lb, gs, [e.copy() for e in es], seed=3, step=1)
+        finally:
+            ref.use_openmp(False)
+        outs.append((p, r))
+    (p0, r0), (p1, r1) = outs
+    assert np.array_equal(p0[0], p1[0]) and np.array_equal(p0[1], p1[1])
+    assert np.array_equal(r0[0].view(np.uint32), r1[0].view(np.uint32))
+    for a, b in zip(r0[1], r1[1]):
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    assert np.array_equal(r0[3], r1[3])
