@@ -290,6 +290,40 @@ def run_ours(args):
         ms = float(t[0])
         stage.update(profile=float(t[1]), solve=float(t[2]), compress_allreduce=float(t[3]))
 
+    # ---- W > 1: NVLink bus bytes of the exchange (2 (W-1)/W S_packed per
+    # rank) over the compress + exchange stage, beside the busbw of a plain NCCL
+    # all-gather of the same byte count measured here
+    xch = None
+    if world > 1:
+        ch_list = choice_d.cpu().tolist()
+        S = ctx.payload_bytes(ch_list)
+        bus = 2.0 * (world - 1) / world * S
+        nb = (S + world - 1) // world
+        src_t = torch.empty(nb, dtype=torch.uint8, device=dev)
+        dst_t = torch.empty(nb * world, dtype=torch.uint8, device=dev)
+        ag = None
+        if not one_dev:
+            for _ in range(3):
+                dist.all_gather_into_tensor(dst_t, src_t)
+            torch.cuda.synchronize()
+            a0, a1 = ev(), ev()
+            a0.record(stream)
+            for _ in range(20):
+                dist.all_gather_into_tensor(dst_t, src_t)
+            a1.record(stream)
+            torch.cuda.synchronize()
+            ag = a0.elapsed_time(a1) / 20
+            t = torch.tensor([ag], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ag = float(t[0])
+        xch = {"payload_bytes": S, "bus_bytes_per_rank": bus,
+               "exchange_busbw_gbs": round(bus / (stage["compress_allreduce"] * 1e-3) / 1e9, 1),
+               "busbw_note": "bus bytes / the whole compress + exchange + decode stage (compute included)",
+               "nccl_allgather_busbw_gbs": (round((world - 1) / world * nb * world / (ag * 1e-3) / 1e9, 1)
+                                            if ag else None),
+               "nccl_allgather_ms": round(ag, 4) if ag else None}
+        del src_t, dst_t
+
     # ---- e2e: public API with host buffers.  Every step copies its gradient from pinned
     # host memory (H2D) and reads its mean gradient back (D2H); the copies run on their
     # own streams, double-buffered, so step s+1's H2D and step s-1's D2H overlap step s's
@@ -376,6 +410,7 @@ def run_ours(args):
                     "steps": n_e2e, "overlap": "H2D(s+1) and D2H(s-1) on copy streams beside step s's kernels",
                     "l2": "not flushed: per-step working set 307 MB > 126 MB L2"},
             "gpu_launches": int(launches),
+            "exchange": xch,
             "clocks": clk,
             "wall_s": round(wall, 3),
         }
@@ -393,31 +428,38 @@ def run_ours(args):
 
 
 def run_extras(dev, rank, world, stream, l2_flush, nccl_dist):
-    """Secondary rows measured the same way (device-timed step, L2 flushed), on
-    device-generated seeded inputs (per-layer sigma log-uniform, Gaussian): C2 PowerSGD,
-    C3 TopK, C5 QSGD.  Reported as extras; the headline line is C4."""
+    """Secondary rows measured the same way (device-timed, L2 flushed before every
+    timed step) on the SURVEY.md 8(d) recipes, drawn on the device (same distributions
+    as workloads.py's CPU generators): C2 PowerSGD (low rank + noise), C3 TopK
+    (Student-t, 90%-zero-row embedding), C5 QSGD (Gaussian + outliers), C5 TopK and C5
+    PowerSGD (BASELINE.json configs[4]: the three families with a DP re-solve every
+    step), and C4 with the stage-1 payload packed and decoded at W = 1 (K5-with-pack + K9,
+    the per-rank work of the W > 1 exchange)."""
     import torch
     import torch.distributed as dist
     from paper_2210_17357_b200 import lgreco
-    specs = [("C2", lgreco.POWERSGD, W.PSGD_RANKS_C2, 2, "ResNet-18 CIFAR-10 PowerSGD r{1,2,4,8,16}"),
-             ("C3", lgreco.TOPK, W.TOPK_PPM_C3, 9, "Transformer-XL TopK 0.1%..10%"),
-             ("C5", lgreco.QSGD, W.QSGD_BITS, 2, "GPT-2-medium-like QSGD 2..8 bits")]
-    only = os.environ.get("LG_EXTRAS")  # diagnostics: comma list of config names to run
+    specs = [("C2", "C2", lgreco.POWERSGD, W.PSGD_RANKS_C2, 2, "low_rank", "ResNet-18 CIFAR-10 PowerSGD r{1,2,4,8,16}"),
+             ("C3", "C3", lgreco.TOPK, W.TOPK_PPM_C3, 9, "student_t", "Transformer-XL TopK 0.1%..10%"),
+             ("C5", "C5", lgreco.QSGD, W.QSGD_BITS, 2, "gaussian", "GPT-2-medium-like QSGD 2..8 bits"),
+             ("C5_topk", "C5", lgreco.TOPK, W.TOPK_PPM_C5, 9, "student_t", "GPT-2-medium-like TopK 1%..100% (K=100)"),
+             ("C5_psgd", "C5", lgreco.POWERSGD, W.PSGD_RANKS_C5, 16, "low_rank",
+              "GPT-2-medium-like PowerSGD r16..64 (K=49)")]
+    only = os.environ.get("LG_EXTRAS")  # diagnostics: comma list of row names to run
     if only:
         specs = [sp for sp in specs if sp[0] in only.split(",")]
     res = {}
-    for name, fam, params, dflt_i, desc in specs:
-        layers = W.config_layers(name)
+    cache = {}
+    for name, cfg, fam, params, dflt_i, recipe, desc in specs:
+        layers = W.config_layers(cfg)
         N = W.total_numel(layers)
         L, K = len(layers), len(params)
-        gen = torch.Generator(device=dev)
-        gen.manual_seed(0x5EED + rank)
-        sig = torch.zeros(N, device=dev)
-        for l in layers:
-            sig[l.offset:l.offset + l.numel] = 10.0 ** (-4 + 3 * torch.rand(1, generator=gen, device=dev))
-        g = torch.randn(N, generator=gen, device=dev) * sig
-        ef = torch.randn(N, generator=gen, device=dev) * sig * 0.1
-        del sig
+        key = (cfg, recipe)
+        if key not in cache:
+            cache.clear()
+            torch.cuda.empty_cache()
+            cache[key] = W.recipe_device(layers, recipe, dev, seed=SEED + rank)
+        g, ef0 = cache[key]
+        ef = ef0.clone()
         out = torch.empty_like(g)
         err = torch.empty(L, K, dtype=torch.float64, device=dev)
         bits = torch.empty(L, K, dtype=torch.int64, device=dev)
@@ -455,6 +497,7 @@ def run_extras(dev, rank, world, stream, l2_flush, nccl_dist):
             t["compress_allreduce"].append(m[2].elapsed_time(m[3]))
             t["step"].append(m[0].elapsed_time(m[3]))
         ctx.check()
+        inf = lgreco.read_info(info)
         ctx.close()
         st = {k: sum(v) / len(v) for k, v in t.items()}
         if world > 1:
@@ -462,11 +505,58 @@ def run_extras(dev, rank, world, stream, l2_flush, nccl_dist):
                               dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             st = dict(zip(("step", "profile", "solve", "compress_allreduce"), tt.tolist()))
-        res[name] = {"workload": desc, "n": N, "gbs": round(world * 4.0 * N / (st["step"] * 1e-3) / 1e9, 2),
-                     "stage_ms": {k: round(v, 4) for k, v in st.items()}, "steps": 5}
-        del g, ef, out
-        torch.cuda.empty_cache()
+        res[name] = {"workload": desc, "inputs": recipe, "n": N, "K": K,
+                     "gbs": round(world * 4.0 * N / (st["step"] * 1e-3) / 1e9, 2),
+                     "stage_ms": {k: round(v, 4) for k, v in st.items()}, "steps": 5,
+                     "plan_bits_vs_default": round(inf.total_bits / max(1, inf.default_bits), 4)}
+        del ef, out
+    cache.clear()
+    torch.cuda.empty_cache()
+    if not only or "C4_pack" in only.split(","):
+        res["C4_pack"] = _extra_pack_decode(dev, rank, stream, l2_flush)
     return res
+
+
+def _extra_pack_decode(dev, rank, stream, l2_flush):
+    """C4, plan fixed (the default 4-bit everywhere), W = 1: K5 writing the packed
+    stage-1 payload + EF, then K9 decoding it (what every rank runs around the
+    exchange at W > 1).  Algorithmic bytes per element: K5 12 + (16b+8)/128, K9
+    (16b+8)/128 + 4."""
+    import torch
+    from paper_2210_17357_b200 import lgreco
+    layers = W.config_layers("C4")
+    N = W.total_numel(layers)
+    g, ef = W.recipe_device(layers, "gaussian", dev, seed=SEED + rank)
+    ctx = lgreco.Context(layers, lgreco.QSGD, W.QSGD_BITS, qbucket=128, seed=SEED)
+    choice = [W.QSGD_BITS.index(4) if l.compress else -1 for l in layers]
+    pay = torch.empty(ctx.payload_bytes(choice), dtype=torch.uint8, device=dev)
+    out = torch.empty_like(g)
+    tp, tu = [], []
+    for s in range(7):
+        if s >= 2:
+            l2_flush.zero_()
+        m = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        m[0].record(stream)
+        ctx.qsgd_pack(choice, g, ef, pay, None, 0, s)
+        m[1].record(stream)
+        ctx.qsgd_unpack(choice, pay, out)
+        m[2].record(stream)
+        if s >= 2:
+            tp.append(m)
+    torch.cuda.synchronize()
+    ctx.check()
+    ctx.close()
+    pk = sum(m[0].elapsed_time(m[1]) for m in tp) / len(tp)
+    up = sum(m[1].elapsed_time(m[2]) for m in tp) / len(tp)
+    S = int(pay.numel())
+    peaks, _ = _peaks()
+    bpk = 12.0 * N + S   # read g, e; write e'; write payload (lossless layers as raw records)
+    bup = S + 4.0 * N    # read payload; write out
+    return {"workload": "C4, 4-bit plan fixed, W = 1: pack (K5 with payload) + decode (K9)", "n": N,
+            "payload_bytes": S, "pack_ms": round(pk, 4), "decode_ms": round(up, 4),
+            "pack_hbm_gbs": round(bpk / (pk * 1e-3) / 1e9, 1), "decode_hbm_gbs": round(bup / (up * 1e-3) / 1e9, 1),
+            "pack_hbm_frac": round(bpk / (pk * 1e-3) / 1e9 / peaks["hbm_gbs"], 4),
+            "decode_hbm_frac": round(bup / (up * 1e-3) / 1e9 / peaks["hbm_gbs"], 4), "steps": 5}
 
 
 def _ncu_traffic():
@@ -479,48 +569,70 @@ def _ncu_traffic():
 
 
 # ------------------------------------------------------------------- oracle arm
-def _oracle_step(ref, layers, g, e, step):
+def _oracle_step(ref, layers, g, e, step, times=None):
     K = len(W.QSGD_BITS)
+    t0 = time.perf_counter()
     err, bits = ref.qsgd_profile(layers, g, e, W.QSGD_BITS, seed=SEED, step=step)
+    t1 = time.perf_counter()
     st, choice, info = ref.solve(err, bits, [W.QSGD_BITS.index(4)] * len(layers), [l.compress for l in layers],
                                  D=D_BINS)
+    t2 = time.perf_counter()
     lbits = [W.QSGD_BITS[c] if c >= 0 else 0 for c in choice]
     out, es, _, _ = ref.qsgd_allreduce(layers, lbits, [g], [e], seed=SEED, step=step)
+    t3 = time.perf_counter()
+    if times is not None:
+        times.append((t1 - t0, t2 - t1, t3 - t2))
     return es[0]
 
 
+def _omp_threads():
+    try:
+        return int(os.environ.get("OMP_NUM_THREADS") or len(os.sched_getaffinity(0)))
+    except Exception:
+        return os.cpu_count() or 1
+
+
 def cpu_baseline_full():
-    """The oracle as it stands, one full C4 step (profile + solve + compress, W=1)."""
+    """The oracle as it stands on one full C4 step (profile + solve + compress, W=1):
+    its OpenMP build (layers on all host cores: the reported value) and the
+    single-thread build beside it, each stage timed (the DP is single-threaded in both)."""
     from oracle import ref
     layers = W.config_layers("C4")
     N = W.total_numel(layers)
     g, e = W.gaussian_outliers(layers, seed=SEED)
-    t0 = time.perf_counter()
-    _oracle_step(ref, layers, g, e, 0)
-    dt = time.perf_counter() - t0
+    res = {}
+    for omp in (True, False):
+        ref.use_openmp(omp)
+        tt = []
+        t0 = time.perf_counter()
+        _oracle_step(ref, layers, g, e.copy(), 0, tt)
+        res[omp] = (time.perf_counter() - t0, tt[0])
+    ref.use_openmp(False)
     cores, aff, model = _cpu_info()
-    return {"value": round(4.0 * N / dt / 1e9, 6), "unit": "GB/s", "cores": 1, "kind": "oracle",
-            "sample": f"one full C4 step (N={N}), single thread, {dt:.2f} s; host {model}, {cores} cpus"}
-
-
-def _sample_layers():
-    layers = W.config_layers("C4")
-    out, n = [], 0
-    for l in layers:  # a prefix of ~1/8 of the model: bounded CPU work per step
-        out.append(l)
-        n += l.numel
-        if n >= 3_200_000:
-            break
-    return out
+    dt, (tp, ts, tc) = res[True]
+    dt1, (tp1, ts1, tc1) = res[False]
+    thr = _omp_threads()
+    return {"value": round(4.0 * N / dt / 1e9, 6), "unit": "GB/s", "cores": thr, "kind": "oracle",
+            "sample": f"one full C4 step (N={N}), OpenMP build on {thr} threads, {dt:.2f} s; host {model}, "
+                      f"{cores} cpus ({aff} in affinity)",
+            "stage_s": {"profile": round(tp, 3), "solve": round(ts, 4), "compress": round(tc, 3)},
+            "dp_solve_ms": round(ts * 1e3, 2),
+            "single_thread": {"value": round(4.0 * N / dt1 / 1e9, 6), "unit": "GB/s", "cores": 1,
+                              "seconds": round(dt1, 2),
+                              "stage_s": {"profile": round(tp1, 3), "solve": round(ts1, 4), "compress": round(tc1, 3)}}}
 
 
 def run_reference(args):
+    """--impl reference: the oracle (OpenMP build, all host cores) on the full C4
+    workload, one full step (profile + DP + compress, W = 1) per timed step -- the same
+    config, metric and unit as our arm."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from oracle import ref
-    layers = _sample_layers()
+    ref.use_openmp(True)
+    layers = W.config_layers("C4")
     n = W.total_numel(layers)
     g, e = W.gaussian_outliers(layers, seed=SEED)
     for s in range(args.warmup):
@@ -530,14 +642,15 @@ def run_reference(args):
         e = _oracle_step(ref, layers, g, e, args.warmup + s)
     dt = (time.perf_counter() - t0) / max(1, args.steps)
     cores, aff, model = _cpu_info()
+    thr = _omp_threads()
     v = 4.0 * n / dt / 1e9
-    sample = f"first {len(layers)} C4 layers ({n} fp32) per step, single thread; host {model}"
+    sample = f"full C4 step ({n} fp32) per timed step, oracle OpenMP build on {thr} threads; host {model}"
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": round(v, 6), "unit": "GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "parallelism": "oracle (CPU, 1 thread)"},
-        "cpu_baseline": {"value": round(v, 6), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "config": {"workload": WORKLOAD, "parallelism": f"oracle (CPU, OpenMP {thr} threads)", "same_config": True},
+        "cpu_baseline": {"value": round(v, 6), "unit": "GB/s", "cores": thr, "kind": "oracle", "sample": sample},
         "e2e": {"value": round(v, 6), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 

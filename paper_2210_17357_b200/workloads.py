@@ -251,3 +251,58 @@ def low_rank_plus_noise(layers, seed: int = 0, rank: int = 64, noise: float = 0.
 def rank_seed(base: int, rank: int) -> int:
     """Per-rank seeds: seed = 0x5EED + rank."""
     return base + rank
+
+
+# ----------------------------------------------------------------------------
+# the same recipes drawn on the device (bench.py's large configs: the CPU generators
+# above would take minutes at 192M / 355M elements).  Same distributions, different
+# bytes -- timing inputs only, never compared with the oracle.
+# ----------------------------------------------------------------------------
+
+def recipe_device(layers, recipe: str, dev, seed: int = 0, with_ef: bool = True, sparse_rows_layer: int | None = 0,
+                  zero_row_frac: float = 0.9, rank: int = 64, noise: float = 0.1):
+    """recipe: "gaussian" (C1/C4: N(0, s^2) + 1% outliers x10), "student_t" (C3:
+    Student-t(3) x s, layer `sparse_rows_layer` row-sparse), "low_rank" (C2: rank-64
+    signal with 1/i spectrum + 10% noise; vectors Gaussian).  Per-layer s log-uniform
+    [1e-4, 1e-1]; e ~ N(0, (0.1 s)^2).  Returns (g, e) flat float32 tensors on dev."""
+    n = total_numel(layers)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed((seed * 0x9E3779B1 + 0x5EED) % (2 ** 63))
+    g = torch.zeros(n, dtype=torch.float32, device=dev)
+    e = torch.zeros(n, dtype=torch.float32, device=dev) if with_ef else None
+    for li, L in enumerate(layers):
+        sig = float(10.0 ** (-4.0 + 3.0 * torch.rand(1, generator=gen, device=dev, dtype=torch.float64).item()))
+        view = g[L.offset:L.offset + L.numel]
+        if recipe == "gaussian" or (recipe == "low_rank" and L.rows == 0):
+            torch.randn(L.numel, generator=gen, device=dev, out=view)
+            view.mul_(sig)
+            if recipe == "gaussian" and L.numel >= 100:
+                idx = torch.randint(0, L.numel, (L.numel // 100,), generator=gen, device=dev)
+                view[idx] *= 10.0
+        elif recipe == "student_t":
+            torch.randn(L.numel, generator=gen, device=dev, out=view)
+            chi = torch.zeros(L.numel, device=dev)
+            for _ in range(3):
+                chi.add_(torch.randn(L.numel, generator=gen, device=dev).pow_(2))
+            view.div_(chi.div_(3.0).sqrt_()).mul_(sig)
+            del chi
+            if sparse_rows_layer is not None and li == sparse_rows_layer and L.rows > 0:
+                keep = (torch.rand(L.rows, generator=gen, device=dev) >= zero_row_frac).float()
+                view.view(L.rows, L.cols).mul_(keep[:, None])
+        elif recipe == "low_rank":
+            r = min(rank, L.rows, L.cols)
+            U = torch.randn(L.rows, r, generator=gen, device=dev) / math.sqrt(L.rows)
+            V = torch.randn(L.cols, r, generator=gen, device=dev) / math.sqrt(L.cols)
+            s = sig / torch.arange(1, r + 1, device=dev, dtype=torch.float32)
+            S = (U * s) @ V.T
+            Nz = torch.randn(L.rows, L.cols, generator=gen, device=dev)
+            Nz.mul_(noise * S.norm() / Nz.norm())
+            view.copy_((S + Nz).reshape(-1))
+            del U, V, S, Nz
+        else:
+            raise ValueError(recipe)
+        if with_ef:
+            ev = e[L.offset:L.offset + L.numel]
+            torch.randn(L.numel, generator=gen, device=dev, out=ev)
+            ev.mul_(0.1 * sig)
+    return g, e
