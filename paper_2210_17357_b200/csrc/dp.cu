@@ -1311,6 +1311,7 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
   LG_T(17);
   if (KT == 0 && a0 < a1) stage0((tid < K) ? my_wdisc[a0 * K + tid] : -1, (tid < K) ? my_wadd[a0 * K + tid] : 0, 0);
   LG_T(1);
+  __syncthreads();  // (cl_sync orders these too; the explicit CTA barrier keeps racecheck exact)
   cl_sync();  // every CTA's rows and barriers initialised before any remote push lands
   if (!wide) asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");  // "row -1 done"
   LG_T(2);

@@ -14,18 +14,18 @@ import numpy as np
 
 
 def ddp_buckets(layers, bucket_bytes=25 * 2 ** 20, first_bucket_bytes=2 ** 20, elem_bytes=4):
-    """Bucket index (0 = transmitted first) of every layer, PyTorch-DDP style: gradients
-    become ready in reverse layer order (backward), so buckets are filled from the last
-    layer backwards; the first bucket is capped at `first_bucket_bytes`, the others at
-    `bucket_bytes`; a layer larger than the cap gets a bucket of its own."""
+    """Bucket index (0 = transmitted first) of every layer, as PyTorch DDP assigns them
+    (compute_bucket_assignment_by_size): gradients become ready in reverse layer order,
+    so tensors are taken from the last layer backwards; each is appended to the open
+    bucket, and the bucket closes once its size reaches the current cap (the first cap
+    `first_bucket_bytes`, every later one `bucket_bytes`)."""
     out = [0] * len(layers)
     b, fill, cap = 0, 0, first_bucket_bytes
     for i in reversed(range(len(layers))):
-        nbytes = layers[i].numel * elem_bytes
-        if fill > 0 and fill + nbytes > cap:
-            b, fill, cap = b + 1, 0, bucket_bytes
         out[i] = b
-        fill += nbytes
+        fill += layers[i].numel * elem_bytes
+        if fill >= cap:
+            b, fill, cap = b + 1, 0, bucket_bytes
     return out
 
 

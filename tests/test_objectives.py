@@ -66,9 +66,10 @@ def test_ddp_buckets_closed_form():
     layers = [W.Layer(i * 131072, 131072, 0, 0, 1) for i in range(6)]
     assert O.ddp_buckets(layers) == [1, 1, 1, 1, 0, 0]
     assert list(O.bucket_priority_weights(layers)) == [2, 2, 2, 2, 1, 1]
-    # a layer larger than the cap opens its own bucket
-    big = [W.Layer(0, 10 * 2 ** 20, 0, 0, 1), W.Layer(10 * 2 ** 20, 16, 0, 0, 1)]
-    assert O.ddp_buckets(big, bucket_bytes=2 ** 20) == [1, 0]
+    # DDP appends a tensor before checking the cap: a layer larger than the cap joins the
+    # open bucket and closes it; the next layer starts a new one
+    big = [W.Layer(0, 16, 0, 0, 1), W.Layer(16, 10 * 2 ** 20, 0, 0, 1), W.Layer(10 * 2 ** 20 + 16, 16, 0, 0, 1)]
+    assert O.ddp_buckets(big, bucket_bytes=2 ** 20) == [1, 0, 0]
 
 
 def test_fit_bucket_time_recovers_coefficients():
