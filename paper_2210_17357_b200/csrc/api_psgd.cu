@@ -17,6 +17,9 @@ struct Psgd {
   lg::PTile* d_et_prof = nullptr;
   int n_prof = 0, nrt_prof = 0, nct_prof = 0, rmax_prof = 0, nrt128_prof = 0, nct128_prof = 0, net_prof = 0;
   int32_t* d_et0_prof = nullptr;
+  lg::PTile *d_gcp_prof = nullptr, *d_gcq_prof = nullptr;  // Gram row chunks (P-shaped / Q-shaped)
+  int32_t *d_gcp0_prof = nullptr, *d_gcq0_prof = nullptr;
+  int ngcp_prof = 0, ngcq_prof = 0;
   int32_t* d_ranks = nullptr;
   int32_t* d_ismat = nullptr;
   // compress launch config (per plan)
@@ -26,6 +29,9 @@ struct Psgd {
   lg::PLayer* d_pl_c = nullptr;
   lg::PTile *d_rt_c = nullptr, *d_ct_c = nullptr, *d_rt128_c = nullptr, *d_ct128_c = nullptr, *d_et_c = nullptr;
   int n_c = 0, nrt_c = 0, nct_c = 0, rmax_c = 0, nrt128_c = 0, nct128_c = 0, net_c = 0;
+  lg::PTile* d_gcp_c = nullptr;
+  int32_t* d_gcp0_c = nullptr;
+  int ngcp_c = 0;
   int32_t* d_initflag = nullptr;
   bool need_init = false;
   lg::RawSeg* d_raw = nullptr;
@@ -38,6 +44,8 @@ struct Psgd {
   float *P = nullptr, *Ph = nullptr, *Qprof = nullptr, *Qws = nullptr, *Qn = nullptr, *part = nullptr;
   float* Ppart = nullptr;  // split-K partials of M Q
   double *G = nullptr, *epart = nullptr;
+  double *gpart = nullptr, *GP = nullptr, *GQ = nullptr, *dpart = nullptr;  // Gram partials, profile-error work
+  int32_t* eflag = nullptr;
   int max_split = 1, max_ks = 1;
   int nb_max = 1;  // distinct candidate ranks <= 64 (error boundary slots)
   uint8_t *d_raw_pay = nullptr, *d_raw_gath = nullptr;
@@ -55,11 +63,16 @@ static int64_t ps_net(int64_t m, int64_t k) { return ((m + PE_ROWS - 1) / PE_ROW
 static constexpr int64_t RAW_CHUNK = 16384;
 
 // Build PLayer + tiles for the ranks `r` (per matrix layer; 0 = skip)
+struct GramChunks { std::vector<lg::PTile> p, q; std::vector<int32_t> p0, q0; };
+static constexpr int64_t GC_ROWS = 1024;  // rows per Gram chunk (psgd.cu k_ps_gramc)
+
 static void ps_config(lgreco_ctx* c, const std::vector<int32_t>& r, std::vector<lg::PLayer>& pl,
                       std::vector<lg::PTile>& rt, std::vector<lg::PTile>& ct, std::vector<int32_t>& et0, int& rmax,
-                      std::vector<lg::PTile>& rt128, std::vector<lg::PTile>& ct128, std::vector<lg::PTile>& et) {
+                      std::vector<lg::PTile>& rt128, std::vector<lg::PTile>& ct128, std::vector<lg::PTile>& et,
+                      GramChunks& gc) {
   Psgd* p = c->ps;
   pl.clear(); rt.clear(); ct.clear(); et0.clear(); rt128.clear(); ct128.clear(); et.clear();
+  gc.p.clear(); gc.q.clear(); gc.p0.clear(); gc.q0.clear();
   rmax = 0;
   for (int i = 0; i < p->nM; ++i) {
     if (r[i] <= 0) continue;
@@ -85,7 +98,19 @@ static void ps_config(lgreco_ctx* c, const std::vector<int32_t>& r, std::vector<
     for (int i0 = 0; i0 < ly.rows; i0 += PE_ROWS)
       for (int c0 = 0; c0 < ly.cols; c0 += PE_COLS) et.push_back(lg::PTile{ci, 0, i0, 0, c0, 0});
   }
+  // Gram row chunks: shorter for small ranks (more CTAs; the r^2 partial per chunk stays small)
+  const int64_t gcr = rmax <= 16 ? 128 : rmax <= 32 ? 256 : GC_ROWS;
+  for (int ci = 0; ci < (int)pl.size(); ++ci) {
+    gc.p0.push_back((int32_t)gc.p.size());
+    for (int64_t i0 = 0; i0 < pl[ci].m; i0 += gcr)
+      gc.p.push_back(lg::PTile{ci, 0, (int)i0, (int)std::min<int64_t>(pl[ci].m, i0 + gcr), 0, 0});
+    gc.q0.push_back((int32_t)gc.q.size());
+    for (int64_t i0 = 0; i0 < pl[ci].k; i0 += gcr)
+      gc.q.push_back(lg::PTile{ci, 0, (int)i0, (int)std::min<int64_t>(pl[ci].k, i0 + gcr), 0, 0});
+  }
   et0.push_back((int32_t)et.size());
+  gc.p0.push_back((int32_t)gc.p.size());
+  gc.q0.push_back((int32_t)gc.q.size());
 }
 
 int psgd_init(lgreco_ctx* c, cudaStream_t st) {
@@ -135,7 +160,10 @@ int psgd_init(lgreco_ctx* c, cudaStream_t st) {
   std::vector<lg::PLayer> pl;
   std::vector<lg::PTile> rt, ct, rt128, ct128, et;
   std::vector<int32_t> et0;
-  ps_config(c, p->rprof, pl, rt, ct, et0, p->rmax_prof, rt128, ct128, et);
+  GramChunks gcs;
+  ps_config(c, p->rprof, pl, rt, ct, et0, p->rmax_prof, rt128, ct128, et, gcs);
+  p->ngcp_prof = (int)gcs.p.size();
+  p->ngcq_prof = (int)gcs.q.size();
   p->n_prof = (int)pl.size(); p->nrt_prof = (int)rt.size(); p->nct_prof = (int)ct.size();
   p->nrt128_prof = (int)rt128.size(); p->nct128_prof = (int)ct128.size(); p->net_prof = (int)et.size();
   // compress configs can use at most all matrix layers / tiles of the profile shapes
@@ -148,9 +176,16 @@ int psgd_init(lgreco_ctx* c, cudaStream_t st) {
     max_et += (size_t)ps_net(ly.rows, ly.cols);
   }
   for (int l = 0; l < L; ++l) max_raw += (c->layers[l].numel + RAW_CHUNK - 1) / RAW_CHUNK;
+  // Gram chunks of any config: at most ceil(rows / 128) per factor (the shortest chunks)
+  size_t max_gc = 1, max_gq = 1;
+  for (int i = 0; i < p->nM; ++i) {
+    max_gc += (size_t)((c->layers[p->mlayer[i]].rows + 127) / 128);
+    max_gq += (size_t)((c->layers[p->mlayer[i]].cols + 127) / 128);
+  }
   p->stage_bytes = sizeof(lg::PLayer) * std::max(1, p->nM) +
                    sizeof(lg::PTile) * (max_rt + 2 * max_ct + max_rt128 + max_et + 8) +
-                   sizeof(int32_t) * (2 * (size_t)std::max(1, p->nM) + 2) + sizeof(lg::RawSeg) * (max_raw + 1) + 256;
+                   sizeof(int32_t) * (2 * (size_t)std::max(1, p->nM) + 2) + sizeof(lg::RawSeg) * (max_raw + 1) + 256 +
+                   sizeof(lg::PTile) * (max_gc + 1) + sizeof(int32_t) * (gcs.p0.size() + 1) + 64;
 #define PS_ALLOC(ptr, bytes)                                                                \
   if (cudaMalloc((void**)&(ptr), std::max<size_t>((size_t)(bytes), 16)) != cudaSuccess) {  \
     lg_set_error("cudaMalloc %zu bytes failed (psgd)", (size_t)(bytes));                    \
@@ -182,6 +217,17 @@ int psgd_init(lgreco_ctx* c, cudaStream_t st) {
   PS_ALLOC(p->Ppart, sizeof(float) * p->Psz * p->max_ks);
   PS_ALLOC(p->G, sizeof(double) * p->Gsz);
   PS_ALLOC(p->epart, sizeof(double) * std::max<size_t>(1, et.size()) * PE_SLOTS);
+  PS_ALLOC(p->gpart, sizeof(double) * 64 * 64 * std::max(max_gc, max_gq));
+  PS_ALLOC(p->GP, sizeof(double) * p->Gsz);
+  PS_ALLOC(p->GQ, sizeof(double) * p->Gsz);
+  PS_ALLOC(p->dpart, sizeof(double) * 65 * std::max<size_t>(1, et.size()));
+  PS_ALLOC(p->eflag, sizeof(int32_t) * std::max(1, p->nM));
+  PS_ALLOC(p->d_gcp_prof, sizeof(lg::PTile) * std::max<size_t>(1, gcs.p.size()));
+  PS_ALLOC(p->d_gcq_prof, sizeof(lg::PTile) * std::max<size_t>(1, gcs.q.size()));
+  PS_ALLOC(p->d_gcp0_prof, sizeof(int32_t) * gcs.p0.size());
+  PS_ALLOC(p->d_gcq0_prof, sizeof(int32_t) * gcs.q0.size());
+  PS_ALLOC(p->d_gcp_c, sizeof(lg::PTile) * max_gc);
+  PS_ALLOC(p->d_gcp0_c, sizeof(int32_t) * gcs.p0.size());
   if (K > 128) { lg_set_error("PowerSGD: at most 128 candidate ranks"); return LGRECO_EINVAL; }
   if (c->world > 1) {
     PS_ALLOC(p->d_raw_pay, raw_cap);
@@ -198,6 +244,12 @@ int psgd_init(lgreco_ctx* c, cudaStream_t st) {
   if (!ct128.empty())
     LG_CUDA(cudaMemcpyAsync(p->d_ct128_prof, ct128.data(), sizeof(lg::PTile) * ct128.size(), cudaMemcpyHostToDevice, st));
   if (!et.empty()) LG_CUDA(cudaMemcpyAsync(p->d_et_prof, et.data(), sizeof(lg::PTile) * et.size(), cudaMemcpyHostToDevice, st));
+  if (!gcs.p.empty())
+    LG_CUDA(cudaMemcpyAsync(p->d_gcp_prof, gcs.p.data(), sizeof(lg::PTile) * gcs.p.size(), cudaMemcpyHostToDevice, st));
+  if (!gcs.q.empty())
+    LG_CUDA(cudaMemcpyAsync(p->d_gcq_prof, gcs.q.data(), sizeof(lg::PTile) * gcs.q.size(), cudaMemcpyHostToDevice, st));
+  LG_CUDA(cudaMemcpyAsync(p->d_gcp0_prof, gcs.p0.data(), sizeof(int32_t) * gcs.p0.size(), cudaMemcpyHostToDevice, st));
+  LG_CUDA(cudaMemcpyAsync(p->d_gcq0_prof, gcs.q0.data(), sizeof(int32_t) * gcs.q0.size(), cudaMemcpyHostToDevice, st));
   LG_CUDA(cudaMemcpyAsync(p->d_et0_prof, et0.data(), sizeof(int32_t) * et0.size(), cudaMemcpyHostToDevice, st));
   LG_CUDA(cudaMemcpyAsync(p->d_ranks, c->params.data(), sizeof(int32_t) * K, cudaMemcpyHostToDevice, st));
   LG_CUDA(cudaMemcpyAsync(p->d_ismat, ismat.data(), sizeof(int32_t) * L, cudaMemcpyHostToDevice, st));
@@ -215,6 +267,9 @@ void psgd_destroy(lgreco_ctx* c) {
   cudaFree(p->d_initflag); cudaFree(p->d_raw); cudaFree(p->P); cudaFree(p->Ph); cudaFree(p->Qprof);
   cudaFree(p->Qws); cudaFree(p->Qn); cudaFree(p->part); cudaFree(p->G);
   cudaFree(p->d_raw_pay); cudaFree(p->d_raw_gath);
+  cudaFree(p->gpart); cudaFree(p->GP); cudaFree(p->GQ); cudaFree(p->dpart); cudaFree(p->eflag);
+  cudaFree(p->d_gcp_prof); cudaFree(p->d_gcq_prof); cudaFree(p->d_gcp0_prof); cudaFree(p->d_gcq0_prof);
+  cudaFree(p->d_gcp_c); cudaFree(p->d_gcp0_c);
   if (p->h_stage) cudaFreeHost(p->h_stage);
   if (p->evt) cudaEventDestroy(p->evt);
   delete p;
@@ -223,14 +278,21 @@ void psgd_destroy(lgreco_ctx* c) {
 
 static lg::PsArgs ps_args_prof(lgreco_ctx* c, const float* g, const float* e) {
   Psgd* p = c->ps;
-  return lg::PsArgs{g, e, p->d_pl_prof, p->n_prof, p->d_rt_prof, p->nrt_prof, p->d_ct_prof, p->nct_prof, p->rmax_prof,
-                    p->d_rt128_prof, p->nrt128_prof, p->d_ct128_prof, p->nct128_prof,
-                    p->d_et_prof, p->net_prof, p->d_et0_prof};
+  lg::PsArgs a{g, e, p->d_pl_prof, p->n_prof, p->d_rt_prof, p->nrt_prof, p->d_ct_prof, p->nct_prof, p->rmax_prof,
+               p->d_rt128_prof, p->nrt128_prof, p->d_ct128_prof, p->nct128_prof,
+               p->d_et_prof, p->net_prof, p->d_et0_prof};
+  a.gcp = p->d_gcp_prof; a.n_gcp = p->ngcp_prof; a.gcp0 = p->d_gcp0_prof;
+  a.gcq = p->d_gcq_prof; a.n_gcq = p->ngcq_prof; a.gcq0 = p->d_gcq0_prof;
+  a.gpart = p->gpart;
+  return a;
 }
 static lg::PsArgs ps_args_c(lgreco_ctx* c, const float* g, const float* e) {
   Psgd* p = c->ps;
-  return lg::PsArgs{g, e, p->d_pl_c, p->n_c, p->d_rt_c, p->nrt_c, p->d_ct_c, p->nct_c, p->rmax_c,
-                    p->d_rt128_c, p->nrt128_c, p->d_ct128_c, p->nct128_c, p->d_et_c, p->net_c, nullptr};
+  lg::PsArgs a{g, e, p->d_pl_c, p->n_c, p->d_rt_c, p->nrt_c, p->d_ct_c, p->nct_c, p->rmax_c,
+               p->d_rt128_c, p->nrt128_c, p->d_ct128_c, p->nct128_c, p->d_et_c, p->net_c, nullptr};
+  a.gcp = p->d_gcp_c; a.n_gcp = p->ngcp_c; a.gcp0 = p->d_gcp0_c;
+  a.gpart = p->gpart;
+  return a;
 }
 
 int psgd_profile(lgreco_ctx* c, const float* g, const float* e, uint64_t step, double* err, int64_t* bits,
@@ -247,10 +309,11 @@ int psgd_profile(lgreco_ctx* c, const float* g, const float* e, uint64_t step, d
     LG_LAUNCH(c, lg::launch_ps_mq(a, p->Qprof, p->P, p->Ppart, st));
     LG_LAUNCH(c, lg::launch_ps_orth(a, p->P, 1.0f, p->G, p->Ph, st));
     LG_LAUNCH(c, lg::launch_ps_mtp(a, p->Ph, p->part, p->Qprof, 1.0f, st));
-    c->launches += 10;  // mq 2 + orth 6 + mtp 2
+    c->launches += 12;  // mq 2 + orth 8 (gram 2 x 2) + mtp 2
   }
-  LG_LAUNCH(c, lg::launch_ps_err(a, p->Ph, p->Qprof, p->d_ranks, c->K, p->nb_max, err, bits, p->epart, st));
-  c->launches += 2;
+  const lg::PsErrBufs w{p->dpart, p->GP, p->GQ, p->eflag};
+  LG_LAUNCH(c, lg::launch_ps_err(a, p->Ph, p->Qprof, p->d_ranks, c->K, p->nb_max, err, bits, p->epart, w, st));
+  c->launches += 8;  // gram 2 x 2 + edot + err_exp + (flagged) err_cols + err_final
   return LGRECO_OK;
 }
 
@@ -285,7 +348,8 @@ static int psgd_set_plan(lgreco_ctx* c, const int32_t* choice, cudaStream_t st) 
   std::vector<lg::PTile> rt, ct, rt128, ct128, et;
   std::vector<int32_t> et0;
   int rmax = 0;
-  ps_config(c, r, pl, rt, ct, et0, rmax, rt128, ct128, et);
+  GramChunks gcs;
+  ps_config(c, r, pl, rt, ct, et0, rmax, rt128, ct128, et, gcs);
   // init flags follow the compress config order (layers with r > 0)
   int ci = 0;
   bool any_init = false;
@@ -318,6 +382,11 @@ static int psgd_set_plan(lgreco_ctx* c, const int32_t* choice, cudaStream_t st) 
   const size_t o_et = put(et.data(), sizeof(lg::PTile) * et.size());
   const size_t o_if = put(initf.data(), sizeof(int32_t) * initf.size());
   const size_t o_sg = put(segs.data(), sizeof(lg::RawSeg) * segs.size());
+  const size_t o_gc = put(gcs.p.data(), sizeof(lg::PTile) * gcs.p.size());
+  const size_t o_gc0 = put(gcs.p0.data(), sizeof(int32_t) * gcs.p0.size());
+  if (!gcs.p.empty())
+    LG_CUDA(cudaMemcpyAsync(p->d_gcp_c, h + o_gc, sizeof(lg::PTile) * gcs.p.size(), cudaMemcpyHostToDevice, st));
+  LG_CUDA(cudaMemcpyAsync(p->d_gcp0_c, h + o_gc0, sizeof(int32_t) * gcs.p0.size(), cudaMemcpyHostToDevice, st));
   if (!pl.empty()) LG_CUDA(cudaMemcpyAsync(p->d_pl_c, h + o_pl, sizeof(lg::PLayer) * pl.size(), cudaMemcpyHostToDevice, st));
   if (!rt.empty()) LG_CUDA(cudaMemcpyAsync(p->d_rt_c, h + o_rt, sizeof(lg::PTile) * rt.size(), cudaMemcpyHostToDevice, st));
   if (!ct.empty()) LG_CUDA(cudaMemcpyAsync(p->d_ct_c, h + o_ct, sizeof(lg::PTile) * ct.size(), cudaMemcpyHostToDevice, st));
@@ -331,6 +400,7 @@ static int psgd_set_plan(lgreco_ctx* c, const int32_t* choice, cudaStream_t st) 
   LG_CUDA(cudaEventRecord(p->evt, st));
   p->n_c = (int)pl.size(); p->nrt_c = (int)rt.size(); p->nct_c = (int)ct.size(); p->rmax_c = rmax;
   p->nrt128_c = (int)rt128.size(); p->nct128_c = (int)ct128.size(); p->net_c = (int)et.size();
+  p->ngcp_c = (int)gcs.p.size();
   p->nraw = (int)segs.size();
   p->Sraw = off;
   p->need_init = any_init;

@@ -138,7 +138,16 @@ struct PsArgs {
   const PTile* rtiles; int n_rtiles; const PTile* ctiles; int n_ctiles; int rmax;
   const PTile* rt128; int n_rt128; const PTile* ct128; int n_ct128;  // tensor-core tiles (128 rows / cols)
   const PTile* etiles; int n_etiles; const int32_t* etile0;           // element tiles (64 rows x 256 cols)
+  // Gram row chunks (<= 1024 rows of one layer) of P-shaped / Q-shaped factors, per-layer
+  // chunk ranges, and the RMAX x RMAX partial per chunk
+  const PTile* gcp = nullptr; int n_gcp = 0; const int32_t* gcp0 = nullptr;
+  const PTile* gcq = nullptr; int n_gcq = 0; const int32_t* gcq0 = nullptr;
+  double* gpart = nullptr;
 };
+// profile-error work buffers: d / ||M||^2 partials [etiles][RMAX+1], G_P, G_Q (per layer
+// r x r at goff), the per-layer fallback flag
+struct PsErrBufs { double* dpart; double* GP; double* GQ; int32_t* flag; };
+cudaError_t launch_ps_gram(const PsArgs& a, const float* X, int isq, float scale, double* G, cudaStream_t st);
 cudaError_t launch_ps_initq(const PsArgs& a, float* Q, uint32_t k0, uint32_t k1, uint32_t step, const int32_t* only,
                             cudaStream_t st);
 cudaError_t launch_ps_mq(const PsArgs& a, const float* Q, float* P, float* Ppart, cudaStream_t st);
@@ -151,7 +160,7 @@ cudaError_t launch_ps_mtp_tc(const PsArgs& a, const PTile* ctiles128, int ntiles
                              cudaStream_t st);
 cudaError_t launch_ps_mtp_scale(const PsArgs& a, const float* src, float* dst, float scale, cudaStream_t st);
 cudaError_t launch_ps_err(const PsArgs& a, const float* Ph, const float* Q, const int32_t* ranks, int K, int nbmax,
-                          double* err, int64_t* bits, double* epart, cudaStream_t st);
+                          double* err, int64_t* bits, double* epart, const PsErrBufs& w, cudaStream_t st);
 cudaError_t launch_ps_lossless_rows(const DevLayer* layers, int L, int K, const int32_t* ismat, double* err,
                                     int64_t* bits, cudaStream_t st);
 cudaError_t launch_ps_out(const PsArgs& a, float* ef, float* out, const float* Ph, const float* Q, cudaStream_t st);

@@ -106,37 +106,47 @@ k_ps_gram(const PLayer* __restrict__ pl, const float* __restrict__ P, float scal
 // <= 1e-24 * G[j][j] (or G[j][j] == 0) marks column j as zero, like MGS's zero column.
 // R overwrites G (upper triangle; the diagonal entry of a zero column is 0).
 template <int RMAX>
-__global__ void __launch_bounds__(32)
+__global__ void __launch_bounds__(256)
 k_ps_chol(const PLayer* __restrict__ pl, double* __restrict__ G) {
+  // one CTA per layer: per step j the pivot (thread 0), the row scaling (threads over
+  // columns b > j) and the trailing update (threads over the pairs j < a <= b) -- every
+  // entry sees the same operations in the same order as a sequential right-looking
+  // Cholesky
   __shared__ double Rm[RMAX][RMAX + 1];
   __shared__ double gdiag[RMAX];
+  __shared__ double s_d;
+  __shared__ int s_z;
   const PLayer p = pl[blockIdx.x];
-  const int r = p.r, lane = threadIdx.x;
-  for (int t = lane; t < r * r; t += 32) {
-    const double v = G[p.goff + t];
-    Rm[t / r][t % r] = v;
-    if (t / r == t % r) gdiag[t / r] = v;
+  const int r = p.r, t = threadIdx.x;
+  for (int q = t; q < r * r; q += blockDim.x) {
+    const double v = G[p.goff + q];
+    Rm[q / r][q % r] = v;
+    if (q / r == q % r) gdiag[q / r] = v;
   }
-  __syncwarp();
+  __syncthreads();
   for (int j = 0; j < r; ++j) {
-    double d = Rm[j][j];
-    const bool z = !(d > 1e-24 * gdiag[j]) || gdiag[j] == 0.0;
-    d = z ? 0.0 : sqrt(d);
-    for (int b = j + 1 + lane; b < r; b += 32) Rm[j][b] = z ? 0.0 : Rm[j][b] / d;
-    __syncwarp();
-    if (lane == 0) Rm[j][j] = d;
-    // trailing update over the pairs a <= b of rows/cols j+1 .. r-1: lane owns column b
-    // (RMAX <= 64: at most two columns per lane), rows a ascending -- the same
-    // operation and rounding per entry as the pair loop, without index decoding
-    for (int bb = j + 1 + lane; bb < r; bb += 32) {
-      const double rb = Rm[j][bb];
-      for (int aa = j + 1; aa <= bb; ++aa) Rm[aa][bb] = fma(-Rm[j][aa], rb, Rm[aa][bb]);
+    if (t == 0) {
+      const double d = Rm[j][j];
+      const bool z = !(d > 1e-24 * gdiag[j]) || gdiag[j] == 0.0;
+      s_z = z;
+      s_d = z ? 0.0 : sqrt(d);
+      Rm[j][j] = s_d;
     }
-    __syncwarp();
+    __syncthreads();
+    const bool z = s_z;
+    const double d = s_d;
+    for (int b = j + 1 + t; b < r; b += blockDim.x) Rm[j][b] = z ? 0.0 : Rm[j][b] / d;
+    __syncthreads();
+    const int nn = r - j - 1;
+    for (int q = t; q < nn * nn; q += blockDim.x) {
+      const int aa = j + 1 + q / nn, bb = j + 1 + q % nn;
+      if (aa <= bb) Rm[aa][bb] = fma(-Rm[j][aa], Rm[j][bb], Rm[aa][bb]);
+    }
+    __syncthreads();
   }
-  for (int t = lane; t < r * r; t += 32) {
-    const int a = t / r, b = t % r;
-    G[p.goff + t] = (b >= a) ? Rm[a][b] : 0.0;
+  for (int q = t; q < r * r; q += blockDim.x) {
+    const int aa = q / r, bb = q % r;
+    G[p.goff + q] = (bb >= aa) ? Rm[aa][bb] : 0.0;
   }
 }
 
@@ -147,10 +157,15 @@ __global__ void __launch_bounds__(PS_TM)
 k_ps_cholsolve(const PLayer* __restrict__ pl, const PTile* __restrict__ tiles, const double* __restrict__ R,
                const float* P, float scale, float* Ph) {  // P may alias Ph (row-local)
   __shared__ double Rm[RMAX][RMAX + 1];
+  __shared__ double rinv[RMAX];  // 1 / R[j][j] (0 for a zero column): a multiply per row instead of a division
   const PTile tl = tiles[blockIdx.x];
   const PLayer p = pl[tl.ci];
   const int r = p.r;
   for (int t = threadIdx.x; t < r * r; t += PS_TM) Rm[t / r][t % r] = R[p.goff + t];
+  for (int t = threadIdx.x; t < r; t += PS_TM) {
+    const double d = R[p.goff + t * r + t];
+    rinv[t] = (d == 0.0) ? 0.0 : 1.0 / d;
+  }
   __syncthreads();
   const int i = threadIdx.x;
   if (i >= min(PS_TM, p.m - tl.i0)) return;
@@ -164,7 +179,7 @@ k_ps_cholsolve(const PLayer* __restrict__ pl, const PTile* __restrict__ tiles, c
       double s = (double)__fmul_rn(pin[j], scale);
 #pragma unroll
       for (int t = 0; t < j; ++t) s -= ph[t] * Rm[t][j];
-      ph[j] = (Rm[j][j] == 0.0) ? 0.0 : s / Rm[j][j];
+      ph[j] = s * rinv[j];
     } else {
       ph[j] = 0.0;
     }
@@ -202,7 +217,8 @@ template <int RMAX>
 __global__ void __launch_bounds__(PE_COLS)
 k_ps_err_cols(const float* __restrict__ g, const float* __restrict__ e, const PLayer* __restrict__ pl,
               const PTile* __restrict__ tiles, const float* __restrict__ Ph, const float* __restrict__ Q,
-              const int32_t* __restrict__ ranks, int K, double* __restrict__ part) {
+              const int32_t* __restrict__ ranks, int K, double* __restrict__ part, const int32_t* __restrict__ only) {
+  if (only && !only[tiles[blockIdx.x].ci]) return;  // (fallback pass: flagged layers only)
   extern __shared__ double s_acc[];  // [nb][PE_COLS]
   __shared__ double Ps[PE_ROWS][RMAX];
   __shared__ unsigned long long s_bm;
@@ -253,14 +269,303 @@ k_ps_err_cols(const float* __restrict__ g, const float* __restrict__ e, const PL
   }
 }
 
+// ---------------------------------------------------------------------------
+// Gram in a fixed order over row chunks (fp64): G = Xbar^T Xbar, Xbar = fl(scale X),
+// X column-major (n rows x r columns, X[j n + i]): P (n = m) or Q (n = k).  One CTA per
+// chunk of <= GC_ROWS rows of one layer writes its RMAX x RMAX partial (staged 64 rows
+// at a time in shared memory as fp64); k_ps_gram_red adds a layer's chunks in order.
+// Thread (ta, tb) of a (RMAX/4)^2 grid owns the 4 x 4 block (4ta.., 4tb..) of G.
+// ---------------------------------------------------------------------------
+template <int RMAX>
+__global__ void __launch_bounds__(256)
+k_ps_gramc(const PLayer* __restrict__ pl, const PTile* __restrict__ chunks, const float* __restrict__ X, int isq,
+           float scale, double* __restrict__ gpart) {
+  // 256 threads = G row groups x (RMAX/4)^2; group g takes rows g, g + G, ... of every
+  // staged sub-chunk; the groups' blocks are added in group order at the end
+  constexpr int TG = (RMAX / 4) * (RMAX / 4), G = 256 / TG, SUB = 32, LD = RMAX + 2;
+  __shared__ __align__(16) double xs[SUB * LD];
+  __shared__ __align__(16) double red[G > 1 ? G * RMAX * RMAX : 1];
+  const PTile ch = chunks[blockIdx.x];
+  const PLayer p = pl[ch.ci];
+  const int n = isq ? p.k : p.m;
+  const int64_t off = isq ? p.qoff : p.poff;
+  const int r = p.r, t = threadIdx.x, grp = t / TG, tt = t - grp * TG, ta = tt / (RMAX / 4), tb = tt % (RMAX / 4);
+  double acc[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+  for (int i0 = ch.i0; i0 < ch.i1; i0 += SUB) {
+    const int nr = min(SUB, ch.i1 - i0);
+    __syncthreads();
+    {
+      constexpr int PT = (SUB * RMAX + 255) / 256;  // elements per thread (all loads in flight)
+      float xv[PT];
+#pragma unroll
+      for (int v = 0; v < PT; ++v) {
+        const int q = t + v * 256, j = q / SUB, i = q - j * SUB;  // consecutive threads: consecutive rows
+        xv[v] = (q < SUB * RMAX && i < nr && j < r) ? __ldg(X + off + (int64_t)j * n + i0 + i) : 0.f;
+      }
+#pragma unroll
+      for (int v = 0; v < PT; ++v) {
+        const int q = t + v * 256, j = q / SUB, i = q - j * SUB;
+        if (q < SUB * RMAX) xs[i * LD + j] = (double)__fmul_rn(xv[v], scale);
+      }
+    }
+    __syncthreads();
+    for (int i = grp; i < nr; i += G) {
+      const double2 a01 = *reinterpret_cast<const double2*>(xs + i * LD + 4 * ta);
+      const double2 a23 = *reinterpret_cast<const double2*>(xs + i * LD + 4 * ta + 2);
+      const double2 b01 = *reinterpret_cast<const double2*>(xs + i * LD + 4 * tb);
+      const double2 b23 = *reinterpret_cast<const double2*>(xs + i * LD + 4 * tb + 2);
+      const double av[4] = {a01.x, a01.y, a23.x, a23.y}, bv[4] = {b01.x, b01.y, b23.x, b23.y};
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = fma(av[u], bv[v], acc[u][v]);
+    }
+  }
+  double* out = gpart + (int64_t)blockIdx.x * RMAX * RMAX;
+  if constexpr (G == 1) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) out[(4 * ta + u) * RMAX + 4 * tb + v] = acc[u][v];
+  } else {
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) red[grp * RMAX * RMAX + (4 * ta + u) * RMAX + 4 * tb + v] = acc[u][v];
+    __syncthreads();
+    for (int q = t; q < RMAX * RMAX; q += 256) {
+      double sum = red[q];
+      for (int g2 = 1; g2 < G; ++g2) sum += red[g2 * RMAX * RMAX + q];
+      out[q] = sum;
+    }
+  }
+}
+
+// G[goff + a r + b] = sum over the layer's chunks [c0[ci], c0[ci+1]) in order
+__global__ void k_ps_gram_red(const PLayer* __restrict__ pl, const int32_t* __restrict__ c0, int RMAX,
+                              const double* __restrict__ gpart, double* __restrict__ G) {
+  const PLayer p = pl[blockIdx.x];
+  const int r = p.r;
+  for (int q = blockIdx.y * blockDim.x + threadIdx.x; q < r * r; q += gridDim.y * blockDim.x) {
+    const int a = q / r, b = q - a * r;
+    double s = 0.0;
+    for (int ch = c0[blockIdx.x]; ch < c0[blockIdx.x + 1]; ++ch) s += gpart[(int64_t)ch * RMAX * RMAX + a * RMAX + b];
+    G[p.goff + q] = s;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Profile error by expansion (fp64): for the profile's factors Phat (m x r_max) and Q
+// (k x r_max), with d_j = phat_j^T M q_j, G_P = Phat^T Phat, G_Q = Q^T Q,
+//   err_r^2 = ||M - Phat_r Q_r^T||_F^2 = ||M||^2 - 2 sum_{j<r} d_j + sum_{j,l<r} G_P[j][l] G_Q[j][l]
+// -- the definition (R11) expanded, exact for the given factors; only fp64 rounding
+// separates it from the direct residual, amplified by ||M||^2 / err^2 (a layer where
+// some err_r^2 < 1e-6 ||M||^2 is recomputed directly: k_ps_err_cols, flagged layers).
+// One pass over M: per element tile (64 rows x 256 columns, four 64-column sub-blocks)
+// T = X^T Phat (fp64 SIMT: thread (cg, rg) owns columns 4cg.. x ranks 8rg.., 32 fp64
+// accumulators), then d_j partial = sum_c T[c][j] Q[c][j]; sum x^2 beside it.  Partials
+// [tile][RMAX + 1] are added per layer in tile order (k_ps_err_exp).
+// ---------------------------------------------------------------------------
+template <int RMAX>
+__global__ void __launch_bounds__(128)
+k_ps_edot(const float* __restrict__ g, const float* __restrict__ e, const PLayer* __restrict__ pl,
+          const PTile* __restrict__ tiles, const float* __restrict__ Ph, const float* __restrict__ Q,
+          double* __restrict__ dpart) {
+  // 128 threads = EG row groups x 16 column groups x RMAX/8 rank groups; row group eg
+  // takes rows eg, eg + EG, ... (its own T and d partial, added in group order)
+  constexpr int NT = 128, EG = 128 / (16 * (RMAX / 8)), LX = 64 + 2, LP = RMAX + 2;
+  extern __shared__ __align__(16) double esm[];
+  double* xs = esm;                  // [PE_ROWS][LX]
+  double* ps = esm + PE_ROWS * LX;   // [PE_ROWS][LP]
+  __shared__ double s_red[NT / 32];
+  __shared__ double s_dk[EG][RMAX];
+  const PTile tl = tiles[blockIdx.x];
+  const PLayer p = pl[tl.ci];
+  const int t = threadIdx.x, cg = t & 15, rg = (t >> 4) % (RMAX / 8), eg = t / (16 * (RMAX / 8)), lane = t & 31;
+  const int rows = min(PE_ROWS, p.m - tl.i0);
+  // (staging loops fully unrolled: every global load of a thread in flight at once)
+#pragma unroll
+  for (int u = 0; u < PE_ROWS * RMAX / NT; u += 8) {
+    float pv[8];
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      const int q = t + (u + v) * NT, j = q / PE_ROWS, i = q - j * PE_ROWS;
+      pv[v] = (i < rows && j < p.r) ? __ldg(Ph + p.poff + (int64_t)j * p.m + tl.i0 + i) : 0.f;
+    }
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+      const int q = t + (u + v) * NT, j = q / PE_ROWS, i = q - j * PE_ROWS;
+      ps[i * LP + j] = (double)pv[v];
+    }
+  }
+  double dk[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) dk[k] = 0.0;
+  double x2 = 0.0;
+  for (int sb = 0; sb < PE_COLS / 64; ++sb) {
+    const int cb = tl.c0 + 64 * sb;
+    if (cb >= p.k) break;
+    const int ncol = min(64, p.k - cb);
+    __syncthreads();  // previous sub-block's reads of xs done
+#pragma unroll
+    for (int u = 0; u < PE_ROWS * 64 / NT; u += 16) {
+      float gv[16], ev[16];
+#pragma unroll
+      for (int v = 0; v < 16; ++v) {
+        const int q = t + (u + v) * NT, i = q >> 6, c = q & 63;
+        const bool ok = i < rows && c < ncol;
+        const int64_t idx = p.moff + (int64_t)(tl.i0 + (ok ? i : 0)) * p.k + cb + (ok ? c : 0);
+        gv[v] = ok ? __ldg(g + idx) : 0.f;
+        ev[v] = (ok && e) ? __ldg(e + idx) : 0.f;
+      }
+#pragma unroll
+      for (int v = 0; v < 16; ++v) {
+        const int q = t + (u + v) * NT, i = q >> 6, c = q & 63;
+        const double xd = (double)canon(gv[v], ev[v]);
+        x2 = fma(xd, xd, x2);
+        xs[i * LX + c] = xd;
+      }
+    }
+    __syncthreads();
+    double T[4][8];
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) T[c][k] = 0.0;
+    for (int i = eg; i < rows; i += EG) {
+      const double2 x01 = *reinterpret_cast<const double2*>(xs + i * LX + 4 * cg);
+      const double2 x23 = *reinterpret_cast<const double2*>(xs + i * LX + 4 * cg + 2);
+      const double xa[4] = {x01.x, x01.y, x23.x, x23.y};
+      double pa[8];
+#pragma unroll
+      for (int k = 0; k < 8; k += 2) {
+        const double2 pv = *reinterpret_cast<const double2*>(ps + i * LP + 8 * rg + k);
+        pa[k] = pv.x;
+        pa[k + 1] = pv.y;
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) T[c][k] = fma(xa[c], pa[k], T[c][k]);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int j = 8 * rg + k;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int col = 4 * cg + c;
+        if (j < p.r && col < ncol) dk[k] = fma(T[c][k], (double)Q[p.qoff + (int64_t)j * p.k + cb + col], dk[k]);
+      }
+    }
+  }
+  // sum over the 16 column groups (lanes cg of one rank group: a fixed xor tree)
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+#pragma unroll
+    for (int o = 8; o; o >>= 1) dk[k] += __shfl_xor_sync(LG_FULL, dk[k], o);
+  double* out = dpart + (int64_t)blockIdx.x * (RMAX + 1);
+  if (cg == 0)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s_dk[eg][8 * rg + k] = dk[k];
+  x2 = warp_sum_d(x2);
+  if (lane == 0) s_red[t >> 5] = x2;
+  __syncthreads();
+  if (t == 0) {
+    double s = 0.0;
+    for (int w = 0; w < NT / 32; ++w) s += s_red[w];
+    out[RMAX] = s;
+  }
+  if (t < RMAX) {
+    double s = s_dk[0][t];
+    for (int g2 = 1; g2 < EG; ++g2) s += s_dk[g2][t];
+    out[t] = s;
+  }
+}
+
+// per layer: d_j and ||M||^2 (tiles in order: four interleaved fixed-order sums, then
+// added in order), S_r = sum_{j,l<r} G_P[j][l] G_Q[j][l] by prefix, err_r for every
+// candidate (R11's lossless rule and bits as k_ps_err_final); flag[ci] = 1 when a
+// candidate's err^2 falls below 1e-6 ||M||^2 (the direct fallback recomputes the layer)
+__global__ void __launch_bounds__(256)
+k_ps_err_exp(const PLayer* __restrict__ pl, const int32_t* __restrict__ tile0, const int32_t* __restrict__ ranks,
+             int K, int RMAX, const double* __restrict__ dpart, const double* __restrict__ GP,
+             const double* __restrict__ GQ, double* __restrict__ err, int64_t* __restrict__ bits,
+             int32_t* __restrict__ flag) {
+  __shared__ double s_d[4][65];
+  __shared__ double s_pre[65];  // prefix sums: D_r = sum_{j<r} d_j, S_r
+  __shared__ double s_S[65];
+  __shared__ double s_row[64];
+  __shared__ int s_flag;
+  const PLayer p = pl[blockIdx.x];
+  const int r = p.r, t = threadIdx.x;
+  const int t0 = tile0[blockIdx.x], t1 = tile0[blockIdx.x + 1];
+  if (t == 0) s_flag = 0;
+  {
+    const int col = t & 127, grp = t >> 7;  // columns 0..RMAX (d_j, then ||M||^2), 2 tile groups
+    const int cols = RMAX + 1;
+    for (int cc = col; cc < cols; cc += 128) {
+      double a0 = 0.0, a1 = 0.0;
+      for (int tt = t0 + 2 * grp; tt < t1; tt += 4) {
+        a0 += dpart[(int64_t)tt * (RMAX + 1) + cc];
+        if (tt + 1 < t1) a1 += dpart[(int64_t)(tt + 1) * (RMAX + 1) + cc];
+      }
+      s_d[2 * grp][cc] = a0;
+      s_d[2 * grp + 1][cc] = a1;
+    }
+  }
+  __syncthreads();
+  // H_jl = G_P[j][l] G_Q[j][l]; row prefix of the strict lower part
+  if (t < r) {
+    double rs = 0.0;
+    for (int l = 0; l < t; ++l) rs += GP[p.goff + t * r + l] * GQ[p.goff + t * r + l];
+    s_row[t] = rs;
+  }
+  __syncthreads();
+  if (t == 0) {
+    const double nM2 = ((s_d[0][RMAX] + s_d[1][RMAX]) + s_d[2][RMAX]) + s_d[3][RMAX];
+    double D = 0.0, S = 0.0;
+    s_pre[0] = 0.0;
+    s_S[0] = 0.0;
+    for (int j = 0; j < r; ++j) {
+      const double dj = ((s_d[0][j] + s_d[1][j]) + s_d[2][j]) + s_d[3][j];
+      D += dj;
+      S += 2.0 * s_row[j] + GP[p.goff + j * r + j] * GQ[p.goff + j * r + j];
+      s_pre[j + 1] = D;
+      s_S[j + 1] = S;
+    }
+    s_d[0][RMAX] = nM2;
+  }
+  __syncthreads();
+  const double nM2 = s_d[0][RMAX];
+  for (int c = t; c < K; c += blockDim.x) {
+    const int rr = ranks[c];
+    const int64_t m = p.m, k = p.k;
+    if ((int64_t)rr * (m + k) >= m * k) {  // lossless-equivalent (R11)
+      err[(int64_t)p.layer * K + c] = 0.0;
+      bits[(int64_t)p.layer * K + c] = 32 * m * k;
+      continue;
+    }
+    const double e2 = nM2 - 2.0 * s_pre[rr] + s_S[rr];
+    if (!(e2 >= 1e-6 * nM2)) atomicExch(&s_flag, 1);
+    err[(int64_t)p.layer * K + c] = sqrt(fmax(e2, 0.0));
+    bits[(int64_t)p.layer * K + c] = 32 * (int64_t)rr * (m + k);
+  }
+  __syncthreads();
+  if (t == 0) flag[blockIdx.x] = s_flag;
+}
+
 // per layer: bits / lossless rows of the table, then err_r = sqrt(sum over the layer's
 // element tiles of the boundary slot of r); one warp per candidate, lanes stride the
 // tiles, fixed shuffle tree (deterministic)
 __global__ void k_ps_err_final(const PLayer* __restrict__ pl, int nC, const int32_t* __restrict__ tile0,
                                const int32_t* __restrict__ ranks, int K, const double* __restrict__ part,
-                               double* __restrict__ err, int64_t* __restrict__ bits) {
+                               double* __restrict__ err, int64_t* __restrict__ bits, const int32_t* __restrict__ only) {
   const int ci = blockIdx.x;
-  if (ci >= nC) return;
+  if (ci >= nC || (only && !only[ci])) return;
   const PLayer p = pl[ci];
   const uint64_t bm = ps_boundaries(p, ranks, K);
   const int lane = threadIdx.x & 31;
@@ -304,7 +609,7 @@ __global__ void __launch_bounds__(PE_COLS)
 k_ps_out_cols(const float* __restrict__ g, float* __restrict__ ef, float* __restrict__ out,
               const PLayer* __restrict__ pl, const PTile* __restrict__ tiles, const float* __restrict__ Ph,
               const float* __restrict__ Q) {
-  __shared__ float Ps[PE_ROWS][RMAX];
+  __shared__ __align__(16) float Ps[PE_ROWS][RMAX];
   const PTile tl = tiles[blockIdx.x];
   const PLayer p = pl[tl.ci];
   const int tid = threadIdx.x;
@@ -320,15 +625,32 @@ k_ps_out_cols(const float* __restrict__ g, float* __restrict__ ef, float* __rest
 #pragma unroll
   for (int j = 0; j < RMAX; ++j) qv[j] = (j < p.r) ? Q[p.qoff + (int64_t)j * p.k + c] : 0.f;
   const int64_t base = p.moff + (int64_t)tl.i0 * p.k + c;
-  for (int i = 0; i < rows; ++i) {
-    const int64_t idx = base + (int64_t)i * p.k;
-    float s = 0.f;
+  // four rows per pass: four independent fma chains (the per-element order over j is
+  // unchanged), the P rows read as float4 broadcasts
+  for (int i = 0; i < rows; i += 4) {
+    float s4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-    for (int j = 0; j < RMAX; ++j)
-      if (j < p.r) s = __fmaf_rn(Ps[i][j], qv[j], s);
-    const float x = canon(__ldg(g + idx), ef ? ef[idx] : 0.f);
-    if (out) out[idx] = s;
-    if (ef) ef[idx] = __fsub_rn(x, s);
+    for (int j = 0; j < RMAX; j += 4) {
+      if (j < p.r) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float4 pv = *reinterpret_cast<const float4*>(&Ps[min(i + u, PE_ROWS - 1)][j]);
+          s4[u] = __fmaf_rn(pv.x, qv[j], s4[u]);
+          s4[u] = __fmaf_rn(pv.y, qv[j + 1], s4[u]);
+          s4[u] = __fmaf_rn(pv.z, qv[j + 2], s4[u]);
+          s4[u] = __fmaf_rn(pv.w, qv[j + 3], s4[u]);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (i + u < rows) {
+        const int64_t idx = base + (int64_t)(i + u) * p.k;
+        const float x = canon(__ldg(g + idx), ef ? ef[idx] : 0.f);
+        if (out) out[idx] = s4[u];
+        if (ef) ef[idx] = __fsub_rn(x, s4[u]);
+      }
+    }
   }
 }
 
@@ -397,6 +719,20 @@ cudaError_t launch_ps_mq(const PsArgs& a, const float* Q, float* P, float* Ppart
   return launch_ps_preduce(a, Ppart, P, st);
 }
 
+// G = Xbar^T Xbar per layer (X = P-shaped when isq == 0, Q-shaped otherwise), fixed order
+cudaError_t launch_ps_gram(const PsArgs& a, const float* X, int isq, float scale, double* G, cudaStream_t st) {
+  const PTile* ch = isq ? a.gcq : a.gcp;
+  const int nch = isq ? a.n_gcq : a.n_gcp;
+  const int32_t* c0 = isq ? a.gcq0 : a.gcp0;
+  if (a.nC == 0 || nch == 0) return cudaSuccess;
+  int RM = 64;
+  if (a.rmax <= 16) { RM = 16; k_ps_gramc<16><<<nch, 256, 0, st>>>(a.pl, ch, X, isq, scale, a.gpart); }
+  else if (a.rmax <= 32) { RM = 32; k_ps_gramc<32><<<nch, 256, 0, st>>>(a.pl, ch, X, isq, scale, a.gpart); }
+  else k_ps_gramc<64><<<nch, 256, 0, st>>>(a.pl, ch, X, isq, scale, a.gpart);
+  k_ps_gram_red<<<dim3(a.nC, (RM * RM + 255) / 256), 256, 0, st>>>(a.pl, c0, RM, a.gpart, G);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_ps_orth(const PsArgs& a, const float* P, float scale, double* G, float* Ph, cudaStream_t st) {
   if (a.nC == 0) return cudaSuccess;
   // Cholesky-QR twice (CholQR2): the second pass restores orthogonality to round-off
@@ -404,19 +740,22 @@ cudaError_t launch_ps_orth(const PsArgs& a, const float* P, float scale, double*
   const dim3 gg(a.nC, (a.rmax * (a.rmax + 1) / 2 + PS_THREADS / 32 - 1) / (PS_THREADS / 32));
   auto solve = [&](const float* src, float sc) {
     if (a.rmax <= 16) {
-      k_ps_chol<16><<<a.nC, 32, 0, st>>>(a.pl, G);
+      k_ps_chol<16><<<a.nC, 256, 0, st>>>(a.pl, G);
       k_ps_cholsolve<16><<<a.n_rtiles, PS_TM, 0, st>>>(a.pl, a.rtiles, G, src, sc, Ph);
     } else if (a.rmax <= 32) {
-      k_ps_chol<32><<<a.nC, 32, 0, st>>>(a.pl, G);
+      k_ps_chol<32><<<a.nC, 256, 0, st>>>(a.pl, G);
       k_ps_cholsolve<32><<<a.n_rtiles, PS_TM, 0, st>>>(a.pl, a.rtiles, G, src, sc, Ph);
     } else {
-      k_ps_chol<64><<<a.nC, 32, 0, st>>>(a.pl, G);
+      k_ps_chol<64><<<a.nC, 256, 0, st>>>(a.pl, G);
       k_ps_cholsolve<64><<<a.n_rtiles, PS_TM, 0, st>>>(a.pl, a.rtiles, G, src, sc, Ph);
     }
   };
-  k_ps_gram<<<gg, PS_THREADS, 0, st>>>(a.pl, P, scale, G);
+  (void)gg;
+  cudaError_t e = launch_ps_gram(a, P, 0, scale, G, st);
+  if (e != cudaSuccess) return e;
   solve(P, scale);
-  k_ps_gram<<<gg, PS_THREADS, 0, st>>>(a.pl, Ph, 1.0f, G);
+  e = launch_ps_gram(a, Ph, 0, 1.0f, G, st);
+  if (e != cudaSuccess) return e;
   solve(Ph, 1.0f);
   return cudaGetLastError();
 }
@@ -425,36 +764,55 @@ cudaError_t launch_ps_mtp(const PsArgs& a, const float* Ph, float* part, float* 
   if (a.n_ctiles == 0) return cudaSuccess;
   cudaError_t e = launch_ps_mtp_tc(a, a.ct128, a.n_ct128, Ph, part, st);
   if (e != cudaSuccess) return e;
-  k_ps_reduce<<<dim3(32, a.nC), 256, 0, st>>>(a.pl, a.nC, part, Q, scale);
+  k_ps_reduce<<<dim3(256, a.nC), 256, 0, st>>>(a.pl, a.nC, part, Q, scale);
   return cudaGetLastError();
 }
 
 cudaError_t launch_ps_mtp_scale(const PsArgs& a, const float* src, float* dst, float scale, cudaStream_t st) {
   if (a.nC == 0) return cudaSuccess;
-  k_ps_scale<<<dim3(32, a.nC), 256, 0, st>>>(a.pl, a.nC, src, dst, scale);
+  k_ps_scale<<<dim3(256, a.nC), 256, 0, st>>>(a.pl, a.nC, src, dst, scale);
   return cudaGetLastError();
 }
 
 cudaError_t launch_ps_err(const PsArgs& a, const float* Ph, const float* Q, const int32_t* ranks, int K, int nbmax,
-                          double* err, int64_t* bits, double* epart, cudaStream_t st) {
+                          double* err, int64_t* bits, double* epart, const PsErrBufs& w, cudaStream_t st) {
   if (a.nC == 0) return cudaSuccess;
   if (nbmax < 1 || nbmax > PE_SLOTS) return cudaErrorInvalidValue;
+  // (1) G_P = Phat^T Phat, G_Q = Q^T Q (fp64, fixed order)
+  cudaError_t e = launch_ps_gram(a, Ph, 0, 1.0f, w.GP, st);
+  if (e == cudaSuccess) e = launch_ps_gram(a, Q, 1, 1.0f, w.GQ, st);
+  if (e != cudaSuccess) return e;
+  // (2) d_j and ||M||^2 partials in one pass over M, (3) the expansion per layer
+  int RM = 64;
+  if (a.n_etiles > 0) {
+#define LG_ED(R)                                                                                        \
+  {                                                                                                     \
+    RM = R;                                                                                             \
+    const size_t smem = sizeof(double) * PE_ROWS * ((64 + 2) + (R + 2));                               \
+    e = memo_smem_attr((const void*)k_ps_edot<R>, smem);                                                \
+    if (e != cudaSuccess) return e;                                                                     \
+    k_ps_edot<R><<<a.n_etiles, 128, smem, st>>>(a.g, a.e, a.pl, a.etiles, Ph, Q, w.dpart);                \
+  }
+    if (a.rmax <= 16) LG_ED(16) else if (a.rmax <= 32) LG_ED(32) else LG_ED(64)
+#undef LG_ED
+  }
+  k_ps_err_exp<<<a.nC, 256, 0, st>>>(a.pl, a.etile0, ranks, K, RM, w.dpart, w.GP, w.GQ, err, bits, w.flag);
+  // (4) direct residual for the flagged layers only (near-exact low rank)
   if (a.n_etiles > 0) {
     const size_t smem = sizeof(double) * nbmax * PE_COLS;  // one slot per distinct candidate rank
-    cudaError_t e = cudaSuccess;
     if (a.rmax <= 16) {
-      e = cudaFuncSetAttribute(k_ps_err_cols<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      k_ps_err_cols<16><<<a.n_etiles, PE_COLS, smem, st>>>(a.g, a.e, a.pl, a.etiles, Ph, Q, ranks, K, epart);
+      e = memo_smem_attr((const void*)k_ps_err_cols<16>, smem);
+      k_ps_err_cols<16><<<a.n_etiles, PE_COLS, smem, st>>>(a.g, a.e, a.pl, a.etiles, Ph, Q, ranks, K, epart, w.flag);
     } else if (a.rmax <= 32) {
-      e = cudaFuncSetAttribute(k_ps_err_cols<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      k_ps_err_cols<32><<<a.n_etiles, PE_COLS, smem, st>>>(a.g, a.e, a.pl, a.etiles, Ph, Q, ranks, K, epart);
+      e = memo_smem_attr((const void*)k_ps_err_cols<32>, smem);
+      k_ps_err_cols<32><<<a.n_etiles, PE_COLS, smem, st>>>(a.g, a.e, a.pl, a.etiles, Ph, Q, ranks, K, epart, w.flag);
     } else {
-      e = cudaFuncSetAttribute(k_ps_err_cols<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      k_ps_err_cols<64><<<a.n_etiles, PE_COLS, smem, st>>>(a.g, a.e, a.pl, a.etiles, Ph, Q, ranks, K, epart);
+      e = memo_smem_attr((const void*)k_ps_err_cols<64>, smem);
+      k_ps_err_cols<64><<<a.n_etiles, PE_COLS, smem, st>>>(a.g, a.e, a.pl, a.etiles, Ph, Q, ranks, K, epart, w.flag);
     }
     if (e != cudaSuccess) return e;
   }
-  k_ps_err_final<<<a.nC, 256, 0, st>>>(a.pl, a.nC, a.etile0, ranks, K, epart, err, bits);
+  k_ps_err_final<<<a.nC, 256, 0, st>>>(a.pl, a.nC, a.etile0, ranks, K, epart, err, bits, w.flag);
   return cudaGetLastError();
 }
 
@@ -474,7 +832,7 @@ cudaError_t launch_ps_out(const PsArgs& a, float* ef, float* out, const float* P
 
 cudaError_t launch_ps_preduce(const PsArgs& a, const float* part, float* P, cudaStream_t st) {
   if (a.nC == 0) return cudaSuccess;
-  k_ps_preduce<<<dim3(16, a.nC), 256, 0, st>>>(a.pl, a.nC, part, P);
+  k_ps_preduce<<<dim3(256, a.nC), 256, 0, st>>>(a.pl, a.nC, part, P);
   return cudaGetLastError();
 }
 

@@ -123,7 +123,9 @@ __device__ __forceinline__ void qparams(float mn, float mx, float s, float& inv,
 // for r in (n-1, n], RU(r) stays in (n-1, n] (every integer below 2^24 is a float), so
 // ceil(RU(r)) = ceil(r) = floor(v) + [u < frac(v)] bit for bit (u = frac(v) -> floor(v)).
 // r in (-1, 0] gives q = -0: (uint32_t) and fmaf(q, unit, mn) treat it as +0 (mn != -0,
-// x is canonical).
+// x is canonical).  With inv = RD(s/range) (R5) v <= s always, so the min with s never
+// binds; the pack/decode kernels (HBM-bound) keep R6's literal min, the profile's paired
+// loop (issue-bound) drops it.
 __device__ __forceinline__ float qcode(float t, float inv, float u, float s) {
   return fminf(ceilf(__fmaf_ru(t, inv, -u)), s);
 }
@@ -214,10 +216,10 @@ __device__ __forceinline__ f2_t f2mul(f2_t a, f2_t b) {
 }
 
 // The same loop on element pairs (s = 0,1 and 2,3): per pair and candidate one FFMA2.RP
-// (w), two ceils, two FMNMX (clamp), one FFMA2 for -dec = fma(q, -unit, -mn) (exactly
-// -RN(q unit + mn): RN is symmetric), one FADD2 for d = x + (-dec) (= RN(x - dec)), one
-// FFMA2 for the square: 4 issue slots per element and candidate instead of 6, every
-// result bit-identical to the scalar form.  The SSE is kept as two fp32 partial sums
+// (w), two ceils, no clamp (inv = RD(s/range) keeps v <= s, R5), one FFMA2 for -dec =
+// fma(q, -unit, -mn) (exactly -RN(q unit + mn): RN is symmetric), one FADD2 for d = x +
+// (-dec) (= RN(x - dec)), one FFMA2 for the square: 3 issue slots per element and
+// candidate instead of 6, every result bit-identical to the scalar form.  The SSE is kept as two fp32 partial sums
 // (even / odd elements) per candidate, added at the end.
 template <int KT, bool SCALED>
 __device__ __forceinline__ void prof_cand16x2(const float* x, float mn, uint32_t c0, uint32_t rankfield, uint32_t step,

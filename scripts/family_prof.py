@@ -14,9 +14,9 @@ from paper_2210_17357_b200 import lgreco, workloads as W  # noqa: E402
 
 SPECS = {  # config, family, params, default index, generator
     "C2": ("C2", lgreco.POWERSGD, W.PSGD_RANKS_C2, 2, "low_rank"),
-    "C3": ("C3", lgreco.TOPK, W.TOPK_PPM_C3, 9, "heavy"),
-    "C5q": ("C5", lgreco.QSGD, W.QSGD_BITS, 2, "gauss"),
-    "C5t": ("C5", lgreco.TOPK, W.TOPK_PPM_C5, 9, "heavy"),
+    "C3": ("C3", lgreco.TOPK, W.TOPK_PPM_C3, 9, "student_t"),
+    "C5q": ("C5", lgreco.QSGD, W.QSGD_BITS, 2, "gaussian"),
+    "C5t": ("C5", lgreco.TOPK, W.TOPK_PPM_C5, 9, "student_t"),
     "C5p": ("C5", lgreco.POWERSGD, W.PSGD_RANKS_C5, 16, "low_rank"),
 }
 
@@ -27,16 +27,10 @@ def main():
     cfg, fam, params, di, gen = SPECS[name]
     layers = W.config_layers(cfg)
     t0 = time.time()
-    if gen == "low_rank":
-        g, e = W.low_rank_plus_noise(layers, seed=0x5EED, with_ef=True)
-    elif gen == "heavy":
-        g, e = W.heavy_tailed(layers, seed=0x5EED)
-    else:
-        g, e = W.gaussian_outliers(layers, seed=0x5EED)
-    print(f"# inputs {time.time() - t0:.1f} s", flush=True)
     dev = torch.device("cuda:0")
-    g = torch.from_numpy(g).to(dev)
-    e = torch.from_numpy(e).to(dev)
+    g, e = W.recipe_device(layers, gen, dev, seed=0x5EED)  # the 8(d) recipe, drawn on the device
+    torch.cuda.synchronize()
+    print(f"# inputs {time.time() - t0:.1f} s", flush=True)
     L, K = len(layers), len(params)
     err = torch.empty(L, K, dtype=torch.float64, device=dev)
     bits = torch.empty(L, K, dtype=torch.int64, device=dev)

@@ -18,6 +18,9 @@ METRICS = {
     "warps_active_pct": ("sm__warps_active.avg.pct_of_peak_sustained_active", 1),
     "inst_executed": ("smsp__inst_executed.sum", 1),
     "registers": ("launch__registers_per_thread", 1),
+    "tensor_pct": ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", 1),
+    "fp64_pct": ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", 1),
+    "fma_pct": ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", 1),
     "grid": ("launch__grid_size", 1),
     "block": ("launch__block_size", 1),
 }
@@ -29,6 +32,13 @@ def _to_mb(v, unit):
     v = float(v)
     scale = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}.get(unit, 1.0)
     return v * scale
+
+
+def _f(v):
+    try:
+        return f"{float(v):.1f}"
+    except (TypeError, ValueError):
+        return "-"
 
 
 def main():
@@ -68,11 +78,13 @@ def main():
     json.dump(res, open(out + ".json", "w"), indent=1)
     with open(out + ".md", "w") as f:
         f.write(f"ncu --set full summary of `{rep}`\n\n")
-        f.write("| kernel | us | DRAM R MB | DRAM W MB | DRAM % | issue % | warps % | inst | regs | top stalls |\n")
-        f.write("|---|---|---|---|---|---|---|---|---|---|\n")
+        f.write("| kernel | us | DRAM R MB | DRAM W MB | DRAM % | issue % | warps % | tensor % | fp64 % | inst | regs | "
+                "top stalls |\n")
+        f.write("|---|---|---|---|---|---|---|---|---|---|---|---|\n")
         for d in res:
             f.write(f"| {d['kernel']} | {d.get('time_us')} | {d.get('dram_read_MB')} | {d.get('dram_write_MB')} | "
                     f"{d.get('dram_pct', 0):.1f} | {d.get('issue_active_pct', 0):.1f} | {d.get('warps_active_pct', 0):.1f} | "
+                    f"{_f(d.get('tensor_pct'))} | {_f(d.get('fp64_pct'))} | "
                     f"{int(d.get('inst_executed', 0))} | {int(d.get('registers', 0))} | "
                     f"{', '.join(f'{k} {v}' for k, v in d['top_stalls'].items())} |\n")
     if len(sys.argv) > 3:  # launch list -> per-kernel share of device time
