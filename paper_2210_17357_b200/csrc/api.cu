@@ -418,7 +418,7 @@ int lgreco_profile(lgreco_ctx* c, const float* d_g, const float* d_ef, uint64_t 
     return LGRECO_OK;
   }
   LG_TRY(check_align16("profile", d_g, d_ef));  // (QSGD above handles any 4-byte alignment)
-  if (c->family == LGRECO_TOPK) return topk_profile(c, d_g, d_ef, d_err, d_bits, st);
+  if (c->family == LGRECO_TOPK) return topk_profile(c, d_g, d_ef, step, d_err, d_bits, st);
   if (c->family == LGRECO_POWERSGD) return psgd_profile(c, d_g, d_ef, step, d_err, d_bits, st);
   lg_set_error("profile: family %d unsupported", c->family);
   return LGRECO_EUNSUPPORTED;
@@ -531,7 +531,7 @@ int lgreco_compress_allreduce(lgreco_ctx* c, const int32_t* h_choice, const floa
   if (!c || !h_choice || !d_g || !d_out) { lg_set_error("null argument"); return LGRECO_EINVAL; }
   LG_TRY(check_align16("compress_allreduce", d_g, d_ef, d_out));
   cudaStream_t st = (cudaStream_t)stream;
-  if (c->family == LGRECO_TOPK) return topk_compress_allreduce(c, h_choice, d_g, d_ef, d_out, st);
+  if (c->family == LGRECO_TOPK) return topk_compress_allreduce(c, h_choice, d_g, d_ef, d_out, step, st);
   if (c->family == LGRECO_POWERSGD) return psgd_compress_allreduce(c, h_choice, d_g, d_ef, d_out, step, st);
   if (c->family != LGRECO_QSGD) { lg_set_error("family unsupported"); return LGRECO_EUNSUPPORTED; }
   if (c->world == 1)  // stage 2 skipped (R13): fused pack + EF + decode, nothing leaves the GPU
@@ -683,7 +683,7 @@ int lgreco_compress_allreduce_dev(lgreco_ctx* c, const int32_t* d_choice, const 
   }
   if (c->world == 1 && c->family == LGRECO_TOPK) {
     c->launches += 0;
-    return topk_compress_dev(c, d_choice, d_g, d_ef, d_out, st);
+    return topk_compress_dev(c, d_choice, d_g, d_ef, d_out, step, st);
   }
   if (c->p2p && c->family == LGRECO_QSGD) {
     // W > 1 over peer memory with the plan laid out on the device: no host round trip
@@ -725,7 +725,7 @@ int lgreco_topk_pack(lgreco_ctx* c, const int32_t* h_choice, const float* d_g, f
                      float* d_out, void* stream) {
   if (!c || !h_choice || !d_g) return LGRECO_EINVAL;
   if (c->family != LGRECO_TOPK) return LGRECO_EUNSUPPORTED;
-  return topk_pack(c, h_choice, d_g, d_ef, d_payload, d_out, (cudaStream_t)stream);
+  return topk_pack(c, h_choice, d_g, d_ef, d_payload, d_out, ~0ull, (cudaStream_t)stream);  // (no step: no reuse)
 }
 
 int lgreco_topk_combine(lgreco_ctx* c, const int32_t* h_choice, int32_t W, const uint8_t* d_gathered, float* d_out,

@@ -30,6 +30,14 @@ struct Topk {
   cudaEvent_t evt = nullptr;
   uint8_t *d_pay = nullptr, *d_gath = nullptr;
   int64_t pay_cap = 0;
+  // the preceding profile's per-(layer, density) thresholds, reusable by a compress of
+  // the same x (same g / e pointers and step; the compress rewrites e, so one use)
+  lg::TQ* qc = nullptr;           // compress queries taken from the profile's
+  int32_t* d_choice = nullptr;    // the host plan's choice, uploaded with the plan
+  const void* prof_g = nullptr;
+  const void* prof_e = nullptr;
+  uint64_t prof_step = 0;
+  bool prof_valid = false;
 };
 
 static int64_t topk_k(int64_t n, int32_t ppm) {
@@ -113,12 +121,15 @@ int topk_init(lgreco_ctx* c, cudaStream_t st) {
   TK_ALLOC(t->ckeys, sizeof(uint32_t) * lg::TK_CKCAP * std::max<size_t>(1, ch.size()));
   TK_ALLOC(t->ckn, sizeof(int32_t) * std::max<size_t>(1, ch.size()));
   TK_ALLOC(t->d_tplan, sizeof(lg::TPlan) * L);
+  TK_ALLOC(t->qc, sizeof(lg::TQ) * nC);
+  TK_ALLOC(t->d_choice, sizeof(int32_t) * L);
   if (c->world > 1) {
     TK_ALLOC(t->d_pay, cap);
     TK_ALLOC(t->d_gath, cap * c->world);
   }
 #undef TK_ALLOC
-  if (cudaMallocHost((void**)&t->h_stage, sizeof(lg::TPlan) * L + sizeof(int64_t) * (2 * nC + 1)) != cudaSuccess)
+  if (cudaMallocHost((void**)&t->h_stage, sizeof(lg::TPlan) * L + sizeof(int64_t) * (2 * nC + 1) +
+                                              sizeof(int32_t) * L) != cudaSuccess)
     return LGRECO_ENOMEM;
   LG_CUDA(cudaEventCreateWithFlags(&t->evt, cudaEventDisableTiming));
   LG_CUDA(cudaMemcpyAsync(t->d_clayer, t->clayer.data(), sizeof(int32_t) * t->nC, cudaMemcpyHostToDevice, st));
@@ -139,6 +150,7 @@ void topk_destroy(lgreco_ctx* c) {
   cudaFree(t->cnt3); cudaFree(t->n1); cudaFree(t->n2); cudaFree(t->sl1); cudaFree(t->sl2); cudaFree(t->q);
   cudaFree(t->d_kprof); cudaFree(t->d_kplan); cudaFree(t->d_kpre); cudaFree(t->ccnt); cudaFree(t->coff);
   cudaFree(t->d_tplan); cudaFree(t->d_pay); cudaFree(t->d_gath); cudaFree(t->ckeys); cudaFree(t->ckn);
+  cudaFree(t->qc); cudaFree(t->d_choice);
   if (t->h_stage) cudaFreeHost(t->h_stage);
   if (t->evt) cudaEventDestroy(t->evt);
   delete t;
@@ -194,6 +206,9 @@ static int topk_set_plan(lgreco_ctx* c, const int32_t* choice, cudaStream_t st) 
   memcpy(p + sizeof(lg::TPlan) * c->L, kplan.data(), sizeof(int64_t) * kplan.size());
   memcpy(p + sizeof(lg::TPlan) * c->L + sizeof(int64_t) * kplan.size(), kpre.data(), sizeof(int64_t) * kpre.size());
   LG_CUDA(cudaMemcpyAsync(t->d_tplan, p, sizeof(lg::TPlan) * c->L, cudaMemcpyHostToDevice, st));
+  int32_t* hc = reinterpret_cast<int32_t*>(p + sizeof(lg::TPlan) * c->L + sizeof(int64_t) * (kplan.size() + kpre.size()));
+  memcpy(hc, chv.data(), sizeof(int32_t) * c->L);
+  LG_CUDA(cudaMemcpyAsync(t->d_choice, hc, sizeof(int32_t) * c->L, cudaMemcpyHostToDevice, st));
   if (t->nC) {
     LG_CUDA(cudaMemcpyAsync(t->d_kplan, p + sizeof(lg::TPlan) * c->L, sizeof(int64_t) * t->nC, cudaMemcpyHostToDevice, st));
     LG_CUDA(cudaMemcpyAsync(t->d_kpre, p + sizeof(lg::TPlan) * c->L + sizeof(int64_t) * kplan.size(),
@@ -215,22 +230,48 @@ int64_t topk_payload_bytes(lgreco_ctx* c, const int32_t* choice) {
   return s == LGRECO_OK ? S : s;
 }
 
-int topk_profile(lgreco_ctx* c, const float* g, const float* e, double* err, int64_t* bits, cudaStream_t st) {
+int topk_profile(lgreco_ctx* c, const float* g, const float* e, uint64_t step, double* err, int64_t* bits,
+                 cudaStream_t st) {
   Topk* t = c->tk;
   const lg::TkArgs a = tk_args(c, t->d_kprof);
   LG_LAUNCH(c, lg::launch_topk_lossless_rows(c->d_layers, c->L, c->K, err, bits, st));
   c->launches += 1;
   if (t->nC) LG_LAUNCH(c, lg::launch_topk_select(g, e, a, c->K, err, bits, c->K, st, &c->launches));
+  t->prof_g = g;
+  t->prof_e = e;
+  t->prof_step = step;
+  t->prof_valid = true;
+  return LGRECO_OK;
+}
+
+// The compress's per-layer queries: taken from the preceding profile when it ran on the
+// same x (same g / e pointers and step: the caller contract of the per-step pipeline,
+// as for QSGD's common random numbers), else a fresh one-query select.  d_choice: the
+// plan on the device.
+static int topk_queries(lgreco_ctx* c, const int32_t* d_choice, const float* g, const float* ef, uint64_t step,
+                        lg::TkArgs& a, cudaStream_t st) {
+  Topk* t = c->tk;
+  const bool reuse = t->prof_valid && t->prof_g == g && t->prof_e == ef && t->prof_step == step &&
+                     step != ~0ull && !getenv("LGRECO_TOPK_NO_REUSE");
+  t->prof_valid = false;  // this compress rewrites e
+  if (reuse) {
+    LG_LAUNCH(c, lg::launch_topk_reuse(d_choice, c->K, t->d_clayer, t->nC, t->q, t->qc, c->d_flag, st));
+    a.q = t->qc;
+    c->launches += 1;
+  } else {
+    LG_LAUNCH(c, lg::launch_topk_select(g, ef, a, 1, nullptr, nullptr, 1, st, &c->launches));
+  }
   return LGRECO_OK;
 }
 
 int topk_pack(lgreco_ctx* c, const int32_t* choice, const float* g, float* ef, uint8_t* payload, float* out,
-              cudaStream_t st) {
+              uint64_t step, cudaStream_t st) {
   Topk* t = c->tk;
   LG_TRY(topk_set_plan(c, choice, st));
-  const lg::TkArgs a = tk_args(c, t->d_kplan);
+  lg::TkArgs a = tk_args(c, t->d_kplan);
+  a.need_off = payload != nullptr;
   if (t->nC) {
-    LG_LAUNCH(c, lg::launch_topk_select(g, ef, a, 1, nullptr, nullptr, 1, st, &c->launches));
+    LG_TRY(topk_queries(c, t->d_choice, g, ef, step, a, st));
     LG_LAUNCH(c, lg::launch_topk_compact(g, ef, payload, out, a, st));
     c->launches += 3;
   }
@@ -251,24 +292,26 @@ int topk_combine(lgreco_ctx* c, const int32_t* choice, int W, const uint8_t* gat
 }
 
 int topk_compress_allreduce(lgreco_ctx* c, const int32_t* choice, const float* g, float* ef, float* out,
-                            cudaStream_t st) {
+                            uint64_t step, cudaStream_t st) {
   Topk* t = c->tk;
-  if (c->world == 1) return topk_pack(c, choice, g, ef, nullptr, out, st);  // W = 1: fused decode
-  LG_TRY(topk_pack(c, choice, g, ef, t->d_pay, nullptr, st));
+  if (c->world == 1) return topk_pack(c, choice, g, ef, nullptr, out, step, st);  // W = 1: fused decode
+  LG_TRY(topk_pack(c, choice, g, ef, t->d_pay, nullptr, step, st));
   LG_NCCL(ncclAllGather(t->d_pay, t->d_gath, (size_t)t->S, ncclUint8, c->comm, st));
   return topk_combine(c, choice, c->world, t->d_gath, out, st);
 }
 
 // W == 1 fused TopK compress with the plan read on the device (no host round trip).
-int topk_compress_dev(lgreco_ctx* c, const int32_t* d_choice, const float* g, float* ef, float* out, cudaStream_t st) {
+int topk_compress_dev(lgreco_ctx* c, const int32_t* d_choice, const float* g, float* ef, float* out, uint64_t step,
+                      cudaStream_t st) {
   Topk* t = c->tk;
   LG_LAUNCH(c, lg::launch_plan_topk_dev(d_choice, c->d_params, c->K, c->d_layers, t->d_clayer, t->nC, t->d_kplan,
                                         c->d_flag, st));
   t->plan_valid = false;  // d_kplan now holds a device-chosen plan
-  const lg::TkArgs a = tk_args(c, t->d_kplan);
+  lg::TkArgs a = tk_args(c, t->d_kplan);
+  a.need_off = 0;  // no payload at W = 1
   c->launches += 1;
   if (t->nC) {
-    LG_LAUNCH(c, lg::launch_topk_select(g, ef, a, 1, nullptr, nullptr, 1, st, &c->launches));
+    LG_TRY(topk_queries(c, d_choice, g, ef, step, a, st));
     LG_LAUNCH(c, lg::launch_topk_compact(g, ef, nullptr, out, a, st));
     c->launches += 3;
   }

@@ -101,14 +101,16 @@ struct lgreco_ctx {
 // family-specific parts (api_topk.cu, api_psgd.cu)
 int topk_init(lgreco_ctx* c, cudaStream_t st);
 void topk_destroy(lgreco_ctx* c);
-int topk_profile(lgreco_ctx* c, const float* g, const float* e, double* err, int64_t* bits, cudaStream_t st);
-int topk_pack(lgreco_ctx* c, const int32_t* choice, const float* g, float* ef, uint8_t* payload, float* out,
+int topk_profile(lgreco_ctx* c, const float* g, const float* e, uint64_t step, double* err, int64_t* bits,
+                 cudaStream_t st);
+int topk_pack(lgreco_ctx* c, const int32_t* choice, const float* g, float* ef, uint8_t* payload, float* out, uint64_t step,
               cudaStream_t st);
 int topk_combine(lgreco_ctx* c, const int32_t* choice, int W, const uint8_t* gathered, float* out, cudaStream_t st);
 int topk_compress_allreduce(lgreco_ctx* c, const int32_t* choice, const float* g, float* ef, float* out,
-                            cudaStream_t st);
+                            uint64_t step, cudaStream_t st);
 int64_t topk_payload_bytes(lgreco_ctx* c, const int32_t* choice);
-int topk_compress_dev(lgreco_ctx* c, const int32_t* d_choice, const float* g, float* ef, float* out, cudaStream_t st);
+int topk_compress_dev(lgreco_ctx* c, const int32_t* d_choice, const float* g, float* ef, float* out, uint64_t step,
+                      cudaStream_t st);
 int psgd_init(lgreco_ctx* c, cudaStream_t st);
 void psgd_destroy(lgreco_ctx* c);
 int psgd_profile(lgreco_ctx* c, const float* g, const float* e, uint64_t step, double* err, int64_t* bits,

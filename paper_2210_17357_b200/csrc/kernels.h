@@ -92,6 +92,7 @@ struct TQ {  // one radix-select query (layer, density)
   int32_t b1, s1, c2, s2; // level-1 bin / slot, level-2 sub-bin / slot
   uint32_t T; int32_t bad;  // threshold key; non-finite input seen
   double below, sse;     // sum x^2 strictly below the current bin; final dropped energy
+  int64_t ties;          // keys equal to T in the layer (after S3)
 };
 struct TPlan { int64_t pay_off; int64_t k; };
 struct TkArgs {
@@ -101,7 +102,10 @@ struct TkArgs {
   int32_t* n1; int32_t* n2; int32_t* sl1; uint32_t* sl2;
   TQ* q; const int64_t* kq; uint2* ccnt; ulonglong2* coff; const TPlan* tplan; unsigned* flag;
   uint32_t* ckeys; int32_t* ckn;  // per chunk: keys of its boundary level-1 bins (pass2 -> pass3), count
+  int need_off = 1;  // 0: no payload (W = 1 fused): chunks of layers keeping all or none of T's ties skip the count
 };
+cudaError_t launch_topk_reuse(const int32_t* choice, int K, const int32_t* clayer, int nC, const TQ* qprof, TQ* qc,
+                              unsigned* flag, cudaStream_t st);
 constexpr int TK_CKCAP = 2048;  // compacted boundary keys kept per 16384-element chunk
 cudaError_t launch_topk_select(const float* g, const float* e, const TkArgs& a, int nq, double* err, int64_t* bits,
                                int K, cudaStream_t st, int64_t* launches);

@@ -306,8 +306,9 @@ __device__ __forceinline__ void warp_find_from_top(const uint32_t* __restrict__ 
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(TK_THREADS)
 k_tk_select2(TkArgs a, int nq) {
+  // one warp per query (grid y: groups of TK_WARPS queries of layer blockIdx.x)
   const int c = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int q = warp; q < nq; q += TK_WARPS) {
+  for (int q = blockIdx.y * TK_WARPS + warp; q < nq; q += gridDim.y * TK_WARPS) {
     TQ& t = a.q[(int64_t)c * nq + q];
     const uint32_t* h = a.cnt2 + (int64_t)t.s1 * 1024;
     const unsigned long long* hs = a.sum2 + (int64_t)t.s1 * 1024;
@@ -323,7 +324,12 @@ k_tk_select2(TkArgs a, int nq) {
     v = warp_sum_d(v) * fx_scale(t.b1);
     if (lane == 0) { t.c2 = c2; t.r = r2; t.below += v; }
   }
-  __syncthreads();
+}
+
+// per layer: distinct (b1, c2) prefixes -> ranks (the level-3 histogram slots)
+__global__ void __launch_bounds__(TK_THREADS)
+k_tk_select2b(TkArgs a, int nq) {
+  const int c = blockIdx.x;
   // distinct (b1, c2) prefixes -> ranks: bitonic sort of <= 256 prefixes in smem
   __shared__ uint32_t sp[256];
   __shared__ uint32_t sfirst[256];
@@ -367,9 +373,6 @@ k_tk_select2(TkArgs a, int nq) {
     }
     t.s2 = c * nq + (int)sfirst[lo];
   }
-  __syncthreads();
-  const int n2 = a.n2[c];
-  for (int64_t i = threadIdx.x; i < (int64_t)n2 * 1024; i += TK_THREADS) a.cnt3[(int64_t)c * nq * 1024 + i] = 0;
 }
 
 // ---------------------------------------------------------------------------
@@ -420,7 +423,7 @@ __global__ void __launch_bounds__(TK_THREADS)
 k_tk_select3(TkArgs a, int nq, double* __restrict__ err, int64_t* __restrict__ bits, int K) {
   const int c = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int l = a.clayer[c];
-  for (int q = warp; q < nq; q += TK_WARPS) {
+  for (int q = blockIdx.y * TK_WARPS + warp; q < nq; q += gridDim.y * TK_WARPS) {
     TQ& t = a.q[(int64_t)c * nq + q];
     const uint32_t* h = a.cnt3 + (int64_t)t.s2 * 1024;
     const uint32_t p = ((uint32_t)t.b1 << 10) | (uint32_t)t.c2;
@@ -438,6 +441,7 @@ k_tk_select3(TkArgs a, int nq, double* __restrict__ err, int64_t* __restrict__ b
       const double sse = t.below + v + (double)((int64_t)h[t3] - r3) * key_sq(T);
       t.T = T;
       t.r = r3;
+      t.ties = h[t3];
       t.sse = t.bad ? __longlong_as_double(0x7ff8000000000000ll) : sse;
       if (err) {
         err[(int64_t)l * K + q] = sqrt(t.sse);
@@ -464,7 +468,12 @@ k_tk_count(const float* __restrict__ g, const float* __restrict__ e, TkArgs a) {
   __shared__ uint32_t sg[TK_WARPS], se[TK_WARPS];
   const TChunk ch = a.chunks[blockIdx.x];
   const DevLayer ly = a.layers[a.clayer[ch.cidx]];
-  const uint32_t T = a.q[ch.cidx].T;
+  const TQ qq = a.q[ch.cidx];
+  const uint32_t T = qq.T;
+  if (!a.need_off && (qq.r == 0 || qq.r == qq.ties)) {  // every tie kept or none: no prefix needed
+    if (threadIdx.x == 0) a.ccnt[blockIdx.x] = make_uint2(0u, 0u);
+    return;
+  }
   uint32_t gt = 0, eq = 0;
   for_chunk(g, e, ly, ch, [&](int64_t, float x) {
     const uint32_t key = tkey(x);
@@ -716,15 +725,37 @@ cudaError_t launch_topk_select(const float* g, const float* e, const TkArgs& a, 
   k_tk_select1<<<a.nC, TK_THREADS, 0, st>>>(a, nq);
   if (ws) k_tk_pass2<true><<<a.nchunks, TK_THREADS, 0, st>>>(g, e, a, nq);
   else k_tk_pass2<false><<<a.nchunks, TK_THREADS, 0, st>>>(g, e, a, nq);
-  k_tk_select2<<<a.nC, TK_THREADS, 0, st>>>(a, nq);
+  const dim3 gq(a.nC, (nq + TK_WARPS - 1) / TK_WARPS);  // a warp per query
+  k_tk_select2<<<gq, TK_THREADS, 0, st>>>(a, nq);
+  k_tk_select2b<<<a.nC, TK_THREADS, 0, st>>>(a, nq);
+  // level-3 histograms (every slot a layer may use: nC x nq x 1024) zeroed at full width
+  r = cudaMemsetAsync(a.cnt3, 0, sizeof(uint32_t) * 1024 * (size_t)a.nC * nq, st);
+  if (r != cudaSuccess) return r;
   k_tk_pass3<<<a.nchunks, TK_THREADS, 0, st>>>(g, e, a, nq);
-  k_tk_select3<<<a.nC, TK_THREADS, 0, st>>>(a, nq, err, bits, K);
-  *launches += 6;
+  k_tk_select3<<<gq, TK_THREADS, 0, st>>>(a, nq, err, bits, K);
+  *launches += 7;
   return cudaGetLastError();
 }
 
 cudaError_t launch_topk_lossless_rows(const DevLayer* layers, int L, int K, double* err, int64_t* bits, cudaStream_t st) {
   k_tk_lossless_rows<<<64, 256, 0, st>>>(layers, L, K, err, bits);
+  return cudaGetLastError();
+}
+
+// compress queries from the preceding profile's (same x): qc[c] = qprof[c K + choice[layer]]
+__global__ void k_tk_reuse(const int32_t* __restrict__ choice, int K, const int32_t* __restrict__ clayer, int nC,
+                           const TQ* __restrict__ qprof, TQ* __restrict__ qc, unsigned* __restrict__ flag) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < nC; c += gridDim.x * blockDim.x) {
+    int j = choice[clayer[c]];
+    if (j < 0 || j >= K) { atomicOr(flag, 2u); j = 0; }
+    qc[c] = qprof[(int64_t)c * K + j];
+  }
+}
+
+cudaError_t launch_topk_reuse(const int32_t* choice, int K, const int32_t* clayer, int nC, const TQ* qprof, TQ* qc,
+                              unsigned* flag, cudaStream_t st) {
+  if (nC == 0) return cudaSuccess;
+  k_tk_reuse<<<(nC + 255) / 256, 256, 0, st>>>(choice, K, clayer, nC, qprof, qc, flag);
   return cudaGetLastError();
 }
 

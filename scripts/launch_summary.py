@@ -12,7 +12,9 @@ for r in csv.reader(open(path)):
         h = r
         continue
     if h and len(r) == len(h):
-        data.append(dict(zip(h, r)))
+        d = dict(zip(h, r))
+        if d.get("Metric Name", "gpu__time_duration.sum") == "gpu__time_duration.sum":
+            data.append(d)
 n = len(data)
 agg = collections.defaultdict(lambda: [0, 0.0])
 for d in data[int(n * (1 - frac)):]:

@@ -189,3 +189,34 @@ def test_compress_allreduce_dev_matches_host_path(lg):
     ctx.compress_allreduce(choice, gd, e1, o1, 0)
     ctx.compress_allreduce_dev(torch.tensor(choice, dtype=torch.int32, device="cuda"), gd, e2, o2, 0)
     assert torch.equal(o1.view(torch.int32), o2.view(torch.int32)) and torch.equal(e1.view(torch.int32), e2.view(torch.int32))
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_compress_reuses_profile_thresholds(lg, ref, seed):
+    """A compress of the same x right after the profile (same g / e pointers and step)
+    takes the profile's per-layer thresholds instead of selecting again: outputs and EF
+    bit-identical to a compress without a preceding profile and to the oracle, with the
+    tie-heavy layers (600 equal magnitudes, 15000 zeros) where only some ties are kept."""
+    layers = _layers()
+    g, e = _data(layers, seed)
+    L, K = len(layers), len(PPM)
+    rng = np.random.default_rng(40 + seed)
+    choice = [int(rng.integers(0, K)) if l.compress else -1 for l in layers]
+    lppm = [PPM[c] if l.compress else 0 for c, l in zip(choice, layers)]
+    out_ref, es_ref, _ = ref.topk_allreduce(layers, lppm, [g], [e])
+    res = []
+    for with_profile in (True, False):
+        ctx = lg.Context(layers, lg.TOPK, PPM)
+        gd, ed = _dev(g), _dev(e)
+        if with_profile:
+            err = torch.empty(L, K, dtype=torch.float64, device="cuda")
+            bits = torch.empty(L, K, dtype=torch.int64, device="cuda")
+            ctx.profile(gd, ed, 5, err, bits)
+        out = torch.empty_like(gd)
+        ctx.compress_allreduce_dev(torch.tensor(choice, dtype=torch.int32, device="cuda"), gd, ed, out, 5)
+        ctx.check()
+        res.append((out.cpu().numpy(), ed.cpu().numpy()))
+        ctx.close()
+    for out, ef in res:
+        assert np.array_equal(out.view(np.uint32), out_ref.view(np.uint32))
+        assert np.array_equal(ef.view(np.uint32), es_ref[0].view(np.uint32))
