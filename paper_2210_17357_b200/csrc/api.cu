@@ -419,7 +419,10 @@ int lgreco_profile(lgreco_ctx* c, const float* d_g, const float* d_ef, uint64_t 
   }
   LG_TRY(check_align16("profile", d_g, d_ef));  // (QSGD above handles any 4-byte alignment)
   if (c->family == LGRECO_TOPK) return topk_profile(c, d_g, d_ef, step, d_err, d_bits, st);
-  if (c->family == LGRECO_POWERSGD) return psgd_profile(c, d_g, d_ef, step, d_err, d_bits, st);
+  if (c->family == LGRECO_POWERSGD) {
+    if (c->psgd_method == LGRECO_PSGD_SVD) return lgreco_psgd_profile_svd(c, d_g, d_ef, d_err, d_bits, stream);
+    return psgd_profile(c, d_g, d_ef, step, d_err, d_bits, st);
+  }
   lg_set_error("profile: family %d unsupported", c->family);
   return LGRECO_EUNSUPPORTED;
 }

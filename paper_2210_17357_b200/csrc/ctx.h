@@ -67,6 +67,7 @@ struct lgreco_ctx {
   int32_t* d_lqseg0 = nullptr;   // per-layer first segment [L+1]
   double* d_segsum = nullptr;    // [nqseg][K]
   unsigned* d_ldone = nullptr;   // per-layer finished-segment counters [L]
+  int psgd_method = 0;           // resolved PowerSGD profile method (LGRECO_PSGD_POWER / _SVD)
   unsigned* d_flag = nullptr;
   // plan
   std::vector<int32_t> plan_choice;

@@ -237,3 +237,29 @@ extern "C" int lgreco_psgd_profile_svd(lgreco_ctx* c, const float* d_g, const fl
   }
   return LGRECO_OK;
 }
+
+// NEXT-2 selector: resolved once per ctx from the layer shapes
+extern "C" int lgreco_psgd_set_method(lgreco_ctx* c, int32_t method) {
+  if (!c || c->family != LGRECO_POWERSGD) { lg_set_error("psgd_set_method: PowerSGD ctx only"); return LGRECO_EINVAL; }
+  if (method == LGRECO_PSGD_POWER || method == LGRECO_PSGD_SVD) { c->psgd_method = method; return LGRECO_OK; }
+  if (method != LGRECO_PSGD_AUTO) { lg_set_error("psgd_set_method: bad method %d", method); return LGRECO_EINVAL; }
+  double t_pow = 0.0, t_svd = 0.0;
+  for (int l = 0; l < c->L; ++l) {
+    const lgreco_layer& ly = c->layers[l];
+    if (!ly.compress || ly.rows <= 0 || ly.cols <= 0) continue;
+    const double m = ly.rows, k = ly.cols, n = std::min(m, k);
+    int rmax = 0;
+    for (int j = 0; j < c->K; ++j)
+      if ((double)c->params[j] * (m + k) < m * k) rmax = std::max(rmax, c->params[j]);
+    if (rmax == 0) continue;
+    t_pow += (double)c->power_steps * m * k * rmax * 1.9e-13;
+    t_svd += m * k * n * 1e-13 + n * n * n * 1e-11;
+  }
+  c->psgd_method = (t_svd < t_pow) ? LGRECO_PSGD_SVD : LGRECO_PSGD_POWER;
+  return LGRECO_OK;
+}
+
+extern "C" int lgreco_psgd_method(lgreco_ctx* c) {
+  if (!c || c->family != LGRECO_POWERSGD) { lg_set_error("psgd_method: PowerSGD ctx only"); return LGRECO_EINVAL; }
+  return c->psgd_method;
+}

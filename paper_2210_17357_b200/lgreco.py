@@ -17,6 +17,7 @@ LIB_PATH = os.environ.get("LGRECO_LIB") or os.path.join(_HERE, "liblgreco.so")  
 
 OK, EINVAL, ENONFINITE, EINFEASIBLE, ECUDA, ENCCL, ENOMEM, EUNSUPPORTED = 0, -1, -2, -3, -4, -5, -6, -7
 QSGD, TOPK, POWERSGD = 0, 1, 2
+PSGD_POWER, PSGD_SVD, PSGD_AUTO = 0, 1, 2  # PowerSGD profile method (NEXT-2 selector)
 METRIC_SQ, DISC_FLOOR = 1, 2
 
 
@@ -61,6 +62,8 @@ _SIGS = {
     "lgreco_solve": (C.c_int, [_VP, _VP, _I32, _I32, _VP, _VP, _I32, _U32, _VP, _VP, _VP, C.c_size_t, _VP]),
     "lgreco_weight_costs": (C.c_int, [_VP, _VP, _I32, _I32, _VP, _VP]),
     "lgreco_psgd_profile_svd": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP]),
+    "lgreco_psgd_set_method": (C.c_int, [_VP, C.c_int32]),
+    "lgreco_psgd_method": (C.c_int, [_VP]),
     "lgreco_layer_norms": (C.c_int, [_VP, _VP, _VP, _VP, _VP]),
     "lgreco_p2p_local": (C.c_int, [_VP, _VP]),
     "lgreco_p2p_export": (C.c_int, [_VP, _VP]),
@@ -173,6 +176,16 @@ class Context:
     def profile(self, g, ef, step, err, bits, stream=None):
         _check(lib().lgreco_profile(self.h, _ptr(g), _ptr(ef), step, _ptr(err), _ptr(bits), _stream(stream)),
                "profile")
+
+    def set_psgd_method(self, method):
+        """PSGD_POWER / PSGD_SVD / PSGD_AUTO (NEXT-2 selector)."""
+        _check(lib().lgreco_psgd_set_method(self.h, int(method)), "psgd_set_method")
+
+    def psgd_method(self) -> int:
+        v = int(lib().lgreco_psgd_method(self.h))
+        if v < 0:
+            _check(v, "psgd_method")
+        return v
 
     def profile_svd(self, g, ef, err, bits, stream=None):
         """PowerSGD errors of every candidate rank from the singular values (NEXT-2)."""

@@ -233,3 +233,41 @@ def test_profile_svd_parity(lg, ref, cfg):
     assert np.all((r_err == 0) == (ge == 0))
     assert (np.abs(ge - r_err) / np.maximum(r_err, 1e-300)).max() <= 1e-6
     ctx.close()
+
+
+def test_profile_method_selector(lg, ref):
+    """NEXT-2 selector: AUTO keeps the power method where the rank
+    range is small against the matrix (C2: r_max 16 on up to 512 x 4608) and takes the
+    singular values where it is large against the smaller side (a 3000 x 40 matrix with
+    ranks up to 16 and a 40 x 700 one: n = 40); lgreco_profile then returns exactly what
+    the chosen method's own entry returns, and the SVD result matches the oracle's SVD."""
+    layers = W.config_layers("C2")
+    ctx = lg.Context(layers, lg.POWERSGD, W.PSGD_RANKS_C2, seed=3)
+    assert ctx.psgd_method() == lg.PSGD_POWER
+    ctx.set_psgd_method(lg.PSGD_AUTO)
+    assert ctx.psgd_method() == lg.PSGD_POWER
+    ctx.close()
+    shapes = [(3000, 40), (40, 700)]
+    tall, off = [], 0
+    for m, k in shapes:
+        tall.append(W.Layer(off, m * k, m, k, 1))
+        off += m * k
+    rng = np.random.default_rng(4)
+    g = rng.standard_normal(off).astype(np.float32)
+    ranks = [1, 2, 4, 8, 16]
+    ctx = lg.Context(tall, lg.POWERSGD, ranks, seed=3)
+    ctx.set_psgd_method(lg.PSGD_AUTO)
+    assert ctx.psgd_method() == lg.PSGD_SVD
+    L, K = len(tall), len(ranks)
+    e1 = torch.empty(L, K, dtype=torch.float64, device="cuda")
+    b1 = torch.empty(L, K, dtype=torch.int64, device="cuda")
+    e2, b2 = torch.empty_like(e1), torch.empty_like(b1)
+    gd = _dev(g)
+    ctx.profile(gd, None, 0, e1, b1)
+    ctx.profile_svd(gd, None, e2, b2)
+    assert torch.equal(e1, e2) and torch.equal(b1, b2)
+    r_err, _ = ref.psgd_svd_profile(tall, g, None, ranks)
+    assert (np.abs(e1.cpu().numpy() - r_err) / np.maximum(r_err, 1e-300)).max() <= 1e-6
+    with pytest.raises(lg.LGrecoError):
+        ctx.set_psgd_method(7)
+    ctx.close()
