@@ -222,6 +222,27 @@ int lgreco_compress_allreduce(lgreco_ctx* ctx, const int32_t* h_choice, const fl
 int lgreco_compress_allreduce_dev(lgreco_ctx* ctx, const int32_t* d_choice, const float* d_g, float* d_ef,
                                   float* d_out, uint64_t step, void* stream);
 
+/* ---- NEXT-4: mixed-family plans ("combining different compression
+ * techniques inside the same model") ------------------------------------------------
+ * A hybrid plan picks, per layer, a (family, parameter) column of a table that holds F
+ * families' candidate lists side by side; one ctx per family (same layer table) compresses
+ * the layers whose column is its own.  LGRECO_CHOICE_SKIP in a ctx's choice vector marks
+ * a compressed layer that another family's ctx owns: that ctx leaves the layer's EF and
+ * output untouched (world == 1 device paths of QSGD and TopK; PowerSGD's host path at
+ * any world size); on a layer sent lossless (compress == 0) it marks a ctx that must not
+ * handle it either (lgreco_hybrid_split leaves those to family 0 alone: a second raw pass
+ * would read the EF the first one already zeroed).
+ * lgreco_hybrid_table: err_out[l][c0_f + j] = err_f[l][j] (likewise bits) for the F
+ *   family tables (DEVICE pointers, L x K_f row-major; h_K: HOST K_f), c0_f the prefix
+ *   sum of K.  lgreco_hybrid_split: d_choice (L, a column of that table or -1) -> F
+ *   per-family vectors d_choice_f[f] (f's own index, LGRECO_CHOICE_SKIP for a column of
+ *   another family; -1 (lossless) kept for family 0, LGRECO_CHOICE_SKIP for the others).  Both enqueued on `stream`; EINVAL on bad sizes. */
+#define LGRECO_CHOICE_SKIP (-2)
+int lgreco_hybrid_table(const double* const* h_err_f, const int64_t* const* h_bits_f, const int32_t* h_K, int32_t F,
+                        int32_t L, double* d_err_out, int64_t* d_bits_out, void* stream);
+int lgreco_hybrid_split(const int32_t* d_choice, const int32_t* h_K, int32_t F, int32_t L, int32_t* const* h_choice_f,
+                        void* stream);
+
 /* ---- peer-memory exchange (QSGD, 1 < world <= 8, no NCCL on the data path) ----------
  * A QSGD ctx created with world > 1 and nccl_unique_id == NULL exchanges through the
  * peers' device memory (NVLink P2P stores; R13 unchanged: same shards, same sums, same

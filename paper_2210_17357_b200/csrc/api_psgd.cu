@@ -326,9 +326,12 @@ static int psgd_set_plan(lgreco_ctx* c, const int32_t* choice, cudaStream_t st) 
   if (p->plan_valid && chv == p->plan_choice) return LGRECO_OK;
   std::vector<int32_t> r(p->nM, 0), initf(std::max(1, p->nM), 0);
   std::vector<char> raw(c->L, 1);
+  for (int l = 0; l < c->L; ++l)  // another family's layers (NEXT-4): neither low-rank nor raw
+    if (choice[l] == LGRECO_CHOICE_SKIP) raw[l] = 0;
   for (int i = 0; i < p->nM; ++i) {
     const int l = p->mlayer[i];
     const int j = choice[l];
+    if (j == LGRECO_CHOICE_SKIP) continue;
     if (j < 0 || j >= c->K) {
       lg_set_error("choice[%d]=%d out of range [0,%d)", l, j, c->K);
       return LGRECO_EINVAL;
@@ -340,7 +343,8 @@ static int psgd_set_plan(lgreco_ctx* c, const int32_t* choice, cudaStream_t st) 
     }
   }
   for (int l = 0; l < c->L; ++l)
-    if (c->layers[l].compress && c->layers[l].rows <= 0 && (choice[l] < 0 || choice[l] >= c->K)) {
+    if (c->layers[l].compress && c->layers[l].rows <= 0 && choice[l] != LGRECO_CHOICE_SKIP &&
+        (choice[l] < 0 || choice[l] >= c->K)) {
       lg_set_error("choice[%d]=%d out of range [0,%d)", l, choice[l], c->K);
       return LGRECO_EINVAL;
     }
@@ -415,6 +419,7 @@ int64_t psgd_payload_bytes(lgreco_ctx* c, const int32_t* choice) {
   for (int l = 0; l < c->L; ++l) {
     const lgreco_layer& ly = c->layers[l];
     bool raw = true;
+    if (choice[l] == LGRECO_CHOICE_SKIP) continue;  // another family's layer
     if (ly.compress && ly.rows > 0) {
       const int j = choice[l];
       if (j < 0 || j >= c->K) return LGRECO_EINVAL;

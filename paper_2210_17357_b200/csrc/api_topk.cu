@@ -194,7 +194,7 @@ static int topk_set_plan(lgreco_ctx* c, const int32_t* choice, cudaStream_t st) 
   Topk* t = c->tk;
   std::vector<int32_t> chv(choice, choice + c->L);
   for (int l = 0; l < c->L; ++l)
-    if (!c->layers[l].compress) chv[l] = -1;
+    if (!c->layers[l].compress && chv[l] != LGRECO_CHOICE_SKIP) chv[l] = -1;
   if (t->plan_valid && chv == t->plan_choice) return LGRECO_OK;
   std::vector<lg::TPlan> plan;
   std::vector<int64_t> kplan, kpre;
@@ -276,7 +276,7 @@ int topk_pack(lgreco_ctx* c, const int32_t* choice, const float* g, float* ef, u
     c->launches += 3;
   }
   if (t->n_ll) {
-    LG_LAUNCH(c, lg::launch_lossless_pack(g, ef, payload, out, c->d_layers, t->d_chunks_ll, t->n_ll, t->d_tplan,
+    LG_LAUNCH(c, lg::launch_lossless_pack(g, ef, payload, out, t->d_choice, c->d_layers, t->d_chunks_ll, t->n_ll, t->d_tplan,
                                           c->d_flag, st));
     c->launches += 1;
   }
@@ -316,7 +316,7 @@ int topk_compress_dev(lgreco_ctx* c, const int32_t* d_choice, const float* g, fl
     c->launches += 3;
   }
   if (t->n_ll) {
-    LG_LAUNCH(c, lg::launch_lossless_pack(g, ef, nullptr, out, c->d_layers, t->d_chunks_ll, t->n_ll, t->d_tplan,
+    LG_LAUNCH(c, lg::launch_lossless_pack(g, ef, nullptr, out, d_choice, c->d_layers, t->d_chunks_ll, t->n_ll, t->d_tplan,
                                           c->d_flag, st));
     c->launches += 1;
   }

@@ -114,7 +114,8 @@ cudaError_t launch_plan_topk_dev(const int32_t* choice, const int32_t* params, i
 cudaError_t launch_topk_lossless_rows(const DevLayer* layers, int L, int K, double* err, int64_t* bits, cudaStream_t st);
 cudaError_t launch_topk_compact(const float* g, float* ef, uint8_t* payload, float* out, const TkArgs& a,
                                 cudaStream_t st);
-cudaError_t launch_lossless_pack(const float* g, float* ef, uint8_t* payload, float* out, const DevLayer* layers,
+cudaError_t launch_lossless_pack(const float* g, float* ef, uint8_t* payload, float* out, const int32_t* choice,
+                                 const DevLayer* layers,
                                  const TChunk* chunks, int nchunks, const TPlan* tplan, unsigned* flag,
                                  cudaStream_t st);
 cudaError_t launch_topk_combine(const uint8_t* gathered, int64_t S, int W, float* out, const DevLayer* layers,

@@ -991,8 +991,10 @@ k_qpack(const float* __restrict__ g, float* __restrict__ ef, uint8_t* __restrict
   DevPlan pl;
   if (choice) {  // W = 1: the bits straight from the device choice (k_plan_qsgd_dev's rule)
     int bits = 0;
+    if (choice[ch.layer] == LGRECO_CHOICE_SKIP) return;  // another family's layer (NEXT-4): untouched
     if (ly.compress) {
       int c = choice[ch.layer];
+      if (c == LGRECO_CHOICE_SKIP) return;  // another family's layer (NEXT-4): untouched
       if (c < 0 || c >= K) {
         if (threadIdx.x == 0) atomicOr(flag, 2u);
         c = 0;

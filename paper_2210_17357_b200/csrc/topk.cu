@@ -470,7 +470,8 @@ k_tk_count(const float* __restrict__ g, const float* __restrict__ e, TkArgs a) {
   const DevLayer ly = a.layers[a.clayer[ch.cidx]];
   const TQ qq = a.q[ch.cidx];
   const uint32_t T = qq.T;
-  if (!a.need_off && (qq.r == 0 || qq.r == qq.ties)) {  // every tie kept or none: no prefix needed
+  if (a.kq[ch.cidx] == 0 ||  // a skipped layer (NEXT-4)
+      (!a.need_off && (qq.r == 0 || qq.r == qq.ties))) {  // every tie kept or none: no prefix needed
     if (threadIdx.x == 0) a.ccnt[blockIdx.x] = make_uint2(0u, 0u);
     return;
   }
@@ -530,6 +531,7 @@ k_tk_write(const float* __restrict__ g, float* __restrict__ ef, uint8_t* __restr
   const TQ q = a.q[c];
   const uint32_t T = q.T;
   const int64_t rties = q.r;
+  if (a.kq[c] == 0) return;  // a skipped layer (NEXT-4): EF and output untouched
   const ulonglong2 off = a.coff[blockIdx.x];
   uint2* pairs = payload ? reinterpret_cast<uint2*>(payload + a.tplan[l].pay_off) : nullptr;
   int64_t eq_run = (int64_t)off.y;                                       // ties before this position
@@ -623,8 +625,9 @@ k_tk_write(const float* __restrict__ g, float* __restrict__ ef, uint8_t* __restr
 __global__ void __launch_bounds__(TK_THREADS)
 k_lossless_pack(const float* __restrict__ g, float* __restrict__ ef, uint8_t* __restrict__ payload,
                 float* __restrict__ out, const DevLayer* __restrict__ layers, const TChunk* __restrict__ chunks,
-                const TPlan* __restrict__ tplan, unsigned* __restrict__ flag) {
+                const TPlan* __restrict__ tplan, unsigned* __restrict__ flag, const int32_t* __restrict__ choice) {
   const TChunk ch = chunks[blockIdx.x];  // cidx = layer index here
+  if (choice && choice[ch.cidx] == LGRECO_CHOICE_SKIP) return;  // another family's ctx owns it (NEXT-4)
   const DevLayer ly = layers[ch.cidx];
   float* raw = payload ? reinterpret_cast<float*>(payload + tplan[ch.cidx].pay_off) : nullptr;
   float bad = 0.f;
@@ -693,6 +696,7 @@ __global__ void k_plan_topk_dev(const int32_t* __restrict__ choice, const int32_
   for (int ci = blockIdx.x * blockDim.x + threadIdx.x; ci < nC; ci += gridDim.x * blockDim.x) {
     const int l = clayer[ci];
     int c = choice[l];
+    if (c == LGRECO_CHOICE_SKIP) { kplan[ci] = 0; continue; }  // another family's layer (NEXT-4)
     if (c < 0 || c >= K) { atomicOr(flag, 2u); c = 0; }
     const int64_t n = layers[l].numel;
     int64_t k = ((int64_t)params[c] * n + 999999) / 1000000;
@@ -747,6 +751,7 @@ __global__ void k_tk_reuse(const int32_t* __restrict__ choice, int K, const int3
                            const TQ* __restrict__ qprof, TQ* __restrict__ qc, unsigned* __restrict__ flag) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < nC; c += gridDim.x * blockDim.x) {
     int j = choice[clayer[c]];
+    if (j == LGRECO_CHOICE_SKIP) continue;  // (the layer's kplan is 0: count / write skip it)
     if (j < 0 || j >= K) { atomicOr(flag, 2u); j = 0; }
     qc[c] = qprof[(int64_t)c * K + j];
   }
@@ -768,11 +773,12 @@ cudaError_t launch_topk_compact(const float* g, float* ef, uint8_t* payload, flo
   return cudaGetLastError();
 }
 
-cudaError_t launch_lossless_pack(const float* g, float* ef, uint8_t* payload, float* out, const DevLayer* layers,
+cudaError_t launch_lossless_pack(const float* g, float* ef, uint8_t* payload, float* out, const int32_t* choice,
+                                 const DevLayer* layers,
                                  const TChunk* chunks, int nchunks, const TPlan* tplan, unsigned* flag,
                                  cudaStream_t st) {
   if (nchunks == 0) return cudaSuccess;
-  k_lossless_pack<<<nchunks, TK_THREADS, 0, st>>>(g, ef, payload, out, layers, chunks, tplan, flag);
+  k_lossless_pack<<<nchunks, TK_THREADS, 0, st>>>(g, ef, payload, out, layers, chunks, tplan, flag, choice);
   return cudaGetLastError();
 }
 

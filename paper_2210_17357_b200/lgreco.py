@@ -18,6 +18,7 @@ LIB_PATH = os.environ.get("LGRECO_LIB") or os.path.join(_HERE, "liblgreco.so")  
 OK, EINVAL, ENONFINITE, EINFEASIBLE, ECUDA, ENCCL, ENOMEM, EUNSUPPORTED = 0, -1, -2, -3, -4, -5, -6, -7
 QSGD, TOPK, POWERSGD = 0, 1, 2
 PSGD_POWER, PSGD_SVD, PSGD_AUTO = 0, 1, 2  # PowerSGD profile method (NEXT-2 selector)
+CHOICE_SKIP = -2  # (NEXT-4) a compressed layer another family's ctx owns: left untouched
 METRIC_SQ, DISC_FLOOR = 1, 2
 
 
@@ -63,6 +64,8 @@ _SIGS = {
     "lgreco_weight_costs": (C.c_int, [_VP, _VP, _I32, _I32, _VP, _VP]),
     "lgreco_psgd_profile_svd": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP]),
     "lgreco_psgd_set_method": (C.c_int, [_VP, C.c_int32]),
+    "lgreco_hybrid_table": (C.c_int, [_VP, _VP, _VP, _I32, _I32, _VP, _VP, _VP]),
+    "lgreco_hybrid_split": (C.c_int, [_VP, _VP, _I32, _I32, _VP, _VP]),
     "lgreco_psgd_method": (C.c_int, [_VP]),
     "lgreco_layer_norms": (C.c_int, [_VP, _VP, _VP, _VP, _VP]),
     "lgreco_p2p_local": (C.c_int, [_VP, _VP]),
@@ -364,6 +367,34 @@ def weight_costs(bits, weight, out=None, stream=None):
         out = torch.empty_like(bits)
     _check(lib().lgreco_weight_costs(_ptr(bits), _ptr(weight), L, K, _ptr(out), _stream(stream)), "weight_costs")
     return out
+
+
+def hybrid_table(errs, bits, err_out=None, bits_out=None, stream=None):
+    """NEXT-4: the families' (L, K_f) device tables side by side -> (L, sum K_f) on the device."""
+    F, L = len(errs), errs[0].shape[0]
+    Ks = [int(e.shape[1]) for e in errs]
+    dev = errs[0].device
+    if err_out is None:
+        err_out = torch.empty(L, sum(Ks), dtype=torch.float64, device=dev)
+    if bits_out is None:
+        bits_out = torch.empty(L, sum(Ks), dtype=torch.int64, device=dev)
+    pe = (C.c_void_p * F)(*[e.data_ptr() for e in errs])
+    pb = (C.c_void_p * F)(*[b.data_ptr() for b in bits])
+    _check(lib().lgreco_hybrid_table(C.cast(pe, C.c_void_p), C.cast(pb, C.c_void_p), _i32(Ks), F, L, _ptr(err_out),
+                                     _ptr(bits_out), _stream(stream)), "hybrid_table")
+    return err_out, bits_out
+
+
+def hybrid_split(choice, Ks, outs=None, stream=None):
+    """NEXT-4: a hybrid plan (device (L,) column indices) -> one device choice vector per
+    family (its own index, CHOICE_SKIP where another family owns the layer)."""
+    L, F = choice.numel(), len(Ks)
+    if outs is None:
+        outs = [torch.empty(L, dtype=torch.int32, device=choice.device) for _ in range(F)]
+    po = (C.c_void_p * F)(*[o.data_ptr() for o in outs])
+    _check(lib().lgreco_hybrid_split(_ptr(choice), _i32(Ks), F, L, C.cast(po, C.c_void_p), _stream(stream)),
+           "hybrid_split")
+    return outs
 
 
 def read_info(info_tensor) -> SolveInfo:

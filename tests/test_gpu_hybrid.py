@@ -1,0 +1,107 @@
+"""NEXT-4 mixed-family compression: one context per family on the same
+layer table, a joint (family, parameter) plan, per-layer dispatch with CHOICE_SKIP.
+Every layer's output and EF must equal its own family's oracle (QSGD / TopK bitwise,
+PowerSGD 1e-5 normwise); the joint table and its solve equal the oracle's."""
+import numpy as np
+import pytest
+import torch
+
+from paper_2210_17357_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+BITS, PPM, RANKS = [2, 4, 8], [10000, 100000], [1, 4]
+SEED = 21
+
+
+@pytest.fixture(scope="module")
+def lg():
+    from paper_2210_17357_b200 import lgreco
+    return lgreco
+
+
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _layers():
+    shapes = [(40, 30, 1), (0, 17, 0), (64, 200, 1), (130, 70, 1), (0, 999, 1), (257, 96, 1), (33, 33, 1)]
+    out, off = [], 0
+    for m, k, c in shapes:
+        n = m * k if m else k
+        out.append(W.Layer(off, n, m, k if m else 0, c))
+        off += n
+    return out
+
+
+def _rel(a, b):
+    return np.linalg.norm(np.asarray(a, np.float64) - np.asarray(b, np.float64)) / max(np.linalg.norm(b), 1e-300)
+
+
+def _oracle(ref, layers, fam, par, g, e, step):
+    """Compose the families' oracles: layer l's out / EF from the oracle of fam[l]."""
+    L = len(layers)
+    lbits = [BITS[par[l]] if fam[l] == 0 and layers[l].compress else 0 for l in range(L)]
+    oq, eq, _, _ = ref.qsgd_allreduce(layers, lbits, [g], [e.copy()], seed=SEED, step=step)
+    lppm = [PPM[par[l]] if fam[l] == 1 else (1000000 if layers[l].compress else 0) for l in range(L)]
+    ot, et, _ = ref.topk_allreduce(layers, lppm, [g], [e.copy()])
+    lrank = [RANKS[par[l]] if fam[l] == 2 else 0 for l in range(L)]
+    Qs = {}
+    for l, ly in enumerate(layers):
+        r = lrank[l]
+        if r and ly.rows and not ref.psgd_lossless(ly.rows, ly.cols, r):
+            Qs[l] = ref.psgd_init_q(SEED, l, step, ly.cols, r)
+    op, ep, _ = ref.psgd_allreduce(layers, lrank, [g], [e.copy()], Qs)
+    return (oq, eq[0]), (ot, et[0]), (op, ep[0]), Qs
+
+
+@pytest.mark.parametrize("mode", ["fixed", "solved"])
+def test_hybrid_plan_dispatch(lg, ref, mode):
+    from paper_2210_17357_b200.hybrid import Hybrid
+    layers = _layers()
+    L = len(layers)
+    g, e = W.low_rank_plus_noise(layers, seed=3, with_ef=True)
+    h = Hybrid(layers, [(lg.QSGD, BITS), (lg.TOPK, PPM), (lg.POWERSGD, RANKS)], seed=SEED, default_family=0,
+               default_idx=1)
+    gd, ed = _dev(g), _dev(e)
+    err, bits = h.profile(gd, ed, 0)
+    # the joint table is the families' tables side by side
+    ks = [len(BITS), len(PPM), len(RANKS)]
+    eq, bq = ref.qsgd_profile(layers, g, e, BITS, seed=SEED, step=0)
+    assert np.array_equal(bits.cpu().numpy()[:, :ks[0]], bq)
+    if mode == "fixed":  # every family owns some layers
+        fam = [0, 0, 1, 2, 1, 0, 2]
+        par = [1, 0, 1, 1, 0, 2, 0]
+        cols = [(h.col0[f] + p) if layers[l].compress else -1 for l, (f, p) in enumerate(zip(fam, par))]
+        choice = torch.tensor(cols, dtype=torch.int32, device="cuda")
+    else:
+        comp = torch.tensor([l.compress for l in layers], dtype=torch.int32, device="cuda")
+        choice, info = h.solve(err, bits, comp)
+        dflt = np.full(L, h.default_col, np.int32)
+        st, c_ref, _ = ref.solve(err.cpu().numpy(), bits.cpu().numpy(), dflt, comp.cpu().numpy(), D=10000)
+        assert list(choice.cpu().numpy()) == list(c_ref)
+        cols = list(c_ref)
+        fam, par = [], []
+        for c in cols:
+            f = 0 if c < 0 else max(i for i in range(3) if c >= h.col0[i])
+            fam.append(f)
+            par.append(0 if c < 0 else c - h.col0[f])
+    out = torch.empty_like(gd)
+    h.compress_allreduce(choice, gd, ed, out, 0)
+    h.check()
+    (oq, eqs), (ot, ets), (op, eps), Qs = _oracle(ref, layers, fam, par, g, e, 0)
+    o, ef = out.cpu().numpy(), ed.cpu().numpy()
+    for l, ly in enumerate(layers):
+        sl = slice(ly.offset, ly.offset + ly.numel)
+        if not ly.compress:
+            assert np.array_equal(o[sl].view(np.uint32), oq[sl].view(np.uint32)) and not ef[sl].any()
+        elif fam[l] == 0:
+            assert np.array_equal(o[sl].view(np.uint32), oq[sl].view(np.uint32)), l
+            assert np.array_equal(ef[sl].view(np.uint32), eqs[sl].view(np.uint32)), l
+        elif fam[l] == 1:
+            assert np.array_equal(o[sl].view(np.uint32), ot[sl].view(np.uint32)), l
+            assert np.array_equal(ef[sl].view(np.uint32), ets[sl].view(np.uint32)), l
+        else:
+            assert _rel(o[sl], op[sl]) <= 1e-5, l
+            assert _rel(ef[sl], eps[sl]) <= 1e-5, l
+    h.close()
