@@ -21,6 +21,7 @@ struct Topk {
   ulonglong2* coff = nullptr;
   uint32_t* ckeys = nullptr;
   int32_t* ckn = nullptr;
+  int32_t* ckz = nullptr;
   lg::TPlan* d_tplan = nullptr;
   // plan cache + pinned staging [TPlan L | kplan nC | kpre nC+1]
   std::vector<int32_t> plan_choice;
@@ -55,7 +56,7 @@ static lg::TkArgs tk_args(lgreco_ctx* c, const int64_t* kq) {
   a.cnt1 = t->cnt1; a.sum1 = t->sum1; a.cnt2 = t->cnt2; a.sum2 = t->sum2; a.cnt3 = t->cnt3;
   a.n1 = t->n1; a.n2 = t->n2; a.sl1 = t->sl1; a.sl2 = t->sl2;
   a.q = t->q; a.kq = kq; a.ccnt = t->ccnt; a.coff = t->coff; a.tplan = t->d_tplan; a.flag = c->d_flag;
-  a.ckeys = t->ckeys; a.ckn = t->ckn;
+  a.ckeys = t->ckeys; a.ckn = t->ckn; a.ckz = t->ckz;
   return a;
 }
 
@@ -120,6 +121,7 @@ int topk_init(lgreco_ctx* c, cudaStream_t st) {
   TK_ALLOC(t->coff, sizeof(ulonglong2) * std::max<size_t>(1, ch.size()));
   TK_ALLOC(t->ckeys, sizeof(uint32_t) * lg::TK_CKCAP * std::max<size_t>(1, ch.size()));
   TK_ALLOC(t->ckn, sizeof(int32_t) * std::max<size_t>(1, ch.size()));
+  TK_ALLOC(t->ckz, sizeof(int32_t) * std::max<size_t>(1, ch.size()));
   TK_ALLOC(t->d_tplan, sizeof(lg::TPlan) * L);
   TK_ALLOC(t->qc, sizeof(lg::TQ) * nC);
   TK_ALLOC(t->d_choice, sizeof(int32_t) * L);
@@ -149,7 +151,7 @@ void topk_destroy(lgreco_ctx* c) {
   cudaFree(t->d_cchunk0); cudaFree(t->cnt1); cudaFree(t->sum1); cudaFree(t->cnt2); cudaFree(t->sum2);
   cudaFree(t->cnt3); cudaFree(t->n1); cudaFree(t->n2); cudaFree(t->sl1); cudaFree(t->sl2); cudaFree(t->q);
   cudaFree(t->d_kprof); cudaFree(t->d_kplan); cudaFree(t->d_kpre); cudaFree(t->ccnt); cudaFree(t->coff);
-  cudaFree(t->d_tplan); cudaFree(t->d_pay); cudaFree(t->d_gath); cudaFree(t->ckeys); cudaFree(t->ckn);
+  cudaFree(t->d_tplan); cudaFree(t->d_pay); cudaFree(t->d_gath); cudaFree(t->ckeys); cudaFree(t->ckn); cudaFree(t->ckz);
   cudaFree(t->qc); cudaFree(t->d_choice);
   if (t->h_stage) cudaFreeHost(t->h_stage);
   if (t->evt) cudaEventDestroy(t->evt);

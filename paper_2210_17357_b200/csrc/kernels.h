@@ -102,6 +102,7 @@ struct TkArgs {
   int32_t* n1; int32_t* n2; int32_t* sl1; uint32_t* sl2;
   TQ* q; const int64_t* kq; uint2* ccnt; ulonglong2* coff; const TPlan* tplan; unsigned* flag;
   uint32_t* ckeys; int32_t* ckn;  // per chunk: keys of its boundary level-1 bins (pass2 -> pass3), count
+  int32_t* ckz;                   // per chunk: its zero keys when the zero bin is a boundary bin (not compacted)
   int need_off = 1;  // 0: no payload (W = 1 fused): chunks of layers keeping all or none of T's ties skip the count
 };
 cudaError_t launch_topk_reuse(const int32_t* choice, int K, const int32_t* clayer, int nC, const TQ* qprof, TQ* qc,

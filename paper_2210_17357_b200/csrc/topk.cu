@@ -253,22 +253,31 @@ k_tk_pass2(const float* __restrict__ g, const float* __restrict__ e, TkArgs a, i
   __syncthreads();
   uint32_t* ck = a.ckeys + (int64_t)blockIdx.x * TK_CKCAP;
   uint32_t zc = 0;
+  __shared__ unsigned s_zc;
+  if (threadIdx.x == 0) s_zc = 0;
+  __syncthreads();
   for_chunk(g, e, ly, ch, [&](int64_t, float x) {
     const uint32_t key = tkey(x);
     const uint32_t s = tbl[key >> 20];
     if (s == 0xFF) return;
+    if (key == 0) { ++zc; return; }  // zeros are counted, not compacted (pass 3 adds ckz)
     // keep the key for pass 3 (order-free counting): no re-read of the chunk there
     const int pos = atomicAdd(&s_kn, 1);
     if (pos < TK_CKCAP) ck[pos] = key;
-    if (key == 0) { ++zc; return; }
     const int64_t idx = (int64_t)s * 1024 + ((key >> 10) & 1023u);
     atomicAdd(c2 + idx, 1u);
     if (WS) atomicAdd(s2 + idx, fx_sq(key));
   });
   zc = warp_sum_u32(zc);
-  if ((threadIdx.x & 31) == 0 && zc) atomicAdd(c2 + (int64_t)tbl[0] * 1024, zc);
+  if ((threadIdx.x & 31) == 0 && zc) {
+    atomicAdd(c2 + (int64_t)tbl[0] * 1024, zc);
+    atomicAdd(&s_zc, zc);
+  }
   __syncthreads();
-  if (threadIdx.x == 0) a.ckn[blockIdx.x] = s_kn;  // > TK_CKCAP: pass 3 rescans the chunk
+  if (threadIdx.x == 0) {
+    a.ckn[blockIdx.x] = s_kn;  // > TK_CKCAP: pass 3 rescans the chunk
+    a.ckz[blockIdx.x] = (int32_t)s_zc;
+  }
 }
 
 // scan a 1024-bin count histogram from the top with one warp: returns the bin holding
@@ -406,9 +415,10 @@ k_tk_pass3(const float* __restrict__ g, const float* __restrict__ e, TkArgs a, i
     atomicAdd(c3 + (int64_t)lo * 1024 + (key & 1023u), 1u);
   };
   const int kn = a.ckn[blockIdx.x];
-  if (kn <= TK_CKCAP) {  // the chunk's boundary keys, compacted by pass 2
+  if (kn <= TK_CKCAP) {  // the chunk's boundary keys, compacted by pass 2 (zeros counted there)
     const uint32_t* ck = a.ckeys + (int64_t)blockIdx.x * TK_CKCAP;
     for (int i = threadIdx.x; i < kn; i += TK_THREADS) count(ck[i]);
+    if (threadIdx.x == 0) zc += (uint32_t)a.ckz[blockIdx.x];
   } else {
     for_chunk(g, e, ly, ch, [&](int64_t, float x) { count(tkey(x)); });
   }
@@ -497,6 +507,10 @@ __global__ void __launch_bounds__(TK_THREADS)
 k_tk_scan(TkArgs a) {
   __shared__ unsigned long long sg[TK_THREADS], se[TK_THREADS];
   const int c = blockIdx.x, tid = threadIdx.x;
+  {  // no payload and a tie-trivial (or skipped) layer: its offsets are never read
+    const TQ qq = a.q[c];
+    if (!a.need_off && (a.kq[c] == 0 || qq.r == 0 || qq.r == qq.ties)) return;
+  }
   const int c0 = a.cchunk0[c], c1 = a.cchunk0[c + 1];
   unsigned long long baseg = 0, basee = 0;
   for (int s = c0; s < c1; s += TK_THREADS) {
