@@ -16,6 +16,7 @@ struct Psgd {
   lg::PTile *d_rt_prof = nullptr, *d_ct_prof = nullptr, *d_rt128_prof = nullptr, *d_ct128_prof = nullptr;
   lg::PTile* d_et_prof = nullptr;
   int n_prof = 0, nrt_prof = 0, nct_prof = 0, rmax_prof = 0, nrt128_prof = 0, nct128_prof = 0, net_prof = 0;
+  int mmax_prof = 0, mmax_c = 0;
   int32_t* d_et0_prof = nullptr;
   lg::PTile *d_gcp_prof = nullptr, *d_gcq_prof = nullptr;  // Gram row chunks (P-shaped / Q-shaped)
   int32_t *d_gcp0_prof = nullptr, *d_gcq0_prof = nullptr;
@@ -162,6 +163,7 @@ int psgd_init(lgreco_ctx* c, cudaStream_t st) {
   std::vector<int32_t> et0;
   GramChunks gcs;
   ps_config(c, p->rprof, pl, rt, ct, et0, p->rmax_prof, rt128, ct128, et, gcs);
+  for (const auto& x : pl) p->mmax_prof = std::max(p->mmax_prof, (int)x.m);
   p->ngcp_prof = (int)gcs.p.size();
   p->ngcq_prof = (int)gcs.q.size();
   p->n_prof = (int)pl.size(); p->nrt_prof = (int)rt.size(); p->nct_prof = (int)ct.size();
@@ -284,6 +286,7 @@ static lg::PsArgs ps_args_prof(lgreco_ctx* c, const float* g, const float* e) {
   a.gcp = p->d_gcp_prof; a.n_gcp = p->ngcp_prof; a.gcp0 = p->d_gcp0_prof;
   a.gcq = p->d_gcq_prof; a.n_gcq = p->ngcq_prof; a.gcq0 = p->d_gcq0_prof;
   a.gpart = p->gpart;
+  a.mmax = p->mmax_prof;
   return a;
 }
 static lg::PsArgs ps_args_c(lgreco_ctx* c, const float* g, const float* e) {
@@ -292,6 +295,7 @@ static lg::PsArgs ps_args_c(lgreco_ctx* c, const float* g, const float* e) {
                p->d_rt128_c, p->nrt128_c, p->d_ct128_c, p->nct128_c, p->d_et_c, p->net_c, nullptr};
   a.gcp = p->d_gcp_c; a.n_gcp = p->ngcp_c; a.gcp0 = p->d_gcp0_c;
   a.gpart = p->gpart;
+  a.mmax = p->mmax_c;
   return a;
 }
 
@@ -354,6 +358,8 @@ static int psgd_set_plan(lgreco_ctx* c, const int32_t* choice, cudaStream_t st) 
   int rmax = 0;
   GramChunks gcs;
   ps_config(c, r, pl, rt, ct, et0, rmax, rt128, ct128, et, gcs);
+  int mmax = 0;
+  for (const auto& x : pl) mmax = std::max(mmax, (int)x.m);
   // init flags follow the compress config order (layers with r > 0)
   int ci = 0;
   bool any_init = false;
@@ -405,6 +411,7 @@ static int psgd_set_plan(lgreco_ctx* c, const int32_t* choice, cudaStream_t st) 
   p->n_c = (int)pl.size(); p->nrt_c = (int)rt.size(); p->nct_c = (int)ct.size(); p->rmax_c = rmax;
   p->nrt128_c = (int)rt128.size(); p->nct128_c = (int)ct128.size(); p->net_c = (int)et.size();
   p->ngcp_c = (int)gcs.p.size();
+  p->mmax_c = mmax;
   p->nraw = (int)segs.size();
   p->Sraw = off;
   p->need_init = any_init;

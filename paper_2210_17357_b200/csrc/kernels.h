@@ -149,6 +149,7 @@ struct PsArgs {
   const PTile* gcp = nullptr; int n_gcp = 0; const int32_t* gcp0 = nullptr;
   const PTile* gcq = nullptr; int n_gcq = 0; const int32_t* gcq0 = nullptr;
   double* gpart = nullptr;
+  int mmax = 0;  // the largest m of the config (the fused small-layer CholQR2 when it fits)
 };
 // profile-error work buffers: d / ||M||^2 partials [etiles][RMAX+1], G_P, G_Q (per layer
 // r x r at goff), the per-layer fallback flag

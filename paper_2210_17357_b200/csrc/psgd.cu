@@ -733,10 +733,122 @@ cudaError_t launch_ps_gram(const PsArgs& a, const float* X, int isq, float scale
   return cudaGetLastError();
 }
 
+// CholQR2 of small layers in one kernel (one CTA per layer, the layer's P in shared
+// memory as fp64): Gram (thread per entry, rows in order), Cholesky (as k_ps_chol),
+// forward substitution per row (as k_ps_cholsolve), the fp32 rounding of Phat, and the
+// same again on that Phat -- one launch per power step instead of eight
+template <int RMAX>
+__global__ void __launch_bounds__(256)
+k_ps_cholqr2_small(const PLayer* __restrict__ pl, const float* __restrict__ P, float scale, float* __restrict__ Ph) {
+  extern __shared__ __align__(16) double qsm_[];
+  constexpr int LG = RMAX + 1, XS = RMAX + 1;  // (odd row strides: the row-per-thread solve is conflict-free)
+  const PLayer p = pl[blockIdx.x];
+  const int m = p.m, r = p.r, t = threadIdx.x, NT = blockDim.x;
+  double* X = qsm_;                      // [m][XS]
+  double* Rm = X + (size_t)m * XS;       // [RMAX][LG]
+  double* gd = Rm + RMAX * LG;           // [RMAX] diagonal of G
+  double* rinv = gd + RMAX;              // [RMAX]
+  __shared__ double s_d;
+  __shared__ int s_z;
+  for (int q0 = 0; q0 < m * RMAX; q0 += 8 * NT) {  // 8 loads in flight per thread
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int q = q0 + u * NT + t, j = q / m, i = q - j * m;  // coalesced along i
+      v[u] = (q < m * RMAX && j < r) ? __ldg(P + p.poff + (int64_t)j * m + i) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int q = q0 + u * NT + t, j = q / m, i = q - j * m;
+      if (q < m * RMAX) X[i * XS + j] = (double)__fmul_rn(v[u], scale);
+    }
+  }
+  __syncthreads();
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int q = t; q < r * r; q += NT) {
+      const int a = q / r, b = q - a * r;
+      double s4[4] = {0.0, 0.0, 0.0, 0.0};  // rows i = 4u + v into s4[v] (four chains), then in order
+      int i = 0;
+      for (; i + 4 <= m; i += 4) {
+#pragma unroll
+        for (int v2 = 0; v2 < 4; ++v2) s4[v2] = fma(X[(i + v2) * XS + a], X[(i + v2) * XS + b], s4[v2]);
+      }
+      for (; i < m; ++i) s4[0] = fma(X[i * XS + a], X[i * XS + b], s4[0]);
+      const double s = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+      Rm[a * LG + b] = s;
+      if (a == b) gd[a] = s;
+    }
+    __syncthreads();
+    for (int j = 0; j < r; ++j) {
+      if (t == 0) {
+        const double d = Rm[j * LG + j];
+        const bool z = !(d > 1e-24 * gd[j]) || gd[j] == 0.0;
+        s_z = z;
+        s_d = z ? 0.0 : sqrt(d);
+        Rm[j * LG + j] = s_d;
+      }
+      __syncthreads();
+      const bool z = s_z;
+      const double d = s_d;
+      for (int b = j + 1 + t; b < r; b += NT) Rm[j * LG + b] = z ? 0.0 : Rm[j * LG + b] / d;
+      __syncthreads();
+      const int nn = r - j - 1;
+      for (int q = t; q < nn * nn; q += NT) {
+        const int aa = j + 1 + q / nn, bb = j + 1 + q % nn;
+        if (aa <= bb) Rm[aa * LG + bb] = fma(-Rm[j * LG + aa], Rm[j * LG + bb], Rm[aa * LG + bb]);
+      }
+      __syncthreads();
+    }
+    for (int j = t; j < r; j += NT) rinv[j] = (Rm[j * LG + j] == 0.0) ? 0.0 : 1.0 / Rm[j * LG + j];
+    __syncthreads();
+    for (int i = t; i < m; i += NT) {  // row i in place (rows are independent)
+      double ph[RMAX];
+#pragma unroll
+      for (int j = 0; j < RMAX; ++j) {
+        if (j < r) {
+          double s = X[i * XS + j];
+#pragma unroll
+          for (int u = 0; u < j; ++u) s -= ph[u] * Rm[u * LG + j];
+          ph[j] = s * rinv[j];
+        } else {
+          ph[j] = 0.0;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < RMAX; ++j) {
+        const float f = (float)ph[j];
+        X[i * XS + j] = (double)f;  // pass 2 works on the rounded Phat, like the chunked path
+        if (pass == 1 && j < r) Ph[p.poff + (int64_t)j * m + i] = f;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 cudaError_t launch_ps_orth(const PsArgs& a, const float* P, float scale, double* G, float* Ph, cudaStream_t st) {
   if (a.nC == 0) return cudaSuccess;
   // Cholesky-QR twice (CholQR2): the second pass restores orthogonality to round-off
   // when P is ill-conditioned (nearly dependent power-iteration columns)
+  // small layers: the whole CholQR2 in one launch
+  {
+    const int RM = a.rmax <= 16 ? 16 : a.rmax <= 32 ? 32 : 64;
+    const size_t smem = sizeof(double) * ((size_t)a.mmax * (RM + 1) + RM * (RM + 1) + 2 * RM);
+    if (a.mmax > 0 && smem <= 160 * 1024 && !getenv("LGRECO_PS_NO_FUSED_QR")) {
+      cudaError_t e = cudaSuccess;
+      if (RM == 16) {
+        e = memo_smem_attr((const void*)k_ps_cholqr2_small<16>, smem);
+        if (e == cudaSuccess) k_ps_cholqr2_small<16><<<a.nC, 256, smem, st>>>(a.pl, P, scale, Ph);
+      } else if (RM == 32) {
+        e = memo_smem_attr((const void*)k_ps_cholqr2_small<32>, smem);
+        if (e == cudaSuccess) k_ps_cholqr2_small<32><<<a.nC, 256, smem, st>>>(a.pl, P, scale, Ph);
+      } else {
+        e = memo_smem_attr((const void*)k_ps_cholqr2_small<64>, smem);
+        if (e == cudaSuccess) k_ps_cholqr2_small<64><<<a.nC, 256, smem, st>>>(a.pl, P, scale, Ph);
+      }
+      if (e != cudaSuccess) return e;
+      return cudaGetLastError();
+    }
+  }
   const dim3 gg(a.nC, (a.rmax * (a.rmax + 1) / 2 + PS_THREADS / 32 - 1) / (PS_THREADS / 32));
   auto solve = [&](const float* src, float sc) {
     if (a.rmax <= 16) {

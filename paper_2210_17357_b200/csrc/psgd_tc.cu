@@ -17,6 +17,7 @@
 // the next tile's MMAs run.  tcgen05.ld 32x32b: warp w reads TMEM lanes 32w..32w+31 =
 // tile rows -> column-major P.
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <algorithm>
 
@@ -370,16 +371,281 @@ k_ps_tc(const float* __restrict__ g, const float* __restrict__ e, const PLayer* 
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "r"(TMEM_COLS));
 }
 
+// ---------------------------------------------------------------------------
+// Warp-specialised variant (round 2): the same math per K step (3xTF32, a fresh TMEM
+// accumulator per step added in fp32 registers), the roles decoupled by mbarriers so the
+// conversion of step s+1, the MMAs of step s and the drain of step s-1 overlap:
+//   warps 0-7  load (cp.async ring, RS stages) + convert into NOS operand stages
+//   warp 8     lane 0 issues the MMAs (waits op_full, tm_empty; commits mma_done, op_empty)
+//   warps 9-12 drain TMEM (lane quarter warp % 4), add, write the tile at its last K step
+// ---------------------------------------------------------------------------
+constexpr int TC2_CONV = 256;  // converter threads (warps 0-7)
+constexpr int TC2_THREADS = TC2_CONV + 32 + 128;
+constexpr int TC2_NOS = 2;
+constexpr int TC2_NTM = 4;
+
+template <int NP>
+struct Tc2Smem {
+  static constexpr int RAW_X = TC_M * TC_KT * 4;
+  static constexpr int RAW_B = NP * TC_KT * 4;
+  static constexpr int RAW = 2 * RAW_X + RAW_B;
+  static constexpr int A_BYTES = TC_M * 128;
+  static constexpr int B_BYTES = NP * 128;
+  static constexpr int OPS = 2 * A_BYTES + 2 * B_BYTES;
+  static constexpr int RS = (TC2_NOS * OPS + 4 * RAW + 1024 <= 220 * 1024) ? 4 : 3;
+  static constexpr int TOTAL = TC2_NOS * OPS + RS * RAW + 1024;
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void conv_sync() { asm volatile("bar.sync 1, %0;" ::"n"(TC2_CONV) : "memory"); }
+
+template <int NP, bool TRANS>
+__global__ void __launch_bounds__(TC2_THREADS, 1)
+k_ps_tc2(const float* __restrict__ g, const float* __restrict__ e, const PLayer* __restrict__ pl,
+         const PTile* __restrict__ tiles, int ntiles, const float* __restrict__ Bsrc, float* __restrict__ out) {
+  using SM = Tc2Smem<NP>;
+  constexpr uint32_t TMEM_COLS = TC2_NTM * NP < 32 ? 32 : TC2_NTM * NP;
+  extern __shared__ __align__(1024) uint8_t smem_dyn[];
+  uint8_t* smem = smem_dyn + ((1024u - (smem_u32(smem_dyn) & 1023u)) & 1023u);
+  uint8_t* raw0 = smem + TC2_NOS * SM::OPS;
+  __shared__ uint64_t op_full[TC2_NOS], op_empty[TC2_NOS], mma_done[TC2_NTM], tm_empty[TC2_NTM];
+  __shared__ uint32_t tmem_base_sh;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  struct TileG { PTile tl; PLayer p; int rows, kbeg, kend, nk; };
+  auto geo = [&](int t) {
+    TileG G;
+    G.tl = tiles[t];
+    G.p = pl[G.tl.ci];
+    G.rows = TRANS ? min(TC_M, G.p.k - G.tl.c0) : min(TC_M, G.p.m - G.tl.i0);
+    G.kbeg = TRANS ? G.tl.i0 : G.tl.c0;
+    G.kend = G.tl.i1;
+    G.nk = (G.kend - G.kbeg + TC_KT - 1) / TC_KT;
+    return G;
+  };
+  int nsteps = 0;
+  for (int t = blockIdx.x; t < ntiles; t += gridDim.x) nsteps += geo(t).nk;
+  constexpr int WM = TC2_CONV / 32;  // the MMA warp; drain warps WM+1 .. WM+4
+  if (warp == WM) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int b = 0; b < TC2_NOS; ++b) { mbar_init(&op_full[b], 1); mbar_init(&op_empty[b], 1); }
+    for (int b = 0; b < TC2_NTM; ++b) { mbar_init(&mma_done[b], 1); mbar_init(&tm_empty[b], 4); }
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem_d = tmem_base_sh;
+
+  if (warp < WM) {
+    // ---- converters: the raw ring (as k_ps_tc, 128 threads) and the operand stages
+    constexpr int TC_RS = SM::RS;
+    int ti = blockIdx.x, kti = 0;
+    TileG gi = geo(min(ti, ntiles - 1));
+    auto issue = [&](int step) {
+      uint8_t* rg = raw0 + (step % TC_RS) * SM::RAW;
+      uint8_t* re = rg + SM::RAW_X;
+      uint8_t* rb = re + SM::RAW_X;
+      const PLayer& p = gi.p;
+      const PTile& tl = gi.tl;
+      const int k0 = gi.kbeg + kti * TC_KT, kend = gi.kend, rows = gi.rows;
+      const bool a16 = ((p.moff & 3) == 0) && ((p.k & 3) == 0);
+      const int64_t bld = TRANS ? (int64_t)p.m : (int64_t)p.k;
+      const int64_t boff = TRANS ? p.poff : p.qoff;
+      const bool b16 = ((boff & 3) == 0) && ((bld & 3) == 0);
+#pragma unroll
+      for (int it = 0; it < TC_M * TC_KT / 4 / TC2_CONV; ++it) {
+        const int idx = it * TC2_CONV + tid;
+        int64_t xi;
+        int nval;
+        if (!TRANS) {
+          const int r_ = idx >> 3, ch = idx & 7, col = k0 + ch * 4;
+          nval = (r_ < rows) ? max(0, min(4, kend - col)) : 0;
+          xi = p.moff + (int64_t)(tl.i0 + min(r_, rows - 1)) * p.k + col;
+        } else {
+          const int kr = idx >> 5, cq = idx & 31, i = k0 + kr, c = tl.c0 + cq * 4;
+          nval = (i < kend) ? max(0, min(4, tl.c0 + rows - c)) : 0;
+          xi = p.moff + (int64_t)min(i, kend - 1) * p.k + c;
+        }
+        const int slot = TRANS ? ((idx & 31) * 32 + ((idx >> 5) ^ (idx & 31))) : idx;
+        if (a16) {
+          cp16(rg + slot * 16, g + xi, 4 * nval);
+          if (e) cp16(re + slot * 16, e + xi, 4 * nval);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            cp4(rg + slot * 16 + 4 * q, g + xi + (q < nval ? q : 0), q < nval ? 4 : 0);
+            if (e) cp4(re + slot * 16 + 4 * q, e + xi + (q < nval ? q : 0), q < nval ? 4 : 0);
+          }
+        }
+      }
+      for (int idx = tid; idx < NP * 8; idx += TC2_CONV) {
+        const int j = idx >> 3, ch = idx & 7, col = k0 + ch * 4;
+        const int nval = (j < p.r) ? max(0, min(4, kend - col)) : 0;
+        const float* src = Bsrc + boff + (int64_t)min(j, p.r - 1) * bld + col;
+        if (b16) {
+          cp16(rb + idx * 16, src, 4 * nval);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) cp4(rb + idx * 16 + 4 * q, src + (q < nval ? q : 0), q < nval ? 4 : 0);
+        }
+      }
+      if (++kti >= gi.nk) {
+        kti = 0;
+        ti += gridDim.x;
+        if (ti < ntiles) gi = geo(ti);
+      }
+    };
+#pragma unroll
+    for (int s = 0; s < TC_RS - 1; ++s) {
+      if (s < nsteps) issue(s);
+      cp_commit();
+    }
+    for (int s = 0; s < nsteps; ++s) {
+      if (s + TC_RS - 1 < nsteps) issue(s + TC_RS - 1);
+      cp_commit();
+      cp_wait<TC_RS - 1>();
+      conv_sync();  // every converter's copies of step s landed
+      const int ob = s % TC2_NOS;
+      if (s >= TC2_NOS) mbar_wait(&op_empty[ob], ((s / TC2_NOS) - 1) & 1);  // MMAs of step s - NOS done
+      const uint8_t* rg = raw0 + (s % TC_RS) * SM::RAW;
+      const uint8_t* re = rg + SM::RAW_X;
+      const uint8_t* rb = re + SM::RAW_X;
+      uint8_t* Ah = smem + ob * SM::OPS;
+      uint8_t* Al = Ah + SM::A_BYTES;
+      uint8_t* Bh = Al + SM::A_BYTES;
+      uint8_t* Bl = Bh + SM::B_BYTES;
+#pragma unroll
+      for (int it = 0; it < TC_M * TC_KT / 4 / TC2_CONV; ++it) {
+        const int idx = it * TC2_CONV + tid;
+        const int kr = idx & 31, cq = idx >> 5;
+        const int slot = TRANS ? (cq * 32 + (kr ^ cq)) : idx;
+        const float4 a = *reinterpret_cast<const float4*>(rg + slot * 16);
+        const float4 b = e ? *reinterpret_cast<const float4*>(re + slot * 16) : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 v = make_float4(canon(a.x, b.x), canon(a.y, b.y), canon(a.z, b.z), canon(a.w, b.w));
+        if (!TRANS) {
+          put_chunk(Ah, Al, idx >> 3, idx & 7, v);
+        } else {
+          const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int arow = cq * 4 + q;
+            const uint32_t off = (uint32_t)arow * 128u + (uint32_t)((((kr >> 2) ^ (arow & 7))) << 4) + (uint32_t)(kr & 3) * 4u;
+            const uint32_t h = tf32_hi(vv[q]);
+            *reinterpret_cast<uint32_t*>(Ah + off) = h;
+            *reinterpret_cast<uint32_t*>(Al + off) = __float_as_uint(__fsub_rn(vv[q], __uint_as_float(h)));
+          }
+        }
+      }
+      for (int idx = tid; idx < NP * 8; idx += TC2_CONV)
+        put_chunk(Bh, Bl, idx >> 3, idx & 7, *reinterpret_cast<const float4*>(rb + idx * 16));
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      conv_sync();  // the stage is complete (and step s's raw slot is free for re-issue)
+      if (tid == 0) mbar_arrive(&op_full[ob]);
+    }
+    cp_wait<0>();
+  } else if (warp == WM) {
+    // ---- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = tf32_idesc(NP);
+      for (int s = 0; s < nsteps; ++s) {
+        const int ob = s % TC2_NOS, tb = s % TC2_NTM;
+        mbar_wait(&op_full[ob], (s / TC2_NOS) & 1);
+        if (s >= TC2_NTM) mbar_wait(&tm_empty[tb], ((s / TC2_NTM) - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        uint8_t* Ah = smem + ob * SM::OPS;
+        const uint32_t sAh = smem_u32(Ah), sAl = sAh + SM::A_BYTES, sBh = sAl + SM::A_BYTES, sBl = sBh + SM::B_BYTES;
+        const uint32_t dbuf = tmem_d + (uint32_t)(tb * NP);
+#pragma unroll
+        for (int kk = 0; kk < TC_KT / 8; ++kk) {
+          const uint32_t koff = kk * 32;
+          const uint64_t dAh = sw128_desc(sAh + koff);
+          const uint64_t dAl = sw128_desc(sAl + koff);
+          mma_tf32(dbuf, dAh, sw128_desc(sBh + koff), idesc, kk > 0 ? 1u : 0u);
+          mma_tf32(dbuf, dAh, sw128_desc(sBl + koff), idesc, 1u);
+          mma_tf32(dbuf, dAl, sw128_desc(sBh + koff), idesc, 1u);
+        }
+        mma_commit(&mma_done[tb]);
+        mma_commit(&op_empty[ob]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---- drain: TMEM lane quarter warp % 4, all NP columns of the row
+    const int dq = warp & 3, row = dq * 32 + lane;
+    float acc[NP];
+#pragma unroll
+    for (int j = 0; j < NP; ++j) acc[j] = 0.f;
+    int td = blockIdx.x, ktd = 0, nkd = (td < ntiles) ? geo(td).nk : 0;
+    for (int s = 0; s < nsteps; ++s) {
+      const int tb = s % TC2_NTM;
+      mbar_wait(&mma_done[tb], (s / TC2_NTM) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+      for (int j0 = 0; j0 < NP; j0 += 8) {
+        uint32_t v[8];
+        const uint32_t taddr = tmem_d + ((uint32_t)(dq * 32) << 16) + (uint32_t)(tb * NP + j0);
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                     : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[j0 + q] = __fadd_rn(acc[j0 + q], __uint_as_float(v[q]));
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tm_empty[tb]);
+      if (++ktd >= nkd) {
+        const TileG G = geo(td);
+        if (row < G.rows) {
+          if (!TRANS) {
+            float* o = out + (int64_t)G.tl.split * G.p.pstride + G.p.poff;
+#pragma unroll
+            for (int j = 0; j < NP; ++j)
+              if (j < G.p.r) o[(int64_t)j * G.p.m + G.tl.i0 + row] = acc[j];
+          } else {
+            float* o = out + (int64_t)G.tl.split * G.p.qstride + G.p.qoff;
+#pragma unroll
+            for (int j = 0; j < NP; ++j)
+              if (j < G.p.r) o[(int64_t)j * G.p.k + G.tl.c0 + row] = acc[j];
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < NP; ++j) acc[j] = 0.f;
+        ktd = 0;
+        td += gridDim.x;
+        nkd = (td < ntiles) ? geo(td).nk : 0;
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == WM)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_d), "r"(TMEM_COLS));
+}
+
 template <int NP, bool TRANS>
 static cudaError_t tc_launch(const PsArgs& a, const PTile* tiles, int ntiles, const float* B, float* out,
                              cudaStream_t st) {
-  const int smem = TcSmem<NP, TRANS>::TOTAL;
-  cudaError_t e = memo_smem_attr((const void*)k_ps_tc<NP, TRANS>, smem);
-  if (e != cudaSuccess) return e;
   int nsm = 0, dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   if (nsm <= 0) nsm = 148;
+  if (!getenv("LGRECO_PS_TC1")) {  // the warp-specialised kernel (LGRECO_PS_TC1=1: the lock-step one, A/B)
+    const int smem = Tc2Smem<NP>::TOTAL;
+    cudaError_t e = memo_smem_attr((const void*)k_ps_tc2<NP, TRANS>, smem);
+    if (e != cudaSuccess) return e;
+    k_ps_tc2<NP, TRANS><<<std::min(ntiles, nsm), TC2_THREADS, smem, st>>>(a.g, a.e, a.pl, tiles, ntiles, B, out);
+    return cudaGetLastError();
+  }
+  const int smem = TcSmem<NP, TRANS>::TOTAL;
+  cudaError_t e = memo_smem_attr((const void*)k_ps_tc<NP, TRANS>, smem);
+  if (e != cudaSuccess) return e;
   k_ps_tc<NP, TRANS><<<std::min(ntiles, nsm), TC_THREADS, smem, st>>>(a.g, a.e, a.pl, tiles, ntiles, B, out);
   return cudaGetLastError();
 }
