@@ -17,6 +17,12 @@ struct Psgd {
   lg::PTile* d_et_prof = nullptr;
   int n_prof = 0, nrt_prof = 0, nct_prof = 0, rmax_prof = 0, nrt128_prof = 0, nct128_prof = 0, net_prof = 0;
   int mmax_prof = 0, mmax_c = 0;
+  // TMA maps of the tensor-core GEMMs (psgd_tc.cu): host layer lists, config versions,
+  // device areas [prof MQ, prof M^T P, compress MQ, compress M^T P] and their caches
+  std::vector<lg::PLayer> hpl_prof, hpl_c;
+  uint64_t ver_c = 1;
+  void* maps[4] = {nullptr, nullptr, nullptr, nullptr};
+  lg::TcMapCache mcache[4];
   int32_t* d_et0_prof = nullptr;
   lg::PTile *d_gcp_prof = nullptr, *d_gcq_prof = nullptr;  // Gram row chunks (P-shaped / Q-shaped)
   int32_t *d_gcp0_prof = nullptr, *d_gcq0_prof = nullptr;
@@ -164,6 +170,7 @@ int psgd_init(lgreco_ctx* c, cudaStream_t st) {
   GramChunks gcs;
   ps_config(c, p->rprof, pl, rt, ct, et0, p->rmax_prof, rt128, ct128, et, gcs);
   for (const auto& x : pl) p->mmax_prof = std::max(p->mmax_prof, (int)x.m);
+  p->hpl_prof = pl;
   p->ngcp_prof = (int)gcs.p.size();
   p->ngcq_prof = (int)gcs.q.size();
   p->n_prof = (int)pl.size(); p->nrt_prof = (int)rt.size(); p->nct_prof = (int)ct.size();
@@ -224,6 +231,7 @@ int psgd_init(lgreco_ctx* c, cudaStream_t st) {
   PS_ALLOC(p->GQ, sizeof(double) * p->Gsz);
   PS_ALLOC(p->dpart, sizeof(double) * 65 * std::max<size_t>(1, et.size()));
   PS_ALLOC(p->eflag, sizeof(int32_t) * std::max(1, p->nM));
+  for (int q = 0; q < 4; ++q) PS_ALLOC(p->maps[q], (size_t)128 * 3 * std::max(1, p->nM));  // CUtensorMap = 128 B
   PS_ALLOC(p->d_gcp_prof, sizeof(lg::PTile) * std::max<size_t>(1, gcs.p.size()));
   PS_ALLOC(p->d_gcq_prof, sizeof(lg::PTile) * std::max<size_t>(1, gcs.q.size()));
   PS_ALLOC(p->d_gcp0_prof, sizeof(int32_t) * gcs.p0.size());
@@ -272,6 +280,7 @@ void psgd_destroy(lgreco_ctx* c) {
   cudaFree(p->gpart); cudaFree(p->GP); cudaFree(p->GQ); cudaFree(p->dpart); cudaFree(p->eflag);
   cudaFree(p->d_gcp_prof); cudaFree(p->d_gcq_prof); cudaFree(p->d_gcp0_prof); cudaFree(p->d_gcq0_prof);
   cudaFree(p->d_gcp_c); cudaFree(p->d_gcp0_c);
+  for (int q = 0; q < 4; ++q) cudaFree(p->maps[q]);
   if (p->h_stage) cudaFreeHost(p->h_stage);
   if (p->evt) cudaEventDestroy(p->evt);
   delete p;
@@ -287,6 +296,8 @@ static lg::PsArgs ps_args_prof(lgreco_ctx* c, const float* g, const float* e) {
   a.gcq = p->d_gcq_prof; a.n_gcq = p->ngcq_prof; a.gcq0 = p->d_gcq0_prof;
   a.gpart = p->gpart;
   a.mmax = p->mmax_prof;
+  a.h_pl = p->hpl_prof.data(); a.cfg_ver = 0;
+  a.maps_mq = p->maps[0]; a.maps_tr = p->maps[1]; a.mc_mq = &p->mcache[0]; a.mc_tr = &p->mcache[1];
   return a;
 }
 static lg::PsArgs ps_args_c(lgreco_ctx* c, const float* g, const float* e) {
@@ -296,6 +307,8 @@ static lg::PsArgs ps_args_c(lgreco_ctx* c, const float* g, const float* e) {
   a.gcp = p->d_gcp_c; a.n_gcp = p->ngcp_c; a.gcp0 = p->d_gcp0_c;
   a.gpart = p->gpart;
   a.mmax = p->mmax_c;
+  a.h_pl = p->hpl_c.data(); a.cfg_ver = p->ver_c;
+  a.maps_mq = p->maps[2]; a.maps_tr = p->maps[3]; a.mc_mq = &p->mcache[2]; a.mc_tr = &p->mcache[3];
   return a;
 }
 
@@ -412,6 +425,8 @@ static int psgd_set_plan(lgreco_ctx* c, const int32_t* choice, cudaStream_t st) 
   p->nrt128_c = (int)rt128.size(); p->nct128_c = (int)ct128.size(); p->net_c = (int)et.size();
   p->ngcp_c = (int)gcs.p.size();
   p->mmax_c = mmax;
+  p->hpl_c = pl;
+  ++p->ver_c;
   p->nraw = (int)segs.size();
   p->Sraw = off;
   p->need_init = any_init;

@@ -138,6 +138,7 @@ struct PLayer {        // one compressed matrix layer in a grouped launch
 // tile of a grouped launch: MQ tensor-core tile (rows i0.., K columns [c0, i1), split);
 // MtP tile (columns c0.., rows [i0, i1), split); row tile (i0); element tile (i0, c0)
 struct PTile { int32_t ci, split, i0, i1, c0, pad; };
+struct TcMapCache { uint64_t ver = ~0ull; const void* g = nullptr; const void* e = nullptr; const void* b = nullptr; };
 struct RawSeg { int64_t off, n, pay_off; };            // raw (uncompressed) segment of the gradient
 struct PsArgs {
   const float* g; const float* e; const PLayer* pl; int nC;
@@ -150,6 +151,11 @@ struct PsArgs {
   const PTile* gcq = nullptr; int n_gcq = 0; const int32_t* gcq0 = nullptr;
   double* gpart = nullptr;
   int mmax = 0;  // the largest m of the config (the fused small-layer CholQR2 when it fits)
+  // TMA tensor maps of the tensor-core GEMMs (psgd_tc.cu): the config's host layer list,
+  // its version, a device area of 3 maps (g, e, B) per layer for each GEMM flavour and the
+  // host cache of what the area currently encodes (nullptr: no TMA, 4-byte copies)
+  const PLayer* h_pl = nullptr; uint64_t cfg_ver = 0;
+  void* maps_mq = nullptr; void* maps_tr = nullptr; TcMapCache* mc_mq = nullptr; TcMapCache* mc_tr = nullptr;
 };
 // profile-error work buffers: d / ||M||^2 partials [etiles][RMAX+1], G_P, G_Q (per layer
 // r x r at goff), the per-layer fallback flag
