@@ -37,6 +37,10 @@ D_BINS = 10000
 # ceil, min s, fma dec, x - dec, fma d^2) x 7 candidates = 49; per element 21 (g + e,
 # x - mn, 2 min/max, Philox4x32-10 15 per element, u word shift + convert 2)
 K1_OPS_PER_ELEM = 70
+FUSED_EXTRA_OPS = 5  # the planned candidate's compress in the fused pass: t*inv - u, ceil, min s, dec, x - dec
+PIPE_NOTE = ("pipelined (PAPER.md:312-314, re-solved every step): step t = the fused profile + compress pass "
+             "(lgreco_profile_compress) with the plan solved from the profile of step t-2, beside the solve of "
+             "step t-1 (LGRECO_PC_CONCURRENT); value = gradient bytes / (K steps' time / K)")
 SEED = 0x5EED
 
 
@@ -232,10 +236,83 @@ def run_ours(args):
         ctx.compress_allreduce_dev(choice_d, gin, ef, gout, s)
         if marks: marks[-1].record(stream)
 
+    # ---- the pipelined schedule (the plan in force compresses the step,
+    # the step's profile feeds the next solve), re-solved EVERY step: step t runs the fused
+    # profile + compress pass (lgreco_profile_compress: one read of g and e) with the plan
+    # solved from the profile of step t - 2, and the solve of step t - 1 runs beside it on
+    # the SMs the fused kernel leaves free (LGRECO_PC_CONCURRENT).  Three plan buffers:
+    # step t reads plans[t % 3], the solve of step t writes plans[(t + 2) % 3].
+    plans = [dflt.clone() for _ in range(3)]
+
+    def step_pipe(s, gin=None, gout=None, conc=True, marks=None, pre_solve=None):
+        gin = g if gin is None else gin
+        gout = out if gout is None else gout
+        staged = marks is not None and len(marks) == 3
+        if marks: marks[0].record(stream)
+        ctx.profile_compress(plans[s % 3], gin, ef, gout, s, err, bits, concurrent=conc)
+        if staged: marks[1].record(stream)
+        if pre_solve: pre_solve()
+        lgreco.solve(err, bits, dflt, comp, D=D_BINS, choice=plans[(s + 2) % 3], info=info_d, workspace=ws)
+        ctx.plan_broadcast(plans[(s + 2) % 3])
+        if marks: marks[-1].record(stream)
+
+    pipelined = args.schedule == "pipelined"
+    conc = world == 1  # (W > 1: profile + compress are two calls inside the library; no overlap)
     for s in range(args.warmup):
         step(s)
+    if pipelined:
+        for s in range(args.warmup):
+            step_pipe(s, conc=conc and s > 0)
     torch.cuda.synchronize()
     ctx.check()
+    pipe = None
+    if pipelined:
+        # headline of the pipelined schedule: K consecutive steps between two events (no
+        # L2 flush between them: it would serialise the overlap; each step streams 204 MB
+        # in and 204 MB out, > the 126 MB L2)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        p0, p1 = ev(), ev()
+        base = args.warmup
+        launches_p0 = ctx.launches()
+        p0.record(stream)
+        for s in range(args.steps):
+            step_pipe(base + s, conc=conc)
+        p1.record(stream)
+        torch.cuda.synchronize()
+        pipe_ms = p0.elapsed_time(p1) / args.steps
+        pipe_launches = ctx.launches() - launches_p0 + args.steps
+        # stage pass of the pipelined step (serial, events between): fused pass, solve
+        pt = {"profile_compress": [], "solve": []}
+        ctx.timing(True)
+        ctx.kernel_ms()
+        allm = []
+        for s in range(args.steps):
+            l2_flush.zero_()
+            m = [ev() for _ in range(3)]
+            step_pipe(base + args.steps + s, conc=False, marks=m)
+            allm.append(m)
+        torch.cuda.synchronize()
+        for m in allm:
+            pt["profile_compress"].append(m[0].elapsed_time(m[1]))
+            pt["solve"].append(m[1].elapsed_time(m[2]))
+        fk_total, fk_n = ctx.kernel_ms()
+        ctx.timing(False)
+        if world > 1:
+            t = torch.tensor([pipe_ms, sum(pt["profile_compress"]) / args.steps, sum(pt["solve"]) / args.steps],
+                             device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            pipe_ms = float(t[0])
+            pt = {"profile_compress": [float(t[1])], "solve": [float(t[2])]}
+        pipe = {"ms": pipe_ms, "launches": pipe_launches,
+                "stage": {k: sum(v) / len(v) for k, v in pt.items()},
+                "fused_ms": fk_total / max(1, fk_n), "fused_n": fk_n}
+        ctx.check()
+        ef.copy_(e0)
+        for pl in plans:
+            pl.copy_(dflt)
+        torch.cuda.synchronize()
 
     clocks = ClockSampler(local)
     times = {"step": [], "profile": [], "solve": [], "compress_allreduce": []}
@@ -343,22 +420,50 @@ def run_ours(args):
     ev_d2h = [torch.cuda.Event() for _ in range(n_e2e)]
     t_first, t_last = ev(), ev()
     t_first.record(s_h2d)
-    for s in range(n_e2e):
-        b = s & 1
+
+    def h2d(s):
         with torch.cuda.stream(s_h2d):
             if s >= 2:
-                s_h2d.wait_event(ev_comp[s - 2])  # g_dev[b] consumed by step s-2
-            g_dev[b].copy_(g_host, non_blocking=True)
+                s_h2d.wait_event(ev_comp[s - 2])  # g_dev[s & 1] consumed by step s-2
+            g_dev[s & 1].copy_(g_host, non_blocking=True)
             ev_h2d[s].record(s_h2d)
-        stream.wait_event(ev_h2d[s])
-        if s >= 2:
-            stream.wait_event(ev_d2h[s - 2])  # o_dev[b] drained by step s-2's D2H
-        step(s, gin=g_dev[b], gout=o_dev[b])
-        ev_comp[s].record(stream)
+
+    def d2h(s):
         with torch.cuda.stream(s_d2h):
             s_d2h.wait_event(ev_comp[s])
-            out_host[b].copy_(o_dev[b], non_blocking=True)
+            out_host[s & 1].copy_(o_dev[s & 1], non_blocking=True)
             ev_d2h[s].record(s_d2h)
+
+    if pipelined:
+        for pl in plans:
+            pl.copy_(dflt)
+        h2d(0)
+        stream.wait_event(ev_h2d[0])
+        for s in range(n_e2e):
+            b = s & 1
+            if s + 1 < n_e2e:
+                h2d(s + 1)
+
+            def waits(s=s):  # step s+1's inputs, enqueued before the solve of step s so the
+                # fused pass of step s+1 follows that solve directly (the overlap)
+                if s + 1 < n_e2e:
+                    stream.wait_event(ev_h2d[s + 1])
+                    if s >= 1:
+                        stream.wait_event(ev_d2h[s - 1])  # o_dev[(s+1) & 1] drained
+
+            step_pipe(s, gin=g_dev[b], gout=o_dev[b], conc=conc and s > 0,
+                      pre_solve=lambda s=s: (ev_comp[s].record(stream), waits()))
+            d2h(s)
+    else:
+        for s in range(n_e2e):
+            b = s & 1
+            h2d(s)
+            stream.wait_event(ev_h2d[s])
+            if s >= 2:
+                stream.wait_event(ev_d2h[s - 2])  # o_dev[b] drained by step s-2's D2H
+            step(s, gin=g_dev[b], gout=o_dev[b])
+            ev_comp[s].record(stream)
+            d2h(s)
     t_last.record(s_d2h)
     torch.cuda.synchronize()
     e2e = t_first.elapsed_time(t_last) / n_e2e
@@ -369,7 +474,8 @@ def run_ours(args):
 
     if rank == 0:
         peaks, src = _peaks()
-        gbs = world * 4.0 * N / (ms * 1e-3) / 1e9
+        same_gbs = world * 4.0 * N / (ms * 1e-3) / 1e9
+        gbs = world * 4.0 * N / (pipe["ms"] * 1e-3) / 1e9 if pipe else same_gbs
         # dominant kernel: K1 qprofile (ncu launch-list share ~0.4 of the library's device
         # time).  It is bound by instruction issue, not HBM:
         # algorithmic lane-ops = K1_OPS_PER_ELEM per compressed element; peak = one
@@ -382,34 +488,71 @@ def run_ours(args):
         alu_peak = nsm * 128 * sm_mhz * 1e6 / 1e12  # T lane-ops/s
         k1_tops = k1_ops / (k1_ms * 1e-3) / 1e12
         traffic = _ncu_traffic()
+        roof_k1 = {"bound": "alu", "kernel": "k_qprofile_q (K1)", "achieved": round(k1_tops, 3),
+                   "peak": round(alu_peak, 3), "unit": "T lane-op/s", "frac": round(k1_tops / alu_peak, 4),
+                   "traffic": traffic, "peak_source": f"derived: {nsm} SMs x 4 SMSP x 32 lanes x {sm_mhz:.0f} MHz",
+                   "kernel_ms": round(k1_ms, 4), "launches_timed": k1_n,
+                   "algorithmic_ops_per_launch": k1_ops, "ops_per_element": K1_OPS_PER_ELEM,
+                   "algorithmic_bytes_per_launch": prof_bytes,
+                   "hbm_achieved_gbs": round(prof_bytes / (k1_ms * 1e-3) / 1e9, 1),
+                   "hbm_frac": round(prof_bytes / (k1_ms * 1e-3) / 1e9 / peaks["hbm_gbs"], 4),
+                   "hbm_peak_gbs": peaks["hbm_gbs"], "hbm_peak_source": src}
+        roof = roof_k1
+        if pipe:
+            # dominant kernel of the pipelined step: the fused pass (K1 + K5's compress).
+            # Algorithmic bytes: read g, e and write e', out = 16 B per element (every layer);
+            # algorithmic lane-ops: K1's 70 + the planned candidate's 5 (t*inv - u, ceil,
+            # min s, dec, x - dec) per compressed element.  Both fractions are reported;
+            # `bound` names the higher one.
+            fms = pipe["fused_ms"]
+            fbytes = 16.0 * N
+            fops = (K1_OPS_PER_ELEM + FUSED_EXTRA_OPS) * ncomp
+            hbm_gbs = fbytes / (fms * 1e-3) / 1e9
+            alu_t = fops / (fms * 1e-3) / 1e12
+            fr_h, fr_a = hbm_gbs / peaks["hbm_gbs"], alu_t / alu_peak
+            ftraffic = _ncu_traffic("fused_dram_bytes.json")
+            common = {"kernel": "k_qprofile_q<7, fused> (K1 + K5 compress)", "kernel_ms": round(fms, 4),
+                      "launches_timed": pipe["fused_n"], "traffic": ftraffic,
+                      "algorithmic_bytes_per_launch": fbytes, "algorithmic_ops_per_launch": fops,
+                      "ops_per_element": K1_OPS_PER_ELEM + FUSED_EXTRA_OPS}
+            if fr_h >= fr_a:
+                roof = {"bound": "hbm", "achieved": round(hbm_gbs, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                        "frac": round(fr_h, 4), "peak_source": src, **common,
+                        "alu_achieved": round(alu_t, 3), "alu_peak": round(alu_peak, 3), "alu_frac": round(fr_a, 4)}
+            else:
+                roof = {"bound": "alu", "achieved": round(alu_t, 3), "peak": round(alu_peak, 3),
+                        "unit": "T lane-op/s", "frac": round(fr_a, 4),
+                        "peak_source": f"derived: {nsm} SMs x 4 SMSP x 32 lanes x {sm_mhz:.0f} MHz", **common,
+                        "hbm_achieved_gbs": round(hbm_gbs, 1), "hbm_peak_gbs": peaks["hbm_gbs"],
+                        "hbm_frac": round(fr_h, 4)}
         line = {
             "metric": METRIC, "value": round(gbs, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": round(pipe["ms"] if pipe else ms, 4), "higher_is_better": True,
+            "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded Gaussian + 1% outliers, EF ~ N(0,(0.1s)^2))",
             "config": {"workload": WORKLOAD, "global_batch": None, "parallelism": f"dp{world}",
-                       "l2": "flushed (512 MiB memset) before every timed step", "family": "qsgd",
-                       "exchange": exchange},
-            "dp_solve_ms": round(stage["solve"], 4),
+                       "schedule": (PIPE_NOTE if pipe else "same-step: profile -> solve -> compress with this step's plan"),
+                       "l2": ("not flushed between the K consecutive steps: each streams 204 MB in and 204 MB out "
+                              "(> 126 MB L2)" if pipe else "flushed (512 MiB memset) before every timed step"),
+                       "family": "qsgd", "exchange": exchange},
+            "dp_solve_ms": round(pipe["stage"]["solve"] if pipe else stage["solve"], 4),
             # the same figure for the per-step path alone (compress + exchange
             # with the plan fixed), which is what runs between replans
             "plan_fixed_gbs": round(world * 4.0 * N / (stage["compress_allreduce"] * 1e-3) / 1e9, 2),
             "stage_ms": {k: round(v, 4) for k, v in stage.items()},
             "stage_note": "step: headline pass (events at step begin/end only); profile/solve/compress: a second "
                           "pass of K steps with events between the stages and around K1",
-            "roofline": {"bound": "alu", "kernel": "k_qprofile_q (K1)", "achieved": round(k1_tops, 3),
-                         "peak": round(alu_peak, 3), "unit": "T lane-op/s", "frac": round(k1_tops / alu_peak, 4),
-                         "traffic": traffic, "peak_source": f"derived: {nsm} SMs x 4 SMSP x 32 lanes x {sm_mhz:.0f} MHz",
-                         "kernel_ms": round(k1_ms, 4), "launches_timed": k1_n,
-                         "algorithmic_ops_per_launch": k1_ops, "ops_per_element": K1_OPS_PER_ELEM,
-                         "algorithmic_bytes_per_launch": prof_bytes,
-                         "hbm_achieved_gbs": round(prof_bytes / (k1_ms * 1e-3) / 1e9, 1),
-                         "hbm_frac": round(prof_bytes / (k1_ms * 1e-3) / 1e9 / peaks["hbm_gbs"], 4),
-                         "hbm_peak_gbs": peaks["hbm_gbs"], "hbm_peak_source": src},
+            "roofline": roof,
+            "same_step": {"value": round(same_gbs, 3), "unit": "GB/s", "ms_per_step": round(ms, 4),
+                          "stage_ms": {k: round(v, 4) for k, v in stage.items()}, "roofline_k1": roof_k1,
+                          "l2": "flushed (512 MiB memset) before every timed step",
+                          "note": "profile -> solve -> compress with the plan of the same step (round-1 headline)"},
+            "pipelined_stage_ms": ({k: round(v, 4) for k, v in pipe["stage"].items()} if pipe else None),
             "e2e": {"value": round(world * 4.0 * N / (e2e * 1e-3) / 1e9, 3), "unit": "GB/s",
                     "h2d_bytes_per_step": 4 * N, "d2h_bytes_per_step": 4 * N, "ms_per_step": round(e2e, 4),
                     "steps": n_e2e, "overlap": "H2D(s+1) and D2H(s-1) on copy streams beside step s's kernels",
                     "l2": "not flushed: per-step working set 307 MB > 126 MB L2"},
-            "gpu_launches": int(launches),
+            "gpu_launches": int(pipe["launches"] if pipe else launches),
             "exchange": xch,
             "clocks": clk,
             "wall_s": round(wall, 3),
@@ -559,9 +702,9 @@ def _extra_pack_decode(dev, rank, stream, l2_flush):
             "decode_hbm_frac": round(bup / (up * 1e-3) / 1e9 / peaks["hbm_gbs"], 4), "steps": 5}
 
 
-def _ncu_traffic():
-    """dram bytes per launch of K1 from the committed ncu capture, if present."""
-    p = os.path.join(ROOT, "profiles", "k1_dram_bytes.json")
+def _ncu_traffic(name="k1_dram_bytes.json"):
+    """dram bytes per launch of the dominant kernel from the committed ncu capture, if present."""
+    p = os.path.join(ROOT, "profiles", name)
     try:
         return json.load(open(p))["dram_bytes_per_launch"]
     except Exception:
@@ -662,6 +805,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--schedule", choices=["pipelined", "same_step"], default="pipelined",
+                    help="headline step: the paper's pipelined schedule (default) or same-step profile->solve->compress")
     ap.add_argument("--no-extras", action="store_true", help="skip the C2/C3/C5 secondary measurements")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":

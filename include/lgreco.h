@@ -222,6 +222,26 @@ int lgreco_compress_allreduce(lgreco_ctx* ctx, const int32_t* h_choice, const fl
 int lgreco_compress_allreduce_dev(lgreco_ctx* ctx, const int32_t* d_choice, const float* d_g, float* d_ef,
                                   float* d_out, uint64_t step, void* stream);
 
+/* (a2 + a8, fused) The per-step pass of the paper's schedule (the
+ * plan in force -- chosen by a preceding solve -- compresses the step, while the profile
+ * of the same step feeds the next solve).  Defined as, and bit-identical to,
+ *   lgreco_profile(ctx, d_g, d_ef, step, d_err, d_bits, stream);
+ *   lgreco_compress_allreduce_dev(ctx, d_choice, d_g, d_ef, d_out, step, stream);
+ * i.e. d_err / d_bits profile x = d_g + d_ef (the EF as it was on entry) and d_choice
+ * (DEVICE, L) compresses the same x (d_ef <- x - decompress(x), d_out <- the mean).  For a
+ * QSGD ctx with world == 1 and B = 128 this is ONE pass over d_g and d_ef (kernel K1 with
+ * the compress of K5 fused: the planned candidate's code comes from the same registers
+ * and Philox uniforms, then K1b), otherwise the two calls.  d_choice must not alias the
+ * output of a solve that reads d_err.  flags: LGRECO_PC_CONCURRENT -- the caller asserts
+ * that the kernel enqueued immediately before this call on `stream` (typically the
+ * lgreco_solve of the previous step, writing a plan other than d_choice) produces nothing
+ * this call reads; the fused kernel may then run beside it on the SMs it leaves free, and
+ * the profile's reduction waits for both.  d_g, d_ef, d_out 16-byte aligned (EINVAL
+ * otherwise); d_err L*K doubles, d_bits L*K int64. */
+#define LGRECO_PC_CONCURRENT 1u
+int lgreco_profile_compress(lgreco_ctx* ctx, const int32_t* d_choice, const float* d_g, float* d_ef, float* d_out,
+                            uint64_t step, double* d_err, int64_t* d_bits, uint32_t flags, void* stream);
+
 /* ---- NEXT-4: mixed-family plans ("combining different compression
  * techniques inside the same model") ------------------------------------------------
  * A hybrid plan picks, per layer, a (family, parameter) column of a table that holds F

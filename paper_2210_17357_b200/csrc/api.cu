@@ -121,6 +121,7 @@ extern "C" {
 int lgreco_ctx_create(lgreco_ctx** out, const lgreco_layer* layers, int32_t L, const lgreco_candidates* cand,
                       int32_t rank, int32_t world, const void* nccl_unique_id, void* stream) {
   if (!out || !layers || L <= 0 || !cand || !cand->params) { lg_set_error("null argument or L <= 0"); return LGRECO_EINVAL; }
+  if (L >= lg::QI_MAX_LAYERS) { lg_set_error("L = %d: at most %d layers", L, lg::QI_MAX_LAYERS - 1); return LGRECO_EINVAL; }
   if (world < 1 || rank < 0 || rank >= world) { lg_set_error("bad rank/world %d/%d", rank, world); return LGRECO_EINVAL; }
   if (cand->K <= 0 || cand->K > 255) { lg_set_error("K=%d out of range", cand->K); return LGRECO_EINVAL; }
   if (cand->family != LGRECO_QSGD && cand->family != LGRECO_TOPK && cand->family != LGRECO_POWERSGD) {
@@ -160,7 +161,7 @@ int lgreco_ctx_create(lgreco_ctx** out, const lgreco_layer* layers, int32_t L, c
   c->N = end;
   c->bucket0.resize(L + 1);
   std::vector<lg::DevLayer> dl(L);
-  std::vector<lg::ProfChunk> chunks, chunks_all;
+  std::vector<lg::ProfChunk> chunks, chunks_all, chunks_raw;
   std::vector<int32_t> lc0(L + 1);
   const int CB = 64;  // buckets per profile chunk
   int64_t gb = 0;
@@ -172,6 +173,7 @@ int lgreco_ctx_create(lgreco_ctx** out, const lgreco_layer* layers, int32_t L, c
     for (int64_t j = 0; j < nb; j += CB) {
       const lg::ProfChunk ch{l, (int32_t)std::min<int64_t>(CB, nb - j), j};
       if (layers[l].compress) chunks.push_back(ch);
+      else chunks_raw.push_back(ch);
       chunks_all.push_back(ch);
     }
     gb += nb;
@@ -181,6 +183,7 @@ int lgreco_ctx_create(lgreco_ctx** out, const lgreco_layer* layers, int32_t L, c
   c->R = gb;
   c->nchunks = (int)chunks.size();
   c->nchunks_all = (int)chunks_all.size();
+  c->nchunks_raw = (int)chunks_raw.size();
   // K1 (B = 128): chunks of <= 4 buckets (one quad) of the compressed layers, handed
   // out to the resident warps (occupancy x SMs CTAs of 8 warps) by a ticket counter: the
   // fine grain keeps every warp busy to the end (a quad is ~1/14 of a warp's share)
@@ -195,7 +198,7 @@ int lgreco_ctx_create(lgreco_ctx** out, const lgreco_layer* layers, int32_t L, c
       const int64_t nb = (layers[l].numel + 127) / 128;
       for (int64_t j = 0; j < nb; j += 4)
         qchunks.push_back(lg::QInfo{layers[l].offset + 128 * j, (uint32_t)(c->bucket0[l] + j),
-                                    (int32_t)std::min<int64_t>(512, layers[l].numel - 128 * j)});
+                                    (int32_t)std::min<int64_t>(512, layers[l].numel - 128 * j) | (l << 10)});
     }
     lqc0[L] = (int32_t)qchunks.size();
     for (int l = 0; l < L; ++l) {
@@ -233,6 +236,7 @@ int lgreco_ctx_create(lgreco_ctx** out, const lgreco_layer* layers, int32_t L, c
   LG_ALLOC(c->d_chunks, sizeof(lg::ProfChunk) * std::max(1, c->nchunks));
   LG_ALLOC(c->d_chunks_all, sizeof(lg::ProfChunk) * std::max(1, c->nchunks_all));
   LG_ALLOC(c->d_layer_chunk0, sizeof(int32_t) * (L + 1));
+  LG_ALLOC(c->d_chunks_raw, sizeof(lg::ProfChunk) * std::max(1, c->nchunks_raw));
   LG_ALLOC(c->d_partial, sizeof(double) * (size_t)std::max(1, std::max(c->nchunks, c->nqchunks)) * c->K);
   LG_ALLOC(c->d_qinfo, sizeof(lg::QInfo) * std::max(1, c->nqchunks));
   LG_ALLOC(c->d_layer_qchunk0, sizeof(int32_t) * (L + 1));
@@ -263,6 +267,9 @@ int lgreco_ctx_create(lgreco_ctx** out, const lgreco_layer* layers, int32_t L, c
     e = cudaMemcpyAsync(c->d_chunks_all, chunks_all.data(), sizeof(lg::ProfChunk) * c->nchunks_all,
                         cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = cudaMemcpyAsync(c->d_layer_chunk0, lc0.data(), sizeof(int32_t) * (L + 1), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess && c->nchunks_raw)
+    e = cudaMemcpyAsync(c->d_chunks_raw, chunks_raw.data(), sizeof(lg::ProfChunk) * c->nchunks_raw,
+                        cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess && c->nqchunks)
     e = cudaMemcpyAsync(c->d_qinfo, qchunks.data(), sizeof(lg::QInfo) * c->nqchunks, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = cudaMemcpyAsync(c->d_layer_qchunk0, lqc0.data(), sizeof(int32_t) * (L + 1), cudaMemcpyHostToDevice, st);
@@ -324,7 +331,7 @@ void lgreco_ctx_destroy(lgreco_ctx* c) {
   psgd_destroy(c);
   if (c->comm) ncclCommDestroy(c->comm);
   cudaFree(c->d_layers); cudaFree(c->d_bucket0); cudaFree(c->d_cand_s); cudaFree(c->d_params);
-  cudaFree(c->d_chunks); cudaFree(c->d_chunks_all); cudaFree(c->d_layer_chunk0); cudaFree(c->d_partial);
+  cudaFree(c->d_chunks); cudaFree(c->d_chunks_all); cudaFree(c->d_chunks_raw); cudaFree(c->d_layer_chunk0); cudaFree(c->d_partial);
   cudaFree(c->d_qinfo); cudaFree(c->d_layer_qchunk0); cudaFree(c->d_ticket);
   cudaFree(c->d_qseg); cudaFree(c->d_lqseg0); cudaFree(c->d_segsum); cudaFree(c->d_ldone); cudaFree(c->d_flag);
   cudaFree(c->d_plan); cudaFree(c->d_pay1); cudaFree(c->d_recv); cudaFree(c->d_pay2);
@@ -722,6 +729,49 @@ int lgreco_compress_allreduce_dev(lgreco_ctx* c, const int32_t* d_choice, const 
   LG_CUDA(cudaMemcpyAsync(c->h_choice_pinned, d_choice, sizeof(int32_t) * c->L, cudaMemcpyDeviceToHost, st));
   LG_CUDA(cudaStreamSynchronize(st));
   return lgreco_compress_allreduce(c, c->h_choice_pinned, d_g, d_ef, d_out, step, stream);
+}
+
+// Fused per-step pass (the plan in force compresses the step, the
+// profile of the same x feeds the next solve): K1 profiles x = g + e for every candidate
+// and, from the same registers and uniforms, quantises x with the planned candidate
+// (K5's arithmetic: out, e'), one read of g and e.  Any other configuration runs the two
+// calls it is defined as.
+int lgreco_profile_compress(lgreco_ctx* c, const int32_t* d_choice, const float* d_g, float* d_ef, float* d_out,
+                            uint64_t step, double* d_err, int64_t* d_bits, uint32_t flags, void* stream) {
+  if (!c || !d_choice || !d_g || !d_out || !d_err || !d_bits) { lg_set_error("null argument"); return LGRECO_EINVAL; }
+  if (flags & ~(uint32_t)LGRECO_PC_CONCURRENT) { lg_set_error("profile_compress: unknown flags 0x%x", flags); return LGRECO_EINVAL; }
+  LG_TRY(check_align16("profile_compress", d_g, d_ef, d_out));
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool fused = c->family == LGRECO_QSGD && c->world == 1 && c->B == 128 && c->nqchunks > 0;
+  if (!fused) {
+    LG_TRY(lgreco_profile(c, d_g, d_ef, step, d_err, d_bits, stream));
+    return lgreco_compress_allreduce_dev(c, d_choice, d_g, d_ef, d_out, step, stream);
+  }
+  uint32_t k0, k1;
+  key_of(c, k0, k1);
+  lg::QProfileArgs a{d_g, d_ef, c->d_layers, c->L, c->d_chunks, c->nchunks, c->d_layer_chunk0,
+                     c->B, c->cs, c->d_params, c->K, k0, k1, (uint32_t)c->rank, (uint32_t)step,
+                     c->d_partial, d_err, d_bits};
+  a.qinfo = c->d_qinfo; a.nqchunks = c->nqchunks; a.layer_qchunk0 = c->d_layer_qchunk0;
+  a.nqwarps = c->nqwarps; a.ticket = c->d_ticket;
+  a.segs = c->d_qseg; a.nseg = c->nqseg; a.lseg0 = c->d_lqseg0; a.segsum = c->d_segsum; a.ldone = c->d_ldone;
+  a.ptr_aligned = 1;  // (checked above)
+  const bool conc = (flags & LGRECO_PC_CONCURRENT) != 0;
+  lg::QFuse fz{d_ef, d_out, d_choice, c->d_flag, c->d_chunks_raw, c->nchunks_raw, c->d_layers, c->B, conc ? 1 : 0,
+                 c->L};
+  a.fuse = &fz;
+  a.reduce_pdl = conc ? 0 : 1;
+  if (c->timing) {
+    cudaEvent_t e0, e1;
+    LG_CUDA(cudaEventCreate(&e0));
+    LG_CUDA(cudaEventCreate(&e1));
+    c->tev.emplace_back(e0, e1);
+    a.ev0 = e0;
+    a.ev1 = e1;
+  }
+  LG_LAUNCH(c, lg::launch_qprofile(a, st));
+  c->launches += 2;
+  return LGRECO_OK;
 }
 
 int lgreco_topk_pack(lgreco_ctx* c, const int32_t* h_choice, const float* d_g, float* d_ef, uint8_t* d_payload,

@@ -111,6 +111,10 @@ __device__ __forceinline__ int find_layer(const int64_t* b0, int L, int64_t gb) 
 // touching anything the predecessor writes (griddepcontrol.wait returns once the
 // predecessor grid has completed and its memory is visible).
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Let the next PDL-launched kernel of the stream be scheduled now (on the SMs this grid
+// leaves free) instead of at this grid's completion; it still sees this grid's memory
+// only after its own pdl_wait().
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,

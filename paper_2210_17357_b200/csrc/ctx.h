@@ -53,6 +53,8 @@ struct lgreco_ctx {
   int nchunks = 0;
   lg::ProfChunk* d_chunks_all = nullptr;  // chunks of every layer (pack / unpack)
   int nchunks_all = 0;
+  lg::ProfChunk* d_chunks_raw = nullptr;  // chunks of the lossless layers (fused profile + compress)
+  int nchunks_raw = 0;
   lg::CandS cs{};
   int32_t* d_layer_chunk0 = nullptr;
   double* d_partial = nullptr;

@@ -980,6 +980,10 @@ k_solve_cl(const double* __restrict__ err, const int64_t* __restrict__ bits, int
 #endif
   LG_T(0);
   pdl_wait();  // the error / size tables of the profile
+  // the next kernel may be scheduled beside the solve now: a compress that reads this
+  // plan waits for it (pdl_wait), the concurrent fused pass of the next step reads an
+  // older plan (LGRECO_PC_CONCURRENT)
+  pdl_trigger();
   LG_T(10);
 
   // ---- prelude (every CTA, identical).  Latency-bound: a handful of block-wide steps,

@@ -17,11 +17,32 @@ struct CandS { float s[16]; };
 
 // K1 (B = 128) work unit: one quad (4 buckets of one layer): flat element offset of its
 // first element, global index of its first bucket (Philox counter base, mod 2^32),
-// number of valid elements (512 unless the layer ends inside the quad).
-struct QInfo { int64_t elem0; uint32_t gb0; int32_t nvalid; };
+// number of valid elements (512 unless the layer ends inside the quad) in bits 0-9 of
+// nv_layer and the quad's layer index in bits 10-31 (the fused profile + compress reads
+// the layer's plan entry).
+struct QInfo { int64_t elem0; uint32_t gb0; int32_t nv_layer; };
+__host__ __device__ __forceinline__ int qi_nvalid(const QInfo& q) { return q.nv_layer & 1023; }
+__host__ __device__ __forceinline__ int qi_layer(const QInfo& q) { return (int)((uint32_t)q.nv_layer >> 10); }
+constexpr int QI_MAX_LAYERS = 1 << 22;
 // K1b segment: <= 256 consecutive quad rows of one layer
 struct QSeg { int32_t layer, row0, nrows, pad; };
   // s_j = 2^{b_j} - 1, passed by value (constant bank)
+
+// Fused profile + compress (lgreco_profile_compress, W = 1): besides the profile's
+// partial rows, K1 quantises every quad with the layer's planned candidate and writes
+// the decoded output and the new EF (K5's arithmetic), and its first warps handle the
+// lossless layers' chunks (raw copy, EF zeroed).
+struct QFuse {
+  float* ef;                 // EF in / out (the profile's e)
+  float* out;                // decoded output
+  const int32_t* choice;     // plan: candidate per layer (LGRECO_CHOICE_SKIP: untouched)
+  unsigned* flag;            // bit 0 non-finite input, bit 1 choice outside [0, K)
+  const ProfChunk* raw; int nraw;  // chunks of the lossless layers
+  const DevLayer* layers; int B;
+  int nowait;                // 1: no griddepcontrol.wait (LGRECO_PC_CONCURRENT)
+  int L;                     // layers (the first QF_LCACHE plan entries are staged in shared memory)
+};
+constexpr int QF_LCACHE = 4096;
 
 struct QProfileArgs {
   const float* g; const float* e;
@@ -37,6 +58,8 @@ struct QProfileArgs {
   int nqwarps = 0; unsigned* ticket = nullptr; int ptr_aligned = 0;
   const QSeg* segs = nullptr; int nseg = 0; const int32_t* lseg0 = nullptr; double* segsum = nullptr;
   unsigned* ldone = nullptr;
+  const QFuse* fuse = nullptr;  // non-null: the fused profile + compress kernel
+  int reduce_pdl = 1;           // 0: K1b launched without PDL (waits for all prior stream work)
 };
 
 // Peer-memory exchange (W <= 8 ranks): device pointers to every rank's stage-1 receive

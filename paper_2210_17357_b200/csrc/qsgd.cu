@@ -221,10 +221,28 @@ __device__ __forceinline__ f2_t f2mul(f2_t a, f2_t b) {
 // (-dec) (= RN(x - dec)), one FFMA2 for the square: 3 issue slots per element and
 // candidate instead of 6, every result bit-identical to the scalar form.  The SSE is kept as two fp32 partial sums
 // (even / odd elements) per candidate, added at the end.
-template <int KT, bool SCALED>
+__device__ __forceinline__ f2_t f2sub(f2_t a, f2_t b) {
+  f2_t r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
+// Fused profile + compress (QFuse): the lane's part of the planned candidate's
+// quantisation of its 16 elements -- K5's arithmetic (qcode, dec = fmaf(q, unit, mn),
+// e' = x - dec, x canonical), from the uniforms the profile draws anyway.
+struct FuseW {
+  float invc, unitc;  // the planned candidate's inv / unit of this bucket
+  int64_t ebase;      // flat index of the lane's element 0 (element 32i + s at ebase + 32i + s)
+  int lim;            // element offsets 32i + s < lim are valid
+  bool vec;           // 16-byte stores (regular quad)
+  bool wr;            // write at all (valid bucket, layer not skipped)
+};
+
+template <int KT, bool SCALED, bool FUSE = false>
 __device__ __forceinline__ void prof_cand16x2(const float* x, float mn, uint32_t c0, uint32_t rankfield, uint32_t step,
                                               const PhiloxRK& rk, const float* inv, const float* unit,
-                                              const CandS& cs, float S, float* acc) {
+                                              const CandS& cs, float S, float* acc, const FuseW& fw = FuseW{},
+                                              float* __restrict__ out = nullptr, float* __restrict__ ef = nullptr) {
   constexpr float MAGIC = 8388609.0f;  // 2^23 + 1
   constexpr float NEG_2M24 = -5.9604644775390625e-08f;
   f2_t a2[KT];
@@ -256,6 +274,28 @@ __device__ __forceinline__ void prof_cand16x2(const float* x, float mn, uint32_t
         f2_t d = f2add(xp[p], f2fma(f2pk(q0, q1), f2pk(-unit[j], -unit[j]), nmn));
         if (SCALED) d = f2mul(d, f2pk(S, S));
         a2[j] = f2fma(d, d, a2[j]);
+      }
+    }
+    if constexpr (FUSE) {
+      if (fw.wr) {
+        float dv[4], ev[4];
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+          float w0, w1;
+          f2up(f2fma_rp(tp[p], f2pk(fw.invc, fw.invc), nu[p]), w0, w1);
+          const f2_t dec = f2fma(f2pk(ceilf(w0), ceilf(w1)), f2pk(fw.unitc, fw.unitc), f2pk(mn, mn));
+          f2up(dec, dv[2 * p], dv[2 * p + 1]);
+          f2up(f2sub(xp[p], dec), ev[2 * p], ev[2 * p + 1]);
+        }
+        const int64_t o = fw.ebase + 32 * i;
+        if (fw.vec) {
+          *reinterpret_cast<float4*>(out + o) = make_float4(dv[0], dv[1], dv[2], dv[3]);
+          *reinterpret_cast<float4*>(ef + o) = make_float4(ev[0], ev[1], ev[2], ev[3]);
+        } else {
+#pragma unroll
+          for (int s2 = 0; s2 < 4; ++s2)
+            if (32 * i + s2 < fw.lim) { out[o + s2] = dv[s2]; ef[o + s2] = ev[s2]; }
+        }
       }
     }
   }
@@ -525,11 +565,14 @@ constexpr int QP_NPART = 16;  // K1 ticket counters (parts of the quad range), 2
 #define Q1_MINB 3   // resident CTAs per SM of the K1 fast kernel (register budget 65536 / (32 Q1_WARPS Q1_MINB))
 #endif
 constexpr int Q1_THREADS = 32 * Q1_WARPS;
-template <int KT>
-__global__ void __launch_bounds__(Q1_THREADS, Q1_MINB)
-k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const QInfo* __restrict__ qinfo, int nqc,
+#ifndef Q1F_MINB
+#define Q1F_MINB 3  // resident CTAs per SM of the fused profile + compress kernel
+#endif
+template <int KT, bool FUSE>
+__global__ void __launch_bounds__(Q1_THREADS, FUSE ? Q1F_MINB : Q1_MINB)
+k_qprofile_q(const float* __restrict__ g, const float* e, const QInfo* __restrict__ qinfo, int nqc,
              unsigned* __restrict__ ticket, const CandS cs, int K, const PhiloxRK rk, uint32_t rankfield,
-             uint32_t step, int ptr_aligned, double* __restrict__ partial) {
+             uint32_t step, int ptr_aligned, double* __restrict__ partial, const QFuse fz) {
   extern __shared__ __align__(128) unsigned char qsm[];
   __shared__ __align__(8) uint64_t bars[Q1_WARPS][2];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -589,9 +632,43 @@ k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const QIn
     if (lane == 0) asm volatile("cp.async.wait_group 1;" ::: "memory");
     __syncwarp();
   };
-  pdl_wait();  // g / e (and the ticket reset) of the preceding kernels
+  // g / e (and the ticket reset) of the preceding kernels; the fused kernel launched
+  // concurrently with a solve it does not read (LGRECO_PC_CONCURRENT) skips the wait
+  if (!(FUSE && fz.nowait)) pdl_wait();
+  float bad = 0.f;  // FUSE: NaN once a non-finite input was seen (K5's rule)
+  // FUSE: the plan staged in shared memory (int8; 127 = outside [-2, K): flagged below)
+  __shared__ int8_t s_ch[FUSE ? QF_LCACHE : 1];
+  if constexpr (FUSE) {
+    const int nc = min(fz.L, QF_LCACHE);
+    for (int i = threadIdx.x; i < nc; i += blockDim.x) {
+      const int v = __ldg(fz.choice + i);
+      s_ch[i] = (int8_t)((v >= LGRECO_CHOICE_SKIP && v < K) ? v : 127);
+    }
+    __syncthreads();
+  }
+  if constexpr (FUSE) {
+    // the lossless layers (few, small): x copied to the output, EF zeroed (K5's raw path)
+    for (int rc = gw; rc < fz.nraw; rc += gridDim.x * Q1_WARPS) {
+      const ProfChunk ch = fz.raw[rc];
+      if (__ldg(fz.choice + ch.layer) == LGRECO_CHOICE_SKIP) continue;
+      const DevLayer ly = fz.layers[ch.layer];
+      const int64_t i_beg = ch.first * (int64_t)fz.B;
+      const int64_t i_end = min(ly.numel, (ch.first + ch.nbk) * (int64_t)fz.B);
+      for (int64_t i = i_beg + lane; i < i_end; i += 32) {
+        const float xv = canon(__ldg(g + ly.offset + i), e ? e[ly.offset + i] : 0.f);
+        bad = __fadd_rn(bad, __fmul_rn(xv, 0.f));
+        fz.out[ly.offset + i] = xv;
+        if (fz.ef) fz.ef[ly.offset + i] = 0.f;
+      }
+    }
+  }
+  auto fin_flag = [&]() {
+    if constexpr (FUSE) {
+      if (!isfinite(bad)) atomicOr(fz.flag, 1u);
+    }
+  };
   int c = resolve(grab_issue());
-  if (c >= nqc) { finish(); return; }
+  if (c >= nqc) { fin_flag(); finish(); return; }
   if (lane == 0) {
     bar_init(&bars[warp][0], 1);
     bar_init(&bars[warp][1], 1);
@@ -610,7 +687,7 @@ k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const QIn
   }
   // bulk copies of quad `in` into stage b (lane 0) when regular: aligned, 4 full buckets
   auto issue = [&](const QInfo& in, int b) -> bool {
-    if (!(pal && (in.elem0 & 3) == 0 && in.nvalid == 512)) return false;
+    if (!(pal && (in.elem0 & 3) == 0 && qi_nvalid(in) == 512)) return false;
     if (lane == 0) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier generic reads of the stage
       bar_expect_tx_a(a_bar + 8 * b, tx);
@@ -651,7 +728,13 @@ k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const QIn
       // two stages: prefetch quad nA into the other stage now; one stage: after the
       // current quad has been read into registers (below)
       bool next_inflight = (Q1_STAGES == 2 && nA < nqc) ? issue(qis[warp][ra], b ^ 1) : false;
-      const bool valid = grp * 128 < ic.nvalid;
+      const int nvalid = qi_nvalid(ic);
+      const bool valid = grp * 128 < nvalid;
+      int jc = 0;  // FUSE: the layer's planned candidate
+      if constexpr (FUSE) {
+        const int lay = qi_layer(ic);
+        jc = lay < QF_LCACHE ? (int)s_ch[lay] : __ldg(fz.choice + lay);
+      }
       float x[16];
       if (cur_regular) {
         bar_wait_a(a_bar + 8 * b, (phase >> b) & 1u);
@@ -663,8 +746,13 @@ k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const QIn
           const float4 a = *reinterpret_cast<const float4*>(sg + 32 * i);
           if (e) {
             const float4 f = *reinterpret_cast<const float4*>(se + 32 * i);
-            f2up(f2add(f2pk(a.x, a.y), f2pk(f.x, f.y)), x[4 * i], x[4 * i + 1]);
-            f2up(f2add(f2pk(a.z, a.w), f2pk(f.z, f.w)), x[4 * i + 2], x[4 * i + 3]);
+            f2_t x01 = f2add(f2pk(a.x, a.y), f2pk(f.x, f.y)), x23 = f2add(f2pk(a.z, a.w), f2pk(f.z, f.w));
+            if (FUSE) { x01 = f2add(x01, f2pk(0.f, 0.f)); x23 = f2add(x23, f2pk(0.f, 0.f)); }  // canon (R2): e' = x - dec
+            f2up(x01, x[4 * i], x[4 * i + 1]);
+            f2up(x23, x[4 * i + 2], x[4 * i + 3]);
+          } else if (FUSE) {
+            f2up(f2add(f2pk(a.x, a.y), f2pk(0.f, 0.f)), x[4 * i], x[4 * i + 1]);
+            f2up(f2add(f2pk(a.z, a.w), f2pk(0.f, 0.f)), x[4 * i + 2], x[4 * i + 3]);
           } else {
             x[4 * i] = a.x; x[4 * i + 1] = a.y; x[4 * i + 2] = a.z; x[4 * i + 3] = a.w;
           }
@@ -679,11 +767,12 @@ k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const QIn
 #pragma unroll
           for (int s2 = 0; s2 < 4; ++s2) {
             const int idx = base + 32 * i + s2;
-            const bool ok = idx < ic.nvalid;
+            const bool ok = idx < nvalid;
             float v = 0.f;
             if (ok) {
               v = __ldg(gl + idx);
-              if (el) v = __fadd_rn(v, __ldg(el + idx));
+              if (el) v = __fadd_rn(v, FUSE ? el[idx] : __ldg(el + idx));
+              if (FUSE) v = __fadd_rn(v, 0.f);
             }
             x[4 * i + s2] = v;
           }
@@ -704,7 +793,7 @@ k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const QIn
 #pragma unroll
         for (int s2 = 0; s2 < 16; ++s2) {
           const int idx = grp * 128 + 4 * l8 + 32 * (s2 >> 2) + (s2 & 3);
-          if (idx < ic.nvalid) { mn = fmin_nan(mn, x[s2]); mx = fmax_nan(mx, x[s2]); }
+          if (idx < nvalid) { mn = fmin_nan(mn, x[s2]); mx = fmax_nan(mx, x[s2]); }
         }
       }
 #pragma unroll
@@ -716,7 +805,7 @@ k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const QIn
 #pragma unroll
         for (int s2 = 0; s2 < 16; ++s2) {
           const int idx = grp * 128 + 4 * l8 + 32 * (s2 >> 2) + (s2 & 3);
-          if (!(idx < ic.nvalid)) x[s2] = mn;  // invalid -> t = 0, q = 0, d = 0
+          if (!(idx < nvalid)) x[s2] = mn;  // invalid -> t = 0, q = 0, d = 0
         }
       }
       float my_inv, my_unit, my_inv2 = 0.f, my_unit2 = 0.f;
@@ -733,6 +822,27 @@ k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const QIn
       double S2inv;
       const bool small = bucket_scale(mn, mx, S, S2inv);
       float a2[KT];
+      if constexpr (FUSE) {
+        FuseW fw;
+        bool wr = valid && jc != LGRECO_CHOICE_SKIP;
+        if (jc != LGRECO_CHOICE_SKIP && (jc < 0 || jc >= K)) {
+          if (lane == 0) atomicOr(fz.flag, 2u);
+          jc = 0;
+        }
+        if (!wr) jc = 0;
+        const int src = (lane & ~7) + (jc & 7);
+        fw.invc = __shfl_sync(LG_FULL, jc < 8 ? my_inv : my_inv2, src);
+        fw.unitc = __shfl_sync(LG_FULL, jc < 8 ? my_unit : my_unit2, src);
+        fw.ebase = ic.elem0 + grp * 128 + 4 * l8;
+        fw.lim = nvalid - (grp * 128 + 4 * l8);
+        fw.vec = cur_regular;
+        fw.wr = wr;
+        if (valid) bad = __fadd_rn(bad, __fmul_rn(__fsub_rn(mx, mn), 0.f));
+        if (__any_sync(LG_FULL, small))
+          prof_cand16x2<KT, true, true>(x, mn, c0, rankfield, step, rk, inv, unit, cs, S, a2, fw, fz.out, fz.ef);
+        else
+          prof_cand16x2<KT, false, true>(x, mn, c0, rankfield, step, rk, inv, unit, cs, 1.f, a2, fw, fz.out, fz.ef);
+      } else {
 #if QP_F32X2
       if (__any_sync(LG_FULL, small)) prof_cand16x2<KT, true>(x, mn, c0, rankfield, step, rk, inv, unit, cs, S, a2);
       else prof_cand16x2<KT, false>(x, mn, c0, rankfield, step, rk, inv, unit, cs, 1.f, a2);
@@ -740,6 +850,7 @@ k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const QIn
       if (__any_sync(LG_FULL, small)) prof_cand16<KT, true>(x, mn, c0, rankfield, step, k0, k1, inv, unit, cs, S, a2);
       else prof_cand16<KT, false>(x, mn, c0, rankfield, step, k0, k1, inv, unit, cs, 1.f, a2);
 #endif
+      }
       if (KT <= 8) {
         // quad row, fixed order: transpose-reduce the 8 lanes of each bucket in fp32
         // (after the xor-4/2/1 halvings lane l8 holds candidate l8's bucket SSE, from
@@ -790,6 +901,7 @@ k_qprofile_q(const float* __restrict__ g, const float* __restrict__ e, const QIn
     else nB = nqc;
     info_async(nB, r_old);
   }
+  fin_flag();
   finish();
 }
 
@@ -984,10 +1096,22 @@ k_qpack(const float* __restrict__ g, float* __restrict__ ef, uint8_t* __restrict
         float* __restrict__ dec_out, const DevLayer* __restrict__ layers, const DevPlan* __restrict__ plan,
         const ProfChunk* __restrict__ chunks, int B, uint32_t k0, uint32_t k1, uint32_t rankfield,
         uint32_t step, unsigned* __restrict__ flag, const P2PDev* __restrict__ p2p,
-        const int32_t* __restrict__ choice, const int32_t* __restrict__ params, int K) {
-  pdl_wait();  // the plan (k_plan_qsgd_dev, or the solve's choice) and the EF of the previous step
-  const ProfChunk ch = chunks[blockIdx.x];
+        const int32_t* __restrict__ choice, const int32_t* __restrict__ params, int K, int l2pf) {
+  const ProfChunk ch = chunks[blockIdx.x];  // (ctx tables: written at ctx creation)
   const DevLayer ly = layers[ch.layer];
+  if (l2pf && threadIdx.x == 0) {
+    // CTAs scheduled while the solve still runs (it triggers its dependents early) pull
+    // their chunk of g and EF into L2 before waiting for the plan: HBM is idle during the
+    // solve.  A prefetch is a hint with no visibility effect (L2 is the coherence point).
+    const int64_t i0 = ly.offset + ch.first * (int64_t)B;
+    const int64_t i1 = ly.offset + min(ly.numel, (ch.first + ch.nbk) * (int64_t)B);
+    const int64_t a0 = (i0 + 3) & ~(int64_t)3, nb = ((i1 - a0) * 4) & ~(int64_t)15;
+    if (nb >= 16 && (((uintptr_t)(g + a0) | (uintptr_t)(ef ? ef + a0 : g)) & 15) == 0) {
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(g + a0), "r"((uint32_t)nb) : "memory");
+      if (ef) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ef + a0), "r"((uint32_t)nb) : "memory");
+    }
+  }
+  pdl_wait();  // the plan (k_plan_qsgd_dev, or the solve's choice) and the EF of the previous step
   DevPlan pl;
   if (choice) {  // W = 1: the bits straight from the device choice (k_plan_qsgd_dev's rule)
     int bits = 0;
@@ -1301,26 +1425,28 @@ cudaError_t launch_qprofile(const QProfileArgs& a, cudaStream_t st) {
     if (quads) {
       const size_t smem = (size_t)Q1_WARPS * Q1_STAGES * 4096;
       const int nsm = a.nqwarps / 32;  // nqwarps = SMs x 4 CTAs x 8 warps (an upper bound)
-#define LG_QQ(KT)                                                                                              \
+#define LG_QQ2(KT, FU)                                                                                         \
   {                                                                                                            \
     long long occm = 0;                                                                                        \
-    if (!memo_get((const void*)k_qprofile_q<KT>, (long long)smem, Q1_THREADS, 0, 0, &occm)) {               \
-      cudaError_t e = memo_smem_attr((const void*)k_qprofile_q<KT>, smem);                                     \
+    if (!memo_get((const void*)k_qprofile_q<KT, FU>, (long long)smem, Q1_THREADS, 0, 0, &occm)) {              \
+      cudaError_t e = memo_smem_attr((const void*)k_qprofile_q<KT, FU>, smem);                                 \
       if (e != cudaSuccess) return e;                                                                          \
       int o = 0;                                                                                               \
-      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_qprofile_q<KT>, Q1_THREADS, smem) != cudaSuccess || \
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_qprofile_q<KT, FU>, Q1_THREADS, smem) !=          \
+              cudaSuccess ||                                                                                   \
           o < 1) { cudaGetLastError(); o = 1; }                                                                 \
       occm = o;                                                                                                \
-      memo_put((const void*)k_qprofile_q<KT>, (long long)smem, Q1_THREADS, 0, 0, occm);                        \
+      memo_put((const void*)k_qprofile_q<KT, FU>, (long long)smem, Q1_THREADS, 0, 0, occm);                    \
     }                                                                                                          \
     const int occ = (int)occm;                                                                                 \
     const int grid = std::max(1, std::min(a.nqwarps / Q1_WARPS, nsm * occ));                                    \
-    const cudaError_t e2 = launch_pdl(k_qprofile_q<KT>, dim3(grid), dim3(Q1_THREADS), smem, st, a.g, a.e,       \
+    const cudaError_t e2 = launch_pdl(k_qprofile_q<KT, FU>, dim3(grid), dim3(Q1_THREADS), smem, st, a.g, a.e,   \
                                       a.qinfo, a.nqchunks, a.ticket, a.cs, a.K, philox_rk(a.k0, a.k1), a.rankfield, \
-                                      a.step,                                                                    \
-                                      a.ptr_aligned, a.partial);                                                 \
+                                      a.step, a.ptr_aligned, a.partial, fz);                                     \
     if (e2 != cudaSuccess) return e2;                                                                            \
   }
+#define LG_QQ(KT) { if (a.fuse) LG_QQ2(KT, true) else LG_QQ2(KT, false) }
+      const QFuse fz = a.fuse ? *a.fuse : QFuse{};
       switch (a.K) {
         case 4: LG_QQ(4); break;
         case 5: LG_QQ(5); break;
@@ -1331,6 +1457,7 @@ cudaError_t launch_qprofile(const QProfileArgs& a, cudaStream_t st) {
           if (a.K < 4) LG_QQ(4) else LG_QQ(16)
       }
 #undef LG_QQ
+#undef LG_QQ2
     } else {
 #define LG_QP(KT)                                                                          \
   k_qprofile<KT><<<a.nchunks, QP_THREADS, 0, st>>>(a.g, a.e, a.layers, a.chunks, a.B, a.cs, a.K, \
@@ -1349,10 +1476,15 @@ cudaError_t launch_qprofile(const QProfileArgs& a, cudaStream_t st) {
     }
     if (a.ev1) cudaEventRecord(a.ev1, st);
   }
-  if (quads) {
+  if (quads && a.reduce_pdl) {
     const cudaError_t e = launch_pdl(k_qprofile_reduce, dim3(a.nseg), dim3(QR_ROWS), 0, st, a.layers, a.segs, a.lseg0,
                                      a.partial, a.segsum, a.ldone, a.params, a.K, a.B, a.err, a.bits);
     if (e != cudaSuccess) return e;
+  } else if (quads) {
+    // a plain launch: waits for ALL prior work of the stream, including a solve the
+    // concurrent fused kernel ran beside (LGRECO_PC_CONCURRENT)
+    k_qprofile_reduce<<<a.nseg, QR_ROWS, 0, st>>>(a.layers, a.segs, a.lseg0, a.partial, a.segsum, a.ldone, a.params,
+                                                  a.K, a.B, a.err, a.bits);
   }
   else
     k_qprofile_reduce_chunks<<<a.L, 256, 0, st>>>(a.layers, a.layer_chunk0, a.partial, a.params, a.K, a.B, a.err,
@@ -1360,11 +1492,20 @@ cudaError_t launch_qprofile(const QProfileArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+// K5's L2 prefetch before its plan wait (LGRECO_K5_PREFETCH=0 disables it, for A/B)
+static int k5_l2_prefetch() {
+  static const int v = [] {
+    const char* s = getenv("LGRECO_K5_PREFETCH");
+    return (s && s[0] == '0') ? 0 : 1;
+  }();
+  return v;
+}
+
 cudaError_t launch_qpack(const QPackArgs& a, cudaStream_t st) {
   if (a.nchunks == 0) return cudaSuccess;
   const cudaError_t e = launch_pdl(k_qpack, dim3(a.nchunks), dim3(QP_THREADS), 0, st, a.g, a.ef, a.payload, a.dec,
                                    a.layers, a.plan, a.chunks, a.B, a.k0, a.k1, a.rankfield, a.step, a.flag, a.p2p,
-                                   a.choice, a.params, a.K);
+                                   a.choice, a.params, a.K, k5_l2_prefetch());
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }

@@ -544,9 +544,12 @@ k_tk_write(const float* __restrict__ g, float* __restrict__ ef, uint8_t* __restr
   const DevLayer ly = a.layers[l];
   const TQ q = a.q[c];
   const uint32_t T = q.T;
-  const int64_t rties = q.r;
   if (a.kq[c] == 0) return;  // a skipped layer (NEXT-4): EF and output untouched
-  const ulonglong2 off = a.coff[blockIdx.x];
+  // no payload and every tie kept or none: k_tk_count / k_tk_scan skipped this layer, its
+  // offsets were never written -- the tie rule needs none (r = 0: no tie, r = ties: all)
+  const bool trivial = !a.need_off && (q.r == 0 || q.r == q.ties);
+  const int64_t rties = trivial ? (q.r == 0 ? (int64_t)0 : INT64_MAX) : q.r;
+  const ulonglong2 off = trivial ? make_ulonglong2(0ull, 0ull) : a.coff[blockIdx.x];
   uint2* pairs = payload ? reinterpret_cast<uint2*>(payload + a.tplan[l].pay_off) : nullptr;
   int64_t eq_run = (int64_t)off.y;                                       // ties before this position
   int64_t kept_run = (int64_t)off.x + min((int64_t)off.y, rties);        // kept entries before

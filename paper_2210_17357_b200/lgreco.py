@@ -18,6 +18,7 @@ LIB_PATH = os.environ.get("LGRECO_LIB") or os.path.join(_HERE, "liblgreco.so")  
 OK, EINVAL, ENONFINITE, EINFEASIBLE, ECUDA, ENCCL, ENOMEM, EUNSUPPORTED = 0, -1, -2, -3, -4, -5, -6, -7
 QSGD, TOPK, POWERSGD = 0, 1, 2
 PSGD_POWER, PSGD_SVD, PSGD_AUTO = 0, 1, 2  # PowerSGD profile method (NEXT-2 selector)
+PC_CONCURRENT = 1  # lgreco_profile_compress: may run beside the preceding kernel (include/lgreco.h)
 CHOICE_SKIP = -2  # (NEXT-4) a compressed layer another family's ctx owns: left untouched
 METRIC_SQ, DISC_FLOOR = 1, 2
 
@@ -76,6 +77,7 @@ _SIGS = {
     "lgreco_plan_broadcast": (C.c_int, [_VP, _VP, _VP]),
     "lgreco_compress_allreduce": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _U64, _VP]),
     "lgreco_compress_allreduce_dev": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _U64, _VP]),
+    "lgreco_profile_compress": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _U64, _VP, _VP, C.c_uint32, _VP]),
     "lgreco_payload_bytes": (_I64, [_VP, _VP]),
     "lgreco_shard_bounds": (C.c_int, [_VP, _VP, _I32, _VP, _VP]),
     "lgreco_qsgd_pack": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, _U32, _U64, _VP]),
@@ -233,6 +235,14 @@ class Context:
     def compress_allreduce_dev(self, d_choice, g, ef, out, step, stream=None):
         _check(lib().lgreco_compress_allreduce_dev(self.h, _ptr(d_choice), _ptr(g), _ptr(ef), _ptr(out), step,
                                                    _stream(stream)), "compress_allreduce_dev")
+
+    def profile_compress(self, d_choice, g, ef, out, step, err, bits, concurrent=False, stream=None):
+        """profile(g, ef, step, err, bits) then compress_allreduce_dev(d_choice, ...), one pass
+        over g and ef (QSGD, W = 1): the paper's per-step schedule (the plan in force
+        compresses the step, the profile feeds the next solve)."""
+        _check(lib().lgreco_profile_compress(self.h, _ptr(d_choice), _ptr(g), _ptr(ef), _ptr(out), step, _ptr(err),
+                                             _ptr(bits), PC_CONCURRENT if concurrent else 0, _stream(stream)),
+               "profile_compress")
 
     def plan_broadcast(self, d_choice, stream=None):
         _check(lib().lgreco_plan_broadcast(self.h, _ptr(d_choice), _stream(stream)), "plan_broadcast")

@@ -220,3 +220,31 @@ def test_compress_reuses_profile_thresholds(lg, ref, seed):
     for out, ef in res:
         assert np.array_equal(out.view(np.uint32), out_ref.view(np.uint32))
         assert np.array_equal(ef.view(np.uint32), es_ref[0].view(np.uint32))
+
+
+def test_no_payload_compress_after_payload_compress(lg, ref):
+    """A W = 1 compress without payload skips the count / scan of layers keeping every
+    tie at T or none (their chunk offsets are not needed); its write pass must not read
+    the offsets a preceding payload-writing call left behind (regression: the last tie of
+    a layer was dropped in the hybrid test).  Continuous layers have ties = r = 1."""
+    layers = _layers()
+    L, K = len(layers), len(PPM)
+    ctx = lg.Context(layers, lg.TOPK, PPM)
+    for it, seed in enumerate((31, 32, 33)):
+        g, e = W.heavy_tailed(layers, seed=seed, sparse_rows_layer=None)
+        rng = np.random.default_rng(seed)
+        choice = [int(rng.integers(0, K)) if l.compress else -1 for l in layers]
+        lppm = [PPM[c] if l.compress else 0 for c, l in zip(choice, layers)]
+        gd = _dev(g)
+        # payload-writing pack first (fills the chunk offsets), on a copy of the EF
+        S = ctx.payload_bytes(choice)
+        pay = torch.zeros(max(S, 16), dtype=torch.uint8, device="cuda")
+        ctx.topk_pack(choice, gd, _dev(e), pay, None)
+        ed = _dev(e)
+        out = torch.empty_like(gd)
+        ctx.compress_allreduce_dev(torch.tensor(choice, dtype=torch.int32, device="cuda"), gd, ed, out, 100 + it)
+        ctx.check()
+        out_ref, es_ref, _ = ref.topk_allreduce(layers, lppm, [g], [e])
+        assert np.array_equal(out.cpu().numpy().view(np.uint32), out_ref.view(np.uint32)), it
+        assert np.array_equal(ed.cpu().numpy().view(np.uint32), es_ref[0].view(np.uint32)), it
+    ctx.close()
