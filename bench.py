@@ -243,16 +243,20 @@ def run_ours(args):
     # the SMs the fused kernel leaves free (LGRECO_PC_CONCURRENT).  Three plan buffers:
     # step t reads plans[t % 3], the solve of step t writes plans[(t + 2) % 3].
     plans = [dflt.clone() for _ in range(3)]
+    # two (err, bits) table pairs: the fused pass of step t writes pair t % 2 while the solve
+    # of step t - 1 beside it still reads pair (t - 1) % 2
+    tabs = [(err, bits), (torch.empty_like(err), torch.empty_like(bits))]
 
     def step_pipe(s, gin=None, gout=None, conc=True, marks=None, pre_solve=None):
         gin = g if gin is None else gin
         gout = out if gout is None else gout
         staged = marks is not None and len(marks) == 3
+        e_t, b_t = tabs[s % 2]
         if marks: marks[0].record(stream)
-        ctx.profile_compress(plans[s % 3], gin, ef, gout, s, err, bits, concurrent=conc)
+        ctx.profile_compress(plans[s % 3], gin, ef, gout, s, e_t, b_t, concurrent=conc)
         if staged: marks[1].record(stream)
         if pre_solve: pre_solve()
-        lgreco.solve(err, bits, dflt, comp, D=D_BINS, choice=plans[(s + 2) % 3], info=info_d, workspace=ws)
+        lgreco.solve(e_t, b_t, dflt, comp, D=D_BINS, choice=plans[(s + 2) % 3], info=info_d, workspace=ws)
         ctx.plan_broadcast(plans[(s + 2) % 3])
         if marks: marks[-1].record(stream)
 

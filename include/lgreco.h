@@ -174,7 +174,9 @@ size_t lgreco_solve_workspace_bytes(int32_t L, int32_t K, int32_t D);
  * d_err/d_bits L*K (from lgreco_profile or any table), d_default_idx L,
  * d_compress L (nullable: all active), d_choice L (out; -1 for inactive layers),
  * d_info (out), d_workspace of lgreco_solve_workspace_bytes(L,K,D) bytes.
- * Single CTA-resident DP on `stream`; no host synchronisation. */
+ * Cluster (or single-CTA) DP on `stream`, launched after ALL prior work of the stream has
+ * completed (no programmatic overlap on its start); it lets its successor be scheduled
+ * once it runs (a compress reading d_choice still waits for it); no host synchronisation. */
 int lgreco_solve(const double* d_err, const int64_t* d_bits, int32_t L, int32_t K,
                  const int32_t* d_default_idx, const int32_t* d_compress, int32_t D,
                  uint32_t flags, int32_t* d_choice, lgreco_solve_info* d_info,
@@ -235,9 +237,11 @@ int lgreco_compress_allreduce_dev(lgreco_ctx* ctx, const int32_t* d_choice, cons
  * output of a solve that reads d_err.  flags: LGRECO_PC_CONCURRENT -- the caller asserts
  * that the kernel enqueued immediately before this call on `stream` (typically the
  * lgreco_solve of the previous step, writing a plan other than d_choice) produces nothing
- * this call reads; the fused kernel may then run beside it on the SMs it leaves free, and
- * the profile's reduction waits for both.  d_g, d_ef, d_out 16-byte aligned (EINVAL
- * otherwise); d_err L*K doubles, d_bits L*K int64. */
+ * this call reads -- in particular d_err / d_bits must not be the tables that solve reads
+ * (alternate two pairs) and d_choice not the plan it writes; the fused kernel may then
+ * run beside it on the SMs it leaves free.  (lgreco_solve is a plain launch: it waits for
+ * all prior work of the stream, the previous solve included.)  d_g, d_ef, d_out 16-byte
+ * aligned (EINVAL otherwise); d_err L*K doubles, d_bits L*K int64. */
 #define LGRECO_PC_CONCURRENT 1u
 int lgreco_profile_compress(lgreco_ctx* ctx, const int32_t* d_choice, const float* d_g, float* d_ef, float* d_out,
                             uint64_t step, double* d_err, int64_t* d_bits, uint32_t flags, void* stream);

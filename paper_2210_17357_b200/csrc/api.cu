@@ -240,7 +240,7 @@ int lgreco_ctx_create(lgreco_ctx** out, const lgreco_layer* layers, int32_t L, c
   LG_ALLOC(c->d_partial, sizeof(double) * (size_t)std::max(1, std::max(c->nchunks, c->nqchunks)) * c->K);
   LG_ALLOC(c->d_qinfo, sizeof(lg::QInfo) * std::max(1, c->nqchunks));
   LG_ALLOC(c->d_layer_qchunk0, sizeof(int32_t) * (L + 1));
-  LG_ALLOC(c->d_ticket, 17 * 64 * sizeof(unsigned));
+  LG_ALLOC(c->d_ticket, lg::QT_WORDS * sizeof(unsigned));
   LG_ALLOC(c->d_qseg, sizeof(lg::QSeg) * std::max(1, c->nqseg));
   LG_ALLOC(c->d_lqseg0, sizeof(int32_t) * (L + 1));
   LG_ALLOC(c->d_segsum, sizeof(double) * std::max(1, c->nqseg) * c->K);
@@ -273,7 +273,7 @@ int lgreco_ctx_create(lgreco_ctx** out, const lgreco_layer* layers, int32_t L, c
   if (e == cudaSuccess && c->nqchunks)
     e = cudaMemcpyAsync(c->d_qinfo, qchunks.data(), sizeof(lg::QInfo) * c->nqchunks, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = cudaMemcpyAsync(c->d_layer_qchunk0, lqc0.data(), sizeof(int32_t) * (L + 1), cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess) e = cudaMemsetAsync(c->d_ticket, 0, 17 * 64 * sizeof(unsigned), st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(c->d_ticket, 0, lg::QT_WORDS * sizeof(unsigned), st);
   if (e == cudaSuccess && c->nqseg)
     e = cudaMemcpyAsync(c->d_qseg, qsegs.data(), sizeof(lg::QSeg) * c->nqseg, cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = cudaMemcpyAsync(c->d_lqseg0, lqs0.data(), sizeof(int32_t) * (L + 1), cudaMemcpyHostToDevice, st);
@@ -760,7 +760,6 @@ int lgreco_profile_compress(lgreco_ctx* c, const int32_t* d_choice, const float*
   lg::QFuse fz{d_ef, d_out, d_choice, c->d_flag, c->d_chunks_raw, c->nchunks_raw, c->d_layers, c->B, conc ? 1 : 0,
                  c->L};
   a.fuse = &fz;
-  a.reduce_pdl = conc ? 0 : 1;
   if (c->timing) {
     cudaEvent_t e0, e1;
     LG_CUDA(cudaEventCreate(&e0));

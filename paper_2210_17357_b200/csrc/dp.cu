@@ -1946,19 +1946,17 @@ static cudaError_t launch_solve_cluster(const SolveArgs& a, uint8_t* pd, int32_t
     if (e != cudaSuccess) { cudaGetLastError(); return cudaErrorNotSupported; }
   }
   cudaLaunchConfig_t cfg = {};
-  cudaLaunchAttribute attr[2];
+  cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = NC;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL: k_solve_cl waits in-kernel
-  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.gridDim = dim3(NC * ngroups, 1, 1);
   cfg.blockDim = dim3(nt, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;  // (occupancy query without PDL)
+  cfg.numAttrs = 1;
   if (!cached) {
     int nclusters = 0;
     e = cudaOccupancyMaxActiveClusters(&nclusters, (const void*)fn, &cfg);
@@ -1970,7 +1968,10 @@ static cudaError_t launch_solve_cluster(const SolveArgs& a, uint8_t* pd, int32_t
       return cudaErrorNotSupported;
     }
   }
-  cfg.numAttrs = 2;
+  // a plain launch (no PDL attribute): the solve waits for ALL prior work of the stream --
+  // in the pipelined schedule that is the previous solve too, whose plan the concurrent
+  // fused pass before this call reads (include/lgreco.h, LGRECO_PC_CONCURRENT)
+  cfg.numAttrs = 1;
   // the launch's token (the group handshake): unique per launch in this process
   static std::atomic<uint64_t> g_tok{0x9E3779B97F4A7C15ull ^ ((uint64_t)time(nullptr) << 24) ^ (uint64_t)getpid()};
   const uint64_t tok = g_tok.fetch_add(2) | 1ull;

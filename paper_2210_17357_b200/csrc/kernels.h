@@ -43,6 +43,8 @@ struct QFuse {
   int L;                     // layers (the first QF_LCACHE plan entries are staged in shared memory)
 };
 constexpr int QF_LCACHE = 4096;
+// K1's ticket words (64 apart): [0, 16) the parts' quad tickets, then the finish counter
+constexpr int QT_ARR = 16, QT_WORDS = 17 * 64;
 
 struct QProfileArgs {
   const float* g; const float* e;
@@ -59,7 +61,6 @@ struct QProfileArgs {
   const QSeg* segs = nullptr; int nseg = 0; const int32_t* lseg0 = nullptr; double* segsum = nullptr;
   unsigned* ldone = nullptr;
   const QFuse* fuse = nullptr;  // non-null: the fused profile + compress kernel
-  int reduce_pdl = 1;           // 0: K1b launched without PDL (waits for all prior stream work)
 };
 
 // Peer-memory exchange (W <= 8 ranks): device pointers to every rank's stage-1 receive

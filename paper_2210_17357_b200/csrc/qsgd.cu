@@ -555,6 +555,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 #define QK_UNROLL 4  // K5 fast path: buckets per warp iteration (loads in flight)
 #endif
 constexpr int QP_NPART = 16;  // K1 ticket counters (parts of the quad range), 256 B apart
+constexpr int QR_ROWS = 256;  // K1b segment: rows of one layer reduced by one fixed tree
 #ifndef Q1_WARPS
 #define Q1_WARPS 8  // warps per CTA of the K1 fast kernel (each double-buffers 4 KB quads: 8 KB of shared memory)
 #endif
@@ -609,8 +610,8 @@ k_qprofile_q(const float* __restrict__ g, const float* e, const QInfo* __restric
     return q;
   };
   auto finish = [&]() {  // after this warp found every part exhausted
-    if (lane == 0 && atomicAdd(&ticket[QP_NPART * 64], 1u) == gridDim.x * Q1_WARPS - 1u) {
-      for (int p2 = 0; p2 <= QP_NPART; ++p2) atomicExch(&ticket[p2 * 64], 0u);
+    if (lane == 0 && atomicAdd(&ticket[QT_ARR * 64], 1u) == gridDim.x * Q1_WARPS - 1u) {
+      for (int p2 = 0; p2 <= QT_ARR; ++p2) atomicExch(&ticket[p2 * 64], 0u);
     }
   };
   // Quad descriptors travel through a 3-slot shared ring per warp (c, nA, nB), filled by
@@ -910,7 +911,6 @@ k_qprofile_q(const float* __restrict__ g, const float* e, const QInfo* __restric
 // loads row seg0 + t (K contiguous doubles), a fixed shared-memory tree per candidate
 // gives the segment sum; the layer's last segment to finish (counter per layer, reset
 // by that CTA) adds the segment sums in segment order and writes err/bits.
-constexpr int QR_ROWS = 256;
 __global__ void __launch_bounds__(QR_ROWS)
 k_qprofile_reduce(const DevLayer* __restrict__ layers, const QSeg* __restrict__ segs, const int32_t* __restrict__ lseg0,
                   const double* __restrict__ partial, double* __restrict__ segsum, unsigned* __restrict__ ldone,
@@ -1476,15 +1476,11 @@ cudaError_t launch_qprofile(const QProfileArgs& a, cudaStream_t st) {
     }
     if (a.ev1) cudaEventRecord(a.ev1, st);
   }
-  if (quads && a.reduce_pdl) {
+  if (quads) {
+    // PDL: its CTAs take the SMs K1's CTAs release and wait in-kernel for K1's completion
     const cudaError_t e = launch_pdl(k_qprofile_reduce, dim3(a.nseg), dim3(QR_ROWS), 0, st, a.layers, a.segs, a.lseg0,
                                      a.partial, a.segsum, a.ldone, a.params, a.K, a.B, a.err, a.bits);
     if (e != cudaSuccess) return e;
-  } else if (quads) {
-    // a plain launch: waits for ALL prior work of the stream, including a solve the
-    // concurrent fused kernel ran beside (LGRECO_PC_CONCURRENT)
-    k_qprofile_reduce<<<a.nseg, QR_ROWS, 0, st>>>(a.layers, a.segs, a.lseg0, a.partial, a.segsum, a.ldone, a.params,
-                                                  a.K, a.B, a.err, a.bits);
   }
   else
     k_qprofile_reduce_chunks<<<a.L, 256, 0, st>>>(a.layers, a.layer_chunk0, a.partial, a.params, a.K, a.B, a.err,

@@ -62,7 +62,7 @@ class _Bucket:
 
 class LGrecoHook:
     def __init__(self, family, params, default_idx, *, warmup_steps=10, replan_every=100, D=10000, seed=0x5EED,
-                 qbucket=128, flags=0, process_group=None, record=False, exchange="p2p"):
+                 qbucket=128, flags=0, process_group=None, record=False, exchange="p2p", timer=None):
         self.family, self.params = family, [int(p) for p in params]
         self.K = len(self.params)
         self.default_idx = int(default_idx)
@@ -75,6 +75,11 @@ class LGrecoHook:
         self.buckets: dict[int, _Bucket] = {}
         self.record = record
         self.last = {}  # bucket index -> (g, ef_before, choice, step) when record=True
+        # NEXT-1: a bucket_timer.BucketSyncTimer brackets every
+        # compressed bucket's synchronisation with device events, recording the bytes the
+        # plan transmits (objectives.fit_bucket_time -> time_weights)
+        self.timer = timer
+        self._timer_open = False
 
     def _state(self, bucket):
         shapes = tuple(tuple(p.shape) for p in bucket.parameters())
@@ -98,6 +103,13 @@ class LGrecoHook:
         st.G.zero_()
         st.added = []
         st.planned = True
+        if self.timer is not None:  # the plan's transmitted bytes (one host round trip per replan)
+            ch = st.choice.cpu().tolist()
+            if self.family != lgreco.POWERSGD:
+                st.sent = st.ctx.payload_bytes(ch)
+            else:  # R11: 32 r (m + k) bits, raw when r (m + k) >= m k
+                st.sent = sum(4 * min(self.params[c] * (l.rows + l.cols), l.numel) if l.compress and c >= 0
+                              else 4 * l.numel for l, c in zip(st.layers, ch))
 
     @staticmethod
     def hook(state: "LGrecoHook", bucket: dist.GradBucket) -> torch.futures.Future[torch.Tensor]:
@@ -116,7 +128,17 @@ class LGrecoHook:
             return fut.then(lambda f: f.value()[0].div_(world))
         rec = (g.clone(), st.ef.clone(), st.choice.clone(), step) if state.record else None
         lgreco.accumulate(st.G, g)
+        tm = state.timer
+        if tm is not None:
+            if bucket.index() == 0:  # DDP hands the buckets over in index order every step
+                if state._timer_open:
+                    tm.end_step()
+                tm.begin_step()
+                state._timer_open = True
+            tm.start(bucket.index())
         st.ctx.compress_allreduce_dev(st.choice, g, st.ef, st.out, step)
+        if tm is not None:
+            tm.stop(bucket.index(), st.sent)
         g.copy_(st.out)
         if rec is not None:
             state.last[bucket.index()] = rec + (st.out.clone(), st.layers)

@@ -36,7 +36,10 @@ def test_ddp_hook_one_gpu(ref):
                                                    else [])) for m in net]).cuda()
         ref_net.load_state_dict(net.state_dict())
         ddp = torch.nn.parallel.DistributedDataParallel(net, device_ids=[0], bucket_cap_mb=0.5)
-        state = LGrecoHook(lgreco.QSGD, W.QSGD_BITS, default_idx=2, warmup_steps=2, replan_every=4, record=True)
+        from paper_2210_17357_b200.bucket_timer import BucketSyncTimer
+        timer = BucketSyncTimer()
+        state = LGrecoHook(lgreco.QSGD, W.QSGD_BITS, default_idx=2, warmup_steps=2, replan_every=4, record=True,
+                           timer=timer)
         ddp.register_comm_hook(state, LGrecoHook.hook)
         opt = torch.optim.SGD(ddp.parameters(), lr=0.05)
         g = torch.Generator(device="cuda").manual_seed(1)
@@ -56,6 +59,14 @@ def test_ddp_hook_one_gpu(ref):
             losses.append(float(loss.detach()))
             opt.step()
         torch.cuda.synchronize()
+        # NEXT-1: the hook's bucket timer saw every compressed step of every bucket, with
+        # the plan's transmitted bytes (lgreco_payload_bytes) and device-timed intervals
+        timer.end_step()
+        sizes, sync, per = timer.samples()
+        assert sizes.shape[0] >= 8 and sizes.shape[1] == len(state.buckets), sizes.shape
+        assert np.all(sizes > 0) and np.all(per > 0) and np.all(sync >= per.max(axis=1) - 1e-6)
+        for idx, stb in state.buckets.items():
+            assert sizes[-1, idx] == stb.ctx.payload_bytes(stb.choice.cpu().tolist())
         assert state.last, "no compressed step was recorded"
         for idx, (gin, ef0, choice, st, out, layers) in state.last.items():
             # the hook's compressed step vs the ORACLE on the recorded inputs (R13, W = 1)

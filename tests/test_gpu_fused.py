@@ -170,8 +170,8 @@ def test_pipelined_chain_matches_oracle(lg, ref, cfg, lag):
     comp = torch.tensor([1 if l.compress else 0 for l in layers], dtype=torch.int32, device="cuda")
     ddef = torch.tensor(dflt, dtype=torch.int32, device="cuda")
     plans = [torch.tensor(dflt, dtype=torch.int32, device="cuda") for _ in range(lag + 1)]
-    err = torch.empty(L, K, dtype=torch.float64, device="cuda")
-    bits = torch.empty(L, K, dtype=torch.int64, device="cuda")
+    tabs = [(torch.empty(L, K, dtype=torch.float64, device="cuda"), torch.empty(L, K, dtype=torch.int64, device="cuda"))
+            for _ in range(2)]  # (the concurrent pass writes one pair while the solve reads the other)
     ws = torch.empty(lg.solve_workspace_bytes(L, K, 10000), dtype=torch.uint8, device="cuda")
     info = torch.empty(64, dtype=torch.uint8, device="cuda")
     g0, e0 = W.gaussian_outliers(layers, seed=11)
@@ -188,6 +188,7 @@ def test_pipelined_chain_matches_oracle(lg, ref, cfg, lag):
         out = torch.empty_like(gd)
         use = plans[t % (lag + 1)]
         used.append(use.clone())  # (the plan buffer is reused lag + 1 steps later)
+        err, bits = tabs[t % 2]
         ctx.profile_compress(use, gd, ed, out, t, err, bits, concurrent=(lag == 2 and t > 0))
         nxt = plans[(t + lag) % (lag + 1)]
         lg.solve(err, bits, ddef, comp, choice=nxt, info=info, workspace=ws)

@@ -1,0 +1,91 @@
+"""NEXT-1 on measured times: the bucket timer measures every DDP
+bucket's synchronisation for random per-bucket compression plans, the linear model
+time ~ sum_b size_b T(b) + c is fitted to those device-timed samples, the fitted T(b)
+become integer layer weights, and the weighted DP on the device equals the oracle's
+weighted DP.  On this one-GPU box a bucket's "synchronisation" is its QSGD pack (K5
+with payload) followed by the copy of the packed payload over the one link the box has
+(PCIe, device -> pinned host); at W > 1 the same timer brackets
+lgreco_compress_allreduce_dev (NVLink)."""
+import numpy as np
+import pytest
+import torch
+
+from paper_2210_17357_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+BITS = W.QSGD_BITS
+
+
+@pytest.fixture(scope="module")
+def lg():
+    from paper_2210_17357_b200 import lgreco
+    return lgreco
+
+
+def test_measured_bucket_times_fit_and_weighted_solve(lg, ref):
+    from paper_2210_17357_b200 import objectives as O
+    from paper_2210_17357_b200.bucket_timer import BucketSyncTimer, r_squared
+    layers = W.config_layers("C4")
+    L, K = len(layers), len(BITS)
+    bk = O.ddp_buckets(layers)
+    nb = max(bk) + 1
+    assert nb >= 3
+    g, _ = W.gaussian_outliers(layers, seed=5)
+    # per bucket: its contiguous run of layers, rebased, with its own ctx and buffers
+    per = []
+    for b in range(nb):
+        idx = [i for i in range(L) if bk[i] == b]
+        assert idx == list(range(idx[0], idx[-1] + 1))
+        o0 = layers[idx[0]].offset
+        sub = [W.Layer(layers[i].offset - o0, layers[i].numel, layers[i].rows, layers[i].cols, layers[i].compress)
+               for i in idx]
+        n = W.total_numel(sub)
+        ctx = lg.Context(sub, lg.QSGD, BITS, seed=3)
+        gd = torch.from_numpy(np.ascontiguousarray(g[o0:o0 + n])).cuda()
+        cap = ctx.payload_bytes([K - 1] * len(sub))
+        pay = torch.empty(cap, dtype=torch.uint8, device="cuda")
+        host = torch.empty(cap, dtype=torch.uint8).pin_memory()
+        per.append((ctx, sub, gd, pay, host))
+    timer = BucketSyncTimer(nb)
+    rng = np.random.default_rng(9)
+    stream = torch.cuda.current_stream()
+    S = 40
+    for s in range(S + 3):
+        cj = rng.integers(0, K, nb)  # one bit-width per bucket: sizes vary independently
+        timer.begin_step()
+        for b in range(nb):
+            ctx, sub, gd, pay, host = per[b]
+            ch = [int(cj[b]) if l.compress else -1 for l in sub]
+            nbytes = ctx.payload_bytes(ch)
+            timer.start(b, stream)
+            ctx.qsgd_pack(ch, gd, None, pay, None, 0, s)
+            host[:nbytes].copy_(pay[:nbytes], non_blocking=True)
+            timer.stop(b, nbytes, stream)
+        timer.end_step()
+    sizes, sync, per_b = timer.samples()
+    sizes, sync = sizes[3:], sync[3:]  # (warm-up)
+    T, c = O.fit_bucket_time(sizes, sync)
+    r2 = r_squared(sizes, sync, T, c)
+    assert r2 >= 0.9, (r2, T, c)
+    assert np.all(T > 0), T
+    # the fitted coefficients are a transfer time per byte: within 4x of each other
+    assert T.max() / T.min() < 4.0, T
+    w = O.time_weights(layers, T, bk)
+    assert w.min() >= 1
+    # weighted solve on a C4 profile table: device == oracle
+    ctx = lg.Context(layers, lg.QSGD, BITS, seed=3)
+    gd = torch.from_numpy(g).cuda()
+    err = torch.empty(L, K, dtype=torch.float64, device="cuda")
+    bits = torch.empty(L, K, dtype=torch.int64, device="cuda")
+    ctx.profile(gd, None, 0, err, bits)
+    wb = lg.weight_costs(bits, torch.from_numpy(w).cuda())
+    comp = torch.tensor([l.compress for l in layers], dtype=torch.int32, device="cuda")
+    dflt = torch.full((L,), BITS.index(4), dtype=torch.int32, device="cuda")
+    choice, _ = lg.solve(err, wb, dflt, comp)
+    e_np, b_np = err.cpu().numpy(), bits.cpu().numpy()
+    _, c_ref, _ = ref.solve(e_np, b_np * w[:, None], dflt.cpu().numpy(), comp.cpu().numpy(), D=10000)
+    assert list(choice.cpu().numpy()) == list(c_ref)
+    for p in per:
+        p[0].close()
+    ctx.close()
