@@ -40,7 +40,8 @@ K1_OPS_PER_ELEM = 70
 FUSED_EXTRA_OPS = 5  # the planned candidate's compress in the fused pass: t*inv - u, ceil, min s, dec, x - dec
 PIPE_NOTE = ("pipelined (PAPER.md:312-314, re-solved every step): step t = the fused profile + compress pass "
              "(lgreco_profile_compress) with the plan solved from the profile of step t-2, beside the solve of "
-             "step t-1 (LGRECO_PC_CONCURRENT); value = gradient bytes / (K steps' time / K)")
+             "step t-1 (LGRECO_PC_CONCURRENT; the solve on 2 x 8-SM clusters, LGRECO_SOLVE_NARROW); "
+             "value = gradient bytes / (K steps' time / K)")
 SEED = 0x5EED
 
 
@@ -256,7 +257,8 @@ def run_ours(args):
         ctx.profile_compress(plans[s % 3], gin, ef, gout, s, e_t, b_t, concurrent=conc)
         if staged: marks[1].record(stream)
         if pre_solve: pre_solve()
-        lgreco.solve(e_t, b_t, dflt, comp, D=D_BINS, choice=plans[(s + 2) % 3], info=info_d, workspace=ws)
+        lgreco.solve(e_t, b_t, dflt, comp, D=D_BINS, flags=lgreco.SOLVE_NARROW, choice=plans[(s + 2) % 3],
+                     info=info_d, workspace=ws)
         ctx.plan_broadcast(plans[(s + 2) % 3])
         if marks: marks[-1].record(stream)
 

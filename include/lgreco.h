@@ -50,6 +50,9 @@ extern "C" {
 #define LGRECO_METRIC_SQ 1u   /* use squared L2 instead of L2 (PAPER.md:180 vs :183) */
 #define LGRECO_DISC_FLOOR 2u  /* floor discretisation instead of ceil */
 #define LGRECO_SOLVE_SINGLE_CTA 4u  /* run Algorithm 1 on one CTA (no 8-SM cluster); same result */
+#define LGRECO_SOLVE_NARROW 8u  /* clusters of 8 CTAs instead of 16 (fewer SMs for longer): for a
+                                   solve that runs beside other work, e.g. next to the fused pass of
+                                   the pipelined schedule (lgreco_profile_compress); same result */
 
 /* One layer of the flat gradient.  rows*cols == numel for matrices (the view is
  * (shape[0], numel/shape[0])); rows == 0 marks a vector.  compress == 0 sends the

@@ -2001,8 +2001,11 @@ cudaError_t launch_solve(const SolveArgs& a, void* ws, cudaStream_t st) {
     int ng = a.L >= 32 ? 2 : 1;
     if (const char* env = getenv("LGRECO_DP_GROUPS")) ng = atoi(env) == 2 ? 2 : 1;
     cudaError_t ce = cudaErrorNotSupported;
-    if (ng == 2) ce = launch_solve_cluster(a, pd, act, wdisc, wadd, wmaxd, 16, 2, rowout, jmeta, st);
-    if (ce == cudaErrorNotSupported) ce = launch_solve_cluster(a, pd, act, wdisc, wadd, wmaxd, 16, 1, rowout, jmeta, st);
+    // LGRECO_SOLVE_NARROW: 8-CTA clusters (beside the fused pass: 2 x 8 SMs for 62 us took
+    // less from it than 2 x 16 SMs for 55 us -- C4 pipelined step 96.5 vs 100.2 us)
+    const int nc = (a.flags & LGRECO_SOLVE_NARROW) ? 8 : 16;
+    if (ng == 2) ce = launch_solve_cluster(a, pd, act, wdisc, wadd, wmaxd, nc, 2, rowout, jmeta, st);
+    if (ce == cudaErrorNotSupported) ce = launch_solve_cluster(a, pd, act, wdisc, wadd, wmaxd, nc, 1, rowout, jmeta, st);
     if (ce == cudaErrorNotSupported) ce = launch_solve_cluster(a, pd, act, wdisc, wadd, wmaxd, 8, 1, rowout, jmeta, st);
     if (ce != cudaErrorNotSupported) return ce;
     if (getenv("LGRECO_DEBUG")) fprintf(stderr, "lgreco: cluster solve not used (L=%d K=%d D=%d)\n", a.L, a.K, a.D);

@@ -30,6 +30,9 @@ namespace lg {
 
 constexpr int QP_THREADS = 256;
 constexpr int QP_WARPS = QP_THREADS / 32;
+#ifndef QF_MAGIC
+#define QF_MAGIC 0  // fused pass: the planned candidate's ceil by the FADD2 magic (1) or FRND.CEIL (0)
+#endif
 #ifndef QP_XU_CEIL
 #define QP_XU_CEIL 5  // candidates of the K1 fast path whose ceil runs on the XU pipe (others: FADD2 magic; A/B: 0-5 equal, 7 +2 %)
 #endif
@@ -281,9 +284,16 @@ __device__ __forceinline__ void prof_cand16x2(const float* x, float mn, uint32_t
         float dv[4], ev[4];
 #pragma unroll
         for (int p = 0; p < 2; ++p) {
-          float w0, w1;
-          f2up(f2fma_rp(tp[p], f2pk(fw.invc, fw.invc), nu[p]), w0, w1);
-          const f2_t dec = f2fma(f2pk(ceilf(w0), ceilf(w1)), f2pk(fw.unitc, fw.unitc), f2pk(mn, mn));
+          const f2_t w = f2fma_rp(tp[p], f2pk(fw.invc, fw.invc), nu[p]);
+          f2_t q;
+          if (QF_MAGIC) {  // ceil on the FMA pipe (the conversion pipe carries the profile's ceils)
+            q = f2add(f2add_rp(w, f2pk(MAGIC, MAGIC)), f2pk(-MAGIC, -MAGIC));
+          } else {
+            float w0, w1;
+            f2up(w, w0, w1);
+            q = f2pk(ceilf(w0), ceilf(w1));
+          }
+          const f2_t dec = f2fma(q, f2pk(fw.unitc, fw.unitc), f2pk(mn, mn));
           f2up(dec, dv[2 * p], dv[2 * p + 1]);
           f2up(f2sub(xp[p], dec), ev[2 * p], ev[2 * p + 1]);
         }

@@ -18,6 +18,7 @@ LIB_PATH = os.environ.get("LGRECO_LIB") or os.path.join(_HERE, "liblgreco.so")  
 OK, EINVAL, ENONFINITE, EINFEASIBLE, ECUDA, ENCCL, ENOMEM, EUNSUPPORTED = 0, -1, -2, -3, -4, -5, -6, -7
 QSGD, TOPK, POWERSGD = 0, 1, 2
 PSGD_POWER, PSGD_SVD, PSGD_AUTO = 0, 1, 2  # PowerSGD profile method (NEXT-2 selector)
+SOLVE_NARROW = 8  # lgreco_solve flag: 8-CTA clusters (a solve running beside other work)
 PC_CONCURRENT = 1  # lgreco_profile_compress: may run beside the preceding kernel (include/lgreco.h)
 CHOICE_SKIP = -2  # (NEXT-4) a compressed layer another family's ctx owns: left untouched
 METRIC_SQ, DISC_FLOOR = 1, 2

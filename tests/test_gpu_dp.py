@@ -33,7 +33,7 @@ def _table(rng, L, K, zero_frac=0.0):
     return err, bits
 
 
-@pytest.mark.parametrize("flags", [0, 1, 2, 3, 4, 7])
+@pytest.mark.parametrize("flags", [0, 1, 2, 3, 4, 7, 8, 9])
 def test_random_tables(lg, ref, flags):
     """flags bit 2 (LGRECO_SOLVE_SINGLE_CTA) selects the one-CTA kernel, otherwise the
     8-CTA cluster kernel runs (K <= 16): both must reproduce the oracle exactly."""
@@ -54,8 +54,10 @@ def test_random_tables(lg, ref, flags):
         assert i_gpu.emax == i_ref.emax and i_gpu.total_err == i_ref.total_err
 
 
-@pytest.mark.parametrize("cfg,K", [("C4", 7), ("C3", 100), ("C5", 100), ("C5", 49)])
-def test_model_sized_tables(lg, ref, cfg, K):
+@pytest.mark.parametrize("cfg,K,flags", [("C4", 7, 0), ("C4", 7, 8), ("C3", 100, 0), ("C5", 100, 0), ("C5", 49, 0),
+                                         ("C5", 7, 8)])
+def test_model_sized_tables(lg, ref, cfg, K, flags):
+    """flags 8 = LGRECO_SOLVE_NARROW (8-CTA clusters, the pipelined bench's solve)."""
     layers = W.config_layers(cfg)
     L = len(layers)
     rng = np.random.default_rng(K + L)
@@ -63,7 +65,7 @@ def test_model_sized_tables(lg, ref, cfg, K):
     comp = np.array([l.compress for l in layers], np.int32)
     dflt = np.full(L, K // 3, np.int32)
     st, c_ref, i_ref = ref.solve(err, bits, dflt, comp, D=10000)
-    c_gpu, i_gpu = _run(lg, err, bits, dflt, comp, 10000, 0)
+    c_gpu, i_gpu = _run(lg, err, bits, dflt, comp, 10000, flags)
     assert list(c_gpu) == list(c_ref) and i_gpu.total_bits == i_ref.total_bits
     assert i_gpu.total_bits <= i_gpu.default_bits
 

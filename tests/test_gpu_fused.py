@@ -191,7 +191,8 @@ def test_pipelined_chain_matches_oracle(lg, ref, cfg, lag):
         err, bits = tabs[t % 2]
         ctx.profile_compress(use, gd, ed, out, t, err, bits, concurrent=(lag == 2 and t > 0))
         nxt = plans[(t + lag) % (lag + 1)]
-        lg.solve(err, bits, ddef, comp, choice=nxt, info=info, workspace=ws)
+        lg.solve(err, bits, ddef, comp, flags=lg.SOLVE_NARROW if lag == 2 else 0, choice=nxt, info=info,
+                 workspace=ws)
         outs.append((out.clone(), ed.clone()))
     torch.cuda.synchronize()
     ctx.check()
