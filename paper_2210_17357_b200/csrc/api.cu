@@ -45,6 +45,13 @@ static int qsgd_layout(const lgreco_ctx* c, const int32_t* choice, std::vector<l
   for (int l = 0; l < c->L; ++l) {
     const lgreco_layer& ly = c->layers[l];
     int bits = 0;
+    if (choice[l] == LGRECO_CHOICE_SKIP) {
+      // another family's layer (NEXT-4, R24): no records and no bytes in this ctx's payload
+      plan[l].pay_off = off;
+      plan[l].bits = -1;
+      plan[l].rec_bytes = 0;
+      continue;
+    }
     if (ly.compress) {
       const int ci = choice[l];
       if (ci < 0 || ci >= c->K) {
@@ -69,6 +76,7 @@ static int64_t rec_off(const lgreco_ctx* c, const std::vector<lg::DevPlan>& plan
   if (r >= c->R) return S;
   const int l = (int)(std::upper_bound(c->bucket0.begin(), c->bucket0.begin() + c->L, r) - c->bucket0.begin()) - 1;
   const int64_t jb = r - c->bucket0[l];
+  if (plan[l].bits < 0) return plan[l].pay_off;  // (a skipped layer has no bytes)
   return plan[l].pay_off + (plan[l].bits > 0 ? jb * (int64_t)plan[l].rec_bytes : jb * 4 * (int64_t)c->B);
 }
 
@@ -94,7 +102,7 @@ static void shard_bounds(const lgreco_ctx* c, const std::vector<lg::DevPlan>& pl
 static int set_plan(lgreco_ctx* c, const int32_t* choice, cudaStream_t st) {
   std::vector<int32_t> ch(choice, choice + c->L);
   for (int l = 0; l < c->L; ++l)
-    if (!c->layers[l].compress) ch[l] = -1;
+    if (!c->layers[l].compress && ch[l] != LGRECO_CHOICE_SKIP) ch[l] = -1;
   if (c->plan_valid && ch == c->plan_choice) return LGRECO_OK;
   std::vector<lg::DevPlan> plan;
   int64_t S = 0;

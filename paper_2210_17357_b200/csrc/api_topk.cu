@@ -171,6 +171,13 @@ static int topk_layout(lgreco_ctx* c, const int32_t* choice, std::vector<lg::TPl
   for (int l = 0; l < c->L; ++l) {
     const lgreco_layer& ly = c->layers[l];
     plan[l].pay_off = off;
+    if (choice[l] == LGRECO_CHOICE_SKIP) {
+      // another family's layer (NEXT-4, R24): no pairs, no bytes; k = -1 marks it for the
+      // combine, which leaves its output untouched
+      plan[l].k = -1;
+      if (ly.compress) kpre[ci + 1] = kpre[ci], kplan[ci++] = 0;
+      continue;
+    }
     if (ly.compress) {
       const int j = choice[l];
       if (j < 0 || j >= c->K) {

@@ -31,7 +31,7 @@ namespace lg {
 constexpr int QP_THREADS = 256;
 constexpr int QP_WARPS = QP_THREADS / 32;
 #ifndef QF_MAGIC
-#define QF_MAGIC 0  // fused pass: the planned candidate's ceil by the FADD2 magic (1) or FRND.CEIL (0)
+#define QF_MAGIC 1  // fused pass: the planned candidate's ceil by the FADD2 magic (1) or FRND.CEIL (0); A/B 96.5 -> 95.0 us per pipelined step (the XU pipe carries the profile's ceils)
 #endif
 #ifndef QP_XU_CEIL
 #define QP_XU_CEIL 5  // candidates of the K1 fast path whose ceil runs on the XU pipe (others: FADD2 magic; A/B: 0-5 equal, 7 +2 %)
@@ -1138,6 +1138,7 @@ k_qpack(const float* __restrict__ g, float* __restrict__ ef, uint8_t* __restrict
     pl = DevPlan{0, bits, 0};
   } else {
     pl = plan[ch.layer];
+    if (pl.bits < 0) return;  // another family's layer (NEXT-4): untouched, no records
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int M = B >> 7;
@@ -1249,6 +1250,7 @@ k_qunpack(const uint8_t* __restrict__ payload, float* __restrict__ out, const De
   const ProfChunk ch = chunks[blockIdx.x];
   const DevLayer ly = layers[ch.layer];
   const DevPlan pl = plan[ch.layer];
+  if (pl.bits < 0) return;  // another family's layer (NEXT-4): output untouched
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int M = B >> 7;
   const bool aligned = (ly.offset & 3) == 0;
@@ -1326,6 +1328,7 @@ k_qreduce(const uint8_t* __restrict__ recv, int64_t shard_bytes, int64_t byte0, 
     const int l = find_layer(sb0, L, gb);
     const DevLayer ly = layers[l];
     const DevPlan pl = plan[l];
+    if (pl.bits < 0) continue;  // another family's layer (NEXT-4): no records
     const int64_t jb = gb - ly.bucket0;
     const int64_t e0 = jb * (int64_t)B;
     if (pl.bits == 0) {
@@ -1626,12 +1629,14 @@ __global__ void k_plan_qsgd_layout(const int32_t* __restrict__ choice, const int
   __shared__ int64_t S_sh;
   for (int l = threadIdx.x; l < L; l += blockDim.x) {
     int bits = 0;
-    if (layers[l].compress) {
+    if (choice[l] == LGRECO_CHOICE_SKIP) {
+      bits = -1;  // another family's layer (NEXT-4): no records, no bytes (R24)
+    } else if (layers[l].compress) {
       int c = choice[l];
       if (c < 0 || c >= K) { atomicOr(flag, 2u); c = 0; }
       bits = params[c];
     }
-    const int32_t rb = bits > 0 ? 16 * bits * (B / 128) + 8 : 4 * B;
+    const int32_t rb = bits > 0 ? 16 * bits * (B / 128) + 8 : bits == 0 ? 4 * B : 0;
     plan[l] = DevPlan{0, bits, rb};
   }
   __syncthreads();
@@ -1640,6 +1645,7 @@ __global__ void k_plan_qsgd_layout(const int32_t* __restrict__ choice, const int
     for (int l = 0; l < L; ++l) {
       const int64_t nb = bucket0[l + 1] - bucket0[l];
       plan[l].pay_off = off;
+      if (plan[l].bits < 0) continue;
       off += plan[l].bits > 0 ? nb * (int64_t)plan[l].rec_bytes : 4 * layers[l].numel;
       off = (off + 15) & ~(int64_t)15;
     }
@@ -1657,7 +1663,7 @@ __global__ void k_plan_qsgd_layout(const int32_t* __restrict__ choice, const int
     }
     const DevPlan pl = plan[lo];
     const int64_t jb = r - bucket0[lo];
-    return pl.pay_off + (pl.bits > 0 ? jb * (int64_t)pl.rec_bytes : jb * 4 * (int64_t)B);
+    return pl.pay_off + (pl.bits > 0 ? jb * (int64_t)pl.rec_bytes : pl.bits == 0 ? jb * 4 * (int64_t)B : 0);
   };
   const int j = threadIdx.x;
   if (j <= W) {

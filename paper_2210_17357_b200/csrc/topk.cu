@@ -667,6 +667,7 @@ k_tk_combine_init(const uint8_t* __restrict__ gathered, int64_t S, int W, float*
                   const DevLayer* __restrict__ layers, const TChunk* __restrict__ chunks,
                   const TPlan* __restrict__ tplan) {
   const TChunk ch = chunks[blockIdx.x];  // chunks over ALL layers, cidx = layer
+  if (tplan[ch.cidx].k < 0) return;  // another family's layer (NEXT-4): output untouched
   const DevLayer ly = layers[ch.cidx];
   const float invW = __fdiv_rn(1.0f, (float)W);
   for (int64_t i = ch.first + threadIdx.x; i < ch.first + ch.n; i += TK_THREADS) {

@@ -7,8 +7,9 @@ the same layer table; every step of the path runs in the library:
   solve     Algorithm 1 on the joint table picks a (family, parameter) per layer
   split     lgreco_hybrid_split -> one choice vector per family (CHOICE_SKIP elsewhere)
   compress  each family's lgreco_compress_allreduce_dev compresses its own layers and
-            leaves the others' EF / output untouched (W = 1 device paths for QSGD and
-            TopK; PowerSGD through its host plan at any W)
+            leaves the others' EF / output untouched, at any W: a CHOICE_SKIP layer has no
+            QSGD records and no TopK pairs in its ctx's exchange (R24); PowerSGD
+            through its host plan
 
 This module is orchestration only (which call when); the defaults of the joint table
 are the column of one family's default (`default_family`, `default_idx`).
