@@ -770,19 +770,20 @@ k_qprofile_q(const float* __restrict__ g, const float* e, const QInfo* __restric
         }
       } else {
         // masked direct loads: element 32i + 4*l8 + s of bucket grp of the quad
-        const int base = grp * 128 + 4 * l8;
-        const float* gl = g + ic.elem0;
-        const float* el = e ? e + ic.elem0 : nullptr;
+        // (offsets against lim = nvalid - lane base: immediate compares, nothing to hoist
+        // into the regular quads' path)
+        const int lim = nvalid - (grp * 128 + 4 * l8);
+        const float* gl = g + ic.elem0 + grp * 128 + 4 * l8;
+        const float* el = e ? e + ic.elem0 + grp * 128 + 4 * l8 : nullptr;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
 #pragma unroll
           for (int s2 = 0; s2 < 4; ++s2) {
-            const int idx = base + 32 * i + s2;
-            const bool ok = idx < nvalid;
+            const bool ok = 32 * i + s2 < lim;
             float v = 0.f;
             if (ok) {
-              v = __ldg(gl + idx);
-              if (el) v = __fadd_rn(v, FUSE ? el[idx] : __ldg(el + idx));
+              v = __ldg(gl + 32 * i + s2);
+              if (el) v = __fadd_rn(v, FUSE ? el[32 * i + s2] : __ldg(el + 32 * i + s2));
               if (FUSE) v = __fadd_rn(v, 0.f);
             }
             x[4 * i + s2] = v;
@@ -801,10 +802,10 @@ k_qprofile_q(const float* __restrict__ g, const float* e, const QInfo* __restric
         for (int s2 = 2; s2 < 16; s2 += 2) { mn = fmin3_nan(mn, x[s2], x[s2 + 1]); mx = fmax3_nan(mx, x[s2], x[s2 + 1]); }
       } else {
         mn = INFINITY; mx = -INFINITY;
+        const int lim = nvalid - (grp * 128 + 4 * l8);
 #pragma unroll
         for (int s2 = 0; s2 < 16; ++s2) {
-          const int idx = grp * 128 + 4 * l8 + 32 * (s2 >> 2) + (s2 & 3);
-          if (idx < nvalid) { mn = fmin_nan(mn, x[s2]); mx = fmax_nan(mx, x[s2]); }
+          if (32 * (s2 >> 2) + (s2 & 3) < lim) { mn = fmin_nan(mn, x[s2]); mx = fmax_nan(mx, x[s2]); }
         }
       }
 #pragma unroll
@@ -813,10 +814,10 @@ k_qprofile_q(const float* __restrict__ g, const float* e, const QInfo* __restric
         mx = fmax_nan(mx, __shfl_xor_sync(LG_FULL, mx, o));
       }
       if (!cur_regular) {
+        const int lim = nvalid - (grp * 128 + 4 * l8);
 #pragma unroll
         for (int s2 = 0; s2 < 16; ++s2) {
-          const int idx = grp * 128 + 4 * l8 + 32 * (s2 >> 2) + (s2 & 3);
-          if (!(idx < nvalid)) x[s2] = mn;  // invalid -> t = 0, q = 0, d = 0
+          if (!(32 * (s2 >> 2) + (s2 & 3) < lim)) x[s2] = mn;  // invalid -> t = 0, q = 0, d = 0
         }
       }
       float my_inv, my_unit, my_inv2 = 0.f, my_unit2 = 0.f;

@@ -77,7 +77,7 @@ def _worker(rank, world, port, fam, mode, q):
         layers = _mat_layers() if fam == "psgd" else _vec_layers()
         family, params = {"qsgd": (lgreco.QSGD, W.QSGD_BITS), "topk": (lgreco.TOPK, PPM),
                           "psgd": (lgreco.POWERSGD, RANKS)}[fam]
-        if mode == "p2p":
+        if mode.startswith("p2p"):
             ctx = lgreco.Context(layers, family, params, seed=SEED, rank=rank, world=world)
             blobs = [None] * world
             dist.all_gather_object(blobs, ctx.p2p_export())
@@ -98,13 +98,21 @@ def _worker(rank, world, port, fam, mode, q):
             prop = [((step + 2 * rank + li) % len(params)) if l.compress else -1 for li, l in enumerate(layers)]
             d_choice = torch.tensor(prop, dtype=torch.int32, device=dev)
             ctx.plan_broadcast(d_choice)
-            if fam == "qsgd":
+            errn = None
+            if fam == "qsgd" and mode.endswith("_pc"):
+                # the pipelined schedule's per-step call: profile of this rank's x + the
+                # compressed exchange with the plan in force
+                err = torch.empty(len(layers), len(params), dtype=torch.float64, device=dev)
+                bits = torch.empty(len(layers), len(params), dtype=torch.int64, device=dev)
+                ctx.profile_compress(d_choice, gd, ed, out, step, err, bits)
+                errn = err.cpu().numpy()
+            elif fam == "qsgd":
                 ctx.compress_allreduce_dev(d_choice, gd, ed, out, step)
             else:
                 ctx.compress_allreduce(d_choice.cpu().tolist(), gd, ed, out, step)
             torch.cuda.synchronize(dev)
             ctx.check()
-            res.append((d_choice.cpu().numpy(), out.cpu().numpy(), ed.cpu().numpy()))
+            res.append((d_choice.cpu().numpy(), out.cpu().numpy(), ed.cpu().numpy(), errn))
         ctx.close()
         q.put((rank, res, None))
     except Exception as ex:  # reported to the parent
@@ -137,10 +145,12 @@ def _worlds(mode="nccl"):
     return [w for w in (2, 4, 8) if w <= n]
 
 
-@pytest.mark.parametrize("mode", ["p2p", "nccl"])
+@pytest.mark.parametrize("mode", ["p2p", "nccl", "p2p_pc"])
 @pytest.mark.parametrize("world", [2, 4, 8])
 def test_qsgd_exchange_multi_gpu(ref, world, mode):
-    if world not in _worlds(mode):
+    """mode p2p_pc: the per-step call of the pipelined schedule (lgreco_profile_compress)
+    -- every rank's profile of its own x as well (rankfield = rank, R3)."""
+    if world not in _worlds(mode.replace("_pc", "")):
         pytest.skip(f"needs {world} GPUs")
     got = _run(world, "qsgd", mode)
     layers = _vec_layers()
@@ -149,9 +159,15 @@ def test_qsgd_exchange_multi_gpu(ref, world, mode):
         plan0 = [((step + li) % len(W.QSGD_BITS)) if l.compress else -1 for li, l in enumerate(layers)]
         gs = [_inputs("qsgd", layers, w, step)[0] for w in range(world)]
         lbits = [W.QSGD_BITS[c] if c >= 0 else 0 for c in plan0]
+        if mode.endswith("_pc"):
+            for w in range(world):
+                rerr, _ = ref.qsgd_profile(layers, gs[w], es[w], W.QSGD_BITS, seed=SEED, rank=w, step=step)
+                gerr = got[w][step][3]
+                assert np.all((rerr == 0) == (gerr == 0))
+                assert (np.abs(gerr - rerr) / np.maximum(rerr, 1e-300)).max() <= 1e-5, (w, step)
         out_ref, es, _, _ = ref.qsgd_allreduce(layers, lbits, gs, es, seed=SEED, step=step)
         for w in range(world):
-            choice, out, ef = got[w][step]
+            choice, out, ef, _ = got[w][step]
             assert list(choice) == plan0
             assert np.array_equal(out.view(np.uint32), out_ref.view(np.uint32)), (w, step)
             assert np.array_equal(ef.view(np.uint32), es[w].view(np.uint32)), (w, step)
@@ -170,7 +186,7 @@ def test_topk_exchange_multi_gpu(ref, world):
         lppm = [PPM[c] if c >= 0 else 0 for c in plan0]
         out_ref, es, _ = ref.topk_allreduce(layers, lppm, gs, es)
         for w in range(world):
-            choice, out, ef = got[w][step]
+            choice, out, ef, _ = got[w][step]
             assert list(choice) == plan0
             assert np.array_equal(out.view(np.uint32), out_ref.view(np.uint32)), (w, step)
             assert np.array_equal(ef.view(np.uint32), es[w].view(np.uint32)), (w, step)
@@ -202,7 +218,7 @@ def test_psgd_exchange_multi_gpu(ref, world):
         gs = [_inputs("psgd", layers, w, step)[0] for w in range(world)]
         out_ref, es, _ = ref.psgd_allreduce(layers, lrank, gs, es, Qs)
         for w in range(world):
-            choice, out, ef = got[w][step]
+            choice, out, ef, _ = got[w][step]
             assert list(choice) == plan0
             for l, ly in enumerate(layers):
                 sl = slice(ly.offset, ly.offset + ly.numel)
