@@ -177,6 +177,10 @@ size_t lgreco_solve_workspace_bytes(int32_t L, int32_t K, int32_t D);
  * d_err/d_bits L*K (from lgreco_profile or any table), d_default_idx L,
  * d_compress L (nullable: all active), d_choice L (out; -1 for inactive layers),
  * d_info (out), d_workspace of lgreco_solve_workspace_bytes(L,K,D) bytes.
+ * Host mode: when d_err, d_bits, d_default_idx, d_compress (if given), d_choice and d_info
+ * are all HOST pointers, they are staged through device scratch around the same kernels
+ * (d_workspace ignored, may be NULL) and the call returns after the plan and the info are
+ * back on the host (stream-synchronous); mixing host and device pointers is EINVAL.
  * Cluster (or single-CTA) DP on `stream`, launched after ALL prior work of the stream has
  * completed (no programmatic overlap on its start); it lets its successor be scheduled
  * once it runs (a compress reading d_choice still waits for it); no host synchronisation. */
@@ -234,9 +238,12 @@ int lgreco_compress_allreduce_dev(lgreco_ctx* ctx, const int32_t* d_choice, cons
  *   lgreco_compress_allreduce_dev(ctx, d_choice, d_g, d_ef, d_out, step, stream);
  * i.e. d_err / d_bits profile x = d_g + d_ef (the EF as it was on entry) and d_choice
  * (DEVICE, L) compresses the same x (d_ef <- x - decompress(x), d_out <- the mean).  For a
- * QSGD ctx with world == 1 and B = 128 this is ONE pass over d_g and d_ef (kernel K1 with
- * the compress of K5 fused: the planned candidate's code comes from the same registers
- * and Philox uniforms, then K1b), otherwise the two calls.  d_choice must not alias the
+ * QSGD ctx with B = 128 this is ONE pass over d_g and d_ef (kernel K1 with the compress of
+ * K5 fused: the planned candidate's code comes from the same registers and Philox
+ * uniforms, then K1b) -- at world == 1 writing the decoded output, at world > 1 over peer
+ * memory (lgreco_p2p_open / _set_peers) storing the stage-1 records straight into their
+ * owners' windows, followed by the peer-memory exchange of lgreco_compress_allreduce_dev;
+ * otherwise (NCCL exchange, B > 128, other families) the two calls.  d_choice must not alias the
  * output of a solve that reads d_err.  flags: LGRECO_PC_CONCURRENT -- the caller asserts
  * that the kernel enqueued immediately before this call on `stream` (typically the
  * lgreco_solve of the previous step, writing a plan other than d_choice) produces nothing

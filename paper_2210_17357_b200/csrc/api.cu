@@ -454,11 +454,65 @@ size_t lgreco_solve_workspace_bytes(int32_t L, int32_t K, int32_t D) {
   return lg::solve_workspace_bytes(L, K, D);
 }
 
+static bool host_ptr(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeUnregistered;
+}
+
+// Host mode of lgreco_solve: the tables and outputs in host memory are staged through
+// device scratch around the same kernels, and the call returns after the results are back.
+static int solve_host(const double* h_err, const int64_t* h_bits, int32_t L, int32_t K, const int32_t* h_def,
+                      const int32_t* h_comp, int32_t D, uint32_t flags, int32_t* h_choice, lgreco_solve_info* h_info,
+                      cudaStream_t st) {
+  const size_t ws = lg::solve_workspace_bytes(L, K, D);
+  const size_t n = (size_t)L * K;
+  const size_t bytes = n * 8 * 2 + (size_t)L * 4 * 3 + sizeof(lgreco_solve_info) + 64 + ws + 256;
+  uint8_t* d = nullptr;
+  if (cudaMallocAsync((void**)&d, bytes, st) != cudaSuccess) { lg_set_error("solve host mode: allocation"); return LGRECO_ENOMEM; }
+  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  uint8_t* q = d;
+  double* e = reinterpret_cast<double*>(q); q += al(n * 8);
+  int64_t* b = reinterpret_cast<int64_t*>(q); q += al(n * 8);
+  int32_t* df = reinterpret_cast<int32_t*>(q); q += al((size_t)L * 4);
+  int32_t* cp = h_comp ? reinterpret_cast<int32_t*>(q) : nullptr; q += al((size_t)L * 4);
+  int32_t* ch = reinterpret_cast<int32_t*>(q); q += al((size_t)L * 4);
+  lgreco_solve_info* inf = reinterpret_cast<lgreco_solve_info*>(q); q += al(sizeof(lgreco_solve_info));
+  cudaError_t ce = cudaSuccess;
+  if (ce == cudaSuccess) ce = cudaMemcpyAsync(e, h_err, n * 8, cudaMemcpyHostToDevice, st);
+  if (ce == cudaSuccess) ce = cudaMemcpyAsync(b, h_bits, n * 8, cudaMemcpyHostToDevice, st);
+  if (ce == cudaSuccess) ce = cudaMemcpyAsync(df, h_def, (size_t)L * 4, cudaMemcpyHostToDevice, st);
+  if (ce == cudaSuccess && cp) ce = cudaMemcpyAsync(cp, h_comp, (size_t)L * 4, cudaMemcpyHostToDevice, st);
+  lg::SolveArgs a{e, b, L, K, df, cp, D, flags, ch, inf, nullptr, nullptr};
+  if (ce == cudaSuccess) ce = lg::launch_solve(a, q, st);
+  if (ce == cudaSuccess) ce = cudaMemcpyAsync(h_choice, ch, (size_t)L * 4, cudaMemcpyDeviceToHost, st);
+  if (ce == cudaSuccess) ce = cudaMemcpyAsync(h_info, inf, sizeof(lgreco_solve_info), cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(d, st);
+  if (ce == cudaSuccess) ce = cudaStreamSynchronize(st);
+  if (ce != cudaSuccess) { lg_set_error("solve host mode: %s", cudaGetErrorString(ce)); return LGRECO_ECUDA; }
+  return LGRECO_OK;
+}
+
 int lgreco_solve(const double* d_err, const int64_t* d_bits, int32_t L, int32_t K, const int32_t* d_default_idx,
                  const int32_t* d_compress, int32_t D, uint32_t flags, int32_t* d_choice, lgreco_solve_info* d_info,
                  void* d_ws, size_t ws_bytes, void* stream) {
   if (L <= 0 || K <= 0 || K > 255 || D <= 0) { lg_set_error("bad L/K/D %d/%d/%d", L, K, D); return LGRECO_EINVAL; }
-  if (!d_err || !d_bits || !d_default_idx || !d_choice || !d_info || !d_ws) { lg_set_error("null argument"); return LGRECO_EINVAL; }
+  if (!d_err || !d_bits || !d_default_idx || !d_choice || !d_info) { lg_set_error("null argument"); return LGRECO_EINVAL; }
+  {
+    const bool h[5] = {host_ptr(d_err), host_ptr(d_bits), host_ptr(d_default_idx), host_ptr(d_choice), host_ptr(d_info)};
+    const bool hc = d_compress ? host_ptr(d_compress) : h[0];
+    if (h[0] || h[1] || h[2] || h[3] || h[4] || hc) {
+      if (!(h[0] && h[1] && h[2] && h[3] && h[4] && hc)) {
+        lg_set_error("solve: tables and outputs must be all host or all device pointers");
+        return LGRECO_EINVAL;
+      }
+      return solve_host(d_err, d_bits, L, K, d_default_idx, d_compress, D, flags, d_choice, d_info, (cudaStream_t)stream);
+    }
+  }
+  if (!d_ws) { lg_set_error("null workspace (device mode)"); return LGRECO_EINVAL; }
   if (ws_bytes < lg::solve_workspace_bytes(L, K, D)) { lg_set_error("workspace too small"); return LGRECO_EINVAL; }
   lg::SolveArgs a{d_err, d_bits, L, K, d_default_idx, d_compress, D, flags, d_choice, d_info, nullptr, nullptr};
   cudaError_t e = lg::launch_solve(a, d_ws, (cudaStream_t)stream);
@@ -605,6 +659,7 @@ int lgreco_p2p_set_peers(lgreco_ctx* c, void* const* h_recv, void* const* h_stag
   // the pointers are needed before the first exchange (plan_broadcast); the shard bounds
   // are refreshed with every plan
   LG_CUDA(cudaMemcpy(c->d_p2p, &c->h_p2p, sizeof(lg::P2PDev), cudaMemcpyHostToDevice));
+  LG_CUDA(lg::preload_p2p_kernels());  // no lazy module load while a peer waits (qsgd.cu)
   c->p2p = true;
   c->plan_valid = false;  // re-upload the descriptor with the next plan
   return LGRECO_OK;
@@ -750,7 +805,8 @@ int lgreco_profile_compress(lgreco_ctx* c, const int32_t* d_choice, const float*
   if (flags & ~(uint32_t)LGRECO_PC_CONCURRENT) { lg_set_error("profile_compress: unknown flags 0x%x", flags); return LGRECO_EINVAL; }
   LG_TRY(check_align16("profile_compress", d_g, d_ef, d_out));
   cudaStream_t st = (cudaStream_t)stream;
-  const bool fused = c->family == LGRECO_QSGD && c->world == 1 && c->B == 128 && c->nqchunks > 0;
+  const bool p2p_fused = c->family == LGRECO_QSGD && c->world > 1 && c->p2p && c->B == 128 && c->nqchunks > 0;
+  const bool fused = (c->family == LGRECO_QSGD && c->world == 1 && c->B == 128 && c->nqchunks > 0) || p2p_fused;
   if (!fused) {
     LG_TRY(lgreco_profile(c, d_g, d_ef, step, d_err, d_bits, stream));
     return lgreco_compress_allreduce_dev(c, d_choice, d_g, d_ef, d_out, step, stream);
@@ -767,6 +823,18 @@ int lgreco_profile_compress(lgreco_ctx* c, const int32_t* d_choice, const float*
   const bool conc = (flags & LGRECO_PC_CONCURRENT) != 0;
   lg::QFuse fz{d_ef, d_out, d_choice, c->d_flag, c->d_chunks_raw, c->nchunks_raw, c->d_layers, c->B, conc ? 1 : 0,
                  c->L};
+  if (p2p_fused) {
+    // W > 1 over peer memory: the plan laid out on the device (payload offsets, shard
+    // bounds), then the fused pass stores every stage-1 record straight into its owner's
+    // window -- the rest is compress_allreduce_dev's peer-memory step (R13)
+    LG_CUDA(lg::launch_plan_qsgd_layout(d_choice, c->d_params, c->K, c->d_layers, c->d_bucket0, c->L, c->R, c->B,
+                                        c->d_plan, c->d_p2p, c->d_flag, st));
+    c->plan_valid = false;  // d_plan / d_p2p now hold a device-chosen plan
+    ++c->epoch;
+    fz.plan = c->d_plan;
+    fz.p2p = c->d_p2p;
+    fz.nowait = 0;  // (the layout kernel precedes it)
+  }
   a.fuse = &fz;
   if (c->timing) {
     cudaEvent_t e0, e1;
@@ -778,6 +846,24 @@ int lgreco_profile_compress(lgreco_ctx* c, const int32_t* d_choice, const float*
   }
   LG_LAUNCH(c, lg::launch_qprofile(a, st));
   c->launches += 2;
+  if (p2p_fused) {
+    const int W = c->world, me = c->rank;
+    LG_CUDA(lg::launch_p2p_signal(c->d_p2p, 0, c->epoch, st));
+    LG_CUDA(lg::launch_p2p_wait(c->d_flags, W, me, 0, c->epoch, st));
+    int nsm = 148, dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    lg::QReduceArgs r{c->d_recv, 0, 0, c->d_pay2, c->d_layers, c->d_plan, c->d_bucket0, c->L, 0, 0, c->B, W, k0, k1,
+                      (uint32_t)step};
+    r.p2p = c->d_p2p;
+    r.device_bounds = 1;
+    r.grid = nsm * 4;
+    LG_LAUNCH(c, lg::launch_qreduce(r, st));
+    LG_CUDA(lg::launch_p2p_signal(c->d_p2p, 1, c->epoch, st));
+    LG_CUDA(lg::launch_p2p_wait(c->d_flags, W, me, 1, c->epoch, st));
+    lg::QUnpackArgs u{c->d_pay2, d_out, c->d_layers, c->d_plan, c->d_chunks_all, c->nchunks_all, c->B};
+    LG_LAUNCH(c, lg::launch_qunpack(u, st));
+    c->launches += 7;
+  }
   return LGRECO_OK;
 }
 

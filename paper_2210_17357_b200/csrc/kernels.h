@@ -28,6 +28,7 @@ constexpr int QI_MAX_LAYERS = 1 << 22;
 struct QSeg { int32_t layer, row0, nrows, pad; };
   // s_j = 2^{b_j} - 1, passed by value (constant bank)
 
+struct P2PDev;
 // Fused profile + compress (lgreco_profile_compress, W = 1): besides the profile's
 // partial rows, K1 quantises every quad with the layer's planned candidate and writes
 // the decoded output and the new EF (K5's arithmetic), and its first warps handle the
@@ -41,6 +42,10 @@ struct QFuse {
   const DevLayer* layers; int B;
   int nowait;                // 1: no griddepcontrol.wait (LGRECO_PC_CONCURRENT)
   int L;                     // layers (the first QF_LCACHE plan entries are staged in shared memory)
+  // W > 1 (peer-memory exchange): stage-1 records (R7) stored into the owners' windows
+  // instead of the decoded output; `plan` is the device layout of `choice`
+  const DevPlan* plan = nullptr;
+  const P2PDev* p2p = nullptr;
 };
 constexpr int QF_LCACHE = 4096;
 // K1's ticket words (64 apart): [0, 16) the parts' quad tickets, then the finish counter
@@ -101,6 +106,7 @@ struct QReduceArgs {
 };
 
 cudaError_t launch_qprofile(const QProfileArgs& a, cudaStream_t st);
+cudaError_t preload_p2p_kernels();
 cudaError_t launch_qpack(const QPackArgs& a, cudaStream_t st);
 cudaError_t launch_qunpack(const QUnpackArgs& a, cudaStream_t st);
 cudaError_t launch_qreduce(const QReduceArgs& a, cudaStream_t st);

@@ -241,11 +241,15 @@ struct FuseW {
   bool wr;            // write at all (valid bucket, layer not skipped)
 };
 
-template <int KT, bool SCALED, bool FUSE = false>
+// FUSE: 0 profile only, 1 + compress with the decoded output (W = 1), 2 + compress
+// keeping the codes for the stage-1 records (W > 1; codes[i] = the lane's 4 codes of
+// sub-block i, one per byte)
+template <int KT, bool SCALED, int FUSE = 0>
 __device__ __forceinline__ void prof_cand16x2(const float* x, float mn, uint32_t c0, uint32_t rankfield, uint32_t step,
                                               const PhiloxRK& rk, const float* inv, const float* unit,
                                               const CandS& cs, float S, float* acc, const FuseW& fw = FuseW{},
-                                              float* __restrict__ out = nullptr, float* __restrict__ ef = nullptr) {
+                                              float* __restrict__ out = nullptr, float* __restrict__ ef = nullptr,
+                                              uint32_t* codes = nullptr) {
   constexpr float MAGIC = 8388609.0f;  // 2^23 + 1
   constexpr float NEG_2M24 = -5.9604644775390625e-08f;
   f2_t a2[KT];
@@ -279,15 +283,23 @@ __device__ __forceinline__ void prof_cand16x2(const float* x, float mn, uint32_t
         a2[j] = f2fma(d, d, a2[j]);
       }
     }
-    if constexpr (FUSE) {
+    if constexpr (FUSE != 0) {
       if (fw.wr) {
         float dv[4], ev[4];
+        uint32_t cw = 0;
 #pragma unroll
         for (int p = 0; p < 2; ++p) {
           const f2_t w = f2fma_rp(tp[p], f2pk(fw.invc, fw.invc), nu[p]);
           f2_t q;
-          if (QF_MAGIC) {  // ceil on the FMA pipe (the conversion pipe carries the profile's ceils)
-            q = f2add(f2add_rp(w, f2pk(MAGIC, MAGIC)), f2pk(-MAGIC, -MAGIC));
+          if (QF_MAGIC || FUSE == 2) {  // ceil on the FMA pipe (the conversion pipe carries the profile's ceils)
+            const f2_t y = f2add_rp(w, f2pk(MAGIC, MAGIC));  // = ceil(w) + 2^23 + 1, exact
+            q = f2add(y, f2pk(-MAGIC, -MAGIC));
+            if (FUSE == 2) {  // the code as an integer: y's mantissa = ceil(w) + 1 (w > -1)
+              float y0, y1;
+              f2up(y, y0, y1);
+              cw |= ((__float_as_uint(y0) & 0x7fffffu) - 1u) << (16 * p);
+              cw |= ((__float_as_uint(y1) & 0x7fffffu) - 1u) << (16 * p + 8);
+            }
           } else {
             float w0, w1;
             f2up(w, w0, w1);
@@ -299,12 +311,21 @@ __device__ __forceinline__ void prof_cand16x2(const float* x, float mn, uint32_t
         }
         const int64_t o = fw.ebase + 32 * i;
         if (fw.vec) {
-          *reinterpret_cast<float4*>(out + o) = make_float4(dv[0], dv[1], dv[2], dv[3]);
+          if (FUSE == 1) *reinterpret_cast<float4*>(out + o) = make_float4(dv[0], dv[1], dv[2], dv[3]);
           *reinterpret_cast<float4*>(ef + o) = make_float4(ev[0], ev[1], ev[2], ev[3]);
         } else {
 #pragma unroll
           for (int s2 = 0; s2 < 4; ++s2)
-            if (32 * i + s2 < fw.lim) { out[o + s2] = dv[s2]; ef[o + s2] = ev[s2]; }
+            if (32 * i + s2 < fw.lim) {
+              if (FUSE == 1) out[o + s2] = dv[s2];
+              ef[o + s2] = ev[s2];
+            }
+        }
+        if (FUSE == 2) {  // codes beyond the layer's end are 0 (x = mn there: t = 0)
+#pragma unroll
+          for (int s2 = 0; s2 < 4; ++s2)
+            if (!(32 * i + s2 < fw.lim)) cw &= ~(0xffu << (8 * s2));
+          codes[i] = cw;
         }
       }
     }
@@ -579,7 +600,17 @@ constexpr int Q1_THREADS = 32 * Q1_WARPS;
 #ifndef Q1F_MINB
 #define Q1F_MINB 2  // resident CTAs per SM of the fused profile + compress kernel (128 registers, no spills: A/B 112.9 -> 86.4 us at 3 CTAs / 80 registers)
 #endif
-template <int KT, bool FUSE>
+// Stage-1 destination of the payload byte at flat offset b: the local payload, or (peer
+// exchange) the owner's receive window, slot `me` (owner o's window holds W slots of its
+// shard size, R13) -- records never straddle a shard bound.
+__device__ __forceinline__ uint8_t* stage1_dst(uint8_t* payload, const P2PDev* __restrict__ p2p, int64_t b) {
+  if (!p2p) return payload + b;
+  int o = 0;
+  while (o + 1 < p2p->W && b >= p2p->bb[o + 1]) ++o;
+  return p2p->recv[o] + (int64_t)p2p->me * (p2p->bb[o + 1] - p2p->bb[o]) + (b - p2p->bb[o]);
+}
+
+template <int KT, int FUSE>
 __global__ void __launch_bounds__(Q1_THREADS, FUSE ? Q1F_MINB : Q1_MINB)
 k_qprofile_q(const float* __restrict__ g, const float* e, const QInfo* __restrict__ qinfo, int nqc,
              unsigned* __restrict__ ticket, const CandS cs, int K, const PhiloxRK rk, uint32_t rankfield,
@@ -668,7 +699,8 @@ k_qprofile_q(const float* __restrict__ g, const float* e, const QInfo* __restric
       for (int64_t i = i_beg + lane; i < i_end; i += 32) {
         const float xv = canon(__ldg(g + ly.offset + i), e ? e[ly.offset + i] : 0.f);
         bad = __fadd_rn(bad, __fmul_rn(xv, 0.f));
-        fz.out[ly.offset + i] = xv;
+        if (FUSE == 1) fz.out[ly.offset + i] = xv;
+        else *reinterpret_cast<float*>(stage1_dst(nullptr, fz.p2p, fz.plan[ch.layer].pay_off + 4 * i)) = xv;  // raw record
         if (fz.ef) fz.ef[ly.offset + i] = 0.f;
       }
     }
@@ -850,10 +882,38 @@ k_qprofile_q(const float* __restrict__ g, const float* e, const QInfo* __restric
         fw.vec = cur_regular;
         fw.wr = wr;
         if (valid) bad = __fadd_rn(bad, __fmul_rn(__fsub_rn(mx, mn), 0.f));
+        uint32_t codes[4] = {0u, 0u, 0u, 0u};
         if (__any_sync(LG_FULL, small))
-          prof_cand16x2<KT, true, true>(x, mn, c0, rankfield, step, rk, inv, unit, cs, S, a2, fw, fz.out, fz.ef);
+          prof_cand16x2<KT, true, FUSE>(x, mn, c0, rankfield, step, rk, inv, unit, cs, S, a2, fw, fz.out, fz.ef, codes);
         else
-          prof_cand16x2<KT, false, true>(x, mn, c0, rankfield, step, rk, inv, unit, cs, 1.f, a2, fw, fz.out, fz.ef);
+          prof_cand16x2<KT, false, FUSE>(x, mn, c0, rankfield, step, rk, inv, unit, cs, 1.f, a2, fw, fz.out, fz.ef,
+                                         codes);
+        if constexpr (FUSE == 2) {
+          // W > 1: the stage-1 record of bucket grp (R7) straight into its owner's window.
+          // Word (p, s) holds bit p of the code of element 4l + s in bit l = 8i + l8 (lane
+          // (grp, l8), sub-block i): four warp ballots per (p, s), byte grp of each.
+          if (__any_sync(LG_FULL, wr)) {
+            const int lay = qi_layer(ic);
+            const DevPlan pl = fz.plan[lay];
+            const int64_t jb = (ic.elem0 - fz.layers[lay].offset) / 128 + grp;
+            uint32_t* rec = reinterpret_cast<uint32_t*>(
+                stage1_dst(nullptr, fz.p2p, pl.pay_off + jb * (int64_t)pl.rec_bytes));
+            const uint32_t sel = (uint32_t)grp | ((4u + (uint32_t)grp) << 4);
+            for (int p = 0; p < pl.bits; ++p) {
+#pragma unroll
+              for (int s2 = 0; s2 < 4; ++s2) {
+                const int sh = 8 * s2 + p;
+                const uint32_t b0 = __ballot_sync(LG_FULL, (codes[0] >> sh) & 1u);
+                const uint32_t b1 = __ballot_sync(LG_FULL, (codes[1] >> sh) & 1u);
+                const uint32_t b2 = __ballot_sync(LG_FULL, (codes[2] >> sh) & 1u);
+                const uint32_t b3 = __ballot_sync(LG_FULL, (codes[3] >> sh) & 1u);
+                const uint32_t word = __byte_perm(__byte_perm(b0, b1, sel), __byte_perm(b2, b3, sel), 0x5410);
+                if (wr && l8 == ((4 * p + s2) & 7)) rec[4 * p + s2] = word;
+              }
+            }
+            if (wr && l8 == 0) *reinterpret_cast<float2*>(rec + 4 * pl.bits) = make_float2(mn, fw.unitc);
+          }
+        }
       } else {
 #if QP_F32X2
       if (__any_sync(LG_FULL, small)) prof_cand16x2<KT, true>(x, mn, c0, rankfield, step, rk, inv, unit, cs, S, a2);
@@ -1092,15 +1152,6 @@ __device__ __forceinline__ void pack_bucket_fast(const X4& xs, int b, int64_t gb
   if (dec_out) *reinterpret_cast<float4*>(dec_out + base) = make_float4(dec[0], dec[1], dec[2], dec[3]);
 }
 
-// Stage-1 destination of the payload byte at flat offset b: the local payload, or (peer
-// exchange) the owner's receive window, slot `me` (owner o's window holds W slots of its
-// shard size, R13) -- records never straddle a shard bound.
-__device__ __forceinline__ uint8_t* stage1_dst(uint8_t* payload, const P2PDev* __restrict__ p2p, int64_t b) {
-  if (!p2p) return payload + b;
-  int o = 0;
-  while (o + 1 < p2p->W && b >= p2p->bb[o + 1]) ++o;
-  return p2p->recv[o] + (int64_t)p2p->me * (p2p->bb[o + 1] - p2p->bb[o]) + (b - p2p->bb[o]);
-}
 
 __global__ void __launch_bounds__(QP_THREADS)
 k_qpack(const float* __restrict__ g, float* __restrict__ ef, uint8_t* __restrict__ payload,
@@ -1459,7 +1510,7 @@ cudaError_t launch_qprofile(const QProfileArgs& a, cudaStream_t st) {
                                       a.step, a.ptr_aligned, a.partial, fz);                                     \
     if (e2 != cudaSuccess) return e2;                                                                            \
   }
-#define LG_QQ(KT) { if (a.fuse) LG_QQ2(KT, true) else LG_QQ2(KT, false) }
+#define LG_QQ(KT) { if (a.fuse && a.fuse->p2p) LG_QQ2(KT, 2) else if (a.fuse) LG_QQ2(KT, 1) else LG_QQ2(KT, 0) }
       const QFuse fz = a.fuse ? *a.fuse : QFuse{};
       switch (a.K) {
         case 4: LG_QQ(4); break;
@@ -1690,6 +1741,28 @@ cudaError_t launch_plan_qsgd_layout(const int32_t* choice, const int32_t* params
                                     unsigned* flag, cudaStream_t st) {
   return launch_pdl(k_plan_qsgd_layout, dim3(1), dim3(256), 0, st, choice, params, K, layers, bucket0, L, R, B, plan, p,
                     flag);
+}
+
+// CUDA 12 loads kernels lazily, at their first launch, and a lazy load waits for the
+// device to go idle -- which never happens while a peer-memory wait kernel spins for a
+// peer whose kernels are the ones being loaded (ranks on streams of one process: the
+// simulated-rank tests deadlocked when run on their own).  Every kernel of the
+// peer-memory step is loaded up front (cudaFuncGetAttributes forces the load).
+cudaError_t preload_p2p_kernels() {
+  cudaFuncAttributes fa;
+  const void* fns[] = {
+      (const void*)k_qpack, (const void*)k_qunpack, (const void*)k_qreduce, (const void*)k_p2p_signal,
+      (const void*)k_p2p_wait, (const void*)k_p2p_push, (const void*)k_p2p_plan_push, (const void*)k_p2p_plan_pull,
+      (const void*)k_plan_qsgd_layout, (const void*)k_plan_qsgd_dev, (const void*)k_qprofile_reduce,
+      (const void*)k_qprofile_q<4, 2>, (const void*)k_qprofile_q<5, 2>, (const void*)k_qprofile_q<6, 2>,
+      (const void*)k_qprofile_q<7, 2>, (const void*)k_qprofile_q<8, 2>, (const void*)k_qprofile_q<16, 2>,
+      (const void*)k_qprofile_q<4, 0>, (const void*)k_qprofile_q<5, 0>, (const void*)k_qprofile_q<6, 0>,
+      (const void*)k_qprofile_q<7, 0>, (const void*)k_qprofile_q<8, 0>, (const void*)k_qprofile_q<16, 0>};
+  for (const void* f : fns) {
+    const cudaError_t e = cudaFuncGetAttributes(&fa, f);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 cudaError_t launch_p2p_signal(const P2PDev* p, int stage, unsigned epoch, cudaStream_t st) {

@@ -364,6 +364,22 @@ def solve(err, bits, default_idx, compress=None, D=10000, flags=0, choice=None, 
     return choice, info
 
 
+def solve_host(err, bits, default_idx, compress=None, D=10000, flags=0, stream=None):
+    """lgreco_solve's host mode: numpy tables in, (choice int32 (L,), SolveInfo) out; the DP
+    runs in the library's kernels (staged through device scratch), stream-synchronous."""
+    import numpy as np
+    e = np.ascontiguousarray(err, dtype=np.float64)
+    b = np.ascontiguousarray(bits, dtype=np.int64)
+    L, K = e.shape
+    d = np.ascontiguousarray(default_idx, dtype=np.int32)
+    c = None if compress is None else np.ascontiguousarray(compress, dtype=np.int32)
+    ch = np.empty(L, dtype=np.int32)
+    info = SolveInfo()
+    _check(lib().lgreco_solve(e.ctypes.data, b.ctypes.data, L, K, d.ctypes.data, None if c is None else c.ctypes.data,
+                              D, flags, ch.ctypes.data, C.addressof(info), None, 0, _stream(stream)), "solve_host")
+    return ch, info
+
+
 def accumulate(G, g, stream=None):
     """K0 (row a1): G += g in fp32 on the device (cuda float32 tensors of equal size)."""
     assert G.dtype == torch.float32 and g.dtype == torch.float32 and G.numel() == g.numel()

@@ -164,3 +164,30 @@ def test_layer_groups_bit_exact(lg, ref, groups, monkeypatch):
         assert i_gpu.emax == i_ref.emax and i_gpu.total_err == i_ref.total_err
         n_multi += trial % 2
     assert n_multi > 0
+
+
+def test_solve_host_mode(lg, ref):
+    """lgreco_solve with HOST tables and outputs (SURVEY 8(b)'s host mode): staged through
+    device scratch around the same kernels; the plan and summary equal the oracle's, and
+    mixing host and device pointers is refused."""
+    layers = W.config_layers("C4")
+    L, K = len(layers), 7
+    rng = np.random.default_rng(5)
+    err, bits = _table(rng, L, K)
+    comp = np.array([l.compress for l in layers], np.int32)
+    dflt = np.full(L, 2, np.int32)
+    st, c_ref, i_ref = ref.solve(err, bits, dflt, comp, D=10000)
+    ch, inf = lg.solve_host(err, bits, dflt, comp)
+    assert list(ch) == list(c_ref) and inf.total_bits == i_ref.total_bits and inf.emax == i_ref.emax
+    ch2, _ = lg.solve_host(err, bits, dflt, None, D=1000, flags=4)
+    st2, c_ref2, _ = ref.solve(err, bits, dflt, None, D=1000)
+    assert list(ch2) == list(c_ref2)
+    import ctypes as C
+    e_d = torch.from_numpy(err).cuda()
+    b_h = np.ascontiguousarray(bits)
+    d_h = np.ascontiguousarray(dflt)
+    out_h = np.empty(L, np.int32)
+    info = lg.SolveInfo()
+    rc = lg.lib().lgreco_solve(e_d.data_ptr(), b_h.ctypes.data, L, K, d_h.ctypes.data, None, 10000, 0,
+                               out_h.ctypes.data, C.addressof(info), None, 0, None)
+    assert rc == lg.EINVAL

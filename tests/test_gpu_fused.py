@@ -211,3 +211,42 @@ def test_pipelined_chain_matches_oracle(lg, ref, cfg, lag):
         e_ref = es_ref[0]
         ref_plans.append([int(c) for c in rch])
     ctx.close()
+
+
+@pytest.mark.parametrize("Wn", [2, 3, 4])
+def test_profile_compress_p2p_simulated_ranks(lg, ref, Wn):
+    """W > 1 over peer memory: the fused pass packs every stage-1 record (R7) in K1's lane
+    layout straight into its owner's window, then the peer-memory exchange runs -- W rank
+    contexts on W streams of the one GPU (peers set in-process); every rank's output and
+    EF bit-identical to the W-rank oracle, every rank's profile of its own x = the
+    oracle's (rankfield = rank)."""
+    layers = _edge_layers()
+    seed, step = 91, 6
+    L, K = len(layers), len(BITS)
+    ctxs = [lg.Context(layers, lg.QSGD, BITS, seed=seed, rank=w, world=Wn) for w in range(Wn)]
+    loc = [c.p2p_local() for c in ctxs]
+    for c in ctxs:
+        c.p2p_set_peers([p[0] for p in loc], [p[1] for p in loc], [p[2] for p in loc])
+    gs, es = zip(*[_edge_data(layers, 700 + w) for w in range(Wn)])
+    rng = np.random.default_rng(Wn + 5)
+    choice = [int(rng.integers(0, K)) if l.compress else -1 for l in layers]
+    lbits = [BITS[c] if l.compress else 0 for c, l in zip(choice, layers)]
+    out_ref, es_ref, _, _ = ref.qsgd_allreduce(layers, lbits, list(gs), list(es), seed=seed, step=step)
+    streams = [torch.cuda.Stream() for _ in range(Wn)]
+    gds, eds = [_dev(g) for g in gs], [_dev(e) for e in es]
+    outs = [torch.empty(len(gs[0]), dtype=torch.float32, device="cuda") for _ in range(Wn)]
+    dch = [torch.tensor(choice, dtype=torch.int32, device="cuda") for _ in range(Wn)]
+    errs = [torch.empty(L, K, dtype=torch.float64, device="cuda") for _ in range(Wn)]
+    bits = [torch.empty(L, K, dtype=torch.int64, device="cuda") for _ in range(Wn)]
+    torch.cuda.synchronize()
+    for w in range(Wn):
+        ctxs[w].profile_compress(dch[w], gds[w], eds[w], outs[w], step, errs[w], bits[w], stream=streams[w])
+    torch.cuda.synchronize()
+    for w in range(Wn):
+        assert np.array_equal(_u32(outs[w]), out_ref.view(np.uint32)), w
+        assert np.array_equal(_u32(eds[w]), es_ref[w].view(np.uint32)), w
+        rerr, rbits = ref.qsgd_profile(layers, gs[w], es[w], BITS, seed=seed, rank=w, step=step)
+        _check_profile(errs[w], bits[w], rerr, rbits)
+    for c in ctxs:
+        c.check()
+        c.close()
