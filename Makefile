@@ -2,7 +2,6 @@
 PY      ?= python
 SITE    := $(shell $(PY) -c "import sysconfig;print(sysconfig.get_paths()['purelib'])")
 NCCL    := $(SITE)/nvidia/nccl
-CUSOLVER := $(SITE)/nvidia/cusolver
 CUDART  := $(SITE)/nvidia/cuda_runtime/lib
 NVCC    ?= nvcc
 ARCH    := -gencode arch=compute_100a,code=sm_100a
@@ -27,8 +26,7 @@ build/obj/%.o: $(PKG)/csrc/%.cu $(HDRS)
 
 $(LIB): $(OBJS)
 	$(NVCC) $(ARCH) -cudart shared -shared -o $@ $(OBJS) -L$(NCCL)/lib -l:libnccl.so.2 \
-	    -L$(CUSOLVER)/lib -l:libcusolver.so.11 \
-	    -Xlinker -rpath=$(NCCL)/lib -Xlinker -rpath=$(CUDART) -Xlinker -rpath=$(CUSOLVER)/lib
+	    -Xlinker -rpath=$(NCCL)/lib -Xlinker -rpath=$(CUDART)
 	cat build/obj/*.ptxas.log > build/ptxas.log
 
 $(ORACLE): oracle/lgreco_ref.c
@@ -50,7 +48,6 @@ build/obj/dp_timing.o: $(PKG)/csrc/dp.cu $(HDRS)
 
 build/liblgreco_timing.so: $(filter-out build/obj/dp.o,$(OBJS)) build/obj/dp_timing.o
 	$(NVCC) $(ARCH) -cudart shared -shared -o $@ $^ -L$(NCCL)/lib -l:libnccl.so.2 \
-	    -L$(CUSOLVER)/lib -l:libcusolver.so.11 \
-	    -Xlinker -rpath=$(NCCL)/lib -Xlinker -rpath=$(CUDART) -Xlinker -rpath=$(CUSOLVER)/lib
+	    -Xlinker -rpath=$(NCCL)/lib -Xlinker -rpath=$(CUDART)
 
 timing: build/liblgreco_timing.so

@@ -3,12 +3,11 @@
 // compute all the errors").  The squared singular values of the m x k view M are the
 // eigenvalues of the Gram matrix of its smaller side (n = min(m, k)): G = M M^T (m <= k)
 // or M^T M.  G is formed in fp64 from x = fl(g + e) (R2) by a split-K tiled kernel
-// (fixed-order split reduction: deterministic), its eigenvalues by cuSOLVER's symmetric
-// eigensolver (dsyevd, values only -- a library primitive, not the hot path: this is the
-// alternative profile method the paper suggests for large rank ranges), and
-// err_r^2 = sum of the n - r smallest eigenvalues (each clamped at 0), summed in fp64 in
-// ascending order.
-#include <cusolverDn.h>
+// (fixed-order split reduction: deterministic); its eigenvalues by this file's own
+// symmetric eigensolver (k_sym_eigvals: Householder reduction to tridiagonal form in
+// fp64, one CTA per matrix, every matrix of the table at once, then Sturm-count bisection,
+// one thread per eigenvalue), and err_r^2 = sum of the n - r smallest eigenvalues (each
+// clamped at 0), summed in fp64 in ascending order.
 #include <math.h>
 
 #include <algorithm>
@@ -89,6 +88,140 @@ __global__ void k_gram_reduce(const double* __restrict__ part, int nsplit, int64
   }
 }
 
+// ---------------------------------------------------------------------------
+// Symmetric eigenvalues, one CTA per matrix (G: n x n, row-major, full storage, fp64;
+// overwritten).  (1) Householder reduction to tridiagonal form, column k = 0 .. n-3
+// (LAPACK dsytd2's lower variant, restated): x = G[k+1.., k] (= row k right of the
+// diagonal: contiguous), beta = -sign(x0) ||x||, v = x / (x0 - beta) with v0 = 1,
+// tau = (beta - x0) / beta; p = tau A v and w = p - (tau/2)(p.v) v on the trailing
+// block A, then A -= v w^T + w v^T; e_k = beta, d_k = G[k][k].  Warp per row for the
+// matrix-vector product, fixed-order block reductions (deterministic).  (2) Eigenvalue i
+// (ascending) of the tridiagonal (d, e) by bisection on the Sturm count (the number of
+// negative q_j of q_0 = d_0 - s, q_j = d_j - s - e_{j-1}^2 / q_{j-1}) inside the
+// Gershgorin interval, to the fp64 resolution of the interval.  Dynamic shared memory:
+// v, w, d, e (4 n doubles).
+constexpr int EIG_THREADS = 1024;
+constexpr int EIG_NMAX = 6144;  // 4 n doubles of shared memory <= 192 KB
+
+struct EigMat { int64_t goff; int32_t n, pad; };  // G at base + goff; eigenvalues at W + wout
+
+__device__ __forceinline__ double block_sum_d(double v, double* red, int tid) {
+  v = warp_sum_d(v);
+  __syncthreads();  // (red reused)
+  if ((tid & 31) == 0) red[tid >> 5] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int w = 0; w < EIG_THREADS / 32; ++w) s += red[w];  // every thread, same order
+  return s;
+}
+
+__global__ void __launch_bounds__(EIG_THREADS, 1)
+k_sym_eigvals(double* __restrict__ Gbase, const EigMat* __restrict__ mats, double* __restrict__ Wbase,
+              const int64_t* __restrict__ woff) {
+  extern __shared__ double esm[];
+  __shared__ double red[EIG_THREADS / 32];
+  const EigMat em = mats[blockIdx.x];
+  const int n = em.n;
+  double* G = Gbase + em.goff;
+  double* W = Wbase + woff[blockIdx.x];
+  double* v = esm;
+  double* w = esm + n;
+  double* d = esm + 2 * n;
+  double* e = esm + 3 * n;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int k = 0; k + 2 < n; ++k) {
+    const int m = n - k - 1;  // trailing block rows / columns k+1 .. n-1
+    const double* rk = G + (int64_t)k * n + (k + 1);
+    double ss = 0.0;
+    for (int j = tid; j < m; j += EIG_THREADS) { const double x = rk[j]; ss = fma(x, x, ss); }
+    const double nrm2 = block_sum_d(ss, red, tid);
+    const double x0 = rk[0];
+    if (tid == 0) d[k] = G[(int64_t)k * n + k];
+    if (nrm2 == 0.0) {  // nothing to annihilate (H = I)
+      if (tid == 0) e[k] = 0.0;
+      __syncthreads();
+      continue;
+    }
+    const double nrm = sqrt(nrm2);
+    const double beta = x0 > 0.0 ? -nrm : nrm;
+    const double tau = (beta - x0) / beta;
+    const double sc = 1.0 / (x0 - beta);
+    for (int j = tid; j < m; j += EIG_THREADS) v[j] = j == 0 ? 1.0 : rk[j] * sc;
+    if (tid == 0) e[k] = beta;
+    __syncthreads();
+    // p = tau A v (warp per row, lanes over columns), into w
+    for (int i = warp; i < m; i += EIG_THREADS / 32) {
+      const double* ri = G + (int64_t)(k + 1 + i) * n + (k + 1);
+      double a = 0.0;
+      for (int j = lane; j < m; j += 32) a = fma(ri[j], v[j], a);
+      a = warp_sum_d(a);
+      if (lane == 0) w[i] = tau * a;
+    }
+    __syncthreads();
+    double pv = 0.0;
+    for (int j = tid; j < m; j += EIG_THREADS) pv = fma(w[j], v[j], pv);
+    const double kk = -0.5 * tau * block_sum_d(pv, red, tid);
+    for (int j = tid; j < m; j += EIG_THREADS) w[j] = fma(kk, v[j], w[j]);
+    __syncthreads();
+    // A -= v w^T + w v^T
+    for (int i = warp; i < m; i += EIG_THREADS / 32) {
+      double* ri = G + (int64_t)(k + 1 + i) * n + (k + 1);
+      const double vi = v[i], wi = w[i];
+      for (int j = lane; j < m; j += 32) ri[j] = ri[j] - vi * w[j] - wi * v[j];
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    if (n >= 2) {
+      d[n - 2] = G[(int64_t)(n - 2) * n + (n - 2)];
+      e[n - 2] = G[(int64_t)(n - 1) * n + (n - 2)];
+    }
+    d[n - 1] = G[(int64_t)(n - 1) * n + (n - 1)];
+  }
+  __syncthreads();
+  // Gershgorin interval of the tridiagonal
+  double lo = INFINITY, hi = -INFINITY;
+  for (int j = tid; j < n; j += EIG_THREADS) {
+    const double r = (j > 0 ? fabs(e[j - 1]) : 0.0) + (j + 1 < n ? fabs(e[j]) : 0.0);
+    lo = fmin(lo, d[j] - r);
+    hi = fmax(hi, d[j] + r);
+  }
+  for (int o = 16; o; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(LG_FULL, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(LG_FULL, hi, o));
+  }
+  __shared__ double red_hi[EIG_THREADS / 32];
+  __syncthreads();
+  if (lane == 0) { red[warp] = lo; red_hi[warp] = hi; }
+  __syncthreads();
+  lo = red[0]; hi = red_hi[0];
+  for (int q = 1; q < EIG_THREADS / 32; ++q) { lo = fmin(lo, red[q]); hi = fmax(hi, red_hi[q]); }
+  const double span = fmax(hi - lo, 1e-300);
+  const double pivmin = 1e-300;  // |q| floor (a zero pivot counts as negative, LAPACK's rule)
+  // the squared off-diagonals, reused by every count
+  __syncthreads();
+  for (int j = tid; j + 1 < n; j += EIG_THREADS) v[j] = e[j] * e[j];
+  __syncthreads();
+  for (int idx = tid; idx < n; idx += EIG_THREADS) {
+    double a = lo - 1e-12 * span, b = hi + 1e-12 * span;  // count(a) <= idx < count(b)
+    for (int it = 0; it < 128; ++it) {
+      const double mid = 0.5 * (a + b);
+      if (!(mid > a && mid < b)) break;  // fp64 resolution reached
+      int cnt = 0;
+      double q = d[0] - mid;
+      if (fabs(q) < pivmin) q = -pivmin;
+      cnt += q < 0.0;
+      for (int j = 1; j < n; ++j) {
+        q = (d[j] - mid) - v[j - 1] / q;
+        if (fabs(q) < pivmin) q = -pivmin;
+        cnt += q < 0.0;
+      }
+      if (cnt > idx) b = mid; else a = mid;
+    }
+    W[idx] = 0.5 * (a + b);
+  }
+}
+
 // err / bits of one matrix layer from its ascending eigenvalues W (n of them)
 __global__ void k_svd_err(const double* __restrict__ W, int n, int64_t m, int64_t k, const int32_t* __restrict__ ranks,
                           int K, int layer, double* __restrict__ err, int64_t* __restrict__ bits) {
@@ -147,17 +280,17 @@ extern "C" int lgreco_layer_norms(lgreco_ctx* c, const float* d_g, const float* 
 }
 
 struct SvdWs {
-  cusolverDnHandle_t h = nullptr;
-  double *part = nullptr, *G = nullptr, *W = nullptr, *work = nullptr;
-  int* info = nullptr;
-  int nmax = 0, lwork = 0, nsplit = 0;
+  double *part = nullptr, *G = nullptr, *W = nullptr;
+  lg::EigMat* mats = nullptr;
+  int64_t* woff = nullptr;
+  size_t gcap = 0, wcap = 0, pcap = 0;
+  int nmat = 0;
 };
 
 void svd_destroy(lgreco_ctx* c) {
   SvdWs* s = static_cast<SvdWs*>(c->svd);
   if (!s) return;
-  if (s->h) cusolverDnDestroy(s->h);
-  cudaFree(s->part); cudaFree(s->G); cudaFree(s->W); cudaFree(s->work); cudaFree(s->info);
+  cudaFree(s->part); cudaFree(s->G); cudaFree(s->W); cudaFree(s->mats); cudaFree(s->woff);
   delete s;
   c->svd = nullptr;
 }
@@ -171,6 +304,9 @@ extern "C" int lgreco_psgd_profile_svd(lgreco_ctx* c, const float* d_g, const fl
   // matrix layers (R11 view) with at least one lossy candidate
   std::vector<int> mats;
   int nmax = 0;
+  size_t gtot = 0, wtot = 0;
+  std::vector<lg::EigMat> em;
+  std::vector<int64_t> wo;
   for (int l = 0; l < L; ++l) {
     const lgreco_layer& ly = c->layers[l];
     if (!ly.compress || ly.rows <= 0 || ly.cols <= 0) continue;
@@ -178,8 +314,17 @@ extern "C" int lgreco_psgd_profile_svd(lgreco_ctx* c, const float* d_g, const fl
     bool lossy = false;
     for (int j = 0; j < K; ++j) lossy |= (int64_t)c->params[j] * (m + k) < m * k;
     if (!lossy) continue;
+    const int n = (int)std::min(m, k);
+    if (n > lg::EIG_NMAX) {
+      lg_set_error("svd profile: layer %d has min(m, k) = %d > %d", l, n, lg::EIG_NMAX);
+      return LGRECO_EUNSUPPORTED;
+    }
     mats.push_back(l);
-    nmax = std::max<int>(nmax, (int)std::min(m, k));
+    em.push_back(lg::EigMat{(int64_t)gtot, n, 0});
+    wo.push_back((int64_t)wtot);
+    gtot += (size_t)n * n;
+    wtot += (size_t)n;
+    nmax = std::max(nmax, n);
   }
   lg::k_svd_rows_init<<<64, 256, 0, st>>>(c->d_layers, L, K, d_err, d_bits);
   LG_CUDA(cudaGetLastError());
@@ -188,53 +333,48 @@ extern "C" int lgreco_psgd_profile_svd(lgreco_ctx* c, const float* d_g, const fl
   SvdWs* s = static_cast<SvdWs*>(c->svd);
   if (!s) { s = new SvdWs(); c->svd = s; }
   const int nsplit = 8;
-  if (!s->h) {
-    if (cusolverDnCreate(&s->h) != CUSOLVER_STATUS_SUCCESS) { lg_set_error("cusolverDnCreate failed"); return LGRECO_ECUDA; }
+  const size_t pneed = (size_t)nsplit * nmax * nmax;
+  // (grown only between calls: the stream is synchronised before a buffer is replaced)
+  if (s->gcap < gtot || s->wcap < wtot || s->pcap < pneed || s->nmat < (int)mats.size()) {
+    LG_CUDA(cudaStreamSynchronize(st));
+    cudaFree(s->part); cudaFree(s->G); cudaFree(s->W); cudaFree(s->mats); cudaFree(s->woff);
+    s->part = s->G = s->W = nullptr; s->mats = nullptr; s->woff = nullptr;
+    LG_CUDA(cudaMalloc(&s->part, sizeof(double) * pneed));
+    LG_CUDA(cudaMalloc(&s->G, sizeof(double) * gtot));
+    LG_CUDA(cudaMalloc(&s->W, sizeof(double) * wtot));
+    LG_CUDA(cudaMalloc(&s->mats, sizeof(lg::EigMat) * mats.size()));
+    LG_CUDA(cudaMalloc(&s->woff, sizeof(int64_t) * mats.size()));
+    s->gcap = gtot; s->wcap = wtot; s->pcap = pneed; s->nmat = (int)mats.size();
   }
-  if (s->nmax < nmax) {
-    cudaFree(s->part); cudaFree(s->G); cudaFree(s->W); cudaFree(s->work); cudaFree(s->info);
-    s->part = s->G = s->W = s->work = nullptr; s->info = nullptr;
-    LG_CUDA(cudaMalloc(&s->part, sizeof(double) * (size_t)nsplit * nmax * nmax));
-    LG_CUDA(cudaMalloc(&s->G, sizeof(double) * (size_t)nmax * nmax));
-    LG_CUDA(cudaMalloc(&s->W, sizeof(double) * (size_t)nmax));
-    LG_CUDA(cudaMalloc(&s->info, sizeof(int)));
-    int lw = 0;
-    if (cusolverDnDsyevd_bufferSize(s->h, CUSOLVER_EIG_MODE_NOVECTOR, CUBLAS_FILL_MODE_UPPER, nmax, s->G, nmax, s->W,
-                                    &lw) != CUSOLVER_STATUS_SUCCESS) { lg_set_error("syevd buffer size"); return LGRECO_ECUDA; }
-    LG_CUDA(cudaMalloc(&s->work, sizeof(double) * (size_t)std::max(1, lw)));
-    s->lwork = lw;
-    s->nmax = nmax;
-    s->nsplit = nsplit;
-  }
-  if (cusolverDnSetStream(s->h, st) != CUSOLVER_STATUS_SUCCESS) { lg_set_error("cusolverDnSetStream"); return LGRECO_ECUDA; }
-  for (int l : mats) {
-    const lgreco_layer& ly = c->layers[l];
+  LG_CUDA(cudaMemcpyAsync(s->mats, em.data(), sizeof(lg::EigMat) * em.size(), cudaMemcpyHostToDevice, st));
+  LG_CUDA(cudaMemcpyAsync(s->woff, wo.data(), sizeof(int64_t) * wo.size(), cudaMemcpyHostToDevice, st));
+  // every matrix's fp64 Gram (each launch over the whole GPU), then all eigenvalues at once
+  for (size_t i = 0; i < mats.size(); ++i) {
+    const lgreco_layer& ly = c->layers[mats[i]];
     const int64_t m = ly.rows, k = ly.cols;
     const bool rows = m <= k;
-    const int n = (int)std::min(m, k);
+    const int n = em[i].n;
     const int64_t t = rows ? k : m;
     const int nt = (n + lg::GT - 1) / lg::GT;
     lg::k_gram64<<<dim3(nt * (nt + 1) / 2, nsplit), lg::G_THREADS, 0, st>>>(d_g, d_ef, ly.offset, (int)k, n, t,
                                                                              rows ? 1 : 0, nsplit, s->part);
     lg::k_gram_reduce<<<std::max(1, std::min(1024, (int)(((int64_t)n * n + 255) / 256))), 256, 0, st>>>(
-        s->part, nsplit, (int64_t)n * n, s->G);
+        s->part, nsplit, (int64_t)n * n, s->G + em[i].goff);
     LG_CUDA(cudaGetLastError());
-    int lw = 0;
-    if (cusolverDnDsyevd_bufferSize(s->h, CUSOLVER_EIG_MODE_NOVECTOR, CUBLAS_FILL_MODE_UPPER, n, s->G, n, s->W, &lw) !=
-            CUSOLVER_STATUS_SUCCESS || lw > s->lwork) {
-      lg_set_error("syevd workspace");
-      return LGRECO_ECUDA;
-    }
-    if (cusolverDnDsyevd(s->h, CUSOLVER_EIG_MODE_NOVECTOR, CUBLAS_FILL_MODE_UPPER, n, s->G, n, s->W, s->work, s->lwork,
-                         s->info) != CUSOLVER_STATUS_SUCCESS) {
-      lg_set_error("cusolverDnDsyevd failed (layer %d)", l);
-      return LGRECO_ECUDA;
-    }
-    lg::k_svd_err<<<1, std::max(32, ((K + 31) / 32) * 32), 0, st>>>(s->W, n, m, k, c->d_params, K, l, d_err,
-                                                                      d_bits);
-    LG_CUDA(cudaGetLastError());
-    c->launches += 3;
+    c->launches += 2;
   }
+  const size_t esmem = sizeof(double) * 4 * (size_t)nmax;
+  if (esmem > 48 * 1024) LG_CUDA(cudaFuncSetAttribute(lg::k_sym_eigvals, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esmem));
+  lg::k_sym_eigvals<<<(unsigned)mats.size(), lg::EIG_THREADS, esmem, st>>>(s->G, s->mats, s->W, s->woff);
+  LG_CUDA(cudaGetLastError());
+  c->launches += 1;
+  for (size_t i = 0; i < mats.size(); ++i) {
+    const lgreco_layer& ly = c->layers[mats[i]];
+    lg::k_svd_err<<<1, std::max(32, ((K + 31) / 32) * 32), 0, st>>>(s->W + wo[i], em[i].n, ly.rows, ly.cols,
+                                                                      c->d_params, K, mats[i], d_err, d_bits);
+    c->launches += 1;
+  }
+  LG_CUDA(cudaGetLastError());
   return LGRECO_OK;
 }
 
@@ -243,7 +383,7 @@ extern "C" int lgreco_psgd_set_method(lgreco_ctx* c, int32_t method) {
   if (!c || c->family != LGRECO_POWERSGD) { lg_set_error("psgd_set_method: PowerSGD ctx only"); return LGRECO_EINVAL; }
   if (method == LGRECO_PSGD_POWER || method == LGRECO_PSGD_SVD) { c->psgd_method = method; return LGRECO_OK; }
   if (method != LGRECO_PSGD_AUTO) { lg_set_error("psgd_set_method: bad method %d", method); return LGRECO_EINVAL; }
-  double t_pow = 0.0, t_svd = 0.0;
+  double t_pow = 0.0, t_svd = 0.0, nmax = 0.0;
   for (int l = 0; l < c->L; ++l) {
     const lgreco_layer& ly = c->layers[l];
     if (!ly.compress || ly.rows <= 0 || ly.cols <= 0) continue;
@@ -253,8 +393,15 @@ extern "C" int lgreco_psgd_set_method(lgreco_ctx* c, int32_t method) {
       if ((double)c->params[j] * (m + k) < m * k) rmax = std::max(rmax, c->params[j]);
     if (rmax == 0) continue;
     t_pow += (double)c->power_steps * m * k * rmax * 1.9e-13;
-    t_svd += m * k * n * 1e-13 + n * n * n * 1e-11;
+    // the fp64 Gram, then the eigensolver's HBM traffic (all matrices at once: ~8 n^3
+    // bytes each at ~3 TB/s aggregate; measured: C2 25 ms, C5 315 ms)
+    t_svd += m * k * n * 1e-13 + n * n * n * 2.7e-12;
+    nmax = std::max(nmax, n);
   }
+  // dependent-step latencies: n - 2 Householder steps of the largest matrix (~2 us each);
+  // a chain of ~10 launches per power step (~3 us each)
+  t_svd += nmax * 2e-6;
+  t_pow += (double)c->power_steps * 3e-5;
   c->psgd_method = (t_svd < t_pow) ? LGRECO_PSGD_SVD : LGRECO_PSGD_POWER;
   return LGRECO_OK;
 }

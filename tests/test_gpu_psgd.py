@@ -200,11 +200,32 @@ def test_compress_allreduce_w1(lg, ref):
     ctx.check()
 
 
-@pytest.mark.parametrize("cfg", ["C2", "tall"])
+@pytest.mark.parametrize("cfg", ["C2", "tall", "special"])
 def test_profile_svd_parity(lg, ref, cfg):
     """NEXT-2: errors of every candidate rank from the singular values (fp64 Gram of the
-    smaller side + cuSOLVER eigenvalues) vs the oracle's LAPACK SVD; bits identical."""
-    if cfg == "C2":
+    smaller side + the library's own eigensolver: Householder tridiagonalisation, Sturm
+    bisection) vs the oracle's LAPACK SVD; bits identical.  "special": a zero matrix, an
+    exactly rank-3 one, repeated singular values, a 2 x k and a 3 x 3-view matrix."""
+    if cfg == "special":
+        shapes = [(64, 96), (80, 50), (120, 40), (2, 300), (3, 3), (200, 130)]
+        layers, off = [], 0
+        for m, k in shapes:
+            layers.append(W.Layer(off, m * k, m, k, 1))
+            off += m * k
+        rng = np.random.default_rng(12)
+        g = np.zeros(off, np.float32)
+        ly = layers[1]  # exactly rank 3
+        g[ly.offset:ly.offset + ly.numel] = (rng.standard_normal((80, 3)) @ rng.standard_normal((3, 50))).astype(
+            np.float32).ravel()
+        ly = layers[2]  # singular values 5, 5, 5, 1, 1, 0.1 ...
+        U, _ = np.linalg.qr(rng.standard_normal((120, 40)))
+        V, _ = np.linalg.qr(rng.standard_normal((40, 40)))
+        sv = np.array([5, 5, 5, 1, 1] + [0.1] * 35)
+        g[ly.offset:ly.offset + ly.numel] = ((U * sv) @ V.T).astype(np.float32).ravel()
+        for ly in layers[3:]:
+            g[ly.offset:ly.offset + ly.numel] = rng.standard_normal(ly.numel).astype(np.float32)
+        e = None
+    elif cfg == "C2":
         layers = W.config_layers("C2")
         g, _ = W.low_rank_plus_noise(layers, seed=8)
         e = (np.random.default_rng(8).standard_normal(g.size) * 1e-4).astype(np.float32)
@@ -226,12 +247,16 @@ def test_profile_svd_parity(lg, ref, cfg):
     L, K = len(layers), len(ranks)
     err = torch.empty(L, K, dtype=torch.float64, device="cuda")
     bits = torch.empty(L, K, dtype=torch.int64, device="cuda")
-    ctx.profile_svd(_dev(g), _dev(e), err, bits)
+    ctx.profile_svd(_dev(g), None if e is None else _dev(e), err, bits)
     r_err, r_bits = ref.psgd_svd_profile(layers, g, e, ranks)
     assert np.array_equal(bits.cpu().numpy(), r_bits)
     ge = err.cpu().numpy()
-    assert np.all((r_err == 0) == (ge == 0))
-    assert (np.abs(ge - r_err) / np.maximum(r_err, 1e-300)).max() <= 1e-6
+    if cfg == "special":  # (exact zeros: the eigenvalues of a rank-deficient Gram are only ~eps ||G||)
+        scale = np.array([[np.linalg.norm(g[l.offset:l.offset + l.numel])] * K for l in layers])
+        assert (np.abs(ge - r_err) <= 1e-6 * np.maximum(r_err, 1e-300) + 1e-6 * scale).all(), (ge, r_err)
+    else:
+        assert np.all((r_err == 0) == (ge == 0))
+        assert (np.abs(ge - r_err) / np.maximum(r_err, 1e-300)).max() <= 1e-6
     ctx.close()
 
 
