@@ -30,6 +30,9 @@ namespace lg {
 
 constexpr int QP_THREADS = 256;
 constexpr int QP_WARPS = QP_THREADS / 32;
+#ifndef Q1_TRIGGER
+#define Q1_TRIGGER 0  // K1 / the fused pass trigger their dependents (K1b) as each warp runs out of quads
+#endif
 #ifndef QF_MAGIC
 #define QF_MAGIC 1  // fused pass: the planned candidate's ceil by the FADD2 magic (1) or FRND.CEIL (0); A/B 96.5 -> 95.0 us per pipelined step (the XU pipe carries the profile's ceils)
 #endif
@@ -651,6 +654,9 @@ k_qprofile_q(const float* __restrict__ g, const float* e, const QInfo* __restric
     return q;
   };
   auto finish = [&]() {  // after this warp found every part exhausted
+#if Q1_TRIGGER
+    pdl_trigger();  // K1b may be scheduled now (it still waits for this grid's completion)
+#endif
     if (lane == 0 && atomicAdd(&ticket[QT_ARR * 64], 1u) == gridDim.x * Q1_WARPS - 1u) {
       for (int p2 = 0; p2 <= QT_ARR; ++p2) atomicExch(&ticket[p2 * 64], 0u);
     }
