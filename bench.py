@@ -669,6 +669,42 @@ def run_extras(dev, rank, world, stream, l2_flush, nccl_dist):
             torch.cuda.synchronize()
             ctx.check()
             pipe_ms = m0.elapsed_time(m1) / 5
+        elif world == 1:
+            # the same schedule for TopK / PowerSGD: the profile and the compress (with the
+            # plan solved two steps earlier; TopK's compress reuses the profile's thresholds
+            # of the same x) on the main stream, the solve of the step on a side stream
+            # beside the next step's kernels
+            side = torch.cuda.Stream(device=dev)
+            plans = [dflt.clone() for _ in range(3)]
+            tabs = [(err, bits), (torch.empty_like(err), torch.empty_like(bits))]
+            ev_solve = {}
+
+            def pstep(s2):
+                e_t, b_t = tabs[s2 % 2]
+                if s2 - 2 in ev_solve:  # plans[s2 % 3] and the table pair: solve of step s2-2 done
+                    stream.wait_event(ev_solve[s2 - 2])
+                ctx.profile(g, ef, s2, e_t, b_t)
+                ev_p = torch.cuda.Event()
+                ev_p.record(stream)
+                ctx.compress_allreduce_dev(plans[s2 % 3], g, ef, out, s2)
+                side.wait_event(ev_p)
+                with torch.cuda.stream(side):
+                    lgreco.solve(e_t, b_t, dflt, comp, D=D_BINS, flags=lgreco.SOLVE_NARROW,
+                                 choice=plans[(s2 + 2) % 3], info=info, workspace=ws, stream=side)
+                ev_solve[s2] = torch.cuda.Event()
+                ev_solve[s2].record(side)
+            for s2 in range(3):
+                pstep(s2)
+            torch.cuda.synchronize()
+            m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            m0.record(stream)
+            for s2 in range(3, 8):
+                pstep(s2)
+            stream.wait_event(ev_solve[7])
+            m1.record(stream)
+            torch.cuda.synchronize()
+            ctx.check()
+            pipe_ms = m0.elapsed_time(m1) / 5
         ctx.close()
         st = {k: sum(v) / len(v) for k, v in t.items()}
         if world > 1:
@@ -683,7 +719,10 @@ def run_extras(dev, rank, world, stream, l2_flush, nccl_dist):
         if pipe_ms is not None:
             res[name]["pipelined"] = {"ms_per_step": round(pipe_ms, 4),
                                       "gbs": round(world * 4.0 * N / (pipe_ms * 1e-3) / 1e9, 2),
-                                      "note": "headline schedule: fused pass + the previous step's solve beside it"}
+                                      "note": ("headline schedule: fused pass + the previous step's solve beside it"
+                                               if fam == lgreco.QSGD else
+                                               "profile + compress with the plan of step t-2, the solve on a side "
+                                               "stream beside the next step")}
         del ef, out
     cache.clear()
     torch.cuda.empty_cache()
