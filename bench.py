@@ -272,6 +272,9 @@ def run_ours(args):
     torch.cuda.synchronize()
     ctx.check()
     pipe = None
+    # SM clocks and throttle reasons sampled from here through both timed passes
+    clocks = ClockSampler(local)
+    clocks.start()
     if pipelined:
         # headline of the pipelined schedule: K consecutive steps between two events (no
         # L2 flush between them: it would serialise the overlap; each step streams 204 MB
@@ -320,14 +323,12 @@ def run_ours(args):
             pl.copy_(dflt)
         torch.cuda.synchronize()
 
-    clocks = ClockSampler(local)
     times = {"step": [], "profile": [], "solve": [], "compress_allreduce": []}
     # ---- headline pass: K steps, events only at each step's begin and end
     launches0 = ctx.launches()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    clocks.start()
     t_wall0 = time.perf_counter()
     all_marks = []
     for s in range(args.steps):
