@@ -246,7 +246,7 @@ int lgreco_compress_allreduce_dev(lgreco_ctx* ctx, const int32_t* d_choice, cons
  * uniforms, then K1b) -- at world == 1 writing the decoded output, at world > 1 over peer
  * memory (lgreco_p2p_open / _set_peers) storing the stage-1 records straight into their
  * owners' windows, followed by the peer-memory exchange of lgreco_compress_allreduce_dev;
- * otherwise (NCCL exchange, B > 128, other families) the two calls.  d_choice must not alias the
+ * otherwise (NCCL exchange, B > 128, d_ef = NULL, other families) the two calls.  d_choice must not alias the
  * output of a solve that reads d_err.  flags: LGRECO_PC_CONCURRENT -- the caller asserts
  * that the kernel enqueued immediately before this call on `stream` (typically the
  * lgreco_solve of the previous step, writing a plan other than d_choice) produces nothing

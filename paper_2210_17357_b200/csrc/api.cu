@@ -806,7 +806,9 @@ int lgreco_profile_compress(lgreco_ctx* c, const int32_t* d_choice, const float*
   LG_TRY(check_align16("profile_compress", d_g, d_ef, d_out));
   cudaStream_t st = (cudaStream_t)stream;
   const bool p2p_fused = c->family == LGRECO_QSGD && c->world > 1 && c->p2p && c->B == 128 && c->nqchunks > 0;
-  const bool fused = (c->family == LGRECO_QSGD && c->world == 1 && c->B == 128 && c->nqchunks > 0) || p2p_fused;
+  // (the fused kernel stores e' unconditionally: without an EF buffer, the two calls)
+  const bool fused = d_ef != nullptr &&
+                     ((c->family == LGRECO_QSGD && c->world == 1 && c->B == 128 && c->nqchunks > 0) || p2p_fused);
   if (!fused) {
     LG_TRY(lgreco_profile(c, d_g, d_ef, step, d_err, d_bits, stream));
     return lgreco_compress_allreduce_dev(c, d_choice, d_g, d_ef, d_out, step, stream);

@@ -250,3 +250,32 @@ def test_profile_compress_p2p_simulated_ranks(lg, ref, Wn):
     for c in ctxs:
         c.check()
         c.close()
+
+
+def test_profile_compress_without_ef(lg, ref):
+    """d_ef = NULL (no error feedback: x = g, the EF is neither read nor written): the fused
+    pass equals the two-call definition and the oracle with a zero EF."""
+    layers = _edge_layers()
+    g, _ = _edge_data(layers, 44)
+    L, K = len(layers), len(BITS)
+    choice = [3 if l.compress else -1 for l in layers]
+    ctx = lg.Context(layers, lg.QSGD, BITS, seed=8)
+    gd = _dev(g)
+    dch = torch.tensor(choice, dtype=torch.int32, device="cuda")
+    out, out2 = torch.empty_like(gd), torch.empty_like(gd)
+    err = torch.empty(L, K, dtype=torch.float64, device="cuda")
+    bits = torch.empty(L, K, dtype=torch.int64, device="cuda")
+    err2, bits2 = torch.empty_like(err), torch.empty_like(bits)
+    ctx.profile_compress(dch, gd, None, out, 2, err, bits)
+    ctx.profile(gd, None, 2, err2, bits2)
+    ctx.compress_allreduce_dev(dch, gd, None, out2, 2)
+    ctx.check()
+    assert torch.equal(out.view(torch.int32), out2.view(torch.int32))
+    assert torch.equal(err.view(torch.int64), err2.view(torch.int64)) and torch.equal(bits, bits2)
+    lbits = [BITS[3] if l.compress else 0 for l in layers]
+    zero = np.zeros_like(g)
+    out_ref, _, _, _ = ref.qsgd_allreduce(layers, lbits, [g], [zero], seed=8, step=2)
+    assert np.array_equal(_u32(out), out_ref.view(np.uint32))
+    rerr, rbits = ref.qsgd_profile(layers, g, None, BITS, seed=8, step=2)
+    _check_profile(err, bits, rerr, rbits)
+    ctx.close()
