@@ -5,6 +5,10 @@
 //                          candidate bit-width from the same Philox uniforms
 //                          (R5, R6).  Deterministic:
 //                          fixed chunk -> per-chunk partial -> ordered reduce.
+//   K1+K5 k_qprofile_q<K, 1|2>  the fused per-step pass (lgreco_profile_compress): K1
+//                          plus the planned candidate's quantisation from the same
+//                          registers and uniforms -- out and e' (W = 1) or the stage-1
+//                          records straight into the owners' windows (W > 1, peer memory).
 //   K1b k_qprofile_reduce  per-layer fixed-order fp64 sum of chunk partials, sqrt.
 //   K5  k_qpack      (a8)  quantise with the chosen bits, bit-plane pack via
 //                          __ballot_sync, fused error feedback e <- x - dec
