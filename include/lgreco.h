@@ -151,7 +151,7 @@ int lgreco_profile(lgreco_ctx* ctx, const float* d_g, const float* d_ef, uint64_
  * values = eigenvalues of the fp64 Gram matrix of the smaller side (the library's own
  * solver: Householder tridiagonalisation + Sturm bisection, one CTA per matrix, every
  * matrix of the table at once); the paper's choice when the rank range is large.
- * PowerSGD ctx only (LGRECO_EUNSUPPORTED otherwise, or when a matrix has min(m, k) > 6144);
+ * PowerSGD ctx only (LGRECO_EUNSUPPORTED otherwise, or when a matrix has min(m, k) > 4096);
  * synchronises the stream only when its workspace grows.  d_g / d_ef 4-byte aligned;
  * d_err L*K doubles, d_bits L*K int64. */
 /* (NEXT-2) The PowerSGD profile method lgreco_profile uses ("the best
@@ -161,7 +161,7 @@ int lgreco_profile(lgreco_ctx* ctx, const float* d_g, const float* d_ef, uint64_
  * host -- power sum_l steps * m k r_max(l) x 1.9e-13 s (one r_max run covers every rank:
  * the pinned prefix property, so O(m k r_max) and not the paper's O(m k r_max^2)), + 3e-5 s
  * of launch latency per power step, against SVD sum_l (m k n x 1e-13 + n^3 x
- * 2.7e-12) + n_max x 2e-6 s, n = min(m, k) (the fp64 Gram + the eigensolver's traffic and
+ * 2.2e-12) + n_max x 2e-6 s, n = min(m, k) (the fp64 Gram + the eigensolver's traffic and
  * step latency), constants measured on B200 (R22).  lgreco_psgd_method returns
  * the resolved method (POWER or SVD).  EINVAL on a bad method / non-PowerSGD ctx. */
 enum { LGRECO_PSGD_POWER = 0, LGRECO_PSGD_SVD = 1, LGRECO_PSGD_AUTO = 2 };

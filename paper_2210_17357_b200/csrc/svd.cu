@@ -95,13 +95,16 @@ __global__ void k_gram_reduce(const double* __restrict__ part, int nsplit, int64
 // diagonal: contiguous), beta = -sign(x0) ||x||, v = x / (x0 - beta) with v0 = 1,
 // tau = (beta - x0) / beta; p = tau A v and w = p - (tau/2)(p.v) v on the trailing
 // block A, then A -= v w^T + w v^T; e_k = beta, d_k = G[k][k].  Warp per row for the
-// matrix-vector product, fixed-order block reductions (deterministic).  (2) Eigenvalue i
+// matrix-vector product, fixed-order block reductions (deterministic).  One pass over the
+// trailing block per step: row k+1 is updated first, the next reflector is formed from it,
+// and the other rows' rank-2 update also accumulates the next step's A v (the old
+// update-then-matvec order read the block twice: C5 315 -> 269 ms).  (2) Eigenvalue i
 // (ascending) of the tridiagonal (d, e) by bisection on the Sturm count (the number of
 // negative q_j of q_0 = d_0 - s, q_j = d_j - s - e_{j-1}^2 / q_{j-1}) inside the
 // Gershgorin interval, to the fp64 resolution of the interval.  Dynamic shared memory:
-// v, w, d, e (4 n doubles).
+// v, w, d, e and the next step's v, p (6 n doubles).
 constexpr int EIG_THREADS = 1024;
-constexpr int EIG_NMAX = 6144;  // 4 n doubles of shared memory <= 192 KB
+constexpr int EIG_NMAX = 4096;  // 6 n doubles of shared memory <= 192 KB
 
 struct EigMat { int64_t goff; int32_t n, pad; };  // G at base + goff; eigenvalues at W + wout
 
@@ -124,52 +127,92 @@ k_sym_eigvals(double* __restrict__ Gbase, const EigMat* __restrict__ mats, doubl
   const int n = em.n;
   double* G = Gbase + em.goff;
   double* W = Wbase + woff[blockIdx.x];
-  double* v = esm;
-  double* w = esm + n;
+  double* v = esm;           // v_k
+  double* w = esm + n;       // p_k = A_k v_k, then w_k = tau p + K v in place
   double* d = esm + 2 * n;
   double* e = esm + 3 * n;
+  double* v2 = esm + 4 * n;  // v_{k+1}
+  double* p2 = esm + 5 * n;  // p_{k+1}
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int k = 0; k + 2 < n; ++k) {
-    const int m = n - k - 1;  // trailing block rows / columns k+1 .. n-1
-    const double* rk = G + (int64_t)k * n + (k + 1);
+  // Householder vector of row r's tail (columns r+1 .. n-1) into vv; returns tau (0: H = I)
+  auto reflector = [&](int r, double* vv) -> double {
+    const int m = n - r - 1;
+    const double* rr = G + (int64_t)r * n + (r + 1);
     double ss = 0.0;
-    for (int j = tid; j < m; j += EIG_THREADS) { const double x = rk[j]; ss = fma(x, x, ss); }
+    for (int j = tid; j < m; j += EIG_THREADS) { const double x = rr[j]; ss = fma(x, x, ss); }
     const double nrm2 = block_sum_d(ss, red, tid);
-    const double x0 = rk[0];
-    if (tid == 0) d[k] = G[(int64_t)k * n + k];
-    if (nrm2 == 0.0) {  // nothing to annihilate (H = I)
-      if (tid == 0) e[k] = 0.0;
-      __syncthreads();
-      continue;
+    const double x0 = rr[0];
+    if (tid == 0) d[r] = G[(int64_t)r * n + r];
+    if (nrm2 == 0.0) {
+      if (tid == 0) e[r] = 0.0;
+      for (int j = tid; j < m; j += EIG_THREADS) vv[j] = 0.0;
+      return 0.0;
     }
     const double nrm = sqrt(nrm2);
     const double beta = x0 > 0.0 ? -nrm : nrm;
-    const double tau = (beta - x0) / beta;
     const double sc = 1.0 / (x0 - beta);
-    for (int j = tid; j < m; j += EIG_THREADS) v[j] = j == 0 ? 1.0 : rk[j] * sc;
-    if (tid == 0) e[k] = beta;
+    for (int j = tid; j < m; j += EIG_THREADS) vv[j] = j == 0 ? 1.0 : rr[j] * sc;
+    if (tid == 0) e[r] = beta;
+    return (beta - x0) / beta;
+  };
+  if (n > 2) {
+    double tau = reflector(0, v);
     __syncthreads();
-    // p = tau A v (warp per row, lanes over columns), into w
-    for (int i = warp; i < m; i += EIG_THREADS / 32) {
-      const double* ri = G + (int64_t)(k + 1 + i) * n + (k + 1);
-      double a = 0.0;
-      for (int j = lane; j < m; j += 32) a = fma(ri[j], v[j], a);
-      a = warp_sum_d(a);
-      if (lane == 0) w[i] = tau * a;
+    // p_0 = A_0 v_0 (warp per row)
+    {
+      const int m = n - 1;
+      for (int i = warp; i < m; i += EIG_THREADS / 32) {
+        const double* ri = G + (int64_t)(1 + i) * n + 1;
+        double a = 0.0;
+        for (int j = lane; j < m; j += 32) a = fma(ri[j], v[j], a);
+        a = warp_sum_d(a);
+        if (lane == 0) w[i] = a;
+      }
     }
     __syncthreads();
-    double pv = 0.0;
-    for (int j = tid; j < m; j += EIG_THREADS) pv = fma(w[j], v[j], pv);
-    const double kk = -0.5 * tau * block_sum_d(pv, red, tid);
-    for (int j = tid; j < m; j += EIG_THREADS) w[j] = fma(kk, v[j], w[j]);
-    __syncthreads();
-    // A -= v w^T + w v^T
-    for (int i = warp; i < m; i += EIG_THREADS / 32) {
-      double* ri = G + (int64_t)(k + 1 + i) * n + (k + 1);
-      const double vi = v[i], wi = w[i];
-      for (int j = lane; j < m; j += 32) ri[j] = ri[j] - vi * w[j] - wi * v[j];
+    for (int k = 0; k + 2 < n; ++k) {
+      const int m = n - k - 1;  // trailing block rows / columns k+1 .. n-1
+      // w = tau p + K v, K = -(tau / 2) (tau p . v)
+      double pv = 0.0;
+      for (int j = tid; j < m; j += EIG_THREADS) pv = fma(w[j], v[j], pv);
+      const double kk = -0.5 * tau * tau * block_sum_d(pv, red, tid);
+      for (int j = tid; j < m; j += EIG_THREADS) w[j] = fma(kk, v[j], tau * w[j]);
+      __syncthreads();
+      // row k+1 (the next reflector's source) updated first
+      {
+        double* r1 = G + (int64_t)(k + 1) * n + (k + 1);
+        const double v0 = v[0], w0 = w[0];
+        for (int j = tid; j < m; j += EIG_THREADS) r1[j] = r1[j] - v0 * w[j] - w0 * v[j];
+      }
+      __syncthreads();
+      const bool more = k + 3 < n;  // another reflector follows
+      double tau2 = 0.0;
+      if (more) tau2 = reflector(k + 1, v2);
+      __syncthreads();
+      // the other rows: A -= v w^T + w v^T, and in the same pass the next step's
+      // p_{k+1}[i'] = sum_{j >= k+2} A_new[i][j] v_{k+1}[j - k - 2] (i' = i - k - 2)
+      for (int i = 1 + warp; i < m; i += EIG_THREADS / 32) {
+        double* ri = G + (int64_t)(k + 1 + i) * n + (k + 1);
+        const double vi = v[i], wi = w[i];
+        double a = 0.0;
+        for (int j = lane; j < m; j += 32) {
+          const double x = ri[j] - vi * w[j] - wi * v[j];
+          ri[j] = x;
+          if (more && j >= 1) a = fma(x, v2[j - 1], a);
+        }
+        if (more) {
+          a = warp_sum_d(a);
+          if (lane == 0) p2[i - 1] = a;
+        }
+      }
+      __syncthreads();
+      if (more) {
+        // swap (v, w) <- (v2, p2)
+        double* t0 = v; v = v2; v2 = t0;
+        double* t1 = w; w = p2; p2 = t1;
+        tau = tau2;
+      }
     }
-    __syncthreads();
   }
   if (tid == 0) {
     if (n >= 2) {
@@ -179,7 +222,7 @@ k_sym_eigvals(double* __restrict__ Gbase, const EigMat* __restrict__ mats, doubl
     d[n - 1] = G[(int64_t)(n - 1) * n + (n - 1)];
   }
   __syncthreads();
-  // Gershgorin interval of the tridiagonal
+  // Gershgorin interval of the tridiagonal (v, w: scratch from here on)
   double lo = INFINITY, hi = -INFINITY;
   for (int j = tid; j < n; j += EIG_THREADS) {
     const double r = (j > 0 ? fabs(e[j - 1]) : 0.0) + (j + 1 < n ? fabs(e[j]) : 0.0);
@@ -363,8 +406,10 @@ extern "C" int lgreco_psgd_profile_svd(lgreco_ctx* c, const float* d_g, const fl
     LG_CUDA(cudaGetLastError());
     c->launches += 2;
   }
-  const size_t esmem = sizeof(double) * 4 * (size_t)nmax;
-  if (esmem > 48 * 1024) LG_CUDA(cudaFuncSetAttribute(lg::k_sym_eigvals, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esmem));
+  const size_t esmem = sizeof(double) * 6 * (size_t)nmax;
+  // (always: with the static reduction arrays, 48 KB of dynamic shared memory already
+  // exceeds the default limit)
+  LG_CUDA(cudaFuncSetAttribute(lg::k_sym_eigvals, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)esmem));
   lg::k_sym_eigvals<<<(unsigned)mats.size(), lg::EIG_THREADS, esmem, st>>>(s->G, s->mats, s->W, s->woff);
   LG_CUDA(cudaGetLastError());
   c->launches += 1;
@@ -394,8 +439,8 @@ extern "C" int lgreco_psgd_set_method(lgreco_ctx* c, int32_t method) {
     if (rmax == 0) continue;
     t_pow += (double)c->power_steps * m * k * rmax * 1.9e-13;
     // the fp64 Gram, then the eigensolver's HBM traffic (all matrices at once: ~8 n^3
-    // bytes each at ~3 TB/s aggregate; measured: C2 25 ms, C5 315 ms)
-    t_svd += m * k * n * 1e-13 + n * n * n * 2.7e-12;
+    // bytes each at ~3.5 TB/s aggregate; measured: C2 20 ms, C5 269 ms)
+    t_svd += m * k * n * 1e-13 + n * n * n * 2.2e-12;
     nmax = std::max(nmax, n);
   }
   // dependent-step latencies: n - 2 Householder steps of the largest matrix (~2 us each);
