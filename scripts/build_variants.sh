@@ -6,7 +6,7 @@ cd "$(dirname "$0")/.."
 TU=$1; shift
 PY=python
 SITE=$($PY -c "import sysconfig;print(sysconfig.get_paths()['purelib'])")
-NCCL=$SITE/nvidia/nccl; CUSOLVER=$SITE/nvidia/cusolver; CUDART=$SITE/nvidia/cuda_runtime/lib
+NCCL=$SITE/nvidia/nccl; CUDART=$SITE/nvidia/cuda_runtime/lib
 ARCH="-gencode arch=compute_100a,code=sm_100a"
 mkdir -p build/var
 OTHERS=$(for f in paper_2210_17357_b200/csrc/*.cu; do b=$(basename $f .cu); [ "$b" != "$TU" ] && echo build/obj/$b.o; done)
@@ -19,7 +19,7 @@ wait
 for spec in "$@"; do
   name=${spec%%:*}
   nvcc $ARCH -cudart shared -shared -o build/var/liblgreco_$name.so build/var/${TU}_$name.o $OTHERS \
-    -L$NCCL/lib -l:libnccl.so.2 -L$CUSOLVER/lib -l:libcusolver.so.11 \
-    -Xlinker -rpath=$NCCL/lib -Xlinker -rpath=$CUDART -Xlinker -rpath=$CUSOLVER/lib
+    -L$NCCL/lib -l:libnccl.so.2 \
+    -Xlinker -rpath=$NCCL/lib -Xlinker -rpath=$CUDART
 done
 ls build/var/*.so
