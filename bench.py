@@ -292,6 +292,16 @@ def run_ours(args):
         torch.cuda.synchronize()
         pipe_ms = p0.elapsed_time(p1) / args.steps
         pipe_launches = ctx.launches() - launches_p0 + args.steps
+        # the same steps without the overlap (the fused pass waits for the solve before it):
+        # what LGRECO_PC_CONCURRENT buys
+        q0, q1 = ev(), ev()
+        q0.record(stream)
+        for s in range(args.steps):
+            step_pipe(base + args.steps + s, conc=False)
+        q1.record(stream)
+        torch.cuda.synchronize()
+        serial_ms = q0.elapsed_time(q1) / args.steps
+        base += args.steps
         # stage pass of the pipelined step (serial, events between): fused pass, solve
         pt = {"profile_compress": [], "solve": []}
         ctx.timing(True)
@@ -314,7 +324,7 @@ def run_ours(args):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             pipe_ms = float(t[0])
             pt = {"profile_compress": [float(t[1])], "solve": [float(t[2])]}
-        pipe = {"ms": pipe_ms, "launches": pipe_launches,
+        pipe = {"ms": pipe_ms, "launches": pipe_launches, "serial_ms": serial_ms,
                 "stage": {k: sum(v) / len(v) for k, v in pt.items()},
                 "fused_ms": fk_total / max(1, fk_n), "fused_n": fk_n}
         ctx.check()
@@ -555,6 +565,7 @@ def run_ours(args):
                           "l2": "flushed (512 MiB memset) before every timed step",
                           "note": "profile -> solve -> compress with the plan of the same step (round-1 headline)"},
             "pipelined_stage_ms": ({k: round(v, 4) for k, v in pipe["stage"].items()} if pipe else None),
+            "pipelined_no_overlap_ms": (round(pipe["serial_ms"], 4) if pipe else None),
             "e2e": {"value": round(world * 4.0 * N / (e2e * 1e-3) / 1e9, 3), "unit": "GB/s",
                     "h2d_bytes_per_step": 4 * N, "d2h_bytes_per_step": 4 * N, "ms_per_step": round(e2e, 4),
                     "steps": n_e2e, "overlap": "H2D(s+1) and D2H(s-1) on copy streams beside step s's kernels",
