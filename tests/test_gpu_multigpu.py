@@ -145,7 +145,7 @@ def _worlds(mode="nccl"):
     return [w for w in (2, 4, 8) if w <= n]
 
 
-@pytest.mark.parametrize("mode", ["p2p", "nccl", "p2p_pc"])
+@pytest.mark.parametrize("mode", ["p2p", "nccl", "p2p_pc", "nccl_pc"])
 @pytest.mark.parametrize("world", [2, 4, 8])
 def test_qsgd_exchange_multi_gpu(ref, world, mode):
     """mode p2p_pc: the per-step call of the pipelined schedule (lgreco_profile_compress)
