@@ -110,3 +110,24 @@ def test_hybrid_table_picks_across_families(ref):
             assert got == sum(int(bits[l, 1]) for l in range(L))
         else:
             assert got == best
+
+
+def test_r_squared_of_the_bucket_time_fit():
+    """bucket_timer.r_squared: 1 on exactly linear samples, lower with noise, and the
+    least-squares fit (objectives.fit_bucket_time) recovers per-byte coefficients from
+    samples shaped like the timer's (bytes per bucket, total sync time)."""
+    import numpy as np
+    from paper_2210_17357_b200 import objectives as O
+    from paper_2210_17357_b200.bucket_timer import r_squared
+    rng = np.random.default_rng(3)
+    sizes = rng.uniform(1e5, 7e6, (40, 5))
+    T = np.array([1.8e-8, 2.0e-8, 1.9e-8, 2.1e-8, 1.7e-8])
+    y = sizes @ T + 3e-5
+    Tf, c = O.fit_bucket_time(sizes, y)
+    assert np.allclose(Tf, T, rtol=1e-9) and abs(c - 3e-5) < 1e-12
+    assert abs(r_squared(sizes, y, Tf, c) - 1.0) < 1e-12
+    yn = y + rng.normal(0, 2e-5, y.shape)
+    Tn, cn = O.fit_bucket_time(sizes, yn)
+    r2 = r_squared(sizes, yn, Tn, cn)
+    assert 0.5 < r2 < 1.0
+    assert np.all(np.abs(Tn - T) / T < 0.5)
